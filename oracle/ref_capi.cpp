@@ -1,0 +1,526 @@
+// C-ABI shim over the UNMODIFIED reference library — TEST INFRASTRUCTURE.
+//
+// Lets the Python tests / bench CPU-baseline legs drive the reference's own
+// operator and solver code (proj/src/forms.hpp:105-170, krylov.hpp:22-66) on
+// the same host arrays the device path receives.  Nothing in the product
+// package links or loads this; it lives in oracle/_ref/libdgref.so.
+#include "forms.hpp"
+#include "kernels.hpp"
+#include "krylov.hpp"
+#include "mesh.hpp"
+#include "space.hpp"
+#include "support/dense_oracle.hpp"
+#include "trbdf2_cpu.hpp"
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <thread>
+#include <vector>
+
+using namespace dgns;
+
+extern "C" {
+typedef void (*ref_bc_fn)(const double* x, double t, double* out, void* user);
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Base {
+  virtual ~Base() = default;
+  int ndim = 0;
+  virtual void info(long long* out) = 0;
+  virtual void set_bc(int id, int type, ref_bc_fn fn, void* user) = 0;
+  virtual void momentum(const double* c, const double* w, const double* x, double* y) = 0;
+  virtual void momentum_diag(const double* c, const double* w, double* d) = 0;
+  virtual void pressure(double mc, const double* x, double* y) = 0;
+  virtual void helmholtz_diag(double mc, double* d) = 0;
+  virtual void laplace(int dir, const double* x, double* y) = 0;
+  virtual void laplace_diag(int dir, double* d) = 0;
+  virtual void mass(int space, const double* x, double* y) = 0;
+  virtual void mass_diag(int space, double* d) = 0;
+  virtual void momentum_rhs(int nm, const double* mc, const double* const* mf, int nv,
+                            const double* vc, const double* const* vf, int na, const double* ac,
+                            const double* const* af, const double* const* aw, int np,
+                            const double* pc, const double* const* pf, double dvisc, double dadv,
+                            const double* dir_w, double time, double* y) = 0;
+  virtual void divergence(const double* u, double* y) = 0;
+  virtual void pressure_rhs(double inv_adt, const double* u, double mc, const double* p_old,
+                            double* y) = 0;
+  virtual void pressure_gradient(const double* p, double* y) = 0;
+  virtual double kinetic_energy(const double* u) = 0;
+  virtual int solve(int op, int solver, const double* coefs, const double* w, const double* b,
+                    double rel_tol, double abs_tol, int max_iter, int restart, int precond,
+                    double* x, int* iters, double* resid, double* hist, int hist_cap,
+                    int* hist_len) = 0;
+  virtual void step(const double* params, const double* u_nm1, const double* u_n,
+                    const double* p_n, double* u_np1, double* p_np1, int* its) = 0;
+  virtual void faces(int* iface, double* imeas, int* bface, double* bmeas) = 0;
+  virtual void cell_vertices(double* xv) = 0;
+  virtual void bface_points(int rule, double* xq) = 0;
+  virtual void interpolate_nodes(int space, double* xn) = 0;
+  virtual double bench(int op, const double* coefs, const double* w, const double* x, int nthreads,
+                       int napplies) = 0;
+  virtual void dense_momentum(const double* c, const double* w, double* A) = 0;
+  virtual void dense_scalar_sip(double mc, int dir, int rule, double* A) = 0;
+};
+
+template <int dim>
+struct Ctx : Base {
+  Mesh<dim> mesh;
+  std::unique_ptr<GeometryCache<dim>> geom;
+  std::unique_ptr<FunctionSpace<dim>> Vu, Vp;
+  BoundaryTable<dim> bc;
+
+  Ctx(Mesh<dim>&& m, int ku, int kp) : mesh(std::move(m)) {
+    this->ndim = dim;
+    geom = std::make_unique<GeometryCache<dim>>(mesh);
+    Vu = std::make_unique<FunctionSpace<dim>>(mesh, ku, dim);
+    Vp = std::make_unique<FunctionSpace<dim>>(mesh, kp, 1);
+  }
+  static Field F(const double* p, int n) { return Field(p, p + n); }
+  int nu() const { return Vu->n_dofs(); }
+  int np() const { return Vp->n_dofs(); }
+
+  void info(long long* out) override {
+    out[0] = mesh.n_active();
+    out[1] = nu();
+    out[2] = np();
+    out[3] = static_cast<long long>(mesh.faces().interior.size());
+    out[4] = static_cast<long long>(mesh.faces().boundary.size());
+    out[5] = Vu->degree();
+    out[6] = Vp->degree();
+    out[7] = dim;
+    out[8] = static_cast<long long>(mesh.vertices.size());
+    int nh = 0;
+    for (const auto& f : mesh.faces().interior) nh += f.hanging;
+    out[9] = nh;
+  }
+  void set_bc(int id, int type, ref_bc_fn fn, void* user) override {
+    auto& e = bc.entries[id];
+    e.type = type == 1 ? BcType::outlet : BcType::dirichlet;
+    if (fn)
+      e.value = [fn, user](const std::array<double, dim>& x, double t, double* out) {
+        fn(x.data(), t, out, user);
+      };
+    else
+      e.value = nullptr;
+  }
+  MomentumCtx<dim> mctx(const double* c, const Field* w) {
+    MomentumCtx<dim> m;
+    m.mass_coef = c[0];
+    m.visc_coef = c[1];
+    m.adv_coef = c[2];
+    m.skew_coef = c[3];
+    m.advecting = w;
+    m.bc = &bc;
+    return m;
+  }
+  void momentum(const double* c, const double* w, const double* x, double* y) override {
+    Field wf = w ? F(w, nu()) : Field();
+    Field out;
+    apply_momentum(*Vu, *geom, mctx(c, w ? &wf : nullptr), F(x, nu()), out);
+    std::memcpy(y, out.data(), sizeof(double) * out.size());
+  }
+  void momentum_diag(const double* c, const double* w, double* d) override {
+    Field wf = w ? F(w, nu()) : Field();
+    Field out;
+    momentum_diagonal(*Vu, *geom, mctx(c, w ? &wf : nullptr), out);
+    std::memcpy(d, out.data(), sizeof(double) * out.size());
+  }
+  void pressure(double mc, const double* x, double* y) override {
+    Field out;
+    apply_pressure_helmholtz(*Vp, *geom, mc, F(x, np()), out);
+    std::memcpy(y, out.data(), sizeof(double) * out.size());
+  }
+  void helmholtz_diag(double mc, double* d) override {
+    Field out;
+    helmholtz_diagonal(*Vp, *geom, mc, out);
+    std::memcpy(d, out.data(), sizeof(double) * out.size());
+  }
+  void laplace(int dir, const double* x, double* y) override {
+    Field out;
+    apply_scalar_laplace(*Vp, *geom, dir != 0, F(x, np()), out);
+    std::memcpy(y, out.data(), sizeof(double) * out.size());
+  }
+  void laplace_diag(int dir, double* d) override {
+    Field out;
+    scalar_laplace_diagonal(*Vp, *geom, dir != 0, out);
+    std::memcpy(d, out.data(), sizeof(double) * out.size());
+  }
+  void mass(int space, const double* x, double* y) override {
+    const auto& V = space == 0 ? *Vu : *Vp;
+    Field out;
+    apply_mass(V, *geom, F(x, V.n_dofs()), out);
+    std::memcpy(y, out.data(), sizeof(double) * out.size());
+  }
+  void mass_diag(int space, double* d) override {
+    const auto& V = space == 0 ? *Vu : *Vp;
+    Field out;
+    mass_diagonal(V, *geom, out);
+    std::memcpy(d, out.data(), sizeof(double) * out.size());
+  }
+  void momentum_rhs(int nm, const double* mc, const double* const* mf, int nv, const double* vc,
+                    const double* const* vf, int na, const double* ac, const double* const* af,
+                    const double* const* aw, int npr, const double* pc, const double* const* pf,
+                    double dvisc, double dadv, const double* dir_w, double time,
+                    double* y) override {
+    std::vector<std::unique_ptr<Field>> keep;
+    auto hold = [&](const double* p, int n) {
+      keep.push_back(std::make_unique<Field>(p, p + n));
+      return keep.back().get();
+    };
+    MomentumRhs<dim> s;
+    for (int i = 0; i < nm; ++i) s.mass.push_back({mc[i], hold(mf[i], nu())});
+    for (int i = 0; i < nv; ++i) s.visc.push_back({vc[i], hold(vf[i], nu())});
+    for (int i = 0; i < na; ++i) s.adv.push_back({ac[i], hold(af[i], nu()), hold(aw[i], nu())});
+    for (int i = 0; i < npr; ++i) s.pres.push_back({pc[i], hold(pf[i], np())});
+    s.dir_visc_coef = dvisc;
+    s.dir_adv_coef = dadv;
+    s.dir_w = dir_w ? hold(dir_w, nu()) : nullptr;
+    s.time = time;
+    s.bc = &bc;
+    Field out;
+    dgns::momentum_rhs(*Vu, *Vp, *geom, s, out);
+    std::memcpy(y, out.data(), sizeof(double) * out.size());
+  }
+  void divergence(const double* u, double* y) override {
+    Field out;
+    divergence_functional(*Vu, *Vp, *geom, F(u, nu()), &bc, out);
+    std::memcpy(y, out.data(), sizeof(double) * out.size());
+  }
+  void pressure_rhs(double inv_adt, const double* u, double mc, const double* p_old,
+                    double* y) override {
+    Field po = p_old ? F(p_old, np()) : Field();
+    Field out;
+    dgns::pressure_rhs(*Vu, *Vp, *geom, inv_adt, F(u, nu()), mc, p_old ? &po : nullptr, &bc, out);
+    std::memcpy(y, out.data(), sizeof(double) * out.size());
+  }
+  void pressure_gradient(const double* p, double* y) override {
+    Field out;
+    pressure_gradient_rhs(*Vu, *Vp, *geom, F(p, np()), out);
+    std::memcpy(y, out.data(), sizeof(double) * out.size());
+  }
+  double kinetic_energy(const double* u) override {
+    return dgns::kinetic_energy(*Vu, *geom, F(u, nu()));
+  }
+
+  // op: 0 momentum(coefs, w), 1 pressure helmholtz(coefs[0]), 2 mass(u), 3 mass(p)
+  // solver: 0 cg, 1 gmres.  precond: 0 none, 1 jacobi(exact diagonal)
+  int solve(int op, int solver, const double* coefs, const double* w, const double* b,
+            double rel_tol, double abs_tol, int max_iter, int restart, int precond, double* x,
+            int* iters, double* resid, double* hist, int hist_cap, int* hist_len) override {
+    const int n = (op == 0 || op == 2) ? nu() : np();
+    Field wf = w ? F(w, nu()) : Field();
+    const auto mc = mctx(coefs, w ? &wf : nullptr);
+    Field tmp, diag;
+    LinearOp A;
+    if (op == 0) {
+      A = [&](const double* xx, double* yy) {
+        apply_momentum(*Vu, *geom, mc, F(xx, n), tmp);
+        std::memcpy(yy, tmp.data(), sizeof(double) * n);
+      };
+      if (precond) momentum_diagonal(*Vu, *geom, mc, diag);
+    } else if (op == 1) {
+      A = [&](const double* xx, double* yy) {
+        apply_pressure_helmholtz(*Vp, *geom, coefs[0], F(xx, n), tmp);
+        std::memcpy(yy, tmp.data(), sizeof(double) * n);
+      };
+      if (precond) helmholtz_diagonal(*Vp, *geom, coefs[0], diag);
+    } else {
+      const auto& V = op == 2 ? *Vu : *Vp;
+      A = [&](const double* xx, double* yy) {
+        apply_mass(V, *geom, F(xx, n), tmp);
+        std::memcpy(yy, tmp.data(), sizeof(double) * n);
+      };
+      if (precond) mass_diagonal(V, *geom, diag);
+    }
+    SolverSettings s;
+    s.rel_tol = rel_tol;
+    s.abs_tol = abs_tol;
+    s.max_iter = max_iter;
+    s.restart = restart;
+    *hist_len = 0;
+    try {
+      std::unique_ptr<JacobiPreconditioner> M;
+      if (precond) M = std::make_unique<JacobiPreconditioner>(diag);
+      auto r = solver == 0 ? cg_solve(n, A, b, s, M.get(), x) : gmres_solve(n, A, b, s, M.get(), x);
+      *iters = r.iterations;
+      *resid = r.residual;
+      return 0;
+    } catch (const SolverError& e) {
+      g_err = e.what();
+      const int m = std::min<int>(hist_cap, static_cast<int>(e.history.size()));
+      for (int i = 0; i < m; ++i) hist[i] = e.history[i];
+      *hist_len = static_cast<int>(e.history.size());
+      return 2;
+    } catch (const std::exception& e) {
+      g_err = e.what();
+      return 1;
+    }
+  }
+
+  // params: dt, Re, c, time, restart, tol_mom, tol_p, tol_mass, max_iter, first_step
+  void step(const double* prm, const double* u_nm1, const double* u_n, const double* p_n,
+            double* u_np1, double* p_np1, int* its) override {
+    oracle_trbdf2::StepParams P;
+    P.dt = prm[0];
+    P.Re = prm[1];
+    P.c = prm[2];
+    P.time = prm[3];
+    P.restart = static_cast<int>(prm[4]);
+    P.tol_mom = prm[5];
+    P.tol_p = prm[6];
+    P.tol_mass = prm[7];
+    P.max_iter = static_cast<int>(prm[8]);
+    P.first_step = prm[9] != 0.0;
+    oracle_trbdf2::StepStats st;
+    Field un1, pn1;
+    oracle_trbdf2::trbdf2_step(*Vu, *Vp, *geom, bc, P, F(u_nm1, nu()), F(u_n, nu()), F(p_n, np()),
+                               un1, pn1, st);
+    std::memcpy(u_np1, un1.data(), sizeof(double) * nu());
+    std::memcpy(p_np1, pn1.data(), sizeof(double) * np());
+    its[0] = st.gmres_its[0];
+    its[1] = st.gmres_its[1];
+    its[2] = st.cg_its[0];
+    its[3] = st.cg_its[1];
+    for (int i = 0; i < 4; ++i) its[4 + i] = st.mass_its[i];
+  }
+
+  // interior: [cell_in, face_in, cell_out, face_out, hanging] per face (active indices)
+  // boundary: [cell_in, face_in, boundary_id]
+  void faces(int* iface, double* imeas, int* bface, double* bmeas) override {
+    const auto& fl = mesh.faces();
+    for (size_t f = 0; f < fl.interior.size(); ++f) {
+      const auto& fi = fl.interior[f];
+      iface[5 * f + 0] = mesh.active_index(fi.cell_in);
+      iface[5 * f + 1] = fi.face_in;
+      iface[5 * f + 2] = mesh.active_index(fi.cell_out);
+      iface[5 * f + 3] = fi.face_out;
+      iface[5 * f + 4] = fi.hanging;
+      imeas[f] = fi.measure;
+    }
+    for (size_t f = 0; f < fl.boundary.size(); ++f) {
+      const auto& fi = fl.boundary[f];
+      bface[3 * f + 0] = mesh.active_index(fi.cell_in);
+      bface[3 * f + 1] = fi.face_in;
+      bface[3 * f + 2] = fi.boundary_id;
+      bmeas[f] = fi.measure;
+    }
+  }
+  // Per active cell, the 2^dim vertex coordinates (lexicographic vertex order).
+  void cell_vertices(double* xv) override {
+    const int nv = Mesh<dim>::n_vertices_per_cell;
+    for (int i = 0; i < mesh.n_active(); ++i) {
+      const auto& c = mesh.cells[mesh.active_cells()[i]];
+      for (int v = 0; v < nv; ++v)
+        for (int d = 0; d < dim; ++d) xv[(static_cast<size_t>(i) * nv + v) * dim + d] = mesh.vertices[c.v[v]][d];
+    }
+  }
+  void bface_points(int rule, double* xq) override {
+    const auto& bfg = geom->boundary_faces(rule);
+    size_t k = 0;
+    for (const auto& fg : bfg)
+      for (const auto& p : fg.xq)
+        for (int d = 0; d < dim; ++d) xq[k++] = p[d];
+  }
+  // Physical coordinates of the nodal points of every cell (space 0: Vu nodes, 1: Vp nodes).
+  void interpolate_nodes(int space, double* xn) override {
+    const auto& V = space == 0 ? *Vu : *Vp;
+    for (int i = 0; i < mesh.n_active(); ++i) {
+      const int c = mesh.active_cells()[i];
+      for (int j = 0; j < V.nb(); ++j) {
+        const auto x = mesh.map_point(c, V.nodes()[j]);
+        for (int d = 0; d < dim; ++d) xn[(static_cast<size_t>(i) * V.nb() + j) * dim + d] = x[d];
+      }
+    }
+  }
+  // Throughput of the reference CPU apply: nthreads concurrent independent
+  // applies (reference code is single-threaded; caches are warmed first so the
+  // lazily-filled GeometryCache / trace tables are read-only during the run).
+  double bench(int op, const double* c, const double* w, const double* x, int nthreads,
+               int napplies) override {
+    const int n = op == 0 ? nu() : np();
+    Field wf = w ? F(w, nu()) : Field();
+    Field xf = F(x, n);
+    const auto m = mctx(c, w ? &wf : nullptr);
+    auto one = [&](Field& out) {
+      if (op == 0)
+        apply_momentum(*Vu, *geom, m, xf, out);
+      else
+        apply_pressure_helmholtz(*Vp, *geom, c[0], xf, out);
+    };
+    {
+      Field warm;
+      one(warm);
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthreads; ++t)
+      th.emplace_back([&]() {
+        Field out;
+        for (int k = 0; k < napplies; ++k) one(out);
+      });
+    for (auto& t : th) t.join();
+    const auto t1 = std::chrono::steady_clock::now();
+    return std::chrono::duration<double>(t1 - t0).count();
+  }
+  void dense_momentum(const double* c, const double* w, double* A) override {
+    Field wf = w ? F(w, nu()) : Field();
+    const auto m = mctx(c, w ? &wf : nullptr);
+    const auto M = oracle::momentum_matrix(*Vu, m, Vu->degree() + 1, Vu->degree() + 2);
+    std::memcpy(A, M.a.data(), sizeof(double) * M.a.size());
+  }
+  void dense_scalar_sip(double mc, int dir, int rule, double* A) override {
+    const auto M = oracle::scalar_sip_matrix(*Vp, mc, dir != 0, rule);
+    std::memcpy(A, M.a.data(), sizeof(double) * M.a.size());
+  }
+};
+
+template <int dim>
+Base* make_cartesian(int n_el, double amp, unsigned seed, int ku, int kp, int refine_first) {
+  std::array<double, dim> lo{}, hi{};
+  hi.fill(1.0);
+  Mesh<dim> m = generate_cartesian<dim>(n_el, lo, hi);
+  if (amp != 0.0) distort(m, amp, seed);
+  if (refine_first) m.refine_and_coarsen({0}, {});
+  return new Ctx<dim>(std::move(m), ku, kp);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+const char* ref_backend() {
+  static std::string s;
+  s = kern::backend_name();
+  return s.c_str();
+}
+
+void* ref_create_cartesian(int dim, int n_el, double amp, unsigned seed, int ku, int kp,
+                           int refine_first) {
+  try {
+    if (dim == 2) return make_cartesian<2>(n_el, amp, seed, ku, kp, refine_first);
+    if (dim == 3) return make_cartesian<3>(n_el, amp, seed, ku, kp, refine_first);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  }
+  return nullptr;
+}
+void* ref_create_from_text(const char* text, int ku, int kp) {
+  try {
+    const std::string s(text);
+    const int d = mesh_file_dim(s);
+    if (d == 2) return new Ctx<2>(import_text<2>(s), ku, kp);
+    return new Ctx<3>(import_text<3>(s), ku, kp);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  }
+  return nullptr;
+}
+void* ref_create_cylinder(int level, int ku, int kp) {
+  try {
+    return new Ctx<2>(generate_cylinder_channel(level), ku, kp);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  }
+  return nullptr;
+}
+void ref_destroy(void* h) { delete static_cast<Base*>(h); }
+void ref_info(void* h, long long* out) { static_cast<Base*>(h)->info(out); }
+void ref_set_bc(void* h, int id, int type, ref_bc_fn fn, void* user) {
+  static_cast<Base*>(h)->set_bc(id, type, fn, user);
+}
+int ref_apply_momentum(void* h, const double* c, const double* w, const double* x, double* y) {
+  try {
+    static_cast<Base*>(h)->momentum(c, w, x, y);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+int ref_momentum_diagonal(void* h, const double* c, const double* w, double* d) {
+  try {
+    static_cast<Base*>(h)->momentum_diag(c, w, d);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+void ref_apply_pressure(void* h, double mc, const double* x, double* y) {
+  static_cast<Base*>(h)->pressure(mc, x, y);
+}
+void ref_helmholtz_diagonal(void* h, double mc, double* d) {
+  static_cast<Base*>(h)->helmholtz_diag(mc, d);
+}
+void ref_apply_laplace(void* h, int dir, const double* x, double* y) {
+  static_cast<Base*>(h)->laplace(dir, x, y);
+}
+void ref_laplace_diagonal(void* h, int dir, double* d) { static_cast<Base*>(h)->laplace_diag(dir, d); }
+void ref_apply_mass(void* h, int space, const double* x, double* y) {
+  static_cast<Base*>(h)->mass(space, x, y);
+}
+void ref_mass_diagonal(void* h, int space, double* d) { static_cast<Base*>(h)->mass_diag(space, d); }
+int ref_momentum_rhs(void* h, int nm, const double* mc, const double* const* mf, int nv,
+                     const double* vc, const double* const* vf, int na, const double* ac,
+                     const double* const* af, const double* const* aw, int np, const double* pc,
+                     const double* const* pf, double dvisc, double dadv, const double* dir_w,
+                     double time, double* y) {
+  try {
+    static_cast<Base*>(h)->momentum_rhs(nm, mc, mf, nv, vc, vf, na, ac, af, aw, np, pc, pf, dvisc,
+                                        dadv, dir_w, time, y);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+void ref_divergence(void* h, const double* u, double* y) { static_cast<Base*>(h)->divergence(u, y); }
+void ref_pressure_rhs(void* h, double inv_adt, const double* u, double mc, const double* p_old,
+                      double* y) {
+  static_cast<Base*>(h)->pressure_rhs(inv_adt, u, mc, p_old, y);
+}
+void ref_pressure_gradient(void* h, const double* p, double* y) {
+  static_cast<Base*>(h)->pressure_gradient(p, y);
+}
+double ref_kinetic_energy(void* h, const double* u) { return static_cast<Base*>(h)->kinetic_energy(u); }
+int ref_solve(void* h, int op, int solver, const double* coefs, const double* w, const double* b,
+              double rel_tol, double abs_tol, int max_iter, int restart, int precond, double* x,
+              int* iters, double* resid, double* hist, int hist_cap, int* hist_len) {
+  return static_cast<Base*>(h)->solve(op, solver, coefs, w, b, rel_tol, abs_tol, max_iter, restart,
+                                      precond, x, iters, resid, hist, hist_cap, hist_len);
+}
+int ref_trbdf2_step(void* h, const double* params, const double* u_nm1, const double* u_n,
+                    const double* p_n, double* u_np1, double* p_np1, int* its) {
+  try {
+    static_cast<Base*>(h)->step(params, u_nm1, u_n, p_n, u_np1, p_np1, its);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+void ref_faces(void* h, int* iface, double* imeas, int* bface, double* bmeas) {
+  static_cast<Base*>(h)->faces(iface, imeas, bface, bmeas);
+}
+void ref_cell_vertices(void* h, double* xv) { static_cast<Base*>(h)->cell_vertices(xv); }
+void ref_bface_points(void* h, int rule, double* xq) { static_cast<Base*>(h)->bface_points(rule, xq); }
+void ref_node_points(void* h, int space, double* xn) { static_cast<Base*>(h)->interpolate_nodes(space, xn); }
+double ref_bench(void* h, int op, const double* c, const double* w, const double* x, int nthreads,
+                 int napplies) {
+  return static_cast<Base*>(h)->bench(op, c, w, x, nthreads, napplies);
+}
+void ref_dense_momentum(void* h, const double* c, const double* w, double* A) {
+  static_cast<Base*>(h)->dense_momentum(c, w, A);
+}
+void ref_dense_scalar_sip(void* h, double mc, int dir, int rule, double* A) {
+  static_cast<Base*>(h)->dense_scalar_sip(mc, dir, rule, A);
+}
+
+}  // extern "C"

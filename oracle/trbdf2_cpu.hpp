@@ -1,0 +1,201 @@
+// Restated TR-BDF2 step on the CPU — TEST INFRASTRUCTURE (the parity oracle).
+//
+// The reference's driver (`src/schemes.cpp`, named at proj/CMakeLists.txt:25)
+// is missing from the tree, so the "reference CPU implementation" of a full
+// step is this restatement.  It calls ONLY unmodified reference functions
+// (forms.hpp / krylov.hpp) and follows SURVEY.md Appendix A, which derives the
+// stage -> operator coefficient map from SPEC.md:345-452, PAPER.md:90-180,
+// 475-491 and the free-stream pin proj/tests/test_forms.cpp:369-422.
+// The device driver (paper_2107_07776_b200/csrc/trbdf2.cu) performs exactly
+// the same sequence of operator / solver calls.
+#pragma once
+
+#include "forms.hpp"
+#include "krylov.hpp"
+
+#include <cmath>
+#include <vector>
+
+namespace oracle_trbdf2 {
+
+using dgns::Field;
+
+struct StepParams {
+  double dt = 1e-3;
+  double Re = 100.0;
+  double c = 1e3;         // artificial sound speed
+  double time = 0.0;      // t^n
+  int restart = 50;       // GMRES restart (krylov.hpp:28; cfg3 uses 30)
+  double tol_mom = 1e-10;
+  double tol_p = 1e-10;
+  double tol_mass = 1e-12;
+  int max_iter = 10000;
+  bool first_step = true;   // n = 0: w1 = u^0
+};
+
+struct StepStats {
+  int gmres_its[2] = {0, 0};
+  int cg_its[2] = {0, 0};
+  int mass_its[4] = {0, 0, 0, 0};
+  double gmres_res[2] = {0, 0};
+  double cg_res[2] = {0, 0};
+};
+
+// y = a*x + b*y
+inline void lincomb(double a, const Field& x, double b, const Field& y, Field& out) {
+  out.resize(x.size());
+  for (std::size_t i = 0; i < x.size(); ++i) out[i] = a * x[i] + b * y[i];
+}
+
+/// Solve M_u ut = pressure_gradient_rhs(p) (CG + Jacobi(mass_diagonal), rel 1e-12, x0 = 0).
+template <int dim>
+int projected_gradient(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<dim>& Vp,
+                       const dgns::GeometryCache<dim>& geom, const Field& p,
+                       const StepParams& P, Field& ut) {
+  Field g;
+  dgns::pressure_gradient_rhs(Vu, Vp, geom, p, g);
+  Field md;
+  dgns::mass_diagonal(Vu, geom, md);
+  const dgns::JacobiPreconditioner M(md);
+  dgns::SolverSettings s;
+  s.rel_tol = P.tol_mass;
+  s.max_iter = P.max_iter;
+  ut.assign(Vu.n_dofs(), 0.0);
+  Field tmp;
+  auto res = dgns::cg_solve(
+      Vu.n_dofs(), [&](const double* x, double* y) {
+        Field xx(x, x + Vu.n_dofs());
+        dgns::apply_mass(Vu, geom, xx, tmp);
+        std::copy(tmp.begin(), tmp.end(), y);
+      },
+      g.data(), s, &M, ut.data());
+  return res.iterations;
+}
+
+/// One stage.  alpha = gamma (stage 1) or 1-gamma (stage 2).
+template <int dim>
+void stage(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<dim>& Vp,
+           const dgns::GeometryCache<dim>& geom, const dgns::BoundaryTable<dim>& bc,
+           const dgns::MomentumCtx<dim>& ctx, const dgns::MomentumRhs<dim>& rhs, double alpha,
+           const Field& u_guess, const Field& p_old, const StepParams& P, Field& u_new,
+           Field& p_new, StepStats& st, int si) {
+  const int nu = Vu.n_dofs(), np = Vp.n_dofs();
+  // momentum: u*
+  Field F;
+  dgns::momentum_rhs(Vu, Vp, geom, rhs, F);
+  Field diag;
+  dgns::momentum_diagonal(Vu, geom, ctx, diag);
+  const dgns::JacobiPreconditioner Mu(diag);
+  dgns::SolverSettings sm;
+  sm.rel_tol = P.tol_mom;
+  sm.restart = P.restart;
+  sm.max_iter = P.max_iter;
+  Field ustar = u_guess;
+  Field tmp;
+  auto rg = dgns::gmres_solve(
+      nu, [&](const double* x, double* y) {
+        Field xx(x, x + nu);
+        dgns::apply_momentum(Vu, geom, ctx, xx, tmp);
+        std::copy(tmp.begin(), tmp.end(), y);
+      },
+      F.data(), sm, &Mu, ustar.data());
+  st.gmres_its[si] = rg.iterations;
+  st.gmres_res[si] = rg.residual;
+
+  const double adt = alpha * P.dt;
+  // u** = u* + alpha dt M^-1 G p_old
+  Field ut_old;
+  st.mass_its[2 * si] = projected_gradient(Vu, Vp, geom, p_old, P, ut_old);
+  Field uss(nu);
+  for (int i = 0; i < nu; ++i) uss[i] = ustar[i] + adt * ut_old[i];
+
+  // pressure Helmholtz
+  const double mass_coef = 1.0 / (P.c * P.c * adt * adt);
+  Field prhs;
+  dgns::pressure_rhs(Vu, Vp, geom, 1.0 / adt, uss, mass_coef, &p_old, &bc, prhs);
+  Field hd;
+  dgns::helmholtz_diagonal(Vp, geom, mass_coef, hd);
+  const dgns::JacobiPreconditioner Mp(hd);
+  dgns::SolverSettings sp;
+  sp.rel_tol = P.tol_p;
+  sp.max_iter = P.max_iter;
+  p_new = p_old;
+  auto rc = dgns::cg_solve(
+      np, [&](const double* x, double* y) {
+        Field xx(x, x + np);
+        dgns::apply_pressure_helmholtz(Vp, geom, mass_coef, xx, tmp);
+        std::copy(tmp.begin(), tmp.end(), y);
+      },
+      prhs.data(), sp, &Mp, p_new.data());
+  st.cg_its[si] = rc.iterations;
+  st.cg_res[si] = rc.residual;
+
+  // u = u** - alpha dt M^-1 G p_new
+  Field ut_new;
+  st.mass_its[2 * si + 1] = projected_gradient(Vu, Vp, geom, p_new, P, ut_new);
+  u_new.resize(nu);
+  for (int i = 0; i < nu; ++i) u_new[i] = uss[i] - adt * ut_new[i];
+}
+
+/// One TR-BDF2 step: (u^{n-1}, u^n, p^n) -> (u^{n+1}, p^{n+1}).
+template <int dim>
+void trbdf2_step(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<dim>& Vp,
+                 const dgns::GeometryCache<dim>& geom, const dgns::BoundaryTable<dim>& bc,
+                 const StepParams& P, const Field& u_nm1, const Field& u_n, const Field& p_n,
+                 Field& u_np1, Field& p_np1, StepStats& st) {
+  const double g = 2.0 - std::sqrt(2.0);
+  const double dt = P.dt, Re = P.Re;
+
+  // ---- stage 1 (alpha = gamma) ----
+  Field w1;
+  if (P.first_step)
+    w1 = u_n;
+  else
+    lincomb(1.0 + g / (2.0 * (1.0 - g)), u_n, -g / (2.0 * (1.0 - g)), u_nm1, w1);
+  dgns::MomentumCtx<dim> c1;
+  c1.mass_coef = 1.0 / (g * dt);
+  c1.visc_coef = 1.0 / (2.0 * Re);
+  c1.adv_coef = 0.5;
+  c1.skew_coef = 0.0;
+  c1.advecting = &w1;
+  c1.bc = &bc;
+  dgns::MomentumRhs<dim> r1;
+  r1.mass = {{1.0 / (g * dt), &u_n}};
+  r1.visc = {{1.0 / (2.0 * Re), &u_n}};
+  r1.adv = {{0.5, &u_n, &w1}};
+  r1.pres = {{1.0, &p_n}};
+  r1.dir_visc_coef = 1.0 / (2.0 * Re);
+  r1.dir_adv_coef = 0.5;
+  r1.dir_w = &w1;
+  r1.time = P.time + g * dt;
+  r1.bc = &bc;
+  Field u_g, p_g;
+  stage(Vu, Vp, geom, bc, c1, r1, g, u_n, p_n, P, u_g, p_g, st, 0);
+
+  // ---- stage 2 (alpha = 1 - gamma) ----
+  const double a33 = 1.0 / (2.0 - g);
+  const double a31 = (1.0 - g) / (2.0 * (2.0 - g));
+  const double a32 = a31;
+  Field w2;
+  lincomb(1.0 + (1.0 - g) / g, u_g, -(1.0 - g) / g, u_n, w2);
+  dgns::MomentumCtx<dim> c2;
+  c2.mass_coef = 1.0 / ((1.0 - g) * dt);
+  c2.visc_coef = a33 / Re;
+  c2.adv_coef = a33;
+  c2.skew_coef = 0.0;
+  c2.advecting = &w2;
+  c2.bc = &bc;
+  dgns::MomentumRhs<dim> r2;
+  r2.mass = {{1.0 / ((1.0 - g) * dt), &u_g}};
+  r2.visc = {{a32 / Re, &u_g}, {a31 / Re, &u_n}};
+  r2.adv = {{a32, &u_g, &u_g}, {a31, &u_n, &u_n}};
+  r2.pres = {{1.0, &p_g}};
+  r2.dir_visc_coef = a33 / Re;
+  r2.dir_adv_coef = a33;
+  r2.dir_w = &w2;
+  r2.time = P.time + dt;
+  r2.bc = &bc;
+  stage(Vu, Vp, geom, bc, c2, r2, 1.0 - g, u_g, p_g, P, u_np1, p_np1, st, 1);
+}
+
+}  // namespace oracle_trbdf2

@@ -1,0 +1,526 @@
+"""B200-native DG / TR-BDF2 hot path: Python mirror of the reference interface.
+
+The reference (``/root/reference/proj/src``) exposes free C++ functions over
+``FunctionSpace`` / ``GeometryCache`` / ``Field`` (forms.hpp:105-170) and the
+Krylov solvers (krylov.hpp:22-66).  This module mirrors those names, argument
+meanings and error behaviour on top of the C-ABI ``libdgb.so`` (include/dgb.h);
+fields are CUDA ``torch.float64`` tensors in the reference DoF layout
+(space.hpp:5-8).  There is no CPU fallback: without the built extension or a
+GPU every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdgb.so")
+
+# status codes (include/dgb.h)
+OK, E_ARG, E_NO_CONVERGENCE, E_BREAKDOWN, E_NOT_SPD, E_ZERO_DIAG, E_CUDA, E_UNSUPPORTED, E_MISSING_FIELD = range(9)
+BC_DIRICHLET, BC_OUTLET = 0, 1
+SPACE_U, SPACE_P = 0, 1
+OP_MOMENTUM, OP_PRESSURE, OP_MASS_U, OP_MASS_P, OP_LAPLACE = range(5)
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_llp = C.POINTER(C.c_longlong)
+
+
+class SolverError(RuntimeError):
+    """krylov.hpp:31-36: raised on non-convergence / breakdown, carries the residual history."""
+
+    def __init__(self, msg: str, history: Sequence[float] = ()):
+        super().__init__(msg)
+        self.history = list(history)
+
+
+class DGBError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[dgb status {code}] {msg}")
+        self.code = code
+
+
+class _RhsDesc(C.Structure):
+    _fields_ = [
+        ("n_mass", C.c_int), ("n_visc", C.c_int), ("n_adv", C.c_int), ("n_pres", C.c_int),
+        ("mass_coef", C.c_double * 4), ("visc_coef", C.c_double * 4),
+        ("adv_coef", C.c_double * 4), ("pres_coef", C.c_double * 4),
+        ("mass_f", C.c_void_p * 4), ("visc_f", C.c_void_p * 4), ("adv_f", C.c_void_p * 4),
+        ("adv_w", C.c_void_p * 4), ("pres_f", C.c_void_p * 4),
+        ("dir_visc_coef", C.c_double), ("dir_adv_coef", C.c_double), ("dir_w", C.c_void_p),
+    ]
+
+
+class _Settings(C.Structure):
+    _fields_ = [("rel_tol", C.c_double), ("abs_tol", C.c_double), ("max_iter", C.c_int), ("restart", C.c_int)]
+
+
+class _Result(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("residual", C.c_double)]
+
+
+class _Operator(C.Structure):
+    _fields_ = [("op", C.c_int), ("coefs", C.c_double * 4), ("d_w", C.c_void_p), ("dirichlet_bdry", C.c_int)]
+
+
+class _StepParams(C.Structure):
+    _fields_ = [("dt", C.c_double), ("Re", C.c_double), ("c", C.c_double), ("time", C.c_double),
+                ("restart", C.c_int), ("tol_mom", C.c_double), ("tol_p", C.c_double),
+                ("tol_mass", C.c_double), ("max_iter", C.c_int), ("first_step", C.c_int)]
+
+
+BC_FN = C.CFUNCTYPE(None, _dp, C.c_double, _dp, C.c_void_p)
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libdgb.so (fails loudly if the extension has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: build it with `make -C paper_2107_07776_b200` "
+                          "(or __graft_entry__.build()); there is no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    L.dgb_last_error.restype = C.c_char_p
+    L.dgb_version.restype = C.c_char_p
+    L.dgb_ctx_create_cartesian.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint, C.c_int, C.c_int, C.c_int,
+                                           C.POINTER(C.c_void_p)]
+    L.dgb_ctx_create_mesh.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _ip, _ip, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(C.c_void_p)]
+    L.dgb_ctx_destroy.argtypes = [C.c_void_p]
+    L.dgb_ctx_destroy.restype = None
+    L.dgb_ctx_info.argtypes = [C.c_void_p, _llp]
+    L.dgb_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+    L.dgb_sync.argtypes = [C.c_void_p]
+    L.dgb_set_boundary_type.argtypes = [C.c_void_p, C.c_int, C.c_int]
+    L.dgb_set_dirichlet_table.argtypes = [C.c_void_p, _dp]
+    L.dgb_set_dirichlet_fn.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_double]
+    L.dgb_boundary_points.argtypes = [C.c_void_p, C.c_int, _dp]
+    L.dgb_node_points.argtypes = [C.c_void_p, C.c_int, _dp]
+    L.dgb_face_lists.argtypes = [C.c_void_p, _ip, _ip]
+    for name in ("dgb_copy_h2d", "dgb_copy_d2h", "dgb_copy_d2d"):
+        getattr(L, name).argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t]
+    L.dgb_fill.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_size_t]
+    L.dgb_momentum_apply.argtypes = [C.c_void_p, _dp, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.dgb_momentum_diag.argtypes = [C.c_void_p, _dp, C.c_void_p, C.c_void_p]
+    L.dgb_pressure_apply.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
+    L.dgb_helmholtz_diag.argtypes = [C.c_void_p, C.c_double, C.c_void_p]
+    L.dgb_laplace_apply.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    L.dgb_laplace_diag.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+    L.dgb_mass_apply.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
+    L.dgb_mass_diag.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+    L.dgb_momentum_rhs.argtypes = [C.c_void_p, C.POINTER(_RhsDesc), C.c_void_p]
+    L.dgb_divergence.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    L.dgb_pressure_rhs.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
+    L.dgb_pressure_gradient.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+    L.dgb_kinetic_energy.argtypes = [C.c_void_p, C.c_void_p, _dp]
+    L.dgb_axpy.argtypes = [C.c_void_p, C.c_size_t, C.c_double, C.c_void_p, C.c_void_p]
+    L.dgb_axpby.argtypes = [C.c_void_p, C.c_size_t, C.c_double, C.c_void_p, C.c_double, C.c_void_p]
+    L.dgb_scal.argtypes = [C.c_void_p, C.c_size_t, C.c_double, C.c_void_p]
+    L.dgb_dot.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, _dp]
+    L.dgb_max_abs_diff.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, _dp]
+    L.dgb_jacobi_inverse.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
+    for name in ("dgb_cg", "dgb_gmres"):
+        getattr(L, name).argtypes = [C.c_void_p, C.POINTER(_Operator), C.POINTER(_Settings), C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.POINTER(_Result), _dp, C.c_int, _ip]
+    L.dgb_trbdf2_step.argtypes = [C.c_void_p, C.POINTER(_StepParams), C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, _ip]
+    L.dgb_seeded_uniform.argtypes = [C.c_ulonglong, C.c_size_t, C.c_double, C.c_double, _dp]
+    L.dgb_synth_init.argtypes = [C.c_int, C.c_ulonglong, C.c_double, _dp]
+    L.dgb_synth_eval.argtypes = [_dp, C.c_double, _dp, C.c_void_p]
+    L.dgb_synth_eval.restype = None
+    L.dgb_interpolate_synth.argtypes = [C.c_void_p, _dp, _dp]
+    L.dgb_timer_start.argtypes = [C.c_void_p]
+    L.dgb_timer_stop.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
+    L.dgb_fp64_peak.argtypes = [C.c_void_p, _dp]
+    L.dgb_launch_count.argtypes = [C.c_void_p]
+    L.dgb_launch_count.restype = C.c_longlong
+    L.dgb_host_mesh_cartesian.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint, _llp, _ip, _ip, _dp, _dp, _dp]
+    L.dgb_host_tables.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _dp]
+    _lib = L
+    return L
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    import torch
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError("fields must be contiguous CUDA float64 tensors")
+    return t.data_ptr()
+
+
+def _np_ptr(a):
+    return a.ctypes.data_as(_dp)
+
+
+def _check(code: int) -> None:
+    if code != OK:
+        msg = lib().dgb_last_error().decode()
+        if code == E_MISSING_FIELD:
+            raise RuntimeError(msg)
+        if code == E_ZERO_DIAG:
+            raise SolverError(msg, [])
+        raise DGBError(code, msg)
+
+
+# ---------------------------------------------------------------------------
+# Context = (Mesh, GeometryCache, FunctionSpace Vu, FunctionSpace Vp) on one GPU
+# ---------------------------------------------------------------------------
+@dataclass
+class BoundaryTable:
+    """forms.hpp:29-51: per boundary id a type and optional data callback g(x, t)."""
+    types: dict = field(default_factory=dict)
+
+
+class DGContext:
+    """Device-resident mesh + geometry + the velocity (degree ku, dim comps) and
+    pressure (degree kp, scalar) spaces.  Mirrors what the reference builds from
+    ``generate_cartesian`` / ``distort`` / ``GeometryCache`` / ``FunctionSpace``."""
+
+    def __init__(self, dim: int, n_el: int, ku: int, kp: int, distort_amp: float = 0.0, distort_seed: int = 0,
+                 device: int = 0, *, mesh_arrays=None):
+        import torch
+        L = lib()
+        h = C.c_void_p()
+        if mesh_arrays is None:
+            _check(L.dgb_ctx_create_cartesian(dim, n_el, float(distort_amp), distort_seed, ku, kp, device,
+                                              C.byref(h)))
+        else:
+            import numpy as np
+            verts, cells, bids = mesh_arrays
+            verts = np.ascontiguousarray(verts, dtype=np.float64)
+            cells = np.ascontiguousarray(cells, dtype=np.int32)
+            bids = np.ascontiguousarray(bids, dtype=np.int32)
+            _check(L.dgb_ctx_create_mesh(dim, verts.shape[0], _np_ptr(verts), cells.shape[0],
+                                         cells.ctypes.data_as(_ip), bids.ctypes.data_as(_ip), ku, kp, device,
+                                         C.byref(h)))
+        self._h = h
+        self.device = device
+        info = (C.c_longlong * 16)()
+        _check(L.dgb_ctx_info(h, info))
+        (self.ncells, self.n_u, self.n_p, self.n_interior, self.n_boundary, self.ku, self.kp, self.dim,
+         affine, self.nqf_bdry) = [int(v) for v in info[:10]]
+        self.affine = bool(affine)
+        # run on torch's current stream so torch ops and our kernels are ordered
+        with torch.cuda.device(device):
+            self.stream = torch.cuda.current_stream()
+        _check(L.dgb_set_stream(h, C.c_void_p(self.stream.cuda_stream)))
+        self._keep = []
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dgb_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- fields -----------------------------------------------------------
+    def zeros(self, space: int = SPACE_U):
+        import torch
+        n = self.n_u if space == SPACE_U else self.n_p
+        return torch.zeros(n, dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def sync(self):
+        _check(lib().dgb_sync(self._h))
+
+    # -- boundary table ---------------------------------------------------
+    def set_boundary_type(self, boundary_id: int, bc_type: int):
+        _check(lib().dgb_set_boundary_type(self._h, boundary_id, bc_type))
+
+    def set_dirichlet_table(self, g):
+        import numpy as np
+        g = None if g is None else np.ascontiguousarray(g, dtype=np.float64)
+        _check(lib().dgb_set_dirichlet_table(self._h, None if g is None else _np_ptr(g)))
+
+    def set_dirichlet_fn(self, boundary_id: int, fn_ptr, user, t: float = 0.0):
+        """fn_ptr: a C function pointer (e.g. lib().dgb_synth_eval) with its user data."""
+        _check(lib().dgb_set_dirichlet_fn(self._h, boundary_id, C.cast(fn_ptr, C.c_void_p), user, t))
+
+    def boundary_points(self, q1d: int):
+        import numpy as np
+        nq = q1d ** (self.dim - 1)
+        out = np.zeros((self.n_boundary, nq, self.dim))
+        _check(lib().dgb_boundary_points(self._h, q1d, _np_ptr(out)))
+        return out
+
+    def face_lists(self):
+        import numpy as np
+        it = np.zeros((self.n_interior, 4), dtype=np.int32)
+        bd = np.zeros((self.n_boundary, 3), dtype=np.int32)
+        _check(lib().dgb_face_lists(self._h, it.ctypes.data_as(_ip), bd.ctypes.data_as(_ip)))
+        return it, bd
+
+    def launch_count(self) -> int:
+        return int(lib().dgb_launch_count(self._h))
+
+
+# ---------------------------------------------------------------------------
+# forms.hpp mirror
+# ---------------------------------------------------------------------------
+@dataclass
+class MomentumCtx:
+    """forms.hpp:56-64"""
+    mass_coef: float = 0.0
+    visc_coef: float = 0.0
+    adv_coef: float = 0.0
+    skew_coef: float = 0.0
+    advecting: object = None  # CUDA tensor (w)
+
+    def coefs(self):
+        return (C.c_double * 4)(self.mass_coef, self.visc_coef, self.adv_coef, self.skew_coef)
+
+
+@dataclass
+class MomentumRhs:
+    """forms.hpp:89-100 (lists of (coef, field) / (coef, field, w))."""
+    mass: List[Tuple[float, object]] = field(default_factory=list)
+    visc: List[Tuple[float, object]] = field(default_factory=list)
+    adv: List[Tuple[float, object, object]] = field(default_factory=list)
+    pres: List[Tuple[float, object]] = field(default_factory=list)
+    dir_visc_coef: float = 0.0
+    dir_adv_coef: float = 0.0
+    dir_w: object = None
+
+
+def apply_momentum(V: DGContext, ctx: MomentumCtx, x, out):
+    _check(lib().dgb_momentum_apply(V.handle, ctx.coefs(), _ptr(ctx.advecting), _ptr(x), _ptr(out)))
+
+
+def momentum_diagonal(V: DGContext, ctx: MomentumCtx, diag):
+    _check(lib().dgb_momentum_diag(V.handle, ctx.coefs(), _ptr(ctx.advecting), _ptr(diag)))
+
+
+def apply_pressure_helmholtz(V: DGContext, mass_coef: float, x, out):
+    _check(lib().dgb_pressure_apply(V.handle, float(mass_coef), _ptr(x), _ptr(out)))
+
+
+def helmholtz_diagonal(V: DGContext, mass_coef: float, diag):
+    _check(lib().dgb_helmholtz_diag(V.handle, float(mass_coef), _ptr(diag)))
+
+
+def apply_scalar_laplace(V: DGContext, dirichlet_bdry: bool, x, out):
+    _check(lib().dgb_laplace_apply(V.handle, int(bool(dirichlet_bdry)), _ptr(x), _ptr(out)))
+
+
+def scalar_laplace_diagonal(V: DGContext, dirichlet_bdry: bool, diag):
+    _check(lib().dgb_laplace_diag(V.handle, int(bool(dirichlet_bdry)), _ptr(diag)))
+
+
+def apply_mass(V: DGContext, space: int, x, out):
+    _check(lib().dgb_mass_apply(V.handle, space, _ptr(x), _ptr(out)))
+
+
+def mass_diagonal(V: DGContext, space: int, diag):
+    _check(lib().dgb_mass_diag(V.handle, space, _ptr(diag)))
+
+
+def momentum_rhs(V: DGContext, spec: MomentumRhs, out):
+    d = _RhsDesc()
+    for name in ("mass", "visc", "pres"):
+        terms = getattr(spec, name)
+        if len(terms) > 4:
+            raise ValueError("at most 4 terms per list")
+        setattr(d, "n_" + name, len(terms))
+        for i, (c, f) in enumerate(terms):
+            getattr(d, name + "_coef")[i] = c
+            getattr(d, name + "_f")[i] = _ptr(f)
+    d.n_adv = len(spec.adv)
+    for i, (c, f, w) in enumerate(spec.adv):
+        d.adv_coef[i] = c
+        d.adv_f[i] = _ptr(f)
+        d.adv_w[i] = _ptr(w)
+    d.dir_visc_coef = spec.dir_visc_coef
+    d.dir_adv_coef = spec.dir_adv_coef
+    d.dir_w = _ptr(spec.dir_w)
+    _check(lib().dgb_momentum_rhs(V.handle, C.byref(d), _ptr(out)))
+
+
+def divergence_functional(V: DGContext, u, out):
+    _check(lib().dgb_divergence(V.handle, _ptr(u), _ptr(out)))
+
+
+def pressure_rhs(V: DGContext, inv_adt: float, u, mass_coef: float, p_old, out):
+    _check(lib().dgb_pressure_rhs(V.handle, float(inv_adt), _ptr(u), float(mass_coef), _ptr(p_old), _ptr(out)))
+
+
+def pressure_gradient_rhs(V: DGContext, p, out):
+    _check(lib().dgb_pressure_gradient(V.handle, _ptr(p), _ptr(out)))
+
+
+def kinetic_energy(V: DGContext, u) -> float:
+    r = C.c_double()
+    _check(lib().dgb_kinetic_energy(V.handle, _ptr(u), C.byref(r)))
+    return r.value
+
+
+# ---------------------------------------------------------------------------
+# krylov.hpp mirror
+# ---------------------------------------------------------------------------
+@dataclass
+class SolverSettings:
+    """krylov.hpp:24-29"""
+    rel_tol: float = 1e-10
+    abs_tol: float = 0.0
+    max_iter: int = 10000
+    restart: int = 50
+
+
+@dataclass
+class SolveResult:
+    iterations: int
+    residual: float
+
+
+class JacobiPreconditioner:
+    """krylov.hpp:40-48: holds 1/diag; raises SolverError naming the first zero-diagonal dof."""
+
+    def __init__(self, V: DGContext, diag):
+        self.inv = diag.new_empty(diag.shape)
+        _check(lib().dgb_jacobi_inverse(V.handle, diag.numel(), _ptr(diag), _ptr(self.inv)))
+
+
+@dataclass
+class LinearOperator:
+    """The LinearOp closure of krylov.hpp:22, restricted to the device operators."""
+    op: int
+    coefs: Tuple[float, float, float, float] = (0.0, 0.0, 0.0, 0.0)
+    w: object = None
+    dirichlet_bdry: bool = False
+
+    @staticmethod
+    def momentum(ctx: MomentumCtx):
+        return LinearOperator(OP_MOMENTUM, (ctx.mass_coef, ctx.visc_coef, ctx.adv_coef, ctx.skew_coef), ctx.advecting)
+
+    @staticmethod
+    def pressure_helmholtz(mass_coef: float):
+        return LinearOperator(OP_PRESSURE, (mass_coef, 0.0, 0.0, 0.0))
+
+    def _c(self):
+        o = _Operator()
+        o.op = self.op
+        for i in range(4):
+            o.coefs[i] = self.coefs[i]
+        o.d_w = _ptr(self.w)
+        o.dirichlet_bdry = int(self.dirichlet_bdry)
+        return o
+
+
+def _solve(fn, V, A: LinearOperator, b, s: SolverSettings, M: Optional[JacobiPreconditioner], x):
+    res = _Result()
+    cap = 100000
+    import numpy as np
+    hist = np.zeros(cap)
+    hl = C.c_int()
+    st = _Settings(s.rel_tol, s.abs_tol, s.max_iter, s.restart)
+    op = A._c()
+    code = fn(V.handle, C.byref(op), C.byref(st), _ptr(M.inv) if M is not None else None, _ptr(b), _ptr(x),
+              C.byref(res), _np_ptr(hist), cap, C.byref(hl))
+    if code in (E_NO_CONVERGENCE, E_BREAKDOWN, E_NOT_SPD):
+        raise SolverError(lib().dgb_last_error().decode(), hist[: min(hl.value, cap)].tolist())
+    _check(code)
+    return SolveResult(res.iterations, res.residual)
+
+
+def cg_solve(V: DGContext, A: LinearOperator, b, s: SolverSettings, M: Optional[JacobiPreconditioner], x):
+    """krylov.hpp:58-60: x is initial guess and solution."""
+    return _solve(lib().dgb_cg, V, A, b, s, M, x)
+
+
+def gmres_solve(V: DGContext, A: LinearOperator, b, s: SolverSettings, M: Optional[JacobiPreconditioner], x):
+    """krylov.hpp:64-66"""
+    return _solve(lib().dgb_gmres, V, A, b, s, M, x)
+
+
+# ---------------------------------------------------------------------------
+# TR-BDF2 step
+# ---------------------------------------------------------------------------
+@dataclass
+class StepParams:
+    dt: float = 1e-3
+    Re: float = 100.0
+    c: float = 1e3
+    time: float = 0.0
+    restart: int = 50
+    tol_mom: float = 1e-10
+    tol_p: float = 1e-10
+    tol_mass: float = 1e-12
+    max_iter: int = 10000
+    first_step: bool = True
+
+    def _c(self):
+        return _StepParams(self.dt, self.Re, self.c, self.time, self.restart, self.tol_mom, self.tol_p,
+                           self.tol_mass, self.max_iter, int(self.first_step))
+
+
+def trbdf2_step(V: DGContext, P: StepParams, u_nm1, u_n, p_n, u_np1, p_np1) -> List[int]:
+    its = (C.c_int * 8)()
+    code = lib().dgb_trbdf2_step(V.handle, C.byref(P._c()), _ptr(u_nm1), _ptr(u_n), _ptr(p_n), _ptr(u_np1),
+                                 _ptr(p_np1), its)
+    if code in (E_NO_CONVERGENCE, E_BREAKDOWN, E_NOT_SPD):
+        raise SolverError(lib().dgb_last_error().decode())
+    _check(code)
+    return list(its)
+
+
+# ---------------------------------------------------------------------------
+# synthetic inputs (BASELINE.json configs)
+# ---------------------------------------------------------------------------
+def seeded_uniform(seed: int, n: int, lo: float = -1.0, hi: float = 1.0):
+    import numpy as np
+    out = np.empty(n)
+    _check(lib().dgb_seeded_uniform(seed, n, lo, hi, _np_ptr(out)))
+    return out
+
+
+class SynthField:
+    """Curl of a random stream function (2D) / vector potential (3D)."""
+
+    def __init__(self, dim: int, seed: int, scale: float = 1.0):
+        import numpy as np
+        self.user = np.zeros(512)
+        _check(lib().dgb_synth_init(dim, seed, scale, _np_ptr(self.user)))
+        self.dim = dim
+
+    @property
+    def user_ptr(self):
+        return self.user.ctypes.data_as(C.c_void_p)
+
+    @property
+    def fn_ptr(self):
+        return C.cast(lib().dgb_synth_eval, C.c_void_p)
+
+    def eval(self, x):
+        import numpy as np
+        out = np.zeros(self.dim)
+        xx = np.ascontiguousarray(x, dtype=np.float64)
+        lib().dgb_synth_eval(_np_ptr(xx), 0.0, _np_ptr(out), self.user_ptr)
+        return out
+
+    def interpolate(self, V: DGContext):
+        import numpy as np
+        out = np.zeros(V.n_u)
+        _check(lib().dgb_interpolate_synth(V.handle, _np_ptr(self.user), _np_ptr(out)))
+        return out
+
+
+def fp64_peak_tflops(V: DGContext) -> float:
+    r = C.c_double()
+    _check(lib().dgb_fp64_peak(V.handle, C.byref(r)))
+    return r.value
+
+
+__all__ = [n for n in dir() if not n.startswith("_")]

@@ -1,0 +1,715 @@
+// Device context, operator wrappers, Krylov solvers and the device TR-BDF2 step.
+#include "context.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "blas.cuh"
+
+namespace dgb {
+
+#define CK(call)                                             \
+  do {                                                       \
+    cudaError_t e_ = (call);                                 \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);      \
+  } while (0)
+#define OK(call)                     \
+  do {                               \
+    int s_ = (call);                 \
+    if (s_ != DGB_OK) return s_;     \
+  } while (0)
+
+int Context::fail(int code, const std::string& msg) {
+  err = msg;
+  return code;
+}
+int Context::cuda_fail(cudaError_t e, const char* where) {
+  if (e == cudaErrorNotSupported) return fail(DGB_E_UNSUPPORTED, std::string("unsupported configuration in ") + where);
+  return fail(DGB_E_CUDA, std::string(cudaGetErrorString(e)) + " in " + where);
+}
+
+void* Context::dalloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes < 8 ? 8 : bytes) != cudaSuccess) return nullptr;
+  allocs_.push_back(p);
+  return p;
+}
+
+Context::~Context() {
+  if (device >= 0) cudaSetDevice(device);
+  if (dc.stream) cudaStreamSynchronize(dc.stream);
+  for (void* p : allocs_) cudaFree(p);
+  for (auto& s : slots_) cudaFree(s.first);
+  for (double* v : gm_basis_) cudaFree(v);
+  if (h_res_) cudaFreeHost(h_res_);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
+  mesh = std::move(m);
+  dim = mesh.dim;
+  ku = ku_;
+  kp = kp_;
+  device = device_;
+  if (ku < 1 || kp < 1 || ku > 4 || kp > 4) {
+    e = "unsupported degrees (device path covers 1 <= k <= 4)";
+    return DGB_E_UNSUPPORTED;
+  }
+  opu = ops_for(dim, ku);
+  opp = ops_for(dim, kp);
+  if (!opu || !opp) {
+    e = "unsupported dimension";
+    return DGB_E_UNSUPPORTED;
+  }
+  cudaError_t ce = cudaSetDevice(device);
+  if (ce != cudaSuccess) {
+    e = cudaGetErrorString(ce);
+    return DGB_E_CUDA;
+  }
+  if ((ce = cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+      (ce = blas_init(device)) != cudaSuccess || (ce = opu->tables()) != cudaSuccess ||
+      (ce = opp->tables()) != cudaSuccess || (ce = cudaEventCreate(&ev0)) != cudaSuccess ||
+      (ce = cudaEventCreate(&ev1)) != cudaSuccess) {
+    e = std::string("context init: ") + cudaGetErrorString(ce);
+    return DGB_E_CUDA;
+  }
+  dc.stream = own_stream;
+  dc.dim = dim;
+  dc.ku = ku;
+  dc.kp = kp;
+  dc.ncells = mesh.ncells;
+  dc.affine = mesh.affine;
+  const int nf = 2 * dim;
+  const size_t nslot = (size_t)mesh.ncells * nf;
+  // penalty ratios (forms.cpp:111-129): interior mean of both sides, boundary own side
+  std::vector<double> pen(nslot);
+  std::vector<int> bslot(nslot, -1);
+  for (int c = 0; c < mesh.ncells; ++c)
+    for (int f = 0; f < nf; ++f) {
+      const size_t s = (size_t)c * nf + f;
+      const int nb = mesh.nbr[s];
+      const double fm = mesh.face_measure[s];
+      pen[s] = nb >= 0 ? 0.5 * (fm / mesh.cell_measure[c] + fm / mesh.cell_measure[nb]) : fm / mesh.cell_measure[c];
+    }
+  for (size_t b = 0; b < n_bface(); ++b) bslot[(size_t)mesh.bface[3 * b] * nf + mesh.bface[3 * b + 1]] = (int)b;
+  int* d_nbr = (int*)dalloc(nslot * sizeof(int));
+  double* d_pen = (double*)dalloc(nslot * sizeof(double));
+  int* d_bslot = (int*)dalloc(nslot * sizeof(int));
+  int* d_bct = (int*)dalloc(64 * sizeof(int));
+  d_partial_ = (double*)dalloc(4096 * sizeof(double));
+  d_res_ = (double*)dalloc(64 * sizeof(double));
+  d_bad_ = (long long*)dalloc(sizeof(long long));
+  if (!d_nbr || !d_pen || !d_bslot || !d_bct || !d_partial_ || !d_res_ || !d_bad_) {
+    e = "out of device memory";
+    return DGB_E_CUDA;
+  }
+  cudaMemcpy(d_nbr, mesh.nbr.data(), nslot * sizeof(int), cudaMemcpyHostToDevice);
+  cudaMemcpy(d_pen, pen.data(), nslot * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(d_bslot, bslot.data(), nslot * sizeof(int), cudaMemcpyHostToDevice);
+  cudaMemcpy(d_bct, bctype_h, sizeof(bctype_h), cudaMemcpyHostToDevice);
+  if (cudaHostAlloc((void**)&h_res_, 64 * sizeof(double), cudaHostAllocDefault) != cudaSuccess) {
+    e = "pinned alloc failed";
+    return DGB_E_CUDA;
+  }
+  dc.mesh.ncells = mesh.ncells;
+  dc.mesh.nbr = d_nbr;
+  dc.mesh.pen = d_pen;
+  dc.mesh.bctype = d_bct;
+  dc.mesh.bslot = d_bslot;
+  // geometry (north-star item 3): per cell if affine, else per quadrature point
+  if (mesh.affine) {
+    std::vector<double> g;
+    build_affine_geometry(mesh, g);
+    double* d = (double*)dalloc(g.size() * sizeof(double));
+    if (!d) {
+      e = "out of device memory (geometry)";
+      return DGB_E_CUDA;
+    }
+    cudaMemcpy(d, g.data(), g.size() * sizeof(double), cudaMemcpyHostToDevice);
+    dc.aff = d;
+  } else {
+    const int rules[3] = {ku + 1, ku + 2, kp + 2};
+    for (int Q : rules) {
+      if (dc.qcell[Q]) continue;
+      QpGeometry g;
+      build_qp_geometry(mesh, Q, g);
+      double* dcell = (double*)dalloc(g.cell.size() * sizeof(double));
+      double* dface = (double*)dalloc(g.face.size() * sizeof(double));
+      if (!dcell || !dface) {
+        e = "out of device memory (qp geometry)";
+        return DGB_E_CUDA;
+      }
+      cudaMemcpy(dcell, g.cell.data(), g.cell.size() * sizeof(double), cudaMemcpyHostToDevice);
+      cudaMemcpy(dface, g.face.data(), g.face.size() * sizeof(double), cudaMemcpyHostToDevice);
+      dc.qcell[Q] = dcell;
+      dc.qface[Q] = dface;
+    }
+  }
+  // Dirichlet table (rule ku+2), zero until set
+  gtab_h_.assign(n_bface() * nqf(ku + 2) * dim, 0.0);
+  d_gtab_ = (double*)dalloc(gtab_h_.size() * sizeof(double));
+  if (!d_gtab_) {
+    e = "out of device memory (dirichlet table)";
+    return DGB_E_CUDA;
+  }
+  cudaMemset(d_gtab_, 0, gtab_h_.size() * sizeof(double));
+  ce = cudaDeviceSynchronize();
+  if (ce != cudaSuccess) {
+    e = cudaGetErrorString(ce);
+    return DGB_E_CUDA;
+  }
+  return DGB_OK;
+}
+
+double* Context::scratch_vec(int slot, size_t n) {
+  if ((int)slots_.size() <= slot) slots_.resize(slot + 1, {nullptr, 0});
+  auto& s = slots_[slot];
+  if (s.second < n) {
+    if (s.first) {
+      cudaStreamSynchronize(dc.stream);
+      cudaFree(s.first);
+    }
+    s.first = nullptr;
+    s.second = 0;
+    if (cudaMalloc(&s.first, n * sizeof(double)) != cudaSuccess) return nullptr;
+    s.second = n;
+  }
+  return s.first;
+}
+
+int Context::host_scalars(int n, double* out) {
+  CK(cudaMemcpyAsync(h_res_, d_res_, n * sizeof(double), cudaMemcpyDeviceToHost, dc.stream));
+  CK(cudaStreamSynchronize(dc.stream));
+  for (int i = 0; i < n; ++i) out[i] = h_res_[i];
+  return DGB_OK;
+}
+
+// ------------------------------------------------------------------ operators
+int Context::momentum(const double* coefs, const double* w, const double* x, double* y) {
+  const MomCoef co{coefs[0], coefs[1], coefs[2], coefs[3]};
+  if ((co.adv != 0.0 || co.skew != 0.0) && !w) return fail(DGB_E_MISSING_FIELD, "apply_momentum: advecting field missing");
+  ++launches;
+  CK(opu->momentum(dc, co, w, x, y));
+  return DGB_OK;
+}
+int Context::momentum_diag(const double* coefs, const double* w, double* d) {
+  const MomCoef co{coefs[0], coefs[1], coefs[2], coefs[3]};
+  if ((co.adv != 0.0 || co.skew != 0.0) && !w)
+    return fail(DGB_E_MISSING_FIELD, "momentum_diagonal: advecting field missing");
+  ++launches;
+  CK(opu->momentum_diag(dc, co, w, d));
+  return DGB_OK;
+}
+int Context::sip(double mc, int dir, const double* x, double* y) {
+  ++launches;
+  CK(opp->sip(dc, mc, dir, x, y));
+  return DGB_OK;
+}
+int Context::sip_diag(double mc, int dir, double* d) {
+  ++launches;
+  CK(opp->sip_diag(dc, mc, dir, d));
+  return DGB_OK;
+}
+int Context::mass(int space, const double* x, double* y) {
+  ++launches;
+  if (space == DGB_SPACE_U)
+    CK(opu->mass(dc, 0, x, y));
+  else
+    CK(opp->mass(dc, 1, x, y));
+  return DGB_OK;
+}
+int Context::mass_diag(int space, double* d) {
+  ++launches;
+  if (space == DGB_SPACE_U)
+    CK(opu->mass_diag(dc, 0, d));
+  else
+    CK(opp->mass_diag(dc, 1, d));
+  return DGB_OK;
+}
+int Context::rhs(const dgb_rhs_desc& ds, double* y) {
+  if (ds.n_mass > kMaxTerms || ds.n_visc > kMaxTerms || ds.n_adv > kMaxTerms || ds.n_pres > kMaxTerms ||
+      ds.n_mass < 0 || ds.n_visc < 0 || ds.n_adv < 0 || ds.n_pres < 0)
+    return fail(DGB_E_ARG, "momentum_rhs: at most 4 terms per list");
+  if (ds.dir_adv_coef != 0.0 && !ds.dir_w) return fail(DGB_E_MISSING_FIELD, "momentum_rhs: dir_w missing");
+  RhsArgs ra;
+  ra.nm = ds.n_mass;
+  ra.nv = ds.n_visc;
+  ra.na = ds.n_adv;
+  ra.np = ds.n_pres;
+  for (int i = 0; i < kMaxTerms; ++i) {
+    ra.mc[i] = ds.mass_coef[i];
+    ra.vc[i] = ds.visc_coef[i];
+    ra.ac[i] = ds.adv_coef[i];
+    ra.pc[i] = ds.pres_coef[i];
+    ra.mf[i] = ds.mass_f[i];
+    ra.vf[i] = ds.visc_f[i];
+    ra.af[i] = ds.adv_f[i];
+    ra.aw[i] = ds.adv_w[i];
+    ra.pf[i] = ds.pres_f[i];
+  }
+  ra.dvisc = ds.dir_visc_coef;
+  ra.dadv = ds.dir_adv_coef;
+  ra.dir_w = ds.dir_w;
+  ra.gtab = d_gtab_;
+  ++launches;
+  CK(opu->rhs(dc, ra, y));
+  return DGB_OK;
+}
+int Context::divergence(const double* u, double* y) {
+  ++launches;
+  CK(opu->divergence(dc, u, y));
+  return DGB_OK;
+}
+int Context::pressure_rhs(double inv_adt, const double* u, double mc, const double* p_old, double* y) {
+  OK(divergence(u, y));
+  if (inv_adt != 1.0) {
+    ++launches;
+    CK(v_scal(dc.stream, np(), inv_adt, y));
+  }
+  if (p_old && mc != 0.0) {
+    double* mp = scratch_vec(20, np());
+    if (!mp) return fail(DGB_E_CUDA, "out of memory");
+    OK(mass(DGB_SPACE_P, p_old, mp));
+    ++launches;
+    CK(v_axpy(dc.stream, np(), mc, mp, y));
+  }
+  return DGB_OK;
+}
+int Context::gradient(const double* p, double* y) {
+  ++launches;
+  CK(opu->gradient(dc, p, y));
+  return DGB_OK;
+}
+int Context::kinetic(const double* u, double* out) {
+  int nb = 0;
+  CK(opu->kinetic(dc, u, nullptr, &nb));
+  double* part = scratch_vec(21, nb);
+  if (!part) return fail(DGB_E_CUDA, "out of memory");
+  launches += 2;
+  CK(opu->kinetic(dc, u, part, &nb));
+  CK(r_sum(dc.stream, nb, part, d_res_));
+  return host_scalars(1, out);
+}
+
+size_t Context::op_size(const dgb_operator& op) const {
+  return (op.op == DGB_OP_MOMENTUM || op.op == DGB_OP_MASS_U) ? nu() : np();
+}
+int Context::apply_op(const dgb_operator& op, const double* x, double* y) {
+  switch (op.op) {
+    case DGB_OP_MOMENTUM: return momentum(op.coefs, op.d_w, x, y);
+    case DGB_OP_PRESSURE: return sip(op.coefs[0], 0, x, y);
+    case DGB_OP_MASS_U: return mass(DGB_SPACE_U, x, y);
+    case DGB_OP_MASS_P: return mass(DGB_SPACE_P, x, y);
+    case DGB_OP_LAPLACE: return sip(0.0, op.dirichlet_bdry, x, y);
+  }
+  return fail(DGB_E_ARG, "unknown operator id");
+}
+
+// ------------------------------------------------------------------ vectors
+int Context::dot(size_t n, const double* x, const double* y, double* out) {
+  launches += 2;
+  CK(r_dot(dc.stream, n, x, y, d_partial_, d_res_));
+  return host_scalars(1, out);
+}
+int Context::max_abs_diff(size_t n, const double* x, const double* y, double* out) {
+  launches += 2;
+  CK(r_maxabsdiff(dc.stream, n, x, y, d_partial_, d_res_));
+  return host_scalars(1, out);
+}
+int Context::jacobi_inverse(size_t n, const double* d, double* inv) {
+  const long long none = -1;
+  CK(cudaMemcpyAsync(d_bad_, &none, sizeof(none), cudaMemcpyHostToDevice, dc.stream));
+  ++launches;
+  CK(v_recip(dc.stream, n, d, inv, d_bad_));
+  long long bad = -1;
+  CK(cudaMemcpyAsync(&bad, d_bad_, sizeof(bad), cudaMemcpyDeviceToHost, dc.stream));
+  CK(cudaStreamSynchronize(dc.stream));
+  if (bad >= 0) return fail(DGB_E_ZERO_DIAG, "jacobi preconditioner: zero diagonal at dof " + std::to_string(bad));
+  return DGB_OK;
+}
+
+// ------------------------------------------------------------------ CG (krylov.cpp:43-101)
+int Context::cg(const dgb_operator& op, const dgb_solver_settings& s, const double* inv, const double* b,
+                double* x, SolveOut& out) {
+  const size_t n = op_size(op);
+  cudaStream_t st = dc.stream;
+  out = SolveOut();
+  double bb;
+  OK(dot(n, b, b, &bb));
+  const double bnorm = std::sqrt(bb);
+  if (bnorm == 0.0) {
+    ++launches;
+    CK(v_fill(st, n, 0.0, x));
+    return DGB_OK;
+  }
+  const double tol = std::max(s.rel_tol * bnorm, s.abs_tol);
+  double* r = scratch_vec(0, n);
+  double* z = scratch_vec(1, n);
+  double* p = scratch_vec(2, n);
+  double* q = scratch_vec(3, n);
+  if (!r || !z || !p || !q) return fail(DGB_E_CUDA, "cg: out of device memory");
+  int iter = 0;
+  while (true) {
+    OK(apply_op(op, x, r));
+    ++launches;
+    CK(v_rsub(st, n, b, r));
+    double rr;
+    OK(dot(n, r, r, &rr));
+    double rnorm = std::sqrt(rr);
+    if (rnorm <= tol) {
+      out.iterations = iter;
+      out.residual = rnorm;
+      return DGB_OK;
+    }
+    if (iter >= s.max_iter)
+      return fail(DGB_E_NO_CONVERGENCE, "cg: no convergence in " + std::to_string(s.max_iter) +
+                                            " iterations (residual " + std::to_string(rnorm) + ")");
+    double rho;
+    launches += 2;
+    CK(r_precond_dot(st, n, r, inv, z, d_partial_, d_res_));
+    OK(host_scalars(1, &rho));
+    double rho_old = 0.0;
+    bool first = true;
+    while (iter < s.max_iter) {
+      if (rho == 0.0) return fail(DGB_E_BREAKDOWN, "cg: breakdown, <r,z> = 0");
+      ++launches;
+      if (first) {
+        CK(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        first = false;
+      } else {
+        CK(v_axpby(st, n, 1.0, z, rho / rho_old, p));
+      }
+      rho_old = rho;
+      OK(apply_op(op, p, q));
+      double pq;
+      OK(dot(n, p, q, &pq));
+      if (pq <= 0.0) return fail(DGB_E_NOT_SPD, "cg: operator not positive definite, <p,Ap> <= 0");
+      const double alpha = rho / pq;
+      launches += 2;
+      CK(r_cg_update(st, n, alpha, p, q, x, r, inv, z, d_partial_, d_res_));
+      double rz[2];
+      OK(host_scalars(2, rz));
+      ++iter;
+      rnorm = std::sqrt(rz[0]);
+      out.history.push_back(rnorm);
+      if (rnorm <= tol) break;
+      rho = rz[1];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ GMRES (krylov.cpp:103-207)
+int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const double* inv, const double* b,
+                   double* x, SolveOut& out) {
+  const size_t n = op_size(op);
+  cudaStream_t st = dc.stream;
+  out = SolveOut();
+  double bb;
+  OK(dot(n, b, b, &bb));
+  const double bnorm = std::sqrt(bb);
+  if (bnorm == 0.0) {
+    ++launches;
+    CK(v_fill(st, n, 0.0, x));
+    return DGB_OK;
+  }
+  const double tol = std::max(s.rel_tol * bnorm, s.abs_tol);
+  const int m = std::max(1, s.restart);
+  if (gm_n_ != n) {
+    cudaStreamSynchronize(st);
+    for (double* v : gm_basis_) cudaFree(v);
+    gm_basis_.clear();
+    gm_n_ = n;
+  }
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1);
+  auto row = [&](int i, int j) -> double& { return H[(size_t)i * m + j]; };
+  double* z = scratch_vec(4, n);
+  double* w = scratch_vec(5, n);
+  double* r = scratch_vec(6, n);
+  if (!z || !w || !r) return fail(DGB_E_CUDA, "gmres: out of device memory");
+  auto basis = [&](int k) -> double* {
+    while ((int)gm_basis_.size() <= k) {
+      double* v = nullptr;
+      if (cudaMalloc(&v, n * sizeof(double)) != cudaSuccess) return nullptr;
+      gm_basis_.push_back(v);
+    }
+    return gm_basis_[k];
+  };
+  int iter = 0;
+  while (true) {
+    OK(apply_op(op, x, r));
+    ++launches;
+    CK(v_rsub(st, n, b, r));
+    double rr;
+    OK(dot(n, r, r, &rr));
+    const double beta = std::sqrt(rr);
+    if (beta <= tol) {
+      out.iterations = iter;
+      out.residual = beta;
+      return DGB_OK;
+    }
+    if (iter >= s.max_iter)
+      return fail(DGB_E_NO_CONVERGENCE, "gmres: no convergence in " + std::to_string(s.max_iter) +
+                                            " iterations (residual " + std::to_string(beta) + ")");
+    double* v0 = basis(0);
+    if (!v0) return fail(DGB_E_CUDA, "gmres: out of device memory (basis)");
+    ++launches;
+    CK(v_scale_copy(st, n, 1.0 / beta, r, v0));
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    std::fill(H.begin(), H.end(), 0.0);
+    int k = 0;
+    while (k < m && iter < s.max_iter) {
+      ++launches;
+      if (inv)
+        CK(v_mul(st, n, basis(k), inv, z));
+      else
+        CK(cudaMemcpyAsync(z, basis(k), n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      OK(apply_op(op, z, w));
+      ++iter;
+      // modified Gram-Schmidt, each subtraction fused with the next projection
+      double h;
+      OK(dot(n, w, basis(0), &h));
+      double hk1sq = 0.0;
+      for (int i = 0; i <= k; ++i) {
+        row(i, k) = h;
+        const double* next = i < k ? basis(i + 1) : w;
+        launches += 2;
+        CK(r_mgs_step(st, n, h, basis(i), w, next, d_partial_, d_res_));
+        double v;
+        OK(host_scalars(1, &v));
+        if (i < k)
+          h = v;
+        else
+          hk1sq = v;
+      }
+      const double hk1 = std::sqrt(hk1sq);
+      row(k + 1, k) = hk1;
+      for (int i = 0; i < k; ++i) {
+        const double t = cs[i] * row(i, k) + sn[i] * row(i + 1, k);
+        row(i + 1, k) = -sn[i] * row(i, k) + cs[i] * row(i + 1, k);
+        row(i, k) = t;
+      }
+      const double denom = std::hypot(row(k, k), row(k + 1, k));
+      if (denom == 0.0) {
+        cs[k] = 1.0;
+        sn[k] = 0.0;
+      } else {
+        cs[k] = row(k, k) / denom;
+        sn[k] = row(k + 1, k) / denom;
+      }
+      row(k, k) = denom;
+      row(k + 1, k) = 0.0;
+      g[k + 1] = -sn[k] * g[k];
+      g[k] = cs[k] * g[k];
+      const double res = std::abs(g[k + 1]);
+      out.history.push_back(res);
+      ++k;
+      if (res <= tol || hk1 == 0.0) break;
+      if (k < m) {
+        double* vk = basis(k);
+        if (!vk) return fail(DGB_E_CUDA, "gmres: out of device memory (basis)");
+        ++launches;
+        CK(v_scale_copy(st, n, 1.0 / hk1, w, vk));
+      }
+    }
+    std::vector<double> y(k, 0.0);
+    for (int i = k - 1; i >= 0; --i) {
+      double t = g[i];
+      for (int j = i + 1; j < k; ++j) t -= row(i, j) * y[j];
+      y[i] = t / row(i, i);
+    }
+    // w = V y (chunks of 64 vectors), then x += M^{-1} w
+    for (int j0 = 0; j0 < k; j0 += 64) {
+      const int kk = std::min(64, k - j0);
+      std::vector<const double*> V(kk);
+      for (int j = 0; j < kk; ++j) V[j] = basis(j0 + j);
+      ++launches;
+      if (j0 == 0) {
+        CK(v_lincomb(st, n, kk, V.data(), y.data() + j0, w));
+      } else {
+        CK(v_lincomb(st, n, kk, V.data(), y.data() + j0, z));
+        CK(v_axpy(st, n, 1.0, z, w));
+      }
+    }
+    ++launches;
+    if (inv)
+      CK(v_addmul(st, n, inv, w, x));
+    else
+      CK(v_axpy(st, n, 1.0, w, x));
+  }
+}
+
+// ------------------------------------------------------------------ Dirichlet data
+int Context::set_dirichlet_table(const double* g) {
+  if (g)
+    std::memcpy(gtab_h_.data(), g, gtab_h_.size() * sizeof(double));
+  else
+    std::fill(gtab_h_.begin(), gtab_h_.end(), 0.0);
+  CK(cudaMemcpyAsync(d_gtab_, gtab_h_.data(), gtab_h_.size() * sizeof(double), cudaMemcpyHostToDevice, dc.stream));
+  CK(cudaStreamSynchronize(dc.stream));
+  return DGB_OK;
+}
+int Context::set_dirichlet_fn(int id, dgb_bc_fn fn, void* user, double t) {
+  const int Q = ku + 2, nq = nqf(Q);
+  std::vector<double> xq;
+  boundary_points(mesh, Q, xq);
+  std::vector<double> gv(dim);
+  for (size_t b = 0; b < n_bface(); ++b) {
+    if (mesh.bface[3 * b + 2] != id) continue;
+    for (int qq = 0; qq < nq; ++qq) {
+      double* o = &gtab_h_[(b * nq + qq) * dim];
+      if (fn)
+        fn(&xq[(b * nq + qq) * dim], t, o, user);
+      else
+        for (int d = 0; d < dim; ++d) o[d] = 0.0;
+    }
+  }
+  CK(cudaMemcpyAsync(d_gtab_, gtab_h_.data(), gtab_h_.size() * sizeof(double), cudaMemcpyHostToDevice, dc.stream));
+  CK(cudaStreamSynchronize(dc.stream));
+  return DGB_OK;
+}
+
+// ------------------------------------------------------------------ TR-BDF2
+// Same call sequence as oracle/trbdf2_cpu.hpp, every operator / solver on the device.
+int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const double* u_n, const double* p_n,
+                         double* u_np1, double* p_np1, int* its) {
+  const size_t NU = nu(), NP = np();
+  cudaStream_t st = dc.stream;
+  const double gm = 2.0 - std::sqrt(2.0);
+  double* wv = scratch_vec(30, NU);     // advecting field
+  double* F = scratch_vec(31, NU);      // momentum rhs
+  double* inv = scratch_vec(32, NU);    // Jacobi of the momentum operator
+  double* g = scratch_vec(33, NU);      // gradient rhs / projected gradient
+  double* uss = scratch_vec(34, NU);    // u**
+  double* u_g = scratch_vec(35, NU);    // u^{n+gamma}
+  double* minv = scratch_vec(36, NU);   // Jacobi of the velocity mass matrix
+  double* ut = scratch_vec(37, NU);
+  double* prhs = scratch_vec(38, NP);
+  double* pinv = scratch_vec(39, NP);
+  double* p_g = scratch_vec(40, NP);
+  if (!wv || !F || !inv || !g || !uss || !u_g || !minv || !ut || !prhs || !pinv || !p_g)
+    return fail(DGB_E_CUDA, "trbdf2: out of device memory");
+  for (int i = 0; i < 8; ++i) its[i] = 0;
+  OK(mass_diag(DGB_SPACE_U, ut));
+  OK(jacobi_inverse(NU, ut, minv));
+  const dgb_solver_settings s_mass{P.tol_mass, 0.0, P.max_iter, 50};
+  const dgb_solver_settings s_mom{P.tol_mom, 0.0, P.max_iter, P.restart};
+  const dgb_solver_settings s_p{P.tol_p, 0.0, P.max_iter, 50};
+  dgb_operator mass_op{};
+  mass_op.op = DGB_OP_MASS_U;
+
+  // projected gradient: out = M^{-1} G p  (CG + Jacobi, x0 = 0)
+  auto proj_grad = [&](const double* p, double* out, int& it) -> int {
+    OK(gradient(p, g));
+    ++launches;
+    CK(v_fill(st, NU, 0.0, out));
+    SolveOut so;
+    OK(cg(mass_op, s_mass, minv, g, out, so));
+    it = so.iterations;
+    return DGB_OK;
+  };
+  // one stage; alpha dt, momentum coefficients, rhs description
+  auto stage = [&](int si, double alpha, const double* mc, const dgb_rhs_desc& rd, const double* u_guess,
+                   const double* p_old, double* u_out, double* p_out) -> int {
+    OK(rhs(rd, F));
+    OK(momentum_diag(mc, wv, g));
+    OK(jacobi_inverse(NU, g, inv));
+    CK(cudaMemcpyAsync(u_out, u_guess, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    dgb_operator mop{};
+    mop.op = DGB_OP_MOMENTUM;
+    for (int i = 0; i < 4; ++i) mop.coefs[i] = mc[i];
+    mop.d_w = wv;
+    SolveOut so;
+    OK(gmres(mop, s_mom, inv, F, u_out, so));
+    its[si] = so.iterations;
+    const double adt = alpha * P.dt;
+    OK(proj_grad(p_old, ut, its[4 + 2 * si]));
+    CK(cudaMemcpyAsync(uss, u_out, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    ++launches;
+    CK(v_axpy(st, NU, adt, ut, uss));
+    const double pmc = 1.0 / (P.c * P.c * adt * adt);
+    OK(pressure_rhs(1.0 / adt, uss, pmc, p_old, prhs));
+    OK(sip_diag(pmc, 0, pinv));
+    OK(jacobi_inverse(NP, pinv, pinv));
+    CK(cudaMemcpyAsync(p_out, p_old, NP * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    dgb_operator pop{};
+    pop.op = DGB_OP_PRESSURE;
+    pop.coefs[0] = pmc;
+    OK(cg(pop, s_p, pinv, prhs, p_out, so));
+    its[2 + si] = so.iterations;
+    OK(proj_grad(p_out, ut, its[5 + 2 * si]));
+    CK(cudaMemcpyAsync(u_out, uss, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    ++launches;
+    CK(v_axpy(st, NU, -adt, ut, u_out));
+    return DGB_OK;
+  };
+
+  // ---- stage 1
+  if (P.first_step)
+    CK(cudaMemcpyAsync(wv, u_n, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  else {
+    CK(cudaMemcpyAsync(wv, u_nm1, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    ++launches;
+    CK(v_axpby(st, NU, 1.0 + gm / (2.0 * (1.0 - gm)), u_n, -gm / (2.0 * (1.0 - gm)), wv));
+  }
+  const double Re = P.Re, dt = P.dt;
+  {
+    const double mc[4] = {1.0 / (gm * dt), 1.0 / (2.0 * Re), 0.5, 0.0};
+    dgb_rhs_desc rd{};
+    rd.n_mass = 1;
+    rd.mass_coef[0] = 1.0 / (gm * dt);
+    rd.mass_f[0] = u_n;
+    rd.n_visc = 1;
+    rd.visc_coef[0] = 1.0 / (2.0 * Re);
+    rd.visc_f[0] = u_n;
+    rd.n_adv = 1;
+    rd.adv_coef[0] = 0.5;
+    rd.adv_f[0] = u_n;
+    rd.adv_w[0] = wv;
+    rd.n_pres = 1;
+    rd.pres_coef[0] = 1.0;
+    rd.pres_f[0] = p_n;
+    rd.dir_visc_coef = 1.0 / (2.0 * Re);
+    rd.dir_adv_coef = 0.5;
+    rd.dir_w = wv;
+    OK(stage(0, gm, mc, rd, u_n, p_n, u_g, p_g));
+  }
+  // ---- stage 2
+  {
+    const double a33 = 1.0 / (2.0 - gm), a31 = (1.0 - gm) / (2.0 * (2.0 - gm)), a32 = a31;
+    CK(cudaMemcpyAsync(wv, u_n, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    ++launches;
+    CK(v_axpby(st, NU, 1.0 + (1.0 - gm) / gm, u_g, -(1.0 - gm) / gm, wv));
+    const double mc[4] = {1.0 / ((1.0 - gm) * dt), a33 / Re, a33, 0.0};
+    dgb_rhs_desc rd{};
+    rd.n_mass = 1;
+    rd.mass_coef[0] = 1.0 / ((1.0 - gm) * dt);
+    rd.mass_f[0] = u_g;
+    rd.n_visc = 2;
+    rd.visc_coef[0] = a32 / Re;
+    rd.visc_f[0] = u_g;
+    rd.visc_coef[1] = a31 / Re;
+    rd.visc_f[1] = u_n;
+    rd.n_adv = 2;
+    rd.adv_coef[0] = a32;
+    rd.adv_f[0] = u_g;
+    rd.adv_w[0] = u_g;
+    rd.adv_coef[1] = a31;
+    rd.adv_f[1] = u_n;
+    rd.adv_w[1] = u_n;
+    rd.n_pres = 1;
+    rd.pres_coef[0] = 1.0;
+    rd.pres_f[0] = p_g;
+    rd.dir_visc_coef = a33 / Re;
+    rd.dir_adv_coef = a33;
+    rd.dir_w = wv;
+    OK(stage(1, 1.0 - gm, mc, rd, u_g, p_g, u_np1, p_np1));
+  }
+  CK(cudaStreamSynchronize(st));
+  return DGB_OK;
+}
+
+}  // namespace dgb

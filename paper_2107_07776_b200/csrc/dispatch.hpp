@@ -1,0 +1,94 @@
+// Plain-C++ view of the device context consumed by the operator launchers,
+// plus the per-dimension operator tables (defined in ops_d2.cu / ops_d3.cu so
+// the two dimensions compile as parallel translation units).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace dgb {
+
+constexpr int kMaxRule = 8;
+constexpr int kMaxTerms = 4;
+
+struct MeshArgs {
+  int ncells = 0;
+  const int* nbr = nullptr;      // [ncells][2dim]: neighbour, or -1 - boundary_id
+  const double* pen = nullptr;   // [ncells][2dim]: interior mean |F|/|K|, boundary |F|/|K|
+  const int* bctype = nullptr;   // [64]: 0 dirichlet, 1 outlet
+  const int* bslot = nullptr;    // [ncells][2dim]: boundary-face index (reference order) or -1
+};
+
+struct GeoArgs {
+  const double* aff = nullptr;    // affine: per cell {Jinv, detJ, per face {n, ds}}
+  const double* qcell = nullptr;  // per-qp cell geometry for this rule
+  const double* qface = nullptr;  // per-qp face geometry for this rule
+  const int* nbr = nullptr;
+};
+
+struct MomCoef {
+  double mass, visc, adv, skew;
+};
+
+struct RhsArgs {
+  int nm = 0, nv = 0, na = 0, np = 0;
+  double mc[kMaxTerms], vc[kMaxTerms], ac[kMaxTerms], pc[kMaxTerms];
+  const double* mf[kMaxTerms];
+  const double* vf[kMaxTerms];
+  const double* af[kMaxTerms];
+  const double* aw[kMaxTerms];
+  const double* pf[kMaxTerms];
+  double dvisc = 0.0, dadv = 0.0;
+  const double* dir_w = nullptr;
+  const double* gtab = nullptr;  // [n_bface][NQF(rule k+2)][DIM], reference boundary-face order
+};
+
+struct DevCtx {
+  int dim = 0, ku = 0, kp = 0, ncells = 0;
+  bool affine = true;
+  MeshArgs mesh;
+  const double* aff = nullptr;
+  const double* qcell[kMaxRule] = {};
+  const double* qface[kMaxRule] = {};
+  cudaStream_t stream = nullptr;
+};
+
+struct OpTable {
+  cudaError_t (*momentum)(const DevCtx&, MomCoef, const double* w, const double* x, double* y);
+  cudaError_t (*momentum_diag)(const DevCtx&, MomCoef, const double* w, double* y);
+  cudaError_t (*rhs)(const DevCtx&, const RhsArgs&, double* y);
+  cudaError_t (*sip)(const DevCtx&, double mc, int dir, const double* x, double* y);
+  cudaError_t (*sip_diag)(const DevCtx&, double mc, int dir, double* y);
+  cudaError_t (*mass)(const DevCtx&, int space, const double* x, double* y);
+  cudaError_t (*mass_diag)(const DevCtx&, int space, double* y);
+  cudaError_t (*gradient)(const DevCtx&, const double* p, double* y);
+  cudaError_t (*divergence)(const DevCtx&, const double* u, double* y);
+  cudaError_t (*kinetic)(const DevCtx&, const double* u, double* partial, int* nblocks);
+  cudaError_t (*tables)();
+};
+
+// defined in ops_d{2,3}_k{1..4}.cu
+#define DGB_DECL_OPS(D, K) const OpTable& ops_d##D##_k##K();
+DGB_DECL_OPS(2, 1) DGB_DECL_OPS(2, 2) DGB_DECL_OPS(2, 3) DGB_DECL_OPS(2, 4)
+DGB_DECL_OPS(3, 1) DGB_DECL_OPS(3, 2) DGB_DECL_OPS(3, 3) DGB_DECL_OPS(3, 4)
+#undef DGB_DECL_OPS
+/// operator table for dimension dim and space degree k (1..4); nullptr if unsupported
+inline const OpTable* ops_for(int dim, int k) {
+  if (dim == 2) {
+    switch (k) {
+      case 1: return &ops_d2_k1();
+      case 2: return &ops_d2_k2();
+      case 3: return &ops_d2_k3();
+      case 4: return &ops_d2_k4();
+    }
+  } else if (dim == 3) {
+    switch (k) {
+      case 1: return &ops_d3_k1();
+      case 2: return &ops_d3_k2();
+      case 3: return &ops_d3_k3();
+      case 4: return &ops_d3_k4();
+    }
+  }
+  return nullptr;
+}
+
+}  // namespace dgb

@@ -1,0 +1,103 @@
+// Host-side setup for the device context: 1D shape tables, the conforming
+// hexahedral / quadrilateral mesh in the reference's numbering, and the
+// per-cell geometry the kernels consume.  Runs once per context.
+//
+// Conventions reproduced from the reference:
+//  * Gauss-Legendre points ascending on [0,1], weights summing to 1
+//    (proj/src/quadrature.cpp:25-46); Gauss-Lobatto nodal basis
+//    (quadrature.cpp:48-69, space.cpp:189-203); barycentric Lagrange values /
+//    product-rule derivatives (lagrange.cpp:10-50).
+//  * vertices lexicographic v = ix + 2 iy + 4 iz, local face 2*axis+side
+//    (mesh.hpp:5-15); Cartesian generator numbering and boundary ids
+//    (mesh.cpp:571-616); seeded interior-vertex distortion (mesh.cpp:618-646).
+//  * cell measure by 2-point Gauss of det J (mesh.cpp:101-109); face measure
+//    from the corners (mesh.cpp:268-292); penalty sigma = (deg+1)^2 |F|/|K|
+//    (forms.hpp:175-177), interior faces use the mean of both sides
+//    (forms.cpp:111-121), boundary faces 2*sigma_K in the operators.
+//  * Jinv stored row-major Jinv[a*dim+j] = d xi_a / d x_j (space.cpp:14-39,81);
+//    face normal = Nanson direction from the owner side (space.cpp:133-142).
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace dgb {
+
+// ---------------------------------------------------------------------------
+// 1D tables
+// ---------------------------------------------------------------------------
+struct Rule1D {
+  std::vector<double> x, w;
+};
+Rule1D gauss_legendre(int n);
+std::vector<double> gauss_lobatto(int n);
+
+/// Lagrange basis on GL nodes evaluated at points: val[q][j], der[q][j].
+void lagrange_tables(const std::vector<double>& nodes, const std::vector<double>& pts,
+                     std::vector<double>& val, std::vector<double>& der);
+
+// ---------------------------------------------------------------------------
+// Mesh (conforming, every interior face with identity corner orientation)
+// ---------------------------------------------------------------------------
+struct HostMesh {
+  int dim = 0;
+  int ncells = 0;
+  std::vector<double> vertices;      // nverts x dim
+  std::vector<int> cell_v;           // ncells x 2^dim (vertex ids)
+  std::vector<int> nbr;              // ncells x 2dim: neighbor cell, or -1 - boundary_id
+  std::vector<double> face_measure;  // ncells x 2dim (from this cell's corners)
+  std::vector<double> cell_measure;  // ncells
+  std::vector<double> cell_diam;     // ncells
+  // reference face lists (owner = lower index, cell-major order; mesh.cpp:316-377)
+  std::vector<int> iface;  // n_interior x 4: cell_in, face_in, cell_out, face_out
+  std::vector<int> bface;  // n_boundary x 3: cell, face, boundary_id
+  bool affine = true;      // every cell a parallelepiped (constant Jacobian)
+
+  int nv_cell() const { return 1 << dim; }
+  int nf_cell() const { return 2 * dim; }
+  const double* vert(int c, int v) const { return &vertices[static_cast<size_t>(cell_v[c * nv_cell() + v]) * dim]; }
+};
+
+/// generate_cartesian on [0,1]^dim (mesh.cpp:571-616) + optional distort (mesh.cpp:618-646).
+HostMesh make_cartesian(int dim, int n_el, double amp, unsigned seed, std::string& err);
+/// From raw arrays (vertices, cell->vertex, boundary ids per cell face (-1 = none)).
+HostMesh make_from_arrays(int dim, int nverts, const double* verts, int ncells, const int* cell_v,
+                          const int* boundary_ids, std::string& err);
+/// Recompute measures, diameters, face lists, affinity. Fills err on failure.
+bool finalize_mesh(HostMesh& m, std::string& err);
+
+// Multilinear map, Jacobian J[d][a] = dx_d/dxi_a, and inverse (space.cpp:14-39 convention).
+void map_point(const HostMesh& m, int c, const double* ref, double* x);
+void jacobian(const HostMesh& m, int c, const double* ref, double* J);
+double invert(int dim, const double* J, double* Jinv);
+
+// ---------------------------------------------------------------------------
+// Geometry tables uploaded to the device
+// ---------------------------------------------------------------------------
+/// Per-quadrature-point geometry for rule Q (general / deformed cells):
+///  cell[c][q] = {Jinv (dim^2), detJ*w}          (CellGeometry, space.hpp:27-32)
+///  face[c][f][q] = {Jinv_self (dim^2), Jinv_nbr (dim^2), n_out (dim), w_ds}
+/// seen from cell c (n points out of c; Jinv_nbr = 0 on boundary faces).
+struct QpGeometry {
+  int Q = 0;
+  std::vector<double> cell, face;
+};
+int cell_geo_stride(int dim);
+int face_geo_stride(int dim);
+void build_qp_geometry(const HostMesh& m, int Q, QpGeometry& g);
+
+/// Per-cell geometry for affine cells: {Jinv (dim^2), detJ} + per face {n (dim), ds}
+int affine_cell_stride(int dim);
+void build_affine_geometry(const HostMesh& m, std::vector<double>& g);
+
+/// Physical points of boundary-face quadrature points for rule Q, in the
+/// reference boundary-face order (GeometryCache::boundary_faces xq).
+void boundary_points(const HostMesh& m, int Q, std::vector<double>& xq);
+
+/// Constant-table fillers (device tables are uploaded from these).
+void host_tab(int N, int Q, double* B, double* D, double* dE);
+void host_w(int Q, double* w);
+
+}  // namespace dgb

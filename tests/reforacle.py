@@ -1,0 +1,246 @@
+"""ctypes wrapper of oracle/_ref/libdgref.so — TEST INFRASTRUCTURE ONLY.
+
+Drives the unmodified reference library (proj/src, compiled by oracle/Makefile)
+through oracle/ref_capi.cpp on numpy arrays.  Used only as the checker by the
+tests, __graft_entry__.smoke() and bench.py's CPU-baseline legs.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libdgref.so")
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+BC_FN = C.CFUNCTYPE(None, _dp, C.c_double, _dp, C.c_void_p)
+
+_lib = None
+
+
+def available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(REF_SO)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_backend.restype = C.c_char_p
+        L.ref_create_cartesian.restype = C.c_void_p
+        L.ref_create_cartesian.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint, C.c_int, C.c_int, C.c_int]
+        L.ref_create_from_text.restype = C.c_void_p
+        L.ref_create_from_text.argtypes = [C.c_char_p, C.c_int, C.c_int]
+        L.ref_create_cylinder.restype = C.c_void_p
+        L.ref_create_cylinder.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.ref_destroy.argtypes = [C.c_void_p]
+        L.ref_info.argtypes = [C.c_void_p, C.POINTER(C.c_longlong)]
+        L.ref_set_bc.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+        L.ref_apply_momentum.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
+        L.ref_momentum_diagonal.argtypes = [C.c_void_p, _dp, _dp, _dp]
+        L.ref_apply_pressure.argtypes = [C.c_void_p, C.c_double, _dp, _dp]
+        L.ref_helmholtz_diagonal.argtypes = [C.c_void_p, C.c_double, _dp]
+        L.ref_apply_laplace.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
+        L.ref_laplace_diagonal.argtypes = [C.c_void_p, C.c_int, _dp]
+        L.ref_apply_mass.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
+        L.ref_mass_diagonal.argtypes = [C.c_void_p, C.c_int, _dp]
+        L.ref_momentum_rhs.argtypes = [C.c_void_p, C.c_int, _dp, C.POINTER(_dp), C.c_int, _dp, C.POINTER(_dp),
+                                       C.c_int, _dp, C.POINTER(_dp), C.POINTER(_dp), C.c_int, _dp,
+                                       C.POINTER(_dp), C.c_double, C.c_double, _dp, C.c_double, _dp]
+        L.ref_divergence.argtypes = [C.c_void_p, _dp, _dp]
+        L.ref_pressure_rhs.argtypes = [C.c_void_p, C.c_double, _dp, C.c_double, _dp, _dp]
+        L.ref_pressure_gradient.argtypes = [C.c_void_p, _dp, _dp]
+        L.ref_kinetic_energy.argtypes = [C.c_void_p, _dp]
+        L.ref_kinetic_energy.restype = C.c_double
+        L.ref_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp, _dp, C.c_double, C.c_double, C.c_int,
+                                C.c_int, C.c_int, _dp, _ip, _dp, _dp, C.c_int, _ip]
+        L.ref_trbdf2_step.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _ip]
+        L.ref_faces.argtypes = [C.c_void_p, _ip, _dp, _ip, _dp]
+        L.ref_cell_vertices.argtypes = [C.c_void_p, _dp]
+        L.ref_bface_points.argtypes = [C.c_void_p, C.c_int, _dp]
+        L.ref_node_points.argtypes = [C.c_void_p, C.c_int, _dp]
+        L.ref_bench.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, C.c_int, C.c_int]
+        L.ref_bench.restype = C.c_double
+        L.ref_dense_momentum.argtypes = [C.c_void_p, _dp, _dp, _dp]
+        L.ref_dense_scalar_sip.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int, _dp]
+        _lib = L
+    return _lib
+
+
+def P(a):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+class RefSolverError(RuntimeError):
+    def __init__(self, msg, history):
+        super().__init__(msg)
+        self.history = history
+
+
+class RefCtx:
+    """Reference Mesh + GeometryCache + FunctionSpace(ku, dim) + FunctionSpace(kp, 1)."""
+
+    def __init__(self, dim=2, n_el=2, ku=2, kp=1, amp=0.0, seed=0, refine_first=False, handle=None):
+        L = lib()
+        h = handle if handle is not None else L.ref_create_cartesian(dim, n_el, amp, seed, ku, kp, int(refine_first))
+        if not h:
+            raise RuntimeError(L.ref_last_error().decode())
+        self.h = h
+        info = (C.c_longlong * 10)()
+        L.ref_info(h, info)
+        (self.ncells, self.n_u, self.n_p, self.n_interior, self.n_boundary, self.ku, self.kp, self.dim,
+         self.nverts, self.n_hanging) = [int(v) for v in info]
+        self._keep = []
+
+    def __del__(self):
+        try:
+            lib().ref_destroy(self.h)
+        except Exception:
+            pass
+
+    def set_bc(self, bid, bc_type, fn_ptr=None, user=None):
+        self._keep.append(user)
+        lib().ref_set_bc(self.h, bid, bc_type, fn_ptr, user)
+
+    def momentum(self, coefs, w, x):
+        y = np.zeros(self.n_u)
+        c = np.ascontiguousarray(coefs, dtype=np.float64)
+        if lib().ref_apply_momentum(self.h, P(c), P(w), P(x), P(y)):
+            raise RuntimeError(lib().ref_last_error().decode())
+        return y
+
+    def momentum_diag(self, coefs, w):
+        y = np.zeros(self.n_u)
+        c = np.ascontiguousarray(coefs, dtype=np.float64)
+        if lib().ref_momentum_diagonal(self.h, P(c), P(w), P(y)):
+            raise RuntimeError(lib().ref_last_error().decode())
+        return y
+
+    def pressure(self, mc, x):
+        y = np.zeros(self.n_p)
+        lib().ref_apply_pressure(self.h, mc, P(x), P(y))
+        return y
+
+    def helmholtz_diag(self, mc):
+        y = np.zeros(self.n_p)
+        lib().ref_helmholtz_diagonal(self.h, mc, P(y))
+        return y
+
+    def laplace(self, dirichlet, x):
+        y = np.zeros(self.n_p)
+        lib().ref_apply_laplace(self.h, int(dirichlet), P(x), P(y))
+        return y
+
+    def laplace_diag(self, dirichlet):
+        y = np.zeros(self.n_p)
+        lib().ref_laplace_diagonal(self.h, int(dirichlet), P(y))
+        return y
+
+    def mass(self, space, x):
+        y = np.zeros(self.n_u if space == 0 else self.n_p)
+        lib().ref_apply_mass(self.h, space, P(x), P(y))
+        return y
+
+    def mass_diag(self, space):
+        y = np.zeros(self.n_u if space == 0 else self.n_p)
+        lib().ref_mass_diagonal(self.h, space, P(y))
+        return y
+
+    def momentum_rhs(self, mass=(), visc=(), adv=(), pres=(), dir_visc=0.0, dir_adv=0.0, dir_w=None, time=0.0):
+        def arr(lst, idx):
+            return (_dp * max(1, len(lst)))(*[P(t[idx]) for t in lst])
+
+        def coefs(lst):
+            return np.ascontiguousarray([t[0] for t in lst] + [0.0], dtype=np.float64)
+
+        cm, cv, ca, cp = coefs(mass), coefs(visc), coefs(adv), coefs(pres)
+        y = np.zeros(self.n_u)
+        rc = lib().ref_momentum_rhs(self.h, len(mass), P(cm), arr(mass, 1), len(visc), P(cv), arr(visc, 1),
+                                    len(adv), P(ca), arr(adv, 1), arr(adv, 2), len(pres), P(cp), arr(pres, 1),
+                                    dir_visc, dir_adv, P(dir_w), time, P(y))
+        if rc:
+            raise RuntimeError(lib().ref_last_error().decode())
+        return y
+
+    def divergence(self, u):
+        y = np.zeros(self.n_p)
+        lib().ref_divergence(self.h, P(u), P(y))
+        return y
+
+    def pressure_rhs(self, inv_adt, u, mc, p_old):
+        y = np.zeros(self.n_p)
+        lib().ref_pressure_rhs(self.h, inv_adt, P(u), mc, P(p_old), P(y))
+        return y
+
+    def gradient(self, p):
+        y = np.zeros(self.n_u)
+        lib().ref_pressure_gradient(self.h, P(p), P(y))
+        return y
+
+    def kinetic_energy(self, u):
+        return lib().ref_kinetic_energy(self.h, P(u))
+
+    def solve(self, op, solver, coefs, w, b, x0, rel_tol=1e-10, abs_tol=0.0, max_iter=10000, restart=50,
+              precond=True):
+        x = np.array(x0, dtype=np.float64, copy=True)
+        it = C.c_int()
+        res = C.c_double()
+        hist = np.zeros(100000)
+        hl = C.c_int()
+        c = np.ascontiguousarray(coefs, dtype=np.float64)
+        rc = lib().ref_solve(self.h, op, solver, P(c), P(w), P(b), rel_tol, abs_tol, max_iter, restart,
+                             int(precond), P(x), C.byref(it), C.byref(res), P(hist), 100000, C.byref(hl))
+        if rc == 2:
+            raise RefSolverError(lib().ref_last_error().decode(), hist[: hl.value].tolist())
+        if rc:
+            raise RuntimeError(lib().ref_last_error().decode())
+        return x, it.value, res.value
+
+    def step(self, params, u_nm1, u_n, p_n):
+        prm = np.ascontiguousarray(params, dtype=np.float64)
+        u1 = np.zeros(self.n_u)
+        p1 = np.zeros(self.n_p)
+        its = (C.c_int * 8)()
+        if lib().ref_trbdf2_step(self.h, P(prm), P(u_nm1), P(u_n), P(p_n), P(u1), P(p1), its):
+            raise RuntimeError(lib().ref_last_error().decode())
+        return u1, p1, list(its)
+
+    def faces(self):
+        it = np.zeros((self.n_interior, 5), dtype=np.int32)
+        im = np.zeros(self.n_interior)
+        bd = np.zeros((self.n_boundary, 3), dtype=np.int32)
+        bm = np.zeros(self.n_boundary)
+        lib().ref_faces(self.h, it.ctypes.data_as(_ip), P(im), bd.ctypes.data_as(_ip), P(bm))
+        return it, im, bd, bm
+
+    def cell_vertices(self):
+        xv = np.zeros((self.ncells, 1 << self.dim, self.dim))
+        lib().ref_cell_vertices(self.h, P(xv))
+        return xv
+
+    def bface_points(self, rule):
+        xq = np.zeros((self.n_boundary, rule ** (self.dim - 1), self.dim))
+        lib().ref_bface_points(self.h, rule, P(xq))
+        return xq
+
+    def bench(self, op, coefs, w, x, nthreads, napplies):
+        c = np.ascontiguousarray(coefs, dtype=np.float64)
+        return lib().ref_bench(self.h, op, P(c), P(w), P(x), nthreads, napplies)
+
+    def dense_momentum(self, coefs, w):
+        A = np.zeros((self.n_u, self.n_u))
+        c = np.ascontiguousarray(coefs, dtype=np.float64)
+        lib().ref_dense_momentum(self.h, P(c), P(w), P(A))
+        return A
+
+    def dense_scalar_sip(self, mc, dirichlet, rule):
+        A = np.zeros((self.n_p, self.n_p))
+        lib().ref_dense_scalar_sip(self.h, mc, int(dirichlet), rule, P(A))
+        return A

@@ -1,0 +1,283 @@
+"""Device path vs the reference CPU implementation on identical seeded inputs.
+
+Gate (BASELINE.json north_star): per-apply relative L2 <= 1e-12 in fp64,
+Krylov iteration counts within +-1, end-of-run fields within relative L2 1e-9.
+Every device call goes through the C-ABI (libdgb.so); the checker is the
+unmodified reference library (oracle/_ref/libdgref.so).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL_APPLY = 1e-12   # per-apply relative L2 (north_star)
+TOL_FIELD = 1e-9    # end-of-run fields (north_star)
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def dev(t):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(t, dtype=np.float64)).cuda()
+
+
+def host(t):
+    import torch
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def pair(ref, gpu, dim, n_el, ku, kp, amp=0.0, seed=7, outlet=None, dirichlet_seed=None):
+    R = ref.RefCtx(dim, n_el, ku, kp, amp, seed)
+    D = gpu.DGContext(dim, n_el, ku, kp, amp, seed)
+    assert (R.n_u, R.n_p, R.ncells) == (D.n_u, D.n_p, D.ncells)
+    assert (R.n_interior, R.n_boundary) == (D.n_interior, D.n_boundary)
+    if outlet is not None:
+        R.set_bc(outlet, 1)
+        D.set_boundary_type(outlet, gpu.BC_OUTLET)
+    if dirichlet_seed is not None:
+        f = gpu.SynthField(dim, dirichlet_seed)
+        for bid in range(2 * dim):
+            if bid == outlet:
+                continue
+            R.set_bc(bid, 0, f.fn_ptr, f.user_ptr)
+            D.set_dirichlet_fn(bid, f.fn_ptr, f.user_ptr, 0.0)
+        R._keep.append(f)
+        D._keep.append(f)
+    return R, D
+
+
+CASES = [
+    # dim, n_el, ku, kp, amp
+    (2, 4, 2, 1, 0.0),
+    (2, 3, 3, 2, 0.05),
+    (2, 3, 4, 3, 0.0),
+    (3, 2, 2, 1, 0.03),
+    (3, 3, 2, 1, 0.0),
+    (3, 2, 3, 2, 0.0),
+    (3, 2, 3, 2, 0.03),
+    (3, 2, 4, 3, 0.02),
+]
+
+
+@pytest.mark.parametrize("dim,n_el,ku,kp,amp", CASES)
+def test_pressure_helmholtz_apply_and_diag(ref, gpu, dim, n_el, ku, kp, amp):
+    R, D = pair(ref, gpu, dim, n_el, ku, kp, amp)
+    x = gpu.seeded_uniform(11, R.n_p)
+    for mc in (2.3, 0.0):
+        want = R.pressure(mc, x)
+        y = D.zeros(gpu.SPACE_P)
+        gpu.apply_pressure_helmholtz(D, mc, dev(x), y)
+        assert rel(host(y), want) <= TOL_APPLY
+        d = D.zeros(gpu.SPACE_P)
+        gpu.helmholtz_diagonal(D, mc, d)
+        assert rel(host(d), R.helmholtz_diag(mc)) <= TOL_APPLY
+
+
+@pytest.mark.parametrize("dim,n_el,ku,kp,amp", [(2, 3, 3, 2, 0.05), (3, 2, 3, 2, 0.03)])
+def test_scalar_laplace_dirichlet(ref, gpu, dim, n_el, ku, kp, amp):
+    R, D = pair(ref, gpu, dim, n_el, ku, kp, amp)
+    x = gpu.seeded_uniform(12, R.n_p)
+    for dirichlet in (True, False):
+        y = D.zeros(gpu.SPACE_P)
+        gpu.apply_scalar_laplace(D, dirichlet, dev(x), y)
+        assert rel(host(y), R.laplace(dirichlet, x)) <= TOL_APPLY
+        d = D.zeros(gpu.SPACE_P)
+        gpu.scalar_laplace_diagonal(D, dirichlet, d)
+        assert rel(host(d), R.laplace_diag(dirichlet)) <= TOL_APPLY
+
+
+@pytest.mark.parametrize("dim,n_el,ku,kp,amp", CASES)
+@pytest.mark.parametrize("coefs", [(3.7, 1.3, 0.9, -0.45), (1.0 / (0.2929 * 1e-3), 0.005, 0.5, 0.0)])
+def test_momentum_apply_and_diag(ref, gpu, dim, n_el, ku, kp, amp, coefs):
+    R, D = pair(ref, gpu, dim, n_el, ku, kp, amp)
+    w = gpu.seeded_uniform(21, R.n_u)
+    x = gpu.seeded_uniform(22, R.n_u)
+    want = R.momentum(coefs, w, x)
+    y = D.zeros()
+    ctx = gpu.MomentumCtx(*coefs, advecting=dev(w))
+    gpu.apply_momentum(D, ctx, dev(x), y)
+    assert rel(host(y), want) <= TOL_APPLY
+    d = D.zeros()
+    gpu.momentum_diagonal(D, ctx, d)
+    assert rel(host(d), R.momentum_diag(coefs, w)) <= TOL_APPLY
+
+
+@pytest.mark.parametrize("dim,n_el,ku,kp,amp", [(2, 3, 2, 1, 0.05), (3, 2, 2, 1, 0.0)])
+def test_momentum_outlet_switch(ref, gpu, dim, n_el, ku, kp, amp):
+    """test_forms.cpp:312-363: outlet faces drop viscous terms and use w.n advection."""
+    R, D = pair(ref, gpu, dim, n_el, ku, kp, amp, outlet=1)
+    w = gpu.seeded_uniform(31, R.n_u)
+    x = gpu.seeded_uniform(32, R.n_u)
+    coefs = (1.0, 0.9, 0.8, 0.0)
+    y = D.zeros()
+    ctx = gpu.MomentumCtx(*coefs, advecting=dev(w))
+    gpu.apply_momentum(D, ctx, dev(x), y)
+    assert rel(host(y), R.momentum(coefs, w, x)) <= TOL_APPLY
+    d = D.zeros()
+    gpu.momentum_diagonal(D, ctx, d)
+    assert rel(host(d), R.momentum_diag(coefs, w)) <= TOL_APPLY
+    u = gpu.seeded_uniform(33, R.n_u)
+    b = D.zeros(gpu.SPACE_P)
+    gpu.divergence_functional(D, dev(u), b)
+    assert rel(host(b), R.divergence(u)) <= TOL_APPLY
+
+
+def test_missing_advecting_field_raises(gpu):
+    D = gpu.DGContext(2, 2, 2, 1)
+    with pytest.raises(RuntimeError, match="advecting field missing"):
+        gpu.apply_momentum(D, gpu.MomentumCtx(1.0, 1.0, 1.0, 0.0), D.zeros(), D.zeros())
+
+
+@pytest.mark.parametrize("dim,n_el,ku,kp,amp", CASES)
+def test_mass_divergence_gradient_kinetic(ref, gpu, dim, n_el, ku, kp, amp):
+    R, D = pair(ref, gpu, dim, n_el, ku, kp, amp)
+    u = gpu.seeded_uniform(41, R.n_u)
+    p = gpu.seeded_uniform(42, R.n_p)
+    for space, v in ((0, u), (1, p)):
+        y = D.zeros(space)
+        gpu.apply_mass(D, space, dev(v), y)
+        assert rel(host(y), R.mass(space, v)) <= TOL_APPLY
+        d = D.zeros(space)
+        gpu.mass_diagonal(D, space, d)
+        assert rel(host(d), R.mass_diag(space)) <= TOL_APPLY
+    if kp == ku - 1:
+        b = D.zeros(gpu.SPACE_P)
+        gpu.divergence_functional(D, dev(u), b)
+        assert rel(host(b), R.divergence(u)) <= TOL_APPLY
+        g = D.zeros()
+        gpu.pressure_gradient_rhs(D, dev(p), g)
+        assert rel(host(g), R.gradient(p)) <= TOL_APPLY
+        pr = D.zeros(gpu.SPACE_P)
+        gpu.pressure_rhs(D, 1.7, dev(u), 7.3, dev(p), pr)
+        assert rel(host(pr), R.pressure_rhs(1.7, u, 7.3, p)) <= TOL_APPLY
+    ke = gpu.kinetic_energy(D, dev(u))
+    assert abs(ke - R.kinetic_energy(u)) <= 1e-12 * abs(R.kinetic_energy(u))
+
+
+@pytest.mark.parametrize("dim,n_el,ku,kp,amp", [(2, 2, 2, 1, 0.05), (2, 3, 3, 2, 0.0), (3, 2, 2, 1, 0.03),
+                                                (3, 2, 3, 2, 0.0)])
+def test_momentum_rhs_full(ref, gpu, dim, n_el, ku, kp, amp):
+    """test_forms.cpp:255-310: 2 viscous, 2 advective, pressure and Dirichlet data terms."""
+    R, D = pair(ref, gpu, dim, n_el, ku, kp, amp, dirichlet_seed=5)
+    un = gpu.seeded_uniform(41, R.n_u)
+    ug = gpu.seeded_uniform(42, R.n_u)
+    wx = gpu.seeded_uniform(43, R.n_u)
+    pp = gpu.seeded_uniform(44, R.n_p)
+    want = R.momentum_rhs(mass=[(2.9, un)], visc=[(0.65, un), (0.3, ug)], adv=[(0.5, un, wx), (0.25, ug, ug)],
+                          pres=[(1.0, pp)], dir_visc=0.65, dir_adv=0.5, dir_w=wx, time=0.0)
+    dun, dug, dwx, dpp = dev(un), dev(ug), dev(wx), dev(pp)
+    spec = gpu.MomentumRhs(mass=[(2.9, dun)], visc=[(0.65, dun), (0.3, dug)],
+                           adv=[(0.5, dun, dwx), (0.25, dug, dug)], pres=[(1.0, dpp)], dir_visc_coef=0.65,
+                           dir_adv_coef=0.5, dir_w=dwx)
+    y = D.zeros()
+    gpu.momentum_rhs(D, spec, y)
+    assert rel(host(y), want) <= TOL_APPLY
+
+
+def test_rhs_outlet_drops_pressure_boundary_flux(ref, gpu):
+    R, D = pair(ref, gpu, 2, 2, 2, 1, 0.0, outlet=1)
+    pp = gpu.seeded_uniform(52, R.n_p)
+    want = R.momentum_rhs(pres=[(1.0, pp)])
+    y = D.zeros()
+    gpu.momentum_rhs(D, gpu.MomentumRhs(pres=[(1.0, dev(pp))]), y)
+    assert rel(host(y), want) <= TOL_APPLY
+
+
+@pytest.mark.parametrize("dim,n_el,ku,kp,amp", [(2, 4, 2, 1, 0.05), (3, 3, 2, 1, 0.0), (3, 2, 3, 2, 0.03)])
+def test_krylov_iteration_parity(ref, gpu, dim, n_el, ku, kp, amp):
+    """Jacobi-CG on the pressure Helmholtz operator and Jacobi-GMRES on the momentum
+    operator (test_krylov.cpp:215-274): iteration counts within +-1, solutions agree."""
+    R, D = pair(ref, gpu, dim, n_el, ku, kp, amp)
+    mc = 1.0 / (1e6 * 0.2929 ** 2 * 1e-6)
+    b = gpu.seeded_uniform(61, R.n_p)
+    x_ref, it_ref, _ = R.solve(1, 0, (mc, 0, 0, 0), None, b, np.zeros(R.n_p))
+    diag = D.zeros(gpu.SPACE_P)
+    gpu.helmholtz_diagonal(D, mc, diag)
+    M = gpu.JacobiPreconditioner(D, diag)
+    x = D.zeros(gpu.SPACE_P)
+    res = gpu.cg_solve(D, gpu.LinearOperator.pressure_helmholtz(mc), dev(b), gpu.SolverSettings(), M, x)
+    assert abs(res.iterations - it_ref) <= 1
+    assert rel(host(x), x_ref) <= 1e-8
+
+    coefs = (1.0 / (0.2929 * 1e-2), 0.005, 0.5, 0.0)
+    w = gpu.seeded_uniform(62, R.n_u)
+    bu = gpu.seeded_uniform(63, R.n_u)
+    xu_ref, itu_ref, _ = R.solve(0, 1, coefs, w, bu, np.zeros(R.n_u), restart=10)
+    ctx = gpu.MomentumCtx(*coefs, advecting=dev(w))
+    diag = D.zeros()
+    gpu.momentum_diagonal(D, ctx, diag)
+    M = gpu.JacobiPreconditioner(D, diag)
+    xu = D.zeros()
+    res = gpu.gmres_solve(D, gpu.LinearOperator.momentum(ctx), dev(bu), gpu.SolverSettings(restart=10), M, xu)
+    assert abs(res.iterations - itu_ref) <= 1
+    assert rel(host(xu), xu_ref) <= 1e-8
+
+
+def test_solver_budget_exhaustion_raises_with_history(ref, gpu):
+    """test_krylov.cpp:317-341: SolverError carries a history of length max_iter."""
+    R, D = pair(ref, gpu, 2, 4, 2, 1)
+    b = gpu.seeded_uniform(71, R.n_p)
+    with pytest.raises(gpu.SolverError) as ei:
+        gpu.cg_solve(D, gpu.LinearOperator.pressure_helmholtz(0.0), dev(b),
+                     gpu.SolverSettings(max_iter=3), None, D.zeros(gpu.SPACE_P))
+    assert len(ei.value.history) == 3
+    with pytest.raises(ref.RefSolverError) as er:
+        R.solve(1, 0, (0.0, 0, 0, 0), None, b, np.zeros(R.n_p), max_iter=3, precond=False)
+    assert len(er.value.history) == 3
+
+
+def test_jacobi_zero_diagonal_names_dof(gpu):
+    D = gpu.DGContext(2, 2, 2, 1)
+    d = D.zeros(gpu.SPACE_P) + 1.0
+    d[2] = 0.0
+    with pytest.raises(gpu.SolverError, match="dof 2"):
+        gpu.JacobiPreconditioner(D, d)
+
+
+def test_zero_rhs_zero_iterations(gpu):
+    D = gpu.DGContext(2, 2, 2, 1)
+    x = D.zeros(gpu.SPACE_P) + 3.0
+    r = gpu.cg_solve(D, gpu.LinearOperator.pressure_helmholtz(1.0), D.zeros(gpu.SPACE_P),
+                     gpu.SolverSettings(), None, x)
+    assert r.iterations == 0 and float(x.abs().max()) == 0.0
+
+
+def _step_case(ref, gpu, dim, n_el, ku, kp, Re, dt, seed, steps, restart=50):
+    R, D = pair(ref, gpu, dim, n_el, ku, kp, 0.0, dirichlet_seed=seed)
+    f = gpu.SynthField(dim, seed)
+    u0 = f.interpolate(D)
+    p0 = np.zeros(R.n_p)
+    u_prev, u, p = u0.copy(), u0.copy(), p0.copy()
+    du_prev, du, dp = dev(u0), dev(u0), dev(p0)
+    for n in range(steps):
+        params = [dt, Re, 1e3, n * dt, restart, 1e-10, 1e-10, 1e-12, 10000, 1.0 if n == 0 else 0.0]
+        u1, p1, its_ref = R.step(params, u_prev, u, p)
+        P = gpu.StepParams(dt=dt, Re=Re, c=1e3, time=n * dt, restart=restart, first_step=(n == 0))
+        du1, dp1 = D.zeros(), D.zeros(gpu.SPACE_P)
+        its = gpu.trbdf2_step(D, P, du_prev, du, dp, du1, dp1)
+        for a, b in zip(its, its_ref):
+            assert abs(a - b) <= 1, (its, its_ref)
+        u_prev, u, p = u, u1, p1
+        du_prev, du, dp = du, du1, dp1
+    hu, hp = host(du), host(dp)
+    assert rel(hu, u) <= TOL_FIELD
+    # pressure compared after removing its mean
+    assert rel(hp - hp.mean(), p - p.mean()) <= TOL_FIELD or rel(hp, p) <= TOL_FIELD
+    return its_ref
+
+
+def test_trbdf2_step_2d_small(ref, gpu):
+    _step_case(ref, gpu, 2, 8, 2, 1, Re=100.0, dt=1e-3, seed=0, steps=2)
+
+
+def test_trbdf2_step_cfg1(ref, gpu):
+    """BASELINE configs[0]: 2D 32x32, Q2/Q1, nu = 1/100, dt = 1e-3, seed 0 (one full step)."""
+    _step_case(ref, gpu, 2, 32, 2, 1, Re=100.0, dt=1e-3, seed=0, steps=1)
+
+
+def test_trbdf2_step_3d_small(ref, gpu):
+    _step_case(ref, gpu, 3, 3, 2, 1, Re=100.0, dt=1e-3, seed=1, steps=1)
