@@ -1,0 +1,342 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 DG hot path (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[2], the north-star config): 3D unit cube,
+64^3 affine hex mesh, velocity DG Q3 (3 comps, 50,331,648 DoF), pressure Q2
+(7,077,888 DoF), fp64.  A "step" is one pass of the hot path over one batch
+of synthetic input: ONE momentum-operator apply (stage-1 TR-BDF2 operator,
+mass 1/(gamma dt) + visc 1/(2Re) + LF advection 1/2 with w = u^0, the seeded
+curl-of-vector-potential field, seed 2) followed by ONE pressure-Helmholtz
+apply (mass_coef 1/(c^2 gamma^2 dt^2)), on U[-1,1] seeded vectors (seeds
+1002 / 2002).  value = (N_u + N_p) / step time [GDoF/s], whole job over N GPUs
+(replicas: the path is single-GPU; each rank runs its own copy, weak scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+--impl reference times the unmodified reference CPU implementation
+(oracle/_ref/libdgref.so: /root/reference/proj/src compiled as-is) with all
+host threads on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+GAMMA = 2.0 - math.sqrt(2.0)
+CFG = dict(workload="cfg3: 3D 64^3 unit cube affine, Q3/Q2 velocity/pressure, fp64 "
+                    "(1 momentum apply + 1 pressure apply per step)",
+           dim=3, n_el=64, ku=3, kp=2, seed=2, Re=1000.0, dt=1e-3, c=1e3)
+# algorithmic fp64 flop / DoF and bytes / DoF at cfg3
+FLOP_PER_DOF = {"momentum": 545.9, "pressure": 406.2}
+BYTES_PER_DOF = {"momentum": 24.0, "pressure": 16.0}
+CPU_SAMPLE_NEL = 16   # reference CPU leg: same degrees/coefficients on a 16^3 mesh
+
+
+def coefficients():
+    dt, Re, c = CFG["dt"], CFG["Re"], CFG["c"]
+    mom = (1.0 / (GAMMA * dt), 1.0 / (2.0 * Re), 0.5, 0.0)
+    pmc = 1.0 / (c * c * GAMMA * GAMMA * dt * dt)
+    return mom, pmc
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference CPU leg
+# ---------------------------------------------------------------------------
+def reference_sample(nthreads: int, napplies: int):
+    """Times the unmodified reference apply_momentum + apply_pressure_helmholtz on
+    nthreads concurrent host threads (the reference is single-threaded; each
+    thread runs its own applies) on a CPU_SAMPLE_NEL^3 mesh, same degrees and
+    coefficients.  Returns (DoF/s, seconds, dofs per thread-step, description)."""
+    import reforacle
+    import paper_2107_07776_b200 as dg  # synthetic inputs only (host code)
+    R = reforacle.RefCtx(CFG["dim"], CPU_SAMPLE_NEL, CFG["ku"], CFG["kp"])
+    mom, pmc = coefficients()
+    f = dg.SynthField(CFG["dim"], CFG["seed"])
+    # w at the reference nodes (host evaluation of the same field)
+    w = np.zeros(R.n_u)
+    xn = np.zeros((R.ncells, (CFG["ku"] + 1) ** 3, 3))
+    reforacle.lib().ref_node_points(R.h, 0, reforacle.P(xn))
+    nb = (CFG["ku"] + 1) ** 3
+    for cell in range(R.ncells):
+        for j in range(nb):
+            v = f.eval(xn[cell, j])
+            for comp in range(3):
+                w[cell * 3 * nb + comp * nb + j] = v[comp]
+    x = dg.seeded_uniform(CFG["seed"] + 1000, R.n_u)
+    xp = dg.seeded_uniform(CFG["seed"] + 2000, R.n_p)
+    t_m = R.bench(0, mom, w, x, nthreads, napplies)
+    t_p = R.bench(1, (pmc, 0, 0, 0), None, xp, nthreads, napplies)
+    dofs = (R.n_u + R.n_p) * nthreads * napplies
+    secs = t_m + t_p
+    desc = (f"{CPU_SAMPLE_NEL}^3 mesh, Q3/Q2, same coefficients; {napplies} momentum + {napplies} pressure "
+            f"applies per thread, {nthreads} thread(s); reference backend {reforacle.lib().ref_backend().decode()}")
+    return dofs / secs, secs, R.n_u + R.n_p, desc, {"momentum_s_per_apply": t_m / napplies,
+                                                      "pressure_s_per_apply": t_p / napplies,
+                                                      "n_u": R.n_u, "n_p": R.n_p}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_info()
+    if rank != 0:
+        return
+    nthreads = max(1, os.cpu_count() or 1)
+    for _ in range(args.warmup):
+        pass  # the reference leg warms its lazy geometry cache inside each ref_bench call
+    rate, secs, _, desc, extra = reference_sample(nthreads, max(1, args.steps))
+    val = rate / 1e9
+    line = {"metric": "fp64 DG op-apply throughput (momentum + pressure), GDoF/s", "value": val,
+            "unit": "GDoF/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": secs / max(1, args.steps) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE cfg3 construction)",
+            "config": {"workload": CFG["workload"], "sample": desc}, "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": "GDoF/s", "cores": nthreads, "kind": "reference",
+                             "sample": desc},
+            "e2e": {"value": val, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "detail": extra}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# device leg
+# ---------------------------------------------------------------------------
+def run_device(args):
+    import torch
+    import paper_2107_07776_b200 as dg
+
+    ws, rank, local = dist_info()
+    if ws > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    mom, pmc = coefficients()
+    t0 = time.time()
+    D = dg.DGContext(CFG["dim"], CFG["n_el"], CFG["ku"], CFG["kp"], device=local)
+    stream = D.stream
+    f = dg.SynthField(CFG["dim"], CFG["seed"])
+    w = D.zeros()
+    dg.interpolate_synth_device(D, f, w)
+    x_h = torch.from_numpy(dg.seeded_uniform(CFG["seed"] + 1000, D.n_u))
+    xp_h = torch.from_numpy(dg.seeded_uniform(CFG["seed"] + 2000, D.n_p))
+    x = x_h.to(dev)
+    xp = xp_h.to(dev)
+    y = D.zeros()
+    yp = D.zeros(dg.SPACE_P)
+    ctx = dg.MomentumCtx(*mom, advecting=w)
+    setup_s = time.time() - t0
+    peak_fp64 = dg.fp64_peak_tflops(D)
+
+    def step():
+        dg.apply_momentum(D, ctx, x, y)
+        dg.apply_pressure_helmholtz(D, pmc, xp, yp)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        tdist.barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 2)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    launches0 = D.launch_count()
+    ev[0].record(stream)
+    for k in range(args.steps):
+        dg.apply_momentum(D, ctx, x, y)
+        ev[1 + 2 * k].record(stream)
+        dg.apply_pressure_helmholtz(D, pmc, xp, yp)
+        ev[2 + 2 * k].record(stream)
+    torch.cuda.synchronize()
+    launches = D.launch_count() - launches0
+    clocks = sampler.stop()
+    total_ms = ev[0].elapsed_time(ev[2 * args.steps])
+    t_mom = [ev[2 * k].elapsed_time(ev[1 + 2 * k]) if k else ev[0].elapsed_time(ev[1]) for k in range(args.steps)]
+    t_prs = [ev[1 + 2 * k].elapsed_time(ev[2 + 2 * k]) for k in range(args.steps)]
+    ms_step = total_ms / args.steps
+    if ws > 1:
+        tt = torch.tensor([ms_step], device=dev)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        ms_step = float(tt.item())
+    dofs_step = D.n_u + D.n_p
+    value = ws * dofs_step / (ms_step * 1e-3) / 1e9
+
+    # ---- end-to-end through the public API with host buffers (pinned), copies timed
+    xh = x_h.pin_memory()
+    wh = w.cpu().pin_memory()
+    xph = xp_h.pin_memory()
+    yh = torch.empty(D.n_u, dtype=torch.float64).pin_memory()
+    yph = torch.empty(D.n_p, dtype=torch.float64).pin_memory()
+    xd, wd, xpd = torch.empty_like(x), torch.empty_like(w), torch.empty_like(xp)
+    ctx_e2e = dg.MomentumCtx(*mom, advecting=wd)
+
+    def e2e_step():
+        xd.copy_(xh, non_blocking=True)
+        wd.copy_(wh, non_blocking=True)
+        xpd.copy_(xph, non_blocking=True)
+        dg.apply_momentum(D, ctx_e2e, xd, y)
+        dg.apply_pressure_helmholtz(D, pmc, xpd, yp)
+        yh.copy_(y, non_blocking=True)
+        yph.copy_(yp, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ne2e = max(1, min(args.steps, 5))
+    e0.record(stream)
+    for _ in range(ne2e):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / ne2e
+    if ws > 1:
+        tt = torch.tensor([e2e_ms], device=dev)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    e2e_val = ws * dofs_step / (e2e_ms * 1e-3) / 1e9
+
+    if rank != 0:
+        if ws > 1:
+            tdist.barrier()
+            tdist.destroy_process_group()
+        return
+    # ---- roofline of the dominant kernel (momentum apply, fp64-bound at cfg3)
+    tm = float(np.mean(t_mom)) * 1e-3
+    tp = float(np.mean(t_prs)) * 1e-3
+    mom_tflops = FLOP_PER_DOF["momentum"] * D.n_u / tm / 1e12
+    prs_tflops = FLOP_PER_DOF["pressure"] * D.n_p / tp / 1e12
+    peaks = measured_peaks()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "momentum_traffic.json")) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "fp64", "achieved": mom_tflops, "peak": peak_fp64, "unit": "TFLOP/s",
+                "frac": mom_tflops / peak_fp64, "traffic": traffic,
+                "kernel": "k_momentum (dgb_momentum_apply)",
+                "algorithmic": f"{FLOP_PER_DOF['momentum']} flop/DoF x {D.n_u} DoF per launch (SURVEY 8d)",
+                "peak_source": "DFMA microbenchmark measured live (dgb_fp64_peak); MEASURED_PEAKS.json has no fp64"}
+    roofline_hbm = {"achieved": BYTES_PER_DOF["momentum"] * D.n_u / tm / 1e9, "peak": peaks.get("hbm_gbs"),
+                    "unit": "GB/s",
+                    "frac": BYTES_PER_DOF["momentum"] * D.n_u / tm / 1e9 / peaks.get("hbm_gbs", 6535.7)}
+    # ---- CPU baseline: reference on one host core, bounded sample
+    cpu = None
+    if ws == 1 and not args.no_cpu:
+        try:
+            rate, secs, _, desc, extra = reference_sample(1, 1)
+            cpu = {"value": rate / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "reference", "sample": desc,
+                   "detail": extra}
+        except Exception as e:  # oracle not built on this box
+            cpu = {"value": None, "unit": "GDoF/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
+    line = {
+        "metric": "fp64 DG op-apply throughput (momentum + pressure), GDoF/s",
+        "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": args.steps, "warmup": max(3, args.warmup),
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded; BASELINE cfg3 vector-potential field, U[-1,1] vectors)",
+        "config": {"workload": CFG["workload"], "mesh": "64^3", "degrees": "Q3/Q2", "n_u": D.n_u, "n_p": D.n_p,
+                   "Re": CFG["Re"], "dt": CFG["dt"], "c": CFG["c"], "parallelism": f"replicas x{ws}",
+                   "l2": "inputs larger than L2 (x, w 403 MB each); the momentum apply streams 1.2 GB between "
+                         "pressure applies"},
+        "ops": {"momentum": {"ms": tm * 1e3, "gdofs": D.n_u / tm / 1e9, "tflops_alg": mom_tflops},
+                "pressure": {"ms": tp * 1e3, "gdofs": D.n_p / tp / 1e9, "tflops_alg": prs_tflops}},
+        "roofline": roofline, "roofline_hbm": roofline_hbm, "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * (2 * D.n_u + D.n_p),
+                "d2h_bytes_per_step": 8 * (D.n_u + D.n_p)},
+        "gpu_launches": int(launches), "clocks": clocks, "setup_s": setup_s,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="dgb", choices=["dgb", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_device(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -60,7 +60,7 @@ void dgb_ctx_destroy(dgb_ctx* ctx);
 /* info[16]: ncells, n_u, n_p, n_interior_faces, n_boundary_faces, ku, kp, dim, affine,
  *           nqf_bdry (points per boundary face at rule ku+2), device, 0... */
 int dgb_ctx_info(dgb_ctx* ctx, long long* info);
-/* Use an external cudaStream_t (NULL = the context's own stream). */
+/* Use an external cudaStream_t (NULL = the legacy default stream); a new context uses its own stream. */
 int dgb_set_stream(dgb_ctx* ctx, void* cuda_stream);
 void* dgb_get_stream(dgb_ctx* ctx);
 int dgb_sync(dgb_ctx* ctx);
@@ -200,6 +200,12 @@ int dgb_synth_init(int dim, unsigned long long seed, double scale, double* user)
 void dgb_synth_eval(const double* x, double t, double* out, void* user);
 /* Nodal interpolation of the synthetic field into the velocity space (host array). */
 int dgb_interpolate_synth(dgb_ctx* ctx, const double* user, double* h_u);
+/* Same on the device (fp64 cos on the GPU; agrees with the host version to rounding). */
+int dgb_interpolate_synth_device(dgb_ctx* ctx, const double* user, double* d_u);
+/* Host-only helpers (no GPU needed): the context's mesh setup and 1D tables. */
+int dgb_host_mesh_cartesian(int dim, int n_el, double amp, unsigned seed, long long* sizes, int* iface,
+                            int* bface, double* cell_measure, double* face_measure, double* vertices);
+int dgb_host_tables(int n, int q, double* B, double* D, double* dE, double* w);
 
 /* ------------------------------------------------------------------ measurement */
 /* Milliseconds of the last kernel launch timed with dgb_timer_* (CUDA events on the ctx stream). */

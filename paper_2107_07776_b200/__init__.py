@@ -135,6 +135,7 @@ def lib() -> C.CDLL:
     L.dgb_synth_eval.argtypes = [_dp, C.c_double, _dp, C.c_void_p]
     L.dgb_synth_eval.restype = None
     L.dgb_interpolate_synth.argtypes = [C.c_void_p, _dp, _dp]
+    L.dgb_interpolate_synth_device.argtypes = [C.c_void_p, _dp, C.c_void_p]
     L.dgb_timer_start.argtypes = [C.c_void_p]
     L.dgb_timer_stop.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
     L.dgb_fp64_peak.argtypes = [C.c_void_p, _dp]
@@ -515,6 +516,10 @@ class SynthField:
         out = np.zeros(V.n_u)
         _check(lib().dgb_interpolate_synth(V.handle, _np_ptr(self.user), _np_ptr(out)))
         return out
+
+
+def interpolate_synth_device(V: DGContext, f: "SynthField", out):
+    _check(lib().dgb_interpolate_synth_device(V.handle, _np_ptr(f.user), _ptr(out)))
 
 
 def fp64_peak_tflops(V: DGContext) -> float:

@@ -95,7 +95,8 @@ int dgb_ctx_info(dgb_ctx* h, long long* info) {
 
 int dgb_set_stream(dgb_ctx* h, void* s) {
   NEED(h, "null ctx");
-  h->c.dc.stream = s ? static_cast<cudaStream_t>(s) : h->c.own_stream;
+  // NULL selects the legacy default stream (what torch's default current stream is)
+  h->c.dc.stream = static_cast<cudaStream_t>(s);
   return DGB_OK;
 }
 void* dgb_get_stream(dgb_ctx* h) { return h ? static_cast<void*>(h->c.dc.stream) : nullptr; }
