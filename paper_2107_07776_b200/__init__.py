@@ -143,6 +143,8 @@ def lib() -> C.CDLL:
     L.dgb_launch_count.restype = C.c_longlong
     L.dgb_host_mesh_cartesian.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint, _llp, _ip, _ip, _dp, _dp, _dp]
     L.dgb_host_tables.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _dp]
+    L.dgb_set_fast_path.argtypes = [C.c_void_p, C.c_int]
+    L.dgb_fast_path_active.argtypes = [C.c_void_p]
     _lib = L
     return L
 
@@ -264,6 +266,14 @@ class DGContext:
         bd = np.zeros((self.n_boundary, 3), dtype=np.int32)
         _check(lib().dgb_face_lists(self._h, it.ctypes.data_as(_ip), bd.ctypes.data_as(_ip)))
         return it, bd
+
+    def set_fast_path(self, enable: bool):
+        """Fast axis-aligned 3D kernels (default) or the generic kernels."""
+        _check(lib().dgb_set_fast_path(self._h, int(bool(enable))))
+
+    @property
+    def fast_path_active(self) -> bool:
+        return bool(lib().dgb_fast_path_active(self._h))
 
     def launch_count(self) -> int:
         return int(lib().dgb_launch_count(self._h))

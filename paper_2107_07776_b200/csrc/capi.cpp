@@ -465,3 +465,12 @@ extern "C" int dgb_host_tables(int n, int q, double* B, double* D, double* dE, d
   dgb::host_w(q, w);
   return DGB_OK;
 }
+
+// Route axis-aligned 3D applies to the fast kernels (1, default) or force the
+// generic kernels (0).  Both are parity-tested against the reference.
+extern "C" int dgb_set_fast_path(dgb_ctx* h, int enable) {
+  NEED(h, "null ctx");
+  h->c.use_fast = enable != 0;
+  return DGB_OK;
+}
+extern "C" int dgb_fast_path_active(dgb_ctx* h) { return h && h->c.use_fast && h->c.dc.axis ? 1 : 0; }

@@ -130,6 +130,19 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
     }
     cudaMemcpy(d, g.data(), g.size() * sizeof(double), cudaMemcpyHostToDevice);
     dc.aff = d;
+    // axis-aligned: every Jinv off-diagonal zero up to rounding (Cartesian generator;
+    // the multilinear Jacobian of a box cell can carry ~1e-17 cancellation residue)
+    const int st = affine_cell_stride(dim);
+    bool axis = dim == 3;
+    for (int c = 0; c < mesh.ncells && axis; ++c)
+      for (int a = 0; a < dim && axis; ++a)
+        for (int b = 0; b < dim; ++b)
+          if (a != b && std::abs(g[(size_t)c * st + a * dim + b]) >
+                            1e-13 * std::abs(g[(size_t)c * st + a * dim + a])) {
+            axis = false;
+            break;
+          }
+    dc.axis = axis;
   } else {
     const int rules[3] = {ku + 1, ku + 2, kp + 2};
     for (int Q : rules) {
@@ -192,6 +205,13 @@ int Context::momentum(const double* coefs, const double* w, const double* x, dou
   const MomCoef co{coefs[0], coefs[1], coefs[2], coefs[3]};
   if ((co.adv != 0.0 || co.skew != 0.0) && !w) return fail(DGB_E_MISSING_FIELD, "apply_momentum: advecting field missing");
   ++launches;
+  if (use_fast && dc.axis) {
+    const cudaError_t e = fast_momentum3(dc, co, w, x, y);
+    if (e != cudaErrorNotSupported) {
+      CK(e);
+      return DGB_OK;
+    }
+  }
   CK(opu->momentum(dc, co, w, x, y));
   return DGB_OK;
 }
@@ -205,6 +225,13 @@ int Context::momentum_diag(const double* coefs, const double* w, double* d) {
 }
 int Context::sip(double mc, int dir, const double* x, double* y) {
   ++launches;
+  if (use_fast && dc.axis) {
+    const cudaError_t e = fast_sip3(dc, mc, dir, x, y);
+    if (e != cudaErrorNotSupported) {
+      CK(e);
+      return DGB_OK;
+    }
+  }
   CK(opp->sip(dc, mc, dir, x, y));
   return DGB_OK;
 }

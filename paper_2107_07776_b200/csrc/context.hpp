@@ -30,6 +30,7 @@ class Context {
   cudaStream_t own_stream = nullptr;
   int bctype_h[64] = {};
   long long launches = 0;
+  bool use_fast = true;  // route axis-aligned 3D applies to fast_axis.cuh
 
   ~Context();
   int init(HostMesh&& m, int ku, int kp, int device, std::string& err);

@@ -45,6 +45,7 @@ struct RhsArgs {
 struct DevCtx {
   int dim = 0, ku = 0, kp = 0, ncells = 0;
   bool affine = true;
+  bool axis = false;  // affine with diagonal Jinv on every cell (fast_axis.cuh)
   MeshArgs mesh;
   const double* aff = nullptr;
   const double* qcell[kMaxRule] = {};
@@ -65,6 +66,10 @@ struct OpTable {
   cudaError_t (*kinetic)(const DevCtx&, const double* u, double* partial, int* nblocks);
   cudaError_t (*tables)();
 };
+
+// fast axis-aligned 3D kernels (fast_d3.cu); cudaErrorNotSupported when not applicable
+cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, double* y);
+cudaError_t fast_momentum3(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);
 
 // defined in ops_d{2,3}_k{1..4}.cu
 #define DGB_DECL_OPS(D, K) const OpTable& ops_d##D##_k##K();
