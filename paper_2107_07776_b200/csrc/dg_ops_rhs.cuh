@@ -453,7 +453,9 @@ __global__ void __launch_bounds__(kThreads) k_momentum_diag(MeshArgs m, GeoArgs 
         double wg = 0.0;
 #pragma unroll
         for (int d = 0; d < DIM; ++d) wg += wq[d * NQ + q] * g[d];
-        s += -co.adv * phi * wg * jxw + co.skew * wq[DIM * NQ + q] * phi * phi * jxw;
+        s += -co.adv * phi * wg * jxw;
+        // div w is only computed (and the slot only initialised) when skew != 0
+        if (co.skew != 0.0) s += co.skew * wq[DIM * NQ + q] * phi * phi * jxw;
       }
     }
     for (int f = 0; f < NF; ++f) {

@@ -1,20 +1,30 @@
 // Fast path for axis-aligned affine hexahedra (every BASELINE config except
 // the deformed cfg4): Jinv = diag(1/h), constant per cell.
 //
-// On such cells every LINEAR term of the reference operators is integrated
-// exactly by its Gauss rule (degree <= 2k integrands with >= k+1 points), so
-// the rule can be replaced by the exact 1D matrices
-//     M = B^T W B   (mass),   K = D^T W D   (stiffness),
-// giving Kronecker-structured cell operators (mass + SIP volume terms) and
-// nodal face terms with tangential mass matrices.  Results equal the
-// reference's quadrature sums up to rounding.
-// The advective (nonlinear) terms keep the reference's k+2 Gauss rule
-// (forms.cpp:501) with sum factorisation; the LF face flux is evaluated at
-// the face Gauss points (forms.cpp:555-573).
+// Exactness.  On such cells every LINEAR term of the reference operators is
+// integrated exactly by its Gauss rule (polynomial integrands of degree <= 2k
+// per direction with >= k+1 points), so the rule can be replaced by the exact
+// 1D matrices  M = B^T W B,  K = D^T W D  and the SIP operator (cell stiffness
+// + interior-penalty / consistency / symmetry face terms, forms.cpp:148-243,
+// :397-495) splits EXACTLY into 1D line operators along each direction:
 //
-// Kernel structure: one CTA owns C cells; each stage is a flat loop of 1D
-// "line" work items over all cells / components / faces, separated by
-// __syncthreads(); element-centric faces (no atomics).
+//     A_sip u = sum_d (S_d (x) M (x) M) u,   S_d = 1D SIP operator along d
+//                                            (stiffness + the two d-faces, which
+//                                            read the neighbours' d-lines)
+//     M u     = (M (x) M (x) M) u
+//
+// (tangential face integrals are the tangential mass matrices).  Results
+// equal the reference's quadrature sums up to rounding.  The
+// advective (nonlinear) terms keep the reference's k+2 Gauss rule
+// (forms.cpp:501) with sum factorisation; the Lax-Friedrichs face flux is
+// evaluated at the face Gauss points (forms.cpp:555-573).
+//
+// Kernel structure: one CTA owns C cells; every stage is a flat loop over 1D
+// "line" work items (all cells / components / directions at once) separated
+// by __syncthreads().  Element-centric faces: each cell integrates all of its
+// faces, reading neighbour lines from global memory (L2), so every output DoF
+// is written exactly once — no atomics, deterministic.  Shared-memory tensors
+// use an odd x-pitch so line accesses are bank-conflict free.
 #pragma once
 
 #include "dg_common.cuh"
@@ -52,40 +62,136 @@ static inline cudaError_t ensure_ftab() {
 // affine record (GeoAff layout): Jinv[9], detJ, faces...
 constexpr int kAffStride3 = 9 + 1 + 6 * 4;
 
-__device__ __forceinline__ bool fa_outlet(const MeshArgs& m, int nb) {
-  const int bid = -1 - nb;
-  return bid >= 0 && bid < 64 && m.bctype[bid] == 1;
+// padded cell tensor: x-pitch odd
+template <int N>
+struct Pad {
+  static constexpr int PX = N | 1;
+  static constexpr int PY = PX * N;
+  static constexpr int CT = PY * N;
+  __device__ __forceinline__ static int idx(int i, int j, int k) { return i + PX * j + PY * k; }
+};
+
+// per-cell face / geometry record kept in shared memory
+struct CellInfo {
+  double ih[3];    // 1/h_d  (Jinv diagonal)
+  double detJ;
+  double A[3];     // face areas detJ / h_d
+  double pen[6];   // (deg+1)^2 * penalty ratio (interior mean / boundary own)
+  double ihn[6];   // neighbour's 1/h_d across each face
+  int nb[6];       // neighbour cell, or -1 - boundary id
+  int type[6];     // 0 interior, 1 dirichlet, 2 outlet
+};
+constexpr int kInfoDoubles = (sizeof(CellInfo) + 7) / 8;
+
+__device__ __forceinline__ void load_info(CellInfo& ci, const MeshArgs& m, const double* __restrict__ aff, int cell,
+                                          double sfac) {
+  const double* r = aff + (size_t)cell * kAffStride3;
+  ci.ih[0] = r[0];
+  ci.ih[1] = r[4];
+  ci.ih[2] = r[8];
+  ci.detJ = r[9];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) ci.A[d] = ci.detJ * ci.ih[d];
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const int nb = m.nbr[(size_t)cell * 6 + f];
+    ci.nb[f] = nb;
+    ci.pen[f] = sfac * m.pen[(size_t)cell * 6 + f];
+    if (nb >= 0) {
+      ci.type[f] = 0;
+      ci.ihn[f] = __ldg(aff + (size_t)nb * kAffStride3 + 4 * (f >> 1));
+    } else {
+      const int bid = -1 - nb;
+      ci.type[f] = (bid >= 0 && bid < 64 && m.bctype[bid] == 1) ? 2 : 1;
+      ci.ihn[f] = 0.0;
+    }
+  }
 }
 
-// index of a cell node with coordinate `layer` along axis a and tangential coords (p, q)
-// (p along the lower tangential axis, q along the upper)
+// 1D SIP line operator along direction d (stiffness + both d-faces), times `scale`.
+// u: own line; uL / uR: neighbour lines across faces 2d / 2d+1 (read only if interior).
+// dirichlet: whether non-interior, non-outlet faces carry the Dirichlet-type terms
+// (momentum: always; pressure Helmholtz: never (natural); Laplacian: flag).
 template <int N>
-__device__ __forceinline__ int face_node(int a, int layer, int p, int q) {
-  if (a == 0) return layer + N * (p + N * q);
-  if (a == 1) return p + N * (layer + N * q);
-  return p + N * (q + N * layer);
-}
-template <int N>
-__device__ __forceinline__ int axis_stride(int a) {
-  return a == 0 ? 1 : (a == 1 ? N : N * N);
+__device__ __forceinline__ void sip_line(const FTab<N, N>& t, const CellInfo& ci, int d, const double* u,
+                                         const double* uL, const double* uR, bool dirichlet, double scale,
+                                         double* out) {
+  const double ih = ci.ih[d], A = ci.A[d];
+  const double stiff = scale * A * ih;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) s = fma(t.K[i][l], u[l], s);
+    out[i] = stiff * s;
+  }
+  // right face (side 1, outward normal +e_d)
+  {
+    const int f = 2 * d + 1;
+    const int ty = ci.type[f];
+    double F = 0.0, GT = 0.0;
+    double gs = 0.0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) gs = fma(t.dE[1][l], u[l], gs);
+    const double us = u[N - 1];
+    if (ty == 0) {
+      double go = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) go = fma(t.dE[0][l], uR[l], go);
+      const double ju = us - uR[0];
+      F = -0.5 * (gs * ih + go * ci.ihn[f]) + ci.pen[f] * ju;
+      GT = -0.5 * ju;
+    } else if (ty == 1 && dirichlet) {
+      F = -gs * ih + 2.0 * ci.pen[f] * us;
+      GT = -us;
+    }
+    const double sa = scale * A;
+    out[N - 1] = fma(sa, F, out[N - 1]);
+    const double g2 = sa * ih * GT;
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = fma(t.dE[1][i], g2, out[i]);
+  }
+  // left face (side 0, outward normal -e_d)
+  {
+    const int f = 2 * d;
+    const int ty = ci.type[f];
+    double F = 0.0, GT = 0.0;
+    double gs = 0.0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) gs = fma(t.dE[0][l], u[l], gs);
+    const double us = u[0];
+    if (ty == 0) {
+      double go = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) go = fma(t.dE[1][l], uL[l], go);
+      const double ju = us - uL[N - 1];
+      F = 0.5 * (gs * ih + go * ci.ihn[f]) + ci.pen[f] * ju;
+      GT = -0.5 * ju;
+    } else if (ty == 1 && dirichlet) {
+      F = gs * ih + 2.0 * ci.pen[f] * us;
+      GT = -us;
+    }
+    const double sa = scale * A;
+    out[0] = fma(sa, F, out[0]);
+    const double g2 = -sa * ih * GT;
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = fma(t.dE[0][i], g2, out[i]);
+  }
 }
 
 // ===========================================================================
 // Scalar SIP (pressure Helmholtz / Laplacian), axis-aligned affine, 3D.
+//   y = mc detJ (M M M) u + sum_d (S_d (x) M (x) M) u
 // ===========================================================================
 template <int KP>
 struct SipAxisCfg {
-  static constexpr int N = KP + 1, Q = KP + 2, NB = N * N * N, NF = N * N;
-  static constexpr int C = KP == 1 ? 64 : (KP == 2 ? 28 : 16);  // cells per CTA
-  static constexpr int T = 256;
-  // per-cell shared layout (doubles)
-  static constexpr int O_U = 0, O_OUT = NB, O_A = 2 * NB, O_B = 3 * NB, O_C = 4 * NB, O_D = 5 * NB;
-  static constexpr int O_F = 6 * NB;              // 6 faces x NF : F
-  static constexpr int O_G = O_F + 6 * NF;        // GT
-  static constexpr int O_F1 = O_G + 6 * NF;       // t1-stage outputs
-  static constexpr int O_G1 = O_F1 + 6 * NF;
-  static constexpr int O_GEO = O_G1 + 6 * NF;     // h0, h1, h2, detJ
-  static constexpr int PER = O_GEO + 4;
+  static constexpr int N = KP + 1, NB = N * N * N, NF = N * N;
+  using P = Pad<N>;
+  static constexpr int C = KP == 1 ? 32 : (KP == 2 ? 16 : 8);  // cells per CTA
+  static constexpr int T = KP == 1 ? 128 : (KP == 2 ? 144 : 128);
+  static constexpr int O_U = 0, O_SX = P::CT, O_SY = 2 * P::CT, O_SZ = 3 * P::CT, O_UX = 4 * P::CT;
+  static constexpr int O_INFO = 5 * P::CT;
+  static constexpr int PER = (O_INFO + kInfoDoubles) | 1;
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
 
@@ -95,243 +201,158 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, cons
                                                                  const double* __restrict__ x,
                                                                  double* __restrict__ y) {
   using G = SipAxisCfg<KP>;
-  constexpr int N = G::N, Q = G::Q, NB = G::NB, NF = G::NF, C = G::C, PER = G::PER;
-  const FTab<N, Q>& tb = c_ft<N, Q>;
+  using P = typename G::P;
+  constexpr int N = G::N, NB = G::NB, NF = G::NF, C = G::C, PER = G::PER, TT = G::T;
+  const FTab<N, N>& ta = c_ft<N, N>;
   extern __shared__ double sm[];
   const int c0 = blockIdx.x * C;
   const int nc = min(C, m.ncells - c0);
-  const double sfac = (double)((KP + 1) * (KP + 1));
   const int tid = threadIdx.x;
+  const double sfac = (double)((KP + 1) * (KP + 1));
+#define CELL(c) (sm + (c) * PER)
+#define INFO(c) (*reinterpret_cast<CellInfo*>(sm + (c) * PER + G::O_INFO))
 
-  // S0: load cell values + geometry
-  for (int idx = tid; idx < nc * NB; idx += G::T) {
+  // S0: cell values (padded) + per-cell info
+  for (int idx = tid; idx < nc * NB; idx += TT) {
     const int c = idx / NB, i = idx - c * NB;
-    sm[c * PER + G::O_U + i] = x[(size_t)(c0 + c) * NB + i];
+    CELL(c)[G::O_U + P::idx(i % N, (i / N) % N, i / NF)] = x[(size_t)(c0 + c) * NB + i];
   }
-  for (int c = tid; c < nc; c += G::T) {
-    const double* r = aff + (size_t)(c0 + c) * kAffStride3;
-    double* g = sm + c * PER + G::O_GEO;
-    g[0] = 1.0 / r[0];
-    g[1] = 1.0 / r[4];
-    g[2] = 1.0 / r[8];
-    g[3] = r[9];
+  for (int c = tid; c < nc; c += TT) {
+    load_info(INFO(c), m, aff, c0 + c, sfac);
+    // the scalar operator ignores outlet ids: all boundary faces are natural, or
+    // all Dirichlet when dir_bdry (forms.cpp:218-242)
+    for (int f = 0; f < 6; ++f)
+      if (INFO(c).type[f] == 2) INFO(c).type[f] = 1;
   }
   __syncthreads();
-  // S1: x-lines  UX = M u (O_A), KX = K u (O_B)
-  for (int idx = tid; idx < nc * NF; idx += G::T) {
-    const int c = idx / NF, jk = idx - c * NF;
-    const double* u = sm + c * PER + G::O_U + jk * N;
-    double v[N];
+  // A: all-direction lines: S_d on raw lines (+ neighbour lines), and Ux = M_x u
+  for (int idx = tid; idx < nc * 3 * NF; idx += TT) {
+    const int c = idx / (3 * NF), r = idx - c * 3 * NF;
+    const int d = r / NF, tl = r - d * NF;
+    const int p = tl % N, q = tl / N;
+    const CellInfo& ci = INFO(c);
+    const int st = d == 0 ? 1 : (d == 1 ? P::PX : P::PY);
+    const int b0 = d == 0 ? P::idx(0, p, q) : (d == 1 ? P::idx(p, 0, q) : P::idx(p, q, 0));
+    const int gst = d == 0 ? 1 : (d == 1 ? N : NF);
+    const int g0 = d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q);
+    double u[N], uL[N], uR[N], o[N];
 #pragma unroll
-    for (int l = 0; l < N; ++l) v[l] = u[l];
-    double* ux = sm + c * PER + G::O_A + jk * N;
-    double* kx = sm + c * PER + G::O_B + jk * N;
+    for (int l = 0; l < N; ++l) u[l] = CELL(c)[G::O_U + b0 + l * st];
+    const int nl = ci.nb[2 * d], nr = ci.nb[2 * d + 1];
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      uL[l] = nl >= 0 ? __ldg(x + (size_t)nl * NB + g0 + l * gst) : 0.0;
+      uR[l] = nr >= 0 ? __ldg(x + (size_t)nr * NB + g0 + l * gst) : 0.0;
+    }
+    sip_line<N>(ta, ci, d, u, uL, uR, dir_bdry != 0, 1.0, o);
+    double* so = CELL(c) + (d == 0 ? G::O_SX : (d == 1 ? G::O_SY : G::O_SZ)) + b0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) so[l * st] = o[l];
+    if (d == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) s = fma(ta.M[i][l], u[l], s);
+        CELL(c)[G::O_UX + b0 + i] = s;
+      }
+    }
+  }
+  __syncthreads();
+  // B: x-lines, in place: SY <- M_x SY, SZ <- M_x SZ
+  for (int idx = tid; idx < nc * NF; idx += TT) {
+    const int c = idx / NF, tl = idx - c * NF;
+    const int b0 = P::idx(0, tl % N, tl / N);
+    double a[N], b[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      a[l] = CELL(c)[G::O_SY + b0 + l];
+      b[l] = CELL(c)[G::O_SZ + b0 + l];
+    }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double s = 0.0, t = 0.0;
 #pragma unroll
       for (int l = 0; l < N; ++l) {
-        s = fma(tb.M[i][l], v[l], s);
-        t = fma(tb.K[i][l], v[l], t);
+        s = fma(ta.M[i][l], a[l], s);
+        t = fma(ta.M[i][l], b[l], t);
       }
-      ux[i] = s;
-      kx[i] = t;
+      CELL(c)[G::O_SY + b0 + i] = s;
+      CELL(c)[G::O_SZ + b0 + i] = t;
     }
   }
   __syncthreads();
-  // S2: y-lines  UY = M UX (O_D); T = mc' UY + cx M KX + cy K UX (O_C)
-  for (int idx = tid; idx < nc * NF; idx += G::T) {
-    const int c = idx / NF, r = idx - c * NF;
-    const int i = r % N, k = r / N;
-    const double* g = sm + c * PER + G::O_GEO;
-    const double detJ = g[3];
-    const double cm = mc * detJ, cx = detJ / (g[0] * g[0]), cy = detJ / (g[1] * g[1]);
-    const int base = i + N * N * k;
-    double a[N], b[N];
+  // C: y-lines: SX <- M_y (SX + mc detJ UX) + SY ; SZ <- M_y SZ
+  for (int idx = tid; idx < nc * NF; idx += TT) {
+    const int c = idx / NF, tl = idx - c * NF;
+    const int b0 = P::idx(tl % N, 0, tl / N);
+    const double cm = mc * INFO(c).detJ;
+    double a[N], b[N], e[N];
 #pragma unroll
     for (int l = 0; l < N; ++l) {
-      a[l] = sm[c * PER + G::O_A + base + N * l];
-      b[l] = sm[c * PER + G::O_B + base + N * l];
+      a[l] = fma(cm, CELL(c)[G::O_UX + b0 + l * P::PX], CELL(c)[G::O_SX + b0 + l * P::PX]);
+      b[l] = CELL(c)[G::O_SZ + b0 + l * P::PX];
+      e[l] = CELL(c)[G::O_SY + b0 + l * P::PX];
     }
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      double uy = 0.0, mk = 0.0, ku = 0.0;
+      double s = e[j], t = 0.0;
 #pragma unroll
       for (int l = 0; l < N; ++l) {
-        uy = fma(tb.M[j][l], a[l], uy);
-        mk = fma(tb.M[j][l], b[l], mk);
-        ku = fma(tb.K[j][l], a[l], ku);
+        s = fma(ta.M[j][l], a[l], s);
+        t = fma(ta.M[j][l], b[l], t);
       }
-      sm[c * PER + G::O_D + base + N * j] = uy;
-      sm[c * PER + G::O_C + base + N * j] = cm * uy + cx * mk + cy * ku;
+      CELL(c)[G::O_SX + b0 + j * P::PX] = s;
+      CELL(c)[G::O_SZ + b0 + j * P::PX] = t;
     }
   }
   __syncthreads();
-  // S3: z-lines  OUT = M T + cz K UY
-  for (int idx = tid; idx < nc * NF; idx += G::T) {
-    const int c = idx / NF, ij = idx - c * NF;
-    const double* g = sm + c * PER + G::O_GEO;
-    const double cz = g[3] / (g[2] * g[2]);
-    double t[N], u[N];
+  // D: z-lines: y = M_z SX + SZ   -> global
+  for (int idx = tid; idx < nc * NF; idx += TT) {
+    const int c = idx / NF, tl = idx - c * NF;
+    const int i = tl % N, j = tl / N;
+    const int b0 = P::idx(i, j, 0);
+    double a[N];
 #pragma unroll
-    for (int l = 0; l < N; ++l) {
-      t[l] = sm[c * PER + G::O_C + ij + NF * l];
-      u[l] = sm[c * PER + G::O_D + ij + NF * l];
-    }
+    for (int l = 0; l < N; ++l) a[l] = CELL(c)[G::O_SX + b0 + l * P::PY];
+    double* yo = y + (size_t)(c0 + c) * NB + i + N * j;
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      double s = 0.0, q = 0.0;
+      double s = CELL(c)[G::O_SZ + b0 + k * P::PY];
 #pragma unroll
-      for (int l = 0; l < N; ++l) {
-        s = fma(tb.M[k][l], t[l], s);
-        q = fma(tb.K[k][l], u[l], q);
-      }
-      sm[c * PER + G::O_OUT + ij + NF * k] = s + cz * q;
+      for (int l = 0; l < N; ++l) s = fma(ta.M[k][l], a[l], s);
+      yo[NF * k] = s;
     }
   }
-  // S4: face-node pointwise (all 6 faces), nodal SIP integrands (forms.cpp:196-213)
-  for (int idx = tid; idx < nc * 6 * NF; idx += G::T) {
-    const int c = idx / (6 * NF), r = idx - c * 6 * NF;
-    const int f = r / NF, t = r - f * NF;
-    const int a = f >> 1, s = f & 1, p = t % N, q = t / N;
-    const int cell = c0 + c;
-    const double* g = sm + c * PER + G::O_GEO;
-    const int st = axis_stride<N>(a);
-    const int b0 = face_node<N>(a, 0, p, q);
-    const double* u = sm + c * PER + G::O_U + b0;
-    double gs = 0.0;
-#pragma unroll
-    for (int l = 0; l < N; ++l) gs = fma(tb.dE[s][l], u[l * st], gs);
-    const double us = u[(s ? N - 1 : 0) * st];
-    const double sgn = s ? 1.0 : -1.0;
-    const double dns = sgn * gs / g[a];
-    const int nb = m.nbr[(size_t)cell * 6 + f];
-    double F = 0.0, GT = 0.0;
-    if (nb >= 0) {
-      const double* un = x + (size_t)nb * NB + b0;
-      double go = 0.0, uo = 0.0;
-#pragma unroll
-      for (int l = 0; l < N; ++l) {
-        const double v = __ldg(un + l * st);
-        go = fma(tb.dE[1 - s][l], v, go);
-        if (l == (s ? 0 : N - 1)) uo = v;
-      }
-      const double ho = 1.0 / __ldg(aff + (size_t)nb * kAffStride3 + 4 * a);
-      const double dno = sgn * go / ho;
-      const double Cp = sfac * m.pen[(size_t)cell * 6 + f];
-      const double ju = us - uo;
-      F = -0.5 * (dns + dno) + Cp * ju;
-      GT = -0.5 * ju;
-    } else if (dir_bdry) {
-      const double sK = sfac * m.pen[(size_t)cell * 6 + f];
-      F = -dns + 2.0 * sK * us;
-      GT = -us;
-    }
-    sm[c * PER + G::O_F + f * NF + t] = F;
-    sm[c * PER + G::O_G + f * NF + t] = GT;
-  }
-  __syncthreads();
-  // S5: tangential mass along p (t1)
-  for (int idx = tid; idx < nc * 6 * N; idx += G::T) {
-    const int c = idx / (6 * N), r = idx - c * 6 * N;
-    const int f = r / N, q = r - f * N;
-    double a1[N], a2[N];
-#pragma unroll
-    for (int p = 0; p < N; ++p) {
-      a1[p] = sm[c * PER + G::O_F + f * NF + p + N * q];
-      a2[p] = sm[c * PER + G::O_G + f * NF + p + N * q];
-    }
-#pragma unroll
-    for (int p = 0; p < N; ++p) {
-      double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-      for (int l = 0; l < N; ++l) {
-        s1 = fma(tb.M[p][l], a1[l], s1);
-        s2 = fma(tb.M[p][l], a2[l], s2);
-      }
-      sm[c * PER + G::O_F1 + f * NF + p + N * q] = s1;
-      sm[c * PER + G::O_G1 + f * NF + p + N * q] = s2;
-    }
-  }
-  __syncthreads();
-  // S6: along q (t2), scale by face area (and sgn / h for the gradient test)
-  for (int idx = tid; idx < nc * 6 * N; idx += G::T) {
-    const int c = idx / (6 * N), r = idx - c * 6 * N;
-    const int f = r / N, p = r - f * N;
-    const int a = f >> 1;
-    const double* g = sm + c * PER + G::O_GEO;
-    const double A = g[3] / g[a];
-    const double gsc = A * ((f & 1) ? 1.0 : -1.0) / g[a];
-    double a1[N], a2[N];
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      a1[q] = sm[c * PER + G::O_F1 + f * NF + p + N * q];
-      a2[q] = sm[c * PER + G::O_G1 + f * NF + p + N * q];
-    }
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-      double s1 = 0.0, s2 = 0.0;
-#pragma unroll
-      for (int l = 0; l < N; ++l) {
-        s1 = fma(tb.M[q][l], a1[l], s1);
-        s2 = fma(tb.M[q][l], a2[l], s2);
-      }
-      sm[c * PER + G::O_F + f * NF + p + N * q] = A * s1;   // reuse F/G slots
-      sm[c * PER + G::O_G + f * NF + p + N * q] = gsc * s2;
-    }
-  }
-  __syncthreads();
-  // S7: gather the 6 faces into every node and store
-  for (int idx = tid; idx < nc * NB; idx += G::T) {
-    const int c = idx / NB, i = idx - c * NB;
-    const int ii[3] = {i % N, (i / N) % N, i / (N * N)};
-    double acc = sm[c * PER + G::O_OUT + i];
-#pragma unroll
-    for (int f = 0; f < 6; ++f) {
-      const int a = f >> 1, s = f & 1;
-      const int p = a == 0 ? ii[1] : ii[0];
-      const int q = a == 2 ? ii[1] : ii[2];
-      const int t = p + N * q;
-      const int la = ii[a];
-      if (la == (s ? N - 1 : 0)) acc += sm[c * PER + G::O_F + f * NF + t];
-      acc = fma(tb.dE[s][la], sm[c * PER + G::O_G + f * NF + t], acc);
-    }
-    y[(size_t)(c0 + c) * NB + i] = acc;
-  }
+#undef CELL
+#undef INFO
 }
-
-}  // namespace dgb
-
-namespace dgb {
 
 // ===========================================================================
 // Momentum operator, axis-aligned affine, 3D, skew = 0:
-//   mass M x + visc A_sip x          (Kronecker / nodal-exact, rule k+1 equivalent)
-// + adv C_lf(w) x                    (k+2 Gauss rule, sum factorisation)
+//   mass M x + visc A_sip x     (line-split, exact)
+// + adv C_lf(w) x               (k+2 Gauss rule; sum factorisation)
 // ===========================================================================
 template <int K>
 struct MomAxisCfg {
   static constexpr int N = K + 1, Q = K + 2, NB = N * N * N, NF = N * N, QN = Q * N, QQ = Q * Q;
-  static constexpr int C = K == 2 ? 12 : 6;    // cells per CTA
-  static constexpr int T = K == 2 ? 256 : 192;  // threads per CTA
+  using P = Pad<N>;
+  static constexpr int CT = P::CT;
+  static constexpr int C = K == 1 ? 16 : (K == 2 ? 10 : 6);      // cells per CTA
+  static constexpr int T = K == 1 ? 128 : (K == 2 ? 192 : 192);  // threads per CTA
   // persistent per-cell regions
-  static constexpr int O_X = 0, O_W = 3 * NB, O_OUT = 6 * NB, O_GEO = 9 * NB, O_WORK = 9 * NB + 4;
-  // phase A (Kronecker cell terms)
-  static constexpr int A_UX = 0, A_KX = 3 * NB, A_T = 6 * NB, A_UY = 9 * NB, A_END = 12 * NB;
+  static constexpr int O_X = 0, O_W = 3 * CT, O_OUT = 6 * CT, O_INFO = 9 * CT;
+  static constexpr int O_WORK = O_INFO + kInfoDoubles;
+  // phase A: SX, SY, SZ, UX (3 comps each)
+  static constexpr int A_SX = 0, A_SY = 3 * CT, A_SZ = 6 * CT, A_UX = 9 * CT, A_END = 12 * CT;
   // phase B (advection cell terms)
-  static constexpr int B_R1 = 0;                 // XB (6 QNN) then TZ/TY/TX (9 QQN)
-  static constexpr int B_R2 = 9 * QQ * N;        // YB (6 QQN) then SA/SB (6 QNN)
+  static constexpr int B_R1 = 0;           // XB (6 QNN) then TZ/TY/TX (9 QQN)
+  static constexpr int B_R2 = 9 * QQ * N;  // YB (6 QQN) then SA/SB (6 QNN)
   static constexpr int B_END = B_R2 + 6 * QQ * N;
-  // face phase (one axis = 2 faces at a time)
-  static constexpr int F_F = 0;                  // [3][2][NF]  F   -> FM
-  static constexpr int F_G = F_F + 6 * NF;       // [3][2][NF]  GT  -> GM
-  static constexpr int F_V = F_G + 6 * NF;       // [8][2][NF]  US(3) UO(3) WS WO (nodal) -> FB [3][2][NF]
-  static constexpr int F_M1 = F_V + 16 * NF;     // [6][2][NF]  mass along p
-  static constexpr int F_V1 = F_M1 + 12 * NF;    // [8][2][QN]  values along p -> FLX [3][2][QQ] -> FL1 [3][2][QN]
-  static constexpr int F_VQ = F_V1 + 16 * QN;    // [8][2][QQ]  values at face Gauss points
-  static constexpr int F_END = F_VQ + 16 * QQ;
+  // face phase (one axis at a time): V1 [8 fields][2 sides][Q x N], FL1 [3][2][Q x N]
+  static constexpr int F_V1 = 0, F_FL = 16 * QN, F_END = F_FL + 6 * QN;
   static constexpr int WORK = A_END > B_END ? (A_END > F_END ? A_END : F_END) : (B_END > F_END ? B_END : F_END);
-  static constexpr int PER = O_WORK + WORK;
+  static constexpr int PER = (O_WORK + WORK) | 1;
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
 
@@ -341,10 +362,11 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
                                                                     const double* __restrict__ w,
                                                                     double* __restrict__ y) {
   using G = MomAxisCfg<K>;
+  using P = typename G::P;
   constexpr int N = G::N, Q = G::Q, NB = G::NB, NF = G::NF, QN = G::QN, QQ = G::QQ, C = G::C, PER = G::PER;
-  constexpr int TT = G::T;
-  const FTab<N, Q>& tq = c_ft<N, Q>;      // k+2 rule: B, D, w (advection)
-  const FTab<N, N>& ta = c_ft<N, N>;      // exact M, K, dE (rule-independent)
+  constexpr int TT = G::T, CT = G::CT;
+  const FTab<N, Q>& tq = c_ft<N, Q>;  // k+2 rule: B, D, w (advection)
+  const FTab<N, N>& ta = c_ft<N, N>;  // exact M, K, dE
   extern __shared__ double sm[];
   const int c0 = blockIdx.x * C;
   const int nc = min(C, m.ncells - c0);
@@ -352,96 +374,120 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
   const double sfac = (double)((K + 1) * (K + 1));
 #define CELL(c) (sm + (c) * PER)
 #define WK(c) (sm + (c) * PER + G::O_WORK)
+#define INFO(c) (*reinterpret_cast<CellInfo*>(sm + (c) * PER + G::O_INFO))
 
-  // ------------------------------------------------------------------ S0: load x, w, geometry
+  // ------------------------------------------------------------------ S0: x, w (padded), info
   for (int idx = tid; idx < nc * 3 * NB; idx += TT) {
-    const int c = idx / (3 * NB), i = idx - c * 3 * NB;
-    CELL(c)[G::O_X + i] = x[(size_t)(c0 + c) * 3 * NB + i];
-    CELL(c)[G::O_W + i] = w[(size_t)(c0 + c) * 3 * NB + i];
+    const int c = idx / (3 * NB), r = idx - c * 3 * NB;
+    const int comp = r / NB, i = r - comp * NB;
+    const int pi = comp * CT + P::idx(i % N, (i / N) % N, i / NF);
+    CELL(c)[G::O_X + pi] = x[(size_t)(c0 + c) * 3 * NB + r];
+    CELL(c)[G::O_W + pi] = w[(size_t)(c0 + c) * 3 * NB + r];
   }
-  for (int c = tid; c < nc; c += TT) {
-    const double* r = aff + (size_t)(c0 + c) * kAffStride3;
-    double* g = CELL(c) + G::O_GEO;
-    g[0] = 1.0 / r[0];
-    g[1] = 1.0 / r[4];
-    g[2] = 1.0 / r[8];
-    g[3] = r[9];
-  }
+  for (int c = tid; c < nc; c += TT) load_info(INFO(c), m, aff, c0 + c, sfac);
   __syncthreads();
 
-  // ------------------------------------------------------------------ pass A cell (Kronecker)
-  // S1: x-lines UX = M u, KX = K u
-  for (int idx = tid; idx < nc * 3 * NF; idx += TT) {
-    const int c = idx / (3 * NF), r = idx - c * 3 * NF;  // r = comp*NF + jk
-    const double* u = CELL(c) + G::O_X + r * N;
-    double v[N];
+  // ------------------------------------------------------------------ pass A: mass + viscous (line split)
+  // A: lines of every direction: S_d (visc) on raw lines, UX = M_x u
+  for (int idx = tid; idx < nc * 9 * NF; idx += TT) {
+    const int c = idx / (9 * NF), r = idx - c * 9 * NF;
+    const int comp = r / (3 * NF), r2 = r - comp * 3 * NF;
+    const int d = r2 / NF, tl = r2 - d * NF;
+    const int p = tl % N, q = tl / N;
+    const CellInfo& ci = INFO(c);
+    const int st = d == 0 ? 1 : (d == 1 ? P::PX : P::PY);
+    const int b0 = d == 0 ? P::idx(0, p, q) : (d == 1 ? P::idx(p, 0, q) : P::idx(p, q, 0));
+    const int gst = d == 0 ? 1 : (d == 1 ? N : NF);
+    const int g0 = comp * NB + (d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q));
+    double u[N], uL[N], uR[N], o[N];
+    const double* us = CELL(c) + G::O_X + comp * CT + b0;
 #pragma unroll
-    for (int l = 0; l < N; ++l) v[l] = u[l];
-    double* ux = WK(c) + G::A_UX + r * N;
-    double* kx = WK(c) + G::A_KX + r * N;
+    for (int l = 0; l < N; ++l) u[l] = us[l * st];
+    const int nl = ci.nb[2 * d], nr = ci.nb[2 * d + 1];
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      uL[l] = nl >= 0 ? __ldg(x + (size_t)nl * 3 * NB + g0 + l * gst) : 0.0;
+      uR[l] = nr >= 0 ? __ldg(x + (size_t)nr * 3 * NB + g0 + l * gst) : 0.0;
+    }
+    sip_line<N>(ta, ci, d, u, uL, uR, true, co.visc, o);
+    double* so = WK(c) + (d == 0 ? G::A_SX : (d == 1 ? G::A_SY : G::A_SZ)) + comp * CT + b0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) so[l * st] = o[l];
+    if (d == 0) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) s = fma(ta.M[i][l], u[l], s);
+        WK(c)[G::A_UX + comp * CT + b0 + i] = s;
+      }
+    }
+  }
+  __syncthreads();
+  // B: x-lines in place: SY <- M_x SY, SZ <- M_x SZ
+  for (int idx = tid; idx < nc * 3 * NF; idx += TT) {
+    const int c = idx / (3 * NF), r = idx - c * 3 * NF;
+    const int comp = r / NF, tl = r - comp * NF;
+    const int b0 = comp * CT + P::idx(0, tl % N, tl / N);
+    double a[N], b[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      a[l] = WK(c)[G::A_SY + b0 + l];
+      b[l] = WK(c)[G::A_SZ + b0 + l];
+    }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double s = 0.0, t = 0.0;
 #pragma unroll
       for (int l = 0; l < N; ++l) {
-        s = fma(ta.M[i][l], v[l], s);
-        t = fma(ta.K[i][l], v[l], t);
+        s = fma(ta.M[i][l], a[l], s);
+        t = fma(ta.M[i][l], b[l], t);
       }
-      ux[i] = s;
-      kx[i] = t;
+      WK(c)[G::A_SY + b0 + i] = s;
+      WK(c)[G::A_SZ + b0 + i] = t;
     }
   }
   __syncthreads();
-  // S2: y-lines UY = M UX ; T = mass' UY + vx M KX + vy K UX
+  // C: y-lines: SX <- M_y (SX + mass detJ UX) + SY ; SZ <- M_y SZ
   for (int idx = tid; idx < nc * 3 * NF; idx += TT) {
     const int c = idx / (3 * NF), r = idx - c * 3 * NF;
-    const int comp = r / NF, ik = r - comp * NF;
-    const int i = ik % N, k = ik / N;
-    const double* g = CELL(c) + G::O_GEO;
-    const double cm = co.mass * g[3], vx = co.visc * g[3] / (g[0] * g[0]), vy = co.visc * g[3] / (g[1] * g[1]);
-    const int base = comp * NB + i + NF * k;
-    double a[N], b[N];
+    const int comp = r / NF, tl = r - comp * NF;
+    const int b0 = comp * CT + P::idx(tl % N, 0, tl / N);
+    const double cm = co.mass * INFO(c).detJ;
+    double a[N], b[N], e[N];
 #pragma unroll
     for (int l = 0; l < N; ++l) {
-      a[l] = WK(c)[G::A_UX + base + N * l];
-      b[l] = WK(c)[G::A_KX + base + N * l];
+      a[l] = fma(cm, WK(c)[G::A_UX + b0 + l * P::PX], WK(c)[G::A_SX + b0 + l * P::PX]);
+      b[l] = WK(c)[G::A_SZ + b0 + l * P::PX];
+      e[l] = WK(c)[G::A_SY + b0 + l * P::PX];
     }
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      double uy = 0.0, mk = 0.0, ku = 0.0;
+      double s = e[j], t = 0.0;
 #pragma unroll
       for (int l = 0; l < N; ++l) {
-        uy = fma(ta.M[j][l], a[l], uy);
-        mk = fma(ta.M[j][l], b[l], mk);
-        ku = fma(ta.K[j][l], a[l], ku);
+        s = fma(ta.M[j][l], a[l], s);
+        t = fma(ta.M[j][l], b[l], t);
       }
-      WK(c)[G::A_UY + base + N * j] = uy;
-      WK(c)[G::A_T + base + N * j] = cm * uy + vx * mk + vy * ku;
+      WK(c)[G::A_SX + b0 + j * P::PX] = s;
+      WK(c)[G::A_SZ + b0 + j * P::PX] = t;
     }
   }
   __syncthreads();
-  // S3: z-lines OUT = M T + vz K UY
+  // D: z-lines: OUT = M_z SX + SZ
   for (int idx = tid; idx < nc * 3 * NF; idx += TT) {
     const int c = idx / (3 * NF), r = idx - c * 3 * NF;
-    const int comp = r / NF, ij = r - comp * NF;
-    const double* g = CELL(c) + G::O_GEO;
-    const double vz = co.visc * g[3] / (g[2] * g[2]);
-    const int base = comp * NB + ij;
-    double t[N], u[N];
+    const int comp = r / NF, tl = r - comp * NF;
+    const int b0 = comp * CT + P::idx(tl % N, tl / N, 0);
+    double a[N];
 #pragma unroll
-    for (int l = 0; l < N; ++l) {
-      t[l] = WK(c)[G::A_T + base + NF * l];
-      u[l] = WK(c)[G::A_UY + base + NF * l];
-    }
+    for (int l = 0; l < N; ++l) a[l] = WK(c)[G::A_SX + b0 + l * P::PY];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      double s = 0.0, q = 0.0;
+      double s = WK(c)[G::A_SZ + b0 + k * P::PY];
 #pragma unroll
-      for (int l = 0; l < N; ++l) {
-        s = fma(ta.M[k][l], t[l], s);
-        q = fma(ta.K[k][l], u[l], q);
-      }
-      CELL(c)[G::O_OUT + base + NF * k] = s + vz * q;
+      for (int l = 0; l < N; ++l) s = fma(ta.M[k][l], a[l], s);
+      CELL(c)[G::O_OUT + b0 + k * P::PY] = s;
     }
   }
   __syncthreads();
@@ -450,7 +496,8 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
   // S4: x-lines for 6 fields (u0..2, w0..2): XB[f][(j,k)][qx]
   for (int idx = tid; idx < nc * 6 * NF; idx += TT) {
     const int c = idx / (6 * NF), r = idx - c * 6 * NF;  // r = f*NF + jk
-    const double* in = CELL(c) + (r < 3 * NF ? G::O_X + r * N : G::O_W + (r - 3 * NF) * N);
+    const int f = r / NF, jk = r - f * NF;
+    const double* in = CELL(c) + (f < 3 ? G::O_X + f * CT : G::O_W + (f - 3) * CT) + P::idx(0, jk % N, jk / N);
     double v[N];
 #pragma unroll
     for (int l = 0; l < N; ++l) v[l] = in[l];
@@ -469,11 +516,11 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
     const int c = idx / (6 * QN), r = idx - c * 6 * QN;
     const int f = r / QN, rk = r - f * QN;
     const int qx = rk % Q, k = rk / Q;
-    const double* in = WK(c) + G::B_R1 + f * Q * NF + qx + Q * N * k;  // + Q*l
+    const double* in = WK(c) + G::B_R1 + f * Q * NF + qx + Q * N * k;
     double v[N];
 #pragma unroll
     for (int l = 0; l < N; ++l) v[l] = in[Q * l];
-    double* o = WK(c) + G::B_R2 + f * QQ * N + qx + QQ * k;  // + Q*qy
+    double* o = WK(c) + G::B_R2 + f * QQ * N + qx + QQ * k;
 #pragma unroll
     for (int qy = 0; qy < Q; ++qy) {
       double s = 0.0;
@@ -483,11 +530,11 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
     }
   }
   __syncthreads();
-  // S6: fused z: evaluate the 6 columns, pointwise flux, z-integration of the 3x3 gradient tests
+  // S6: fused z: evaluate 6 columns, pointwise advective flux, z-integration of the 3x3 gradient tests
   for (int idx = tid; idx < nc * QQ; idx += TT) {
     const int c = idx / QQ, qxy = idx - c * QQ;
-    const double* g = CELL(c) + G::O_GEO;
-    const double wxy = g[3] * tq.w[qxy % Q] * tq.w[qxy / Q];
+    const CellInfo& ci = INFO(c);
+    const double wxy = ci.detJ * tq.w[qxy % Q] * tq.w[qxy / Q];
     double col[6][Q];
 #pragma unroll
     for (int f = 0; f < 6; ++f) {
@@ -502,7 +549,7 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
         col[f][qz] = s;
       }
     }
-    const double ih[3] = {-co.adv / g[0], -co.adv / g[1], -co.adv / g[2]};
+    const double ih0 = -co.adv * ci.ih[0], ih1 = -co.adv * ci.ih[1], ih2 = -co.adv * ci.ih[2];
 #pragma unroll
     for (int comp = 0; comp < 3; ++comp) {
       double tz[N], ty[N], tx[N];
@@ -511,9 +558,9 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
 #pragma unroll
       for (int qz = 0; qz < Q; ++qz) {
         const double uj = col[comp][qz] * wxy * tq.w[qz];
-        const double rx = uj * col[3][qz] * ih[0];
-        const double ry = uj * col[4][qz] * ih[1];
-        const double rz = uj * col[5][qz] * ih[2];
+        const double rx = uj * col[3][qz] * ih0;
+        const double ry = uj * col[4][qz] * ih1;
+        const double rz = uj * col[5][qz] * ih2;
 #pragma unroll
         for (int l = 0; l < N; ++l) {
           tz[l] = fma(tq.D[qz][l], rz, tz[l]);
@@ -570,7 +617,7 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
       va[qx] = sa[qx];
       vb[qx] = sa[QN * N + qx];
     }
-    double* o = CELL(c) + G::O_OUT + comp * NB + N * jl;
+    double* o = CELL(c) + G::O_OUT + comp * CT + P::idx(0, jl % N, jl / N);
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double s = o[i];
@@ -584,226 +631,133 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
   }
   __syncthreads();
 
-  // ------------------------------------------------------------------ faces, one axis (2 faces) at a time
-  for (int a = 0; a < 3; ++a) {
-    const int st = axis_stride<N>(a);
-    // S9: face-node pointwise: SIP integrands (nodal) + traces for the LF flux
-    for (int idx = tid; idx < nc * 2 * NF; idx += TT) {
-      const int c = idx / (2 * NF), r = idx - c * 2 * NF;
-      const int s = r / NF, t = r - s * NF;  // local face s (side), node t
-      const int f = 2 * a + s;
-      const int p = t % N, q = t / N;
-      const int cell = c0 + c;
-      const double* g = CELL(c) + G::O_GEO;
-      const int b0 = face_node<N>(a, 0, p, q);
-      const int Ls = s ? N - 1 : 0, Lo = s ? 0 : N - 1;
-      const double sgn = s ? 1.0 : -1.0;
-      const int nb = m.nbr[(size_t)cell * 6 + f];
-      double* wk = WK(c);
-      const bool interior = nb >= 0;
-      const bool outlet = !interior && fa_outlet(m, nb);
-      const double ho = interior ? 1.0 / __ldg(aff + (size_t)nb * kAffStride3 + 4 * a) : 1.0;
-      const double pen = sfac * m.pen[(size_t)cell * 6 + f];
+  // ------------------------------------------------------------------ LF advective faces, one axis at a time
+  if (co.adv != 0.0) {
+    for (int a = 0; a < 3; ++a) {
+      const int st = a == 0 ? 1 : (a == 1 ? P::PX : P::PY);
+      const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
+      // F1: traces of u (3 comps, own + neighbour) and w_a (own + neighbour) on the face-node
+      //     line q, contracted along p with B:  V1[field][s][qp + Q q]
+      for (int idx = tid; idx < nc * 2 * N; idx += TT) {
+        const int c = idx / (2 * N), r = idx - c * 2 * N;
+        const int s = r / N, q = r - s * N;
+        const CellInfo& ci = INFO(c);
+        const int nb = ci.nb[2 * a + s];
+        const int Ls = s ? N - 1 : 0, Lo = s ? 0 : N - 1;
+        double v[8][N];
 #pragma unroll
-      for (int comp = 0; comp < 3; ++comp) {
-        const double* u = CELL(c) + G::O_X + comp * NB + b0;
-        double gs = 0.0;
+        for (int p = 0; p < N; ++p) {
+          const int li = a == 0 ? P::idx(Ls, p, q) : (a == 1 ? P::idx(p, Ls, q) : P::idx(p, q, Ls));
+          const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + Lo * gst;
 #pragma unroll
-        for (int l = 0; l < N; ++l) gs = fma(ta.dE[s][l], u[l * st], gs);
-        const double us = u[Ls * st];
-        const double dns = sgn * gs / g[a];
-        double F = 0.0, GT = 0.0, uo = 0.0;
-        if (interior) {
-          const double* un = x + (size_t)nb * 3 * NB + comp * NB + b0;
-          double go = 0.0;
-#pragma unroll
-          for (int l = 0; l < N; ++l) {
-            const double v = __ldg(un + l * st);
-            go = fma(ta.dE[1 - s][l], v, go);
-            if (l == Lo) uo = v;
+          for (int comp = 0; comp < 3; ++comp) {
+            v[comp][p] = CELL(c)[G::O_X + comp * CT + li];
+            v[3 + comp][p] = nb >= 0 ? __ldg(x + (size_t)nb * 3 * NB + comp * NB + go) : 0.0;
           }
-          const double dno = sgn * go / ho;
-          const double ju = us - uo;
-          F = co.visc * (-0.5 * (dns + dno) + pen * ju);
-          GT = -co.visc * 0.5 * ju;
-        } else if (!outlet) {
-          F = co.visc * (-dns + 2.0 * pen * us);
-          GT = -co.visc * us;
+          v[6][p] = CELL(c)[G::O_W + a * CT + li];
+          v[7][p] = nb >= 0 ? __ldg(w + (size_t)nb * 3 * NB + a * NB + go) : 0.0;
         }
-        wk[G::F_F + (comp * 2 + s) * NF + t] = F;
-        wk[G::F_G + (comp * 2 + s) * NF + t] = GT;
-        wk[G::F_V + (comp * 2 + s) * NF + t] = us;
-        wk[G::F_V + ((3 + comp) * 2 + s) * NF + t] = uo;
+        double* o = WK(c) + G::F_V1 + s * QN + Q * q;
+#pragma unroll
+        for (int fl = 0; fl < 8; ++fl)
+#pragma unroll
+          for (int qp = 0; qp < Q; ++qp) {
+            double acc = 0.0;
+#pragma unroll
+            for (int l = 0; l < N; ++l) acc = fma(tq.B[qp][l], v[fl][l], acc);
+            o[fl * 2 * QN + qp] = acc;
+          }
       }
-      wk[G::F_V + (6 * 2 + s) * NF + t] = CELL(c)[G::O_W + a * NB + b0 + Ls * st];
-      wk[G::F_V + (7 * 2 + s) * NF + t] = interior ? __ldg(w + (size_t)nb * 3 * NB + a * NB + b0 + Lo * st) : 0.0;
-    }
-    __syncthreads();
-    // S10: along p: mass for the 6 SIP fields, B for the 8 value fields
-    for (int idx = tid; idx < nc * 2 * N * 14; idx += TT) {
-      const int c = idx / (2 * N * 14), r = idx - c * 2 * N * 14;
-      const int fld = r / (2 * N), r2 = r - fld * 2 * N;
-      const int s = r2 / N, q = r2 - s * N;
-      double* wk = WK(c);
-      double v[N];
-      if (fld < 6) {  // F0..2, GT0..2
-        const double* in = wk + (fld < 3 ? G::F_F + (fld * 2 + s) * NF : G::F_G + ((fld - 3) * 2 + s) * NF) + N * q;
+      __syncthreads();
+      // F2: along q: values at the face Gauss points, LF flux, B^T back along q -> FL [comp][s][qp + Q l]
+      for (int idx = tid; idx < nc * 2 * Q; idx += TT) {
+        const int c = idx / (2 * Q), r = idx - c * 2 * Q;
+        const int s = r / Q, qp = r - s * Q;
+        const CellInfo& ci = INFO(c);
+        const int f = 2 * a + s;
+        const double* in = WK(c) + G::F_V1 + s * QN + qp;
+        double v[8][N];
 #pragma unroll
-        for (int l = 0; l < N; ++l) v[l] = in[l];
-        double* o = wk + G::F_M1 + (fld * 2 + s) * NF + N * q;
+        for (int fl = 0; fl < 8; ++fl)
 #pragma unroll
-        for (int pp = 0; pp < N; ++pp) {
-          double acc = 0.0;
+          for (int l = 0; l < N; ++l) v[fl][l] = in[fl * 2 * QN + Q * l];
+        const double sgn = s ? 1.0 : -1.0;
+        const double wbase = co.adv * ci.A[a] * tq.w[qp];
+        const int ty = ci.type[f];
+        double out[3][N];
 #pragma unroll
-          for (int l = 0; l < N; ++l) acc = fma(ta.M[pp][l], v[l], acc);
-          o[pp] = acc;
-        }
-      } else {
-        const int vf = fld - 6;
-        const double* in = wk + G::F_V + (vf * 2 + s) * NF + N * q;
+        for (int comp = 0; comp < 3; ++comp)
 #pragma unroll
-        for (int l = 0; l < N; ++l) v[l] = in[l];
-        double* o = wk + G::F_V1 + (vf * 2 + s) * QN + Q * q;
-#pragma unroll
-        for (int qp = 0; qp < Q; ++qp) {
-          double acc = 0.0;
-#pragma unroll
-          for (int l = 0; l < N; ++l) acc = fma(tq.B[qp][l], v[l], acc);
-          o[qp] = acc;
-        }
-      }
-    }
-    __syncthreads();
-    // S11: along q: mass (scaled by the face area, and sgn/h for the gradient test) / B for values
-    for (int idx = tid; idx < nc * 2 * (6 * N + 8 * Q); idx += TT) {
-      const int c = idx / (2 * (6 * N + 8 * Q)), r = idx - c * 2 * (6 * N + 8 * Q);
-      double* wk = WK(c);
-      const double* g = CELL(c) + G::O_GEO;
-      if (r < 2 * 6 * N) {
-        const int fld = r / (2 * N), r2 = r - fld * 2 * N;
-        const int s = r2 / N, pp = r2 - s * N;
-        const double A = g[3] / g[a];
-        const double scale = fld < 3 ? A : A * (s ? 1.0 : -1.0) / g[a];
-        double v[N];
-#pragma unroll
-        for (int l = 0; l < N; ++l) v[l] = wk[G::F_M1 + (fld * 2 + s) * NF + pp + N * l];
-        double* o = wk + (fld < 3 ? G::F_F + (fld * 2 + s) * NF : G::F_G + ((fld - 3) * 2 + s) * NF) + pp;
-#pragma unroll
-        for (int qq = 0; qq < N; ++qq) {
-          double acc = 0.0;
-#pragma unroll
-          for (int l = 0; l < N; ++l) acc = fma(ta.M[qq][l], v[l], acc);
-          o[N * qq] = scale * acc;
-        }
-      } else {
-        const int r3 = r - 2 * 6 * N;
-        const int vf = r3 / (2 * Q), r4 = r3 - vf * 2 * Q;
-        const int s = r4 / Q, qp = r4 - s * Q;
-        double v[N];
-#pragma unroll
-        for (int l = 0; l < N; ++l) v[l] = wk[G::F_V1 + (vf * 2 + s) * QN + qp + Q * l];
-        double* o = wk + G::F_VQ + (vf * 2 + s) * QQ + qp;
+          for (int l = 0; l < N; ++l) out[comp][l] = 0.0;
 #pragma unroll
         for (int qq = 0; qq < Q; ++qq) {
-          double acc = 0.0;
+          double val[8];
 #pragma unroll
-          for (int l = 0; l < N; ++l) acc = fma(tq.B[qq][l], v[l], acc);
-          o[Q * qq] = acc;
+          for (int fl = 0; fl < 8; ++fl) {
+            double acc = 0.0;
+#pragma unroll
+            for (int l = 0; l < N; ++l) acc = fma(tq.B[qq][l], v[fl][l], acc);
+            val[fl] = acc;
+          }
+          const double wq = wbase * tq.w[qq];
+          const double wns = sgn * val[6];
+          double fl3[3];
+          if (ty == 0) {  // forms.cpp:555-573
+            const double wno = sgn * val[7];
+            const double lam = fmax(fabs(wns), fabs(wno));
+#pragma unroll
+            for (int comp = 0; comp < 3; ++comp)
+              fl3[comp] = wq * (0.5 * (val[comp] * wns + val[3 + comp] * wno) + 0.5 * lam * (val[comp] - val[3 + comp]));
+          } else {  // forms.cpp:592-599
+            const double cf = ty == 2 ? wns : fabs(wns);
+#pragma unroll
+            for (int comp = 0; comp < 3; ++comp) fl3[comp] = wq * cf * val[comp];
+          }
+#pragma unroll
+          for (int comp = 0; comp < 3; ++comp)
+#pragma unroll
+            for (int l = 0; l < N; ++l) out[comp][l] = fma(tq.B[qq][l], fl3[comp], out[comp][l]);
         }
+        double* o = WK(c) + G::F_FL + s * QN + qp;
+#pragma unroll
+        for (int comp = 0; comp < 3; ++comp)
+#pragma unroll
+          for (int l = 0; l < N; ++l) o[comp * 2 * QN + Q * l] = out[comp][l];
       }
-    }
-    __syncthreads();
-    // S12: LF flux at the face Gauss points (forms.cpp:555-573, boundary :592-599)
-    for (int idx = tid; idx < nc * 2 * QQ; idx += TT) {
-      const int c = idx / (2 * QQ), r = idx - c * 2 * QQ;
-      const int s = r / QQ, gp = r - s * QQ;
-      const int f = 2 * a + s;
-      const int nb = m.nbr[(size_t)(c0 + c) * 6 + f];
-      double* wk = WK(c);
-      const double* g = CELL(c) + G::O_GEO;
-      const double sgn = s ? 1.0 : -1.0;
-      const double wq = co.adv * (g[3] / g[a]) * tq.w[gp % Q] * tq.w[gp / Q];
-      const double wns = sgn * wk[G::F_VQ + (6 * 2 + s) * QQ + gp];
-      double fl[3];
-      if (nb >= 0) {
-        const double wno = sgn * wk[G::F_VQ + (7 * 2 + s) * QQ + gp];
-        const double lam = fmax(fabs(wns), fabs(wno));
+      __syncthreads();
+      // F3: B^T along p, add into the face layer of OUT
+      for (int idx = tid; idx < nc * 2 * N; idx += TT) {
+        const int c = idx / (2 * N), r = idx - c * 2 * N;
+        const int s = r / N, q = r - s * N;
+        const int Ls = s ? N - 1 : 0;
+        const double* in = WK(c) + G::F_FL + s * QN + Q * q;
 #pragma unroll
         for (int comp = 0; comp < 3; ++comp) {
-          const double us = wk[G::F_VQ + (comp * 2 + s) * QQ + gp];
-          const double uo = wk[G::F_VQ + ((3 + comp) * 2 + s) * QQ + gp];
-          fl[comp] = wq * (0.5 * (us * wns + uo * wno) + 0.5 * lam * (us - uo));
+          double v[Q];
+#pragma unroll
+          for (int qp = 0; qp < Q; ++qp) v[qp] = in[comp * 2 * QN + qp];
+#pragma unroll
+          for (int p = 0; p < N; ++p) {
+            double acc = 0.0;
+#pragma unroll
+            for (int qp = 0; qp < Q; ++qp) acc = fma(tq.B[qp][p], v[qp], acc);
+            const int li = a == 0 ? P::idx(Ls, p, q) : (a == 1 ? P::idx(p, Ls, q) : P::idx(p, q, Ls));
+            CELL(c)[G::O_OUT + comp * CT + li] += acc;
+          }
         }
-      } else {
-        const double cf = fa_outlet(m, nb) ? wns : fabs(wns);
-#pragma unroll
-        for (int comp = 0; comp < 3; ++comp) fl[comp] = wq * cf * wk[G::F_VQ + (comp * 2 + s) * QQ + gp];
       }
-#pragma unroll
-      for (int comp = 0; comp < 3; ++comp) wk[G::F_V1 + (comp * 2 + s) * QQ + gp] = fl[comp];  // FLX
+      __syncthreads();
     }
-    __syncthreads();
-    // S13: integrate along q (Q -> N): FL1 [3][2][Q x N] (into F_VQ region)
-    for (int idx = tid; idx < nc * 6 * Q; idx += TT) {
-      const int c = idx / (6 * Q), r = idx - c * 6 * Q;
-      const int cs = r / Q, qp = r - cs * Q;  // cs = comp*2+s
-      double* wk = WK(c);
-      double v[Q];
-#pragma unroll
-      for (int qq = 0; qq < Q; ++qq) v[qq] = wk[G::F_V1 + cs * QQ + qp + Q * qq];
-      double* o = wk + G::F_VQ + cs * QN + qp;
-#pragma unroll
-      for (int l = 0; l < N; ++l) {
-        double acc = 0.0;
-#pragma unroll
-        for (int qq = 0; qq < Q; ++qq) acc = fma(tq.B[qq][l], v[qq], acc);
-        o[Q * l] = acc;
-      }
-    }
-    __syncthreads();
-    // S14: along p (Q -> N), add into FM (the value-test nodal integrand)
-    for (int idx = tid; idx < nc * 6 * N; idx += TT) {
-      const int c = idx / (6 * N), r = idx - c * 6 * N;
-      const int cs = r / N, q = r - cs * N;
-      double* wk = WK(c);
-      double v[Q];
-#pragma unroll
-      for (int qp = 0; qp < Q; ++qp) v[qp] = wk[G::F_VQ + cs * QN + qp + Q * q];
-      double* o = wk + G::F_F + cs * NF + N * q;
-#pragma unroll
-      for (int pp = 0; pp < N; ++pp) {
-        double acc = o[pp];
-#pragma unroll
-        for (int qp = 0; qp < Q; ++qp) acc = fma(tq.B[qp][pp], v[qp], acc);
-        o[pp] = acc;
-      }
-    }
-    __syncthreads();
-    // S15: gather both faces of this axis into every node
-    for (int idx = tid; idx < nc * 3 * NB; idx += TT) {
-      const int c = idx / (3 * NB), r = idx - c * 3 * NB;
-      const int comp = r / NB, i = r - comp * NB;
-      const int ii[3] = {i % N, (i / N) % N, i / NF};
-      const int p = a == 0 ? ii[1] : ii[0];
-      const int q = a == 2 ? ii[1] : ii[2];
-      const int t = p + N * q;
-      const int la = ii[a];
-      const double* wk = WK(c);
-      double acc = CELL(c)[G::O_OUT + r];
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        if (la == (s ? N - 1 : 0)) acc += wk[G::F_F + (comp * 2 + s) * NF + t];
-        acc = fma(ta.dE[s][la], wk[G::F_G + (comp * 2 + s) * NF + t], acc);
-      }
-      if (a < 2)
-        CELL(c)[G::O_OUT + r] = acc;
-      else
-        y[(size_t)(c0 + c) * 3 * NB + r] = acc;
-    }
-    __syncthreads();
+  }
+  // ------------------------------------------------------------------ store
+  for (int idx = tid; idx < nc * 3 * NB; idx += TT) {
+    const int c = idx / (3 * NB), r = idx - c * 3 * NB;
+    const int comp = r / NB, i = r - comp * NB;
+    y[(size_t)(c0 + c) * 3 * NB + r] = CELL(c)[G::O_OUT + comp * CT + P::idx(i % N, (i / N) % N, i / NF)];
   }
 #undef CELL
 #undef WK
+#undef INFO
 }
 
 }  // namespace dgb

@@ -29,7 +29,7 @@ static cudaError_t set_smem(KernelT kern, size_t smem) {
 template <int KP>
 static cudaError_t run_sip_axis(const DevCtx& c, double mc, int dir, const double* x, double* y) {
   using G = SipAxisCfg<KP>;
-  cudaError_t e = ensure_ftab<KP + 1, KP + 2>();
+  cudaError_t e = ensure_ftab<KP + 1, KP + 1>();
   if (e == cudaSuccess) e = set_smem(k_sip_axis<KP>, G::SMEM);
   if (e != cudaSuccess) return e;
   const int grid = (c.ncells + G::C - 1) / G::C;
