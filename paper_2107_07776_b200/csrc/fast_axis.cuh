@@ -333,13 +333,13 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, cons
 //   mass M x + visc A_sip x     (line-split, exact)
 // + adv C_lf(w) x               (k+2 Gauss rule; sum factorisation)
 // ===========================================================================
-template <int K>
+template <int K, int CC, int TH>
 struct MomAxisCfg {
   static constexpr int N = K + 1, Q = K + 2, NB = N * N * N, NF = N * N, QN = Q * N, QQ = Q * Q;
   using P = Pad<N>;
   static constexpr int CT = P::CT;
-  static constexpr int C = K == 1 ? 16 : (K == 2 ? 10 : 6);      // cells per CTA
-  static constexpr int T = K == 1 ? 128 : (K == 2 ? 192 : 192);  // threads per CTA
+  static constexpr int C = CC;   // cells per CTA
+  static constexpr int T = TH;   // threads per CTA
   // persistent per-cell regions
   static constexpr int O_X = 0, O_W = 3 * CT, O_OUT = 6 * CT, O_INFO = 9 * CT;
   static constexpr int O_WORK = O_INFO + kInfoDoubles;
@@ -349,19 +349,23 @@ struct MomAxisCfg {
   static constexpr int B_R1 = 0;           // XB (6 QNN) then TZ/TY/TX (9 QQN)
   static constexpr int B_R2 = 9 * QQ * N;  // YB (6 QQN) then SA/SB (6 QNN)
   static constexpr int B_END = B_R2 + 6 * QQ * N;
-  // face phase (one axis at a time): V1 [8 fields][2 sides][Q x N], FL1 [3][2][Q x N]
-  static constexpr int F_V1 = 0, F_FL = 16 * QN, F_END = F_FL + 6 * QN;
+  // face phase (all 6 faces at once): V1 [8 fields][6][Q x N] -> FB [3][6][N x N];  FL [3][6][Q x N]
+  static constexpr int F_V1 = 0, F_FB = 0, F_FL = 48 * QN, F_END = F_FL + 18 * QN;
   static constexpr int WORK = A_END > B_END ? (A_END > F_END ? A_END : F_END) : (B_END > F_END ? B_END : F_END);
   static constexpr int PER = (O_WORK + WORK) | 1;
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
+// default tuning per degree
+template <int K> struct MomAxisTune { static constexpr int C = 6, T = 192; };
+template <> struct MomAxisTune<1> { static constexpr int C = 16, T = 128; };
+template <> struct MomAxisTune<2> { static constexpr int C = 8, T = 192; };
+template <> struct MomAxisTune<3> { static constexpr int C = 3, T = 96; };
 
-template <int K>
-__global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, const double* __restrict__ aff,
-                                                                    MomCoef co, const double* __restrict__ x,
-                                                                    const double* __restrict__ w,
-                                                                    double* __restrict__ y) {
-  using G = MomAxisCfg<K>;
+template <int K, int CC, int TH>
+__global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, const double* __restrict__ aff, MomCoef co,
+                                                      const double* __restrict__ x, const double* __restrict__ w,
+                                                      double* __restrict__ y) {
+  using G = MomAxisCfg<K, CC, TH>;
   using P = typename G::P;
   constexpr int N = G::N, Q = G::Q, NB = G::NB, NF = G::NF, QN = G::QN, QQ = G::QQ, C = G::C, PER = G::PER;
   constexpr int TT = G::T, CT = G::CT;
@@ -372,6 +376,7 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
   const int nc = min(C, m.ncells - c0);
   const int tid = threadIdx.x;
   const double sfac = (double)((K + 1) * (K + 1));
+  const bool faces = co.adv != 0.0;
 #define CELL(c) (sm + (c) * PER)
 #define WK(c) (sm + (c) * PER + G::O_WORK)
 #define INFO(c) (*reinterpret_cast<CellInfo*>(sm + (c) * PER + G::O_INFO))
@@ -388,38 +393,70 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
   __syncthreads();
 
   // ------------------------------------------------------------------ pass A: mass + viscous (line split)
-  // A: lines of every direction: S_d (visc) on raw lines, UX = M_x u
-  for (int idx = tid; idx < nc * 9 * NF; idx += TT) {
-    const int c = idx / (9 * NF), r = idx - c * 9 * NF;
-    const int comp = r / (3 * NF), r2 = r - comp * 3 * NF;
-    const int d = r2 / NF, tl = r2 - d * NF;
-    const int p = tl % N, q = tl / N;
-    const CellInfo& ci = INFO(c);
-    const int st = d == 0 ? 1 : (d == 1 ? P::PX : P::PY);
-    const int b0 = d == 0 ? P::idx(0, p, q) : (d == 1 ? P::idx(p, 0, q) : P::idx(p, q, 0));
-    const int gst = d == 0 ? 1 : (d == 1 ? N : NF);
-    const int g0 = comp * NB + (d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q));
-    double u[N], uL[N], uR[N], o[N];
-    const double* us = CELL(c) + G::O_X + comp * CT + b0;
+  // A: lines of every direction: S_d (visc) on raw lines, UX = M_x u.  The two
+  //    neighbour lines of the next item are prefetched while the current one computes.
+  {
+    constexpr int NIT = 9 * NF;
+    const int total = nc * NIT;
+    auto gbase = [&](int idx, int& nl, int& nr, int& g0, int& gst) {
+      const int c = idx / NIT, r = idx - c * NIT;
+      const int comp = r / (3 * NF), r2 = r - comp * 3 * NF;
+      const int d = r2 / NF, tl = r2 - d * NF;
+      const int p = tl % N, q = tl / N;
+      nl = INFO(c).nb[2 * d];
+      nr = INFO(c).nb[2 * d + 1];
+      gst = d == 0 ? 1 : (d == 1 ? N : NF);
+      g0 = comp * NB + (d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q));
+    };
+    double pL[N], pR[N];
+    if (tid < total) {
+      int nl, nr, g0, gst;
+      gbase(tid, nl, nr, g0, gst);
 #pragma unroll
-    for (int l = 0; l < N; ++l) u[l] = us[l * st];
-    const int nl = ci.nb[2 * d], nr = ci.nb[2 * d + 1];
-#pragma unroll
-    for (int l = 0; l < N; ++l) {
-      uL[l] = nl >= 0 ? __ldg(x + (size_t)nl * 3 * NB + g0 + l * gst) : 0.0;
-      uR[l] = nr >= 0 ? __ldg(x + (size_t)nr * 3 * NB + g0 + l * gst) : 0.0;
+      for (int l = 0; l < N; ++l) {
+        pL[l] = nl >= 0 ? __ldg(x + (size_t)nl * 3 * NB + g0 + l * gst) : 0.0;
+        pR[l] = nr >= 0 ? __ldg(x + (size_t)nr * 3 * NB + g0 + l * gst) : 0.0;
+      }
     }
-    sip_line<N>(ta, ci, d, u, uL, uR, true, co.visc, o);
-    double* so = WK(c) + (d == 0 ? G::A_SX : (d == 1 ? G::A_SY : G::A_SZ)) + comp * CT + b0;
+    for (int idx = tid; idx < total; idx += TT) {
+      double uL[N], uR[N];
 #pragma unroll
-    for (int l = 0; l < N; ++l) so[l * st] = o[l];
-    if (d == 0) {
+      for (int l = 0; l < N; ++l) {
+        uL[l] = pL[l];
+        uR[l] = pR[l];
+      }
+      if (idx + TT < total) {
+        int nl, nr, g0, gst;
+        gbase(idx + TT, nl, nr, g0, gst);
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double s = 0.0;
+        for (int l = 0; l < N; ++l) {
+          pL[l] = nl >= 0 ? __ldg(x + (size_t)nl * 3 * NB + g0 + l * gst) : 0.0;
+          pR[l] = nr >= 0 ? __ldg(x + (size_t)nr * 3 * NB + g0 + l * gst) : 0.0;
+        }
+      }
+      const int c = idx / NIT, r = idx - c * NIT;
+      const int comp = r / (3 * NF), r2 = r - comp * 3 * NF;
+      const int d = r2 / NF, tl = r2 - d * NF;
+      const int p = tl % N, q = tl / N;
+      const CellInfo& ci = INFO(c);
+      const int st = d == 0 ? 1 : (d == 1 ? P::PX : P::PY);
+      const int b0 = d == 0 ? P::idx(0, p, q) : (d == 1 ? P::idx(p, 0, q) : P::idx(p, q, 0));
+      double u[N], o[N];
+      const double* us = CELL(c) + G::O_X + comp * CT + b0;
 #pragma unroll
-        for (int l = 0; l < N; ++l) s = fma(ta.M[i][l], u[l], s);
-        WK(c)[G::A_UX + comp * CT + b0 + i] = s;
+      for (int l = 0; l < N; ++l) u[l] = us[l * st];
+      sip_line<N>(ta, ci, d, u, uL, uR, true, co.visc, o);
+      double* so = WK(c) + (d == 0 ? G::A_SX : (d == 1 ? G::A_SY : G::A_SZ)) + comp * CT + b0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) so[l * st] = o[l];
+      if (d == 0) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = 0.0;
+#pragma unroll
+          for (int l = 0; l < N; ++l) s = fma(ta.M[i][l], u[l], s);
+          WK(c)[G::A_UX + comp * CT + b0 + i] = s;
+        }
       }
     }
   }
@@ -631,129 +668,137 @@ __global__ void __launch_bounds__(MomAxisCfg<K>::T) k_momentum_axis(MeshArgs m, 
   }
   __syncthreads();
 
-  // ------------------------------------------------------------------ LF advective faces, one axis at a time
-  if (co.adv != 0.0) {
-    for (int a = 0; a < 3; ++a) {
-      const int st = a == 0 ? 1 : (a == 1 ? P::PX : P::PY);
+  // ------------------------------------------------------------------ LF advective faces, all 6 at once
+  if (faces) {
+    // F1: traces of u (3 comps, own + neighbour) and w_a (own + neighbour) on face-node line q,
+    //     contracted along p with B:  V1[field][f][qp + Q q]
+    for (int idx = tid; idx < nc * 6 * N; idx += TT) {
+      const int c = idx / (6 * N), r = idx - c * 6 * N;
+      const int f = r / N, q = r - f * N;
+      const int a = f >> 1, s = f & 1;
       const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
-      // F1: traces of u (3 comps, own + neighbour) and w_a (own + neighbour) on the face-node
-      //     line q, contracted along p with B:  V1[field][s][qp + Q q]
-      for (int idx = tid; idx < nc * 2 * N; idx += TT) {
-        const int c = idx / (2 * N), r = idx - c * 2 * N;
-        const int s = r / N, q = r - s * N;
-        const CellInfo& ci = INFO(c);
-        const int nb = ci.nb[2 * a + s];
-        const int Ls = s ? N - 1 : 0, Lo = s ? 0 : N - 1;
-        double v[8][N];
+      const CellInfo& ci = INFO(c);
+      const int nb = ci.nb[f];
+      const int Ls = s ? N - 1 : 0, Lo = s ? 0 : N - 1;
+      double v[8][N];
 #pragma unroll
-        for (int p = 0; p < N; ++p) {
-          const int li = a == 0 ? P::idx(Ls, p, q) : (a == 1 ? P::idx(p, Ls, q) : P::idx(p, q, Ls));
-          const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + Lo * gst;
-#pragma unroll
-          for (int comp = 0; comp < 3; ++comp) {
-            v[comp][p] = CELL(c)[G::O_X + comp * CT + li];
-            v[3 + comp][p] = nb >= 0 ? __ldg(x + (size_t)nb * 3 * NB + comp * NB + go) : 0.0;
-          }
-          v[6][p] = CELL(c)[G::O_W + a * CT + li];
-          v[7][p] = nb >= 0 ? __ldg(w + (size_t)nb * 3 * NB + a * NB + go) : 0.0;
-        }
-        double* o = WK(c) + G::F_V1 + s * QN + Q * q;
-#pragma unroll
-        for (int fl = 0; fl < 8; ++fl)
-#pragma unroll
-          for (int qp = 0; qp < Q; ++qp) {
-            double acc = 0.0;
-#pragma unroll
-            for (int l = 0; l < N; ++l) acc = fma(tq.B[qp][l], v[fl][l], acc);
-            o[fl * 2 * QN + qp] = acc;
-          }
-      }
-      __syncthreads();
-      // F2: along q: values at the face Gauss points, LF flux, B^T back along q -> FL [comp][s][qp + Q l]
-      for (int idx = tid; idx < nc * 2 * Q; idx += TT) {
-        const int c = idx / (2 * Q), r = idx - c * 2 * Q;
-        const int s = r / Q, qp = r - s * Q;
-        const CellInfo& ci = INFO(c);
-        const int f = 2 * a + s;
-        const double* in = WK(c) + G::F_V1 + s * QN + qp;
-        double v[8][N];
-#pragma unroll
-        for (int fl = 0; fl < 8; ++fl)
-#pragma unroll
-          for (int l = 0; l < N; ++l) v[fl][l] = in[fl * 2 * QN + Q * l];
-        const double sgn = s ? 1.0 : -1.0;
-        const double wbase = co.adv * ci.A[a] * tq.w[qp];
-        const int ty = ci.type[f];
-        double out[3][N];
+      for (int p = 0; p < N; ++p) {
+        const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + Lo * gst;
 #pragma unroll
         for (int comp = 0; comp < 3; ++comp)
+          v[3 + comp][p] = nb >= 0 ? __ldg(x + (size_t)nb * 3 * NB + comp * NB + go) : 0.0;
+        v[7][p] = nb >= 0 ? __ldg(w + (size_t)nb * 3 * NB + a * NB + go) : 0.0;
+      }
 #pragma unroll
-          for (int l = 0; l < N; ++l) out[comp][l] = 0.0;
+      for (int p = 0; p < N; ++p) {
+        const int li = a == 0 ? P::idx(Ls, p, q) : (a == 1 ? P::idx(p, Ls, q) : P::idx(p, q, Ls));
 #pragma unroll
-        for (int qq = 0; qq < Q; ++qq) {
-          double val[8];
+        for (int comp = 0; comp < 3; ++comp) v[comp][p] = CELL(c)[G::O_X + comp * CT + li];
+        v[6][p] = CELL(c)[G::O_W + a * CT + li];
+      }
+      double* o = WK(c) + G::F_V1 + f * QN + Q * q;
 #pragma unroll
-          for (int fl = 0; fl < 8; ++fl) {
-            double acc = 0.0;
+      for (int fl = 0; fl < 8; ++fl)
 #pragma unroll
-            for (int l = 0; l < N; ++l) acc = fma(tq.B[qq][l], v[fl][l], acc);
-            val[fl] = acc;
-          }
-          const double wq = wbase * tq.w[qq];
-          const double wns = sgn * val[6];
-          double fl3[3];
-          if (ty == 0) {  // forms.cpp:555-573
-            const double wno = sgn * val[7];
-            const double lam = fmax(fabs(wns), fabs(wno));
+        for (int qp = 0; qp < Q; ++qp) {
+          double acc = 0.0;
 #pragma unroll
-            for (int comp = 0; comp < 3; ++comp)
-              fl3[comp] = wq * (0.5 * (val[comp] * wns + val[3 + comp] * wno) + 0.5 * lam * (val[comp] - val[3 + comp]));
-          } else {  // forms.cpp:592-599
-            const double cf = ty == 2 ? wns : fabs(wns);
+          for (int l = 0; l < N; ++l) acc = fma(tq.B[qp][l], v[fl][l], acc);
+          o[fl * 6 * QN + qp] = acc;
+        }
+    }
+    __syncthreads();
+    // F2: along q: values at the face Gauss points, LF flux, B^T back along q -> FL [comp][f][qp + Q l]
+    for (int idx = tid; idx < nc * 6 * Q; idx += TT) {
+      const int c = idx / (6 * Q), r = idx - c * 6 * Q;
+      const int f = r / Q, qp = r - f * Q;
+      const int a = f >> 1, s = f & 1;
+      const CellInfo& ci = INFO(c);
+      const double* in = WK(c) + G::F_V1 + f * QN + qp;
+      double v[8][N];
 #pragma unroll
-            for (int comp = 0; comp < 3; ++comp) fl3[comp] = wq * cf * val[comp];
-          }
+      for (int fl = 0; fl < 8; ++fl)
+#pragma unroll
+        for (int l = 0; l < N; ++l) v[fl][l] = in[fl * 6 * QN + Q * l];
+      const double sgn = s ? 1.0 : -1.0;
+      const double wbase = co.adv * ci.A[a] * tq.w[qp];
+      const int ty = ci.type[f];
+      double out[3][N];
+#pragma unroll
+      for (int comp = 0; comp < 3; ++comp)
+#pragma unroll
+        for (int l = 0; l < N; ++l) out[comp][l] = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < Q; ++qq) {
+        double val[8];
+#pragma unroll
+        for (int fl = 0; fl < 8; ++fl) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < N; ++l) acc = fma(tq.B[qq][l], v[fl][l], acc);
+          val[fl] = acc;
+        }
+        const double wq = wbase * tq.w[qq];
+        const double wns = sgn * val[6];
+        double fl3[3];
+        if (ty == 0) {  // forms.cpp:555-573
+          const double wno = sgn * val[7];
+          const double lam = fmax(fabs(wns), fabs(wno));
 #pragma unroll
           for (int comp = 0; comp < 3; ++comp)
+            fl3[comp] = wq * (0.5 * (val[comp] * wns + val[3 + comp] * wno) + 0.5 * lam * (val[comp] - val[3 + comp]));
+        } else {  // forms.cpp:592-599
+          const double cf = ty == 2 ? wns : fabs(wns);
 #pragma unroll
-            for (int l = 0; l < N; ++l) out[comp][l] = fma(tq.B[qq][l], fl3[comp], out[comp][l]);
+          for (int comp = 0; comp < 3; ++comp) fl3[comp] = wq * cf * val[comp];
         }
-        double* o = WK(c) + G::F_FL + s * QN + qp;
 #pragma unroll
         for (int comp = 0; comp < 3; ++comp)
 #pragma unroll
-          for (int l = 0; l < N; ++l) o[comp * 2 * QN + Q * l] = out[comp][l];
+          for (int l = 0; l < N; ++l) out[comp][l] = fma(tq.B[qq][l], fl3[comp], out[comp][l]);
       }
-      __syncthreads();
-      // F3: B^T along p, add into the face layer of OUT
-      for (int idx = tid; idx < nc * 2 * N; idx += TT) {
-        const int c = idx / (2 * N), r = idx - c * 2 * N;
-        const int s = r / N, q = r - s * N;
-        const int Ls = s ? N - 1 : 0;
-        const double* in = WK(c) + G::F_FL + s * QN + Q * q;
+      double* o = WK(c) + G::F_FL + f * QN + qp;
 #pragma unroll
-        for (int comp = 0; comp < 3; ++comp) {
-          double v[Q];
+      for (int comp = 0; comp < 3; ++comp)
 #pragma unroll
-          for (int qp = 0; qp < Q; ++qp) v[qp] = in[comp * 2 * QN + qp];
-#pragma unroll
-          for (int p = 0; p < N; ++p) {
-            double acc = 0.0;
-#pragma unroll
-            for (int qp = 0; qp < Q; ++qp) acc = fma(tq.B[qp][p], v[qp], acc);
-            const int li = a == 0 ? P::idx(Ls, p, q) : (a == 1 ? P::idx(p, Ls, q) : P::idx(p, q, Ls));
-            CELL(c)[G::O_OUT + comp * CT + li] += acc;
-          }
-        }
-      }
-      __syncthreads();
+        for (int l = 0; l < N; ++l) o[comp * 6 * QN + Q * l] = out[comp][l];
     }
+    __syncthreads();
+    // F3: B^T along p -> nodal face contributions FB [comp][f][p + N q]
+    for (int idx = tid; idx < nc * 18 * N; idx += TT) {
+      const int c = idx / (18 * N), r = idx - c * 18 * N;
+      const int cf = r / N, q = r - cf * N;  // cf = comp*6 + f
+      const double* in = WK(c) + G::F_FL + cf * QN + Q * q;
+      double v[Q];
+#pragma unroll
+      for (int qp = 0; qp < Q; ++qp) v[qp] = in[qp];
+      double* o = WK(c) + G::F_FB + cf * NF + N * q;
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        double acc = 0.0;
+#pragma unroll
+        for (int qp = 0; qp < Q; ++qp) acc = fma(tq.B[qp][p], v[qp], acc);
+        o[p] = acc;
+      }
+    }
+    __syncthreads();
   }
-  // ------------------------------------------------------------------ store
+  // ------------------------------------------------------------------ store (+ gather the face-layer contributions)
   for (int idx = tid; idx < nc * 3 * NB; idx += TT) {
     const int c = idx / (3 * NB), r = idx - c * 3 * NB;
     const int comp = r / NB, i = r - comp * NB;
-    y[(size_t)(c0 + c) * 3 * NB + r] = CELL(c)[G::O_OUT + comp * CT + P::idx(i % N, (i / N) % N, i / NF)];
+    const int ii[3] = {i % N, (i / N) % N, i / NF};
+    double v = CELL(c)[G::O_OUT + comp * CT + P::idx(ii[0], ii[1], ii[2])];
+    if (faces) {
+      const double* fb = WK(c) + G::F_FB + comp * 6 * NF;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int t = (a == 0 ? ii[1] : ii[0]) + N * (a == 2 ? ii[1] : ii[2]);
+        if (ii[a] == 0) v += fb[(2 * a) * NF + t];
+        if (ii[a] == N - 1) v += fb[(2 * a + 1) * NF + t];
+      }
+    }
+    y[(size_t)(c0 + c) * 3 * NB + r] = v;
   }
 #undef CELL
 #undef WK

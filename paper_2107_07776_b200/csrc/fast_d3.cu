@@ -39,13 +39,14 @@ static cudaError_t run_sip_axis(const DevCtx& c, double mc, int dir, const doubl
 
 template <int K>
 static cudaError_t run_momentum_axis(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y) {
-  using G = MomAxisCfg<K>;
+  constexpr int CC = MomAxisTune<K>::C, TH = MomAxisTune<K>::T;
+  using G = MomAxisCfg<K, CC, TH>;
   cudaError_t e = ensure_ftab<K + 1, K + 2>();
   if (e == cudaSuccess) e = ensure_ftab<K + 1, K + 1>();
-  if (e == cudaSuccess) e = set_smem(k_momentum_axis<K>, G::SMEM);
+  if (e == cudaSuccess) e = set_smem(k_momentum_axis<K, CC, TH>, G::SMEM);
   if (e != cudaSuccess) return e;
   const int grid = (c.ncells + G::C - 1) / G::C;
-  k_momentum_axis<K><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.aff, co, x, w, y);
+  k_momentum_axis<K, CC, TH><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.aff, co, x, w, y);
   return cudaGetLastError();
 }
 

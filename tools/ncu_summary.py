@@ -1,0 +1,26 @@
+"""Summarise an ncu report: key metrics per kernel + top source lines by stall samples."""
+import csv, collections, subprocess, sys
+rep = sys.argv[1]
+pat = sys.argv[2] if len(sys.argv) > 2 else "k_"
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()
+rows = list(csv.reader(raw))
+hdr = rows[0]
+keys = ["gpu__time_duration.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed.avg.per_cycle_active", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__warps_active.avg.per_cycle_active",
+        "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread",
+        "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"]
+for r in rows[2:]:
+    name = r[hdr.index("Kernel Name")]
+    if pat not in name:
+        continue
+    print("=====", name[:60])
+    for k in keys:
+        if k in hdr:
+            print(f"  {k} = {r[hdr.index(k)]} {rows[1][hdr.index(k)]}")
