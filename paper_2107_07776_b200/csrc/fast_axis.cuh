@@ -108,6 +108,51 @@ __device__ __forceinline__ void load_info(CellInfo& ci, const MeshArgs& m, const
   }
 }
 
+// Parallel fill of the CellInfo records of nc cells: one thread per (cell, slot),
+// slot 0..5 = faces, slot 6 = cell geometry (independent L2 loads in flight together).
+template <int TT>
+__device__ __forceinline__ void load_info_par(double* base, int per, int off, int nc, const MeshArgs& m,
+                                              const double* __restrict__ aff, int c0, double sfac) {
+  for (int idx = threadIdx.x; idx < nc * 7; idx += TT) {
+    const int c = idx / 7, f = idx - c * 7;
+    CellInfo& ci = *reinterpret_cast<CellInfo*>(base + c * per + off);
+    const int cell = c0 + c;
+    if (f == 6) {
+      const double* r = aff + (size_t)cell * kAffStride3;
+      const double i0 = r[0], i1 = r[4], i2 = r[8], dj = r[9];
+      ci.ih[0] = i0;
+      ci.ih[1] = i1;
+      ci.ih[2] = i2;
+      ci.detJ = dj;
+      ci.A[0] = dj * i0;
+      ci.A[1] = dj * i1;
+      ci.A[2] = dj * i2;
+    } else {
+      const int nb = m.nbr[(size_t)cell * 6 + f];
+      const double pen = sfac * m.pen[(size_t)cell * 6 + f];
+      int ty = 0;
+      double ihn = 0.0;
+      if (nb >= 0) {
+        ihn = __ldg(aff + (size_t)nb * kAffStride3 + 4 * (f >> 1));
+      } else {
+        const int bid = -1 - nb;
+        ty = (bid >= 0 && bid < 64 && m.bctype[bid] == 1) ? 2 : 1;
+      }
+      ci.nb[f] = nb;
+      ci.pen[f] = pen;
+      ci.type[f] = ty;
+      ci.ihn[f] = ihn;
+    }
+  }
+}
+
+// 8-byte asynchronous global -> shared copy (LDGSTS); many in flight per thread.
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // 1D SIP line operator along direction d (stiffness + both d-faces), times `scale`.
 // u: own line; uL / uR: neighbour lines across faces 2d / 2d+1 (read only if interior).
 // dirichlet: whether non-interior, non-outlet faces carry the Dirichlet-type terms
@@ -215,14 +260,16 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, cons
   // S0: cell values (padded) + per-cell info
   for (int idx = tid; idx < nc * NB; idx += TT) {
     const int c = idx / NB, i = idx - c * NB;
-    CELL(c)[G::O_U + P::idx(i % N, (i / N) % N, i / NF)] = x[(size_t)(c0 + c) * NB + i];
+    cp_async8(CELL(c) + G::O_U + P::idx(i % N, (i / N) % N, i / NF), x + (size_t)(c0 + c) * NB + i);
   }
-  for (int c = tid; c < nc; c += TT) {
-    load_info(INFO(c), m, aff, c0 + c, sfac);
-    // the scalar operator ignores outlet ids: all boundary faces are natural, or
-    // all Dirichlet when dir_bdry (forms.cpp:218-242)
-    for (int f = 0; f < 6; ++f)
-      if (INFO(c).type[f] == 2) INFO(c).type[f] = 1;
+  load_info_par<TT>(sm, PER, G::O_INFO, nc, m, aff, c0, sfac);
+  cp_async_wait_all();
+  __syncthreads();
+  // the scalar operator ignores outlet ids: all boundary faces are natural, or all
+  // Dirichlet when dir_bdry (forms.cpp:218-242)
+  for (int idx = tid; idx < nc * 6; idx += TT) {
+    CellInfo& ci = INFO(idx / 6);
+    if (ci.type[idx % 6] == 2) ci.type[idx % 6] = 1;
   }
   __syncthreads();
   // A: all-direction lines: S_d on raw lines (+ neighbour lines), and Ux = M_x u
@@ -386,10 +433,11 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, const double* 
     const int c = idx / (3 * NB), r = idx - c * 3 * NB;
     const int comp = r / NB, i = r - comp * NB;
     const int pi = comp * CT + P::idx(i % N, (i / N) % N, i / NF);
-    CELL(c)[G::O_X + pi] = x[(size_t)(c0 + c) * 3 * NB + r];
-    CELL(c)[G::O_W + pi] = w[(size_t)(c0 + c) * 3 * NB + r];
+    cp_async8(CELL(c) + G::O_X + pi, x + (size_t)(c0 + c) * 3 * NB + r);
+    cp_async8(CELL(c) + G::O_W + pi, w + (size_t)(c0 + c) * 3 * NB + r);
   }
-  for (int c = tid; c < nc; c += TT) load_info(INFO(c), m, aff, c0 + c, sfac);
+  load_info_par<TT>(sm, PER, G::O_INFO, nc, m, aff, c0, sfac);
+  cp_async_wait_all();
   __syncthreads();
 
   // ------------------------------------------------------------------ pass A: mass + viscous (line split)
