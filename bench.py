@@ -111,6 +111,25 @@ def dist_info():
     return ws, rank, local
 
 
+def reduce_max(x: float) -> float:
+    """Max over ranks (device timing rule: the job takes as long as its slowest rank).
+    NCCL on GPU ranks, gloo on CPU (tests/test_multirank.py)."""
+    import torch
+    import torch.distributed as tdist
+    if not (tdist.is_available() and tdist.is_initialized()) or tdist.get_world_size() == 1:
+        return x
+    dev = torch.device("cuda", torch.cuda.current_device()) if tdist.get_backend() == "nccl" else torch.device("cpu")
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(ws: int, units_per_rank: int, ms_max: float) -> float:
+    """Replicas (weak scaling): every rank processes its own copy of the workload;
+    value = all units processed / the slowest rank's time."""
+    return ws * units_per_rank / (ms_max * 1e-3)
+
+
 # ---------------------------------------------------------------------------
 # reference CPU leg
 # ---------------------------------------------------------------------------
@@ -225,13 +244,9 @@ def run_device(args):
     total_ms = ev[0].elapsed_time(ev[2 * args.steps])
     t_mom = [ev[2 * k].elapsed_time(ev[1 + 2 * k]) if k else ev[0].elapsed_time(ev[1]) for k in range(args.steps)]
     t_prs = [ev[1 + 2 * k].elapsed_time(ev[2 + 2 * k]) for k in range(args.steps)]
-    ms_step = total_ms / args.steps
-    if ws > 1:
-        tt = torch.tensor([ms_step], device=dev)
-        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-        ms_step = float(tt.item())
+    ms_step = reduce_max(total_ms / args.steps)
     dofs_step = D.n_u + D.n_p
-    value = ws * dofs_step / (ms_step * 1e-3) / 1e9
+    value = whole_job_rate(ws, dofs_step, ms_step) / 1e9
 
     # ---- end-to-end through the public API with host buffers (pinned), copies timed
     xh = x_h.pin_memory()
@@ -261,12 +276,8 @@ def run_device(args):
         e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / ne2e
-    if ws > 1:
-        tt = torch.tensor([e2e_ms], device=dev)
-        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
-    e2e_val = ws * dofs_step / (e2e_ms * 1e-3) / 1e9
+    e2e_ms = reduce_max(e0.elapsed_time(e1) / ne2e)
+    e2e_val = whole_job_rate(ws, dofs_step, e2e_ms) / 1e9
 
     if rank != 0:
         if ws > 1:

@@ -1,0 +1,232 @@
+// dgb_reference_adapter.hpp — drop-in binding of the reference's operator /
+// solver API (proj/src/forms.hpp, krylov.hpp) onto libdgb.so (include/dgb.h).
+//
+// A maintainer of the reference adds this header and links libdgb.so; call
+// sites keep their signatures and semantics:
+//
+//   dgns::apply_momentum(Vu, geom, ctx, x, out)        forms.hpp:111-113
+//   dgns::momentum_diagonal(Vu, geom, ctx, diag)       forms.hpp:114-116
+//   dgns::apply_pressure_helmholtz(Vp, geom, mc, x, y) forms.hpp:126-128
+//   dgns::helmholtz_diagonal(Vp, geom, mc, diag)       forms.hpp:129-131
+//   dgns::apply_mass / mass_diagonal                   forms.hpp:105-109
+//   dgns::divergence_functional / pressure_rhs /
+//         pressure_gradient_rhs                        forms.hpp:136-150
+//   dgns::kinetic_energy                               forms.hpp:168-170
+//   dgns::cg_solve / gmres_solve (device operators)    krylov.hpp:58-66
+//
+// become  dgb_adapter::Device dev(mesh, Vu, Vp);  dev.apply_momentum(ctx, x, out); ...
+// Outputs are resized and overwritten like the reference (out.assign(n, 0)),
+// errors are re-raised as the reference's exception types (SolverError with the
+// residual history, std::runtime_error for a missing advecting field).
+// Host Fields are staged through persistent device buffers; keep fields on the
+// device (Device::DeviceField) inside time loops to avoid PCIe traffic.
+#pragma once
+
+#include <algorithm>
+#include <array>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dgb.h"
+#include "forms.hpp"
+#include "krylov.hpp"
+#include "mesh.hpp"
+#include "space.hpp"
+
+namespace dgb_adapter {
+
+inline void check(int status) {
+  if (status == DGB_OK) return;
+  const std::string msg = dgb_last_error();
+  if (status == DGB_E_MISSING_FIELD) throw std::runtime_error(msg);
+  if (status == DGB_E_NO_CONVERGENCE || status == DGB_E_BREAKDOWN || status == DGB_E_NOT_SPD ||
+      status == DGB_E_ZERO_DIAG)
+    throw dgns::SolverError(msg, {});
+  throw std::runtime_error("dgb: " + msg);
+}
+
+class DeviceField {
+ public:
+  DeviceField(dgb_ctx* c, size_t n) : ctx_(c), n_(n) { check(dgb_alloc(c, n, &p_)); }
+  ~DeviceField() { dgb_free(ctx_, p_); }
+  DeviceField(const DeviceField&) = delete;
+  DeviceField& operator=(const DeviceField&) = delete;
+  void upload(const dgns::Field& f) { check(dgb_copy_h2d(ctx_, p_, f.data(), n_)); }
+  void download(dgns::Field& f) const {
+    f.resize(n_);
+    check(dgb_copy_d2h(ctx_, f.data(), p_, n_));
+  }
+  double* get() const { return p_; }
+  size_t size() const { return n_; }
+
+ private:
+  dgb_ctx* ctx_;
+  size_t n_;
+  double* p_ = nullptr;
+};
+
+/// Device context built from the reference's host objects (Mesh + spaces).
+template <int dim>
+class Device {
+ public:
+  Device(const dgns::Mesh<dim>& mesh, const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<dim>& Vp,
+         int device = 0) {
+    // active cells become the context's cells (reference active order, space.hpp:5-8)
+    const int nv = dgns::Mesh<dim>::n_vertices_per_cell, nf = 2 * dim;
+    std::vector<double> verts(mesh.vertices.size() * dim);
+    for (size_t v = 0; v < mesh.vertices.size(); ++v)
+      for (int d = 0; d < dim; ++d) verts[v * dim + d] = mesh.vertices[v][d];
+    std::vector<int> cells, bids;
+    for (int c : mesh.active_cells()) {
+      for (int v = 0; v < nv; ++v) cells.push_back(mesh.cells[c].v[v]);
+      for (int f = 0; f < nf; ++f) bids.push_back(mesh.cells[c].boundary_id[f]);
+    }
+    check(dgb_ctx_create_mesh(dim, (int)mesh.vertices.size(), verts.data(), mesh.n_active(), cells.data(),
+                              bids.data(), Vu.degree(), Vp.degree(), device, &ctx_));
+    nu_ = Vu.n_dofs();
+    np_ = Vp.n_dofs();
+  }
+  ~Device() {
+    x_u_.reset(), w_u_.reset(), y_u_.reset(), x_p_.reset(), y_p_.reset(), d_.reset(), b_.reset(), s_.reset();
+    dgb_ctx_destroy(ctx_);
+  }
+  dgb_ctx* ctx() const { return ctx_; }
+
+  /// BoundaryTable (forms.hpp:29-51): types + Dirichlet data tabulated at time t.
+  void set_boundary(const dgns::BoundaryTable<dim>& bc, double t) {
+    for (const auto& [id, e] : bc.entries) {
+      check(dgb_set_boundary_type(ctx_, id, e.type == dgns::BcType::outlet ? DGB_BC_OUTLET : DGB_BC_DIRICHLET));
+      if (e.value) {
+        const auto* fn = &e.value;
+        check(dgb_set_dirichlet_fn(
+            ctx_, id,
+            [](const double* x, double tt, double* out, void* user) {
+              std::array<double, dim> xx;
+              for (int d = 0; d < dim; ++d) xx[d] = x[d];
+              (*static_cast<const decltype(fn)>(user))(xx, tt, out);
+            },
+            const_cast<void*>(static_cast<const void*>(fn)), t));
+      }
+    }
+  }
+
+  void apply_momentum(const dgns::MomentumCtx<dim>& m, const dgns::Field& x, dgns::Field& out) {
+    const double coefs[4] = {m.mass_coef, m.visc_coef, m.adv_coef, m.skew_coef};
+    up(x_u_, x, nu_);
+    const double* w = nullptr;
+    if (m.advecting) {
+      up(w_u_, *m.advecting, nu_);
+      w = w_u_->get();
+    }
+    check(dgb_momentum_apply(ctx_, coefs, w, x_u_->get(), y_u()->get()));
+    y_u_->download(out);
+  }
+  void momentum_diagonal(const dgns::MomentumCtx<dim>& m, dgns::Field& diag) {
+    const double coefs[4] = {m.mass_coef, m.visc_coef, m.adv_coef, m.skew_coef};
+    const double* w = nullptr;
+    if (m.advecting) {
+      up(w_u_, *m.advecting, nu_);
+      w = w_u_->get();
+    }
+    check(dgb_momentum_diag(ctx_, coefs, w, y_u()->get()));
+    y_u_->download(diag);
+  }
+  void apply_pressure_helmholtz(double mc, const dgns::Field& x, dgns::Field& out) {
+    up(x_p_, x, np_);
+    check(dgb_pressure_apply(ctx_, mc, x_p_->get(), y_p()->get()));
+    y_p_->download(out);
+  }
+  void helmholtz_diagonal(double mc, dgns::Field& diag) {
+    check(dgb_helmholtz_diag(ctx_, mc, y_p()->get()));
+    y_p_->download(diag);
+  }
+  void divergence_functional(const dgns::Field& u, dgns::Field& out) {
+    up(x_u_, u, nu_);
+    check(dgb_divergence(ctx_, x_u_->get(), y_p()->get()));
+    y_p_->download(out);
+  }
+  void pressure_gradient_rhs(const dgns::Field& p, dgns::Field& out) {
+    up(x_p_, p, np_);
+    check(dgb_pressure_gradient(ctx_, x_p_->get(), y_u()->get()));
+    y_u_->download(out);
+  }
+
+  /// cg_solve on the device pressure operator (krylov.hpp:58-60 semantics).
+  dgns::SolveResult cg_pressure(double mc, const dgns::Field& b, const dgns::SolverSettings& s, bool jacobi,
+                                dgns::Field& x) {
+    dgb_operator op{};
+    op.op = DGB_OP_PRESSURE;
+    op.coefs[0] = mc;
+    return solve(op, b, s, jacobi, x, np_, false);
+  }
+  /// gmres_solve on the device momentum operator (krylov.hpp:64-66 semantics).
+  dgns::SolveResult gmres_momentum(const dgns::MomentumCtx<dim>& m, const dgns::Field& b,
+                                   const dgns::SolverSettings& s, bool jacobi, dgns::Field& x) {
+    dgb_operator op{};
+    op.op = DGB_OP_MOMENTUM;
+    op.coefs[0] = m.mass_coef;
+    op.coefs[1] = m.visc_coef;
+    op.coefs[2] = m.adv_coef;
+    op.coefs[3] = m.skew_coef;
+    if (m.advecting) {
+      up(w_u_, *m.advecting, nu_);
+      op.d_w = w_u_->get();
+    }
+    return solve(op, b, s, jacobi, x, nu_, true);
+  }
+
+ private:
+  dgb_ctx* ctx_ = nullptr;
+  size_t nu_ = 0, np_ = 0;
+  std::unique_ptr<DeviceField> x_u_, w_u_, y_u_, x_p_, y_p_, d_, b_, s_;
+
+  void up(std::unique_ptr<DeviceField>& f, const dgns::Field& h, size_t n) {
+    if (!f) f = std::make_unique<DeviceField>(ctx_, n);
+    f->upload(h);
+  }
+  DeviceField* y_u() {
+    if (!y_u_) y_u_ = std::make_unique<DeviceField>(ctx_, nu_);
+    return y_u_.get();
+  }
+  DeviceField* y_p() {
+    if (!y_p_) y_p_ = std::make_unique<DeviceField>(ctx_, np_);
+    return y_p_.get();
+  }
+  dgns::SolveResult solve(const dgb_operator& op, const dgns::Field& b, const dgns::SolverSettings& s, bool jacobi,
+                          dgns::Field& x, size_t n, bool gmres) {
+    d_ = std::make_unique<DeviceField>(ctx_, n);
+    b_ = std::make_unique<DeviceField>(ctx_, n);
+    s_ = std::make_unique<DeviceField>(ctx_, n);
+    b_->upload(b);
+    s_->upload(x);
+    const double* inv = nullptr;
+    if (jacobi) {
+      if (op.op == DGB_OP_MOMENTUM)
+        check(dgb_momentum_diag(ctx_, op.coefs, op.d_w, d_->get()));
+      else
+        check(dgb_helmholtz_diag(ctx_, op.coefs[0], d_->get()));
+      check(dgb_jacobi_inverse(ctx_, n, d_->get(), d_->get()));
+      inv = d_->get();
+    }
+    const dgb_solver_settings st{s.rel_tol, s.abs_tol, s.max_iter, s.restart};
+    dgb_solve_result r{};
+    std::vector<double> hist(std::max(1, s.max_iter));
+    int hl = 0;
+    const int status = gmres ? dgb_gmres(ctx_, &op, &st, inv, b_->get(), s_->get(), &r, hist.data(),
+                                         (int)hist.size(), &hl)
+                             : dgb_cg(ctx_, &op, &st, inv, b_->get(), s_->get(), &r, hist.data(),
+                                      (int)hist.size(), &hl);
+    if (status == DGB_E_NO_CONVERGENCE || status == DGB_E_BREAKDOWN || status == DGB_E_NOT_SPD) {
+      hist.resize(std::min<size_t>(hist.size(), hl));
+      throw dgns::SolverError(dgb_last_error(), hist);
+    }
+    check(status);
+    s_->download(x);
+    return {r.iterations, r.residual};
+  }
+};
+
+}  // namespace dgb_adapter
