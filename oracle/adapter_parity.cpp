@@ -46,10 +46,10 @@ static int run(int n_el, double amp, int ku) {
   m.advecting = &w;
   m.bc = &bc;
   int bad = 0;
-  auto cmp = [&](const char* what, const Field& a, const Field& b) {
+  auto cmp = [&](const char* what, const Field& a, const Field& b, double tol = 1e-12) {
     const double e = rel(a, b);
-    std::printf("  %-28s rel L2 %.3e\n", what, e);
-    bad += !(e <= 1e-12);
+    std::printf("  %-28s rel L2 %.3e (tol %.0e)\n", what, e, tol);
+    bad += !(e <= tol);
   };
   Field r1, r2;
   apply_momentum(Vu, geom, m, x, r1);
@@ -85,7 +85,7 @@ static int run(int n_el, double amp, int ku) {
   auto dc = dev.cg_pressure(2.3, xp, s, true, xd);
   std::printf("  cg iterations  ref %d  dev %d\n", rc.iterations, dc.iterations);
   bad += std::abs(rc.iterations - dc.iterations) > 1;
-  cmp("cg solution", xd, xr);
+  cmp("cg solution", xd, xr, 1e-8);  // both stopped at rel tol 1e-10, iterations may differ by 1
   return bad;
 }
 
