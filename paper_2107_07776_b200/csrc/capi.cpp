@@ -113,6 +113,10 @@ int dgb_set_boundary_type(dgb_ctx* h, int id, int type) {
   NEED(id >= 0 && id < 64, "boundary id must be in [0, 64)");
   NEED(type == DGB_BC_DIRICHLET || type == DGB_BC_OUTLET, "bad boundary type");
   h->c.bctype_h[id] = type;
+  if (type == DGB_BC_OUTLET)
+    h->c.dc.ug.outlet_mask |= 1ull << id;
+  else
+    h->c.dc.ug.outlet_mask &= ~(1ull << id);
   const cudaError_t e = cudaMemcpyAsync(const_cast<int*>(h->c.dc.mesh.bctype), h->c.bctype_h, sizeof(h->c.bctype_h),
                                         cudaMemcpyHostToDevice, h->c.dc.stream);
   if (e != cudaSuccess) return ret(h, h->c.cuda_fail(e, "dgb_set_boundary_type"));

@@ -143,6 +143,35 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
             break;
           }
     dc.axis = axis;
+    // uniform structured grid (generate_cartesian order, one h): neighbours / boundary ids
+    // / geometry follow from the cell index in the fast kernels (no mesh-table loads)
+    if (axis) {
+      const int n = (int)std::lround(std::cbrt((double)mesh.ncells));
+      bool uni = (long long)n * n * n == mesh.ncells;
+      const double ih0 = g[0];
+      for (int c = 0; c < mesh.ncells && uni; ++c) {
+        const double* r = &g[(size_t)c * st];
+        for (int a = 0; a < 3 && uni; ++a) uni = std::abs(r[a * 3 + a] - ih0) <= 1e-13 * ih0;
+        for (int f = 0; f < 6 && uni; ++f) {
+          const int d = f >> 1, s = f & 1;
+          const int co = d == 0 ? c % n : (d == 1 ? (c / n) % n : c / (n * n));
+          const int stride = d == 0 ? 1 : (d == 1 ? n : n * n);
+          const int want = s == 0 ? (co == 0 ? -1 - f : c - stride) : (co == n - 1 ? -1 - f : c + stride);
+          uni = mesh.nbr[(size_t)c * 6 + f] == want;
+          if (uni) {
+            const double pw = mesh.nbr[(size_t)c * 6 + f] >= 0 ? pen[(size_t)c * 6 + f] : 0.0;
+            if (pw != 0.0 && std::abs(pw - pen[1]) > 1e-13 * pen[1]) uni = false;
+          }
+        }
+      }
+      if (uni && n > 1) {
+        dc.ug.n = n;
+        dc.ug.ih = ih0;
+        dc.ug.detJ = g[9];
+        dc.ug.pen_int = pen[1];  // cell 0, face 1 is interior
+        dc.ug.pen_bdry = pen[0];  // cell 0, face 0 is on the boundary
+      }
+    }
   } else {
     const int rules[3] = {ku + 1, ku + 2, kp + 2};
     for (int Q : rules) {

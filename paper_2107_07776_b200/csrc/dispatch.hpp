@@ -42,10 +42,20 @@ struct RhsArgs {
   const double* gtab = nullptr;  // [n_bface][NQF(rule k+2)][DIM], reference boundary-face order
 };
 
+// Uniform structured (generate_cartesian, lexicographic cells, equal h): neighbours,
+// boundary ids and geometry follow from the cell index, so the fast kernels need
+// no mesh-table loads (n == 0: use the tables).
+struct UniformGrid {
+  int n = 0;
+  double ih = 0.0, detJ = 0.0, pen_int = 0.0, pen_bdry = 0.0;
+  unsigned long long outlet_mask = 0;
+};
+
 struct DevCtx {
   int dim = 0, ku = 0, kp = 0, ncells = 0;
   bool affine = true;
   bool axis = false;  // affine with diagonal Jinv on every cell (fast_axis.cuh)
+  UniformGrid ug;
   MeshArgs mesh;
   const double* aff = nullptr;
   const double* qcell[kMaxRule] = {};

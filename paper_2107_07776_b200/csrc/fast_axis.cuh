@@ -27,6 +27,8 @@
 // use an odd x-pitch so line accesses are bank-conflict free.
 #pragma once
 
+#include <type_traits>
+
 #include "dg_common.cuh"
 #include "dispatch.hpp"
 
@@ -80,6 +82,9 @@ struct CellInfo {
   double ihn[6];   // neighbour's 1/h_d across each face
   int nb[6];       // neighbour cell, or -1 - boundary id
   int type[6];     // 0 interior, 1 dirichlet, 2 outlet
+  // branch-free SIP face terms (see face_coefs):  F = cgs gs + cgo go + cus us + cuo uo,
+  // GT = gus us + guo uo  (gs / go: own / neighbour reference normal derivative)
+  double fc[6][6];
 };
 constexpr int kInfoDoubles = (sizeof(CellInfo) + 7) / 8;
 
@@ -108,15 +113,43 @@ __device__ __forceinline__ void load_info(CellInfo& ci, const MeshArgs& m, const
   }
 }
 
+__device__ __forceinline__ int uniform_nbr(const UniformGrid& g, int cell, int f) {
+  const int n = g.n, d = f >> 1, s = f & 1;
+  const int co = d == 0 ? cell % n : (d == 1 ? (cell / n) % n : cell / (n * n));
+  const int stride = d == 0 ? 1 : (d == 1 ? n : n * n);
+  if (s == 0) return co == 0 ? -1 - f : cell - stride;
+  return co == n - 1 ? -1 - f : cell + stride;
+}
+template <bool UNI>
+__device__ __forceinline__ int cell_nbr(const MeshArgs& m, const UniformGrid& g, int cell, int f) {
+  if (UNI) return uniform_nbr(g, cell, f);
+  return m.nbr[(size_t)cell * 6 + f];
+}
+
 // Parallel fill of the CellInfo records of nc cells: one thread per (cell, slot),
 // slot 0..5 = faces, slot 6 = cell geometry (independent L2 loads in flight together).
-template <int TT>
+template <int TT, bool UNI>
 __device__ __forceinline__ void load_info_par(double* base, int per, int off, int nc, const MeshArgs& m,
-                                              const double* __restrict__ aff, int c0, double sfac) {
+                                              const UniformGrid& g, const double* __restrict__ aff, int c0,
+                                              double sfac) {
   for (int idx = threadIdx.x; idx < nc * 7; idx += TT) {
     const int c = idx / 7, f = idx - c * 7;
     CellInfo& ci = *reinterpret_cast<CellInfo*>(base + c * per + off);
     const int cell = c0 + c;
+    if (UNI) {  // no memory traffic: everything follows from the cell index
+      if (f == 6) {
+        ci.ih[0] = ci.ih[1] = ci.ih[2] = g.ih;
+        ci.detJ = g.detJ;
+        ci.A[0] = ci.A[1] = ci.A[2] = g.detJ * g.ih;
+      } else {
+        const int nb = uniform_nbr(g, cell, f);
+        ci.nb[f] = nb;
+        ci.pen[f] = sfac * (nb >= 0 ? g.pen_int : g.pen_bdry);
+        ci.ihn[f] = nb >= 0 ? g.ih : 0.0;
+        ci.type[f] = nb >= 0 ? 0 : (((g.outlet_mask >> f) & 1ull) ? 2 : 1);
+      }
+      continue;
+    }
     if (f == 6) {
       const double* r = aff + (size_t)cell * kAffStride3;
       const double i0 = r[0], i1 = r[4], i2 = r[8], dj = r[9];
@@ -146,12 +179,72 @@ __device__ __forceinline__ void load_info_par(double* base, int per, int off, in
   }
 }
 
+// Branch-free coefficients of the 1D SIP face terms (forms.cpp:196-213 interior,
+// :232-240 / :481-490 boundary), per face of one cell; `dirichlet` selects whether
+// non-interior faces carry Dirichlet-type terms (outlets never do when
+// outlet_natural).
+__device__ __forceinline__ void face_coefs(CellInfo& ci, int f, bool dirichlet, bool outlet_natural) {
+  const int d = f >> 1, s = f & 1;
+  const double ih = ci.ih[d];
+  const double sg = s ? -1.0 : 1.0;  // right face: -1/2 (...) ; left face: +1/2 (...)
+  double* c = ci.fc[f];
+  for (int i = 0; i < 6; ++i) c[i] = 0.0;
+  const int ty = ci.type[f];
+  if (ty == 0) {
+    c[0] = 0.5 * sg * ih;
+    c[1] = 0.5 * sg * ci.ihn[f];
+    c[2] = ci.pen[f];
+    c[3] = -ci.pen[f];
+    c[4] = -0.5;
+    c[5] = 0.5;
+  } else if (dirichlet && !(ty == 2 && outlet_natural)) {
+    c[0] = sg * ih;
+    c[2] = 2.0 * ci.pen[f];
+    c[4] = -1.0;
+  }
+}
+
 // 8-byte asynchronous global -> shared copy (LDGSTS); many in flight per thread.
 __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Branch-free 1D SIP line operator along compile-time direction D (coefficients from
+// face_coefs); neighbour lines of non-interior faces are multiplied by zero.
+template <int N, int D>
+__device__ __forceinline__ void sip_line_bf(const FTab<N, N>& t, const CellInfo& ci, const double* u,
+                                            const double* uL, const double* uR, double scale, double* out) {
+  const double ih = ci.ih[D], sa = scale * ci.A[D];
+  const double stiff = sa * ih;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) s = fma(t.K[i][l], u[l], s);
+    out[i] = stiff * s;
+  }
+  double gsR = 0.0, goR = 0.0, gsL = 0.0, goL = 0.0;
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    gsR = fma(t.dE[1][l], u[l], gsR);
+    goR = fma(t.dE[0][l], uR[l], goR);
+    gsL = fma(t.dE[0][l], u[l], gsL);
+    goL = fma(t.dE[1][l], uL[l], goL);
+  }
+  const double* cR = ci.fc[2 * D + 1];
+  const double* cL = ci.fc[2 * D];
+  const double FR = cR[0] * gsR + cR[1] * goR + cR[2] * u[N - 1] + cR[3] * uR[0];
+  const double GR = cR[4] * u[N - 1] + cR[5] * uR[0];
+  const double FL = cL[0] * gsL + cL[1] * goL + cL[2] * u[0] + cL[3] * uL[N - 1];
+  const double GL = cL[4] * u[0] + cL[5] * uL[N - 1];
+  out[N - 1] = fma(sa, FR, out[N - 1]);
+  out[0] = fma(sa, FL, out[0]);
+  const double g2R = stiff * GR, g2L = -stiff * GL;
+#pragma unroll
+  for (int i = 0; i < N; ++i) out[i] = fma(t.dE[1][i], g2R, fma(t.dE[0][i], g2L, out[i]));
+}
 
 // 1D SIP line operator along direction d (stiffness + both d-faces), times `scale`.
 // u: own line; uL / uR: neighbour lines across faces 2d / 2d+1 (read only if interior).
@@ -240,8 +333,8 @@ struct SipAxisCfg {
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
 
-template <int KP>
-__global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, const double* __restrict__ aff,
+template <int KP, bool UNI>
+__global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff,
                                                                  double mc, int dir_bdry,
                                                                  const double* __restrict__ x,
                                                                  double* __restrict__ y) {
@@ -262,7 +355,7 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, cons
     const int c = idx / NB, i = idx - c * NB;
     cp_async8(CELL(c) + G::O_U + P::idx(i % N, (i / N) % N, i / NF), x + (size_t)(c0 + c) * NB + i);
   }
-  load_info_par<TT>(sm, PER, G::O_INFO, nc, m, aff, c0, sfac);
+  load_info_par<TT, UNI>(sm, PER, G::O_INFO, nc, m, ug, aff, c0, sfac);
   cp_async_wait_all();
   __syncthreads();
   // the scalar operator ignores outlet ids: all boundary faces are natural, or all
@@ -380,7 +473,8 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, cons
 //   mass M x + visc A_sip x     (line-split, exact)
 // + adv C_lf(w) x               (k+2 Gauss rule; sum factorisation)
 // ===========================================================================
-template <int K, int CC, int TH>
+// MODE 0: fused operator; 1: mass + viscous only (writes y); 2: advection only (adds into y)
+template <int K, int CC, int TH, int MODE = 0>
 struct MomAxisCfg {
   static constexpr int N = K + 1, Q = K + 2, NB = N * N * N, NF = N * N, QN = Q * N, QQ = Q * Q;
   using P = Pad<N>;
@@ -398,21 +492,25 @@ struct MomAxisCfg {
   static constexpr int B_END = B_R2 + 6 * QQ * N;
   // face phase (all 6 faces at once): V1 [8 fields][6][Q x N] -> FB [3][6][N x N];  FL [3][6][Q x N]
   static constexpr int F_V1 = 0, F_FB = 0, F_FL = 48 * QN, F_END = F_FL + 18 * QN;
-  static constexpr int WORK = A_END > B_END ? (A_END > F_END ? A_END : F_END) : (B_END > F_END ? B_END : F_END);
+  static constexpr int BF = B_END > F_END ? B_END : F_END;
+  static constexpr int WORK = MODE == 1 ? A_END : (MODE == 2 ? BF : (A_END > BF ? A_END : BF));
   static constexpr int PER = (O_WORK + WORK) | 1;
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
 // default tuning per degree
-template <int K> struct MomAxisTune { static constexpr int C = 6, T = 192; };
-template <> struct MomAxisTune<1> { static constexpr int C = 16, T = 128; };
-template <> struct MomAxisTune<2> { static constexpr int C = 8, T = 192; };
-template <> struct MomAxisTune<3> { static constexpr int C = 3, T = 96; };
+// (SPLIT: launch mass+viscous and advection as two kernels with their own occupancy)
+template <int K, int MODE> struct MomAxisTune { static constexpr int C = 6, T = 192; static constexpr bool SPLIT = false; };
+template <int MODE> struct MomAxisTune<1, MODE> { static constexpr int C = 16, T = 128; static constexpr bool SPLIT = false; };
+template <int MODE> struct MomAxisTune<2, MODE> { static constexpr int C = 8, T = 192; static constexpr bool SPLIT = false; };
+template <> struct MomAxisTune<3, 0> { static constexpr int C = 3, T = 96; static constexpr bool SPLIT = false; };
+template <> struct MomAxisTune<3, 1> { static constexpr int C = 4, T = 128; static constexpr bool SPLIT = true; };
+template <> struct MomAxisTune<3, 2> { static constexpr int C = 3, T = 96; static constexpr bool SPLIT = true; };
 
-template <int K, int CC, int TH>
-__global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, const double* __restrict__ aff, MomCoef co,
+template <int K, int CC, int TH, int MODE, bool UNI>
+__global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff, MomCoef co,
                                                       const double* __restrict__ x, const double* __restrict__ w,
                                                       double* __restrict__ y) {
-  using G = MomAxisCfg<K, CC, TH>;
+  using G = MomAxisCfg<K, CC, TH, MODE>;
   using P = typename G::P;
   constexpr int N = G::N, Q = G::Q, NB = G::NB, NF = G::NF, QN = G::QN, QQ = G::QQ, C = G::C, PER = G::PER;
   constexpr int TT = G::T, CT = G::CT;
@@ -423,7 +521,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, const double* 
   const int nc = min(C, m.ncells - c0);
   const int tid = threadIdx.x;
   const double sfac = (double)((K + 1) * (K + 1));
-  const bool faces = co.adv != 0.0;
+  const bool faces = MODE != 1 && co.adv != 0.0;
 #define CELL(c) (sm + (c) * PER)
 #define WK(c) (sm + (c) * PER + G::O_WORK)
 #define INFO(c) (*reinterpret_cast<CellInfo*>(sm + (c) * PER + G::O_INFO))
@@ -434,80 +532,91 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, const double* 
     const int comp = r / NB, i = r - comp * NB;
     const int pi = comp * CT + P::idx(i % N, (i / N) % N, i / NF);
     cp_async8(CELL(c) + G::O_X + pi, x + (size_t)(c0 + c) * 3 * NB + r);
-    cp_async8(CELL(c) + G::O_W + pi, w + (size_t)(c0 + c) * 3 * NB + r);
+    if (MODE != 1) cp_async8(CELL(c) + G::O_W + pi, w + (size_t)(c0 + c) * 3 * NB + r);
   }
-  load_info_par<TT>(sm, PER, G::O_INFO, nc, m, aff, c0, sfac);
+  // Pass-A neighbour lines: every thread issues the loads of ALL its stage-A items now
+  // (registers), overlapping the cp.async staging and the info loads.  Neighbours
+  // owned by this CTA are read from shared memory later instead.  Items of one
+  // direction: (cell, comp, line) with the line index fastest.
+  const bool passA = MODE != 2 && (co.mass != 0.0 || co.visc != 0.0);
+  constexpr int NID = 3 * NF;                      // items per cell and direction
+  constexpr int MAXJ = (C * NID + TT - 1) / TT;    // items per thread and direction
+  double nbL[3][MAXJ][N], nbR[3][MAXJ][N];
+#pragma unroll
+  for (int d = 0; d < 3; ++d)
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int it = tid + j * TT;
+#pragma unroll
+      for (int l = 0; l < N; ++l) nbL[d][j][l] = nbR[d][j][l] = 0.0;
+      if (passA && it < nc * NID) {
+        const int c = it / NID, r = it - c * NID;
+        const int comp = r / NF, tl = r - comp * NF;
+        const int p = tl % N, q = tl / N;
+        const int nl = cell_nbr<UNI>(m, ug, c0 + c, 2 * d), nr = cell_nbr<UNI>(m, ug, c0 + c, 2 * d + 1);
+        const int gst = d == 0 ? 1 : (d == 1 ? N : NF);
+        const int g0 = comp * NB + (d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q));
+        const bool extL = nl >= 0 && (nl < c0 || nl >= c0 + nc);
+        const bool extR = nr >= 0 && (nr < c0 || nr >= c0 + nc);
+#pragma unroll
+        for (int l = 0; l < N; ++l) {
+          if (extL) nbL[d][j][l] = __ldg(x + (size_t)nl * 3 * NB + g0 + l * gst);
+          if (extR) nbR[d][j][l] = __ldg(x + (size_t)nr * 3 * NB + g0 + l * gst);
+        }
+      }
+    }
+  load_info_par<TT, UNI>(sm, PER, G::O_INFO, nc, m, ug, aff, c0, sfac);
   cp_async_wait_all();
+  __syncthreads();
+  for (int idx = tid; idx < nc * 6; idx += TT) face_coefs(INFO(idx / 6), idx % 6, true, true);
   __syncthreads();
 
   // ------------------------------------------------------------------ pass A: mass + viscous (line split)
-  // A: lines of every direction: S_d (visc) on raw lines, UX = M_x u.  The two
-  //    neighbour lines of the next item are prefetched while the current one computes.
-  {
-    constexpr int NIT = 9 * NF;
-    const int total = nc * NIT;
-    auto gbase = [&](int idx, int& nl, int& nr, int& g0, int& gst) {
-      const int c = idx / NIT, r = idx - c * NIT;
-      const int comp = r / (3 * NF), r2 = r - comp * 3 * NF;
-      const int d = r2 / NF, tl = r2 - d * NF;
-      const int p = tl % N, q = tl / N;
-      nl = INFO(c).nb[2 * d];
-      nr = INFO(c).nb[2 * d + 1];
-      gst = d == 0 ? 1 : (d == 1 ? N : NF);
-      g0 = comp * NB + (d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q));
-    };
-    double pL[N], pR[N];
-    if (tid < total) {
-      int nl, nr, g0, gst;
-      gbase(tid, nl, nr, g0, gst);
+  if (passA) {
+  // A: lines of every direction: S_d (visc) on raw lines (+ neighbour lines), UX = M_x u
+  auto stage_a = [&](auto dtag) {
+    constexpr int d = decltype(dtag)::value;
+    constexpr int st = d == 0 ? 1 : (d == 1 ? P::PX : P::PY);
+    double* sdst = WK(0) + (d == 0 ? G::A_SX : (d == 1 ? G::A_SY : G::A_SZ));
 #pragma unroll
-      for (int l = 0; l < N; ++l) {
-        pL[l] = nl >= 0 ? __ldg(x + (size_t)nl * 3 * NB + g0 + l * gst) : 0.0;
-        pR[l] = nr >= 0 ? __ldg(x + (size_t)nr * 3 * NB + g0 + l * gst) : 0.0;
-      }
-    }
-    for (int idx = tid; idx < total; idx += TT) {
-      double uL[N], uR[N];
+    for (int j = 0; j < MAXJ; ++j) {
+      const int it = tid + j * TT;
+      if (it < nc * NID) {
+        const int c = it / NID, r = it - c * NID;
+        const int comp = r / NF, tl = r - comp * NF;
+        const int p = tl % N, q = tl / N;
+        const CellInfo& ci = INFO(c);
+        const int b0 = comp * CT + (d == 0 ? P::idx(0, p, q) : (d == 1 ? P::idx(p, 0, q) : P::idx(p, q, 0)));
+        double u[N], o[N], uL[N], uR[N];
+        const double* us = CELL(c) + G::O_X + b0;
 #pragma unroll
-      for (int l = 0; l < N; ++l) {
-        uL[l] = pL[l];
-        uR[l] = pR[l];
-      }
-      if (idx + TT < total) {
-        int nl, nr, g0, gst;
-        gbase(idx + TT, nl, nr, g0, gst);
+        for (int l = 0; l < N; ++l) u[l] = us[l * st];
+        const int nl = ci.nb[2 * d], nr = ci.nb[2 * d + 1];
+        const bool inL = nl >= c0 && nl < c0 + nc, inR = nr >= c0 && nr < c0 + nc;
 #pragma unroll
         for (int l = 0; l < N; ++l) {
-          pL[l] = nl >= 0 ? __ldg(x + (size_t)nl * 3 * NB + g0 + l * gst) : 0.0;
-          pR[l] = nr >= 0 ? __ldg(x + (size_t)nr * 3 * NB + g0 + l * gst) : 0.0;
+          uL[l] = inL ? CELL(nl - c0)[G::O_X + b0 + l * st] : nbL[d][j][l];
+          uR[l] = inR ? CELL(nr - c0)[G::O_X + b0 + l * st] : nbR[d][j][l];
         }
-      }
-      const int c = idx / NIT, r = idx - c * NIT;
-      const int comp = r / (3 * NF), r2 = r - comp * 3 * NF;
-      const int d = r2 / NF, tl = r2 - d * NF;
-      const int p = tl % N, q = tl / N;
-      const CellInfo& ci = INFO(c);
-      const int st = d == 0 ? 1 : (d == 1 ? P::PX : P::PY);
-      const int b0 = d == 0 ? P::idx(0, p, q) : (d == 1 ? P::idx(p, 0, q) : P::idx(p, q, 0));
-      double u[N], o[N];
-      const double* us = CELL(c) + G::O_X + comp * CT + b0;
+        sip_line_bf<N, d>(ta, ci, u, uL, uR, co.visc, o);
+        double* so = sdst + c * PER + b0;
 #pragma unroll
-      for (int l = 0; l < N; ++l) u[l] = us[l * st];
-      sip_line<N>(ta, ci, d, u, uL, uR, true, co.visc, o);
-      double* so = WK(c) + (d == 0 ? G::A_SX : (d == 1 ? G::A_SY : G::A_SZ)) + comp * CT + b0;
+        for (int l = 0; l < N; ++l) so[l * st] = o[l];
+        if (d == 0) {
 #pragma unroll
-      for (int l = 0; l < N; ++l) so[l * st] = o[l];
-      if (d == 0) {
+          for (int i = 0; i < N; ++i) {
+            double sacc = 0.0;
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          double s = 0.0;
-#pragma unroll
-          for (int l = 0; l < N; ++l) s = fma(ta.M[i][l], u[l], s);
-          WK(c)[G::A_UX + comp * CT + b0 + i] = s;
+            for (int l = 0; l < N; ++l) sacc = fma(ta.M[i][l], u[l], sacc);
+            WK(c)[G::A_UX + b0 + i] = sacc;
+          }
         }
       }
     }
-  }
+  };
+  stage_a(std::integral_constant<int, 0>{});
+  stage_a(std::integral_constant<int, 1>{});
+  stage_a(std::integral_constant<int, 2>{});
   __syncthreads();
   // B: x-lines in place: SY <- M_x SY, SZ <- M_x SZ
   for (int idx = tid; idx < nc * 3 * NF; idx += TT) {
@@ -577,7 +686,13 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, const double* 
   }
   __syncthreads();
 
+  } else {
+    for (int idx = tid; idx < nc * 3 * CT; idx += TT) CELL(idx / (3 * CT))[G::O_OUT + idx % (3 * CT)] = 0.0;
+    __syncthreads();
+  }
+
   // ------------------------------------------------------------------ pass B cell (advection, rule k+2)
+  if (faces) {
   // S4: x-lines for 6 fields (u0..2, w0..2): XB[f][(j,k)][qx]
   for (int idx = tid; idx < nc * 6 * NF; idx += TT) {
     const int c = idx / (6 * NF), r = idx - c * 6 * NF;  // r = f*NF + jk
@@ -716,6 +831,8 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, const double* 
   }
   __syncthreads();
 
+  }
+
   // ------------------------------------------------------------------ LF advective faces, all 6 at once
   if (faces) {
     // F1: traces of u (3 comps, own + neighbour) and w_a (own + neighbour) on face-node line q,
@@ -846,6 +963,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, const double* 
         if (ii[a] == N - 1) v += fb[(2 * a + 1) * NF + t];
       }
     }
+    if (MODE == 2) v += y[(size_t)(c0 + c) * 3 * NB + r];
     y[(size_t)(c0 + c) * 3 * NB + r] = v;
   }
 #undef CELL

@@ -30,24 +30,45 @@ template <int KP>
 static cudaError_t run_sip_axis(const DevCtx& c, double mc, int dir, const double* x, double* y) {
   using G = SipAxisCfg<KP>;
   cudaError_t e = ensure_ftab<KP + 1, KP + 1>();
-  if (e == cudaSuccess) e = set_smem(k_sip_axis<KP>, G::SMEM);
   if (e != cudaSuccess) return e;
   const int grid = (c.ncells + G::C - 1) / G::C;
-  k_sip_axis<KP><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.aff, mc, dir, x, y);
+  if (c.ug.n > 0) {
+    if ((e = set_smem(k_sip_axis<KP, true>, G::SMEM)) != cudaSuccess) return e;
+    k_sip_axis<KP, true><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, mc, dir, x, y);
+  } else {
+    if ((e = set_smem(k_sip_axis<KP, false>, G::SMEM)) != cudaSuccess) return e;
+    k_sip_axis<KP, false><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, mc, dir, x, y);
+  }
+  return cudaGetLastError();
+}
+
+template <int K, int MODE>
+static cudaError_t launch_momentum_axis(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y) {
+  constexpr int CC = MomAxisTune<K, MODE>::C, TH = MomAxisTune<K, MODE>::T;
+  using G = MomAxisCfg<K, CC, TH, MODE>;
+  cudaError_t e;
+  const int grid = (c.ncells + G::C - 1) / G::C;
+  if (c.ug.n > 0) {
+    if ((e = set_smem(k_momentum_axis<K, CC, TH, MODE, true>, G::SMEM)) != cudaSuccess) return e;
+    k_momentum_axis<K, CC, TH, MODE, true><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, co, x, w, y);
+  } else {
+    if ((e = set_smem(k_momentum_axis<K, CC, TH, MODE, false>, G::SMEM)) != cudaSuccess) return e;
+    k_momentum_axis<K, CC, TH, MODE, false><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, co, x, w, y);
+  }
   return cudaGetLastError();
 }
 
 template <int K>
 static cudaError_t run_momentum_axis(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y) {
-  constexpr int CC = MomAxisTune<K>::C, TH = MomAxisTune<K>::T;
-  using G = MomAxisCfg<K, CC, TH>;
   cudaError_t e = ensure_ftab<K + 1, K + 2>();
   if (e == cudaSuccess) e = ensure_ftab<K + 1, K + 1>();
-  if (e == cudaSuccess) e = set_smem(k_momentum_axis<K, CC, TH>, G::SMEM);
   if (e != cudaSuccess) return e;
-  const int grid = (c.ncells + G::C - 1) / G::C;
-  k_momentum_axis<K, CC, TH><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.aff, co, x, w, y);
-  return cudaGetLastError();
+  if (MomAxisTune<K, 0>::SPLIT && co.adv != 0.0 && (co.mass != 0.0 || co.visc != 0.0)) {
+    e = launch_momentum_axis<K, 1>(c, co, w, x, y);   // mass + viscous -> y
+    if (e != cudaSuccess) return e;
+    return launch_momentum_axis<K, 2>(c, co, w, x, y);  // + advection
+  }
+  return launch_momentum_axis<K, 0>(c, co, w, x, y);
 }
 
 cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, double* y) {
