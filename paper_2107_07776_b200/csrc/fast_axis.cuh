@@ -478,7 +478,7 @@ template <int K, int CC, int TH, int MODE = 0>
 struct MomAxisCfg {
   static constexpr int N = K + 1, Q = K + 2, NB = N * N * N, NF = N * N, QN = Q * N, QQ = Q * Q;
   using P = Pad<N>;
-  static constexpr int CT = P::CT;
+  static constexpr int CT = P::CT | 1;  // odd component stride (bank-conflict-free field interleave)
   static constexpr int C = CC;   // cells per CTA
   static constexpr int T = TH;   // threads per CTA
   // persistent per-cell regions
@@ -693,41 +693,37 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
 
   // ------------------------------------------------------------------ pass B cell (advection, rule k+2)
   if (faces) {
-  // S4: x-lines for 6 fields (u0..2, w0..2): XB[f][(j,k)][qx]
-  for (int idx = tid; idx < nc * 6 * NF; idx += TT) {
-    const int c = idx / (6 * NF), r = idx - c * 6 * NF;  // r = f*NF + jk
-    const int f = r / NF, jk = r - f * NF;
-    const double* in = CELL(c) + (f < 3 ? G::O_X + f * CT : G::O_W + (f - 3) * CT) + P::idx(0, jk % N, jk / N);
-    double v[N];
+  // S45: xy-planes of the 6 fields (u0..2, w0..2) at z-layer k: B along x then y, in
+  //      registers  -> YB[f][k][qy][qx]
+  for (int idx = tid; idx < nc * 6 * N; idx += TT) {
+    const int c = idx / (6 * N), r = idx - c * 6 * N;
+    const int f = r / N, k = r - f * N;
+    const double* in = CELL(c) + (f < 3 ? G::O_X + f * CT : G::O_W + (f - 3) * CT) + P::idx(0, 0, k);
+    double pl[N][N];  // [j][i]
 #pragma unroll
-    for (int l = 0; l < N; ++l) v[l] = in[l];
-    double* o = WK(c) + G::B_R1 + r * Q;
+    for (int j = 0; j < N; ++j)
 #pragma unroll
-    for (int qx = 0; qx < Q; ++qx) {
-      double s = 0.0;
+      for (int i = 0; i < N; ++i) pl[j][i] = in[i + P::PX * j];
+    double px[Q][N];  // [qx][j]
 #pragma unroll
-      for (int l = 0; l < N; ++l) s = fma(tq.B[qx][l], v[l], s);
-      o[qx] = s;
-    }
-  }
-  __syncthreads();
-  // S5: y-lines: YB[f][k][qy][qx]
-  for (int idx = tid; idx < nc * 6 * QN; idx += TT) {
-    const int c = idx / (6 * QN), r = idx - c * 6 * QN;
-    const int f = r / QN, rk = r - f * QN;
-    const int qx = rk % Q, k = rk / Q;
-    const double* in = WK(c) + G::B_R1 + f * Q * NF + qx + Q * N * k;
-    double v[N];
+    for (int qx = 0; qx < Q; ++qx)
 #pragma unroll
-    for (int l = 0; l < N; ++l) v[l] = in[Q * l];
-    double* o = WK(c) + G::B_R2 + f * QQ * N + qx + QQ * k;
+      for (int j = 0; j < N; ++j) {
+        double sacc = 0.0;
 #pragma unroll
-    for (int qy = 0; qy < Q; ++qy) {
-      double s = 0.0;
+        for (int i = 0; i < N; ++i) sacc = fma(tq.B[qx][i], pl[j][i], sacc);
+        px[qx][j] = sacc;
+      }
+    double* o = WK(c) + G::B_R2 + f * QQ * N + QQ * k;
 #pragma unroll
-      for (int l = 0; l < N; ++l) s = fma(tq.B[qy][l], v[l], s);
-      o[Q * qy] = s;
-    }
+    for (int qy = 0; qy < Q; ++qy)
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) sacc = fma(tq.B[qy][j], px[qx][j], sacc);
+        o[qx + Q * qy] = sacc;
+      }
   }
   __syncthreads();
   // S6: fused z: evaluate 6 columns, pointwise advective flux, z-integration of the 3x3 gradient tests
@@ -778,59 +774,46 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
     }
   }
   __syncthreads();
-  // S7: y-lines: SA = B^T TZ + D^T TY, SB = B^T TX   -> [comp][l][j][qx]
-  for (int idx = tid; idx < nc * 3 * QN; idx += TT) {
-    const int c = idx / (3 * QN), r = idx - c * 3 * QN;
-    const int comp = r / QN, rl = r - comp * QN;
-    const int qx = rl % Q, l = rl / Q;
-    const double* tzp = WK(c) + G::B_R1 + comp * 3 * QQ * N + qx + QQ * l;
-    double vz[Q], vy[Q], vx[Q];
+  // S78: per (component, z-layer l): y- then x-integration of the three gradient tests,
+  //      qx by qx in registers, accumulated into OUT
+  for (int idx = tid; idx < nc * 3 * N; idx += TT) {
+    const int c = idx / (3 * N), r = idx - c * 3 * N;
+    const int comp = r / N, l = r - comp * N;
+    const double* tp = WK(c) + G::B_R1 + comp * 3 * QQ * N + QQ * l;
+    double acc[N][N];  // [j][i]
 #pragma unroll
-    for (int qy = 0; qy < Q; ++qy) {
-      vz[qy] = tzp[Q * qy];
-      vy[qy] = tzp[QQ * N + Q * qy];
-      vx[qy] = tzp[2 * QQ * N + Q * qy];
-    }
-    double* sa = WK(c) + G::B_R2 + comp * 2 * QN * N + qx + QN * l;
+    for (int j = 0; j < N; ++j)
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-      double a = 0.0, b = 0.0;
-#pragma unroll
-      for (int qy = 0; qy < Q; ++qy) {
-        a = fma(tq.B[qy][j], vz[qy], a);
-        a = fma(tq.D[qy][j], vy[qy], a);
-        b = fma(tq.B[qy][j], vx[qy], b);
-      }
-      sa[Q * j] = a;
-      sa[QN * N + Q * j] = b;
-    }
-  }
-  __syncthreads();
-  // S8: x-lines: OUT += B^T SA + D^T SB
-  for (int idx = tid; idx < nc * 3 * NF; idx += TT) {
-    const int c = idx / (3 * NF), r = idx - c * 3 * NF;
-    const int comp = r / NF, jl = r - comp * NF;
-    const double* sa = WK(c) + G::B_R2 + comp * 2 * QN * N + Q * jl;
-    double va[Q], vb[Q];
+      for (int i = 0; i < N; ++i) acc[j][i] = 0.0;
 #pragma unroll
     for (int qx = 0; qx < Q; ++qx) {
-      va[qx] = sa[qx];
-      vb[qx] = sa[QN * N + qx];
-    }
-    double* o = CELL(c) + G::O_OUT + comp * CT + P::idx(0, jl % N, jl / N);
+      double vz[Q], vy[Q], vx[Q];
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double s = o[i];
-#pragma unroll
-      for (int qx = 0; qx < Q; ++qx) {
-        s = fma(tq.B[qx][i], va[qx], s);
-        s = fma(tq.D[qx][i], vb[qx], s);
+      for (int qy = 0; qy < Q; ++qy) {
+        vz[qy] = tp[qx + Q * qy];
+        vy[qy] = tp[QQ * N + qx + Q * qy];
+        vx[qy] = tp[2 * QQ * N + qx + Q * qy];
       }
-      o[i] = s;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double sa = 0.0, sb = 0.0;
+#pragma unroll
+        for (int qy = 0; qy < Q; ++qy) {
+          sa = fma(tq.B[qy][j], vz[qy], sa);
+          sa = fma(tq.D[qy][j], vy[qy], sa);
+          sb = fma(tq.B[qy][j], vx[qy], sb);
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) acc[j][i] = fma(tq.B[qx][i], sa, fma(tq.D[qx][i], sb, acc[j][i]));
+      }
     }
+    double* o = CELL(c) + G::O_OUT + comp * CT + P::idx(0, 0, l);
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) o[i + P::PX * j] += acc[j][i];
   }
   __syncthreads();
-
   }
 
   // ------------------------------------------------------------------ LF advective faces, all 6 at once
