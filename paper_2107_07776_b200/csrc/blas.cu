@@ -173,6 +173,195 @@ __global__ void k_sum_parts(int nparts, int nv, const double* __restrict__ parti
   }
 }
 
+// ---------------------------------------------------------------- device-resident CG
+__global__ void k_cg_begin_part(size_t n, const double* __restrict__ r, const double* __restrict__ inv,
+                                double* __restrict__ z, double* __restrict__ partial) {
+  double acc[1] = {0.0};
+  GRID_STRIDE(i, n) {
+    const double ri = r[i];
+    const double zi = inv ? ri * inv[i] : ri;
+    z[i] = zi;
+    acc[0] = fma(ri, zi, acc[0]);
+  }
+  block_reduce_store<1>(acc, partial);
+}
+__device__ __forceinline__ double block_sum_parts(int nparts, const double* __restrict__ partial) {
+  __shared__ double red[kBlasThreads / 32];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) a += partial[i];
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  double b = 0.0;
+  if (threadIdx.x < 32) {
+    b = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  return b;  // valid in thread 0
+}
+__global__ void k_cg_begin_final(int nparts, const double* __restrict__ partial, CgState* st) {
+  const double rho = block_sum_parts(nparts, partial);
+  if (threadIdx.x == 0) {
+    st->rho = rho;
+    st->first = 1;
+    st->done = 0;
+    st->err = 0;
+    if (rho == 0.0) {
+      st->err = 3;  // DGB_E_BREAKDOWN
+      st->done = 3;
+    }
+  }
+}
+__global__ void k_cg_dir(size_t n, const double* __restrict__ z, double* __restrict__ p, const CgState* st) {
+  if (st->done) return;
+  const int first = st->first;
+  const double beta = first ? 0.0 : st->rho / st->rho_old;
+  GRID_STRIDE(i, n) p[i] = first ? z[i] : fma(beta, p[i], z[i]);
+}
+__global__ void k_cg_pq_part(size_t n, const double* __restrict__ p, const double* __restrict__ q,
+                             double* __restrict__ partial, const CgState* st) {
+  if (st->done) return;
+  double acc[1] = {0.0};
+  GRID_STRIDE(i, n) acc[0] = fma(p[i], q[i], acc[0]);
+  block_reduce_store<1>(acc, partial);
+}
+__global__ void k_cg_alpha_final(int nparts, const double* __restrict__ partial, CgState* st) {
+  if (st->done) return;
+  const double pq = block_sum_parts(nparts, partial);
+  if (threadIdx.x == 0) {
+    if (pq <= 0.0) {
+      st->err = 4;  // DGB_E_NOT_SPD
+      st->done = 3;
+    } else {
+      st->alpha = st->rho / pq;
+    }
+  }
+}
+__global__ void k_cg_upd_part(size_t n, const double* __restrict__ p, const double* __restrict__ q,
+                              double* __restrict__ x, double* __restrict__ r, const double* __restrict__ inv,
+                              double* __restrict__ z, double* __restrict__ partial, const CgState* st) {
+  if (st->done) return;
+  const double a = st->alpha;
+  double acc[2] = {0.0, 0.0};
+  GRID_STRIDE(i, n) {
+    x[i] = fma(a, p[i], x[i]);
+    const double ri = fma(-a, q[i], r[i]);
+    r[i] = ri;
+    const double zi = inv ? ri * inv[i] : ri;
+    z[i] = zi;
+    acc[0] = fma(ri, ri, acc[0]);
+    acc[1] = fma(ri, zi, acc[1]);
+  }
+  block_reduce_store<2>(acc, partial);
+}
+__global__ void k_cg_upd_final(int nparts, const double* __restrict__ partial, CgState* st,
+                               double* __restrict__ hist) {
+  if (st->done) return;
+  const double rr = block_sum_parts(nparts, partial);
+  __syncthreads();
+  const double rz = block_sum_parts(nparts, partial + nparts);
+  if (threadIdx.x == 0) {
+    const int it = st->iter + 1;
+    st->iter = it;
+    const double rn = sqrt(rr);
+    st->rnorm = rn;
+    hist[it - 1] = rn;
+    st->first = 0;
+    st->rho_old = st->rho;
+    st->rho = rz;
+    if (rn <= st->tol) {
+      st->done = 1;  // converged: back to the outer true-residual check
+    } else if (it >= st->max_iter) {
+      st->done = 2;  // budget exhausted
+    } else if (rz == 0.0) {
+      st->err = 3;  // next iteration's "<r,z> = 0" breakdown (krylov.cpp:77-78)
+      st->done = 3;
+    }
+  }
+}
+__global__ void k_mgs_part_dev(size_t n, const double* __restrict__ hp, const double* __restrict__ vi,
+                               double* __restrict__ w, const double* __restrict__ vnext,
+                               double* __restrict__ partial) {
+  const double h = *hp;
+  double acc[1] = {0.0};
+  const bool self = (vnext == w);
+  GRID_STRIDE(i, n) {
+    const double wi = fma(-h, vi[i], w[i]);
+    w[i] = wi;
+    acc[0] = fma(wi, self ? wi : vnext[i], acc[0]);
+  }
+  block_reduce_store<1>(acc, partial);
+}
+
+// ---------------------------------------------------------------- one-reduce MGS
+struct GsPack {
+  const double* u[kGsChunk];
+};
+// NV basis vectors per pass, compile-time so that every load of an element
+// iteration is issued before the first FMA (a runtime bound serialises them)
+template <int NV>
+__global__ void __launch_bounds__(kBlasThreads) k_gs_dots_part(size_t n, GsPack P, const double* __restrict__ w,
+                                                             const double* __restrict__ uk, int nl,
+                                                             double* __restrict__ partial) {
+  double acc[2 * NV];
+#pragma unroll
+  for (int j = 0; j < 2 * NV; ++j) acc[j] = 0.0;
+  const double* ub = nl > 0 ? uk : w;  // harmless stand-in when there is no Gram row
+  GRID_STRIDE(i, n) {
+    const double wi = w[i];
+    const double ui = ub[i];
+    double v[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = P.u[j][i];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      acc[j] = fma(v[j], wi, acc[j]);
+      acc[NV + j] = fma(v[j], ui, acc[NV + j]);
+    }
+  }
+  block_reduce_store<2 * NV>(acc, partial);
+}
+__global__ void k_gs_solve(int k, const double* __restrict__ ab, double* __restrict__ L, int ldl,
+                           double* __restrict__ sv, double sk, double* __restrict__ h, double* __restrict__ g) {
+  if (threadIdx.x != 0) return;
+  sv[k] = sk;
+  // row k of the Gram matrix: L[k][j] = <v_k, v_j>, j < k
+  for (int j = 0; j < k; ++j) {
+    const double b = ab[(j / kGsChunk) * 2 * kGsChunk + kGsChunk + (j % kGsChunk)];
+    L[(size_t)k * ldl + j] = sk * sv[j] * b;
+  }
+  for (int j = 0; j <= k; ++j) {
+    double t = sv[j] * ab[(j / kGsChunk) * 2 * kGsChunk + (j % kGsChunk)];
+    for (int i = 0; i < j; ++i) t -= h[i] * L[(size_t)j * ldl + i];
+    h[j] = t;
+    g[j] = t * sv[j];
+  }
+}
+template <int NV>
+__global__ void __launch_bounds__(kBlasThreads) k_gs_update_part(size_t n, GsPack P, const double* __restrict__ g,
+                                                               double* __restrict__ w, int want_norm,
+                                                               double* __restrict__ partial) {
+  double c[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) c[j] = g[j];
+  double acc[1] = {0.0};
+  GRID_STRIDE(i, n) {
+    double v[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = P.u[j][i];
+    double wi = w[i];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) wi = fma(-c[j], v[j], wi);
+    w[i] = wi;
+    acc[0] = fma(wi, wi, acc[0]);
+  }
+  if (want_norm) block_reduce_store<1>(acc, partial);
+}
+__global__ void k_mul_scaled(size_t n, double a, const double* __restrict__ r, const double* __restrict__ d,
+                             double* __restrict__ z) {
+  GRID_STRIDE(i, n) z[i] = d ? a * r[i] * d[i] : a * r[i];
+}
+
 // ---------------------------------------------------------------- launchers
 #define L1(kern, ...)                                              \
   do {                                                             \
@@ -230,6 +419,81 @@ cudaError_t r_precond_dot(cudaStream_t s, size_t n, const double* r, const doubl
                           double* scratch, double* d_out) {
   const int g = blas_grid(n);
   k_precond_dot_part<<<g, kBlasThreads, 0, s>>>(n, r, inv, z, scratch);
+  k_sum_parts<<<1, kBlasThreads, 0, s>>>(g, 1, scratch, d_out, 0);
+  return cudaGetLastError();
+}
+cudaError_t cg_begin(cudaStream_t s, size_t n, const double* r, const double* inv, double* z, double* scratch,
+                     CgState* st) {
+  const int g = blas_grid(n);
+  k_cg_begin_part<<<g, kBlasThreads, 0, s>>>(n, r, inv, z, scratch);
+  k_cg_begin_final<<<1, kBlasThreads, 0, s>>>(g, scratch, st);
+  return cudaGetLastError();
+}
+cudaError_t cg_direction(cudaStream_t s, size_t n, const double* z, double* p, const CgState* st) {
+  k_cg_dir<<<blas_grid(n), kBlasThreads, 0, s>>>(n, z, p, st);
+  return cudaGetLastError();
+}
+cudaError_t cg_alpha(cudaStream_t s, size_t n, const double* p, const double* q, double* scratch, CgState* st) {
+  const int g = blas_grid(n);
+  k_cg_pq_part<<<g, kBlasThreads, 0, s>>>(n, p, q, scratch, st);
+  k_cg_alpha_final<<<1, kBlasThreads, 0, s>>>(g, scratch, st);
+  return cudaGetLastError();
+}
+cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q, double* x, double* r,
+                      const double* inv, double* z, double* scratch, CgState* st, double* hist) {
+  const int g = blas_grid(n);
+  k_cg_upd_part<<<g, kBlasThreads, 0, s>>>(n, p, q, x, r, inv, z, scratch, st);
+  k_cg_upd_final<<<1, kBlasThreads, 0, s>>>(g, scratch, st, hist);
+  return cudaGetLastError();
+}
+cudaError_t gs_dots(cudaStream_t s, size_t n, int nv, const double* const* U, const double* w, const double* uk,
+                    int nl, double* scratch, double* d_ab) {
+  if (nv < 1 || nv > kGsChunk || nl > nv) return cudaErrorInvalidValue;
+  GsPack P{};
+  for (int j = 0; j < nv; ++j) P.u[j] = U[j];
+  const int g = blas_grid(n);
+  switch (nv) {
+#define GS_CASE(NV)                                                               \
+  case NV:                                                                        \
+    k_gs_dots_part<NV><<<g, kBlasThreads, 0, s>>>(n, P, w, uk, nl, scratch);      \
+    k_sum_parts<<<1, kBlasThreads, 0, s>>>(g, NV, scratch, d_ab, 0);              \
+    if (nl > 0) k_sum_parts<<<1, kBlasThreads, 0, s>>>(g, NV, scratch + (size_t)NV * g, d_ab + kGsChunk, 0); \
+    break;
+    GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6) GS_CASE(7) GS_CASE(8)
+    GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12) GS_CASE(13) GS_CASE(14) GS_CASE(15) GS_CASE(16)
+#undef GS_CASE
+  }
+  return cudaGetLastError();
+}
+cudaError_t gs_solve(cudaStream_t s, int k, const double* d_ab, double* L, int ldl, double* d_s, double sk,
+                     double* d_h, double* d_g) {
+  k_gs_solve<<<1, 32, 0, s>>>(k, d_ab, L, ldl, d_s, sk, d_h, d_g);
+  return cudaGetLastError();
+}
+cudaError_t gs_update(cudaStream_t s, size_t n, int nv, const double* const* U, const double* g, double* w,
+                      double* scratch, double* norm_out) {
+  if (nv < 1 || nv > kGsChunk) return cudaErrorInvalidValue;
+  GsPack P{};
+  for (int j = 0; j < nv; ++j) P.u[j] = U[j];
+  const int gr = blas_grid(n);
+  switch (nv) {
+#define GS_CASE(NV)                                                                          \
+  case NV: k_gs_update_part<NV><<<gr, kBlasThreads, 0, s>>>(n, P, g, w, norm_out ? 1 : 0, scratch); break;
+    GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6) GS_CASE(7) GS_CASE(8)
+    GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12) GS_CASE(13) GS_CASE(14) GS_CASE(15) GS_CASE(16)
+#undef GS_CASE
+  }
+  if (norm_out) k_sum_parts<<<1, kBlasThreads, 0, s>>>(gr, 1, scratch, norm_out, 0);
+  return cudaGetLastError();
+}
+cudaError_t v_mul_scaled(cudaStream_t s, size_t n, double a, const double* r, const double* d, double* z) {
+  k_mul_scaled<<<blas_grid(n), kBlasThreads, 0, s>>>(n, a, r, d, z);
+  return cudaGetLastError();
+}
+cudaError_t r_mgs_step_dev(cudaStream_t s, size_t n, const double* h, const double* vi, double* w,
+                           const double* vnext, double* scratch, double* d_out) {
+  const int g = blas_grid(n);
+  k_mgs_part_dev<<<g, kBlasThreads, 0, s>>>(n, h, vi, w, vnext, scratch);
   k_sum_parts<<<1, kBlasThreads, 0, s>>>(g, 1, scratch, d_out, 0);
   return cudaGetLastError();
 }

@@ -51,4 +51,44 @@ cudaError_t r_mgs_step(cudaStream_t s, size_t n, double h, const double* vi, dou
 // sum of nparts partials -> d_out
 cudaError_t r_sum(cudaStream_t s, int nparts, const double* partial, double* d_out);
 
+// ---- device-resident CG (krylov.cpp:69-98 inner loop without host round trips)
+struct CgState {
+  double rho, rho_old, alpha, rnorm, tol;
+  int iter, max_iter, done, err, first;
+};
+// first iteration of an inner loop: z = M r, rho = <r,z>; sets first = 1, done = 0
+cudaError_t cg_begin(cudaStream_t s, size_t n, const double* r, const double* inv, double* z, double* scratch,
+                     CgState* st);
+// p = z (first) or z + (rho/rho_old) p
+cudaError_t cg_direction(cudaStream_t s, size_t n, const double* z, double* p, const CgState* st);
+// alpha = rho / <p,q>  (flags NOT_SPD)
+cudaError_t cg_alpha(cudaStream_t s, size_t n, const double* p, const double* q, double* scratch, CgState* st);
+// x += alpha p, r -= alpha q, z = M r, rnorm -> history, convergence / breakdown flags
+cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q, double* x, double* r,
+                      const double* inv, double* z, double* scratch, CgState* st, double* hist);
+// MGS step with the projection read from device memory: w -= (*h) v_i ; *out = <w, v_next>
+cudaError_t r_mgs_step_dev(cudaStream_t s, size_t n, const double* h, const double* vi, double* w,
+                           const double* vnext, double* scratch, double* d_out);
+
+// ---- one-reduce modified Gram-Schmidt for GMRES (krylov.cpp:140-160 restated).
+// The basis is stored unnormalised, v_j = s_j U_j.  MGS's projections follow
+// from one pass of dot products through the lower-triangular Gram correction
+//   h_j = <w, v_j> - sum_{i<j} h_i <v_i, v_j>,
+// which is MGS in exact arithmetic; the second pass applies w -= sum_j h_j v_j
+// and yields |w|^2.  2k+5 vector passes per Arnoldi step instead of 4(k+1).
+constexpr int kGsChunk = 16;
+// a_j = <w, U_j> (j < nv) and b_j = <uk, U_j> (j < nl) for one chunk of <= 16 vectors
+// -> d_ab[0..16) = a, d_ab[16..32) = b
+cudaError_t gs_dots(cudaStream_t s, size_t n, int nv, const double* const* U, const double* w, const double* uk,
+                    int nl, double* scratch, double* d_ab);
+// single-thread solve: row k of L from b, h (MGS projections) and g_j = h_j s_j
+//   d_ab: per chunk 32 values (a, b); L: (ldl x ldl) device matrix; d_s[k] = sk
+cudaError_t gs_solve(cudaStream_t s, int k, const double* d_ab, double* L, int ldl, double* d_s, double sk,
+                     double* d_h, double* d_g);
+// w -= sum_{j<nv} g_j U_j ; if norm_out: *norm_out = |w|^2
+cudaError_t gs_update(cudaStream_t s, size_t n, int nv, const double* const* U, const double* g, double* w,
+                      double* scratch, double* norm_out);
+// z = a * r * d (d may be null: z = a r)
+cudaError_t v_mul_scaled(cudaStream_t s, size_t n, double a, const double* r, const double* d, double* z);
+
 }  // namespace dgb

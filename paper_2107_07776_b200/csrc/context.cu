@@ -3,6 +3,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "blas.cuh"
@@ -43,6 +46,11 @@ Context::~Context() {
   for (auto& s : slots_) cudaFree(s.first);
   for (double* v : gm_basis_) cudaFree(v);
   if (h_res_) cudaFreeHost(h_res_);
+  if (h_cg_) cudaFreeHost(h_cg_);
+  if (h_gm_) cudaFreeHost(h_gm_);
+  if (d_hist_) cudaFree(d_hist_);
+  for (cudaEvent_t e : poll_ev_)
+    if (e) cudaEventDestroy(e);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (own_stream) cudaStreamDestroy(own_stream);
@@ -102,7 +110,8 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
   d_partial_ = (double*)dalloc(4096 * sizeof(double));
   d_res_ = (double*)dalloc(64 * sizeof(double));
   d_bad_ = (long long*)dalloc(sizeof(long long));
-  if (!d_nbr || !d_pen || !d_bslot || !d_bct || !d_partial_ || !d_res_ || !d_bad_) {
+  d_cg_ = (CgState*)dalloc(sizeof(CgState));
+  if (!d_nbr || !d_pen || !d_bslot || !d_bct || !d_partial_ || !d_res_ || !d_bad_ || !d_cg_) {
     e = "out of device memory";
     return DGB_E_CUDA;
   }
@@ -110,7 +119,10 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
   cudaMemcpy(d_pen, pen.data(), nslot * sizeof(double), cudaMemcpyHostToDevice);
   cudaMemcpy(d_bslot, bslot.data(), nslot * sizeof(int), cudaMemcpyHostToDevice);
   cudaMemcpy(d_bct, bctype_h, sizeof(bctype_h), cudaMemcpyHostToDevice);
-  if (cudaHostAlloc((void**)&h_res_, 64 * sizeof(double), cudaHostAllocDefault) != cudaSuccess) {
+  if (cudaHostAlloc((void**)&h_res_, 64 * sizeof(double), cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc((void**)&h_cg_, 3 * sizeof(CgState), cudaHostAllocDefault) != cudaSuccess ||
+      cudaEventCreateWithFlags(&poll_ev_[0], cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&poll_ev_[1], cudaEventDisableTiming) != cudaSuccess) {
     e = "pinned alloc failed";
     return DGB_E_CUDA;
   }
@@ -423,37 +435,70 @@ int Context::cg(const dgb_operator& op, const dgb_solver_settings& s, const doub
     if (iter >= s.max_iter)
       return fail(DGB_E_NO_CONVERGENCE, "cg: no convergence in " + std::to_string(s.max_iter) +
                                             " iterations (residual " + std::to_string(rnorm) + ")");
-    double rho;
-    launches += 2;
-    CK(r_precond_dot(st, n, r, inv, z, d_partial_, d_res_));
-    OK(host_scalars(1, &rho));
-    double rho_old = 0.0;
-    bool first = true;
-    while (iter < s.max_iter) {
-      if (rho == 0.0) return fail(DGB_E_BREAKDOWN, "cg: breakdown, <r,z> = 0");
-      ++launches;
-      if (first) {
-        CK(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-        first = false;
-      } else {
-        CK(v_axpby(st, n, 1.0, z, rho / rho_old, p));
-      }
-      rho_old = rho;
-      OK(apply_op(op, p, q));
-      double pq;
-      OK(dot(n, p, q, &pq));
-      if (pq <= 0.0) return fail(DGB_E_NOT_SPD, "cg: operator not positive definite, <p,Ap> <= 0");
-      const double alpha = rho / pq;
-      launches += 2;
-      CK(r_cg_update(st, n, alpha, p, q, x, r, inv, z, d_partial_, d_res_));
-      double rz[2];
-      OK(host_scalars(2, rz));
-      ++iter;
-      rnorm = std::sqrt(rz[0]);
-      out.history.push_back(rnorm);
-      if (rnorm <= tol) break;
-      rho = rz[1];
+    // Inner loop on the device: the CG scalars live in d_cg_, every kernel of an
+    // iteration reads them from device memory and turns into a no-op once the
+    // update kernel has flagged convergence / breakdown / budget.  The host only
+    // enqueues batches of iterations and polls the flag of the batch before.
+    if (hist_cap_ < (size_t)s.max_iter) {
+      cudaStreamSynchronize(st);
+      if (d_hist_) cudaFree(d_hist_);
+      d_hist_ = nullptr;
+      hist_cap_ = 0;
+      if (cudaMalloc(&d_hist_, (size_t)s.max_iter * sizeof(double)) != cudaSuccess)
+        return fail(DGB_E_CUDA, "cg: out of device memory (history)");
+      hist_cap_ = s.max_iter;
     }
+    CK(cudaStreamSynchronize(st));  // staging slot h_cg_[2] is free
+    CgState& init = h_cg_[2];
+    init = CgState();
+    init.tol = tol;
+    init.max_iter = s.max_iter;
+    init.iter = iter;
+    CK(cudaMemcpyAsync(d_cg_, &init, sizeof(CgState), cudaMemcpyHostToDevice, st));
+    launches += 2;
+    CK(cg_begin(st, n, r, inv, z, d_partial_, d_cg_));
+    const int batch = 8;
+    dc.mesh.skip = &d_cg_->done;
+    auto enqueue = [&](int slot) -> int {
+      for (int b = 0; b < batch; ++b) {
+        launches += 5;  // + the operator's own count
+        CK(cg_direction(st, n, z, p, d_cg_));
+        OK(apply_op(op, p, q));
+        CK(cg_alpha(st, n, p, q, d_partial_, d_cg_));
+        CK(cg_update(st, n, p, q, x, r, inv, z, d_partial_, d_cg_, d_hist_));
+      }
+      CK(cudaMemcpyAsync(&h_cg_[slot], d_cg_, sizeof(CgState), cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(poll_ev_[slot], st));
+      return DGB_OK;
+    };
+    int rc = enqueue(0);
+    int j = 0;
+    while (rc == DGB_OK) {
+      const int left = s.max_iter - iter - batch * (j + 1);
+      if (left > 0) rc = enqueue((j + 1) & 1);
+      if (rc != DGB_OK) break;
+      if (cudaEventSynchronize(poll_ev_[j & 1]) != cudaSuccess) {
+        rc = cuda_fail(cudaGetLastError(), "cg poll");
+        break;
+      }
+      if (h_cg_[j & 1].done || left <= 0) break;
+      ++j;
+    }
+    dc.mesh.skip = nullptr;
+    if (rc != DGB_OK) return rc;
+    CK(cudaStreamSynchronize(st));
+    const CgState fin = h_cg_[j & 1];
+    if (!fin.done) return fail(DGB_E_CUDA, "cg: device loop ended without a verdict");
+    if (fin.iter > iter) {
+      const size_t h0 = out.history.size();
+      out.history.resize(h0 + (fin.iter - iter));
+      CK(cudaMemcpy(out.history.data() + h0, d_hist_ + iter, (fin.iter - iter) * sizeof(double),
+                    cudaMemcpyDeviceToHost));
+    }
+    iter = fin.iter;
+    if (fin.err == DGB_E_BREAKDOWN) return fail(DGB_E_BREAKDOWN, "cg: breakdown, <r,z> = 0");
+    if (fin.err == DGB_E_NOT_SPD)
+      return fail(DGB_E_NOT_SPD, "cg: operator not positive definite, <p,Ap> <= 0");
   }
 }
 
@@ -479,13 +524,33 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
     gm_basis_.clear();
     gm_n_ = n;
   }
-  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1);
+  std::vector<double> H((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), sh(m + 1, 1.0);
   auto row = [&](int i, int j) -> double& { return H[(size_t)i * m + j]; };
   double* z = scratch_vec(4, n);
-  double* w = scratch_vec(5, n);
   double* r = scratch_vec(6, n);
-  if (!z || !w || !r) return fail(DGB_E_CUDA, "gmres: out of device memory");
-  auto basis = [&](int k) -> double* {
+  // device scalars: Gram matrix L (ldl x ldl), scales s_j, projections h, update coefficients g, chunk dots
+  const int ldl = m + 1, nchunk = (m + kGsChunk) / kGsChunk;
+  double* d_small = scratch_vec(22, (size_t)ldl * ldl + 3 * (size_t)(m + 2) + 2 * kGsChunk * (size_t)nchunk);
+  double* gpart = scratch_vec(23, 2 * kGsChunk * (size_t)blas_grid(n));
+  if (!z || !r || !d_small || !gpart) return fail(DGB_E_CUDA, "gmres: out of device memory");
+  double* d_L = d_small;
+  double* d_s = d_L + (size_t)ldl * ldl;
+  double* d_h = d_s + (m + 2);
+  double* d_g = d_h + (m + 2);
+  double* d_ab = d_g + (m + 2);
+  if (h_gm_cap_ < (size_t)m + 2) {
+    CK(cudaStreamSynchronize(st));
+    if (h_gm_) cudaFreeHost(h_gm_);
+    h_gm_ = nullptr;
+    h_gm_cap_ = 0;
+    if (cudaHostAlloc((void**)&h_gm_, (m + 2) * sizeof(double), cudaHostAllocDefault) != cudaSuccess)
+      return fail(DGB_E_CUDA, "gmres: pinned alloc failed");
+    h_gm_cap_ = m + 2;
+  }
+  // basis pool: slots 0..m hold U_j (v_j = s_j U_j), slot m+1 the Arnoldi vector w;
+  // the orthogonalised w becomes U_{k+1} by swapping slots (no copy, no normalisation pass)
+  const int W = m + 1;
+  auto pool = [&](int k) -> double* {
     while ((int)gm_basis_.size() <= k) {
       double* v = nullptr;
       if (cudaMalloc(&v, n * sizeof(double)) != cudaSuccess) return nullptr;
@@ -493,6 +558,8 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
     }
     return gm_basis_[k];
   };
+  if (!pool(W)) return fail(DGB_E_CUDA, "gmres: out of device memory (basis)");
+  const double* Uc[kGsChunk];
   int iter = 0;
   while (true) {
     OK(apply_op(op, x, r));
@@ -509,39 +576,41 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
     if (iter >= s.max_iter)
       return fail(DGB_E_NO_CONVERGENCE, "gmres: no convergence in " + std::to_string(s.max_iter) +
                                             " iterations (residual " + std::to_string(beta) + ")");
-    double* v0 = basis(0);
-    if (!v0) return fail(DGB_E_CUDA, "gmres: out of device memory (basis)");
     ++launches;
-    CK(v_scale_copy(st, n, 1.0 / beta, r, v0));
+    CK(v_scale_copy(st, n, 1.0 / beta, r, pool(0)));
+    std::fill(sh.begin(), sh.end(), 1.0);
     std::fill(g.begin(), g.end(), 0.0);
     g[0] = beta;
     std::fill(H.begin(), H.end(), 0.0);
     int k = 0;
     while (k < m && iter < s.max_iter) {
+      double* w = gm_basis_[W];
       ++launches;
-      if (inv)
-        CK(v_mul(st, n, basis(k), inv, z));
-      else
-        CK(cudaMemcpyAsync(z, basis(k), n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      CK(v_mul_scaled(st, n, sh[k], gm_basis_[k], inv, z));  // z = M^{-1} v_k
       OK(apply_op(op, z, w));
       ++iter;
-      // modified Gram-Schmidt, each subtraction fused with the next projection
-      double h;
-      OK(dot(n, w, basis(0), &h));
-      double hk1sq = 0.0;
-      for (int i = 0; i <= k; ++i) {
-        row(i, k) = h;
-        const double* next = i < k ? basis(i + 1) : w;
-        launches += 2;
-        CK(r_mgs_step(st, n, h, basis(i), w, next, d_partial_, d_res_));
-        double v;
-        OK(host_scalars(1, &v));
-        if (i < k)
-          h = v;
-        else
-          hk1sq = v;
+      // pass 1: <w, U_j> (j <= k) and the Gram row <U_k, U_j> (j < k)
+      for (int c0 = 0; c0 <= k; c0 += kGsChunk) {
+        const int nv = std::min(kGsChunk, k + 1 - c0);
+        const int nl = std::min(nv, std::max(0, k - c0));
+        for (int j = 0; j < nv; ++j) Uc[j] = gm_basis_[c0 + j];
+        launches += nl > 0 ? 3 : 2;
+        CK(gs_dots(st, n, nv, Uc, w, gm_basis_[k], nl, gpart, d_ab + 2 * kGsChunk * (c0 / kGsChunk)));
       }
-      const double hk1 = std::sqrt(hk1sq);
+      ++launches;
+      CK(gs_solve(st, k, d_ab, d_L, ldl, d_s, sh[k], d_h, d_g));
+      // pass 2: w -= sum_j h_j v_j, |w|^2
+      for (int c0 = 0; c0 <= k; c0 += kGsChunk) {
+        const int nv = std::min(kGsChunk, k + 1 - c0);
+        const bool last = c0 + kGsChunk > k;
+        for (int j = 0; j < nv; ++j) Uc[j] = gm_basis_[c0 + j];
+        launches += last ? 2 : 1;
+        CK(gs_update(st, n, nv, Uc, d_g + c0, w, gpart, last ? d_h + k + 1 : nullptr));
+      }
+      CK(cudaMemcpyAsync(h_gm_, d_h, (k + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int i = 0; i <= k; ++i) row(i, k) = h_gm_[i];
+      const double hk1 = std::sqrt(h_gm_[k + 1]);
       row(k + 1, k) = hk1;
       for (int i = 0; i < k; ++i) {
         const double t = cs[i] * row(i, k) + sn[i] * row(i + 1, k);
@@ -565,10 +634,9 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
       ++k;
       if (res <= tol || hk1 == 0.0) break;
       if (k < m) {
-        double* vk = basis(k);
-        if (!vk) return fail(DGB_E_CUDA, "gmres: out of device memory (basis)");
-        ++launches;
-        CK(v_scale_copy(st, n, 1.0 / hk1, w, vk));
+        if (!pool(k)) return fail(DGB_E_CUDA, "gmres: out of device memory (basis)");
+        std::swap(gm_basis_[k], gm_basis_[W]);
+        sh[k] = 1.0 / hk1;
       }
     }
     std::vector<double> y(k, 0.0);
@@ -577,11 +645,13 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
       for (int j = i + 1; j < k; ++j) t -= row(i, j) * y[j];
       y[i] = t / row(i, i);
     }
+    for (int j = 0; j < k; ++j) y[j] *= sh[j];
     // w = V y (chunks of 64 vectors), then x += M^{-1} w
+    double* w = gm_basis_[W];
     for (int j0 = 0; j0 < k; j0 += 64) {
       const int kk = std::min(64, k - j0);
       std::vector<const double*> V(kk);
-      for (int j = 0; j < kk; ++j) V[j] = basis(j0 + j);
+      for (int j = 0; j < kk; ++j) V[j] = gm_basis_[j0 + j];
       ++launches;
       if (j0 == 0) {
         CK(v_lincomb(st, n, kk, V.data(), y.data() + j0, w));
@@ -649,6 +719,17 @@ int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const do
   if (!wv || !F || !inv || !g || !uss || !u_g || !minv || !ut || !prhs || !pinv || !p_g)
     return fail(DGB_E_CUDA, "trbdf2: out of device memory");
   for (int i = 0; i < 8; ++i) its[i] = 0;
+  // DGB_PHASES=1: synchronise and print the wall time of every phase (diagnostics only)
+  static const bool phases = std::getenv("DGB_PHASES") != nullptr;
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* name) {
+    if (!phases) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[dgb phase] %-14s %9.3f ms\n", name,
+                 std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   OK(mass_diag(DGB_SPACE_U, ut));
   OK(jacobi_inverse(NU, ut, minv));
   const dgb_solver_settings s_mass{P.tol_mass, 0.0, P.max_iter, 50};
@@ -670,9 +751,12 @@ int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const do
   // one stage; alpha dt, momentum coefficients, rhs description
   auto stage = [&](int si, double alpha, const double* mc, const dgb_rhs_desc& rd, const double* u_guess,
                    const double* p_old, double* u_out, double* p_out) -> int {
+    phase("setup");
     OK(rhs(rd, F));
+    phase("rhs");
     OK(momentum_diag(mc, wv, g));
     OK(jacobi_inverse(NU, g, inv));
+    phase("mom diag");
     CK(cudaMemcpyAsync(u_out, u_guess, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
     dgb_operator mop{};
     mop.op = DGB_OP_MOMENTUM;
@@ -681,8 +765,10 @@ int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const do
     SolveOut so;
     OK(gmres(mop, s_mom, inv, F, u_out, so));
     its[si] = so.iterations;
+    phase("gmres");
     const double adt = alpha * P.dt;
     OK(proj_grad(p_old, ut, its[4 + 2 * si]));
+    phase("proj grad");
     CK(cudaMemcpyAsync(uss, u_out, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
     ++launches;
     CK(v_axpy(st, NU, adt, ut, uss));
@@ -690,13 +776,16 @@ int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const do
     OK(pressure_rhs(1.0 / adt, uss, pmc, p_old, prhs));
     OK(sip_diag(pmc, 0, pinv));
     OK(jacobi_inverse(NP, pinv, pinv));
+    phase("p rhs+diag");
     CK(cudaMemcpyAsync(p_out, p_old, NP * sizeof(double), cudaMemcpyDeviceToDevice, st));
     dgb_operator pop{};
     pop.op = DGB_OP_PRESSURE;
     pop.coefs[0] = pmc;
     OK(cg(pop, s_p, pinv, prhs, p_out, so));
     its[2 + si] = so.iterations;
+    phase("pressure cg");
     OK(proj_grad(p_out, ut, its[5 + 2 * si]));
+    phase("proj grad");
     CK(cudaMemcpyAsync(u_out, uss, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
     ++launches;
     CK(v_axpy(st, NU, -adt, ut, u_out));

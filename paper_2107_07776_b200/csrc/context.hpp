@@ -10,6 +10,7 @@
 
 #include "../../include/dgb.h"
 #include "dispatch.hpp"
+#include "blas.cuh"
 #include "host_setup.hpp"
 
 namespace dgb {
@@ -101,6 +102,13 @@ class Context {
   std::vector<double> gtab_h_;
   std::vector<std::pair<double*, size_t>> slots_;
   std::vector<double*> gm_basis_;
+  CgState* d_cg_ = nullptr;         // device-resident CG scalars
+  CgState* h_cg_ = nullptr;         // pinned: [0..1] polled status, [2] staging
+  double* d_hist_ = nullptr;        // device residual history
+  size_t hist_cap_ = 0;
+  double* h_gm_ = nullptr;          // pinned GMRES Hessenberg column
+  size_t h_gm_cap_ = 0;
+  cudaEvent_t poll_ev_[2] = {nullptr, nullptr};
   size_t gm_n_ = 0;
   int ensure_geometry();
 };

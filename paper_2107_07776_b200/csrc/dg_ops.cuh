@@ -149,6 +149,7 @@ template <int DIM, int K, template <int, int> class Geo>
 __global__ void __launch_bounds__(kThreads) k_momentum(MeshArgs m, GeoArgs gA, GeoArgs gB, MomCoef co,
                                                        const double* __restrict__ x,
                                                        const double* __restrict__ w, double* __restrict__ y) {
+  if (m.skip && *m.skip) return;
   using L = MomLayout<DIM, K>;
   using EA = typename L::EA;
   using EB = typename L::EB;
@@ -330,6 +331,7 @@ struct SipLayout {
 template <int DIM, int KP, template <int, int> class Geo>
 __global__ void __launch_bounds__(kThreads) k_sip(MeshArgs m, GeoArgs gq, double mass_coef, int dir_bdry,
                                                   const double* __restrict__ x, double* __restrict__ y) {
+  if (m.skip && *m.skip) return;
   using L = SipLayout<DIM, KP>;
   using E = typename L::E;
   constexpr int NB = L::NB, NF = L::NF, CB = L::CB, NQ = E::NQ, NQF = E::NQF;
@@ -429,6 +431,7 @@ struct CellLayout {
 template <int DIM, int N, int Q, int NCOMP, template <int, int> class Geo>
 __global__ void __launch_bounds__(kThreads) k_mass(MeshArgs m, GeoArgs gq, const double* __restrict__ x,
                                                    double* __restrict__ y) {
+  if (m.skip && *m.skip) return;
   using L = CellLayout<DIM, N, Q>;
   using E = typename L::E;
   constexpr int NB = E::NB, NQ = E::NQ, CB = L::CB;

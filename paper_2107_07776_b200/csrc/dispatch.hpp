@@ -16,6 +16,7 @@ struct MeshArgs {
   const double* pen = nullptr;   // [ncells][2dim]: interior mean |F|/|K|, boundary |F|/|K|
   const int* bctype = nullptr;   // [64]: 0 dirichlet, 1 outlet
   const int* bslot = nullptr;    // [ncells][2dim]: boundary-face index (reference order) or -1
+  const int* skip = nullptr;     // device flag: nonzero -> the launch is a no-op (device-side Krylov exit)
 };
 
 struct GeoArgs {

@@ -338,6 +338,7 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
                                                                  double mc, int dir_bdry,
                                                                  const double* __restrict__ x,
                                                                  double* __restrict__ y) {
+  if (m.skip && *m.skip) return;
   using G = SipAxisCfg<KP>;
   using P = typename G::P;
   constexpr int N = G::N, NB = G::NB, NF = G::NF, C = G::C, PER = G::PER, TT = G::T;
@@ -510,6 +511,7 @@ template <int K, int CC, int TH, int MODE, bool UNI>
 __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff, MomCoef co,
                                                       const double* __restrict__ x, const double* __restrict__ w,
                                                       double* __restrict__ y) {
+  if (m.skip && *m.skip) return;
   using G = MomAxisCfg<K, CC, TH, MODE>;
   using P = typename G::P;
   constexpr int N = G::N, Q = G::Q, NB = G::NB, NF = G::NF, QN = G::QN, QQ = G::QQ, C = G::C, PER = G::PER;
