@@ -390,6 +390,30 @@ Base* make_cartesian(int n_el, double amp, unsigned seed, int ku, int kp, int re
   return new Ctx<dim>(std::move(m), ku, kp);
 }
 
+// Same construction as import_text (mesh.cpp:793-817) from raw arrays: vertices
+// [nv][dim], cell vertices [nc][2^dim], boundary ids [nc][2dim] (-1 interior), then
+// Mesh::finalize().  (Avoids the iostream parse, which is fragile when the host
+// process has already loaded another libstdc++.)
+template <int dim>
+Mesh<dim> mesh_from_arrays(int nv, const double* xv, int nc, const int* cv, const int* bid) {
+  Mesh<dim> m;
+  m.vertices.resize(nv);
+  for (int v = 0; v < nv; ++v)
+    for (int a = 0; a < dim; ++a) m.vertices[v][a] = xv[(size_t)v * dim + a];
+  m.cells.resize(nc);
+  for (int c = 0; c < nc; ++c) {
+    for (int v = 0; v < Mesh<dim>::n_vertices_per_cell; ++v) {
+      const int id = cv[(size_t)c * Mesh<dim>::n_vertices_per_cell + v];
+      if (id < 0 || id >= nv) throw std::runtime_error("mesh arrays: bad cell vertex index");
+      m.cells[c].v[v] = id;
+    }
+    for (int f = 0; f < Mesh<dim>::n_faces_per_cell; ++f)
+      m.cells[c].boundary_id[f] = bid[(size_t)c * Mesh<dim>::n_faces_per_cell + f];
+  }
+  m.finalize();
+  return m;
+}
+
 }  // namespace
 
 extern "C" {
@@ -417,6 +441,17 @@ void* ref_create_from_text(const char* text, int ku, int kp) {
     const int d = mesh_file_dim(s);
     if (d == 2) return new Ctx<2>(import_text<2>(s), ku, kp);
     return new Ctx<3>(import_text<3>(s), ku, kp);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  }
+  return nullptr;
+}
+void* ref_create_from_arrays(int dim, int nv, const double* xv, int nc, const int* cv, const int* bid, int ku,
+                             int kp) {
+  try {
+    if (dim == 2) return new Ctx<2>(mesh_from_arrays<2>(nv, xv, nc, cv, bid), ku, kp);
+    if (dim == 3) return new Ctx<3>(mesh_from_arrays<3>(nv, xv, nc, cv, bid), ku, kp);
+    g_err = "mesh arrays: dim must be 2 or 3";
   } catch (const std::exception& e) {
     g_err = e.what();
   }

@@ -322,6 +322,17 @@ int Context::rhs(const dgb_rhs_desc& ds, double* y) {
   ra.dadv = ds.dir_adv_coef;
   ra.dir_w = ds.dir_w;
   ra.gtab = d_gtab_;
+  if (use_fast && dc.axis) {
+    double* ptmp = scratch_vec(24, np());
+    if (!ptmp) return fail(DGB_E_CUDA, "out of memory");
+    const cudaError_t e = fast_rhs3(dc, ra, y, ptmp);
+    if (e == cudaSuccess) {
+      launches += 2 + ra.na + (ra.np > 0 ? ra.np + 1 : 0);
+      return DGB_OK;
+    }
+    if (e != cudaErrorNotSupported) return cuda_fail(e, "momentum_rhs");
+    cudaGetLastError();
+  }
   ++launches;
   CK(opu->rhs(dc, ra, y));
   return DGB_OK;

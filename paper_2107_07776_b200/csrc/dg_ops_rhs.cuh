@@ -60,6 +60,15 @@ __global__ void __launch_bounds__(kThreads) k_momentum_rhs(MeshArgs m, GeoArgs g
   const int nc = min(CB, m.ncells - c0);
   const double sfac = (double)((K + 1) * (K + 1));
   const bool any_dir = ra.dvisc != 0.0 || ra.dadv != 0.0;
+  if (ra.accumulate && ra.nm + ra.nv + ra.na + ra.np == 0) {
+    // boundary-data terms only: blocks without a Dirichlet face contribute nothing
+    bool any = false;
+    for (int i = 0; i < nc * NF; ++i) {
+      const int nb = m.nbr[(size_t)c0 * NF + i];
+      any = any || (nb < 0 && !is_outlet(m, nb));
+    }
+    if (!any) return;
+  }
   const Geo<DIM, L::QA> geoA(gA);
   const Geo<DIM, L::QB> geoB(gB);
 
@@ -309,7 +318,14 @@ __global__ void __launch_bounds__(kThreads) k_momentum_rhs(MeshArgs m, GeoArgs g
         EB::template integrate_face_rt<true>(f, FT, SCR, OUT, NB, nc);
       }
     }
-    store_block<NB>(OUT, NB, y, c0, DIM * NB, comp * NB, nc);
+    if (ra.accumulate) {
+      for (int idx = threadIdx.x; idx < nc * NB; idx += blockDim.x) {
+        const int c = idx / NB, i = idx - c * NB;
+        y[(size_t)(c0 + c) * DIM * NB + comp * NB + i] += OUT[c * NB + i];
+      }
+    } else {
+      store_block<NB>(OUT, NB, y, c0, DIM * NB, comp * NB, nc);
+    }
     __syncthreads();
   }
 }

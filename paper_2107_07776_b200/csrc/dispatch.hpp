@@ -41,6 +41,7 @@ struct RhsArgs {
   double dvisc = 0.0, dadv = 0.0;
   const double* dir_w = nullptr;
   const double* gtab = nullptr;  // [n_bface][NQF(rule k+2)][DIM], reference boundary-face order
+  int accumulate = 0;            // y += result (blocks without Dirichlet faces skip when only data terms)
 };
 
 // Uniform structured (generate_cartesian, lexicographic cells, equal h): neighbours,
@@ -81,6 +82,8 @@ struct OpTable {
 // fast axis-aligned 3D kernels (fast_d3.cu); cudaErrorNotSupported when not applicable
 cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, double* y);
 cudaError_t fast_momentum3(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);
+// stage right-hand side (momentum_rhs) on axis-aligned 3D meshes; ptmp: pressure-space scratch
+cudaError_t fast_rhs3(const DevCtx& c, const RhsArgs& ra, double* y, double* ptmp);
 
 // defined in ops_d{2,3}_k{1..4}.cu
 #define DGB_DECL_OPS(D, K) const OpTable& ops_d##D##_k##K();

@@ -183,7 +183,8 @@ __device__ __forceinline__ void load_info_par(double* base, int per, int off, in
 // :232-240 / :481-490 boundary), per face of one cell; `dirichlet` selects whether
 // non-interior faces carry Dirichlet-type terms (outlets never do when
 // outlet_natural).
-__device__ __forceinline__ void face_coefs(CellInfo& ci, int f, bool dirichlet, bool outlet_natural) {
+__device__ __forceinline__ void face_coefs(CellInfo& ci, int f, bool dirichlet, bool outlet_natural,
+                                           bool consistency_only = false) {
   const int d = f >> 1, s = f & 1;
   const double ih = ci.ih[d];
   const double sg = s ? -1.0 : 1.0;  // right face: -1/2 (...) ; left face: +1/2 (...)
@@ -193,14 +194,18 @@ __device__ __forceinline__ void face_coefs(CellInfo& ci, int f, bool dirichlet, 
   if (ty == 0) {
     c[0] = 0.5 * sg * ih;
     c[1] = 0.5 * sg * ci.ihn[f];
-    c[2] = ci.pen[f];
-    c[3] = -ci.pen[f];
-    c[4] = -0.5;
-    c[5] = 0.5;
+    if (!consistency_only) {
+      c[2] = ci.pen[f];
+      c[3] = -ci.pen[f];
+      c[4] = -0.5;
+      c[5] = 0.5;
+    }
   } else if (dirichlet && !(ty == 2 && outlet_natural)) {
     c[0] = sg * ih;
-    c[2] = 2.0 * ci.pen[f];
-    c[4] = -1.0;
+    if (!consistency_only) {
+      c[2] = 2.0 * ci.pen[f];
+      c[4] = -1.0;
+    }
   }
 }
 
@@ -507,10 +512,14 @@ template <> struct MomAxisTune<3, 0> { static constexpr int C = 3, T = 96; stati
 template <> struct MomAxisTune<3, 1> { static constexpr int C = 4, T = 128; static constexpr bool SPLIT = true; };
 template <> struct MomAxisTune<3, 2> { static constexpr int C = 3, T = 96; static constexpr bool SPLIT = true; };
 
-template <int K, int CC, int TH, int MODE, bool UNI>
+// RHS: the explicit stage right-hand side operator of momentum_rhs (forms.cpp:816-1084)
+// instead: consistency-only viscous faces (no symmetry / penalty) and the central
+// advective flux with w.n f on every boundary face; the caller passes the negated
+// viscous / advective coefficients.  acc: y += result.
+template <int K, int CC, int TH, int MODE, bool UNI, bool RHS = false>
 __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff, MomCoef co,
                                                       const double* __restrict__ x, const double* __restrict__ w,
-                                                      double* __restrict__ y) {
+                                                      double* __restrict__ y, int acc) {
   if (m.skip && *m.skip) return;
   using G = MomAxisCfg<K, CC, TH, MODE>;
   using P = typename G::P;
@@ -570,7 +579,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   load_info_par<TT, UNI>(sm, PER, G::O_INFO, nc, m, ug, aff, c0, sfac);
   cp_async_wait_all();
   __syncthreads();
-  for (int idx = tid; idx < nc * 6; idx += TT) face_coefs(INFO(idx / 6), idx % 6, true, true);
+  for (int idx = tid; idx < nc * 6; idx += TT) face_coefs(INFO(idx / 6), idx % 6, true, true, RHS);
   __syncthreads();
 
   // ------------------------------------------------------------------ pass A: mass + viscous (line split)
@@ -893,12 +902,12 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         double fl3[3];
         if (ty == 0) {  // forms.cpp:555-573
           const double wno = sgn * val[7];
-          const double lam = fmax(fabs(wns), fabs(wno));
+          const double lam = RHS ? 0.0 : fmax(fabs(wns), fabs(wno));
 #pragma unroll
           for (int comp = 0; comp < 3; ++comp)
             fl3[comp] = wq * (0.5 * (val[comp] * wns + val[3 + comp] * wno) + 0.5 * lam * (val[comp] - val[3 + comp]));
         } else {  // forms.cpp:592-599
-          const double cf = ty == 2 ? wns : fabs(wns);
+          const double cf = (RHS || ty == 2) ? wns : fabs(wns);  // rhs: forms.cpp:1036-1048
 #pragma unroll
           for (int comp = 0; comp < 3; ++comp) fl3[comp] = wq * cf * val[comp];
         }
@@ -948,11 +957,131 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         if (ii[a] == N - 1) v += fb[(2 * a + 1) * NF + t];
       }
     }
-    if (MODE == 2) v += y[(size_t)(c0 + c) * 3 * NB + r];
+    if (MODE == 2 || acc) v += y[(size_t)(c0 + c) * 3 * NB + r];
     y[(size_t)(c0 + c) * 3 * NB + r] = v;
   }
 #undef CELL
 #undef WK
+#undef INFO
+}
+
+// ===========================================================================
+// Weak pressure gradient of momentum_rhs (forms.cpp:850-855 cell, :895-912
+// interior faces, :940-948 boundary faces), axis-aligned affine, 3D:
+//   y_d += (G_d (x) Mvp (x) Mvp) p,
+// G_d = 1D line operator along d (velocity test derivative x pressure value,
+// exact for the k+1 rule) plus the {p} n_d v face terms at the two line ends;
+// Mvp = mixed velocity/pressure 1D mass.  p already carries the coefficient.
+// ===========================================================================
+template <int K>
+struct PTab {
+  double Mvp[K + 1][K];  // sum_q w phi_i psi_j
+  double G1[K + 1][K];   // sum_q w phi_i' psi_j
+};
+template <int K>
+__constant__ PTab<K> c_pt;
+
+template <int K>
+struct PGradCfg {
+  static constexpr int N = K + 1, NP = K, NBP = NP * NP * NP, NB = N * N * N;
+  static constexpr int C = 8, T = 128;
+  static constexpr int L1 = 3 * N * NP * NP, L2 = 3 * N * N * NP;
+  static constexpr int PER = (NBP + L1 + L2 + kInfoDoubles) | 1;
+  static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
+};
+
+template <int K, bool UNI>
+__global__ void __launch_bounds__(PGradCfg<K>::T) k_pgrad_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff,
+                                                               const double* __restrict__ p, double* __restrict__ y) {
+  using G = PGradCfg<K>;
+  constexpr int N = G::N, NP = G::NP, NBP = G::NBP, NB = G::NB, C = G::C, PER = G::PER, TT = G::T;
+  const PTab<K>& pt = c_pt<K>;
+  extern __shared__ double sm[];
+  const int c0 = blockIdx.x * C;
+  const int nc = min(C, m.ncells - c0);
+  const int tid = threadIdx.x;
+#define CELL(c) (sm + (c) * PER)
+#define INFO(c) (*reinterpret_cast<const CellInfo*>(sm + (c) * PER + NBP + G::L1 + G::L2))
+  for (int idx = tid; idx < nc * NBP; idx += TT) CELL(idx / NBP)[idx % NBP] = p[(size_t)c0 * NBP + idx];
+  load_info_par<TT, UNI>(sm, PER, NBP + G::L1 + G::L2, nc, m, ug, aff, c0, 1.0);
+  __syncthreads();
+  // S1: line operator along d on the raw pressure lines (tangential (a, b), t1 < t2)
+  for (int idx = tid; idx < nc * 3 * NP * NP; idx += TT) {
+    const int c = idx / (3 * NP * NP), r = idx - c * 3 * NP * NP;
+    const int d = r / (NP * NP), ab = r - d * NP * NP;
+    const int a = ab % NP, b = ab / NP;
+    const int st = d == 0 ? 1 : (d == 1 ? NP : NP * NP);
+    const int b0 = d == 0 ? NP * a + NP * NP * b : (d == 1 ? a + NP * NP * b : a + NP * b);
+    const CellInfo& ci = INFO(c);
+    double pl[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) pl[j] = CELL(c)[b0 + j * st];
+    const double cs = ci.detJ * ci.ih[d], A = ci.A[d];
+    double o[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) acc = fma(pt.G1[i][j], pl[j], acc);
+      o[i] = cs * acc;
+    }
+    // left face (n_d = -1): -{p} n_d -> +A pf at node 0; right face (n_d = +1): -A pf at node N-1
+    {
+      const int f = 2 * d, nb = ci.nb[f], ty = ci.type[f];
+      const double own = pl[0];
+      const double pf = ty == 0 ? 0.5 * (own + __ldg(p + (size_t)nb * NBP + b0 + (NP - 1) * st)) : (ty == 1 ? own : 0.0);
+      o[0] = fma(A, pf, o[0]);
+    }
+    {
+      const int f = 2 * d + 1, nb = ci.nb[f], ty = ci.type[f];
+      const double own = pl[NP - 1];
+      const double pf = ty == 0 ? 0.5 * (own + __ldg(p + (size_t)nb * NBP + b0)) : (ty == 1 ? own : 0.0);
+      o[N - 1] = fma(-A, pf, o[N - 1]);
+    }
+    double* t1 = CELL(c) + NBP + d * N * NP * NP;
+#pragma unroll
+    for (int i = 0; i < N; ++i) t1[i + N * ab] = o[i];
+  }
+  __syncthreads();
+  // S2: Mvp along t1:  t2[d][i + N (a' + N b)]
+  for (int idx = tid; idx < nc * 3 * N * NP; idx += TT) {
+    const int c = idx / (3 * N * NP), r = idx - c * 3 * N * NP;
+    const int d = r / (N * NP), ib = r - d * N * NP;
+    const int i = ib % N, b = ib / N;
+    const double* t1 = CELL(c) + NBP + d * N * NP * NP;
+    double v[NP];
+#pragma unroll
+    for (int a = 0; a < NP; ++a) v[a] = t1[i + N * (a + NP * b)];
+    double* t2 = CELL(c) + NBP + G::L1 + d * N * N * NP;
+#pragma unroll
+    for (int a2 = 0; a2 < N; ++a2) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < NP; ++a) acc = fma(pt.Mvp[a2][a], v[a], acc);
+      t2[i + N * (a2 + N * b)] = acc;
+    }
+  }
+  __syncthreads();
+  // S3: Mvp along t2, add into y
+  for (int idx = tid; idx < nc * 3 * N * N; idx += TT) {
+    const int c = idx / (3 * N * N), r = idx - c * 3 * N * N;
+    const int d = r / (N * N), ia = r - d * N * N;
+    const int i = ia % N, a2 = ia / N;
+    const double* t2 = CELL(c) + NBP + G::L1 + d * N * N * NP;
+    double v[NP];
+#pragma unroll
+    for (int b = 0; b < NP; ++b) v[b] = t2[i + N * (a2 + N * b)];
+    double* yo = y + (size_t)(c0 + c) * 3 * NB + d * NB;
+#pragma unroll
+    for (int b2 = 0; b2 < N; ++b2) {
+      double acc = 0.0;
+#pragma unroll
+      for (int b = 0; b < NP; ++b) acc = fma(pt.Mvp[b2][b], v[b], acc);
+      const int node = d == 0 ? i + N * a2 + N * N * b2 : (d == 1 ? a2 + N * i + N * N * b2 : a2 + N * b2 + N * N * i);
+      yo[node] += acc;
+    }
+  }
+#undef CELL
 #undef INFO
 }
 

@@ -1,6 +1,10 @@
 // Axis-aligned affine 3D fast kernels (fast_axis.cuh) + their launchers.
 #include "fast_axis.cuh"
 
+#include <vector>
+
+#include "blas.cuh"
+
 namespace dgb {
 
 void host_tab(int N, int Q, double* B, double* D, double* dE);
@@ -19,6 +23,37 @@ void host_ftab(int N, int Q, double* M, double* K, double* B, double* D, double*
       M[i * N + j] = m;
       K[i * N + j] = k;
     }
+}
+
+// mixed velocity / pressure 1D tables (rule k+1): Mvp = sum_q w phi_i psi_j, G1 = sum_q w phi_i' psi_j
+static void host_ptab(int K, double* Mvp, double* G1) {
+  const int N = K + 1, NP = K, Q = K + 1;
+  std::vector<double> Bn(Q * N), Dn(Q * N), En(2 * N), Bp(Q * NP), Dp(Q * NP), Ep(2 * NP), w(Q);
+  host_tab(N, Q, Bn.data(), Dn.data(), En.data());
+  host_tab(NP, Q, Bp.data(), Dp.data(), Ep.data());
+  host_w(Q, w.data());
+  for (int i = 0; i < N; ++i)
+    for (int j = 0; j < NP; ++j) {
+      double mv = 0.0, g = 0.0;
+      for (int q = 0; q < Q; ++q) {
+        mv += w[q] * Bn[q * N + i] * Bp[q * NP + j];
+        g += w[q] * Dn[q * N + i] * Bp[q * NP + j];
+      }
+      Mvp[i * NP + j] = mv;
+      G1[i * NP + j] = g;
+    }
+}
+template <int K>
+static cudaError_t ensure_ptab() {
+  static int done_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done_dev == dev) return cudaSuccess;
+  PTab<K> t;
+  host_ptab(K, &t.Mvp[0][0], &t.G1[0][0]);
+  const cudaError_t e = cudaMemcpyToSymbol(c_pt<K>, &t, sizeof(t));
+  if (e == cudaSuccess) done_dev = dev;
+  return e;
 }
 
 template <class KernelT>
@@ -42,18 +77,19 @@ static cudaError_t run_sip_axis(const DevCtx& c, double mc, int dir, const doubl
   return cudaGetLastError();
 }
 
-template <int K, int MODE>
-static cudaError_t launch_momentum_axis(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y) {
+template <int K, int MODE, bool RHS = false>
+static cudaError_t launch_momentum_axis(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y,
+                                        int acc = 0) {
   constexpr int CC = MomAxisTune<K, MODE>::C, TH = MomAxisTune<K, MODE>::T;
   using G = MomAxisCfg<K, CC, TH, MODE>;
   cudaError_t e;
   const int grid = (c.ncells + G::C - 1) / G::C;
   if (c.ug.n > 0) {
-    if ((e = set_smem(k_momentum_axis<K, CC, TH, MODE, true>, G::SMEM)) != cudaSuccess) return e;
-    k_momentum_axis<K, CC, TH, MODE, true><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, co, x, w, y);
+    if ((e = set_smem(k_momentum_axis<K, CC, TH, MODE, true, RHS>, G::SMEM)) != cudaSuccess) return e;
+    k_momentum_axis<K, CC, TH, MODE, true, RHS><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, co, x, w, y, acc);
   } else {
-    if ((e = set_smem(k_momentum_axis<K, CC, TH, MODE, false>, G::SMEM)) != cudaSuccess) return e;
-    k_momentum_axis<K, CC, TH, MODE, false><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, co, x, w, y);
+    if ((e = set_smem(k_momentum_axis<K, CC, TH, MODE, false, RHS>, G::SMEM)) != cudaSuccess) return e;
+    k_momentum_axis<K, CC, TH, MODE, false, RHS><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, co, x, w, y, acc);
   }
   return cudaGetLastError();
 }
@@ -69,6 +105,85 @@ static cudaError_t run_momentum_axis(const DevCtx& c, MomCoef co, const double* 
     return launch_momentum_axis<K, 2>(c, co, w, x, y);  // + advection
   }
   return launch_momentum_axis<K, 0>(c, co, w, x, y);
+}
+
+// Stage right-hand side (forms.cpp:816-1084) as a sum of fast launches:
+//   one RHS-mode momentum launch per distinct (field, advecting field) pair
+//   (mass + consistency-only viscous + central advective terms, coefficients
+//   merged per field), the weak pressure gradient of sum_i pc_i p_i, and the
+//   boundary-data terms through the generic kernel (only blocks that own a
+//   Dirichlet face do work).
+template <int K>
+static cudaError_t run_rhs_axis(const DevCtx& c, const RhsArgs& ra, double* y, double* ptmp) {
+  cudaError_t e = ensure_ftab<K + 1, K + 2>();
+  if (e == cudaSuccess) e = ensure_ftab<K + 1, K + 1>();
+  if (e == cudaSuccess && ra.np > 0) e = ensure_ptab<K>();
+  if (e != cudaSuccess) return e;
+  struct Call {
+    const double* x;
+    const double* w;
+    MomCoef co;
+  };
+  std::vector<Call> calls;
+  auto find = [&](const double* x, const double* w, bool need_w) -> Call& {
+    for (Call& cl : calls)
+      if (cl.x == x && (!need_w || cl.w == w || cl.w == nullptr)) {
+        if (need_w) cl.w = w;
+        return cl;
+      }
+    calls.push_back(Call{x, need_w ? w : nullptr, MomCoef{0.0, 0.0, 0.0, 0.0}});
+    return calls.back();
+  };
+  for (int i = 0; i < ra.na; ++i) find(ra.af[i], ra.aw[i], true).co.adv -= ra.ac[i];
+  for (int i = 0; i < ra.nm; ++i) find(ra.mf[i], nullptr, false).co.mass += ra.mc[i];
+  for (int i = 0; i < ra.nv; ++i) find(ra.vf[i], nullptr, false).co.visc -= ra.vc[i];
+  const size_t nu = (size_t)c.ncells * 3 * (K + 1) * (K + 1) * (K + 1);
+  if (calls.empty()) {
+    if ((e = cudaMemsetAsync(y, 0, nu * sizeof(double), c.stream)) != cudaSuccess) return e;
+  }
+  for (size_t i = 0; i < calls.size(); ++i) {
+    const Call& cl = calls[i];
+    e = launch_momentum_axis<K, 0, true>(c, cl.co, cl.w ? cl.w : cl.x, cl.x, y, i > 0 ? 1 : 0);
+    if (e != cudaSuccess) return e;
+  }
+  if (ra.np > 0) {
+    const size_t np = (size_t)c.ncells * K * K * K;
+    if ((e = v_scale_copy(c.stream, np, ra.pc[0], ra.pf[0], ptmp)) != cudaSuccess) return e;
+    for (int i = 1; i < ra.np; ++i)
+      if ((e = v_axpy(c.stream, np, ra.pc[i], ra.pf[i], ptmp)) != cudaSuccess) return e;
+    using G = PGradCfg<K>;
+    const int grid = (c.ncells + G::C - 1) / G::C;
+    if (c.ug.n > 0) {
+      if ((e = set_smem(k_pgrad_axis<K, true>, G::SMEM)) != cudaSuccess) return e;
+      k_pgrad_axis<K, true><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, ptmp, y);
+    } else {
+      if ((e = set_smem(k_pgrad_axis<K, false>, G::SMEM)) != cudaSuccess) return e;
+      k_pgrad_axis<K, false><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, ptmp, y);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (ra.dvisc != 0.0 || ra.dadv != 0.0) {
+    RhsArgs rd;
+    rd.dvisc = ra.dvisc;
+    rd.dadv = ra.dadv;
+    rd.dir_w = ra.dir_w;
+    rd.gtab = ra.gtab;
+    rd.accumulate = 1;
+    const OpTable* ops = ops_for(3, K);
+    if (!ops) return cudaErrorNotSupported;
+    return ops->rhs(c, rd, y);
+  }
+  return cudaSuccess;
+}
+
+cudaError_t fast_rhs3(const DevCtx& c, const RhsArgs& ra, double* y, double* ptmp) {
+  if ((c.kp != c.ku - 1 && ra.np > 0) || !ptmp) return cudaErrorNotSupported;
+  switch (c.ku) {
+    case 1: return run_rhs_axis<1>(c, ra, y, ptmp);
+    case 2: return run_rhs_axis<2>(c, ra, y, ptmp);
+    case 3: return run_rhs_axis<3>(c, ra, y, ptmp);
+  }
+  return cudaErrorNotSupported;
 }
 
 cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, double* y) {

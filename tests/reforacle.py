@@ -35,6 +35,8 @@ def lib():
         L.ref_create_cartesian.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint, C.c_int, C.c_int, C.c_int]
         L.ref_create_from_text.restype = C.c_void_p
         L.ref_create_from_text.argtypes = [C.c_char_p, C.c_int, C.c_int]
+        L.ref_create_from_arrays.restype = C.c_void_p
+        L.ref_create_from_arrays.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _ip, _ip, C.c_int, C.c_int]
         L.ref_create_cylinder.restype = C.c_void_p
         L.ref_create_cylinder.argtypes = [C.c_int, C.c_int, C.c_int]
         L.ref_destroy.argtypes = [C.c_void_p]

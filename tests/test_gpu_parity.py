@@ -318,3 +318,119 @@ def test_trbdf2_step_cfg1(ref, gpu):
 
 def test_trbdf2_step_3d_small(ref, gpu):
     _step_case(ref, gpu, 3, 3, 2, 1, Re=100.0, dt=1e-3, seed=1, steps=1)
+
+
+# ---------------------------------------------------------------- graded axis-aligned meshes
+def graded_box(n):
+    """3D box with graded (non-uniform) tensor-product spacing: axis-aligned cells of
+    different sizes, so the fast kernels take their mesh-table path (no uniform grid).
+    Returns the reference mesh text (mesh.cpp:793-817 format) and the C-ABI arrays."""
+    t = np.linspace(0.0, 1.0, n + 1)
+    axes = [t ** 1.4, 0.5 * (t + t ** 2), np.sin(0.5 * np.pi * t)]
+    nv1 = n + 1
+    verts = np.array([[axes[0][i], axes[1][j], axes[2][k]] for k in range(nv1) for j in range(nv1)
+                      for i in range(nv1)])
+    cells, bids = [], []
+    for k in range(n):
+        for j in range(n):
+            for i in range(n):
+                cells.append([(i + dx) + nv1 * (j + dy) + nv1 * nv1 * (k + dz)
+                              for dz in (0, 1) for dy in (0, 1) for dx in (0, 1)])
+                co = (i, j, k)
+                bids.append([2 * a + s if co[a] == (0 if s == 0 else n - 1) else -1
+                             for a in range(3) for s in (0, 1)])
+    lines = [f"3 {len(verts)} {len(cells)}"]
+    lines += [" ".join(repr(float(v)) for v in p) for p in verts]
+    lines += [" ".join(str(v) for v in c) for c in cells]
+    lines += [f"{c} {f} {b}" for c, row in enumerate(bids) for f, b in enumerate(row) if b >= 0]
+    return "\n".join(lines) + "\n", (verts, np.array(cells, dtype=np.int32), np.array(bids, dtype=np.int32))
+
+
+def graded_pair(ref, gpu, n, ku, kp, outlet=None, dirichlet_seed=None):
+    _, arrays = graded_box(n)
+    verts, cells, bids = arrays
+    verts = np.ascontiguousarray(verts, dtype=np.float64)
+    h = ref.lib().ref_create_from_arrays(3, len(verts), ref.P(verts), len(cells), cells.ctypes.data_as(ref._ip),
+                                         bids.ctypes.data_as(ref._ip), ku, kp)
+    assert h, ref.lib().ref_last_error().decode()
+    R = ref.RefCtx(handle=h)
+    D = gpu.DGContext(3, n, ku, kp, mesh_arrays=arrays)
+    assert (R.n_u, R.n_p, R.ncells) == (D.n_u, D.n_p, D.ncells)
+    if outlet is not None:
+        R.set_bc(outlet, 1)
+        D.set_boundary_type(outlet, gpu.BC_OUTLET)
+    if dirichlet_seed is not None:
+        f = gpu.SynthField(3, dirichlet_seed)
+        for bid in range(6):
+            if bid == outlet:
+                continue
+            R.set_bc(bid, 0, f.fn_ptr, f.user_ptr)
+            D.set_dirichlet_fn(bid, f.fn_ptr, f.user_ptr, 0.0)
+        R._keep.append(f)
+        D._keep.append(f)
+    return R, D
+
+
+@pytest.mark.parametrize("n,ku,kp", [(3, 2, 1), (3, 3, 2), (2, 4, 3)])
+@pytest.mark.parametrize("outlet", [None, 1])
+def test_graded_axis_mesh_operators(ref, gpu, n, ku, kp, outlet):
+    """Non-uniform axis-aligned cells: fast kernels with mesh tables (no uniform-grid
+    shortcut) against the reference on the same imported mesh."""
+    R, D = graded_pair(ref, gpu, n, ku, kp, outlet=outlet, dirichlet_seed=9)
+    assert D.fast_path_active
+    w = gpu.seeded_uniform(91, R.n_u)
+    x = gpu.seeded_uniform(92, R.n_u)
+    xp = gpu.seeded_uniform(93, R.n_p)
+    for coefs in ((1.0 / (0.2929 * 1e-3), 1.0 / 2000.0, 0.5, 0.0), (0.3, 2.0, 1.5, 0.0)):
+        y = D.zeros()
+        gpu.apply_momentum(D, gpu.MomentumCtx(*coefs, advecting=dev(w)), dev(x), y)
+        assert rel(host(y), R.momentum(coefs, w, x)) <= TOL_APPLY
+    for mc in (2.3, 0.0):
+        yp = D.zeros(gpu.SPACE_P)
+        gpu.apply_pressure_helmholtz(D, mc, dev(xp), yp)
+        assert rel(host(yp), R.pressure(mc, xp)) <= TOL_APPLY
+    ug = gpu.seeded_uniform(94, R.n_u)
+    want = R.momentum_rhs(mass=[(2.9, x)], visc=[(0.65, x), (0.3, ug)], adv=[(0.5, x, w), (0.25, ug, ug)],
+                          pres=[(1.0, xp), (-0.4, xp)], dir_visc=0.65, dir_adv=0.5, dir_w=w, time=0.0)
+    spec = gpu.MomentumRhs(mass=[(2.9, dev(x))], visc=[(0.65, dev(x)), (0.3, dev(ug))],
+                           adv=[(0.5, dev(x), dev(w)), (0.25, dev(ug), dev(ug))],
+                           pres=[(1.0, dev(xp)), (-0.4, dev(xp))], dir_visc_coef=0.65, dir_adv_coef=0.5,
+                           dir_w=dev(w))
+    y = D.zeros()
+    gpu.momentum_rhs(D, spec, y)
+    assert rel(host(y), want) <= TOL_APPLY
+
+
+@pytest.mark.parametrize("n_el,ku,kp", [(3, 2, 1), (2, 3, 2), (2, 4, 3)])
+@pytest.mark.parametrize("outlet", [None, 1])
+def test_fast_rhs_matches_reference_and_generic(ref, gpu, n_el, ku, kp, outlet):
+    """Stage right-hand side through the fast launches (uniform grid) vs the reference
+    and the generic device kernel; also single-term lists (pressure only, mass only)."""
+    R, D = pair(ref, gpu, 3, n_el, ku, kp, 0.0, outlet=outlet, dirichlet_seed=4)
+    assert D.fast_path_active
+    un = gpu.seeded_uniform(61, R.n_u)
+    ug = gpu.seeded_uniform(62, R.n_u)
+    wv = gpu.seeded_uniform(63, R.n_u)
+    pp = gpu.seeded_uniform(64, R.n_p)
+    cases = [
+        (dict(mass=[(2.9, un)], visc=[(0.3, ug), (0.65, un)], adv=[(0.25, ug, ug), (0.5, un, un)],
+              pres=[(1.0, pp)], dir_visc=0.65, dir_adv=0.5, dir_w=wv), True),
+        (dict(pres=[(1.3, pp)]), False),
+        (dict(mass=[(0.7, ug)]), False),
+        (dict(adv=[(0.5, un, wv)], dir_adv=0.5, dir_w=wv), True),
+    ]
+    for kw, has_dir in cases:
+        want = R.momentum_rhs(time=0.0, **kw)
+        tr = lambda lst: [tuple(dev(v) if isinstance(v, np.ndarray) else v for v in t) for t in lst]
+        spec = gpu.MomentumRhs(mass=tr(kw.get("mass", [])), visc=tr(kw.get("visc", [])),
+                               adv=tr(kw.get("adv", [])), pres=tr(kw.get("pres", [])),
+                               dir_visc_coef=kw.get("dir_visc", 0.0), dir_adv_coef=kw.get("dir_adv", 0.0),
+                               dir_w=dev(kw["dir_w"]) if "dir_w" in kw else None)
+        outs = []
+        for fast in (True, False):
+            D.set_fast_path(fast)
+            y = D.zeros()
+            gpu.momentum_rhs(D, spec, y)
+            outs.append(host(y))
+            assert rel(outs[-1], want) <= TOL_APPLY, (kw.keys(), fast)
+        D.set_fast_path(True)
