@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdgb.so")
+LIB_PATH = os.environ.get("DGB_LIB") or os.path.join(_HERE, "libdgb.so")  # DGB_LIB: tuning builds only
 
 # status codes (include/dgb.h)
 OK, E_ARG, E_NO_CONVERGENCE, E_BREAKDOWN, E_NOT_SPD, E_ZERO_DIAG, E_CUDA, E_UNSUPPORTED, E_MISSING_FIELD = range(9)

@@ -68,26 +68,6 @@ __global__ void k_recip(size_t n, const double* __restrict__ d, double* __restri
 }
 
 // ---------------------------------------------------------------- reductions
-template <int NV>
-__device__ __forceinline__ void block_reduce_store(double (&acc)[NV], double* partial) {
-  __shared__ double red[NV][kBlasThreads / 32];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) {
-    double a = acc[v];
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    if ((threadIdx.x & 31) == 0) red[v][threadIdx.x >> 5] = a;
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      double a = threadIdx.x < (blockDim.x >> 5) ? red[v][threadIdx.x] : 0.0;
-      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      if (threadIdx.x == 0) partial[v * gridDim.x + blockIdx.x] = a;
-    }
-  }
-}
-
 __global__ void k_dot_part(size_t n, const double* __restrict__ x, const double* __restrict__ y,
                            double* __restrict__ partial) {
   double acc[1] = {0.0};
@@ -437,6 +417,10 @@ cudaError_t cg_alpha(cudaStream_t s, size_t n, const double* p, const double* q,
   const int g = blas_grid(n);
   k_cg_pq_part<<<g, kBlasThreads, 0, s>>>(n, p, q, scratch, st);
   k_cg_alpha_final<<<1, kBlasThreads, 0, s>>>(g, scratch, st);
+  return cudaGetLastError();
+}
+cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, const double* partial, CgState* st) {
+  k_cg_alpha_final<<<1, kBlasThreads, 0, s>>>(nparts, partial, st);
   return cudaGetLastError();
 }
 cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q, double* x, double* r,

@@ -12,6 +12,30 @@ namespace dgb {
 
 constexpr int kBlasThreads = 512;
 
+#ifdef __CUDACC__
+// per-block partial sums of NV accumulators -> partial[v * gridDim.x + blockIdx.x]
+// (blockDim.x a multiple of 32, <= kBlasThreads)
+template <int NV>
+__device__ __forceinline__ void block_reduce_store(double (&acc)[NV], double* partial) {
+  __shared__ double red[NV][kBlasThreads / 32];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double a = acc[v];
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((threadIdx.x & 31) == 0) red[v][threadIdx.x >> 5] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      double a = threadIdx.x < (blockDim.x >> 5) ? red[v][threadIdx.x] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (threadIdx.x == 0) partial[v * gridDim.x + blockIdx.x] = a;
+    }
+  }
+}
+#endif
+
 cudaError_t blas_init(int device);  // caches the SM count
 int blas_grid(size_t n);            // blocks for an n-element pass
 
@@ -67,6 +91,8 @@ cudaError_t cg_alpha(cudaStream_t s, size_t n, const double* p, const double* q,
 cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q, double* x, double* r,
                       const double* inv, double* z, double* scratch, CgState* st, double* hist);
 // MGS step with the projection read from device memory: w -= (*h) v_i ; *out = <w, v_next>
+// alpha = rho / sum(partial[0..nparts))  (CG with the <p,q> partials from a fused apply)
+cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, const double* partial, CgState* st);
 cudaError_t r_mgs_step_dev(cudaStream_t s, size_t n, const double* h, const double* vi, double* w,
                            const double* vnext, double* scratch, double* d_out);
 

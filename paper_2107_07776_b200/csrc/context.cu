@@ -470,8 +470,24 @@ int Context::cg(const dgb_operator& op, const dgb_solver_settings& s, const doub
     CK(cg_begin(st, n, r, inv, z, d_partial_, d_cg_));
     const int batch = 8;
     dc.mesh.skip = &d_cg_->done;
+    // scalar SIP operators on axis-aligned meshes: <p, q> fused into the apply's epilogue
+    const bool fused = use_fast && dc.axis && (op.op == DGB_OP_PRESSURE || op.op == DGB_OP_LAPLACE) &&
+                       fast_sip3_cg_blocks(dc) > 0;
+    const int fblocks = fused ? fast_sip3_cg_blocks(dc) : 0;
+    double* fpart = fused ? scratch_vec(25, fblocks) : nullptr;
+    if (fused && !fpart) return fail(DGB_E_CUDA, "cg: out of device memory");
     auto enqueue = [&](int slot) -> int {
       for (int b = 0; b < batch; ++b) {
+        if (fused) {
+          launches += 5;
+          const double mc = op.op == DGB_OP_PRESSURE ? op.coefs[0] : 0.0;
+          const int dir = op.op == DGB_OP_PRESSURE ? 0 : op.dirichlet_bdry;
+          CK(cg_direction(st, n, z, p, d_cg_));
+          CK(fast_sip3_cg(dc, mc, dir, p, q, fpart));
+          CK(cg_alpha_from_partials(st, fblocks, fpart, d_cg_));
+          CK(cg_update(st, n, p, q, x, r, inv, z, d_partial_, d_cg_, d_hist_));
+          continue;
+        }
         launches += 5;  // + the operator's own count
         CK(cg_direction(st, n, z, p, d_cg_));
         OK(apply_op(op, p, q));

@@ -29,6 +29,7 @@
 
 #include <type_traits>
 
+#include "blas.cuh"
 #include "dg_common.cuh"
 #include "dispatch.hpp"
 
@@ -338,11 +339,18 @@ struct SipAxisCfg {
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
 
-template <int KP, bool UNI>
+// CGF: the CG apply q = A p with the <p, q> partial of the block fused into the
+// epilogue (krylov.cpp:84-87): partial[block] = sum over the block's DoFs of p q.
+static_assert(SipAxisCfg<1>::T <= 256 && SipAxisCfg<2>::T <= 256 && SipAxisCfg<3>::T <= 256, "CG reduction buffer");
+struct SipCgArgs {
+  double* partial = nullptr;
+};
+
+template <int KP, bool UNI, bool CGF = false>
 __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff,
                                                                  double mc, int dir_bdry,
                                                                  const double* __restrict__ x,
-                                                                 double* __restrict__ y) {
+                                                                 double* __restrict__ y, SipCgArgs cg) {
   if (m.skip && *m.skip) return;
   using G = SipAxisCfg<KP>;
   using P = typename G::P;
@@ -454,6 +462,7 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
   }
   __syncthreads();
   // D: z-lines: y = M_z SX + SZ   -> global
+  double pq[1] = {0.0};
   for (int idx = tid; idx < nc * NF; idx += TT) {
     const int c = idx / NF, tl = idx - c * NF;
     const int i = tl % N, j = tl / N;
@@ -468,6 +477,19 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
 #pragma unroll
       for (int l = 0; l < N; ++l) s = fma(ta.M[k][l], a[l], s);
       yo[NF * k] = s;
+      if (CGF) pq[0] = fma(CELL(c)[G::O_U + b0 + k * P::PY], s, pq[0]);
+    }
+  }
+  if (CGF) {  // deterministic block sum for any blockDim (<= 256): lanes of warp 0 stride, then shuffle
+    __shared__ double red[256];
+    red[tid] = pq[0];
+    __syncthreads();
+    if (tid < 32) {
+      double a = 0.0;
+      for (int i = tid; i < TT; i += 32) a += red[i];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+      if (tid == 0) cg.partial[blockIdx.x] = a;
     }
   }
 #undef CELL
@@ -508,7 +530,11 @@ struct MomAxisCfg {
 template <int K, int MODE> struct MomAxisTune { static constexpr int C = 6, T = 192; static constexpr bool SPLIT = false; };
 template <int MODE> struct MomAxisTune<1, MODE> { static constexpr int C = 16, T = 128; static constexpr bool SPLIT = false; };
 template <int MODE> struct MomAxisTune<2, MODE> { static constexpr int C = 8, T = 192; static constexpr bool SPLIT = false; };
-template <> struct MomAxisTune<3, 0> { static constexpr int C = 3, T = 96; static constexpr bool SPLIT = false; };
+#ifndef DGB_MOM3_C  // tuning overrides for experiments (tools/tune_mom.sh)
+#define DGB_MOM3_C 6
+#define DGB_MOM3_T 192
+#endif
+template <> struct MomAxisTune<3, 0> { static constexpr int C = DGB_MOM3_C, T = DGB_MOM3_T; static constexpr bool SPLIT = false; };
 template <> struct MomAxisTune<3, 1> { static constexpr int C = 4, T = 128; static constexpr bool SPLIT = true; };
 template <> struct MomAxisTune<3, 2> { static constexpr int C = 3, T = 96; static constexpr bool SPLIT = true; };
 

@@ -61,18 +61,19 @@ static cudaError_t set_smem(KernelT kern, size_t smem) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-template <int KP>
-static cudaError_t run_sip_axis(const DevCtx& c, double mc, int dir, const double* x, double* y) {
+template <int KP, bool CGF = false>
+static cudaError_t run_sip_axis(const DevCtx& c, double mc, int dir, const double* x, double* y,
+                                SipCgArgs cg = SipCgArgs()) {
   using G = SipAxisCfg<KP>;
   cudaError_t e = ensure_ftab<KP + 1, KP + 1>();
   if (e != cudaSuccess) return e;
   const int grid = (c.ncells + G::C - 1) / G::C;
   if (c.ug.n > 0) {
-    if ((e = set_smem(k_sip_axis<KP, true>, G::SMEM)) != cudaSuccess) return e;
-    k_sip_axis<KP, true><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, mc, dir, x, y);
+    if ((e = set_smem(k_sip_axis<KP, true, CGF>, G::SMEM)) != cudaSuccess) return e;
+    k_sip_axis<KP, true, CGF><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, mc, dir, x, y, cg);
   } else {
-    if ((e = set_smem(k_sip_axis<KP, false>, G::SMEM)) != cudaSuccess) return e;
-    k_sip_axis<KP, false><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, mc, dir, x, y);
+    if ((e = set_smem(k_sip_axis<KP, false, CGF>, G::SMEM)) != cudaSuccess) return e;
+    k_sip_axis<KP, false, CGF><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, mc, dir, x, y, cg);
   }
   return cudaGetLastError();
 }
@@ -191,6 +192,26 @@ cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, doub
     case 1: return run_sip_axis<1>(c, mc, dir, x, y);
     case 2: return run_sip_axis<2>(c, mc, dir, x, y);
     case 3: return run_sip_axis<3>(c, mc, dir, x, y);
+  }
+  return cudaErrorNotSupported;
+}
+
+int fast_sip3_cg_blocks(const DevCtx& c) {
+  switch (c.kp) {
+    case 1: return (c.ncells + SipAxisCfg<1>::C - 1) / SipAxisCfg<1>::C;
+    case 2: return (c.ncells + SipAxisCfg<2>::C - 1) / SipAxisCfg<2>::C;
+    case 3: return (c.ncells + SipAxisCfg<3>::C - 1) / SipAxisCfg<3>::C;
+  }
+  return 0;
+}
+
+cudaError_t fast_sip3_cg(const DevCtx& c, double mc, int dir, const double* p, double* q, double* partial) {
+  SipCgArgs a;
+  a.partial = partial;
+  switch (c.kp) {
+    case 1: return run_sip_axis<1, true>(c, mc, dir, p, q, a);
+    case 2: return run_sip_axis<2, true>(c, mc, dir, p, q, a);
+    case 3: return run_sip_axis<3, true>(c, mc, dir, p, q, a);
   }
   return cudaErrorNotSupported;
 }
