@@ -520,7 +520,11 @@ struct MomAxisCfg {
   static constexpr int B_END = B_R2 + 6 * QQ * N;
   // face phase (all 6 faces at once): V1 [8 fields][6][Q x N] -> FB [3][6][N x N];  FL [3][6][Q x N]
   static constexpr int F_V1 = 0, F_FB = 0, F_FL = 48 * QN, F_END = F_FL + 18 * QN;
-  static constexpr int BF = B_END > F_END ? B_END : F_END;
+  // neighbour face traces [f][x0, x1, x2, w_normal][p + N q], filled during S0 / pass A and
+  // read by F1; disjoint from the pass-A regions and from V1
+  static constexpr int F_NB = A_END > 48 * QN ? A_END : 48 * QN, F_NB_END = F_NB + 24 * NF;
+  static constexpr int BF0 = B_END > F_END ? B_END : F_END;
+  static constexpr int BF = BF0 > F_NB_END ? BF0 : F_NB_END;
   static constexpr int WORK = MODE == 1 ? A_END : (MODE == 2 ? BF : (A_END > BF ? A_END : BF));
   static constexpr int PER = (O_WORK + WORK) | 1;
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
@@ -602,6 +606,21 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         }
       }
     }
+  if (faces) {  // neighbour w_a traces on each face (async; zeros on boundary faces)
+    for (int idx = tid; idx < nc * 6 * NF; idx += TT) {
+      const int c = idx / (6 * NF), r = idx - c * 6 * NF;
+      const int f = r / NF, t = r - f * NF;
+      const int a = f >> 1, p = t % N, q = t / N;
+      const int nb = cell_nbr<UNI>(m, ug, c0 + c, f);
+      const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
+      const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + ((f & 1) ? 0 : N - 1) * gst;
+      double* dst = WK(c) + G::F_NB + (4 * f + 3) * NF + t;
+      if (nb >= 0)
+        cp_async8(dst, w + (size_t)nb * 3 * NB + a * NB + go);
+      else
+        *dst = 0.0;
+    }
+  }
   load_info_par<TT, UNI>(sm, PER, G::O_INFO, nc, m, ug, aff, c0, sfac);
   cp_async_wait_all();
   __syncthreads();
@@ -634,6 +653,10 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         for (int l = 0; l < N; ++l) {
           uL[l] = inL ? CELL(nl - c0)[G::O_X + b0 + l * st] : nbL[d][j][l];
           uR[l] = inR ? CELL(nr - c0)[G::O_X + b0 + l * st] : nbR[d][j][l];
+        }
+        if (faces) {  // neighbour x traces for the advective faces (F1)
+          WK(c)[G::F_NB + (4 * (2 * d) + comp) * NF + tl] = uL[N - 1];
+          WK(c)[G::F_NB + (4 * (2 * d + 1) + comp) * NF + tl] = uR[0];
         }
         sip_line_bf<N, d>(ta, ci, u, uL, uR, co.visc, o);
         double* so = sdst + c * PER + b0;
@@ -725,9 +748,151 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
 
   } else {
     for (int idx = tid; idx < nc * 3 * CT; idx += TT) CELL(idx / (3 * CT))[G::O_OUT + idx % (3 * CT)] = 0.0;
+    if (faces) {
+      for (int idx = tid; idx < nc * 18 * NF; idx += TT) {
+        const int c = idx / (18 * NF), r = idx - c * 18 * NF;
+        const int f = r / (3 * NF), r2 = r - f * 3 * NF;
+        const int comp = r2 / NF, t = r2 - comp * NF;
+        const int a = f >> 1, p = t % N, q = t / N;
+        const int nb = INFO(c).nb[f];
+        const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
+        const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + ((f & 1) ? 0 : N - 1) * gst;
+        WK(c)[G::F_NB + (4 * f + comp) * NF + t] = nb >= 0 ? __ldg(x + (size_t)nb * 3 * NB + comp * NB + go) : 0.0;
+      }
+    }
     __syncthreads();
   }
 
+  // ------------------------------------------------------------------ LF advective faces, all 6 at once
+  if (faces) {
+    // F1: traces of u (3 comps, own + neighbour) and w_a (own + neighbour) on face-node line q,
+    //     contracted along p with B:  V1[field][f][qp + Q q]
+    for (int idx = tid; idx < nc * 6 * N; idx += TT) {
+      const int c = idx / (6 * N), r = idx - c * 6 * N;
+      const int f = r / N, q = r - f * N;
+      const int a = f >> 1, s = f & 1;
+      const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
+      const CellInfo& ci = INFO(c);
+      const int nb = ci.nb[f];
+      const int Ls = s ? N - 1 : 0, Lo = s ? 0 : N - 1;
+      double v[8][N];
+      const double* nbt = WK(c) + G::F_NB + 4 * f * NF + N * q;
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+#pragma unroll
+        for (int comp = 0; comp < 3; ++comp) v[3 + comp][p] = nbt[comp * NF + p];
+        v[7][p] = nbt[3 * NF + p];
+      }
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        const int li = a == 0 ? P::idx(Ls, p, q) : (a == 1 ? P::idx(p, Ls, q) : P::idx(p, q, Ls));
+#pragma unroll
+        for (int comp = 0; comp < 3; ++comp) v[comp][p] = CELL(c)[G::O_X + comp * CT + li];
+        v[6][p] = CELL(c)[G::O_W + a * CT + li];
+      }
+      double* o = WK(c) + G::F_V1 + f * QN + Q * q;
+#pragma unroll
+      for (int fl = 0; fl < 8; ++fl)
+#pragma unroll
+        for (int qp = 0; qp < Q; ++qp) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < N; ++l) acc = fma(tq.B[qp][l], v[fl][l], acc);
+          o[fl * 6 * QN + qp] = acc;
+        }
+    }
+    __syncthreads();
+    // F2: along q: values at the face Gauss points, LF flux, B^T back along q -> FL [comp][f][qp + Q l]
+    for (int idx = tid; idx < nc * 6 * Q; idx += TT) {
+      const int c = idx / (6 * Q), r = idx - c * 6 * Q;
+      const int f = r / Q, qp = r - f * Q;
+      const int a = f >> 1, s = f & 1;
+      const CellInfo& ci = INFO(c);
+      const double* in = WK(c) + G::F_V1 + f * QN + qp;
+      double v[8][N];
+#pragma unroll
+      for (int fl = 0; fl < 8; ++fl)
+#pragma unroll
+        for (int l = 0; l < N; ++l) v[fl][l] = in[fl * 6 * QN + Q * l];
+      const double sgn = s ? 1.0 : -1.0;
+      const double wbase = co.adv * ci.A[a] * tq.w[qp];
+      const int ty = ci.type[f];
+      double out[3][N];
+#pragma unroll
+      for (int comp = 0; comp < 3; ++comp)
+#pragma unroll
+        for (int l = 0; l < N; ++l) out[comp][l] = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < Q; ++qq) {
+        double val[8];
+#pragma unroll
+        for (int fl = 0; fl < 8; ++fl) {
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < N; ++l) acc = fma(tq.B[qq][l], v[fl][l], acc);
+          val[fl] = acc;
+        }
+        const double wq = wbase * tq.w[qq];
+        const double wns = sgn * val[6];
+        double fl3[3];
+        if (ty == 0) {  // forms.cpp:555-573
+          const double wno = sgn * val[7];
+          const double lam = RHS ? 0.0 : fmax(fabs(wns), fabs(wno));
+#pragma unroll
+          for (int comp = 0; comp < 3; ++comp)
+            fl3[comp] = wq * (0.5 * (val[comp] * wns + val[3 + comp] * wno) + 0.5 * lam * (val[comp] - val[3 + comp]));
+        } else {  // forms.cpp:592-599
+          const double cf = (RHS || ty == 2) ? wns : fabs(wns);  // rhs: forms.cpp:1036-1048
+#pragma unroll
+          for (int comp = 0; comp < 3; ++comp) fl3[comp] = wq * cf * val[comp];
+        }
+#pragma unroll
+        for (int comp = 0; comp < 3; ++comp)
+#pragma unroll
+          for (int l = 0; l < N; ++l) out[comp][l] = fma(tq.B[qq][l], fl3[comp], out[comp][l]);
+      }
+      double* o = WK(c) + G::F_FL + f * QN + qp;
+#pragma unroll
+      for (int comp = 0; comp < 3; ++comp)
+#pragma unroll
+        for (int l = 0; l < N; ++l) o[comp * 6 * QN + Q * l] = out[comp][l];
+    }
+    __syncthreads();
+    // F3: B^T along p -> nodal face contributions FB [comp][f][p + N q]
+    for (int idx = tid; idx < nc * 18 * N; idx += TT) {
+      const int c = idx / (18 * N), r = idx - c * 18 * N;
+      const int cf = r / N, q = r - cf * N;  // cf = comp*6 + f
+      const double* in = WK(c) + G::F_FL + cf * QN + Q * q;
+      double v[Q];
+#pragma unroll
+      for (int qp = 0; qp < Q; ++qp) v[qp] = in[qp];
+      double* o = WK(c) + G::F_FB + cf * NF + N * q;
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        double acc = 0.0;
+#pragma unroll
+        for (int qp = 0; qp < Q; ++qp) acc = fma(tq.B[qp][p], v[qp], acc);
+        o[p] = acc;
+      }
+    }
+    __syncthreads();
+    // gather the face-layer contributions into OUT (frees the work area for the cell stages)
+    for (int idx = tid; idx < nc * 3 * NB; idx += TT) {
+      const int c = idx / (3 * NB), r = idx - c * 3 * NB;
+      const int comp = r / NB, i = r - comp * NB;
+      const int ii[3] = {i % N, (i / N) % N, i / NF};
+      const double* fb = WK(c) + G::F_FB + comp * 6 * NF;
+      double v = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int t = (a == 0 ? ii[1] : ii[0]) + N * (a == 2 ? ii[1] : ii[2]);
+        if (ii[a] == 0) v += fb[(2 * a) * NF + t];
+        if (ii[a] == N - 1) v += fb[(2 * a + 1) * NF + t];
+      }
+      if (v != 0.0) CELL(c)[G::O_OUT + comp * CT + P::idx(ii[0], ii[1], ii[2])] += v;
+    }
+    __syncthreads();
+  }
   // ------------------------------------------------------------------ pass B cell (advection, rule k+2)
   if (faces) {
   // S45: xy-planes of the 6 fields (u0..2, w0..2) at z-layer k: B along x then y, in
@@ -853,136 +1018,12 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   __syncthreads();
   }
 
-  // ------------------------------------------------------------------ LF advective faces, all 6 at once
-  if (faces) {
-    // F1: traces of u (3 comps, own + neighbour) and w_a (own + neighbour) on face-node line q,
-    //     contracted along p with B:  V1[field][f][qp + Q q]
-    for (int idx = tid; idx < nc * 6 * N; idx += TT) {
-      const int c = idx / (6 * N), r = idx - c * 6 * N;
-      const int f = r / N, q = r - f * N;
-      const int a = f >> 1, s = f & 1;
-      const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
-      const CellInfo& ci = INFO(c);
-      const int nb = ci.nb[f];
-      const int Ls = s ? N - 1 : 0, Lo = s ? 0 : N - 1;
-      double v[8][N];
-#pragma unroll
-      for (int p = 0; p < N; ++p) {
-        const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + Lo * gst;
-#pragma unroll
-        for (int comp = 0; comp < 3; ++comp)
-          v[3 + comp][p] = nb >= 0 ? __ldg(x + (size_t)nb * 3 * NB + comp * NB + go) : 0.0;
-        v[7][p] = nb >= 0 ? __ldg(w + (size_t)nb * 3 * NB + a * NB + go) : 0.0;
-      }
-#pragma unroll
-      for (int p = 0; p < N; ++p) {
-        const int li = a == 0 ? P::idx(Ls, p, q) : (a == 1 ? P::idx(p, Ls, q) : P::idx(p, q, Ls));
-#pragma unroll
-        for (int comp = 0; comp < 3; ++comp) v[comp][p] = CELL(c)[G::O_X + comp * CT + li];
-        v[6][p] = CELL(c)[G::O_W + a * CT + li];
-      }
-      double* o = WK(c) + G::F_V1 + f * QN + Q * q;
-#pragma unroll
-      for (int fl = 0; fl < 8; ++fl)
-#pragma unroll
-        for (int qp = 0; qp < Q; ++qp) {
-          double acc = 0.0;
-#pragma unroll
-          for (int l = 0; l < N; ++l) acc = fma(tq.B[qp][l], v[fl][l], acc);
-          o[fl * 6 * QN + qp] = acc;
-        }
-    }
-    __syncthreads();
-    // F2: along q: values at the face Gauss points, LF flux, B^T back along q -> FL [comp][f][qp + Q l]
-    for (int idx = tid; idx < nc * 6 * Q; idx += TT) {
-      const int c = idx / (6 * Q), r = idx - c * 6 * Q;
-      const int f = r / Q, qp = r - f * Q;
-      const int a = f >> 1, s = f & 1;
-      const CellInfo& ci = INFO(c);
-      const double* in = WK(c) + G::F_V1 + f * QN + qp;
-      double v[8][N];
-#pragma unroll
-      for (int fl = 0; fl < 8; ++fl)
-#pragma unroll
-        for (int l = 0; l < N; ++l) v[fl][l] = in[fl * 6 * QN + Q * l];
-      const double sgn = s ? 1.0 : -1.0;
-      const double wbase = co.adv * ci.A[a] * tq.w[qp];
-      const int ty = ci.type[f];
-      double out[3][N];
-#pragma unroll
-      for (int comp = 0; comp < 3; ++comp)
-#pragma unroll
-        for (int l = 0; l < N; ++l) out[comp][l] = 0.0;
-#pragma unroll
-      for (int qq = 0; qq < Q; ++qq) {
-        double val[8];
-#pragma unroll
-        for (int fl = 0; fl < 8; ++fl) {
-          double acc = 0.0;
-#pragma unroll
-          for (int l = 0; l < N; ++l) acc = fma(tq.B[qq][l], v[fl][l], acc);
-          val[fl] = acc;
-        }
-        const double wq = wbase * tq.w[qq];
-        const double wns = sgn * val[6];
-        double fl3[3];
-        if (ty == 0) {  // forms.cpp:555-573
-          const double wno = sgn * val[7];
-          const double lam = RHS ? 0.0 : fmax(fabs(wns), fabs(wno));
-#pragma unroll
-          for (int comp = 0; comp < 3; ++comp)
-            fl3[comp] = wq * (0.5 * (val[comp] * wns + val[3 + comp] * wno) + 0.5 * lam * (val[comp] - val[3 + comp]));
-        } else {  // forms.cpp:592-599
-          const double cf = (RHS || ty == 2) ? wns : fabs(wns);  // rhs: forms.cpp:1036-1048
-#pragma unroll
-          for (int comp = 0; comp < 3; ++comp) fl3[comp] = wq * cf * val[comp];
-        }
-#pragma unroll
-        for (int comp = 0; comp < 3; ++comp)
-#pragma unroll
-          for (int l = 0; l < N; ++l) out[comp][l] = fma(tq.B[qq][l], fl3[comp], out[comp][l]);
-      }
-      double* o = WK(c) + G::F_FL + f * QN + qp;
-#pragma unroll
-      for (int comp = 0; comp < 3; ++comp)
-#pragma unroll
-        for (int l = 0; l < N; ++l) o[comp * 6 * QN + Q * l] = out[comp][l];
-    }
-    __syncthreads();
-    // F3: B^T along p -> nodal face contributions FB [comp][f][p + N q]
-    for (int idx = tid; idx < nc * 18 * N; idx += TT) {
-      const int c = idx / (18 * N), r = idx - c * 18 * N;
-      const int cf = r / N, q = r - cf * N;  // cf = comp*6 + f
-      const double* in = WK(c) + G::F_FL + cf * QN + Q * q;
-      double v[Q];
-#pragma unroll
-      for (int qp = 0; qp < Q; ++qp) v[qp] = in[qp];
-      double* o = WK(c) + G::F_FB + cf * NF + N * q;
-#pragma unroll
-      for (int p = 0; p < N; ++p) {
-        double acc = 0.0;
-#pragma unroll
-        for (int qp = 0; qp < Q; ++qp) acc = fma(tq.B[qp][p], v[qp], acc);
-        o[p] = acc;
-      }
-    }
-    __syncthreads();
-  }
-  // ------------------------------------------------------------------ store (+ gather the face-layer contributions)
+  // ------------------------------------------------------------------ store
   for (int idx = tid; idx < nc * 3 * NB; idx += TT) {
     const int c = idx / (3 * NB), r = idx - c * 3 * NB;
     const int comp = r / NB, i = r - comp * NB;
     const int ii[3] = {i % N, (i / N) % N, i / NF};
     double v = CELL(c)[G::O_OUT + comp * CT + P::idx(ii[0], ii[1], ii[2])];
-    if (faces) {
-      const double* fb = WK(c) + G::F_FB + comp * 6 * NF;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const int t = (a == 0 ? ii[1] : ii[0]) + N * (a == 2 ? ii[1] : ii[2]);
-        if (ii[a] == 0) v += fb[(2 * a) * NF + t];
-        if (ii[a] == N - 1) v += fb[(2 * a + 1) * NF + t];
-      }
-    }
     if (MODE == 2 || acc) v += y[(size_t)(c0 + c) * 3 * NB + r];
     y[(size_t)(c0 + c) * 3 * NB + r] = v;
   }
