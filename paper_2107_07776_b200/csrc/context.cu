@@ -177,7 +177,7 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
         }
       }
       if (uni && n > 1) {
-        dc.ug.n = n;
+        uniform_grid_set_divisor(dc.ug, n);
         dc.ug.ih = ih0;
         dc.ug.detJ = g[9];
         dc.ug.pen_int = pen[1];  // cell 0, face 1 is interior

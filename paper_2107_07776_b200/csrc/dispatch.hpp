@@ -49,9 +49,18 @@ struct RhsArgs {
 // no mesh-table loads (n == 0: use the tables).
 struct UniformGrid {
   int n = 0;
+  unsigned magic = 0, shift = 0;  // x / n == (umulhi(x, magic) + ((x - umulhi) >> 1)) >> (shift - 1), x < 2^32
   double ih = 0.0, detJ = 0.0, pen_int = 0.0, pen_bdry = 0.0;
   unsigned long long outlet_mask = 0;
 };
+// round-up multiplier for exact unsigned division by n >= 1 (Granlund-Montgomery)
+inline void uniform_grid_set_divisor(UniformGrid& g, int n) {
+  unsigned l = 0;
+  while ((1ull << l) < (unsigned long long)n) ++l;
+  g.n = n;
+  g.shift = l;
+  g.magic = (unsigned)(((1ull << 32) * ((1ull << l) - (unsigned long long)n)) / (unsigned long long)n + 1);
+}
 
 struct DevCtx {
   int dim = 0, ku = 0, kp = 0, ncells = 0;

@@ -114,9 +114,15 @@ __device__ __forceinline__ void load_info(CellInfo& ci, const MeshArgs& m, const
   }
 }
 
+__device__ __forceinline__ unsigned udiv_n(const UniformGrid& g, unsigned x) {
+  if (g.shift == 0) return x;  // n == 1
+  const unsigned t = __umulhi(x, g.magic);
+  return (t + ((x - t) >> 1)) >> (g.shift - 1);
+}
 __device__ __forceinline__ int uniform_nbr(const UniformGrid& g, int cell, int f) {
   const int n = g.n, d = f >> 1, s = f & 1;
-  const int co = d == 0 ? cell % n : (d == 1 ? (cell / n) % n : cell / (n * n));
+  const unsigned q1 = udiv_n(g, (unsigned)cell);
+  const int co = d == 0 ? cell - n * (int)q1 : (d == 1 ? (int)q1 - n * (int)udiv_n(g, q1) : (int)udiv_n(g, q1));
   const int stride = d == 0 ? 1 : (d == 1 ? n : n * n);
   if (s == 0) return co == 0 ? -1 - f : cell - stride;
   return co == n - 1 ? -1 - f : cell + stride;
@@ -607,18 +613,22 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       }
     }
   if (faces) {  // neighbour w_a traces on each face (async; zeros on boundary faces)
-    for (int idx = tid; idx < nc * 6 * NF; idx += TT) {
-      const int c = idx / (6 * NF), r = idx - c * 6 * NF;
-      const int f = r / NF, t = r - f * NF;
-      const int a = f >> 1, p = t % N, q = t / N;
+    for (int idx = tid; idx < nc * 6; idx += TT) {
+      const int c = idx / 6, f = idx - c * 6;
+      const int a = f >> 1;
       const int nb = cell_nbr<UNI>(m, ug, c0 + c, f);
       const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
-      const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + ((f & 1) ? 0 : N - 1) * gst;
-      double* dst = WK(c) + G::F_NB + (4 * f + 3) * NF + t;
-      if (nb >= 0)
-        cp_async8(dst, w + (size_t)nb * 3 * NB + a * NB + go);
-      else
-        *dst = 0.0;
+      double* dst = WK(c) + G::F_NB + (4 * f + 3) * NF;
+      const double* src = w + (size_t)(nb >= 0 ? nb : 0) * 3 * NB + a * NB + ((f & 1) ? 0 : N - 1) * gst;
+#pragma unroll
+      for (int t = 0; t < NF; ++t) {
+        const int p = t % N, q = t / N;
+        const int go = a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q);
+        if (nb >= 0)
+          cp_async8(dst + t, src + go);
+        else
+          dst[t] = 0.0;
+      }
     }
   }
   load_info_par<TT, UNI>(sm, PER, G::O_INFO, nc, m, ug, aff, c0, sfac);
@@ -771,10 +781,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       const int c = idx / (6 * N), r = idx - c * 6 * N;
       const int f = r / N, q = r - f * N;
       const int a = f >> 1, s = f & 1;
-      const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
-      const CellInfo& ci = INFO(c);
-      const int nb = ci.nb[f];
-      const int Ls = s ? N - 1 : 0, Lo = s ? 0 : N - 1;
+      const int Ls = s ? N - 1 : 0;
       double v[8][N];
       const double* nbt = WK(c) + G::F_NB + 4 * f * NF + N * q;
 #pragma unroll
