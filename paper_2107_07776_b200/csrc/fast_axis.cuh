@@ -525,10 +525,14 @@ struct MomAxisCfg {
   static constexpr int B_R2 = 9 * QQ * N;  // YB (6 QQN) then SA/SB (6 QNN)
   static constexpr int B_END = B_R2 + 6 * QQ * N;
   // face phase (all 6 faces at once): V1 [8 fields][6][Q x N] -> FB [3][6][N x N];  FL [3][6][Q x N]
-  static constexpr int F_V1 = 0, F_FB = 0, F_FL = 48 * QN, F_END = F_FL + 18 * QN;
-  // neighbour face traces [f][x0, x1, x2, w_normal][p + N q], filled during S0 / pass A and
-  // read by F1; disjoint from the pass-A regions and from V1
-  static constexpr int F_NB = A_END > 48 * QN ? A_END : 48 * QN, F_NB_END = F_NB + 24 * NF;
+  // V1 [field][q][f][qp]: face-Gauss-point rows of all 6 faces contiguous (F2 reads them
+  // conflict-free); the q-block stride VB is chosen so F1's (f, q) writes hit distinct banks
+  static constexpr int VB = K == 3 ? 36 : 6 * Q, V1_SIZE = 8 * N * VB;
+  static constexpr int F_V1 = 0, F_FL = V1_SIZE, F_END = F_FL + 18 * QN;
+  // neighbour face traces [f (stride NBS)][x0, x1, x2, w_normal][p + N q], filled during S0 /
+  // pass A and read by F1; disjoint from the pass-A regions and from V1
+  static constexpr int NBS = 4 * NF + 1;
+  static constexpr int F_NB = A_END > V1_SIZE ? A_END : V1_SIZE, F_NB_END = F_NB + 6 * NBS;
   static constexpr int BF0 = B_END > F_END ? B_END : F_END;
   static constexpr int BF = BF0 > F_NB_END ? BF0 : F_NB_END;
   static constexpr int WORK = MODE == 1 ? A_END : (MODE == 2 ? BF : (A_END > BF ? A_END : BF));
@@ -613,22 +617,18 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       }
     }
   if (faces) {  // neighbour w_a traces on each face (async; zeros on boundary faces)
-    for (int idx = tid; idx < nc * 6; idx += TT) {
-      const int c = idx / 6, f = idx - c * 6;
-      const int a = f >> 1;
+    for (int idx = tid; idx < nc * 6 * NF; idx += TT) {
+      const int c = idx / (6 * NF), r = idx - c * 6 * NF;
+      const int f = r / NF, t = r - f * NF;
+      const int a = f >> 1, p = t % N, q = t / N;
       const int nb = cell_nbr<UNI>(m, ug, c0 + c, f);
       const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
-      double* dst = WK(c) + G::F_NB + (4 * f + 3) * NF;
-      const double* src = w + (size_t)(nb >= 0 ? nb : 0) * 3 * NB + a * NB + ((f & 1) ? 0 : N - 1) * gst;
-#pragma unroll
-      for (int t = 0; t < NF; ++t) {
-        const int p = t % N, q = t / N;
-        const int go = a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q);
-        if (nb >= 0)
-          cp_async8(dst + t, src + go);
-        else
-          dst[t] = 0.0;
-      }
+      const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + ((f & 1) ? 0 : N - 1) * gst;
+      double* dst = WK(c) + G::F_NB + f * G::NBS + 3 * NF + t;
+      if (nb >= 0)
+        cp_async8(dst, w + (size_t)nb * 3 * NB + a * NB + go);
+      else
+        *dst = 0.0;
     }
   }
   load_info_par<TT, UNI>(sm, PER, G::O_INFO, nc, m, ug, aff, c0, sfac);
@@ -665,8 +665,8 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
           uR[l] = inR ? CELL(nr - c0)[G::O_X + b0 + l * st] : nbR[d][j][l];
         }
         if (faces) {  // neighbour x traces for the advective faces (F1)
-          WK(c)[G::F_NB + (4 * (2 * d) + comp) * NF + tl] = uL[N - 1];
-          WK(c)[G::F_NB + (4 * (2 * d + 1) + comp) * NF + tl] = uR[0];
+          WK(c)[G::F_NB + (2 * d) * G::NBS + comp * NF + tl] = uL[N - 1];
+          WK(c)[G::F_NB + (2 * d + 1) * G::NBS + comp * NF + tl] = uR[0];
         }
         sip_line_bf<N, d>(ta, ci, u, uL, uR, co.visc, o);
         double* so = sdst + c * PER + b0;
@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         const int nb = INFO(c).nb[f];
         const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
         const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + ((f & 1) ? 0 : N - 1) * gst;
-        WK(c)[G::F_NB + (4 * f + comp) * NF + t] = nb >= 0 ? __ldg(x + (size_t)nb * 3 * NB + comp * NB + go) : 0.0;
+        WK(c)[G::F_NB + f * G::NBS + comp * NF + t] = nb >= 0 ? __ldg(x + (size_t)nb * 3 * NB + comp * NB + go) : 0.0;
       }
     }
     __syncthreads();
@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       const int a = f >> 1, s = f & 1;
       const int Ls = s ? N - 1 : 0;
       double v[8][N];
-      const double* nbt = WK(c) + G::F_NB + 4 * f * NF + N * q;
+      const double* nbt = WK(c) + G::F_NB + f * G::NBS + N * q;
 #pragma unroll
       for (int p = 0; p < N; ++p) {
 #pragma unroll
@@ -797,7 +797,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         for (int comp = 0; comp < 3; ++comp) v[comp][p] = CELL(c)[G::O_X + comp * CT + li];
         v[6][p] = CELL(c)[G::O_W + a * CT + li];
       }
-      double* o = WK(c) + G::F_V1 + f * QN + Q * q;
+      double* o = WK(c) + G::F_V1 + q * G::VB + f * Q;
 #pragma unroll
       for (int fl = 0; fl < 8; ++fl)
 #pragma unroll
@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
           double acc = 0.0;
 #pragma unroll
           for (int l = 0; l < N; ++l) acc = fma(tq.B[qp][l], v[fl][l], acc);
-          o[fl * 6 * QN + qp] = acc;
+          o[fl * N * G::VB + qp] = acc;
         }
     }
     __syncthreads();
@@ -815,12 +815,12 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       const int f = r / Q, qp = r - f * Q;
       const int a = f >> 1, s = f & 1;
       const CellInfo& ci = INFO(c);
-      const double* in = WK(c) + G::F_V1 + f * QN + qp;
+      const double* in = WK(c) + G::F_V1 + f * Q + qp;
       double v[8][N];
 #pragma unroll
       for (int fl = 0; fl < 8; ++fl)
 #pragma unroll
-        for (int l = 0; l < N; ++l) v[fl][l] = in[fl * 6 * QN + Q * l];
+        for (int l = 0; l < N; ++l) v[fl][l] = in[fl * N * G::VB + l * G::VB];
       const double sgn = s ? 1.0 : -1.0;
       const double wbase = co.adv * ci.A[a] * tq.w[qp];
       const int ty = ci.type[f];
@@ -865,41 +865,32 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         for (int l = 0; l < N; ++l) o[comp * 6 * QN + Q * l] = out[comp][l];
     }
     __syncthreads();
-    // F3: B^T along p -> nodal face contributions FB [comp][f][p + N q]
-    for (int idx = tid; idx < nc * 18 * N; idx += TT) {
-      const int c = idx / (18 * N), r = idx - c * 18 * N;
-      const int cf = r / N, q = r - cf * N;  // cf = comp*6 + f
-      const double* in = WK(c) + G::F_FL + cf * QN + Q * q;
-      double v[Q];
+    // F3: B^T along p, added straight into OUT at the face nodes; one axis at a time so
+    //     edge / corner nodes shared by faces of different axes are never updated concurrently
+#pragma unroll 1
+    for (int a = 0; a < 3; ++a) {
+      for (int idx = tid; idx < nc * 6 * N; idx += TT) {
+        const int c = idx / (6 * N), r = idx - c * 6 * N;
+        const int cs = r / N, q = r - cs * N;  // cs = comp * 2 + side
+        const int comp = cs >> 1, f = 2 * a + (cs & 1);
+        const double* in = WK(c) + G::F_FL + (comp * 6 + f) * QN + Q * q;
+        double v[Q];
 #pragma unroll
-      for (int qp = 0; qp < Q; ++qp) v[qp] = in[qp];
-      double* o = WK(c) + G::F_FB + cf * NF + N * q;
+        for (int qp = 0; qp < Q; ++qp) v[qp] = in[qp];
+        const int L = (f & 1) ? N - 1 : 0;
+        double* o = CELL(c) + G::O_OUT + comp * CT;
 #pragma unroll
-      for (int p = 0; p < N; ++p) {
-        double acc = 0.0;
+        for (int p = 0; p < N; ++p) {
+          double acc = 0.0;
 #pragma unroll
-        for (int qp = 0; qp < Q; ++qp) acc = fma(tq.B[qp][p], v[qp], acc);
-        o[p] = acc;
+          for (int qp = 0; qp < Q; ++qp) acc = fma(tq.B[qp][p], v[qp], acc);
+          o[a == 0 ? P::idx(L, p, q) : (a == 1 ? P::idx(p, L, q) : P::idx(p, q, L))] += acc;
+        }
       }
+      __syncthreads();
     }
-    __syncthreads();
-    // gather the face-layer contributions into OUT (frees the work area for the cell stages)
-    for (int idx = tid; idx < nc * 3 * NB; idx += TT) {
-      const int c = idx / (3 * NB), r = idx - c * 3 * NB;
-      const int comp = r / NB, i = r - comp * NB;
-      const int ii[3] = {i % N, (i / N) % N, i / NF};
-      const double* fb = WK(c) + G::F_FB + comp * 6 * NF;
-      double v = 0.0;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const int t = (a == 0 ? ii[1] : ii[0]) + N * (a == 2 ? ii[1] : ii[2]);
-        if (ii[a] == 0) v += fb[(2 * a) * NF + t];
-        if (ii[a] == N - 1) v += fb[(2 * a + 1) * NF + t];
-      }
-      if (v != 0.0) CELL(c)[G::O_OUT + comp * CT + P::idx(ii[0], ii[1], ii[2])] += v;
-    }
-    __syncthreads();
   }
+
   // ------------------------------------------------------------------ pass B cell (advection, rule k+2)
   if (faces) {
   // S45: xy-planes of the 6 fields (u0..2, w0..2) at z-layer k: B along x then y, in
