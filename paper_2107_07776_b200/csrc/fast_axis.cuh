@@ -573,6 +573,23 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   const int tid = threadIdx.x;
   const double sfac = (double)((K + 1) * (K + 1));
   const bool faces = MODE != 1 && co.adv != 0.0;
+  // WPC: one warp per cell when the CTA has exactly 32 threads per cell.  After the
+  // CTA-wide staging barrier every stage touches only its own cell (neighbour data is
+  // read from the staged x or the trace stash), so stages sync with __syncwarp.
+  constexpr bool WPC = TT == 32 * C;
+  const int lane = tid & 31, wcell = tid >> 5;
+  const int it0 = WPC ? lane : tid;
+  constexpr int IST = WPC ? 32 : TT;
+#define ITEMS(X) (WPC ? (wcell < nc ? (X) : 0) : nc * (X))
+#define CELLOF(idx, X) (WPC ? wcell : (idx) / (X))
+#define RESTOF(idx, c, X) (WPC ? (idx) : (idx) - (c) * (X))
+#define SYNC_CELL()    \
+  do {                 \
+    if (WPC)           \
+      __syncwarp();    \
+    else               \
+      __syncthreads(); \
+  } while (0)
 #define CELL(c) (sm + (c) * PER)
 #define WK(c) (sm + (c) * PER + G::O_WORK)
 #define INFO(c) (*reinterpret_cast<CellInfo*>(sm + (c) * PER + G::O_INFO))
@@ -591,17 +608,17 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   // direction: (cell, comp, line) with the line index fastest.
   const bool passA = MODE != 2 && (co.mass != 0.0 || co.visc != 0.0);
   constexpr int NID = 3 * NF;                      // items per cell and direction
-  constexpr int MAXJ = (C * NID + TT - 1) / TT;    // items per thread and direction
+  constexpr int MAXJ = WPC ? (NID + 31) / 32 : (C * NID + TT - 1) / TT;  // items per thread and direction
   double nbL[3][MAXJ][N], nbR[3][MAXJ][N];
 #pragma unroll
   for (int d = 0; d < 3; ++d)
 #pragma unroll
     for (int j = 0; j < MAXJ; ++j) {
-      const int it = tid + j * TT;
+      const int it = it0 + j * IST;
 #pragma unroll
       for (int l = 0; l < N; ++l) nbL[d][j][l] = nbR[d][j][l] = 0.0;
-      if (passA && it < nc * NID) {
-        const int c = it / NID, r = it - c * NID;
+      if (passA && it < ITEMS(NID)) {
+        const int c = CELLOF(it, NID), r = RESTOF(it, c, NID);
         const int comp = r / NF, tl = r - comp * NF;
         const int p = tl % N, q = tl / N;
         const int nl = cell_nbr<UNI>(m, ug, c0 + c, 2 * d), nr = cell_nbr<UNI>(m, ug, c0 + c, 2 * d + 1);
@@ -634,8 +651,11 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   load_info_par<TT, UNI>(sm, PER, G::O_INFO, nc, m, ug, aff, c0, sfac);
   cp_async_wait_all();
   __syncthreads();
-  for (int idx = tid; idx < nc * 6; idx += TT) face_coefs(INFO(idx / 6), idx % 6, true, true, RHS);
-  __syncthreads();
+  for (int idx = it0; idx < ITEMS(6); idx += IST) {
+    const int c = CELLOF(idx, 6);
+    face_coefs(INFO(c), RESTOF(idx, c, 6), true, true, RHS);
+  }
+  SYNC_CELL();
 
   // ------------------------------------------------------------------ pass A: mass + viscous (line split)
   if (passA) {
@@ -646,9 +666,9 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
     double* sdst = WK(0) + (d == 0 ? G::A_SX : (d == 1 ? G::A_SY : G::A_SZ));
 #pragma unroll
     for (int j = 0; j < MAXJ; ++j) {
-      const int it = tid + j * TT;
-      if (it < nc * NID) {
-        const int c = it / NID, r = it - c * NID;
+      const int it = it0 + j * IST;
+      if (it < ITEMS(NID)) {
+        const int c = CELLOF(it, NID), r = RESTOF(it, c, NID);
         const int comp = r / NF, tl = r - comp * NF;
         const int p = tl % N, q = tl / N;
         const CellInfo& ci = INFO(c);
@@ -687,10 +707,10 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   stage_a(std::integral_constant<int, 0>{});
   stage_a(std::integral_constant<int, 1>{});
   stage_a(std::integral_constant<int, 2>{});
-  __syncthreads();
+  SYNC_CELL();
   // B: x-lines in place: SY <- M_x SY, SZ <- M_x SZ
-  for (int idx = tid; idx < nc * 3 * NF; idx += TT) {
-    const int c = idx / (3 * NF), r = idx - c * 3 * NF;
+  for (int idx = it0; idx < ITEMS(3 * NF); idx += IST) {
+    const int c = CELLOF(idx, 3 * NF), r = RESTOF(idx, c, 3 * NF);
     const int comp = r / NF, tl = r - comp * NF;
     const int b0 = comp * CT + P::idx(0, tl % N, tl / N);
     double a[N], b[N];
@@ -711,10 +731,10 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       WK(c)[G::A_SZ + b0 + i] = t;
     }
   }
-  __syncthreads();
+  SYNC_CELL();
   // C: y-lines: SX <- M_y (SX + mass detJ UX) + SY ; SZ <- M_y SZ
-  for (int idx = tid; idx < nc * 3 * NF; idx += TT) {
-    const int c = idx / (3 * NF), r = idx - c * 3 * NF;
+  for (int idx = it0; idx < ITEMS(3 * NF); idx += IST) {
+    const int c = CELLOF(idx, 3 * NF), r = RESTOF(idx, c, 3 * NF);
     const int comp = r / NF, tl = r - comp * NF;
     const int b0 = comp * CT + P::idx(tl % N, 0, tl / N);
     const double cm = co.mass * INFO(c).detJ;
@@ -737,10 +757,10 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       WK(c)[G::A_SZ + b0 + j * P::PX] = t;
     }
   }
-  __syncthreads();
+  SYNC_CELL();
   // D: z-lines: OUT = M_z SX + SZ
-  for (int idx = tid; idx < nc * 3 * NF; idx += TT) {
-    const int c = idx / (3 * NF), r = idx - c * 3 * NF;
+  for (int idx = it0; idx < ITEMS(3 * NF); idx += IST) {
+    const int c = CELLOF(idx, 3 * NF), r = RESTOF(idx, c, 3 * NF);
     const int comp = r / NF, tl = r - comp * NF;
     const int b0 = comp * CT + P::idx(tl % N, tl / N, 0);
     double a[N];
@@ -754,13 +774,16 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       CELL(c)[G::O_OUT + b0 + k * P::PY] = s;
     }
   }
-  __syncthreads();
+  SYNC_CELL();
 
   } else {
-    for (int idx = tid; idx < nc * 3 * CT; idx += TT) CELL(idx / (3 * CT))[G::O_OUT + idx % (3 * CT)] = 0.0;
+    for (int idx = it0; idx < ITEMS(3 * CT); idx += IST) {
+      const int c = CELLOF(idx, 3 * CT);
+      CELL(c)[G::O_OUT + RESTOF(idx, c, 3 * CT)] = 0.0;
+    }
     if (faces) {
-      for (int idx = tid; idx < nc * 18 * NF; idx += TT) {
-        const int c = idx / (18 * NF), r = idx - c * 18 * NF;
+      for (int idx = it0; idx < ITEMS(18 * NF); idx += IST) {
+        const int c = CELLOF(idx, 18 * NF), r = RESTOF(idx, c, 18 * NF);
         const int f = r / (3 * NF), r2 = r - f * 3 * NF;
         const int comp = r2 / NF, t = r2 - comp * NF;
         const int a = f >> 1, p = t % N, q = t / N;
@@ -770,15 +793,15 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         WK(c)[G::F_NB + f * G::NBS + comp * NF + t] = nb >= 0 ? __ldg(x + (size_t)nb * 3 * NB + comp * NB + go) : 0.0;
       }
     }
-    __syncthreads();
+    SYNC_CELL();
   }
 
   // ------------------------------------------------------------------ LF advective faces, all 6 at once
   if (faces) {
     // F1: traces of u (3 comps, own + neighbour) and w_a (own + neighbour) on face-node line q,
     //     contracted along p with B:  V1[field][f][qp + Q q]
-    for (int idx = tid; idx < nc * 6 * N; idx += TT) {
-      const int c = idx / (6 * N), r = idx - c * 6 * N;
+    for (int idx = it0; idx < ITEMS(6 * N); idx += IST) {
+      const int c = CELLOF(idx, 6 * N), r = RESTOF(idx, c, 6 * N);
       const int f = r / N, q = r - f * N;
       const int a = f >> 1, s = f & 1;
       const int Ls = s ? N - 1 : 0;
@@ -808,10 +831,10 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
           o[fl * N * G::VB + qp] = acc;
         }
     }
-    __syncthreads();
+    SYNC_CELL();
     // F2: along q: values at the face Gauss points, LF flux, B^T back along q -> FL [comp][f][qp + Q l]
-    for (int idx = tid; idx < nc * 6 * Q; idx += TT) {
-      const int c = idx / (6 * Q), r = idx - c * 6 * Q;
+    for (int idx = it0; idx < ITEMS(6 * Q); idx += IST) {
+      const int c = CELLOF(idx, 6 * Q), r = RESTOF(idx, c, 6 * Q);
       const int f = r / Q, qp = r - f * Q;
       const int a = f >> 1, s = f & 1;
       const CellInfo& ci = INFO(c);
@@ -864,13 +887,13 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
 #pragma unroll
         for (int l = 0; l < N; ++l) o[comp * 6 * QN + Q * l] = out[comp][l];
     }
-    __syncthreads();
+    SYNC_CELL();
     // F3: B^T along p, added straight into OUT at the face nodes; one axis at a time so
     //     edge / corner nodes shared by faces of different axes are never updated concurrently
 #pragma unroll 1
     for (int a = 0; a < 3; ++a) {
-      for (int idx = tid; idx < nc * 6 * N; idx += TT) {
-        const int c = idx / (6 * N), r = idx - c * 6 * N;
+      for (int idx = it0; idx < ITEMS(6 * N); idx += IST) {
+        const int c = CELLOF(idx, 6 * N), r = RESTOF(idx, c, 6 * N);
         const int cs = r / N, q = r - cs * N;  // cs = comp * 2 + side
         const int comp = cs >> 1, f = 2 * a + (cs & 1);
         const double* in = WK(c) + G::F_FL + (comp * 6 + f) * QN + Q * q;
@@ -887,7 +910,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
           o[a == 0 ? P::idx(L, p, q) : (a == 1 ? P::idx(p, L, q) : P::idx(p, q, L))] += acc;
         }
       }
-      __syncthreads();
+      SYNC_CELL();
     }
   }
 
@@ -895,8 +918,8 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   if (faces) {
   // S45: xy-planes of the 6 fields (u0..2, w0..2) at z-layer k: B along x then y, in
   //      registers  -> YB[f][k][qy][qx]
-  for (int idx = tid; idx < nc * 6 * N; idx += TT) {
-    const int c = idx / (6 * N), r = idx - c * 6 * N;
+  for (int idx = it0; idx < ITEMS(6 * N); idx += IST) {
+    const int c = CELLOF(idx, 6 * N), r = RESTOF(idx, c, 6 * N);
     const int f = r / N, k = r - f * N;
     const double* in = CELL(c) + (f < 3 ? G::O_X + f * CT : G::O_W + (f - 3) * CT) + P::idx(0, 0, k);
     double pl[N][N];  // [j][i]
@@ -925,10 +948,10 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         o[qx + Q * qy] = sacc;
       }
   }
-  __syncthreads();
+  SYNC_CELL();
   // S6: fused z: evaluate 6 columns, pointwise advective flux, z-integration of the 3x3 gradient tests
-  for (int idx = tid; idx < nc * QQ; idx += TT) {
-    const int c = idx / QQ, qxy = idx - c * QQ;
+  for (int idx = it0; idx < ITEMS(QQ); idx += IST) {
+    const int c = CELLOF(idx, QQ), qxy = RESTOF(idx, c, QQ);
     const CellInfo& ci = INFO(c);
     const double wxy = ci.detJ * tq.w[qxy % Q] * tq.w[qxy / Q];
     double col[6][Q];
@@ -973,11 +996,11 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       }
     }
   }
-  __syncthreads();
+  SYNC_CELL();
   // S78: per (component, z-layer l): y- then x-integration of the three gradient tests,
   //      qx by qx in registers, accumulated into OUT
-  for (int idx = tid; idx < nc * 3 * N; idx += TT) {
-    const int c = idx / (3 * N), r = idx - c * 3 * N;
+  for (int idx = it0; idx < ITEMS(3 * N); idx += IST) {
+    const int c = CELLOF(idx, 3 * N), r = RESTOF(idx, c, 3 * N);
     const int comp = r / N, l = r - comp * N;
     const double* tp = WK(c) + G::B_R1 + comp * 3 * QQ * N + QQ * l;
     double acc[N][N];  // [j][i]
@@ -1013,12 +1036,12 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
 #pragma unroll
       for (int i = 0; i < N; ++i) o[i + P::PX * j] += acc[j][i];
   }
-  __syncthreads();
+  SYNC_CELL();
   }
 
   // ------------------------------------------------------------------ store
-  for (int idx = tid; idx < nc * 3 * NB; idx += TT) {
-    const int c = idx / (3 * NB), r = idx - c * 3 * NB;
+  for (int idx = it0; idx < ITEMS(3 * NB); idx += IST) {
+    const int c = CELLOF(idx, 3 * NB), r = RESTOF(idx, c, 3 * NB);
     const int comp = r / NB, i = r - comp * NB;
     const int ii[3] = {i % N, (i / N) % N, i / NF};
     double v = CELL(c)[G::O_OUT + comp * CT + P::idx(ii[0], ii[1], ii[2])];
@@ -1028,6 +1051,10 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
 #undef CELL
 #undef WK
 #undef INFO
+#undef ITEMS
+#undef CELLOF
+#undef RESTOF
+#undef SYNC_CELL
 }
 
 // ===========================================================================
