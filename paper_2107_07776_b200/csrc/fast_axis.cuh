@@ -999,13 +999,16 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   SYNC_CELL();
   // S78: per (component, z-layer l): y- then x-integration of the three gradient tests,
   //      qx by qx in registers, accumulated into OUT
-  for (int idx = it0; idx < ITEMS(3 * N); idx += IST) {
-    const int c = CELLOF(idx, 3 * N), r = RESTOF(idx, c, 3 * N);
-    const int comp = r / N, l = r - comp * N;
+  // (items split over halves of the output y-rows so a warp-cell keeps more lanes busy)
+  constexpr int JH = WPC ? 2 : 1, NJ = (N + JH - 1) / JH;
+  for (int idx = it0; idx < ITEMS(3 * N * JH); idx += IST) {
+    const int c = CELLOF(idx, 3 * N * JH), r = RESTOF(idx, c, 3 * N * JH);
+    const int comp = r / (N * JH), r2 = r - comp * N * JH;
+    const int l = r2 / JH, j0 = (r2 - l * JH) * NJ;
     const double* tp = WK(c) + G::B_R1 + comp * 3 * QQ * N + QQ * l;
-    double acc[N][N];  // [j][i]
+    double acc[NJ][N];  // [j - j0][i]
 #pragma unroll
-    for (int j = 0; j < N; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int i = 0; i < N; ++i) acc[j][i] = 0.0;
 #pragma unroll
@@ -1018,23 +1021,27 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         vx[qy] = tp[2 * QQ * N + qx + Q * qy];
       }
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        double sa = 0.0, sb = 0.0;
+      for (int jj = 0; jj < NJ; ++jj) {
+        const int j = j0 + jj;
+        if (j < N) {
+          double sa = 0.0, sb = 0.0;
 #pragma unroll
-        for (int qy = 0; qy < Q; ++qy) {
-          sa = fma(tq.B[qy][j], vz[qy], sa);
-          sa = fma(tq.D[qy][j], vy[qy], sa);
-          sb = fma(tq.B[qy][j], vx[qy], sb);
+          for (int qy = 0; qy < Q; ++qy) {
+            sa = fma(tq.B[qy][j], vz[qy], sa);
+            sa = fma(tq.D[qy][j], vy[qy], sa);
+            sb = fma(tq.B[qy][j], vx[qy], sb);
+          }
+#pragma unroll
+          for (int i = 0; i < N; ++i) acc[jj][i] = fma(tq.B[qx][i], sa, fma(tq.D[qx][i], sb, acc[jj][i]));
         }
-#pragma unroll
-        for (int i = 0; i < N; ++i) acc[j][i] = fma(tq.B[qx][i], sa, fma(tq.D[qx][i], sb, acc[j][i]));
       }
     }
     double* o = CELL(c) + G::O_OUT + comp * CT + P::idx(0, 0, l);
 #pragma unroll
-    for (int j = 0; j < N; ++j)
+    for (int jj = 0; jj < NJ; ++jj)
 #pragma unroll
-      for (int i = 0; i < N; ++i) o[i + P::PX * j] += acc[j][i];
+      for (int i = 0; i < N; ++i)
+        if (j0 + jj < N) o[i + P::PX * (j0 + jj)] += acc[jj][i];
   }
   SYNC_CELL();
   }
