@@ -337,8 +337,12 @@ template <int KP>
 struct SipAxisCfg {
   static constexpr int N = KP + 1, NB = N * N * N, NF = N * N;
   using P = Pad<N>;
-  static constexpr int C = KP == 1 ? 32 : (KP == 2 ? 16 : 8);  // cells per CTA
-  static constexpr int T = KP == 1 ? 128 : (KP == 2 ? 144 : 128);
+#ifndef DGB_SIP2_C  // tuning overrides for experiments (tools/tune_sip.sh)
+#define DGB_SIP2_C 16
+#define DGB_SIP2_T 128
+#endif
+  static constexpr int C = KP == 1 ? 32 : (KP == 2 ? DGB_SIP2_C : 8);  // cells per CTA
+  static constexpr int T = KP == 1 ? 128 : (KP == 2 ? DGB_SIP2_T : 128);
   static constexpr int O_U = 0, O_SX = P::CT, O_SY = 2 * P::CT, O_SZ = 3 * P::CT, O_UX = 4 * P::CT;
   static constexpr int O_INFO = 5 * P::CT;
   static constexpr int PER = (O_INFO + kInfoDoubles) | 1;
