@@ -278,25 +278,39 @@ struct GsPack {
   const double* u[kGsChunk];
 };
 // NV basis vectors per pass, compile-time so that every load of an element
-// iteration is issued before the first FMA (a runtime bound serialises them)
+// iteration is issued before the first FMA (a runtime bound serialises them).
+// Pairs of elements per thread (16-byte loads); the basis slots, w and uk are
+// 16-byte aligned (pool allocations); an odd tail element is taken by thread 0.
+constexpr int kGsThreads = 256;
 template <int NV>
-__global__ void __launch_bounds__(kBlasThreads) k_gs_dots_part(size_t n, GsPack P, const double* __restrict__ w,
-                                                             const double* __restrict__ uk, int nl,
-                                                             double* __restrict__ partial) {
+__global__ void __launch_bounds__(kGsThreads) k_gs_dots_part(size_t n, GsPack P, const double* __restrict__ w,
+                                                           const double* __restrict__ uk, int nl,
+                                                           double* __restrict__ partial) {
   double acc[2 * NV];
 #pragma unroll
   for (int j = 0; j < 2 * NV; ++j) acc[j] = 0.0;
   const double* ub = nl > 0 ? uk : w;  // harmless stand-in when there is no Gram row
-  GRID_STRIDE(i, n) {
-    const double wi = w[i];
-    const double ui = ub[i];
-    double v[NV];
+  const size_t n2 = n >> 1;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  const double2* u2 = reinterpret_cast<const double2*>(ub);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (size_t)gridDim.x * blockDim.x) {
+    const double2 wi = w2[i];
+    const double2 ui = u2[i];
+    double2 v[NV];
 #pragma unroll
-    for (int j = 0; j < NV; ++j) v[j] = P.u[j][i];
+    for (int j = 0; j < NV; ++j) v[j] = reinterpret_cast<const double2*>(P.u[j])[i];
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      acc[j] = fma(v[j], wi, acc[j]);
-      acc[NV + j] = fma(v[j], ui, acc[NV + j]);
+      acc[j] = fma(v[j].y, wi.y, fma(v[j].x, wi.x, acc[j]));
+      acc[NV + j] = fma(v[j].y, ui.y, fma(v[j].x, ui.x, acc[NV + j]));
+    }
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const size_t i = n - 1;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      acc[j] = fma(P.u[j][i], w[i], acc[j]);
+      acc[NV + j] = fma(P.u[j][i], ub[i], acc[NV + j]);
     }
   }
   block_reduce_store<2 * NV>(acc, partial);
@@ -318,20 +332,33 @@ __global__ void k_gs_solve(int k, const double* __restrict__ ab, double* __restr
   }
 }
 template <int NV>
-__global__ void __launch_bounds__(kBlasThreads) k_gs_update_part(size_t n, GsPack P, const double* __restrict__ g,
-                                                               double* __restrict__ w, int want_norm,
-                                                               double* __restrict__ partial) {
+__global__ void __launch_bounds__(kGsThreads) k_gs_update_part(size_t n, GsPack P, const double* __restrict__ g,
+                                                             double* __restrict__ w, int want_norm,
+                                                             double* __restrict__ partial) {
   double c[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) c[j] = g[j];
   double acc[1] = {0.0};
-  GRID_STRIDE(i, n) {
-    double v[NV];
+  const size_t n2 = n >> 1;
+  double2* w2 = reinterpret_cast<double2*>(w);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (size_t)gridDim.x * blockDim.x) {
+    double2 v[NV];
 #pragma unroll
-    for (int j = 0; j < NV; ++j) v[j] = P.u[j][i];
+    for (int j = 0; j < NV; ++j) v[j] = reinterpret_cast<const double2*>(P.u[j])[i];
+    double2 wi = w2[i];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      wi.x = fma(-c[j], v[j].x, wi.x);
+      wi.y = fma(-c[j], v[j].y, wi.y);
+    }
+    w2[i] = wi;
+    acc[0] = fma(wi.y, wi.y, fma(wi.x, wi.x, acc[0]));
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const size_t i = n - 1;
     double wi = w[i];
 #pragma unroll
-    for (int j = 0; j < NV; ++j) wi = fma(-c[j], v[j], wi);
+    for (int j = 0; j < NV; ++j) wi = fma(-c[j], P.u[j][i], wi);
     w[i] = wi;
     acc[0] = fma(wi, wi, acc[0]);
   }
@@ -430,16 +457,23 @@ cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q
   k_cg_upd_final<<<1, kBlasThreads, 0, s>>>(g, scratch, st, hist);
   return cudaGetLastError();
 }
+static int gs_grid(size_t n) {
+  size_t g = ((n >> 1) + kGsThreads - 1) / kGsThreads;
+  const size_t cap = (size_t)g_sms * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
 cudaError_t gs_dots(cudaStream_t s, size_t n, int nv, const double* const* U, const double* w, const double* uk,
                     int nl, double* scratch, double* d_ab) {
   if (nv < 1 || nv > kGsChunk || nl > nv) return cudaErrorInvalidValue;
   GsPack P{};
   for (int j = 0; j < nv; ++j) P.u[j] = U[j];
-  const int g = blas_grid(n);
+  const int g = gs_grid(n);
   switch (nv) {
 #define GS_CASE(NV)                                                               \
   case NV:                                                                        \
-    k_gs_dots_part<NV><<<g, kBlasThreads, 0, s>>>(n, P, w, uk, nl, scratch);      \
+    k_gs_dots_part<NV><<<g, kGsThreads, 0, s>>>(n, P, w, uk, nl, scratch);        \
     k_sum_parts<<<1, kBlasThreads, 0, s>>>(g, NV, scratch, d_ab, 0);              \
     if (nl > 0) k_sum_parts<<<1, kBlasThreads, 0, s>>>(g, NV, scratch + (size_t)NV * g, d_ab + kGsChunk, 0); \
     break;
@@ -459,10 +493,10 @@ cudaError_t gs_update(cudaStream_t s, size_t n, int nv, const double* const* U, 
   if (nv < 1 || nv > kGsChunk) return cudaErrorInvalidValue;
   GsPack P{};
   for (int j = 0; j < nv; ++j) P.u[j] = U[j];
-  const int gr = blas_grid(n);
+  const int gr = gs_grid(n);
   switch (nv) {
 #define GS_CASE(NV)                                                                          \
-  case NV: k_gs_update_part<NV><<<gr, kBlasThreads, 0, s>>>(n, P, g, w, norm_out ? 1 : 0, scratch); break;
+  case NV: k_gs_update_part<NV><<<gr, kGsThreads, 0, s>>>(n, P, g, w, norm_out ? 1 : 0, scratch); break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6) GS_CASE(7) GS_CASE(8)
     GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12) GS_CASE(13) GS_CASE(14) GS_CASE(15) GS_CASE(16)
 #undef GS_CASE

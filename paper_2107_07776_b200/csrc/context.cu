@@ -44,7 +44,7 @@ Context::~Context() {
   if (dc.stream) cudaStreamSynchronize(dc.stream);
   for (void* p : allocs_) cudaFree(p);
   for (auto& s : slots_) cudaFree(s.first);
-  for (double* v : gm_basis_) cudaFree(v);
+  for (double* v : gm_raw_) cudaFree(v);
   if (h_res_) cudaFreeHost(h_res_);
   if (h_cg_) cudaFreeHost(h_cg_);
   if (h_gm_) cudaFreeHost(h_gm_);
@@ -547,7 +547,8 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
   const int m = std::max(1, s.restart);
   if (gm_n_ != n) {
     cudaStreamSynchronize(st);
-    for (double* v : gm_basis_) cudaFree(v);
+    for (double* v : gm_raw_) cudaFree(v);
+    gm_raw_.clear();
     gm_basis_.clear();
     gm_n_ = n;
   }
@@ -558,7 +559,7 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
   // device scalars: Gram matrix L (ldl x ldl), scales s_j, projections h, update coefficients g, chunk dots
   const int ldl = m + 1, nchunk = (m + kGsChunk) / kGsChunk;
   double* d_small = scratch_vec(22, (size_t)ldl * ldl + 3 * (size_t)(m + 2) + 2 * kGsChunk * (size_t)nchunk);
-  double* gpart = scratch_vec(23, 2 * kGsChunk * (size_t)blas_grid(n));
+  double* gpart = scratch_vec(23, 2 * kGsChunk * (size_t)4096);  // >= partials of the widest GS grid
   if (!z || !r || !d_small || !gpart) return fail(DGB_E_CUDA, "gmres: out of device memory");
   double* d_L = d_small;
   double* d_s = d_L + (size_t)ldl * ldl;
@@ -579,9 +580,14 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
   const int W = m + 1;
   auto pool = [&](int k) -> double* {
     while ((int)gm_basis_.size() <= k) {
+      // stagger the slots by a non-power-of-two offset so the same element of every
+      // basis vector does not land on the same DRAM channel / bank (the multi-vector
+      // Gram-Schmidt passes stream up to 18 of them at once)
+      const size_t off = (gm_basis_.size() * 136) % 4352;
       double* v = nullptr;
-      if (cudaMalloc(&v, n * sizeof(double)) != cudaSuccess) return nullptr;
-      gm_basis_.push_back(v);
+      if (cudaMalloc(&v, (n + 4352) * sizeof(double)) != cudaSuccess) return nullptr;
+      gm_raw_.push_back(v);
+      gm_basis_.push_back(v + off);
     }
     return gm_basis_[k];
   };

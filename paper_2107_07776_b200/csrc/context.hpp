@@ -101,7 +101,8 @@ class Context {
   double* d_gtab_ = nullptr;
   std::vector<double> gtab_h_;
   std::vector<std::pair<double*, size_t>> slots_;
-  std::vector<double*> gm_basis_;
+  std::vector<double*> gm_basis_;  // GMRES basis slots (offset into gm_raw_)
+  std::vector<double*> gm_raw_;    // their allocations
   CgState* d_cg_ = nullptr;         // device-resident CG scalars
   CgState* h_cg_ = nullptr;         // pinned: [0..1] polled status, [2] staging
   double* d_hist_ = nullptr;        // device residual history
