@@ -593,6 +593,23 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
   };
   if (!pool(W)) return fail(DGB_E_CUDA, "gmres: out of device memory (basis)");
   const double* Uc[kGsChunk];
+  // DGB_GMRES_PROF=1: per-part GPU time of the Arnoldi steps (diagnostics only)
+  static const bool gprof = std::getenv("DGB_GMRES_PROF") != nullptr;
+  cudaEvent_t gev[5] = {};
+  double gacc[4] = {0, 0, 0, 0};
+  if (gprof)
+    for (auto& e : gev) cudaEventCreate(&e);
+  struct GProfOut {
+    bool on;
+    cudaEvent_t* ev;
+    double* acc;
+    ~GProfOut() {
+      if (!on) return;
+      std::fprintf(stderr, "[dgb gmres] mul+apply %.1f ms, dots+solve %.1f ms, update %.1f ms, gaps %.1f ms\n",
+                   acc[0], acc[1], acc[2], acc[3]);
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);
+    }
+  } gprof_out{gprof, gev, gacc};
   int iter = 0;
   while (true) {
     OK(apply_op(op, x, r));
@@ -618,9 +635,11 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
     int k = 0;
     while (k < m && iter < s.max_iter) {
       double* w = gm_basis_[W];
+      if (gprof) cudaEventRecord(gev[0], st);
       ++launches;
       CK(v_mul_scaled(st, n, sh[k], gm_basis_[k], inv, z));  // z = M^{-1} v_k
       OK(apply_op(op, z, w));
+      if (gprof) cudaEventRecord(gev[1], st);
       ++iter;
       // pass 1: <w, U_j> (j <= k) and the Gram row <U_k, U_j> (j < k)
       for (int c0 = 0; c0 <= k; c0 += kGsChunk) {
@@ -632,6 +651,7 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
       }
       ++launches;
       CK(gs_solve(st, k, d_ab, d_L, ldl, d_s, sh[k], d_h, d_g));
+      if (gprof) cudaEventRecord(gev[2], st);
       // pass 2: w -= sum_j h_j v_j, |w|^2
       for (int c0 = 0; c0 <= k; c0 += kGsChunk) {
         const int nv = std::min(kGsChunk, k + 1 - c0);
@@ -640,8 +660,21 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
         launches += last ? 2 : 1;
         CK(gs_update(st, n, nv, Uc, d_g + c0, w, gpart, last ? d_h + k + 1 : nullptr));
       }
+      if (gprof) cudaEventRecord(gev[3], st);
       CK(cudaMemcpyAsync(h_gm_, d_h, (k + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      if (gprof) {
+        float t;
+        for (int i = 0; i < 3; ++i) {
+          cudaEventElapsedTime(&t, gev[i], gev[i + 1]);
+          gacc[i] += t;
+        }
+        if (k > 0) {
+          cudaEventElapsedTime(&t, gev[4], gev[0]);
+          gacc[3] += t;  // GPU idle between the previous step's copy-back and this step
+        }
+        cudaEventRecord(gev[4], st);
+      }
       for (int i = 0; i <= k; ++i) row(i, k) = h_gm_[i];
       const double hk1 = std::sqrt(h_gm_[k + 1]);
       row(k + 1, k) = hk1;
