@@ -329,7 +329,7 @@ struct SipLayout {
 };
 
 template <int DIM, int KP, template <int, int> class Geo>
-__global__ void __launch_bounds__(kThreads) k_sip(MeshArgs m, GeoArgs gq, double mass_coef, int dir_bdry,
+__global__ void __launch_bounds__(kThreads, 2) k_sip(MeshArgs m, GeoArgs gq, double mass_coef, int dir_bdry,
                                                   const double* __restrict__ x, double* __restrict__ y) {
   if (m.skip && *m.skip) return;
   using L = SipLayout<DIM, KP>;

@@ -547,7 +547,11 @@ struct MomAxisCfg {
 // (SPLIT: launch mass+viscous and advection as two kernels with their own occupancy)
 template <int K, int MODE> struct MomAxisTune { static constexpr int C = 6, T = 192; static constexpr bool SPLIT = false; };
 template <int MODE> struct MomAxisTune<1, MODE> { static constexpr int C = 16, T = 128; static constexpr bool SPLIT = false; };
-template <int MODE> struct MomAxisTune<2, MODE> { static constexpr int C = 8, T = 192; static constexpr bool SPLIT = false; };
+#ifndef DGB_MOM2_C
+#define DGB_MOM2_C 8
+#define DGB_MOM2_T 192
+#endif
+template <int MODE> struct MomAxisTune<2, MODE> { static constexpr int C = DGB_MOM2_C, T = DGB_MOM2_T; static constexpr bool SPLIT = false; };
 #ifndef DGB_MOM3_C  // tuning overrides for experiments (tools/tune_mom.sh)
 #define DGB_MOM3_C 6
 #define DGB_MOM3_T 192
