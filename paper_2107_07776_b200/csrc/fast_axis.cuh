@@ -716,70 +716,87 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   stage_a(std::integral_constant<int, 1>{});
   stage_a(std::integral_constant<int, 2>{});
   SYNC_CELL();
+  // B, C, D work on independent output lines.  SPL = 2 splits each (comp, line) item in
+  // two (the two fields of B / C, halves of the z-outputs of D) so 96 items fill three
+  // full warp rounds instead of 48 filling two; measured slower at K = 3 (more shared
+  // loads per FMA: 1.92 vs 1.81 ms), so it stays 1.
+  constexpr int SPL = 1;
   // B: x-lines in place: SY <- M_x SY, SZ <- M_x SZ
-  for (int idx = it0; idx < ITEMS(3 * NF); idx += IST) {
-    const int c = CELLOF(idx, 3 * NF), r = RESTOF(idx, c, 3 * NF);
+  for (int idx = it0; idx < ITEMS(3 * NF * SPL); idx += IST) {
+    const int c = CELLOF(idx, 3 * NF * SPL), r0 = RESTOF(idx, c, 3 * NF * SPL);
+    const int r = r0 / SPL, part = r0 - r * SPL;
     const int comp = r / NF, tl = r - comp * NF;
     const int b0 = comp * CT + P::idx(0, tl % N, tl / N);
-    double a[N], b[N];
 #pragma unroll
-    for (int l = 0; l < N; ++l) {
-      a[l] = WK(c)[G::A_SY + b0 + l];
-      b[l] = WK(c)[G::A_SZ + b0 + l];
-    }
+    for (int h = 0; h < 3 - SPL; ++h) {
+      double* ln = WK(c) + ((SPL == 2 ? part : h) ? G::A_SZ : G::A_SY) + b0;
+      double a[N];
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double s = 0.0, t = 0.0;
+      for (int l = 0; l < N; ++l) a[l] = ln[l];
 #pragma unroll
-      for (int l = 0; l < N; ++l) {
-        s = fma(ta.M[i][l], a[l], s);
-        t = fma(ta.M[i][l], b[l], t);
+      for (int i = 0; i < N; ++i) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) sacc = fma(ta.M[i][l], a[l], sacc);
+        ln[i] = sacc;
       }
-      WK(c)[G::A_SY + b0 + i] = s;
-      WK(c)[G::A_SZ + b0 + i] = t;
     }
   }
   SYNC_CELL();
   // C: y-lines: SX <- M_y (SX + mass detJ UX) + SY ; SZ <- M_y SZ
-  for (int idx = it0; idx < ITEMS(3 * NF); idx += IST) {
-    const int c = CELLOF(idx, 3 * NF), r = RESTOF(idx, c, 3 * NF);
+  for (int idx = it0; idx < ITEMS(3 * NF * SPL); idx += IST) {
+    const int c = CELLOF(idx, 3 * NF * SPL), r0 = RESTOF(idx, c, 3 * NF * SPL);
+    const int r = r0 / SPL, part = r0 - r * SPL;
     const int comp = r / NF, tl = r - comp * NF;
     const int b0 = comp * CT + P::idx(tl % N, 0, tl / N);
-    const double cm = co.mass * INFO(c).detJ;
-    double a[N], b[N], e[N];
 #pragma unroll
-    for (int l = 0; l < N; ++l) {
-      a[l] = fma(cm, WK(c)[G::A_UX + b0 + l * P::PX], WK(c)[G::A_SX + b0 + l * P::PX]);
-      b[l] = WK(c)[G::A_SZ + b0 + l * P::PX];
-      e[l] = WK(c)[G::A_SY + b0 + l * P::PX];
-    }
+    for (int h = 0; h < 3 - SPL; ++h) {
+      const bool zpart = SPL == 2 ? part != 0 : h != 0;
+      double a[N], e[N];
+      if (!zpart) {
+        const double cm = co.mass * INFO(c).detJ;
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-      double s = e[j], t = 0.0;
+        for (int l = 0; l < N; ++l) {
+          a[l] = fma(cm, WK(c)[G::A_UX + b0 + l * P::PX], WK(c)[G::A_SX + b0 + l * P::PX]);
+          e[l] = WK(c)[G::A_SY + b0 + l * P::PX];
+        }
+      } else {
 #pragma unroll
-      for (int l = 0; l < N; ++l) {
-        s = fma(ta.M[j][l], a[l], s);
-        t = fma(ta.M[j][l], b[l], t);
+        for (int l = 0; l < N; ++l) {
+          a[l] = WK(c)[G::A_SZ + b0 + l * P::PX];
+          e[l] = 0.0;
+        }
       }
-      WK(c)[G::A_SX + b0 + j * P::PX] = s;
-      WK(c)[G::A_SZ + b0 + j * P::PX] = t;
+      double* dst = WK(c) + (zpart ? G::A_SZ : G::A_SX) + b0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double sacc = e[j];
+#pragma unroll
+        for (int l = 0; l < N; ++l) sacc = fma(ta.M[j][l], a[l], sacc);
+        dst[j * P::PX] = sacc;
+      }
     }
   }
   SYNC_CELL();
   // D: z-lines: OUT = M_z SX + SZ
-  for (int idx = it0; idx < ITEMS(3 * NF); idx += IST) {
-    const int c = CELLOF(idx, 3 * NF), r = RESTOF(idx, c, 3 * NF);
+  constexpr int NK = (N + SPL - 1) / SPL;
+  for (int idx = it0; idx < ITEMS(3 * NF * SPL); idx += IST) {
+    const int c = CELLOF(idx, 3 * NF * SPL), r0 = RESTOF(idx, c, 3 * NF * SPL);
+    const int r = r0 / SPL, k0 = (r0 - r * SPL) * NK;
     const int comp = r / NF, tl = r - comp * NF;
     const int b0 = comp * CT + P::idx(tl % N, tl / N, 0);
     double a[N];
 #pragma unroll
     for (int l = 0; l < N; ++l) a[l] = WK(c)[G::A_SX + b0 + l * P::PY];
 #pragma unroll
-    for (int k = 0; k < N; ++k) {
-      double s = WK(c)[G::A_SZ + b0 + k * P::PY];
+    for (int kk = 0; kk < NK; ++kk) {
+      const int k = k0 + kk;
+      if (k < N) {
+        double sacc = WK(c)[G::A_SZ + b0 + k * P::PY];
 #pragma unroll
-      for (int l = 0; l < N; ++l) s = fma(ta.M[k][l], a[l], s);
-      CELL(c)[G::O_OUT + b0 + k * P::PY] = s;
+        for (int l = 0; l < N; ++l) sacc = fma(ta.M[k][l], a[l], sacc);
+        CELL(c)[G::O_OUT + b0 + k * P::PY] = sacc;
+      }
     }
   }
   SYNC_CELL();
@@ -977,6 +994,15 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       }
     }
     const double ih0 = -co.adv * ci.ih[0], ih1 = -co.adv * ci.ih[1], ih2 = -co.adv * ci.ih[2];
+    // weighted advecting-field factors, shared by the three components
+    double fx[Q], fy[Q], fz[Q];
+#pragma unroll
+    for (int qz = 0; qz < Q; ++qz) {
+      const double wq = wxy * tq.w[qz];
+      fx[qz] = col[3][qz] * (wq * ih0);
+      fy[qz] = col[4][qz] * (wq * ih1);
+      fz[qz] = col[5][qz] * (wq * ih2);
+    }
 #pragma unroll
     for (int comp = 0; comp < 3; ++comp) {
       double tz[N], ty[N], tx[N];
@@ -984,10 +1010,10 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       for (int l = 0; l < N; ++l) tz[l] = ty[l] = tx[l] = 0.0;
 #pragma unroll
       for (int qz = 0; qz < Q; ++qz) {
-        const double uj = col[comp][qz] * wxy * tq.w[qz];
-        const double rx = uj * col[3][qz] * ih0;
-        const double ry = uj * col[4][qz] * ih1;
-        const double rz = uj * col[5][qz] * ih2;
+        const double uj = col[comp][qz];
+        const double rx = uj * fx[qz];
+        const double ry = uj * fy[qz];
+        const double rz = uj * fz[qz];
 #pragma unroll
         for (int l = 0; l < N; ++l) {
           tz[l] = fma(tq.D[qz][l], rz, tz[l]);
