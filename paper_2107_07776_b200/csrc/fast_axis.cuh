@@ -66,9 +66,9 @@ static inline cudaError_t ensure_ftab() {
 constexpr int kAffStride3 = 9 + 1 + 6 * 4;
 
 // padded cell tensor: x-pitch odd
-template <int N>
+template <int N, int PXV = (N | 1)>
 struct Pad {
-  static constexpr int PX = N | 1;
+  static constexpr int PX = PXV;
   static constexpr int PY = PX * N;
   static constexpr int CT = PY * N;
   __device__ __forceinline__ static int idx(int i, int j, int k) { return i + PX * j + PY * k; }
@@ -515,7 +515,10 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
 template <int K, int CC, int TH, int MODE = 0>
 struct MomAxisCfg {
   static constexpr int N = K + 1, Q = K + 2, NB = N * N * N, NF = N * N, QN = Q * N, QQ = Q * Q;
-  using P = Pad<N>;
+#ifndef DGB_MOM_PX2
+#define DGB_MOM_PX2 3
+#endif
+  using P = Pad<N, N == 3 ? DGB_MOM_PX2 : (N | 1)>;  // x-pitch of the staged cell tensors
   static constexpr int CT = P::CT | 1;  // odd component stride (bank-conflict-free field interleave)
   static constexpr int C = CC;   // cells per CTA
   static constexpr int T = TH;   // threads per CTA
