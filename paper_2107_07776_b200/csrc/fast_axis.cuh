@@ -528,13 +528,16 @@ struct MomAxisCfg {
   // phase A: SX, SY, SZ, UX (3 comps each)
   static constexpr int A_SX = 0, A_SY = 3 * CT, A_SZ = 6 * CT, A_UX = 9 * CT, A_END = 12 * CT;
   // phase B (advection cell terms)
-  static constexpr int B_R1 = 0;           // XB (6 QNN) then TZ/TY/TX (9 QQN)
-  static constexpr int B_R2 = 9 * QQ * N;  // YB (6 QQN) then SA/SB (6 QNN)
-  static constexpr int B_END = B_R2 + 6 * QQ * N;
+  // quadrature-plane stride of the YB / T tensors, odd so that per-layer items
+  // (one plane each) start on different banks
+  static constexpr int QQP = QQ | 1;
+  static constexpr int B_R1 = 0;            // TZ/TY/TX [comp][test][l][qxy] (9 QQP N)
+  static constexpr int B_R2 = 9 * QQP * N;  // YB [field][k][qxy] (6 QQP N)
+  static constexpr int B_END = B_R2 + 6 * QQP * N;
   // face phase (all 6 faces at once): V1 [8 fields][6][Q x N] -> FB [3][6][N x N];  FL [3][6][Q x N]
   // V1 [field][q][f][qp]: face-Gauss-point rows of all 6 faces contiguous (F2 reads them
   // conflict-free); the q-block stride VB is chosen so F1's (f, q) writes hit distinct banks
-  static constexpr int VB = K == 3 ? 36 : 6 * Q, V1_SIZE = 8 * N * VB;
+  static constexpr int VB = K == 3 ? 36 : (K == 2 ? 33 : 6 * Q), V1_SIZE = 8 * N * VB;
   static constexpr int F_V1 = 0, F_FL = V1_SIZE, F_END = F_FL + 18 * QN;
   // neighbour face traces [f (stride NBS)][x0, x1, x2, w_normal][p + N q], filled during S0 /
   // pass A and read by F1; disjoint from the pass-A regions and from V1
@@ -965,7 +968,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         for (int i = 0; i < N; ++i) sacc = fma(tq.B[qx][i], pl[j][i], sacc);
         px[qx][j] = sacc;
       }
-    double* o = WK(c) + G::B_R2 + f * QQ * N + QQ * k;
+    double* o = WK(c) + G::B_R2 + (f * N + k) * G::QQP;
 #pragma unroll
     for (int qy = 0; qy < Q; ++qy)
 #pragma unroll
@@ -987,7 +990,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
     for (int f = 0; f < 6; ++f) {
       double v[N];
 #pragma unroll
-      for (int l = 0; l < N; ++l) v[l] = WK(c)[G::B_R2 + f * QQ * N + qxy + QQ * l];
+      for (int l = 0; l < N; ++l) v[l] = WK(c)[G::B_R2 + (f * N + l) * G::QQP + qxy];
 #pragma unroll
       for (int qz = 0; qz < Q; ++qz) {
         double s = 0.0;
@@ -1024,12 +1027,12 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
           tx[l] = fma(tq.B[qz][l], rx, tx[l]);
         }
       }
-      double* o = WK(c) + G::B_R1 + comp * 3 * QQ * N + qxy;
+      double* o = WK(c) + G::B_R1 + comp * 3 * G::QQP * N + qxy;
 #pragma unroll
       for (int l = 0; l < N; ++l) {
-        o[QQ * l] = tz[l];
-        o[QQ * N + QQ * l] = ty[l];
-        o[2 * QQ * N + QQ * l] = tx[l];
+        o[G::QQP * l] = tz[l];
+        o[G::QQP * (N + l)] = ty[l];
+        o[G::QQP * (2 * N + l)] = tx[l];
       }
     }
   }
@@ -1042,7 +1045,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
     const int c = CELLOF(idx, 3 * N * JH), r = RESTOF(idx, c, 3 * N * JH);
     const int comp = r / (N * JH), r2 = r - comp * N * JH;
     const int l = r2 / JH, j0 = (r2 - l * JH) * NJ;
-    const double* tp = WK(c) + G::B_R1 + comp * 3 * QQ * N + QQ * l;
+    const double* tp = WK(c) + G::B_R1 + comp * 3 * G::QQP * N + G::QQP * l;
     double acc[NJ][N];  // [j - j0][i]
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
@@ -1054,8 +1057,8 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
 #pragma unroll
       for (int qy = 0; qy < Q; ++qy) {
         vz[qy] = tp[qx + Q * qy];
-        vy[qy] = tp[QQ * N + qx + Q * qy];
-        vx[qy] = tp[2 * QQ * N + qx + Q * qy];
+        vy[qy] = tp[G::QQP * N + qx + Q * qy];
+        vx[qy] = tp[2 * G::QQP * N + qx + Q * qy];
       }
 #pragma unroll
       for (int jj = 0; jj < NJ; ++jj) {
