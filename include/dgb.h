@@ -101,6 +101,13 @@ int dgb_momentum_apply(dgb_ctx* ctx, const double* coefs, const double* d_w, con
 int dgb_momentum_diag(dgb_ctx* ctx, const double* coefs, const double* d_w, double* d_diag);
 /* replaces apply_pressure_helmholtz (forms.hpp:126-128, forms.cpp:1090-1095) */
 int dgb_pressure_apply(dgb_ctx* ctx, double mass_coef, const double* d_x, double* d_y);
+/* Host-buffer variants (blocking; the result is in h_y on return): the same operators
+ * on HOST arrays, the reference's calling convention (apply_momentum(V, geom, ctx, x,
+ * out) with host Fields).  On uniform Cartesian 3D meshes the host->device copies, the
+ * apply and the device->host copy are pipelined over z-slabs on separate streams
+ * (overlap needs page-locked buffers); otherwise copy in / apply / copy out. */
+int dgb_momentum_apply_host(dgb_ctx* ctx, const double* coefs, const double* h_w, const double* h_x, double* h_y);
+int dgb_pressure_apply_host(dgb_ctx* ctx, double mass_coef, const double* h_x, double* h_y);
 /* replaces helmholtz_diagonal (forms.hpp:129-131, forms.cpp:1097-1102) */
 int dgb_helmholtz_diag(dgb_ctx* ctx, double mass_coef, double* d_diag);
 /* replaces apply_scalar_laplace / scalar_laplace_diagonal on the scalar space (forms.hpp:157-162) */

@@ -109,6 +109,8 @@ def lib() -> C.CDLL:
     L.dgb_momentum_apply.argtypes = [C.c_void_p, _dp, C.c_void_p, C.c_void_p, C.c_void_p]
     L.dgb_momentum_diag.argtypes = [C.c_void_p, _dp, C.c_void_p, C.c_void_p]
     L.dgb_pressure_apply.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
+    L.dgb_momentum_apply_host.argtypes = [C.c_void_p, _dp, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.dgb_pressure_apply_host.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
     L.dgb_helmholtz_diag.argtypes = [C.c_void_p, C.c_double, C.c_void_p]
     L.dgb_laplace_apply.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
     L.dgb_laplace_diag.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
@@ -155,6 +157,22 @@ def _ptr(t) -> Optional[int]:
     import torch
     if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
         raise ValueError("fields must be contiguous CUDA float64 tensors")
+    return t.data_ptr()
+
+
+def _host_ptr(t) -> Optional[int]:
+    """Host field: contiguous CPU float64 torch tensor (pinned for copy/compute overlap)
+    or numpy array."""
+    if t is None:
+        return None
+    import numpy as np
+    if isinstance(t, np.ndarray):
+        if not (t.dtype == np.float64 and t.flags.c_contiguous):
+            raise ValueError("host fields must be contiguous float64 arrays")
+        return t.ctypes.data
+    import torch
+    if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise ValueError("host fields must be contiguous CPU float64 tensors")
     return t.data_ptr()
 
 
@@ -309,6 +327,17 @@ class MomentumRhs:
 
 def apply_momentum(V: DGContext, ctx: MomentumCtx, x, out):
     _check(lib().dgb_momentum_apply(V.handle, ctx.coefs(), _ptr(ctx.advecting), _ptr(x), _ptr(out)))
+
+
+def apply_momentum_host(V: DGContext, coefs, w_host, x_host, out_host):
+    """apply_momentum on HOST fields (blocking): copies in, applies and copies back with
+    the copies pipelined against the apply over z-slabs on uniform 3D meshes."""
+    c = (C.c_double * 4)(*[float(v) for v in coefs])
+    _check(lib().dgb_momentum_apply_host(V.handle, c, _host_ptr(w_host), _host_ptr(x_host), _host_ptr(out_host)))
+
+
+def apply_pressure_helmholtz_host(V: DGContext, mass_coef: float, x_host, out_host):
+    _check(lib().dgb_pressure_apply_host(V.handle, float(mass_coef), _host_ptr(x_host), _host_ptr(out_host)))
 
 
 def momentum_diagonal(V: DGContext, ctx: MomentumCtx, diag):

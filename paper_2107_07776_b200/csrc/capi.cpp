@@ -206,6 +206,16 @@ int dgb_momentum_apply(dgb_ctx* h, const double* coefs, const double* w, const d
   NEED(x != y, "x and y must not alias");
   return ret(h, h->c.momentum(coefs, w, x, y));
 }
+int dgb_momentum_apply_host(dgb_ctx* h, const double* coefs, const double* h_w, const double* h_x, double* h_y) {
+  NEED(h && coefs && h_x && h_y, "null argument");
+  NEED(h_x != h_y, "x and y must not alias");
+  return ret(h, h->c.apply_host(true, coefs, 0.0, h_w, h_x, h_y));
+}
+int dgb_pressure_apply_host(dgb_ctx* h, double mc, const double* h_x, double* h_y) {
+  NEED(h && h_x && h_y, "null argument");
+  NEED(h_x != h_y, "x and y must not alias");
+  return ret(h, h->c.apply_host(false, nullptr, mc, nullptr, h_x, h_y));
+}
 int dgb_momentum_diag(dgb_ctx* h, const double* coefs, const double* w, double* d) {
   NEED(h && coefs && d, "null argument");
   return ret(h, h->c.momentum_diag(coefs, w, d));

@@ -51,6 +51,13 @@ Context::~Context() {
   if (d_hist_) cudaFree(d_hist_);
   for (cudaEvent_t e : poll_ev_)
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < kMaxSlabs; ++i) {
+    if (ev_in_[i]) cudaEventDestroy(ev_in_[i]);
+    if (ev_k_[i]) cudaEventDestroy(ev_k_[i]);
+  }
+  if (ev_start_) cudaEventDestroy(ev_start_);
+  if (cp_in_) cudaStreamDestroy(cp_in_);
+  if (cp_out_) cudaStreamDestroy(cp_out_);
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (own_stream) cudaStreamDestroy(own_stream);
@@ -275,6 +282,75 @@ int Context::sip(double mc, int dir, const double* x, double* y) {
   }
   CK(opp->sip(dc, mc, dir, x, y));
   return DGB_OK;
+}
+// Host-buffer applies.  On a uniform lexicographic grid with the fast kernels the cells
+// of a z-slab are one contiguous range and an apply over a slab reads only the slab and
+// its two neighbour slabs, so the host->device copies of the inputs (copy stream 1), the
+// fast-kernel launches per slab (context stream) and the device->host copies of the
+// result (copy stream 2) overlap: slab s is computed as soon as slab s+1 has arrived and
+// shipped back as soon as it is computed.  Otherwise: copy in, apply, copy out.
+// Overlap needs page-locked host buffers (pageable ones work, the driver stages them).
+int Context::apply_host(bool mom, const double* coefs, double mc, const double* h_w, const double* h_x,
+                        double* h_y) {
+  const size_t nbc = mom ? (size_t)dim * ipow(ku + 1, dim) : ipow(kp + 1, dim);  // doubles per cell
+  const size_t n = (size_t)mesh.ncells * nbc;
+  double* dx = scratch_vec(26, n);
+  double* dy = scratch_vec(27, n);
+  double* dw = (mom && h_w) ? scratch_vec(28, n) : nullptr;
+  if (!dx || !dy || (mom && h_w && !dw)) return fail(DGB_E_CUDA, "apply_host: out of device memory");
+  if (mom && (coefs[2] != 0.0 || coefs[3] != 0.0) && !h_w)
+    return fail(DGB_E_MISSING_FIELD, "apply_momentum: advecting field missing");
+  cudaStream_t st = dc.stream;
+  const bool pipe = use_fast && dc.axis && dc.ug.n > 0 && dim == 3 && (!mom || coefs[3] == 0.0);
+  if (!pipe) {
+    CK(cudaMemcpyAsync(dx, h_x, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    if (dw) CK(cudaMemcpyAsync(dw, h_w, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    OK(mom ? momentum(coefs, dw, dx, dy) : sip(mc, 0, dx, dy));
+    CK(cudaMemcpyAsync(h_y, dy, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return DGB_OK;
+  }
+  if (!cp_in_) {
+    CK(cudaStreamCreateWithFlags(&cp_in_, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&cp_out_, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ev_start_, cudaEventDisableTiming));
+    for (int i = 0; i < kMaxSlabs; ++i) {
+      CK(cudaEventCreateWithFlags(&ev_in_[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_k_[i], cudaEventDisableTiming));
+    }
+  }
+  const int nl = dc.ug.n, layer = nl * nl;
+  const int per = (nl + 15) / 16;             // z-layers per slab (<= 16 slabs)
+  const int ns = (nl + per - 1) / per;
+  auto cells = [&](int s) { return std::min(nl, s * per) * layer; };
+  CK(cudaEventRecord(ev_start_, st));  // after everything already queued on the context stream
+  CK(cudaStreamWaitEvent(cp_in_, ev_start_, 0));
+  CK(cudaStreamWaitEvent(cp_out_, ev_start_, 0));
+  for (int s = 0; s < ns; ++s) {
+    const size_t o = (size_t)cells(s) * nbc, len = (size_t)(cells(s + 1) - cells(s)) * nbc;
+    CK(cudaMemcpyAsync(dx + o, h_x + o, len * sizeof(double), cudaMemcpyHostToDevice, cp_in_));
+    if (dw) CK(cudaMemcpyAsync(dw + o, h_w + o, len * sizeof(double), cudaMemcpyHostToDevice, cp_in_));
+    CK(cudaEventRecord(ev_in_[s], cp_in_));
+  }
+  const MomCoef co = mom ? MomCoef{coefs[0], coefs[1], coefs[2], coefs[3]} : MomCoef{};
+  int rc = DGB_OK;
+  for (int s = 0; s < ns && rc == DGB_OK; ++s) {
+    CK(cudaStreamWaitEvent(st, ev_in_[std::min(s + 1, ns - 1)], 0));
+    dc.mesh.cell0 = cells(s);
+    dc.mesh.cell1 = cells(s + 1);
+    ++launches;
+    const cudaError_t e = mom ? fast_momentum3(dc, co, dw ? dw : dx, dx, dy) : fast_sip3(dc, mc, 0, dx, dy);
+    if (e != cudaSuccess) rc = cuda_fail(e, "apply_host");
+    CK(cudaEventRecord(ev_k_[s], st));
+    CK(cudaStreamWaitEvent(cp_out_, ev_k_[s], 0));
+    const size_t o = (size_t)cells(s) * nbc, len = (size_t)(cells(s + 1) - cells(s)) * nbc;
+    CK(cudaMemcpyAsync(h_y + o, dy + o, len * sizeof(double), cudaMemcpyDeviceToHost, cp_out_));
+  }
+  dc.mesh.cell0 = 0;
+  dc.mesh.cell1 = -1;
+  CK(cudaStreamSynchronize(cp_out_));
+  CK(cudaStreamSynchronize(st));
+  return rc;
 }
 int Context::sip_diag(double mc, int dir, double* d) {
   ++launches;

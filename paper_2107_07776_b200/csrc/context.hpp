@@ -50,6 +50,9 @@ class Context {
   int momentum(const double* coefs, const double* w, const double* x, double* y);
   int momentum_diag(const double* coefs, const double* w, double* d);
   int sip(double mc, int dir, const double* x, double* y);
+  // host-buffer applies (blocking): H2D, apply, D2H pipelined over z-slabs when possible
+  int apply_host(bool momentum_op, const double* coefs, double mc, const double* h_w, const double* h_x,
+                 double* h_y);
   int sip_diag(double mc, int dir, double* d);
   int mass(int space, const double* x, double* y);
   int mass_diag(int space, double* d);
@@ -110,6 +113,10 @@ class Context {
   double* h_gm_ = nullptr;          // pinned GMRES Hessenberg column
   size_t h_gm_cap_ = 0;
   cudaEvent_t poll_ev_[2] = {nullptr, nullptr};
+  // host-buffer pipeline: two copy streams + per-slab events
+  static constexpr int kMaxSlabs = 32;
+  cudaStream_t cp_in_ = nullptr, cp_out_ = nullptr;
+  cudaEvent_t ev_start_ = nullptr, ev_in_[kMaxSlabs] = {}, ev_k_[kMaxSlabs] = {};
   size_t gm_n_ = 0;
   int ensure_geometry();
 };

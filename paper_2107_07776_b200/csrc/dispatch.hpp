@@ -17,6 +17,7 @@ struct MeshArgs {
   const int* bctype = nullptr;   // [64]: 0 dirichlet, 1 outlet
   const int* bslot = nullptr;    // [ncells][2dim]: boundary-face index (reference order) or -1
   const int* skip = nullptr;     // device flag: nonzero -> the launch is a no-op (device-side Krylov exit)
+  int cell0 = 0, cell1 = -1;     // fast kernels: process cells [cell0, cell1) only (-1: ncells)
 };
 
 struct GeoArgs {

@@ -367,8 +367,8 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
   constexpr int N = G::N, NB = G::NB, NF = G::NF, C = G::C, PER = G::PER, TT = G::T;
   const FTab<N, N>& ta = c_ft<N, N>;
   extern __shared__ double sm[];
-  const int c0 = blockIdx.x * C;
-  const int nc = min(C, m.ncells - c0);
+  const int c0 = m.cell0 + blockIdx.x * C;
+  const int nc = min(C, (m.cell1 < 0 ? m.ncells : m.cell1) - c0);
   const int tid = threadIdx.x;
   const double sfac = (double)((KP + 1) * (KP + 1));
 #define CELL(c) (sm + (c) * PER)
@@ -582,8 +582,8 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   const FTab<N, Q>& tq = c_ft<N, Q>;  // k+2 rule: B, D, w (advection)
   const FTab<N, N>& ta = c_ft<N, N>;  // exact M, K, dE
   extern __shared__ double sm[];
-  const int c0 = blockIdx.x * C;
-  const int nc = min(C, m.ncells - c0);
+  const int c0 = m.cell0 + blockIdx.x * C;
+  const int nc = min(C, (m.cell1 < 0 ? m.ncells : m.cell1) - c0);
   const int tid = threadIdx.x;
   const double sfac = (double)((K + 1) * (K + 1));
   const bool faces = MODE != 1 && co.adv != 0.0;

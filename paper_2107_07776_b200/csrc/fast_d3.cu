@@ -56,6 +56,12 @@ static cudaError_t ensure_ptab() {
   return e;
 }
 
+// cells a fast launch covers (a z-slab range for the host-buffer pipelines)
+static int fast_cells(const DevCtx& c) {
+  const int c1 = c.mesh.cell1 < 0 ? c.ncells : c.mesh.cell1;
+  return c1 - c.mesh.cell0;
+}
+
 template <class KernelT>
 static cudaError_t set_smem(KernelT kern, size_t smem) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -67,7 +73,7 @@ static cudaError_t run_sip_axis(const DevCtx& c, double mc, int dir, const doubl
   using G = SipAxisCfg<KP>;
   cudaError_t e = ensure_ftab<KP + 1, KP + 1>();
   if (e != cudaSuccess) return e;
-  const int grid = (c.ncells + G::C - 1) / G::C;
+  const int grid = (fast_cells(c) + G::C - 1) / G::C;
   if (c.ug.n > 0) {
     if ((e = set_smem(k_sip_axis<KP, true, CGF>, G::SMEM)) != cudaSuccess) return e;
     k_sip_axis<KP, true, CGF><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, mc, dir, x, y, cg);
@@ -84,7 +90,7 @@ static cudaError_t launch_momentum_axis(const DevCtx& c, MomCoef co, const doubl
   constexpr int CC = MomAxisTune<K, MODE>::C, TH = MomAxisTune<K, MODE>::T;
   using G = MomAxisCfg<K, CC, TH, MODE>;
   cudaError_t e;
-  const int grid = (c.ncells + G::C - 1) / G::C;
+  const int grid = (fast_cells(c) + G::C - 1) / G::C;
   if (c.ug.n > 0) {
     if ((e = set_smem(k_momentum_axis<K, CC, TH, MODE, true, RHS>, G::SMEM)) != cudaSuccess) return e;
     k_momentum_axis<K, CC, TH, MODE, true, RHS><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, co, x, w, y, acc);
