@@ -343,6 +343,10 @@ struct SipAxisCfg {
 #endif
   static constexpr int C = KP == 1 ? 32 : (KP == 2 ? DGB_SIP2_C : 8);  // cells per CTA
   static constexpr int T = KP == 1 ? 128 : (KP == 2 ? DGB_SIP2_T : 128);
+  // cells per warp: a warp owns CPW cells after the staging barrier (per-cell stages then
+  // sync with __syncwarp); chosen so the N^2-item line stages fill 32 lanes
+  static constexpr int CPW = KP == 1 ? 8 : (KP == 2 ? 3 : 2);
+  static constexpr bool WPG = C % CPW == 0 && T == 32 * (C / CPW);
   static constexpr int O_U = 0, O_SX = P::CT, O_SY = 2 * P::CT, O_SZ = 3 * P::CT, O_UX = 4 * P::CT;
   static constexpr int O_INFO = 5 * P::CT;
   static constexpr int PER = (O_INFO + kInfoDoubles) | 1;
@@ -371,8 +375,22 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
   const int nc = min(C, (m.cell1 < 0 ? m.ncells : m.cell1) - c0);
   const int tid = threadIdx.x;
   const double sfac = (double)((KP + 1) * (KP + 1));
+  constexpr bool WPG = G::WPG;
+  constexpr int CPW = G::CPW;
+  const int lane = tid & 31, wbase = (tid >> 5) * CPW;
+  const int it0 = WPG ? lane : tid;
+  constexpr int IST = WPG ? 32 : TT;
+  const int gbase = WPG ? wbase : 0;
+  const int gcnt = WPG ? max(0, min(CPW, nc - wbase)) : nc;
 #define CELL(c) (sm + (c) * PER)
 #define INFO(c) (*reinterpret_cast<CellInfo*>(sm + (c) * PER + G::O_INFO))
+#define SYNC_G()       \
+  do {                 \
+    if (WPG)           \
+      __syncwarp();    \
+    else               \
+      __syncthreads(); \
+  } while (0)
 
   // S0: cell values (padded) + per-cell info
   for (int idx = tid; idx < nc * NB; idx += TT) {
@@ -384,14 +402,14 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
   __syncthreads();
   // the scalar operator ignores outlet ids: all boundary faces are natural, or all
   // Dirichlet when dir_bdry (forms.cpp:218-242)
-  for (int idx = tid; idx < nc * 6; idx += TT) {
-    CellInfo& ci = INFO(idx / 6);
+  for (int idx = it0; idx < gcnt * 6; idx += IST) {
+    CellInfo& ci = INFO(gbase + idx / 6);
     if (ci.type[idx % 6] == 2) ci.type[idx % 6] = 1;
   }
-  __syncthreads();
+  SYNC_G();
   // A: all-direction lines: S_d on raw lines (+ neighbour lines), and Ux = M_x u
-  for (int idx = tid; idx < nc * 3 * NF; idx += TT) {
-    const int c = idx / (3 * NF), r = idx - c * 3 * NF;
+  for (int idx = it0; idx < gcnt * 3 * NF; idx += IST) {
+    const int cl = idx / (3 * NF), c = gbase + cl, r = idx - cl * 3 * NF;
     const int d = r / NF, tl = r - d * NF;
     const int p = tl % N, q = tl / N;
     const CellInfo& ci = INFO(c);
@@ -422,10 +440,10 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
       }
     }
   }
-  __syncthreads();
+  SYNC_G();
   // B: x-lines, in place: SY <- M_x SY, SZ <- M_x SZ
-  for (int idx = tid; idx < nc * NF; idx += TT) {
-    const int c = idx / NF, tl = idx - c * NF;
+  for (int idx = it0; idx < gcnt * NF; idx += IST) {
+    const int cl = idx / NF, c = gbase + cl, tl = idx - cl * NF;
     const int b0 = P::idx(0, tl % N, tl / N);
     double a[N], b[N];
 #pragma unroll
@@ -445,10 +463,10 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
       CELL(c)[G::O_SZ + b0 + i] = t;
     }
   }
-  __syncthreads();
+  SYNC_G();
   // C: y-lines: SX <- M_y (SX + mc detJ UX) + SY ; SZ <- M_y SZ
-  for (int idx = tid; idx < nc * NF; idx += TT) {
-    const int c = idx / NF, tl = idx - c * NF;
+  for (int idx = it0; idx < gcnt * NF; idx += IST) {
+    const int cl = idx / NF, c = gbase + cl, tl = idx - cl * NF;
     const int b0 = P::idx(tl % N, 0, tl / N);
     const double cm = mc * INFO(c).detJ;
     double a[N], b[N], e[N];
@@ -470,11 +488,11 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
       CELL(c)[G::O_SZ + b0 + j * P::PX] = t;
     }
   }
-  __syncthreads();
+  SYNC_G();
   // D: z-lines: y = M_z SX + SZ   -> global
   double pq[1] = {0.0};
-  for (int idx = tid; idx < nc * NF; idx += TT) {
-    const int c = idx / NF, tl = idx - c * NF;
+  for (int idx = it0; idx < gcnt * NF; idx += IST) {
+    const int cl = idx / NF, c = gbase + cl, tl = idx - cl * NF;
     const int i = tl % N, j = tl / N;
     const int b0 = P::idx(i, j, 0);
     double a[N];
@@ -504,6 +522,7 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
   }
 #undef CELL
 #undef INFO
+#undef SYNC_G
 }
 
 // ===========================================================================
