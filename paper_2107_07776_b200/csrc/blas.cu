@@ -199,27 +199,22 @@ __global__ void k_cg_dir(size_t n, const double* __restrict__ z, double* __restr
   GRID_STRIDE(i, n) p[i] = first ? z[i] : fma(beta, p[i], z[i]);
 }
 __global__ void k_cg_pq_part(size_t n, const double* __restrict__ p, const double* __restrict__ q,
-                             double* __restrict__ partial, const CgState* st) {
+                             double* __restrict__ partial, CgState* st) {
   if (st->done) return;
   double acc[1] = {0.0};
   GRID_STRIDE(i, n) acc[0] = fma(p[i], q[i], acc[0]);
   block_reduce_store<1>(acc, partial);
+  if (last_block_arrival(&st->cnt_pq)) cg_alpha_finish(gridDim.x, partial, st);
 }
 __global__ void k_cg_alpha_final(int nparts, const double* __restrict__ partial, CgState* st) {
   if (st->done) return;
-  const double pq = block_sum_parts(nparts, partial);
-  if (threadIdx.x == 0) {
-    if (pq <= 0.0) {
-      st->err = 4;  // DGB_E_NOT_SPD
-      st->done = 3;
-    } else {
-      st->alpha = st->rho / pq;
-    }
-  }
+  cg_alpha_finish(nparts, partial, st);
 }
+__device__ __forceinline__ void cg_upd_finish(int nparts, const double* partial, CgState* st, double* hist);
 __global__ void k_cg_upd_part(size_t n, const double* __restrict__ p, const double* __restrict__ q,
                               double* __restrict__ x, double* __restrict__ r, const double* __restrict__ inv,
-                              double* __restrict__ z, double* __restrict__ partial, const CgState* st) {
+                              double* __restrict__ z, double* __restrict__ partial, CgState* st,
+                              double* __restrict__ hist) {
   if (st->done) return;
   const double a = st->alpha;
   double acc[2] = {0.0, 0.0};
@@ -233,13 +228,12 @@ __global__ void k_cg_upd_part(size_t n, const double* __restrict__ p, const doub
     acc[1] = fma(ri, zi, acc[1]);
   }
   block_reduce_store<2>(acc, partial);
+  if (last_block_arrival(&st->cnt_upd)) cg_upd_finish(gridDim.x, partial, st, hist);
 }
-__global__ void k_cg_upd_final(int nparts, const double* __restrict__ partial, CgState* st,
-                               double* __restrict__ hist) {
-  if (st->done) return;
-  const double rr = block_sum_parts(nparts, partial);
-  __syncthreads();
-  const double rz = block_sum_parts(nparts, partial + nparts);
+// <r,r>, <r,z> from the partials; history, convergence / budget / breakdown flags
+__device__ __forceinline__ void cg_upd_finish(int nparts, const double* partial, CgState* st, double* hist) {
+  const double rr = block_sum_l2(nparts, partial);
+  const double rz = block_sum_l2(nparts, partial + nparts);
   if (threadIdx.x == 0) {
     const int it = st->iter + 1;
     st->iter = it;
@@ -442,8 +436,7 @@ cudaError_t cg_direction(cudaStream_t s, size_t n, const double* z, double* p, c
 }
 cudaError_t cg_alpha(cudaStream_t s, size_t n, const double* p, const double* q, double* scratch, CgState* st) {
   const int g = blas_grid(n);
-  k_cg_pq_part<<<g, kBlasThreads, 0, s>>>(n, p, q, scratch, st);
-  k_cg_alpha_final<<<1, kBlasThreads, 0, s>>>(g, scratch, st);
+  k_cg_pq_part<<<g, kBlasThreads, 0, s>>>(n, p, q, scratch, st);  // last block computes alpha
   return cudaGetLastError();
 }
 cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, const double* partial, CgState* st) {
@@ -453,8 +446,7 @@ cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, const double* par
 cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q, double* x, double* r,
                       const double* inv, double* z, double* scratch, CgState* st, double* hist) {
   const int g = blas_grid(n);
-  k_cg_upd_part<<<g, kBlasThreads, 0, s>>>(n, p, q, x, r, inv, z, scratch, st);
-  k_cg_upd_final<<<1, kBlasThreads, 0, s>>>(g, scratch, st, hist);
+  k_cg_upd_part<<<g, kBlasThreads, 0, s>>>(n, p, q, x, r, inv, z, scratch, st, hist);  // last block finishes
   return cudaGetLastError();
 }
 static int gs_grid(size_t n) {

@@ -79,7 +79,54 @@ cudaError_t r_sum(cudaStream_t s, int nparts, const double* partial, double* d_o
 struct CgState {
   double rho, rho_old, alpha, rnorm, tol;
   int iter, max_iter, done, err, first;
+  unsigned cnt_pq, cnt_upd;  // arrival counters of the last-block reductions (kept at 0 between launches)
 };
+
+#ifdef __CUDACC__
+// true in the block that arrives last (after every block has published its partial);
+// the counter is reset there, and that block then reads all partials
+__device__ __forceinline__ bool last_block_arrival(unsigned* cnt) {
+  __shared__ bool is_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(cnt, 1u);
+    is_last = t == gridDim.x - 1;
+    if (is_last) *cnt = 0u;
+  }
+  __syncthreads();
+  if (is_last) __threadfence();
+  return is_last;
+}
+// sum of partial[0..nparts) by the whole block, fixed order; L2 loads (written by other SMs)
+__device__ __forceinline__ double block_sum_l2(int nparts, const double* partial) {
+  __shared__ double red2[32];
+  double a = 0.0;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) a += __ldcg(partial + i);
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  if ((threadIdx.x & 31) == 0) red2[threadIdx.x >> 5] = a;
+  __syncthreads();
+  double b = 0.0;
+  if (threadIdx.x < 32) {
+    b = threadIdx.x < (blockDim.x >> 5) ? red2[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  __syncthreads();
+  return b;  // valid in thread 0
+}
+// alpha = rho / <p, q> from the partials (krylov.cpp:84-87); flags NOT_SPD
+__device__ __forceinline__ void cg_alpha_finish(int nparts, const double* partial, CgState* st) {
+  const double pq = block_sum_l2(nparts, partial);
+  if (threadIdx.x == 0) {
+    if (pq <= 0.0) {
+      st->err = 4;  // DGB_E_NOT_SPD
+      st->done = 3;
+    } else {
+      st->alpha = st->rho / pq;
+    }
+  }
+}
+#endif
 // first iteration of an inner loop: z = M r, rho = <r,z>; sets first = 1, done = 0
 cudaError_t cg_begin(cudaStream_t s, size_t n, const double* r, const double* inv, double* z, double* scratch,
                      CgState* st);

@@ -555,16 +555,16 @@ int Context::cg(const dgb_operator& op, const dgb_solver_settings& s, const doub
     auto enqueue = [&](int slot) -> int {
       for (int b = 0; b < batch; ++b) {
         if (fused) {
-          launches += 5;
+          launches += 4;
           const double mc = op.op == DGB_OP_PRESSURE ? op.coefs[0] : 0.0;
           const int dir = op.op == DGB_OP_PRESSURE ? 0 : op.dirichlet_bdry;
           CK(cg_direction(st, n, z, p, d_cg_));
-          CK(fast_sip3_cg(dc, mc, dir, p, q, fpart));
+          CK(fast_sip3_cg(dc, mc, dir, p, q, fpart, d_cg_));
           CK(cg_alpha_from_partials(st, fblocks, fpart, d_cg_));
           CK(cg_update(st, n, p, q, x, r, inv, z, d_partial_, d_cg_, d_hist_));
           continue;
         }
-        launches += 5;  // + the operator's own count
+        launches += 3;  // + the operator's own count
         CK(cg_direction(st, n, z, p, d_cg_));
         OK(apply_op(op, p, q));
         CK(cg_alpha(st, n, p, q, d_partial_, d_cg_));

@@ -92,9 +92,11 @@ struct OpTable {
 // fast axis-aligned 3D kernels (fast_d3.cu); cudaErrorNotSupported when not applicable
 cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, double* y);
 cudaError_t fast_momentum3(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);
-// CG apply on the axis-aligned scalar SIP operator with the <p, q> block partials fused
-// (fast_axis.cuh k_sip_axis<.., CGF>): q = A p, partial[block] = <p, q>_block
-cudaError_t fast_sip3_cg(const DevCtx& c, double mc, int dir, const double* p, double* q, double* partial);
+struct CgState;
+// CG apply on the axis-aligned scalar SIP operator with <p, q> fused (fast_axis.cuh
+// k_sip_axis<.., CGF>): q = A p, block partials, alpha written to st by the last block
+cudaError_t fast_sip3_cg(const DevCtx& c, double mc, int dir, const double* p, double* q, double* partial,
+                         CgState* st);
 int fast_sip3_cg_blocks(const DevCtx& c);  // number of partials fast_sip3_cg writes (0: unsupported)
 // stage right-hand side (momentum_rhs) on axis-aligned 3D meshes; ptmp: pressure-space scratch
 cudaError_t fast_rhs3(const DevCtx& c, const RhsArgs& ra, double* y, double* ptmp);

@@ -353,11 +353,13 @@ struct SipAxisCfg {
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
 
-// CGF: the CG apply q = A p with the <p, q> partial of the block fused into the
-// epilogue (krylov.cpp:84-87): partial[block] = sum over the block's DoFs of p q.
+// CGF: the CG apply q = A p with <p, q> fused into the epilogue (krylov.cpp:84-87):
+// partial[block] = sum over the block's DoFs of p q (alpha: cg_alpha_from_partials;
+// a last-block finish here was slower — one block summing ~16k partials at the tail).
 static_assert(SipAxisCfg<1>::T <= 256 && SipAxisCfg<2>::T <= 256 && SipAxisCfg<3>::T <= 256, "CG reduction buffer");
 struct SipCgArgs {
   double* partial = nullptr;
+  CgState* st = nullptr;
 };
 
 template <int KP, bool UNI, bool CGF = false>

@@ -211,9 +211,11 @@ int fast_sip3_cg_blocks(const DevCtx& c) {
   return 0;
 }
 
-cudaError_t fast_sip3_cg(const DevCtx& c, double mc, int dir, const double* p, double* q, double* partial) {
+cudaError_t fast_sip3_cg(const DevCtx& c, double mc, int dir, const double* p, double* q, double* partial,
+                         CgState* st) {
   SipCgArgs a;
   a.partial = partial;
+  a.st = st;
   switch (c.kp) {
     case 1: return run_sip_axis<1, true>(c, mc, dir, p, q, a);
     case 2: return run_sip_axis<2, true>(c, mc, dir, p, q, a);
