@@ -85,3 +85,29 @@ def test_host_pipeline_exact_at_cfg3(gpu):
     yh = torch.empty(D.n_u, dtype=torch.float64).pin_memory()
     gpu.apply_momentum_host(D, coefs, w.cpu().pin_memory(), x.pin_memory(), yh)
     assert torch.equal(yh, y.cpu())
+
+
+@pytest.mark.parametrize("n_el,ku,seed,Re,restart", [(32, 2, 1, 100.0, 50)])
+def test_full_trbdf2_step_fast_vs_generic(gpu, n_el, ku, seed, Re, restart):
+    """BASELINE cfg2 TR-BDF2 step with the fast kernels vs the generic kernels:
+    Krylov iteration counts within +-1, end fields within relative L2 1e-9."""
+    import torch
+    D = gpu.DGContext(3, n_el, ku, ku - 1)
+    f = gpu.SynthField(3, seed)
+    for bid in range(6):
+        D.set_dirichlet_fn(bid, f.fn_ptr, f.user_ptr, 0.0)
+    u0 = D.zeros()
+    gpu.interpolate_synth_device(D, f, u0)
+    p0 = D.zeros(gpu.SPACE_P)
+    sp = gpu.StepParams(dt=1e-3, Re=Re, c=1e3, restart=restart, first_step=True)
+    res = {}
+    for fast in (True, False):
+        D.set_fast_path(fast)
+        u1, p1 = D.zeros(), D.zeros(gpu.SPACE_P)
+        its = gpu.trbdf2_step(D, sp, u0, u0, p0, u1, p1)
+        torch.cuda.synchronize()
+        res[fast] = (its, u1, p1)
+    D.set_fast_path(True)
+    assert all(abs(a - b) <= 1 for a, b in zip(res[True][0], res[False][0])), (res[True][0], res[False][0])
+    assert rel(res[True][1], res[False][1]) <= 1e-9
+    assert rel(res[True][2], res[False][2]) <= 1e-9
