@@ -92,6 +92,7 @@ struct OpTable {
 // fast axis-aligned 3D kernels (fast_d3.cu); cudaErrorNotSupported when not applicable
 cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, double* y);
 cudaError_t fast_momentum3(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);
+cudaError_t fast_momentum_diag3(const DevCtx& c, MomCoef co, const double* w, double* y);
 struct CgState;
 // CG apply on the axis-aligned scalar SIP operator with <p, q> fused (fast_axis.cuh
 // k_sip_axis<.., CGF>): q = A p, block partials, alpha written to st by the last block

@@ -1245,4 +1245,259 @@ __global__ void __launch_bounds__(PGradCfg<K>::T) k_pgrad_axis(MeshArgs m, Unifo
 #undef INFO
 }
 
+// ===========================================================================
+// Exact diagonal of the momentum operator (momentum_diagonal, forms.cpp:606-810),
+// axis-aligned affine, 3D, skew = 0.  One warp per cell.
+//   mass + viscous: diag of sum_d (S_d (x) M (x) M) + mc detJ M (x) M (x) M, i.e. the 1D
+//     line-operator diagonals (stiffness + the own-side face terms) times the mass
+//     diagonals — exact, like the apply;
+//   advection (k+2 rule): -adv detJ sum_d ih_d sum_q w_d(q) phi_b dphi_b/dxi_d, a
+//     sum-factorised contraction of w_d at the Gauss points with w B^2 / w B D tables;
+//   LF faces: adv sum_q (0.5 w.n + 0.5 lambda) phi_b^2 (|w.n| or w.n on boundaries) on
+//     the face-layer nodes, w.n of both sides interpolated to the face Gauss points.
+// The value is the same for the three components (forms.cpp:635).
+// ===========================================================================
+template <int K>
+struct MomDiagCfg {
+  static constexpr int N = K + 1, Q = K + 2, NB = N * N * N, NF = N * N, QN = Q * N, QQ = Q * Q;
+  static constexpr int C = 4, T = 32 * C;
+  // per cell: w (3 NB) | info | work: XW (3 Q N N), YW (3 Q Q N), WQ (3 Q^3), R (3 Q Q N / 3 Q N N), faces
+  static constexpr int O_W = 0, O_INFO = 3 * NB;
+  static constexpr int O_WK = O_INFO + kInfoDoubles;
+  static constexpr int XW = 0, YW = XW + 3 * Q * NF, WQ = YW + 3 * QQ * N, R1 = WQ + 3 * QQ * Q,
+                       R2 = R1 + 3 * QQ * N, R3 = R2 + 3 * Q * NF, FV = R3 + 3 * NB,
+                       FG = FV + 6 * 2 * QN, FD = FG + 6 * QN, WEND = FD + 6 * NF;
+  static constexpr int PER = (O_WK + WEND) | 1;
+  static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
+};
+
+template <int K, bool UNI>
+__global__ void __launch_bounds__(MomDiagCfg<K>::T) k_momentum_diag_axis(MeshArgs m, UniformGrid ug,
+                                                                          const double* __restrict__ aff,
+                                                                          MomCoef co, const double* __restrict__ w,
+                                                                          double* __restrict__ y) {
+  using G = MomDiagCfg<K>;
+  constexpr int N = G::N, Q = G::Q, NB = G::NB, NF = G::NF, QN = G::QN, QQ = G::QQ, C = G::C, PER = G::PER;
+  const FTab<N, Q>& tq = c_ft<N, Q>;
+  const FTab<N, N>& ta = c_ft<N, N>;
+  extern __shared__ double sm[];
+  const int c0 = blockIdx.x * C;
+  const int nc = min(C, m.ncells - c0);
+  const int tid = threadIdx.x, lane = tid & 31, wc = tid >> 5;
+  const bool adv = co.adv != 0.0;
+  double* cell = sm + wc * PER;
+  double* wk = cell + G::O_WK;
+  CellInfo& ci = *reinterpret_cast<CellInfo*>(cell + G::O_INFO);
+  for (int idx = tid; idx < nc * 3 * NB; idx += G::T) {
+    const int c = idx / (3 * NB), r = idx - c * 3 * NB;
+    if (adv) cp_async8(sm + c * PER + G::O_W + r, w + (size_t)(c0 + c) * 3 * NB + r);
+  }
+  load_info_par<G::T, UNI>(sm, PER, G::O_INFO, nc, m, ug, aff, c0, (double)(N * N));
+  cp_async_wait_all();
+  __syncthreads();
+  if (wc >= nc) return;
+  const int cell_id = c0 + wc;
+  if (lane < 6) face_coefs(ci, lane, true, true, false);
+  __syncwarp();
+  if (adv) {
+    // w at the Gauss points: x, then y, then z (3 fields)
+    for (int it = lane; it < 3 * NF; it += 32) {  // XW[f][qx][j][k]
+      const int f = it / NF, jk = it - f * NF;
+      double v[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) v[i] = cell[G::O_W + f * NB + i + N * jk];
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        double a = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) a = fma(tq.B[qx][i], v[i], a);
+        wk[G::XW + f * Q * NF + qx * NF + jk] = a;
+      }
+    }
+    __syncwarp();
+    for (int it = lane; it < 3 * Q * N; it += 32) {  // YW[f][qx][qy][k]
+      const int f = it / (Q * N), r = it - f * Q * N, qx = r / N, k = r - qx * N;
+      double v[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = wk[G::XW + f * Q * NF + qx * NF + j + N * k];
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        double a = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) a = fma(tq.B[qy][j], v[j], a);
+        wk[G::YW + f * QQ * N + (qx * Q + qy) * N + k] = a;
+      }
+    }
+    __syncwarp();
+    for (int it = lane; it < 3 * QQ; it += 32) {  // WQ[f][qx][qy][qz]
+      const int f = it / QQ, r = it - f * QQ;
+      double v[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) v[k] = wk[G::YW + f * QQ * N + r * N + k];
+#pragma unroll
+      for (int qz = 0; qz < Q; ++qz) {
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) a = fma(tq.B[qz][k], v[k], a);
+        wk[G::WQ + f * QQ * Q + r * Q + qz] = a;
+      }
+    }
+    __syncwarp();
+    // T_d = sum_q w_d(q) prod_e tab_e[b_e][q_e], tab_d = w B D, tab_e = w B^2 (e != d)
+    for (int it = lane; it < 3 * QQ; it += 32) {  // R1[d][qx][qy][bz]
+      const int d = it / QQ, r = it - d * QQ;
+      double v[Q];
+#pragma unroll
+      for (int qz = 0; qz < Q; ++qz) v[qz] = wk[G::WQ + d * QQ * Q + r * Q + qz];
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        double a = 0.0;
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz)
+          a = fma(tq.w[qz] * tq.B[qz][b] * (d == 2 ? tq.D[qz][b] : tq.B[qz][b]), v[qz], a);
+        wk[G::R1 + d * QQ * N + r * N + b] = a;
+      }
+    }
+    __syncwarp();
+    for (int it = lane; it < 3 * Q * N; it += 32) {  // R2[d][qx][by][bz]
+      const int d = it / (Q * N), r = it - d * Q * N, qx = r / N, bz = r - qx * N;
+      double v[Q];
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) v[qy] = wk[G::R1 + d * QQ * N + (qx * Q + qy) * N + bz];
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        double a = 0.0;
+#pragma unroll
+        for (int qy = 0; qy < Q; ++qy)
+          a = fma(tq.w[qy] * tq.B[qy][b] * (d == 1 ? tq.D[qy][b] : tq.B[qy][b]), v[qy], a);
+        wk[G::R2 + d * Q * NF + qx * NF + b * N + bz] = a;
+      }
+    }
+    __syncwarp();
+    for (int it = lane; it < 3 * NF; it += 32) {  // R3[d][bx][by][bz]
+      const int d = it / NF, r = it - d * NF;  // r = by * N + bz
+      double v[Q];
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) v[qx] = wk[G::R2 + d * Q * NF + qx * NF + r];
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        double a = 0.0;
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx)
+          a = fma(tq.w[qx] * tq.B[qx][b] * (d == 0 ? tq.D[qx][b] : tq.B[qx][b]), v[qx], a);
+        {
+          const int by = r / N, bz = r - by * N;
+          wk[G::R3 + d * NB + b + N * by + NF * bz] = a;
+        }
+      }
+    }
+    // LF face diagonals: w.n of both sides at the face Gauss points, then
+    // adv * coef * (w B^2) (x) (w B^2) onto the face-layer nodes
+    for (int it = lane; it < 6 * N; it += 32) {  // FV[f][side][q][qp]: B along p
+      const int f = it / N, q = it - f * N, a = f >> 1, s = f & 1;
+      const int Ls = s ? N - 1 : 0, Lo = s ? 0 : N - 1;
+      const int nb = ci.nb[f];
+      const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
+      double vs[N], vo[N];
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        const int base = a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q);
+        vs[p] = cell[G::O_W + a * NB + base + Ls * gst];
+        vo[p] = nb >= 0 ? __ldg(w + (size_t)nb * 3 * NB + a * NB + base + Lo * gst) : 0.0;
+      }
+#pragma unroll
+      for (int qp = 0; qp < Q; ++qp) {
+        double as = 0.0, ao = 0.0;
+#pragma unroll
+        for (int p = 0; p < N; ++p) {
+          as = fma(tq.B[qp][p], vs[p], as);
+          ao = fma(tq.B[qp][p], vo[p], ao);
+        }
+        wk[G::FV + (f * 2 + 0) * QN + q * Q + qp] = as;
+        wk[G::FV + (f * 2 + 1) * QN + q * Q + qp] = ao;
+      }
+    }
+    __syncwarp();
+    for (int it = lane; it < 6 * Q; it += 32) {  // FG[f][qp][q_]: B along q, coef, (w B^2) back along q
+      const int f = it / Q, qp = it - f * Q, s = f & 1;
+      const int ty = ci.type[f];
+      const double sgn = s ? 1.0 : -1.0;
+      double vs[N], vo[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        vs[q] = wk[G::FV + (f * 2 + 0) * QN + q * Q + qp];
+        vo[q] = wk[G::FV + (f * 2 + 1) * QN + q * Q + qp];
+      }
+      double g[N];
+#pragma unroll
+      for (int b = 0; b < N; ++b) g[b] = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < Q; ++qq) {
+        double ws = 0.0, wo = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          ws = fma(tq.B[qq][q], vs[q], ws);
+          wo = fma(tq.B[qq][q], vo[q], wo);
+        }
+        const double wns = sgn * ws, wno = sgn * wo;
+        const double cf = ty == 0 ? 0.5 * wns + 0.5 * fmax(fabs(wns), fabs(wno)) : (ty == 2 ? wns : fabs(wns));
+#pragma unroll
+        for (int b = 0; b < N; ++b) g[b] = fma(tq.w[qq] * tq.B[qq][b] * tq.B[qq][b], cf, g[b]);
+      }
+#pragma unroll
+      for (int b = 0; b < N; ++b) wk[G::FG + f * QN + qp * N + b] = g[b];
+    }
+    __syncwarp();
+    for (int it = lane; it < 6 * N; it += 32) {  // FD[f][p_ + N q_]: (w B^2) along p
+      const int f = it / N, bq = it - f * N;
+      double v[Q];
+#pragma unroll
+      for (int qp = 0; qp < Q; ++qp) v[qp] = wk[G::FG + f * QN + qp * N + bq];
+      const double fa = co.adv * ci.A[f >> 1];
+#pragma unroll
+      for (int bp = 0; bp < N; ++bp) {
+        double a = 0.0;
+#pragma unroll
+        for (int qp = 0; qp < Q; ++qp) a = fma(tq.w[qp] * tq.B[qp][bp] * tq.B[qp][bp], v[qp], a);
+        wk[G::FD + f * NF + bp + N * bq] = fa * a;
+      }
+    }
+    __syncwarp();
+  }
+  // assemble: mass + viscous (line diagonals) + advection (cell + faces)
+  const double cm = co.mass * ci.detJ;
+  const double ca = -co.adv * ci.detJ;
+  for (int b = lane; b < NB; b += 32) {
+    const int bi[3] = {b % N, (b / N) % N, b / NF};
+    double md[3], sd[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int i = bi[d];
+      md[d] = ta.M[i][i];
+      const double ih = ci.ih[d], sa = co.visc * ci.A[d], stiff = sa * ih;
+      const double* cR = ci.fc[2 * d + 1];
+      const double* cL = ci.fc[2 * d];
+      double v = stiff * ta.K[i][i];
+      if (i == N - 1) v += sa * (cR[0] * ta.dE[1][i] + cR[2]) + ta.dE[1][i] * stiff * cR[4];
+      if (i == 0) v += sa * (cL[0] * ta.dE[0][i] + cL[2]) - ta.dE[0][i] * stiff * cL[4];
+      sd[d] = v;
+    }
+    double v = sd[0] * md[1] * md[2] + md[0] * sd[1] * md[2] + md[0] * md[1] * sd[2] + cm * md[0] * md[1] * md[2];
+    if (adv) {
+      v += ca * (ci.ih[0] * wk[G::R3 + 0 * NB + b] + ci.ih[1] * wk[G::R3 + 1 * NB + b] +
+                 ci.ih[2] * wk[G::R3 + 2 * NB + b]);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const int t = (a == 0 ? bi[1] : bi[0]) + N * (a == 2 ? bi[1] : bi[2]);
+        if (bi[a] == 0) v += wk[G::FD + (2 * a) * NF + t];
+        if (bi[a] == N - 1) v += wk[G::FD + (2 * a + 1) * NF + t];
+      }
+    }
+    double* yo = y + (size_t)cell_id * 3 * NB + b;
+    yo[0] = v;
+    yo[NB] = v;
+    yo[2 * NB] = v;
+  }
+}
+
 }  // namespace dgb

@@ -224,6 +224,33 @@ cudaError_t fast_sip3_cg(const DevCtx& c, double mc, int dir, const double* p, d
   return cudaErrorNotSupported;
 }
 
+template <int K>
+static cudaError_t run_momentum_diag_axis(const DevCtx& c, MomCoef co, const double* w, double* y) {
+  cudaError_t e = ensure_ftab<K + 1, K + 2>();
+  if (e == cudaSuccess) e = ensure_ftab<K + 1, K + 1>();
+  if (e != cudaSuccess) return e;
+  using G = MomDiagCfg<K>;
+  const int grid = (c.ncells + G::C - 1) / G::C;
+  if (c.ug.n > 0) {
+    if ((e = set_smem(k_momentum_diag_axis<K, true>, G::SMEM)) != cudaSuccess) return e;
+    k_momentum_diag_axis<K, true><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, co, w, y);
+  } else {
+    if ((e = set_smem(k_momentum_diag_axis<K, false>, G::SMEM)) != cudaSuccess) return e;
+    k_momentum_diag_axis<K, false><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, co, w, y);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t fast_momentum_diag3(const DevCtx& c, MomCoef co, const double* w, double* y) {
+  if (co.skew != 0.0 || (co.adv != 0.0 && w == nullptr)) return cudaErrorNotSupported;
+  switch (c.ku) {
+    case 1: return run_momentum_diag_axis<1>(c, co, w, y);
+    case 2: return run_momentum_diag_axis<2>(c, co, w, y);
+    case 3: return run_momentum_diag_axis<3>(c, co, w, y);
+  }
+  return cudaErrorNotSupported;
+}
+
 cudaError_t fast_momentum3(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y) {
   if (co.skew != 0.0 || w == nullptr) return cudaErrorNotSupported;
   switch (c.ku) {

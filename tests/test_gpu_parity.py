@@ -146,6 +146,13 @@ def test_fast_axis_path_matches_reference(ref, gpu, n_el, ku, kp, outlet):
         gpu.apply_momentum(D, ctx, dev(x), y)
         outs.append(host(y))
         assert rel(outs[-1], want) <= TOL_APPLY, fast
+    want_d = R.momentum_diag(coefs, w)
+    for fast in (True, False):
+        D.set_fast_path(fast)
+        d = D.zeros()
+        gpu.momentum_diagonal(D, ctx, d)
+        assert rel(host(d), want_d) <= TOL_APPLY, ("diag", fast)
+    D.set_fast_path(True)
     # a viscous-dominated operator exercises the face terms harder
     coefs2 = (0.3, 2.0, 1.5, 0.0)
     want2 = R.momentum(coefs2, w, x)
@@ -385,6 +392,9 @@ def test_graded_axis_mesh_operators(ref, gpu, n, ku, kp, outlet):
         y = D.zeros()
         gpu.apply_momentum(D, gpu.MomentumCtx(*coefs, advecting=dev(w)), dev(x), y)
         assert rel(host(y), R.momentum(coefs, w, x)) <= TOL_APPLY
+        dg_ = D.zeros()
+        gpu.momentum_diagonal(D, gpu.MomentumCtx(*coefs, advecting=dev(w)), dg_)
+        assert rel(host(dg_), R.momentum_diag(coefs, w)) <= TOL_APPLY
     for mc in (2.3, 0.0):
         yp = D.zeros(gpu.SPACE_P)
         gpu.apply_pressure_helmholtz(D, mc, dev(xp), yp)
