@@ -361,6 +361,13 @@ int Context::apply_host(bool mom, const double* coefs, double mc, const double* 
 }
 int Context::sip_diag(double mc, int dir, double* d) {
   ++launches;
+  if (use_fast && dc.axis) {
+    const cudaError_t e = fast_sip_diag3(dc, mc, dir, d);
+    if (e != cudaErrorNotSupported) {
+      CK(e);
+      return DGB_OK;
+    }
+  }
   CK(opp->sip_diag(dc, mc, dir, d));
   return DGB_OK;
 }
@@ -422,6 +429,13 @@ int Context::rhs(const dgb_rhs_desc& ds, double* y) {
 }
 int Context::divergence(const double* u, double* y) {
   ++launches;
+  if (use_fast && dc.axis) {
+    const cudaError_t e = fast_divergence3(dc, u, y);
+    if (e != cudaErrorNotSupported) {
+      CK(e);
+      return DGB_OK;
+    }
+  }
   CK(opu->divergence(dc, u, y));
   return DGB_OK;
 }

@@ -1137,6 +1137,7 @@ template <int K>
 struct PTab {
   double Mvp[K + 1][K];  // sum_q w phi_i psi_j
   double G1[K + 1][K];   // sum_q w phi_i' psi_j
+  double Dpv[K][K + 1];  // sum_q w psi_i' phi_j (divergence: pressure-test derivative x velocity)
 };
 template <int K>
 __constant__ PTab<K> c_pt;
@@ -1497,6 +1498,150 @@ __global__ void __launch_bounds__(MomDiagCfg<K>::T) k_momentum_diag_axis(MeshArg
     yo[0] = v;
     yo[NB] = v;
     yo[2 * NB] = v;
+  }
+}
+
+// ===========================================================================
+// Divergence functional (divergence_functional, forms.cpp:1118-1197), axis-aligned
+// affine, 3D:  y = sum_d (D_d (x) Mpv (x) Mpv) u_d,  D_d = 1D line operator along d
+// (pressure-test derivative x velocity value, exact for the k+1 rule) plus the
+// -{u_d} n_d q faces at the two line ends (own trace on non-outlet boundaries);
+// Mpv = Mvp^T (pressure test x velocity value).
+// ===========================================================================
+template <int K>
+struct DivCfg {
+  static constexpr int N = K + 1, NP = K, NB = N * N * N, NBP = NP * NP * NP;
+  static constexpr int C = 8, T = 128;
+  static constexpr int L1 = 3 * NP * N * N, L2 = 3 * NP * NP * N;
+  static constexpr int PER = (3 * NB + L1 + L2 + kInfoDoubles) | 1;
+  static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
+};
+
+template <int K, bool UNI>
+__global__ void __launch_bounds__(DivCfg<K>::T) k_div_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff,
+                                                           const double* __restrict__ u, double* __restrict__ y) {
+  using G = DivCfg<K>;
+  constexpr int N = G::N, NP = G::NP, NB = G::NB, NBP = G::NBP, C = G::C, PER = G::PER, TT = G::T;
+  const PTab<K>& pt = c_pt<K>;
+  extern __shared__ double sm[];
+  const int c0 = blockIdx.x * C;
+  const int nc = min(C, m.ncells - c0);
+  const int tid = threadIdx.x;
+#define CELL(c) (sm + (c) * PER)
+#define INFO(c) (*reinterpret_cast<const CellInfo*>(sm + (c) * PER + 3 * NB + G::L1 + G::L2))
+  for (int idx = tid; idx < nc * 3 * NB; idx += TT) cp_async8(CELL(idx / (3 * NB)) + idx % (3 * NB), u + (size_t)c0 * 3 * NB + idx);
+  load_info_par<TT, UNI>(sm, PER, 3 * NB + G::L1 + G::L2, nc, m, ug, aff, c0, 1.0);
+  cp_async_wait_all();
+  __syncthreads();
+  // S1: line operator along d on the u_d lines (tangential (a, b), t1 < t2) -> T1[d][i][a][b]
+  for (int idx = tid; idx < nc * 3 * N * N; idx += TT) {
+    const int c = idx / (3 * N * N), r = idx - c * 3 * N * N;
+    const int d = r / (N * N), ab = r - d * N * N;
+    const int a = ab % N, b = ab / N;
+    const int st = d == 0 ? 1 : (d == 1 ? N : N * N);
+    const int b0 = d * NB + (d == 0 ? N * a + N * N * b : (d == 1 ? a + N * N * b : a + N * b));
+    const CellInfo& ci = INFO(c);
+    double ul[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) ul[j] = CELL(c)[b0 + j * st];
+    const double cs = ci.detJ * ci.ih[d], A = ci.A[d];
+    double o[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc = fma(pt.Dpv[i][j], ul[j], acc);
+      o[i] = cs * acc;
+    }
+    {  // left face, n_d = -1: -{u_d} n_d -> +A uf at pressure node 0
+      const int f = 2 * d, nb = ci.nb[f], ty = ci.type[f];
+      const double own = ul[0];
+      const double uf = ty == 0 ? 0.5 * (own + __ldg(u + (size_t)nb * 3 * NB + b0 + (N - 1) * st)) : (ty == 1 ? own : 0.0);
+      o[0] = fma(A, uf, o[0]);
+    }
+    {  // right face, n_d = +1: -A uf at pressure node NP-1
+      const int f = 2 * d + 1, nb = ci.nb[f], ty = ci.type[f];
+      const double own = ul[N - 1];
+      const double uf = ty == 0 ? 0.5 * (own + __ldg(u + (size_t)nb * 3 * NB + b0)) : (ty == 1 ? own : 0.0);
+      o[NP - 1] = fma(-A, uf, o[NP - 1]);
+    }
+    double* t1 = CELL(c) + 3 * NB + d * NP * N * N;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) t1[i + NP * ab] = o[i];
+  }
+  __syncthreads();
+  // S2: Mpv along t1 -> T2[d][i + NP (a' + NP b)]
+  for (int idx = tid; idx < nc * 3 * NP * N; idx += TT) {
+    const int c = idx / (3 * NP * N), r = idx - c * 3 * NP * N;
+    const int d = r / (NP * N), ib = r - d * NP * N;
+    const int i = ib % NP, b = ib / NP;
+    const double* t1 = CELL(c) + 3 * NB + d * NP * N * N;
+    double v[N];
+#pragma unroll
+    for (int a = 0; a < N; ++a) v[a] = t1[i + NP * (a + N * b)];
+    double* t2 = CELL(c) + 3 * NB + G::L1 + d * NP * NP * N;
+#pragma unroll
+    for (int a2 = 0; a2 < NP; ++a2) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < N; ++a) acc = fma(pt.Mvp[a][a2], v[a], acc);
+      t2[i + NP * (a2 + NP * b)] = acc;
+    }
+  }
+  __syncthreads();
+  // S3: Mpv along t2, summed over d, -> y
+  for (int idx = tid; idx < nc * NBP; idx += TT) {
+    const int c = idx / NBP, node = idx - c * NBP;
+    const int ix = node % NP, iy = (node / NP) % NP, iz = node / (NP * NP);
+    double sum = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int i = d == 0 ? ix : (d == 1 ? iy : iz);
+      const int a2 = d == 0 ? iy : ix, b2 = d == 2 ? iy : iz;
+      const double* t2 = CELL(c) + 3 * NB + G::L1 + d * NP * NP * N;
+#pragma unroll
+      for (int b = 0; b < N; ++b) sum = fma(pt.Mvp[b][b2], t2[i + NP * (a2 + NP * b)], sum);
+    }
+    y[(size_t)(c0 + c) * NBP + node] = sum;
+  }
+#undef CELL
+#undef INFO
+}
+
+// Exact diagonal of the scalar SIP operator (scalar_sip_diagonal, forms.cpp:246-329):
+// diag(mc M (x) M (x) M + sum_d S_d (x) M (x) M).
+template <int KP, bool UNI>
+__global__ void __launch_bounds__(128) k_sip_diag_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff,
+                                                       double mc, int dir_bdry, double* __restrict__ y) {
+  constexpr int N = KP + 1, NB = N * N * N, C = 16;
+  const FTab<N, N>& ta = c_ft<N, N>;
+  __shared__ double info[C][kInfoDoubles];
+  const int c0 = blockIdx.x * C;
+  const int nc = min(C, m.ncells - c0);
+  load_info_par<128, UNI>(&info[0][0], kInfoDoubles, 0, nc, m, ug, aff, c0, (double)(N * N));
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < nc * 6; idx += 128)
+    face_coefs(*reinterpret_cast<CellInfo*>(info[idx / 6]), idx % 6, dir_bdry != 0, false);
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < nc * NB; idx += 128) {
+    const int c = idx / NB, b = idx - c * NB;
+    const CellInfo& ci = *reinterpret_cast<const CellInfo*>(info[c]);
+    const int bi[3] = {b % N, (b / N) % N, b / (N * N)};
+    double md[3], sd[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int i = bi[d];
+      md[d] = ta.M[i][i];
+      const double ih = ci.ih[d], sa = ci.A[d], stiff = sa * ih;
+      const double* cR = ci.fc[2 * d + 1];
+      const double* cL = ci.fc[2 * d];
+      double v = stiff * ta.K[i][i];
+      if (i == N - 1) v += sa * (cR[0] * ta.dE[1][i] + cR[2]) + ta.dE[1][i] * stiff * cR[4];
+      if (i == 0) v += sa * (cL[0] * ta.dE[0][i] + cL[2]) - ta.dE[0][i] * stiff * cL[4];
+      sd[d] = v;
+    }
+    y[(size_t)(c0 + c) * NB + b] = sd[0] * md[1] * md[2] + md[0] * sd[1] * md[2] + md[0] * md[1] * sd[2] +
+                                   mc * ci.detJ * md[0] * md[1] * md[2];
   }
 }
 

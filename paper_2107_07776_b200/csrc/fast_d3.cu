@@ -26,7 +26,7 @@ void host_ftab(int N, int Q, double* M, double* K, double* B, double* D, double*
 }
 
 // mixed velocity / pressure 1D tables (rule k+1): Mvp = sum_q w phi_i psi_j, G1 = sum_q w phi_i' psi_j
-static void host_ptab(int K, double* Mvp, double* G1) {
+static void host_ptab(int K, double* Mvp, double* G1, double* Dpv) {
   const int N = K + 1, NP = K, Q = K + 1;
   std::vector<double> Bn(Q * N), Dn(Q * N), En(2 * N), Bp(Q * NP), Dp(Q * NP), Ep(2 * NP), w(Q);
   host_tab(N, Q, Bn.data(), Dn.data(), En.data());
@@ -42,6 +42,12 @@ static void host_ptab(int K, double* Mvp, double* G1) {
       Mvp[i * NP + j] = mv;
       G1[i * NP + j] = g;
     }
+  for (int i = 0; i < NP; ++i)
+    for (int j = 0; j < N; ++j) {
+      double dv = 0.0;
+      for (int q = 0; q < Q; ++q) dv += w[q] * Dp[q * NP + i] * Bn[q * N + j];
+      Dpv[i * N + j] = dv;
+    }
 }
 template <int K>
 static cudaError_t ensure_ptab() {
@@ -50,7 +56,7 @@ static cudaError_t ensure_ptab() {
   cudaGetDevice(&dev);
   if (done_dev == dev) return cudaSuccess;
   PTab<K> t;
-  host_ptab(K, &t.Mvp[0][0], &t.G1[0][0]);
+  host_ptab(K, &t.Mvp[0][0], &t.G1[0][0], &t.Dpv[0][0]);
   const cudaError_t e = cudaMemcpyToSymbol(c_pt<K>, &t, sizeof(t));
   if (e == cudaSuccess) done_dev = dev;
   return e;
@@ -247,6 +253,51 @@ cudaError_t fast_momentum_diag3(const DevCtx& c, MomCoef co, const double* w, do
     case 1: return run_momentum_diag_axis<1>(c, co, w, y);
     case 2: return run_momentum_diag_axis<2>(c, co, w, y);
     case 3: return run_momentum_diag_axis<3>(c, co, w, y);
+  }
+  return cudaErrorNotSupported;
+}
+
+template <int K>
+static cudaError_t run_div_axis(const DevCtx& c, const double* u, double* y) {
+  cudaError_t e = ensure_ptab<K>();
+  if (e != cudaSuccess) return e;
+  using G = DivCfg<K>;
+  const int grid = (c.ncells + G::C - 1) / G::C;
+  if (c.ug.n > 0) {
+    if ((e = set_smem(k_div_axis<K, true>, G::SMEM)) != cudaSuccess) return e;
+    k_div_axis<K, true><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, u, y);
+  } else {
+    if ((e = set_smem(k_div_axis<K, false>, G::SMEM)) != cudaSuccess) return e;
+    k_div_axis<K, false><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, c.ug, c.aff, u, y);
+  }
+  return cudaGetLastError();
+}
+cudaError_t fast_divergence3(const DevCtx& c, const double* u, double* y) {
+  if (c.kp != c.ku - 1) return cudaErrorNotSupported;
+  switch (c.ku) {
+    case 2: return run_div_axis<2>(c, u, y);
+    case 3: return run_div_axis<3>(c, u, y);
+    case 4: return run_div_axis<4>(c, u, y);
+  }
+  return cudaErrorNotSupported;
+}
+
+template <int KP>
+static cudaError_t run_sip_diag_axis(const DevCtx& c, double mc, int dir, double* y) {
+  cudaError_t e = ensure_ftab<KP + 1, KP + 1>();
+  if (e != cudaSuccess) return e;
+  const int grid = (c.ncells + 15) / 16;
+  if (c.ug.n > 0)
+    k_sip_diag_axis<KP, true><<<grid, 128, 0, c.stream>>>(c.mesh, c.ug, c.aff, mc, dir, y);
+  else
+    k_sip_diag_axis<KP, false><<<grid, 128, 0, c.stream>>>(c.mesh, c.ug, c.aff, mc, dir, y);
+  return cudaGetLastError();
+}
+cudaError_t fast_sip_diag3(const DevCtx& c, double mc, int dir, double* y) {
+  switch (c.kp) {
+    case 1: return run_sip_diag_axis<1>(c, mc, dir, y);
+    case 2: return run_sip_diag_axis<2>(c, mc, dir, y);
+    case 3: return run_sip_diag_axis<3>(c, mc, dir, y);
   }
   return cudaErrorNotSupported;
 }

@@ -399,6 +399,12 @@ def test_graded_axis_mesh_operators(ref, gpu, n, ku, kp, outlet):
         yp = D.zeros(gpu.SPACE_P)
         gpu.apply_pressure_helmholtz(D, mc, dev(xp), yp)
         assert rel(host(yp), R.pressure(mc, xp)) <= TOL_APPLY
+        dp = D.zeros(gpu.SPACE_P)
+        gpu.helmholtz_diagonal(D, mc, dp)
+        assert rel(host(dp), R.helmholtz_diag(mc)) <= TOL_APPLY
+    b = D.zeros(gpu.SPACE_P)
+    gpu.divergence_functional(D, dev(x), b)
+    assert rel(host(b), R.divergence(x)) <= TOL_APPLY
     ug = gpu.seeded_uniform(94, R.n_u)
     want = R.momentum_rhs(mass=[(2.9, x)], visc=[(0.65, x), (0.3, ug)], adv=[(0.5, x, w), (0.25, ug, ug)],
                           pres=[(1.0, xp), (-0.4, xp)], dir_visc=0.65, dir_adv=0.5, dir_w=w, time=0.0)
