@@ -28,6 +28,15 @@
 namespace dgb {
 
 constexpr int kThreads = 256;
+// generic momentum kernel: threads per block and shared-memory budget per block
+// (tools/tune_gmom.sh overrides; measured best: k = 4 (cfg4) 64 threads / 48 KB: 45.8 -> 39.9 ms)
+#ifdef DGB_GMOM_T
+template <int K> constexpr int mom_threads() { return DGB_GMOM_T; }
+template <int K> constexpr int mom_smem_kb() { return DGB_GMOM_KB; }
+#else
+template <int K> constexpr int mom_threads() { return K == 4 ? 64 : 256; }
+template <int K> constexpr int mom_smem_kb() { return K == 4 ? 48 : 96; }
+#endif
 
 __device__ __forceinline__ bool is_outlet(const MeshArgs& m, int nb) {
   const int bid = -1 - nb;
@@ -88,7 +97,7 @@ struct MomLayout {
   static constexpr int WQ = (DIM + 1) * EB::NQ;       // w values + div w at rule-B points
   static constexpr int WF = NF * 2 * DIM * EB::NQF;    // w traces, both sides, every face
   static constexpr int PER_CELL = NB * (2 + NF) + SCR + QBK + 2 * FBK + WQ + WF;
-  static constexpr int CB_RAW = (96 * 1024 / 8) / PER_CELL;
+  static constexpr int CB_RAW = (mom_smem_kb<K>() * 1024 / 8) / PER_CELL;
   static constexpr int CB = CB_RAW < 1 ? 1 : (CB_RAW > 16 ? 16 : CB_RAW);
   static constexpr size_t SMEM = (size_t)CB * PER_CELL * sizeof(double);
 };
@@ -146,7 +155,7 @@ __device__ void momentum_w_phase(const MeshArgs& m, const GeoArgs& gB, bool skew
 }
 
 template <int DIM, int K, template <int, int> class Geo>
-__global__ void __launch_bounds__(kThreads) k_momentum(MeshArgs m, GeoArgs gA, GeoArgs gB, MomCoef co,
+__global__ void __launch_bounds__(mom_threads<K>()) k_momentum(MeshArgs m, GeoArgs gA, GeoArgs gB, MomCoef co,
                                                        const double* __restrict__ x,
                                                        const double* __restrict__ w, double* __restrict__ y) {
   if (m.skip && *m.skip) return;

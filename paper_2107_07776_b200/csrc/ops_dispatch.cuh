@@ -29,7 +29,7 @@ cudaError_t run_momentum(const DevCtx& c, MomCoef co, const double* w, const dou
   cudaError_t e = prep(kern, L::SMEM);
   if (e != cudaSuccess) return e;
   const int grid = (c.ncells + L::CB - 1) / L::CB;
-  kern<<<grid, kThreads, L::SMEM, c.stream>>>(c.mesh, geo_for(c, K + 1), geo_for(c, K + 2), co, x, w, y);
+  kern<<<grid, mom_threads<K>(), L::SMEM, c.stream>>>(c.mesh, geo_for(c, K + 1), geo_for(c, K + 2), co, x, w, y);
   return cudaGetLastError();
 }
 
