@@ -336,7 +336,10 @@ __device__ __forceinline__ void sip_line(const FTab<N, N>& t, const CellInfo& ci
 template <int KP>
 struct SipAxisCfg {
   static constexpr int N = KP + 1, NB = N * N * N, NF = N * N;
-  using P = Pad<N>;
+  #ifndef DGB_SIP_PX3
+#define DGB_SIP_PX3 3
+#endif
+  using P = Pad<N, N == 3 ? DGB_SIP_PX3 : (N | 1)>;
 #ifndef DGB_SIP2_C  // tuning overrides for experiments (tools/tune_sip.sh)
 #define DGB_SIP2_C 16
 #define DGB_SIP2_T 128
