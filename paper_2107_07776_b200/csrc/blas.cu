@@ -88,43 +88,6 @@ __global__ void k_mad_part(size_t n, const double* __restrict__ x, const double*
     if (threadIdx.x == 0) partial[blockIdx.x] = a;
   }
 }
-__global__ void k_cg_update_part(size_t n, double a, const double* __restrict__ p, const double* __restrict__ q,
-                                 double* __restrict__ x, double* __restrict__ r, const double* __restrict__ inv,
-                                 double* __restrict__ z, double* __restrict__ partial) {
-  double acc[2] = {0.0, 0.0};
-  GRID_STRIDE(i, n) {
-    x[i] = fma(a, p[i], x[i]);
-    const double ri = fma(-a, q[i], r[i]);
-    r[i] = ri;
-    const double zi = inv ? ri * inv[i] : ri;
-    z[i] = zi;
-    acc[0] = fma(ri, ri, acc[0]);
-    acc[1] = fma(ri, zi, acc[1]);
-  }
-  block_reduce_store<2>(acc, partial);
-}
-__global__ void k_precond_dot_part(size_t n, const double* __restrict__ r, const double* __restrict__ inv,
-                                   double* __restrict__ z, double* __restrict__ partial) {
-  double acc[1] = {0.0};
-  GRID_STRIDE(i, n) {
-    const double ri = r[i];
-    const double zi = inv ? ri * inv[i] : ri;
-    z[i] = zi;
-    acc[0] = fma(ri, zi, acc[0]);
-  }
-  block_reduce_store<1>(acc, partial);
-}
-__global__ void k_mgs_part(size_t n, double h, const double* __restrict__ vi, double* __restrict__ w,
-                           const double* __restrict__ vnext, double* __restrict__ partial) {
-  double acc[1] = {0.0};
-  const bool self = (vnext == w);
-  GRID_STRIDE(i, n) {
-    const double wi = fma(-h, vi[i], w[i]);
-    w[i] = wi;
-    acc[0] = fma(wi, self ? wi : vnext[i], acc[0]);
-  }
-  block_reduce_store<1>(acc, partial);
-}
 // one block: out[v] = sum_b partial[v*nparts + b]
 __global__ void k_sum_parts(int nparts, int nv, const double* __restrict__ partial, double* __restrict__ out,
                             int is_max) {
@@ -252,19 +215,6 @@ __device__ __forceinline__ void cg_upd_finish(int nparts, const double* partial,
       st->done = 3;
     }
   }
-}
-__global__ void k_mgs_part_dev(size_t n, const double* __restrict__ hp, const double* __restrict__ vi,
-                               double* __restrict__ w, const double* __restrict__ vnext,
-                               double* __restrict__ partial) {
-  const double h = *hp;
-  double acc[1] = {0.0};
-  const bool self = (vnext == w);
-  GRID_STRIDE(i, n) {
-    const double wi = fma(-h, vi[i], w[i]);
-    w[i] = wi;
-    acc[0] = fma(wi, self ? wi : vnext[i], acc[0]);
-  }
-  block_reduce_store<1>(acc, partial);
 }
 
 // ---------------------------------------------------------------- one-reduce MGS
@@ -409,20 +359,6 @@ cudaError_t r_maxabsdiff(cudaStream_t s, size_t n, const double* x, const double
   k_sum_parts<<<1, kBlasThreads, 0, s>>>(g, 1, scratch, d_out, 1);
   return cudaGetLastError();
 }
-cudaError_t r_cg_update(cudaStream_t s, size_t n, double a, const double* p, const double* q, double* x,
-                        double* r, const double* inv, double* z, double* scratch, double* d_out) {
-  const int g = blas_grid(n);
-  k_cg_update_part<<<g, kBlasThreads, 0, s>>>(n, a, p, q, x, r, inv, z, scratch);
-  k_sum_parts<<<1, kBlasThreads, 0, s>>>(g, 2, scratch, d_out, 0);
-  return cudaGetLastError();
-}
-cudaError_t r_precond_dot(cudaStream_t s, size_t n, const double* r, const double* inv, double* z,
-                          double* scratch, double* d_out) {
-  const int g = blas_grid(n);
-  k_precond_dot_part<<<g, kBlasThreads, 0, s>>>(n, r, inv, z, scratch);
-  k_sum_parts<<<1, kBlasThreads, 0, s>>>(g, 1, scratch, d_out, 0);
-  return cudaGetLastError();
-}
 cudaError_t cg_begin(cudaStream_t s, size_t n, const double* r, const double* inv, double* z, double* scratch,
                      CgState* st) {
   const int g = blas_grid(n);
@@ -498,20 +434,6 @@ cudaError_t gs_update(cudaStream_t s, size_t n, int nv, const double* const* U, 
 }
 cudaError_t v_mul_scaled(cudaStream_t s, size_t n, double a, const double* r, const double* d, double* z) {
   k_mul_scaled<<<blas_grid(n), kBlasThreads, 0, s>>>(n, a, r, d, z);
-  return cudaGetLastError();
-}
-cudaError_t r_mgs_step_dev(cudaStream_t s, size_t n, const double* h, const double* vi, double* w,
-                           const double* vnext, double* scratch, double* d_out) {
-  const int g = blas_grid(n);
-  k_mgs_part_dev<<<g, kBlasThreads, 0, s>>>(n, h, vi, w, vnext, scratch);
-  k_sum_parts<<<1, kBlasThreads, 0, s>>>(g, 1, scratch, d_out, 0);
-  return cudaGetLastError();
-}
-cudaError_t r_mgs_step(cudaStream_t s, size_t n, double h, const double* vi, double* w, const double* vnext,
-                       double* scratch, double* d_out) {
-  const int g = blas_grid(n);
-  k_mgs_part<<<g, kBlasThreads, 0, s>>>(n, h, vi, w, vnext, scratch);
-  k_sum_parts<<<1, kBlasThreads, 0, s>>>(g, 1, scratch, d_out, 0);
   return cudaGetLastError();
 }
 

@@ -63,15 +63,6 @@ cudaError_t v_recip(cudaStream_t s, size_t n, const double* d, double* inv, long
 cudaError_t r_dot(cudaStream_t s, size_t n, const double* x, const double* y, double* scratch, double* d_out);
 cudaError_t r_maxabsdiff(cudaStream_t s, size_t n, const double* x, const double* y, double* scratch,
                          double* d_out);
-// CG fused update: x += a p; r -= a q; z = r * inv (or r); out = {<r,r>, <r,z>}
-cudaError_t r_cg_update(cudaStream_t s, size_t n, double a, const double* p, const double* q, double* x,
-                        double* r, const double* inv, double* z, double* scratch, double* d_out);
-// z = r * inv (or copy); out = {<r,z>}
-cudaError_t r_precond_dot(cudaStream_t s, size_t n, const double* r, const double* inv, double* z,
-                          double* scratch, double* d_out);
-// MGS step: w -= h v_i ; out = <w, v_next> (v_next may equal w for the norm)
-cudaError_t r_mgs_step(cudaStream_t s, size_t n, double h, const double* vi, double* w, const double* vnext,
-                       double* scratch, double* d_out);
 // sum of nparts partials -> d_out
 cudaError_t r_sum(cudaStream_t s, int nparts, const double* partial, double* d_out);
 
@@ -140,8 +131,6 @@ cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q
 // MGS step with the projection read from device memory: w -= (*h) v_i ; *out = <w, v_next>
 // alpha = rho / sum(partial[0..nparts))  (CG with the <p,q> partials from a fused apply)
 cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, const double* partial, CgState* st);
-cudaError_t r_mgs_step_dev(cudaStream_t s, size_t n, const double* h, const double* vi, double* w,
-                           const double* vnext, double* scratch, double* d_out);
 
 // ---- one-reduce modified Gram-Schmidt for GMRES (krylov.cpp:140-160 restated).
 // The basis is stored unnormalised, v_j = s_j U_j.  MGS's projections follow
