@@ -280,12 +280,13 @@ int Context::momentum_diag(const double* coefs, const double* w, double* d) {
 }
 int Context::sip(double mc, int dir, const double* x, double* y) {
   ++launches;
-  if (use_fast && dc.axis) {
-    const cudaError_t e = fast_sip3(dc, mc, dir, x, y);
+  if (use_fast && (dc.axis || !dc.affine)) {
+    const cudaError_t e = dc.axis ? fast_sip3(dc, mc, dir, x, y) : fast_sip3_qp(dc, mc, dir, x, y);
     if (e != cudaErrorNotSupported) {
       CK(e);
       return DGB_OK;
     }
+    cudaGetLastError();
   }
   CK(opp->sip(dc, mc, dir, x, y));
   return DGB_OK;

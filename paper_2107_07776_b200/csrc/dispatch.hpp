@@ -91,6 +91,8 @@ struct OpTable {
 
 // fast axis-aligned 3D kernels (fast_d3.cu); cudaErrorNotSupported when not applicable
 cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, double* y);
+// deformed (per-qp geometry) 3D meshes (fast_deformed.cuh)
+cudaError_t fast_sip3_qp(const DevCtx& c, double mc, int dir, const double* x, double* y);
 cudaError_t fast_momentum3(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);
 cudaError_t fast_momentum_diag3(const DevCtx& c, MomCoef co, const double* w, double* y);
 cudaError_t fast_divergence3(const DevCtx& c, const double* u, double* y);

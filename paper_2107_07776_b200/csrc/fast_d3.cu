@@ -1,5 +1,6 @@
 // Axis-aligned affine 3D fast kernels (fast_axis.cuh) + their launchers.
 #include "fast_axis.cuh"
+#include "fast_deformed.cuh"
 
 #include <vector>
 
@@ -298,6 +299,29 @@ cudaError_t fast_sip_diag3(const DevCtx& c, double mc, int dir, double* y) {
     case 1: return run_sip_diag_axis<1>(c, mc, dir, y);
     case 2: return run_sip_diag_axis<2>(c, mc, dir, y);
     case 3: return run_sip_diag_axis<3>(c, mc, dir, y);
+  }
+  return cudaErrorNotSupported;
+}
+
+template <int KP>
+static cudaError_t run_sip_qp(const DevCtx& c, double mc, int dir, const double* x, double* y) {
+  cudaError_t e = ensure_ftab<KP + 1, KP + 2>();
+  if (e != cudaSuccess) return e;
+  using G = SipQpCfg<KP>;
+  const double* gc = c.qcell[KP + 2];
+  const double* gf = c.qface[KP + 2];
+  if (!gc || !gf) return cudaErrorNotSupported;
+  if ((e = set_smem(k_sip_qp<KP>, G::SMEM)) != cudaSuccess) return e;
+  const int grid = (c.ncells + G::C - 1) / G::C;
+  k_sip_qp<KP><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, gc, gf, mc, dir, x, y);
+  return cudaGetLastError();
+}
+cudaError_t fast_sip3_qp(const DevCtx& c, double mc, int dir, const double* x, double* y) {
+  if (c.dim != 3 || c.affine) return cudaErrorNotSupported;
+  switch (c.kp) {
+    case 1: return run_sip_qp<1>(c, mc, dir, x, y);
+    case 2: return run_sip_qp<2>(c, mc, dir, x, y);
+    case 3: return run_sip_qp<3>(c, mc, dir, x, y);
   }
   return cudaErrorNotSupported;
 }

@@ -479,3 +479,28 @@ def test_host_buffer_applies_match_device_applies(ref, gpu, n_el, ku, kp, graded
     gpu.apply_pressure_helmholtz_host(D, 2.3, np.ascontiguousarray(xp), yph)  # pageable numpy buffers
     assert np.array_equal(yph, host(yp_dev))
     assert rel(yph, R.pressure(2.3, xp)) <= TOL_APPLY
+
+
+@pytest.mark.parametrize("n_el,kp,amp", [(3, 1, 0.05), (2, 2, 0.04), (2, 3, 0.03)])
+def test_deformed_sip_kernel_matches_reference_and_generic(ref, gpu, n_el, kp, amp):
+    """fast_deformed.cuh k_sip_qp (per-qp geometry streamed) vs the reference and the
+    generic device kernel on distorted 3D meshes: pressure Helmholtz and the Dirichlet /
+    natural scalar Laplacian."""
+    R, D = pair(ref, gpu, 3, n_el, kp + 1, kp, amp)
+    assert not D.affine
+    xp = gpu.seeded_uniform(95, R.n_p)
+    for mc in (2.3, 0.0):
+        want = R.pressure(mc, xp)
+        for fast in (True, False):
+            D.set_fast_path(fast)
+            yp = D.zeros(gpu.SPACE_P)
+            gpu.apply_pressure_helmholtz(D, mc, dev(xp), yp)
+            assert rel(host(yp), want) <= TOL_APPLY, (mc, fast)
+    for dirichlet in (True, False):
+        want = R.laplace(dirichlet, xp)
+        for fast in (True, False):
+            D.set_fast_path(fast)
+            yl = D.zeros(gpu.SPACE_P)
+            gpu.apply_scalar_laplace(D, dirichlet, dev(xp), yl)
+            assert rel(host(yl), want) <= TOL_APPLY, (dirichlet, fast)
+    D.set_fast_path(True)
