@@ -207,6 +207,43 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
       cudaMemcpy(dface, g.face.data(), g.face.size() * sizeof(double), cudaMemcpyHostToDevice);
       dc.qcell[Q] = dcell;
       dc.qface[Q] = dface;
+      if (dim == 3) {  // compact records for the deformed fast kernels
+        const size_t ncq = g.cell.size() / 10, nfq = g.face.size() / 22;
+        std::vector<double> cm(ncq * 7), fn(nfq * 7);
+        for (size_t i = 0; i < ncq; ++i) {
+          const double* r = &g.cell[i * 10];
+          const double jxw = r[9];
+          double* o = &cm[i * 7];
+          int k = 0;
+          for (int a = 0; a < 3; ++a)
+            for (int b = a; b < 3; ++b) {
+              double v = 0.0;
+              for (int d = 0; d < 3; ++d) v += r[a * 3 + d] * r[b * 3 + d];
+              o[k++] = jxw * v;
+            }
+          o[6] = jxw;
+        }
+        for (size_t i = 0; i < nfq; ++i) {
+          const double* r = &g.face[i * 22];
+          const double* n = r + 18;
+          double* o = &fn[i * 7];
+          for (int a = 0; a < 3; ++a) {
+            o[a] = r[a * 3] * n[0] + r[a * 3 + 1] * n[1] + r[a * 3 + 2] * n[2];
+            o[3 + a] = r[9 + a * 3] * n[0] + r[9 + a * 3 + 1] * n[1] + r[9 + a * 3 + 2] * n[2];
+          }
+          o[6] = r[21];
+        }
+        double* dcm = (double*)dalloc(cm.size() * sizeof(double));
+        double* dfn = (double*)dalloc(fn.size() * sizeof(double));
+        if (!dcm || !dfn) {
+          e = "out of device memory (qp geometry)";
+          return DGB_E_CUDA;
+        }
+        cudaMemcpy(dcm, cm.data(), cm.size() * sizeof(double), cudaMemcpyHostToDevice);
+        cudaMemcpy(dfn, fn.data(), fn.size() * sizeof(double), cudaMemcpyHostToDevice);
+        dc.qcm[Q] = dcm;
+        dc.qfn[Q] = dfn;
+      }
     }
   }
   // Dirichlet table (rule ku+2), zero until set

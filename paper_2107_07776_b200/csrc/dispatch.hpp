@@ -72,6 +72,10 @@ struct DevCtx {
   const double* aff = nullptr;
   const double* qcell[kMaxRule] = {};
   const double* qface[kMaxRule] = {};
+  // compact per-qp geometry for the deformed fast kernels (fast_deformed.cuh):
+  // cell {detJw Jinv Jinv^T (xx, xy, xz, yy, yz, zz), detJw}; face {Jinv n (3), Jinv_nbr n (3), w ds}
+  const double* qcm[kMaxRule] = {};
+  const double* qfn[kMaxRule] = {};
   cudaStream_t stream = nullptr;
 };
 

@@ -308,8 +308,8 @@ static cudaError_t run_sip_qp(const DevCtx& c, double mc, int dir, const double*
   cudaError_t e = ensure_ftab<KP + 1, KP + 2>();
   if (e != cudaSuccess) return e;
   using G = SipQpCfg<KP>;
-  const double* gc = c.qcell[KP + 2];
-  const double* gf = c.qface[KP + 2];
+  const double* gc = c.qcm[KP + 2];
+  const double* gf = c.qfn[KP + 2];
   if (!gc || !gf) return cudaErrorNotSupported;
   if ((e = set_smem(k_sip_qp<KP>, G::SMEM)) != cudaSuccess) return e;
   const int grid = (c.ncells + G::C - 1) / G::C;

@@ -4,7 +4,10 @@
 // forms.cpp:148-243) with the per-quadrature-point geometry of the reference's
 // GeometryCache (cell: Jinv + detJ w per Gauss point; faces: Jinv of both sides,
 // unit normal, w ds per face point) streamed from HBM — SURVEY 8(d) counts this
-// path HBM-bound.  Same quadrature sums as the reference (rule kp+2), sum-factorised:
+// path HBM-bound.  The records are pre-contracted at setup to what the integrands
+// consume: the cell metric detJw Jinv Jinv^T (6) + detJw, and per face point
+// Jinv n, Jinv_nbr n (3 + 3) + w ds — 7 + 7 doubles instead of 10 + 22.
+// Same quadrature sums as the reference (rule kp+2), sum-factorised:
 //   cell: u and its reference gradient at the Q^3 points (x, y, z passes), the
 //         pointwise metric Jinv^T (.) detJ w Jinv, the transposed passes back;
 //   faces (element-centric, outward normal, all 6 at once): trace, tangential and
@@ -23,7 +26,7 @@ template <int KP>
 struct SipQpCfg {
   static constexpr int N = KP + 1, Q = KP + 2, NB = N * N * N, NF = N * N, NQ = Q * Q * Q, NQF = Q * Q;
   static constexpr int C = 4, T = 32 * C;
-  static constexpr int CS = 10, FS = 22;  // cell / face geometry record (doubles)
+  static constexpr int CS = 7, FS = 7;  // compact cell / face geometry records (DevCtx::qcm / qfn)
   // per cell: U | OUT | info (nb, type as doubles; pen) | work
   static constexpr int O_U = 0, O_OUT = NB, O_NB = 2 * NB, O_TY = O_NB + 6, O_PEN = O_TY + 6, O_WK = O_PEN + 6;
   // cell phase
@@ -148,15 +151,12 @@ __global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const do
         gr[0] = fma(t.B[qz][k], vx[k], gr[0]);
       }
       const double* geo = gcell + (size_t)(qx + Q * qy + Q * Q * qz) * G::CS;
-      double Ji[9];
-#pragma unroll
-      for (int i = 0; i < 9; ++i) Ji[i] = __ldg(geo + i);
-      const double jxw = __ldg(geo + 9);
-      double s[3], ra[3];
-#pragma unroll
-      for (int d = 0; d < 3; ++d) s[d] = (Ji[d] * gr[0] + Ji[3 + d] * gr[1] + Ji[6 + d] * gr[2]) * jxw;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) ra[a] = Ji[3 * a] * s[0] + Ji[3 * a + 1] * s[1] + Ji[3 * a + 2] * s[2];
+      const double g00 = __ldg(geo), g01 = __ldg(geo + 1), g02 = __ldg(geo + 2), g11 = __ldg(geo + 3),
+                   g12 = __ldg(geo + 4), g22 = __ldg(geo + 5), jxw = __ldg(geo + 6);
+      double ra[3];  // detJw Jinv Jinv^T (reference gradient)
+      ra[0] = g00 * gr[0] + g01 * gr[1] + g02 * gr[2];
+      ra[1] = g01 * gr[0] + g11 * gr[1] + g12 * gr[2];
+      ra[2] = g02 * gr[0] + g12 * gr[1] + g22 * gr[2];
       const double vi = mc * val * jxw;
 #pragma unroll
       for (int k = 0; k < N; ++k) {
@@ -296,32 +296,22 @@ __global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const do
           dnr_o = fma(t.B[qq][q], v[5][q], dnr_o);
         }
         const double* geo = gface + ((size_t)f * NQF + qp + Q * qq) * G::FS;
-        double Ji[9], nrm[3];
+        double jn[3];  // Jinv n: physical normal derivative = reference gradient . (Jinv n)
 #pragma unroll
-        for (int i = 0; i < 9; ++i) Ji[i] = __ldg(geo + i);
-#pragma unroll
-        for (int d = 0; d < 3; ++d) nrm[d] = __ldg(geo + 18 + d);
-        const double wds = __ldg(geo + 21);
+        for (int d = 0; d < 3; ++d) jn[d] = __ldg(geo + d);
+        const double wds = __ldg(geo + 6);
         double grs[3];
         grs[a] = dnr_s;
         grs[t1] = d1s;
         grs[t2] = d2s;
-        double dns = 0.0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) dns = fma(nrm[d], Ji[d] * grs[0] + Ji[3 + d] * grs[1] + Ji[6 + d] * grs[2], dns);
+        const double dns = jn[0] * grs[0] + jn[1] * grs[1] + jn[2] * grs[2];
         double F, ssym;
         if (nb >= 0) {
-          double Jo[9];
-#pragma unroll
-          for (int i = 0; i < 9; ++i) Jo[i] = __ldg(geo + 9 + i);
           double gro[3];
           gro[a] = dnr_o;
           gro[t1] = d1o;
           gro[t2] = d2o;
-          double dno = 0.0;
-#pragma unroll
-          for (int d = 0; d < 3; ++d)
-            dno = fma(nrm[d], Jo[d] * gro[0] + Jo[3 + d] * gro[1] + Jo[6 + d] * gro[2], dno);
+          const double dno = __ldg(geo + 3) * gro[0] + __ldg(geo + 4) * gro[1] + __ldg(geo + 5) * gro[2];
           const double ju = us - uo;
           F = (-0.5 * (dns + dno) + pen * ju) * wds;  // forms.cpp:199-209
           ssym = -0.5 * ju * wds;
@@ -332,8 +322,7 @@ __global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const do
         (void)ty;
         double rr[3];
 #pragma unroll
-        for (int aa = 0; aa < 3; ++aa)
-          rr[aa] = (Ji[3 * aa] * nrm[0] + Ji[3 * aa + 1] * nrm[1] + Ji[3 * aa + 2] * nrm[2]) * ssym;
+        for (int aa = 0; aa < 3; ++aa) rr[aa] = jn[aa] * ssym;
 #pragma unroll
         for (int b = 0; b < N; ++b) {
           A1[b] = fma(t.B[qq][b], F, fma(t.D[qq][b], rr[t2], A1[b]));
