@@ -22,13 +22,10 @@
 
 namespace dgb {
 
-template <int KP>
-struct SipQpCfg {
-  static constexpr int N = KP + 1, Q = KP + 2, NB = N * N * N, NF = N * N, NQ = Q * Q * Q, NQF = Q * Q;
-  static constexpr int C = 4, T = 32 * C;
-  static constexpr int CS = 7, FS = 7;  // compact cell / face geometry records (DevCtx::qcm / qfn)
-  // per cell: U | OUT | info (nb, type as doubles; pen) | work
-  static constexpr int O_U = 0, O_OUT = NB, O_NB = 2 * NB, O_TY = O_NB + 6, O_PEN = O_TY + 6, O_WK = O_PEN + 6;
+// work-area layout of one scalar SIP field on one cell (N nodes, Q Gauss points per direction)
+template <int N, int Q>
+struct QpSipWork {
+  static constexpr int NF = N * N;
   // cell phase
   static constexpr int XB = 0, XD = XB + Q * NF, YBB = XD + Q * NF, YDB = YBB + Q * Q * N, YBD = YDB + Q * Q * N,
                        PP = YBD + Q * Q * N, R0 = PP + Q * Q * N, R1 = R0 + Q * Q * N, P2 = R1 + Q * Q * N,
@@ -36,9 +33,7 @@ struct SipQpCfg {
   // face phase
   static constexpr int FL = 0, FP = FL + 6 * 4 * NF, FA = FP + 6 * 6 * N * Q, FON = FA + 6 * 3 * Q * N,
                        FACE_END = FON + 6 * 2 * NF;
-  static constexpr int WORK = CELL_END > FACE_END ? CELL_END : FACE_END;
-  static constexpr int PER = (O_WK + WORK) | 1;
-  static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
+  static constexpr int SIZE = CELL_END > FACE_END ? CELL_END : FACE_END;
 };
 
 // linear node index of (normal-axis position l, tangential (p, q)) on a face of axis a
@@ -47,14 +42,337 @@ __device__ __forceinline__ int face_node(int a, int l, int p, int q) {
   return a == 0 ? l + N * (p + N * q) : (a == 1 ? p + N * (l + N * q) : p + N * (q + N * l));
 }
 
+// One scalar field through the SIP operator on one cell (warp-cooperative, lane loops +
+// __syncwarp): OUT = mc M u + visc (K u + interior SIP faces + Dirichlet-type boundary
+// faces where bit f of bdir is set).  U: the cell's nodal values in shared memory; the
+// neighbours' values are read from xg[nb * nstride + noff + node].  Geometry: the
+// compact records of this cell (7 doubles per cell point / per face point).
+template <int N, int Q>
+__device__ __forceinline__ void qp_sip_field(const double* U, const double* __restrict__ xg, int nstride, int noff,
+                                             const double* nbv, const double* penv, int bdir, double mc, double visc,
+                                             const double* __restrict__ gcell, const double* __restrict__ gface,
+                                             double* W, double* OUT, int lane) {
+  using Wl = QpSipWork<N, Q>;
+  constexpr int NF = N * N, NQF = Q * Q;
+  const FTab<N, Q>& t = c_ft<N, Q>;
+  // ---- cell term
+  for (int jk = lane; jk < NF; jk += 32) {  // C1: x pass (values, x-derivative)
+    double u[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) u[i] = U[i + N * jk];
+#pragma unroll
+    for (int qx = 0; qx < Q; ++qx) {
+      double b = 0.0, d = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        b = fma(t.B[qx][i], u[i], b);
+        d = fma(t.D[qx][i], u[i], d);
+      }
+      W[Wl::XB + qx * NF + jk] = b;
+      W[Wl::XD + qx * NF + jk] = d;
+    }
+  }
+  __syncwarp();
+  for (int it = lane; it < Q * N; it += 32) {  // C2: y pass
+    const int qx = it / N, k = it - qx * N;
+    double vb[N], vd[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      vb[j] = W[Wl::XB + qx * NF + j + N * k];
+      vd[j] = W[Wl::XD + qx * NF + j + N * k];
+    }
+#pragma unroll
+    for (int qy = 0; qy < Q; ++qy) {
+      double bb = 0.0, db = 0.0, bd = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        bb = fma(t.B[qy][j], vb[j], bb);
+        db = fma(t.D[qy][j], vb[j], db);
+        bd = fma(t.B[qy][j], vd[j], bd);
+      }
+      const int o = (qx * Q + qy) * N + k;
+      W[Wl::YBB + o] = bb;
+      W[Wl::YDB + o] = db;
+      W[Wl::YBD + o] = bd;
+    }
+  }
+  __syncwarp();
+  for (int r = lane; r < Q * Q; r += 32) {  // C3: z pass, metric, z integration
+    const int qx = r / Q, qy = r - qx * Q;
+    double vb[N], vy[N], vx[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      vb[k] = W[Wl::YBB + r * N + k];
+      vy[k] = W[Wl::YDB + r * N + k];
+      vx[k] = W[Wl::YBD + r * N + k];
+    }
+    double pp[N], r0[N], r1[N];
+#pragma unroll
+    for (int k = 0; k < N; ++k) pp[k] = r0[k] = r1[k] = 0.0;
+#pragma unroll
+    for (int qz = 0; qz < Q; ++qz) {
+      double val = 0.0, gr[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        val = fma(t.B[qz][k], vb[k], val);
+        gr[2] = fma(t.D[qz][k], vb[k], gr[2]);
+        gr[1] = fma(t.B[qz][k], vy[k], gr[1]);
+        gr[0] = fma(t.B[qz][k], vx[k], gr[0]);
+      }
+      const double* geo = gcell + (size_t)(qx + Q * qy + Q * Q * qz) * 7;
+      const double g00 = __ldg(geo), g01 = __ldg(geo + 1), g02 = __ldg(geo + 2), g11 = __ldg(geo + 3),
+                   g12 = __ldg(geo + 4), g22 = __ldg(geo + 5), jxw = __ldg(geo + 6);
+      double ra[3];  // detJw Jinv Jinv^T (reference gradient)
+      ra[0] = g00 * gr[0] + g01 * gr[1] + g02 * gr[2];
+      ra[1] = g01 * gr[0] + g11 * gr[1] + g12 * gr[2];
+      ra[2] = g02 * gr[0] + g12 * gr[1] + g22 * gr[2];
+      const double vi = mc * val * jxw;
+      ra[0] *= visc;
+      ra[1] *= visc;
+      ra[2] *= visc;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        pp[k] = fma(t.B[qz][k], vi, fma(t.D[qz][k], ra[2], pp[k]));
+        r0[k] = fma(t.B[qz][k], ra[0], r0[k]);
+        r1[k] = fma(t.B[qz][k], ra[1], r1[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      W[Wl::PP + r * N + k] = pp[k];
+      W[Wl::R0 + r * N + k] = r0[k];
+      W[Wl::R1 + r * N + k] = r1[k];
+    }
+  }
+  __syncwarp();
+  for (int it = lane; it < Q * N; it += 32) {  // C4: y integration
+    const int qx = it / N, k = it - qx * N;
+    double p[Q], a0[Q], a1[Q];
+#pragma unroll
+    for (int qy = 0; qy < Q; ++qy) {
+      const int o = (qx * Q + qy) * N + k;
+      p[qy] = W[Wl::PP + o];
+      a0[qy] = W[Wl::R0 + o];
+      a1[qy] = W[Wl::R1 + o];
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double s = 0.0, u = 0.0;
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        s = fma(t.B[qy][j], p[qy], fma(t.D[qy][j], a1[qy], s));
+        u = fma(t.B[qy][j], a0[qy], u);
+      }
+      W[Wl::P2 + qx * NF + j + N * k] = s;
+      W[Wl::R02 + qx * NF + j + N * k] = u;
+    }
+  }
+  __syncwarp();
+  for (int jk = lane; jk < NF; jk += 32) {  // C5: x integration -> OUT
+    double p[Q], a0[Q];
+#pragma unroll
+    for (int qx = 0; qx < Q; ++qx) {
+      p[qx] = W[Wl::P2 + qx * NF + jk];
+      a0[qx] = W[Wl::R02 + qx * NF + jk];
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) s = fma(t.B[qx][i], p[qx], fma(t.D[qx][i], a0[qx], s));
+      OUT[i + N * jk] = s;
+    }
+  }
+  __syncwarp();
+
+  // ---- faces (all six at once)
+  for (int it = lane; it < 6 * NF; it += 32) {  // F1: traces and normal reference derivatives, both sides
+    const int f = it / NF, tn = it - f * NF;
+    const int a = f >> 1, s = f & 1, p = tn % N, q = tn / N;
+    const int nb = (int)nbv[f];
+    const int Ls = s ? N - 1 : 0, Lo = s ? 0 : N - 1;
+    double dns = 0.0, dno = 0.0, vo = 0.0;
+#pragma unroll
+    for (int l = 0; l < N; ++l) dns = fma(t.dE[s][l], U[face_node<N>(a, l, p, q)], dns);
+    if (nb >= 0) {
+      const double* xn = xg + (size_t)nb * nstride + noff;
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        const double v = __ldg(xn + face_node<N>(a, l, p, q));
+        dno = fma(t.dE[1 - s][l], v, dno);
+        if (l == Lo) vo = v;
+      }
+    }
+    double* fl = W + Wl::FL + f * 4 * NF;
+    fl[0 * NF + tn] = U[face_node<N>(a, Ls, p, q)];
+    fl[1 * NF + tn] = dns;
+    fl[2 * NF + tn] = vo;
+    fl[3 * NF + tn] = dno;
+  }
+  __syncwarp();
+  for (int it = lane; it < 6 * N; it += 32) {  // F2: along p (first tangential axis)
+    const int f = it / N, q = it - f * N;
+    const double* fl = W + Wl::FL + f * 4 * NF + N * q;
+    double v[4][N];
+#pragma unroll
+    for (int fld = 0; fld < 4; ++fld)
+#pragma unroll
+      for (int p = 0; p < N; ++p) v[fld][p] = fl[fld * NF + p];
+    double* fp = W + Wl::FP + f * 6 * N * Q + q * Q;
+#pragma unroll
+    for (int qp = 0; qp < Q; ++qp) {
+      double o[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        o[0] = fma(t.B[qp][p], v[0][p], o[0]);  // own value
+        o[1] = fma(t.D[qp][p], v[0][p], o[1]);  // own d/dt1
+        o[2] = fma(t.B[qp][p], v[1][p], o[2]);  // own d/dn
+        o[3] = fma(t.B[qp][p], v[2][p], o[3]);  // nbr value
+        o[4] = fma(t.D[qp][p], v[2][p], o[4]);  // nbr d/dt1
+        o[5] = fma(t.B[qp][p], v[3][p], o[5]);  // nbr d/dn
+      }
+#pragma unroll
+      for (int fld = 0; fld < 6; ++fld) fp[fld * N * Q + qp] = o[fld];
+    }
+  }
+  __syncwarp();
+  for (int it = lane; it < 6 * Q; it += 32) {  // F3: along q, SIP terms at the points, test integration along q
+    const int f = it / Q, qp = it - f * Q;
+    const int a = f >> 1;
+    const int t1 = a == 0 ? 1 : 0, t2 = a == 2 ? 1 : 2;
+    const int nb = (int)nbv[f];
+    const double pen = penv[f];
+    const bool act = nb >= 0 || ((bdir >> f) & 1);
+    const double* fp = W + Wl::FP + f * 6 * N * Q + qp;
+    double v[6][N];
+#pragma unroll
+    for (int fld = 0; fld < 6; ++fld)
+#pragma unroll
+      for (int q = 0; q < N; ++q) v[fld][q] = fp[fld * N * Q + q * Q];
+    double A1[N], A2[N], A3[N];
+#pragma unroll
+    for (int b = 0; b < N; ++b) A1[b] = A2[b] = A3[b] = 0.0;
+    if (act) {
+#pragma unroll
+      for (int qq = 0; qq < Q; ++qq) {
+        double us = 0.0, d1s = 0.0, d2s = 0.0, dnr_s = 0.0, uo = 0.0, d1o = 0.0, d2o = 0.0, dnr_o = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          us = fma(t.B[qq][q], v[0][q], us);
+          d1s = fma(t.B[qq][q], v[1][q], d1s);
+          d2s = fma(t.D[qq][q], v[0][q], d2s);
+          dnr_s = fma(t.B[qq][q], v[2][q], dnr_s);
+          uo = fma(t.B[qq][q], v[3][q], uo);
+          d1o = fma(t.B[qq][q], v[4][q], d1o);
+          d2o = fma(t.D[qq][q], v[3][q], d2o);
+          dnr_o = fma(t.B[qq][q], v[5][q], dnr_o);
+        }
+        const double* geo = gface + ((size_t)f * NQF + qp + Q * qq) * 7;
+        double jn[3];  // Jinv n: physical normal derivative = reference gradient . (Jinv n)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) jn[d] = __ldg(geo + d);
+        const double wds = __ldg(geo + 6);
+        double grs[3];
+        grs[a] = dnr_s;
+        grs[t1] = d1s;
+        grs[t2] = d2s;
+        const double dns = jn[0] * grs[0] + jn[1] * grs[1] + jn[2] * grs[2];
+        double F, ssym;
+        if (nb >= 0) {
+          double gro[3];
+          gro[a] = dnr_o;
+          gro[t1] = d1o;
+          gro[t2] = d2o;
+          const double dno = __ldg(geo + 3) * gro[0] + __ldg(geo + 4) * gro[1] + __ldg(geo + 5) * gro[2];
+          const double ju = us - uo;
+          F = visc * (-0.5 * (dns + dno) + pen * ju) * wds;  // forms.cpp:199-209 / 443-461
+          ssym = -0.5 * visc * ju * wds;
+        } else {  // Dirichlet-type boundary, forms.cpp:232-240
+          F = visc * (-dns + 2.0 * pen * us) * wds;
+          ssym = -visc * us * wds;
+        }
+        double rr[3];
+#pragma unroll
+        for (int aa = 0; aa < 3; ++aa) rr[aa] = jn[aa] * ssym;
+#pragma unroll
+        for (int b = 0; b < N; ++b) {
+          A1[b] = fma(t.B[qq][b], F, fma(t.D[qq][b], rr[t2], A1[b]));
+          A2[b] = fma(t.B[qq][b], rr[t1], A2[b]);
+          A3[b] = fma(t.B[qq][b], rr[a], A3[b]);
+        }
+      }
+    }
+    double* fa = W + Wl::FA + f * 3 * Q * N + qp * N;
+#pragma unroll
+    for (int b = 0; b < N; ++b) {
+      fa[b] = A1[b];
+      fa[Q * N + b] = A2[b];
+      fa[2 * Q * N + b] = A3[b];
+    }
+  }
+  __syncwarp();
+  for (int it = lane; it < 6 * N; it += 32) {  // F4: along p -> face-layer (value / tangential) and normal-test parts
+    const int f = it / N, bq = it - f * N;
+    const double* fa = W + Wl::FA + f * 3 * Q * N + bq;
+    double a1[Q], a2[Q], a3[Q];
+#pragma unroll
+    for (int qp = 0; qp < Q; ++qp) {
+      a1[qp] = fa[qp * N];
+      a2[qp] = fa[Q * N + qp * N];
+      a3[qp] = fa[2 * Q * N + qp * N];
+    }
+    double* fo = W + Wl::FON + f * 2 * NF;
+#pragma unroll
+    for (int bp = 0; bp < N; ++bp) {
+      double lo = 0.0, ln = 0.0;
+#pragma unroll
+      for (int qp = 0; qp < Q; ++qp) {
+        lo = fma(t.B[qp][bp], a1[qp], fma(t.D[qp][bp], a2[qp], lo));
+        ln = fma(t.B[qp][bp], a3[qp], ln);
+      }
+      fo[bp + N * bq] = lo;
+      fo[NF + bp + N * bq] = ln;
+    }
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int a = 0; a < 3; ++a) {  // F5: per axis, the two faces' contributions along each normal line
+    for (int tn = lane; tn < NF; tn += 32) {
+      const int p = tn % N, q = tn / N;
+      const double* f0 = W + Wl::FON + (2 * a) * 2 * NF;
+      const double* f1 = W + Wl::FON + (2 * a + 1) * 2 * NF;
+      const double n0 = f0[NF + tn], n1 = f1[NF + tn];
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        double v = t.dE[0][l] * n0 + t.dE[1][l] * n1;
+        if (l == 0) v += f0[tn];
+        if (l == N - 1) v += f1[tn];
+        OUT[face_node<N>(a, l, p, q)] += v;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+template <int KP>
+struct SipQpCfg {
+  static constexpr int N = KP + 1, Q = KP + 2, NB = N * N * N, NF = N * N, NQ = Q * Q * Q, NQF = Q * Q;
+  static constexpr int C = 4, T = 32 * C;
+  static constexpr int CS = 7, FS = 7;  // compact cell / face geometry records (DevCtx::qcm / qfn)
+  // per cell: U | OUT | info (nb, type as doubles; pen) | work
+  static constexpr int O_U = 0, O_OUT = NB, O_NB = 2 * NB, O_TY = O_NB + 6, O_PEN = O_TY + 6, O_WK = O_PEN + 6;
+  static constexpr int WORK = QpSipWork<N, Q>::SIZE;
+  static constexpr int PER = (O_WK + WORK) | 1;
+  static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
+};
+
 template <int KP>
 __global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const double* __restrict__ gc,
                                                              const double* __restrict__ gf, double mc, int dir_bdry,
                                                              const double* __restrict__ x, double* __restrict__ y) {
   if (m.skip && *m.skip) return;
   using G = SipQpCfg<KP>;
-  constexpr int N = G::N, Q = G::Q, NB = G::NB, NF = G::NF, NQ = G::NQ, NQF = G::NQF, C = G::C, PER = G::PER;
-  const FTab<N, Q>& t = c_ft<N, Q>;
+  constexpr int N = G::N, Q = G::Q, NB = G::NB, NQ = G::NQ, NQF = G::NQF, C = G::C, PER = G::PER;
   extern __shared__ double sm[];
   const int c0 = blockIdx.x * C;
   const int nc = min(C, m.ncells - c0);
@@ -86,301 +404,8 @@ __global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const do
   const double* gcell = gc + (size_t)cid * NQ * G::CS;
   const double* gface = gf + (size_t)cid * 6 * NQF * G::FS;
 
-  // ---- cell term
-  for (int jk = lane; jk < NF; jk += 32) {  // C1: x pass (values, x-derivative)
-    double u[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) u[i] = U[i + N * jk];
-#pragma unroll
-    for (int qx = 0; qx < Q; ++qx) {
-      double b = 0.0, d = 0.0;
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        b = fma(t.B[qx][i], u[i], b);
-        d = fma(t.D[qx][i], u[i], d);
-      }
-      W[G::XB + qx * NF + jk] = b;
-      W[G::XD + qx * NF + jk] = d;
-    }
-  }
-  __syncwarp();
-  for (int it = lane; it < Q * N; it += 32) {  // C2: y pass
-    const int qx = it / N, k = it - qx * N;
-    double vb[N], vd[N];
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-      vb[j] = W[G::XB + qx * NF + j + N * k];
-      vd[j] = W[G::XD + qx * NF + j + N * k];
-    }
-#pragma unroll
-    for (int qy = 0; qy < Q; ++qy) {
-      double bb = 0.0, db = 0.0, bd = 0.0;
-#pragma unroll
-      for (int j = 0; j < N; ++j) {
-        bb = fma(t.B[qy][j], vb[j], bb);
-        db = fma(t.D[qy][j], vb[j], db);
-        bd = fma(t.B[qy][j], vd[j], bd);
-      }
-      const int o = (qx * Q + qy) * N + k;
-      W[G::YBB + o] = bb;
-      W[G::YDB + o] = db;
-      W[G::YBD + o] = bd;
-    }
-  }
-  __syncwarp();
-  for (int r = lane; r < Q * Q; r += 32) {  // C3: z pass, metric, z integration
-    const int qx = r / Q, qy = r - qx * Q;
-    double vb[N], vy[N], vx[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      vb[k] = W[G::YBB + r * N + k];
-      vy[k] = W[G::YDB + r * N + k];
-      vx[k] = W[G::YBD + r * N + k];
-    }
-    double pp[N], r0[N], r1[N];
-#pragma unroll
-    for (int k = 0; k < N; ++k) pp[k] = r0[k] = r1[k] = 0.0;
-#pragma unroll
-    for (int qz = 0; qz < Q; ++qz) {
-      double val = 0.0, gr[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        val = fma(t.B[qz][k], vb[k], val);
-        gr[2] = fma(t.D[qz][k], vb[k], gr[2]);
-        gr[1] = fma(t.B[qz][k], vy[k], gr[1]);
-        gr[0] = fma(t.B[qz][k], vx[k], gr[0]);
-      }
-      const double* geo = gcell + (size_t)(qx + Q * qy + Q * Q * qz) * G::CS;
-      const double g00 = __ldg(geo), g01 = __ldg(geo + 1), g02 = __ldg(geo + 2), g11 = __ldg(geo + 3),
-                   g12 = __ldg(geo + 4), g22 = __ldg(geo + 5), jxw = __ldg(geo + 6);
-      double ra[3];  // detJw Jinv Jinv^T (reference gradient)
-      ra[0] = g00 * gr[0] + g01 * gr[1] + g02 * gr[2];
-      ra[1] = g01 * gr[0] + g11 * gr[1] + g12 * gr[2];
-      ra[2] = g02 * gr[0] + g12 * gr[1] + g22 * gr[2];
-      const double vi = mc * val * jxw;
-#pragma unroll
-      for (int k = 0; k < N; ++k) {
-        pp[k] = fma(t.B[qz][k], vi, fma(t.D[qz][k], ra[2], pp[k]));
-        r0[k] = fma(t.B[qz][k], ra[0], r0[k]);
-        r1[k] = fma(t.B[qz][k], ra[1], r1[k]);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < N; ++k) {
-      W[G::PP + r * N + k] = pp[k];
-      W[G::R0 + r * N + k] = r0[k];
-      W[G::R1 + r * N + k] = r1[k];
-    }
-  }
-  __syncwarp();
-  for (int it = lane; it < Q * N; it += 32) {  // C4: y integration
-    const int qx = it / N, k = it - qx * N;
-    double p[Q], a0[Q], a1[Q];
-#pragma unroll
-    for (int qy = 0; qy < Q; ++qy) {
-      const int o = (qx * Q + qy) * N + k;
-      p[qy] = W[G::PP + o];
-      a0[qy] = W[G::R0 + o];
-      a1[qy] = W[G::R1 + o];
-    }
-#pragma unroll
-    for (int j = 0; j < N; ++j) {
-      double s = 0.0, u = 0.0;
-#pragma unroll
-      for (int qy = 0; qy < Q; ++qy) {
-        s = fma(t.B[qy][j], p[qy], fma(t.D[qy][j], a1[qy], s));
-        u = fma(t.B[qy][j], a0[qy], u);
-      }
-      W[G::P2 + qx * NF + j + N * k] = s;
-      W[G::R02 + qx * NF + j + N * k] = u;
-    }
-  }
-  __syncwarp();
-  for (int jk = lane; jk < NF; jk += 32) {  // C5: x integration -> OUT
-    double p[Q], a0[Q];
-#pragma unroll
-    for (int qx = 0; qx < Q; ++qx) {
-      p[qx] = W[G::P2 + qx * NF + jk];
-      a0[qx] = W[G::R02 + qx * NF + jk];
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      double s = 0.0;
-#pragma unroll
-      for (int qx = 0; qx < Q; ++qx) s = fma(t.B[qx][i], p[qx], fma(t.D[qx][i], a0[qx], s));
-      OUT[i + N * jk] = s;
-    }
-  }
-  __syncwarp();
-
-  // ---- faces (all six at once)
-  for (int it = lane; it < 6 * NF; it += 32) {  // F1: traces and normal reference derivatives, both sides
-    const int f = it / NF, tn = it - f * NF;
-    const int a = f >> 1, s = f & 1, p = tn % N, q = tn / N;
-    const int nb = (int)cell[G::O_NB + f];
-    const int Ls = s ? N - 1 : 0, Lo = s ? 0 : N - 1;
-    double dns = 0.0, dno = 0.0, vo = 0.0;
-#pragma unroll
-    for (int l = 0; l < N; ++l) dns = fma(t.dE[s][l], U[face_node<N>(a, l, p, q)], dns);
-    if (nb >= 0) {
-      const double* xn = x + (size_t)nb * NB;
-#pragma unroll
-      for (int l = 0; l < N; ++l) {
-        const double v = __ldg(xn + face_node<N>(a, l, p, q));
-        dno = fma(t.dE[1 - s][l], v, dno);
-        if (l == Lo) vo = v;
-      }
-    }
-    double* fl = W + G::FL + f * 4 * NF;
-    fl[0 * NF + tn] = U[face_node<N>(a, Ls, p, q)];
-    fl[1 * NF + tn] = dns;
-    fl[2 * NF + tn] = vo;
-    fl[3 * NF + tn] = dno;
-  }
-  __syncwarp();
-  for (int it = lane; it < 6 * N; it += 32) {  // F2: along p (first tangential axis)
-    const int f = it / N, q = it - f * N;
-    const double* fl = W + G::FL + f * 4 * NF + N * q;
-    double v[4][N];
-#pragma unroll
-    for (int fld = 0; fld < 4; ++fld)
-#pragma unroll
-      for (int p = 0; p < N; ++p) v[fld][p] = fl[fld * NF + p];
-    double* fp = W + G::FP + f * 6 * N * Q + q * Q;
-#pragma unroll
-    for (int qp = 0; qp < Q; ++qp) {
-      double o[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int p = 0; p < N; ++p) {
-        o[0] = fma(t.B[qp][p], v[0][p], o[0]);  // own value
-        o[1] = fma(t.D[qp][p], v[0][p], o[1]);  // own d/dt1
-        o[2] = fma(t.B[qp][p], v[1][p], o[2]);  // own d/dn
-        o[3] = fma(t.B[qp][p], v[2][p], o[3]);  // nbr value
-        o[4] = fma(t.D[qp][p], v[2][p], o[4]);  // nbr d/dt1
-        o[5] = fma(t.B[qp][p], v[3][p], o[5]);  // nbr d/dn
-      }
-#pragma unroll
-      for (int fld = 0; fld < 6; ++fld) fp[fld * N * Q + qp] = o[fld];
-    }
-  }
-  __syncwarp();
-  for (int it = lane; it < 6 * Q; it += 32) {  // F3: along q, SIP terms at the points, test integration along q
-    const int f = it / Q, qp = it - f * Q;
-    const int a = f >> 1;
-    const int t1 = a == 0 ? 1 : 0, t2 = a == 2 ? 1 : 2;
-    const int nb = (int)cell[G::O_NB + f], ty = (int)cell[G::O_TY + f];
-    const double pen = cell[G::O_PEN + f];
-    const bool act = nb >= 0 || dir_bdry != 0;
-    const double* fp = W + G::FP + f * 6 * N * Q + qp;
-    double v[6][N];
-#pragma unroll
-    for (int fld = 0; fld < 6; ++fld)
-#pragma unroll
-      for (int q = 0; q < N; ++q) v[fld][q] = fp[fld * N * Q + q * Q];
-    double A1[N], A2[N], A3[N];
-#pragma unroll
-    for (int b = 0; b < N; ++b) A1[b] = A2[b] = A3[b] = 0.0;
-    if (act) {
-#pragma unroll
-      for (int qq = 0; qq < Q; ++qq) {
-        double us = 0.0, d1s = 0.0, d2s = 0.0, dnr_s = 0.0, uo = 0.0, d1o = 0.0, d2o = 0.0, dnr_o = 0.0;
-#pragma unroll
-        for (int q = 0; q < N; ++q) {
-          us = fma(t.B[qq][q], v[0][q], us);
-          d1s = fma(t.B[qq][q], v[1][q], d1s);
-          d2s = fma(t.D[qq][q], v[0][q], d2s);
-          dnr_s = fma(t.B[qq][q], v[2][q], dnr_s);
-          uo = fma(t.B[qq][q], v[3][q], uo);
-          d1o = fma(t.B[qq][q], v[4][q], d1o);
-          d2o = fma(t.D[qq][q], v[3][q], d2o);
-          dnr_o = fma(t.B[qq][q], v[5][q], dnr_o);
-        }
-        const double* geo = gface + ((size_t)f * NQF + qp + Q * qq) * G::FS;
-        double jn[3];  // Jinv n: physical normal derivative = reference gradient . (Jinv n)
-#pragma unroll
-        for (int d = 0; d < 3; ++d) jn[d] = __ldg(geo + d);
-        const double wds = __ldg(geo + 6);
-        double grs[3];
-        grs[a] = dnr_s;
-        grs[t1] = d1s;
-        grs[t2] = d2s;
-        const double dns = jn[0] * grs[0] + jn[1] * grs[1] + jn[2] * grs[2];
-        double F, ssym;
-        if (nb >= 0) {
-          double gro[3];
-          gro[a] = dnr_o;
-          gro[t1] = d1o;
-          gro[t2] = d2o;
-          const double dno = __ldg(geo + 3) * gro[0] + __ldg(geo + 4) * gro[1] + __ldg(geo + 5) * gro[2];
-          const double ju = us - uo;
-          F = (-0.5 * (dns + dno) + pen * ju) * wds;  // forms.cpp:199-209
-          ssym = -0.5 * ju * wds;
-        } else {  // Dirichlet-type boundary, forms.cpp:232-240
-          F = (-dns + 2.0 * pen * us) * wds;
-          ssym = -us * wds;
-        }
-        (void)ty;
-        double rr[3];
-#pragma unroll
-        for (int aa = 0; aa < 3; ++aa) rr[aa] = jn[aa] * ssym;
-#pragma unroll
-        for (int b = 0; b < N; ++b) {
-          A1[b] = fma(t.B[qq][b], F, fma(t.D[qq][b], rr[t2], A1[b]));
-          A2[b] = fma(t.B[qq][b], rr[t1], A2[b]);
-          A3[b] = fma(t.B[qq][b], rr[a], A3[b]);
-        }
-      }
-    }
-    double* fa = W + G::FA + f * 3 * Q * N + qp * N;
-#pragma unroll
-    for (int b = 0; b < N; ++b) {
-      fa[b] = A1[b];
-      fa[Q * N + b] = A2[b];
-      fa[2 * Q * N + b] = A3[b];
-    }
-  }
-  __syncwarp();
-  for (int it = lane; it < 6 * N; it += 32) {  // F4: along p -> face-layer (value / tangential) and normal-test parts
-    const int f = it / N, bq = it - f * N;
-    const double* fa = W + G::FA + f * 3 * Q * N + bq;
-    double a1[Q], a2[Q], a3[Q];
-#pragma unroll
-    for (int qp = 0; qp < Q; ++qp) {
-      a1[qp] = fa[qp * N];
-      a2[qp] = fa[Q * N + qp * N];
-      a3[qp] = fa[2 * Q * N + qp * N];
-    }
-    double* fo = W + G::FON + f * 2 * NF;
-#pragma unroll
-    for (int bp = 0; bp < N; ++bp) {
-      double lo = 0.0, ln = 0.0;
-#pragma unroll
-      for (int qp = 0; qp < Q; ++qp) {
-        lo = fma(t.B[qp][bp], a1[qp], fma(t.D[qp][bp], a2[qp], lo));
-        ln = fma(t.B[qp][bp], a3[qp], ln);
-      }
-      fo[bp + N * bq] = lo;
-      fo[NF + bp + N * bq] = ln;
-    }
-  }
-  __syncwarp();
-#pragma unroll 1
-  for (int a = 0; a < 3; ++a) {  // F5: per axis, the two faces' contributions along each normal line
-    for (int tn = lane; tn < NF; tn += 32) {
-      const int p = tn % N, q = tn / N;
-      const double* f0 = W + G::FON + (2 * a) * 2 * NF;
-      const double* f1 = W + G::FON + (2 * a + 1) * 2 * NF;
-      const double n0 = f0[NF + tn], n1 = f1[NF + tn];
-#pragma unroll
-      for (int l = 0; l < N; ++l) {
-        double v = t.dE[0][l] * n0 + t.dE[1][l] * n1;
-        if (l == 0) v += f0[tn];
-        if (l == N - 1) v += f1[tn];
-        OUT[face_node<N>(a, l, p, q)] += v;
-      }
-    }
-    __syncwarp();
-  }
+  const int bdir = dir_bdry ? 0x3f : 0;  // the scalar operator: all boundary faces Dirichlet or all natural
+  qp_sip_field<N, Q>(U, x, NB, 0, cell + G::O_NB, cell + G::O_PEN, bdir, mc, 1.0, gcell, gface, W, OUT, lane);
   for (int i = lane; i < NB; i += 32) y[(size_t)cid * NB + i] = OUT[i];
 }
 
