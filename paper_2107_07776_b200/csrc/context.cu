@@ -243,6 +243,31 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
         cudaMemcpy(dfn, fn.data(), fn.size() * sizeof(double), cudaMemcpyHostToDevice);
         dc.qcm[Q] = dcm;
         dc.qfn[Q] = dfn;
+        if (Q == ku + 2) {  // advection records of the deformed momentum kernel (SoA per cell)
+          const int nq = Q * Q * Q, nqf = Q * Q;
+          std::vector<double> ga((size_t)mesh.ncells * 9 * nq), gw((size_t)mesh.ncells * 18 * nqf);
+          for (int c = 0; c < mesh.ncells; ++c) {
+            for (int q = 0; q < nq; ++q) {
+              const double* r = &g.cell[((size_t)c * nq + q) * 10];
+              for (int i = 0; i < 9; ++i) ga[((size_t)c * 9 + i) * nq + q] = r[9] * r[i];
+            }
+            for (int f = 0; f < 6; ++f)
+              for (int t = 0; t < nqf; ++t) {
+                const double* r = &g.face[(((size_t)c * 6 + f) * nqf + t) * 22];
+                for (int d = 0; d < 3; ++d) gw[(((size_t)c * 6 + f) * 3 + d) * nqf + t] = r[18 + d] * r[21];
+              }
+          }
+          double* dga = (double*)dalloc(ga.size() * sizeof(double));
+          double* dgw = (double*)dalloc(gw.size() * sizeof(double));
+          if (!dga || !dgw) {
+            e = "out of device memory (qp geometry)";
+            return DGB_E_CUDA;
+          }
+          cudaMemcpy(dga, ga.data(), ga.size() * sizeof(double), cudaMemcpyHostToDevice);
+          cudaMemcpy(dgw, gw.data(), gw.size() * sizeof(double), cudaMemcpyHostToDevice);
+          dc.qadv[Q] = dga;
+          dc.qfw[Q] = dgw;
+        }
       }
     }
   }
@@ -290,12 +315,13 @@ int Context::momentum(const double* coefs, const double* w, const double* x, dou
   const MomCoef co{coefs[0], coefs[1], coefs[2], coefs[3]};
   if ((co.adv != 0.0 || co.skew != 0.0) && !w) return fail(DGB_E_MISSING_FIELD, "apply_momentum: advecting field missing");
   ++launches;
-  if (use_fast && dc.axis) {
-    const cudaError_t e = fast_momentum3(dc, co, w, x, y);
+  if (use_fast && (dc.axis || !dc.affine)) {
+    const cudaError_t e = dc.axis ? fast_momentum3(dc, co, w, x, y) : fast_momentum3_qp(dc, co, w, x, y);
     if (e != cudaErrorNotSupported) {
       CK(e);
       return DGB_OK;
     }
+    cudaGetLastError();
   }
   CK(opu->momentum(dc, co, w, x, y));
   return DGB_OK;

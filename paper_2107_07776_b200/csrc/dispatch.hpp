@@ -76,6 +76,10 @@ struct DevCtx {
   // cell {detJw Jinv Jinv^T (xx, xy, xz, yy, yz, zz), detJw}; face {Jinv n (3), Jinv_nbr n (3), w ds}
   const double* qcm[kMaxRule] = {};
   const double* qfn[kMaxRule] = {};
+  // pass-B (advection) records of the deformed momentum kernel, per cell SoA:
+  // detJ w Jinv [9][Q^3] and n ds w [6 faces][3][Q^2] (rule k_u+2 only)
+  const double* qadv[kMaxRule] = {};
+  const double* qfw[kMaxRule] = {};
   cudaStream_t stream = nullptr;
 };
 
@@ -98,6 +102,7 @@ cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, doub
 // deformed (per-qp geometry) 3D meshes (fast_deformed.cuh)
 cudaError_t fast_sip3_qp(const DevCtx& c, double mc, int dir, const double* x, double* y);
 cudaError_t fast_momentum3(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);
+cudaError_t fast_momentum3_qp(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);
 cudaError_t fast_momentum_diag3(const DevCtx& c, MomCoef co, const double* w, double* y);
 cudaError_t fast_divergence3(const DevCtx& c, const double* u, double* y);
 cudaError_t fast_sip_diag3(const DevCtx& c, double mc, int dir, double* y);

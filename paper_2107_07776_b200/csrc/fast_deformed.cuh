@@ -409,4 +409,425 @@ __global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const do
   for (int i = lane; i < NB; i += 32) y[(size_t)cid * NB + i] = OUT[i];
 }
 
+// ===========================================================================
+// Momentum operator on deformed hexahedra (apply_momentum, forms.cpp:389-604)
+// ===========================================================================
+// Pass A (rule k+1, mass + SIP viscous) per component through qp_sip_field with the
+// compact records of rule k+1.  Pass B (rule k+2, Lax-Friedrichs advection) needs the
+// advecting field only through component-independent pointwise factors, computed once
+// per cell before the component loop:
+//   cell:  Wt_a(q) = -adv sum_d (detJ w Jinv)[a][d] w_d(q)   (the reference's
+//          to_ref(Ji, -adv u w jxw) with u factored out, forms.cpp:509-530)
+//   faces: flux = a_s u_s + a_o u_o with a_s = adv/2 (w_s.n + lam) ds w,
+//          a_o = adv/2 (w_o.n - lam) ds w, lam = max(|w_s.n|, |w_o.n|) (forms.cpp:555-573);
+//          boundary a_s = adv |w.n| ds w (outlet: adv w.n ds w), a_o = 0 (forms.cpp:592-599).
+// Streamed pass-B geometry (DevCtx::qadv / qfw, rule k+2, per cell SoA): detJ w Jinv
+// [9][Q^3] and n ds w [6][3][Q^2].
+template <int K>
+struct MomQpCfg {
+  static constexpr int N = K + 1, QA = K + 1, QB = K + 2, NB = N * N * N, NF = N * N;
+  static constexpr int NQB = QB * QB * QB, NQFB = QB * QB, NQA = QA * QA * QA, NQFA = QA * QA;
+  static constexpr int WSIP = QpSipWork<N, QA>::SIZE;
+  // pass-B work areas (offsets inside WORK)
+  static constexpr int BX = 0, BY = BX + QB * NF, BA = BY + QB * QB * N, B_CELL_END = BA + 3 * QB * QB * N;
+  static constexpr int X0 = 0, X12 = X0 + QB * NF;  // y-integrated (reuse BX / BY)
+  static constexpr int FPB = 0, FAB = FPB + 6 * 2 * N * QB, FOB = FAB + 6 * QB * N, B_FACE_END = FOB + 6 * NF;
+  static constexpr int FPW = 0, W_END_F = FPW + 6 * 2 * 3 * N * QB, W_END_C = BY + QB * QB * N;
+  static constexpr int W_END = W_END_F > W_END_C ? W_END_F : W_END_C;
+  static constexpr int mx(int a, int b) { return a > b ? a : b; }
+  static constexpr int WORK = mx(mx(WSIP, B_CELL_END), mx(B_FACE_END, W_END + 3 * NB));
+  static constexpr int O_WS = WORK - 3 * NB;  // advecting field staged at the tail of WORK
+  // per cell: X (3 comps) | OUT | nb | type | pen | WT | FC | WORK
+  static constexpr int O_X = 0, O_OUT = 3 * NB, O_NB = O_OUT + NB, O_TY = O_NB + 6, O_PEN = O_TY + 6,
+                       O_WT = O_PEN + 6, O_FC = O_WT + 3 * NQB, O_WK = O_FC + 2 * 6 * NQFB;
+  static constexpr int PER = (O_WK + WORK) | 1;
+  static constexpr int C_FIT = (227 * 1024 / 8) / PER;
+  static constexpr int C = C_FIT > 8 ? 8 : C_FIT, T = 32 * C;
+  static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
+};
+
+template <int K>
+__global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, const double* __restrict__ gcA,
+                                                                const double* __restrict__ gfA,
+                                                                const double* __restrict__ gadv,
+                                                                const double* __restrict__ gfw, MomCoef co,
+                                                                const double* __restrict__ x,
+                                                                const double* __restrict__ w, double* __restrict__ y) {
+  if (m.skip && *m.skip) return;
+  using G = MomQpCfg<K>;
+  constexpr int N = G::N, QA = G::QA, QB = G::QB, NB = G::NB, NF = G::NF, NQB = G::NQB, NQFB = G::NQFB;
+  constexpr int C = G::C, PER = G::PER;
+  extern __shared__ double sm[];
+  const int c0 = blockIdx.x * C;
+  const int nc = min(C, m.ncells - c0);
+  const int tid = threadIdx.x, lane = tid & 31, wc = tid >> 5;
+  const bool passA = co.mass != 0.0 || co.visc != 0.0;
+  const bool passB = co.adv != 0.0;
+  const double sfac = (double)(N * N);  // sip_sigma (deg+1)^2, forms.hpp:175
+  // ---- staging (CTA-wide): the cells' x (all components) and w, neighbours, face types, penalties
+  for (int idx = tid; idx < nc * 3 * NB; idx += G::T) {
+    const int c = idx / (3 * NB), i = idx - c * 3 * NB;
+    cp_async8(sm + c * PER + G::O_X + i, x + (size_t)c0 * 3 * NB + idx);
+    if (passB) cp_async8(sm + c * PER + G::O_WK + G::O_WS + i, w + (size_t)c0 * 3 * NB + idx);
+  }
+  for (int idx = tid; idx < nc * 6; idx += G::T) {
+    const int c = idx / 6, f = idx - c * 6;
+    double* cell = sm + c * PER;
+    const int nb = m.nbr[(size_t)(c0 + c) * 6 + f];
+    int ty = 0;  // 0 interior, 1 Dirichlet wall, 2 outlet
+    if (nb < 0) {
+      const int bid = -1 - nb;
+      ty = (bid >= 0 && bid < 64 && m.bctype[bid] == 1) ? 2 : 1;
+    }
+    cell[G::O_NB + f] = (double)nb;
+    cell[G::O_TY + f] = (double)ty;
+    cell[G::O_PEN + f] = sfac * m.pen[(size_t)(c0 + c) * 6 + f];
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (wc >= nc) return;
+  const int cid = c0 + wc;
+  double* cell = sm + wc * PER;
+  double* OUT = cell + G::O_OUT;
+  double* WT = cell + G::O_WT;
+  double* FC = cell + G::O_FC;
+  double* W = cell + G::O_WK;
+  const double* nbv = cell + G::O_NB;
+  const double* tyv = cell + G::O_TY;
+  const FTab<N, QB>& tb = c_ft<N, QB>;
+  int bdir = 0;  // viscous Dirichlet faces (outlets skip the viscous boundary terms, forms.cpp:469-493)
+#pragma unroll
+  for (int f = 0; f < 6; ++f) bdir |= ((int)tyv[f] == 1) << f;
+
+  if (passB) {
+    // ---- W1: advecting field at the rule-B points -> Wt (component-independent)
+    const double* WS = W + G::O_WS;
+#pragma unroll 1
+    for (int d = 0; d < 3; ++d) {
+      const double* Wd = WS + d * NB;
+      for (int jk = lane; jk < NF; jk += 32) {
+        double u[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) u[i] = Wd[i + N * jk];
+#pragma unroll
+        for (int qx = 0; qx < QB; ++qx) {
+          double b = 0.0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) b = fma(tb.B[qx][i], u[i], b);
+          W[G::BX + qx * NF + jk] = b;
+        }
+      }
+      __syncwarp();
+      for (int it = lane; it < QB * N; it += 32) {
+        const int qx = it / N, k = it - qx * N;
+        double v[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[j] = W[G::BX + qx * NF + j + N * k];
+#pragma unroll
+        for (int qy = 0; qy < QB; ++qy) {
+          double b = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) b = fma(tb.B[qy][j], v[j], b);
+          W[G::BY + (qx * QB + qy) * N + k] = b;
+        }
+      }
+      __syncwarp();
+      for (int r = lane; r < QB * QB; r += 32) {
+        const int qx = r / QB, qy = r - qx * QB;
+        double v[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = W[G::BY + r * N + k];
+#pragma unroll
+        for (int qz = 0; qz < QB; ++qz) {
+          double b = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) b = fma(tb.B[qz][k], v[k], b);
+          WT[d * NQB + qx + QB * qy + QB * QB * qz] = b;
+        }
+      }
+      __syncwarp();
+    }
+    {
+      const double* g = gadv + (size_t)cid * 9 * NQB;
+      for (int q = lane; q < NQB; q += 32) {
+        const double w0 = WT[q], w1 = WT[NQB + q], w2 = WT[2 * NQB + q];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double t = __ldg(g + (a * 3 + 0) * NQB + q) * w0 + __ldg(g + (a * 3 + 1) * NQB + q) * w1 +
+                           __ldg(g + (a * 3 + 2) * NQB + q) * w2;
+          WT[a * NQB + q] = -co.adv * t;
+        }
+      }
+    }
+    // ---- W2: face factors a_s, a_o at the rule-B face points
+    for (int it = lane; it < 6 * 2 * N; it += 32) {
+      const int f = it / (2 * N), rem = it - f * 2 * N, side = rem / N, q = rem - side * N;
+      const int a = f >> 1, s = f & 1;
+      const int nb = (int)nbv[f];
+      double* fp = W + G::FPW + (f * 2 + side) * 3 * N * QB + q * QB;
+#pragma unroll 1
+      for (int d = 0; d < 3; ++d) {
+        double v[N];
+        if (side == 0) {
+#pragma unroll
+          for (int p = 0; p < N; ++p) v[p] = WS[d * NB + face_node<N>(a, s ? N - 1 : 0, p, q)];
+        } else if (nb >= 0) {
+          const double* wn = w + (size_t)nb * 3 * NB + d * NB;
+#pragma unroll
+          for (int p = 0; p < N; ++p) v[p] = __ldg(wn + face_node<N>(a, s ? 0 : N - 1, p, q));
+        } else {
+#pragma unroll
+          for (int p = 0; p < N; ++p) v[p] = 0.0;
+        }
+#pragma unroll
+        for (int qp = 0; qp < QB; ++qp) {
+          double b = 0.0;
+#pragma unroll
+          for (int p = 0; p < N; ++p) b = fma(tb.B[qp][p], v[p], b);
+          fp[d * N * QB + qp] = b;
+        }
+      }
+    }
+    __syncwarp();
+    for (int it = lane; it < 6 * QB; it += 32) {
+      const int f = it / QB, qp = it - f * QB;
+      const int ty = (int)tyv[f];
+      const double* nw = gfw + ((size_t)cid * 6 + f) * 3 * NQFB;
+      double vs[3][N], vo[3][N];
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          vs[d][q] = W[G::FPW + (f * 2 + 0) * 3 * N * QB + d * N * QB + q * QB + qp];
+          vo[d][q] = W[G::FPW + (f * 2 + 1) * 3 * N * QB + d * N * QB + q * QB + qp];
+        }
+#pragma unroll
+      for (int qq = 0; qq < QB; ++qq) {
+        const int t = qp + QB * qq;
+        double wns = 0.0, wno = 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          double ws = 0.0, wo = 0.0;
+#pragma unroll
+          for (int q = 0; q < N; ++q) {
+            ws = fma(tb.B[qq][q], vs[d][q], ws);
+            wo = fma(tb.B[qq][q], vo[d][q], wo);
+          }
+          const double nd = __ldg(nw + d * NQFB + t);
+          wns = fma(ws, nd, wns);
+          wno = fma(wo, nd, wno);
+        }
+        double as, ao;
+        if (ty == 0) {
+          const double lam = fmax(fabs(wns), fabs(wno));
+          as = 0.5 * co.adv * (wns + lam);
+          ao = 0.5 * co.adv * (wno - lam);
+        } else {
+          as = co.adv * (ty == 2 ? wns : fabs(wns));
+          ao = 0.0;
+        }
+        FC[f * NQFB + t] = as;
+        FC[6 * NQFB + f * NQFB + t] = ao;
+      }
+    }
+    __syncwarp();
+  }
+
+#pragma unroll 1
+  for (int comp = 0; comp < 3; ++comp) {
+    const double* U = cell + G::O_X + comp * NB;
+    // ---- pass A: mass + SIP viscous at rule k+1
+    if (passA) {
+      qp_sip_field<N, QA>(U, x, 3 * NB, comp * NB, nbv, cell + G::O_PEN, bdir, co.mass, co.visc,
+                          gcA + (size_t)cid * G::NQA * 7, gfA + (size_t)cid * 6 * G::NQFA * 7, W, OUT, lane);
+    } else {
+      for (int i = lane; i < NB; i += 32) OUT[i] = 0.0;
+      __syncwarp();
+    }
+    if (passB) {
+      // ---- pass B cell: u at the rule-B points, times Wt, integrated against the reference gradient tests
+      for (int jk = lane; jk < NF; jk += 32) {
+        double u[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) u[i] = U[i + N * jk];
+#pragma unroll
+        for (int qx = 0; qx < QB; ++qx) {
+          double b = 0.0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) b = fma(tb.B[qx][i], u[i], b);
+          W[G::BX + qx * NF + jk] = b;
+        }
+      }
+      __syncwarp();
+      for (int it = lane; it < QB * N; it += 32) {
+        const int qx = it / N, k = it - qx * N;
+        double v[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[j] = W[G::BX + qx * NF + j + N * k];
+#pragma unroll
+        for (int qy = 0; qy < QB; ++qy) {
+          double b = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) b = fma(tb.B[qy][j], v[j], b);
+          W[G::BY + (qx * QB + qy) * N + k] = b;
+        }
+      }
+      __syncwarp();
+      for (int r = lane; r < QB * QB; r += 32) {
+        const int qx = r / QB, qy = r - qx * QB;
+        double v[N], a0[N], a1[N], a2[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          v[k] = W[G::BY + r * N + k];
+          a0[k] = a1[k] = a2[k] = 0.0;
+        }
+#pragma unroll
+        for (int qz = 0; qz < QB; ++qz) {
+          double val = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) val = fma(tb.B[qz][k], v[k], val);
+          const int pt = qx + QB * qy + QB * QB * qz;
+          const double r0 = val * WT[pt], r1 = val * WT[NQB + pt], r2 = val * WT[2 * NQB + pt];
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            a0[k] = fma(tb.B[qz][k], r0, a0[k]);
+            a1[k] = fma(tb.B[qz][k], r1, a1[k]);
+            a2[k] = fma(tb.D[qz][k], r2, a2[k]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          W[G::BA + r * N + k] = a0[k];
+          W[G::BA + QB * QB * N + r * N + k] = a1[k];
+          W[G::BA + 2 * QB * QB * N + r * N + k] = a2[k];
+        }
+      }
+      __syncwarp();
+      for (int it = lane; it < QB * N; it += 32) {
+        const int qx = it / N, k = it - qx * N;
+        double p0[QB], p1[QB], p2[QB];
+#pragma unroll
+        for (int qy = 0; qy < QB; ++qy) {
+          const int o = (qx * QB + qy) * N + k;
+          p0[qy] = W[G::BA + o];
+          p1[qy] = W[G::BA + QB * QB * N + o];
+          p2[qy] = W[G::BA + 2 * QB * QB * N + o];
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          double s0 = 0.0, s12 = 0.0;
+#pragma unroll
+          for (int qy = 0; qy < QB; ++qy) {
+            s0 = fma(tb.B[qy][j], p0[qy], s0);
+            s12 = fma(tb.D[qy][j], p1[qy], fma(tb.B[qy][j], p2[qy], s12));
+          }
+          W[G::X0 + qx * NF + j + N * k] = s0;
+          W[G::X12 + qx * NF + j + N * k] = s12;
+        }
+      }
+      __syncwarp();
+      for (int jk = lane; jk < NF; jk += 32) {
+        double p0[QB], p12[QB];
+#pragma unroll
+        for (int qx = 0; qx < QB; ++qx) {
+          p0[qx] = W[G::X0 + qx * NF + jk];
+          p12[qx] = W[G::X12 + qx * NF + jk];
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double s = OUT[i + N * jk];
+#pragma unroll
+          for (int qx = 0; qx < QB; ++qx) s = fma(tb.D[qx][i], p0[qx], fma(tb.B[qx][i], p12[qx], s));
+          OUT[i + N * jk] = s;
+        }
+      }
+      __syncwarp();
+      // ---- pass B faces: Lax-Friedrichs flux at the rule-B face points, tested with the face-layer traces
+      for (int it = lane; it < 6 * 2 * N; it += 32) {
+        const int f = it / (2 * N), rem = it - f * 2 * N, side = rem / N, q = rem - side * N;
+        const int a = f >> 1, s = f & 1;
+        const int nb = (int)nbv[f];
+        double v[N];
+        if (side == 0) {
+#pragma unroll
+          for (int p = 0; p < N; ++p) v[p] = U[face_node<N>(a, s ? N - 1 : 0, p, q)];
+        } else if (nb >= 0) {
+          const double* xn = x + (size_t)nb * 3 * NB + comp * NB;
+#pragma unroll
+          for (int p = 0; p < N; ++p) v[p] = __ldg(xn + face_node<N>(a, s ? 0 : N - 1, p, q));
+        } else {
+#pragma unroll
+          for (int p = 0; p < N; ++p) v[p] = 0.0;
+        }
+        double* fp = W + G::FPB + ((f * 2 + side) * N + q) * QB;
+#pragma unroll
+        for (int qp = 0; qp < QB; ++qp) {
+          double b = 0.0;
+#pragma unroll
+          for (int p = 0; p < N; ++p) b = fma(tb.B[qp][p], v[p], b);
+          fp[qp] = b;
+        }
+      }
+      __syncwarp();
+      for (int it = lane; it < 6 * QB; it += 32) {
+        const int f = it / QB, qp = it - f * QB;
+        double vs[N], vo[N], A[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          vs[q] = W[G::FPB + ((f * 2 + 0) * N + q) * QB + qp];
+          vo[q] = W[G::FPB + ((f * 2 + 1) * N + q) * QB + qp];
+          A[q] = 0.0;
+        }
+#pragma unroll
+        for (int qq = 0; qq < QB; ++qq) {
+          double us = 0.0, uo = 0.0;
+#pragma unroll
+          for (int q = 0; q < N; ++q) {
+            us = fma(tb.B[qq][q], vs[q], us);
+            uo = fma(tb.B[qq][q], vo[q], uo);
+          }
+          const int t = qp + QB * qq;
+          const double fl = FC[f * NQFB + t] * us + FC[6 * NQFB + f * NQFB + t] * uo;
+#pragma unroll
+          for (int b = 0; b < N; ++b) A[b] = fma(tb.B[qq][b], fl, A[b]);
+        }
+#pragma unroll
+        for (int b = 0; b < N; ++b) W[G::FAB + (f * QB + qp) * N + b] = A[b];
+      }
+      __syncwarp();
+      for (int it = lane; it < 6 * N; it += 32) {
+        const int f = it / N, b = it - f * N;
+        double av[QB];
+#pragma unroll
+        for (int qp = 0; qp < QB; ++qp) av[qp] = W[G::FAB + (f * QB + qp) * N + b];
+#pragma unroll
+        for (int bp = 0; bp < N; ++bp) {
+          double s = 0.0;
+#pragma unroll
+          for (int qp = 0; qp < QB; ++qp) s = fma(tb.B[qp][bp], av[qp], s);
+          W[G::FOB + f * NF + bp + N * b] = s;
+        }
+      }
+      __syncwarp();
+    }
+    // ---- store (face-layer contributions of pass B added on the way out)
+    double* yc = y + ((size_t)cid * 3 + comp) * NB;
+    for (int n = lane; n < NB; n += 32) {
+      double v = OUT[n];
+      if (passB) {
+        const int i = n % N, j = (n / N) % N, k = n / NF;
+        const double* fo = W + G::FOB;
+        if (i == 0) v += fo[0 * NF + j + N * k];
+        if (i == N - 1) v += fo[1 * NF + j + N * k];
+        if (j == 0) v += fo[2 * NF + i + N * k];
+        if (j == N - 1) v += fo[3 * NF + i + N * k];
+        if (k == 0) v += fo[4 * NF + i + N * j];
+        if (k == N - 1) v += fo[5 * NF + i + N * j];
+      }
+      yc[n] = v;
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace dgb

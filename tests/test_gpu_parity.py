@@ -504,3 +504,26 @@ def test_deformed_sip_kernel_matches_reference_and_generic(ref, gpu, n_el, kp, a
             gpu.apply_scalar_laplace(D, dirichlet, dev(xp), yl)
             assert rel(host(yl), want) <= TOL_APPLY, (dirichlet, fast)
     D.set_fast_path(True)
+
+
+@pytest.mark.parametrize("n_el,ku,amp,outlet", [(3, 2, 0.05, None), (2, 3, 0.04, 1), (2, 4, 0.03, None),
+                                               (2, 4, 0.03, 4), (3, 1, 0.05, None)])
+@pytest.mark.parametrize("coefs", [(1.0 / (0.2929 * 1e-3), 0.005, 0.5, 0.0), (3.7, 1.3, 0.9, 0.0),
+                                   (2.1, 0.0, 0.7, 0.0), (0.0, 0.0, 1.1, 0.0), (1.9, 0.6, 0.0, 0.0)])
+def test_deformed_momentum_kernel_matches_reference_and_generic(ref, gpu, n_el, ku, amp, outlet, coefs):
+    """fast_deformed.cuh k_momentum_qp (pass A through the per-field SIP body at rule k+1,
+    Lax-Friedrichs advection at rule k+2 with per-qp geometry) vs the reference and the
+    generic device kernel on distorted 3D meshes, with walls / an outlet and every
+    combination of mass / viscous / advective coefficients."""
+    R, D = pair(ref, gpu, 3, n_el, ku, ku - 1 if ku > 1 else 1, amp, outlet=outlet)
+    assert not D.affine
+    w = gpu.seeded_uniform(41, R.n_u)
+    x = gpu.seeded_uniform(42, R.n_u)
+    want = R.momentum(coefs, w, x)
+    ctx = gpu.MomentumCtx(*coefs, advecting=dev(w))
+    for fast in (True, False):
+        D.set_fast_path(fast)
+        y = D.zeros()
+        gpu.apply_momentum(D, ctx, dev(x), y)
+        assert rel(host(y), want) <= TOL_APPLY, fast
+    D.set_fast_path(True)
