@@ -22,20 +22,31 @@
 
 namespace dgb {
 
-// work-area layout of one scalar SIP field on one cell (N nodes, Q Gauss points per direction)
+// work-area layout of one scalar SIP field on one cell (N nodes, Q Gauss points per direction).
+// Stages overwrite inputs they no longer need: C3 writes PP/R0/R1 in place of the
+// y-pass arrays it consumes (each lane owns its rows), C4 writes P2/R02 over the
+// x-pass arrays; F3 writes FA over FL, F4 writes FON over FP.
 template <int N, int Q>
 struct QpSipWork {
   static constexpr int NF = N * N;
   // cell phase
   static constexpr int XB = 0, XD = XB + Q * NF, YBB = XD + Q * NF, YDB = YBB + Q * Q * N, YBD = YDB + Q * Q * N,
-                       PP = YBD + Q * Q * N, R0 = PP + Q * Q * N, R1 = R0 + Q * Q * N, P2 = R1 + Q * Q * N,
-                       R02 = P2 + Q * NF, CELL_END = R02 + Q * NF;
+                       PP = YBB, R0 = YDB, R1 = YBD, P2 = XB, R02 = XD, CELL_END = YBD + Q * Q * N;
   // face phase
-  static constexpr int FL = 0, FP = FL + 6 * 4 * NF, FA = FP + 6 * 6 * N * Q, FON = FA + 6 * 3 * Q * N,
-                       FACE_END = FON + 6 * 2 * NF;
+  static constexpr int FL = 0, FP = FL + 6 * 4 * NF, FON = FP;
+  static constexpr int FA = 3 * Q <= 4 * N ? FL : FP + 6 * 6 * N * Q;  // over FL when it fits
+  static constexpr int FACE_END = FA + 6 * 3 * Q * N > FP + 6 * 6 * N * Q ? FA + 6 * 3 * Q * N : FP + 6 * 6 * N * Q;
   static constexpr int SIZE = CELL_END > FACE_END ? CELL_END : FACE_END;
 };
 
+// strides of a face of axis a: node = l * sl + p * sp + q * sq (l along the normal,
+// (p, q) the tangential axes in increasing order)
+template <int N>
+__device__ __forceinline__ void face_strides(int a, int& sl, int& sp, int& sq) {
+  sl = a == 0 ? 1 : (a == 1 ? N : N * N);
+  sp = a == 0 ? N : 1;
+  sq = a == 2 ? N : N * N;
+}
 // linear node index of (normal-axis position l, tangential (p, q)) on a face of axis a
 template <int N>
 __device__ __forceinline__ int face_node(int a, int l, int p, int q) {
@@ -189,22 +200,28 @@ __device__ __forceinline__ void qp_sip_field(const double* U, const double* __re
   for (int it = lane; it < 6 * NF; it += 32) {  // F1: traces and normal reference derivatives, both sides
     const int f = it / NF, tn = it - f * NF;
     const int a = f >> 1, s = f & 1, p = tn % N, q = tn / N;
+    int sl, sp, sq;
+    face_strides<N>(a, sl, sp, sq);
+    const int base = p * sp + q * sq;
     const int nb = (int)nbv[f];
-    const int Ls = s ? N - 1 : 0, Lo = s ? 0 : N - 1;
-    double dns = 0.0, dno = 0.0, vo = 0.0;
+    double dns = 0.0, dno = 0.0, vo = 0.0, vs = 0.0;
 #pragma unroll
-    for (int l = 0; l < N; ++l) dns = fma(t.dE[s][l], U[face_node<N>(a, l, p, q)], dns);
+    for (int l = 0; l < N; ++l) {
+      const double v = U[base + l * sl];
+      dns = fma(t.dE[s][l], v, dns);
+      if (l == (s ? N - 1 : 0)) vs = v;
+    }
     if (nb >= 0) {
-      const double* xn = xg + (size_t)nb * nstride + noff;
+      const double* xn = xg + (size_t)nb * nstride + noff + base;
 #pragma unroll
       for (int l = 0; l < N; ++l) {
-        const double v = __ldg(xn + face_node<N>(a, l, p, q));
+        const double v = __ldg(xn + l * sl);
         dno = fma(t.dE[1 - s][l], v, dno);
-        if (l == Lo) vo = v;
+        if (l == (s ? 0 : N - 1)) vo = v;
       }
     }
     double* fl = W + Wl::FL + f * 4 * NF;
-    fl[0 * NF + tn] = U[face_node<N>(a, Ls, p, q)];
+    fl[0 * NF + tn] = vs;
     fl[1 * NF + tn] = dns;
     fl[2 * NF + tn] = vo;
     fl[3 * NF + tn] = dno;
@@ -335,7 +352,7 @@ __device__ __forceinline__ void qp_sip_field(const double* U, const double* __re
     }
   }
   __syncwarp();
-#pragma unroll 1
+#pragma unroll
   for (int a = 0; a < 3; ++a) {  // F5: per axis, the two faces' contributions along each normal line
     for (int tn = lane; tn < NF; tn += 32) {
       const int p = tn % N, q = tn / N;
@@ -428,21 +445,25 @@ struct MomQpCfg {
   static constexpr int N = K + 1, QA = K + 1, QB = K + 2, NB = N * N * N, NF = N * N;
   static constexpr int NQB = QB * QB * QB, NQFB = QB * QB, NQA = QA * QA * QA, NQFA = QA * QA;
   static constexpr int WSIP = QpSipWork<N, QA>::SIZE;
-  // pass-B work areas (offsets inside WORK)
-  static constexpr int BX = 0, BY = BX + QB * NF, BA = BY + QB * QB * N, B_CELL_END = BA + 3 * QB * QB * N;
-  static constexpr int X0 = 0, X12 = X0 + QB * NF;  // y-integrated (reuse BX / BY)
+  // pass-B work areas (offsets inside WORK): x / y passes, z-integrated A0 (over BY), A1, A2;
+  // y-integrated X0 (over BX), X12
+  static constexpr int BX = 0, BY = BX + QB * NF, BA0 = BY, BA1 = BY + QB * QB * N, BA2 = BA1 + QB * QB * N,
+                       X0 = BX, X12 = BA2 + QB * QB * N, B_CELL_END = X12 + QB * NF;
   static constexpr int FPB = 0, FAB = FPB + 6 * 2 * N * QB, FOB = FAB + 6 * QB * N, B_FACE_END = FOB + 6 * NF;
   static constexpr int FPW = 0, W_END_F = FPW + 6 * 2 * 3 * N * QB, W_END_C = BY + QB * QB * N;
-  static constexpr int W_END = W_END_F > W_END_C ? W_END_F : W_END_C;
   static constexpr int mx(int a, int b) { return a > b ? a : b; }
-  static constexpr int WORK = mx(mx(WSIP, B_CELL_END), mx(B_FACE_END, W_END + 3 * NB));
-  static constexpr int O_WS = WORK - 3 * NB;  // advecting field staged at the tail of WORK
-  // per cell: X (3 comps) | OUT | nb | type | pen | WT | FC | WORK
+  static constexpr int WORK = mx(mx(WSIP, B_CELL_END), mx(B_FACE_END, mx(W_END_F, W_END_C)));
+  // per cell: X (3 comps) | OUT | nb | type | pen | WT | FC | WORK; the advecting field is
+  // staged in FC (free until the face factors are written, after its last read)
   static constexpr int O_X = 0, O_OUT = 3 * NB, O_NB = O_OUT + NB, O_TY = O_NB + 6, O_PEN = O_TY + 6,
-                       O_WT = O_PEN + 6, O_FC = O_WT + 3 * NQB, O_WK = O_FC + 2 * 6 * NQFB;
+                       O_WT = O_PEN + 6, O_FC = O_WT + 3 * NQB, O_WS = O_FC, O_WK = O_FC + 2 * 6 * NQFB;
+  static_assert(3 * NB <= 2 * 6 * NQFB, "advecting field must fit in FC");
   static constexpr int PER = (O_WK + WORK) | 1;
   static constexpr int C_FIT = (227 * 1024 / 8) / PER;
-  static constexpr int C = C_FIT > 8 ? 8 : C_FIT, T = 32 * C;
+#ifndef DGB_MQP_CMAX
+#define DGB_MQP_CMAX 8  // 8 warps: 2 per SM sub-partition at <= 256 registers
+#endif
+  static constexpr int C = C_FIT > DGB_MQP_CMAX ? DGB_MQP_CMAX : C_FIT, T = 32 * C;
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
 
@@ -468,7 +489,7 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
   for (int idx = tid; idx < nc * 3 * NB; idx += G::T) {
     const int c = idx / (3 * NB), i = idx - c * 3 * NB;
     cp_async8(sm + c * PER + G::O_X + i, x + (size_t)c0 * 3 * NB + idx);
-    if (passB) cp_async8(sm + c * PER + G::O_WK + G::O_WS + i, w + (size_t)c0 * 3 * NB + idx);
+    if (passB) cp_async8(sm + c * PER + G::O_WS + i, w + (size_t)c0 * 3 * NB + idx);
   }
   for (int idx = tid; idx < nc * 6; idx += G::T) {
     const int c = idx / 6, f = idx - c * 6;
@@ -501,7 +522,7 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
 
   if (passB) {
     // ---- W1: advecting field at the rule-B points -> Wt (component-independent)
-    const double* WS = W + G::O_WS;
+    const double* WS = cell + G::O_WS;
 #pragma unroll 1
     for (int d = 0; d < 3; ++d) {
       const double* Wd = WS + d * NB;
@@ -564,17 +585,20 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
       const int f = it / (2 * N), rem = it - f * 2 * N, side = rem / N, q = rem - side * N;
       const int a = f >> 1, s = f & 1;
       const int nb = (int)nbv[f];
+      int sl, sp, sq;
+      face_strides<N>(a, sl, sp, sq);
       double* fp = W + G::FPW + (f * 2 + side) * 3 * N * QB + q * QB;
 #pragma unroll 1
       for (int d = 0; d < 3; ++d) {
         double v[N];
         if (side == 0) {
+          const double* ws = WS + d * NB + (s ? N - 1 : 0) * sl + q * sq;
 #pragma unroll
-          for (int p = 0; p < N; ++p) v[p] = WS[d * NB + face_node<N>(a, s ? N - 1 : 0, p, q)];
+          for (int p = 0; p < N; ++p) v[p] = ws[p * sp];
         } else if (nb >= 0) {
-          const double* wn = w + (size_t)nb * 3 * NB + d * NB;
+          const double* wn = w + (size_t)nb * 3 * NB + d * NB + (s ? 0 : N - 1) * sl + q * sq;
 #pragma unroll
-          for (int p = 0; p < N; ++p) v[p] = __ldg(wn + face_node<N>(a, s ? 0 : N - 1, p, q));
+          for (int p = 0; p < N; ++p) v[p] = __ldg(wn + p * sp);
         } else {
 #pragma unroll
           for (int p = 0; p < N; ++p) v[p] = 0.0;
@@ -697,9 +721,9 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
         }
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-          W[G::BA + r * N + k] = a0[k];
-          W[G::BA + QB * QB * N + r * N + k] = a1[k];
-          W[G::BA + 2 * QB * QB * N + r * N + k] = a2[k];
+          W[G::BA0 + r * N + k] = a0[k];
+          W[G::BA1 + r * N + k] = a1[k];
+          W[G::BA2 + r * N + k] = a2[k];
         }
       }
       __syncwarp();
@@ -709,9 +733,9 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
 #pragma unroll
         for (int qy = 0; qy < QB; ++qy) {
           const int o = (qx * QB + qy) * N + k;
-          p0[qy] = W[G::BA + o];
-          p1[qy] = W[G::BA + QB * QB * N + o];
-          p2[qy] = W[G::BA + 2 * QB * QB * N + o];
+          p0[qy] = W[G::BA0 + o];
+          p1[qy] = W[G::BA1 + o];
+          p2[qy] = W[G::BA2 + o];
         }
 #pragma unroll
         for (int j = 0; j < N; ++j) {
@@ -747,14 +771,17 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
         const int f = it / (2 * N), rem = it - f * 2 * N, side = rem / N, q = rem - side * N;
         const int a = f >> 1, s = f & 1;
         const int nb = (int)nbv[f];
+        int sl, sp, sq;
+        face_strides<N>(a, sl, sp, sq);
         double v[N];
         if (side == 0) {
+          const double* us = U + (s ? N - 1 : 0) * sl + q * sq;
 #pragma unroll
-          for (int p = 0; p < N; ++p) v[p] = U[face_node<N>(a, s ? N - 1 : 0, p, q)];
+          for (int p = 0; p < N; ++p) v[p] = us[p * sp];
         } else if (nb >= 0) {
-          const double* xn = x + (size_t)nb * 3 * NB + comp * NB;
+          const double* xn = x + (size_t)nb * 3 * NB + comp * NB + (s ? 0 : N - 1) * sl + q * sq;
 #pragma unroll
-          for (int p = 0; p < N; ++p) v[p] = __ldg(xn + face_node<N>(a, s ? 0 : N - 1, p, q));
+          for (int p = 0; p < N; ++p) v[p] = __ldg(xn + p * sp);
         } else {
 #pragma unroll
           for (int p = 0; p < N; ++p) v[p] = 0.0;
