@@ -36,7 +36,10 @@ struct QpSipWork {
   static constexpr int FL = 0, FP = FL + 6 * 4 * NF, FON = FP;
   static constexpr int FA = 3 * Q <= 4 * N ? FL : FP + 6 * 6 * N * Q;  // over FL when it fits
   static constexpr int FACE_END = FA + 6 * 3 * Q * N > FP + 6 * 6 * N * Q ? FA + 6 * 3 * Q * N : FP + 6 * 6 * N * Q;
-  static constexpr int SIZE = CELL_END > FACE_END ? CELL_END : FACE_END;
+  // the six neighbour blocks (cp.async-staged by the caller, read in F1): after the cell
+  // phase's arrays, overwritten by F2 onwards
+  static constexpr int NBR = CELL_END, NBR_END = NBR + 6 * N * N * N;
+  static constexpr int SIZE = NBR_END > FACE_END ? NBR_END : FACE_END;
 };
 
 // strides of a face of axis a: node = l * sl + p * sp + q * sq (l along the normal,
@@ -53,13 +56,44 @@ __device__ __forceinline__ int face_node(int a, int l, int p, int q) {
   return a == 0 ? l + N * (p + N * q) : (a == 1 ? p + N * (l + N * q) : p + N * (q + N * l));
 }
 
+// Bulk prefetch of a byte range into L2 (cp.async.bulk.prefetch.L2; 16-byte granular,
+// clipped to [lo, hi) so it never reaches outside the array).  Issued for a cell's
+// geometry records when the cell is staged, so the per-point loads of the later
+// stages hit L2 instead of waiting on HBM.
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes, const void* lo, const void* hi) {
+  uintptr_t a = (uintptr_t)p, e = a + bytes;
+  const uintptr_t l = ((uintptr_t)lo + 15) & ~(uintptr_t)15, h = (uintptr_t)hi & ~(uintptr_t)15;
+  a = a & ~(uintptr_t)15;
+  e = (e + 15) & ~(uintptr_t)15;
+  if (a < l) a = l;
+  if (e > h) e = h;
+  if (e > a)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
+}
+
+// cp.async the six neighbour blocks of one field into NBR (warp-cooperative; faces
+// without a neighbour are skipped, F1 never reads them).  Completed by the
+// cp.async wait inside qp_sip_field, so the copies overlap its cell phase.
+template <int N>
+__device__ __forceinline__ void qp_stage_nbrs(double* NBR, const double* __restrict__ xg, int nstride, int noff,
+                                              const double* nbv, int lane) {
+  constexpr int NB = N * N * N;
+#pragma unroll
+  for (int f = 0; f < 6; ++f) {
+    const int nb = (int)nbv[f];
+    if (nb < 0) continue;
+    const double* src = xg + (size_t)nb * nstride + noff;
+    for (int n = lane; n < NB; n += 32) cp_async8(NBR + f * NB + n, src + n);
+  }
+}
+
 // One scalar field through the SIP operator on one cell (warp-cooperative, lane loops +
 // __syncwarp): OUT = mc M u + visc (K u + interior SIP faces + Dirichlet-type boundary
 // faces where bit f of bdir is set).  U: the cell's nodal values in shared memory; the
 // neighbours' values are read from xg[nb * nstride + noff + node].  Geometry: the
 // compact records of this cell (7 doubles per cell point / per face point).
 template <int N, int Q>
-__device__ __forceinline__ void qp_sip_field(const double* U, const double* __restrict__ xg, int nstride, int noff,
+__device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
                                              const double* nbv, const double* penv, int bdir, double mc, double visc,
                                              const double* __restrict__ gcell, const double* __restrict__ gface,
                                              double* W, double* OUT, int lane) {
@@ -197,6 +231,8 @@ __device__ __forceinline__ void qp_sip_field(const double* U, const double* __re
   __syncwarp();
 
   // ---- faces (all six at once)
+  cp_async_wait_all();  // the neighbour blocks (qp_stage_nbrs)
+  __syncwarp();
   for (int it = lane; it < 6 * NF; it += 32) {  // F1: traces and normal reference derivatives, both sides
     const int f = it / NF, tn = it - f * NF;
     const int a = f >> 1, s = f & 1, p = tn % N, q = tn / N;
@@ -212,10 +248,10 @@ __device__ __forceinline__ void qp_sip_field(const double* U, const double* __re
       if (l == (s ? N - 1 : 0)) vs = v;
     }
     if (nb >= 0) {
-      const double* xn = xg + (size_t)nb * nstride + noff + base;
+      const double* xn = W + Wl::NBR + f * N * NF + base;
 #pragma unroll
       for (int l = 0; l < N; ++l) {
-        const double v = __ldg(xn + l * sl);
+        const double v = xn[l * sl];
         dno = fma(t.dE[1 - s][l], v, dno);
         if (l == (s ? 0 : N - 1)) vo = v;
       }
@@ -225,6 +261,7 @@ __device__ __forceinline__ void qp_sip_field(const double* U, const double* __re
     fl[1 * NF + tn] = dns;
     fl[2 * NF + tn] = vo;
     fl[3 * NF + tn] = dno;
+    if (NBF) NBF[f * NF + tn] = vo;
   }
   __syncwarp();
   for (int it = lane; it < 6 * N; it += 32) {  // F2: along p (first tangential axis)
@@ -410,6 +447,11 @@ __global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const do
     cell[G::O_TY + f] = (double)ty;
     cell[G::O_PEN + f] = sfac * m.pen[(size_t)(c0 + c) * 6 + f];
   }
+  if (tid < nc) {  // geometry of the CTA's cells -> L2
+    const size_t cb = (size_t)NQ * G::CS * sizeof(double), fb = (size_t)6 * NQF * G::FS * sizeof(double);
+    prefetch_l2(gc + (size_t)(c0 + tid) * NQ * G::CS, cb, gc, gc + (size_t)m.ncells * NQ * G::CS);
+    prefetch_l2(gf + (size_t)(c0 + tid) * 6 * NQF * G::FS, fb, gf, gf + (size_t)m.ncells * 6 * NQF * G::FS);
+  }
   cp_async_wait_all();
   __syncthreads();
   if (wc >= nc) return;
@@ -422,7 +464,8 @@ __global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const do
   const double* gface = gf + (size_t)cid * 6 * NQF * G::FS;
 
   const int bdir = dir_bdry ? 0x3f : 0;  // the scalar operator: all boundary faces Dirichlet or all natural
-  qp_sip_field<N, Q>(U, x, NB, 0, cell + G::O_NB, cell + G::O_PEN, bdir, mc, 1.0, gcell, gface, W, OUT, lane);
+  qp_stage_nbrs<N>(W + QpSipWork<N, Q>::NBR, x, NB, 0, cell + G::O_NB, lane);
+  qp_sip_field<N, Q>(U, nullptr, cell + G::O_NB, cell + G::O_PEN, bdir, mc, 1.0, gcell, gface, W, OUT, lane);
   for (int i = lane; i < NB; i += 32) y[(size_t)cid * NB + i] = OUT[i];
 }
 
@@ -452,11 +495,13 @@ struct MomQpCfg {
   static constexpr int FPB = 0, FAB = FPB + 6 * 2 * N * QB, FOB = FAB + 6 * QB * N, B_FACE_END = FOB + 6 * NF;
   static constexpr int FPW = 0, W_END_F = FPW + 6 * 2 * 3 * N * QB, W_END_C = BY + QB * QB * N;
   static constexpr int mx(int a, int b) { return a > b ? a : b; }
-  static constexpr int WORK = mx(mx(WSIP, B_CELL_END), mx(B_FACE_END, mx(W_END_F, W_END_C)));
+  static constexpr int NW = W_END_F;  // the neighbours' advecting-field face layers [6][3][NF] (cp.async)
+  static constexpr int WORK = mx(mx(WSIP, B_CELL_END), mx(B_FACE_END, mx(NW + 6 * 3 * NF, W_END_C)));
   // per cell: X (3 comps) | OUT | nb | type | pen | WT | FC | WORK; the advecting field is
   // staged in FC (free until the face factors are written, after its last read)
   static constexpr int O_X = 0, O_OUT = 3 * NB, O_NB = O_OUT + NB, O_TY = O_NB + 6, O_PEN = O_TY + 6,
-                       O_WT = O_PEN + 6, O_FC = O_WT + 3 * NQB, O_WS = O_FC, O_WK = O_FC + 2 * 6 * NQFB;
+                       O_WT = O_PEN + 6, O_FC = O_WT + 3 * NQB, O_WS = O_FC, O_NBF = O_FC + 2 * 6 * NQFB,
+                       O_WK = O_NBF + 6 * NF;
   static_assert(3 * NB <= 2 * 6 * NQFB, "advecting field must fit in FC");
   static constexpr int PER = (O_WK + WORK) | 1;
   static constexpr int C_FIT = (227 * 1024 / 8) / PER;
@@ -504,6 +549,17 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
     cell[G::O_TY + f] = (double)ty;
     cell[G::O_PEN + f] = sfac * m.pen[(size_t)(c0 + c) * 6 + f];
   }
+  if (tid < nc) {  // geometry of the CTA's cells -> L2 (pass B records first: used first)
+    const size_t n = m.ncells, c = c0 + tid;
+    if (passB) {
+      prefetch_l2(gadv + c * 9 * NQB, 9 * NQB * sizeof(double), gadv, gadv + n * 9 * NQB);
+      prefetch_l2(gfw + c * 18 * NQFB, 18 * NQFB * sizeof(double), gfw, gfw + n * 18 * NQFB);
+    }
+    if (passA) {
+      prefetch_l2(gcA + c * G::NQA * 7, G::NQA * 7 * sizeof(double), gcA, gcA + n * G::NQA * 7);
+      prefetch_l2(gfA + c * 6 * G::NQFA * 7, 6 * G::NQFA * 7 * sizeof(double), gfA, gfA + n * 6 * G::NQFA * 7);
+    }
+  }
   cp_async_wait_all();
   __syncthreads();
   if (wc >= nc) return;
@@ -521,6 +577,15 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
   for (int f = 0; f < 6; ++f) bdir |= ((int)tyv[f] == 1) << f;
 
   if (passB) {
+    // the neighbours' advecting-field face layers -> NW (waited for before W2)
+    for (int i = lane; i < 6 * 3 * NF; i += 32) {
+      const int f = i / (3 * NF), r = i - f * 3 * NF, d = r / NF, tn = r - d * NF;
+      const int nb = (int)nbv[f];
+      if (nb < 0) continue;
+      int sl, sp, sq;
+      face_strides<N>(f >> 1, sl, sp, sq);
+      cp_async8(W + G::NW + i, w + (size_t)nb * 3 * NB + d * NB + ((f & 1) ? 0 : N - 1) * sl + (tn % N) * sp + (tn / N) * sq);
+    }
     // ---- W1: advecting field at the rule-B points -> Wt (component-independent)
     const double* WS = cell + G::O_WS;
 #pragma unroll 1
@@ -581,6 +646,8 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
       }
     }
     // ---- W2: face factors a_s, a_o at the rule-B face points
+    cp_async_wait_all();
+    __syncwarp();
     for (int it = lane; it < 6 * 2 * N; it += 32) {
       const int f = it / (2 * N), rem = it - f * 2 * N, side = rem / N, q = rem - side * N;
       const int a = f >> 1, s = f & 1;
@@ -596,9 +663,9 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
 #pragma unroll
           for (int p = 0; p < N; ++p) v[p] = ws[p * sp];
         } else if (nb >= 0) {
-          const double* wn = w + (size_t)nb * 3 * NB + d * NB + (s ? 0 : N - 1) * sl + q * sq;
+          const double* wn = W + G::NW + (f * 3 + d) * NF + N * q;
 #pragma unroll
-          for (int p = 0; p < N; ++p) v[p] = __ldg(wn + p * sp);
+          for (int p = 0; p < N; ++p) v[p] = wn[p];
         } else {
 #pragma unroll
           for (int p = 0; p < N; ++p) v[p] = 0.0;
@@ -662,7 +729,8 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
     const double* U = cell + G::O_X + comp * NB;
     // ---- pass A: mass + SIP viscous at rule k+1
     if (passA) {
-      qp_sip_field<N, QA>(U, x, 3 * NB, comp * NB, nbv, cell + G::O_PEN, bdir, co.mass, co.visc,
+      qp_stage_nbrs<N>(W + QpSipWork<N, QA>::NBR, x, 3 * NB, comp * NB, nbv, lane);
+      qp_sip_field<N, QA>(U, passB ? cell + G::O_NBF : nullptr, nbv, cell + G::O_PEN, bdir, co.mass, co.visc,
                           gcA + (size_t)cid * G::NQA * 7, gfA + (size_t)cid * 6 * G::NQFA * 7, W, OUT, lane);
     } else {
       for (int i = lane; i < NB; i += 32) OUT[i] = 0.0;
@@ -779,9 +847,15 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
 #pragma unroll
           for (int p = 0; p < N; ++p) v[p] = us[p * sp];
         } else if (nb >= 0) {
-          const double* xn = x + (size_t)nb * 3 * NB + comp * NB + (s ? 0 : N - 1) * sl + q * sq;
+          if (passA) {  // the neighbour face layer F1 left in NBF
+            const double* xn = cell + G::O_NBF + f * NF + N * q;
 #pragma unroll
-          for (int p = 0; p < N; ++p) v[p] = __ldg(xn + p * sp);
+            for (int p = 0; p < N; ++p) v[p] = xn[p];
+          } else {
+            const double* xn = x + (size_t)nb * 3 * NB + comp * NB + (s ? 0 : N - 1) * sl + q * sq;
+#pragma unroll
+            for (int p = 0; p < N; ++p) v[p] = __ldg(xn + p * sp);
+          }
         } else {
 #pragma unroll
           for (int p = 0; p < N; ++p) v[p] = 0.0;
