@@ -1,0 +1,50 @@
+"""BASELINE cfg5: 20 consecutive TR-BDF2 steps on the device (3D 96^3 affine, Q2/Q1,
+Re 1600, initial velocity from the vector potential (seed 4) scaled to max nodal |u| = 1,
+dt for CFL 0.5 = 0.5 * H / (k U) with H = min cell diameter sqrt(3)/96,
+GMRES restart 50 / Jacobi-CG, rel tol 1e-10).  Per-step device time (CUDA events) and
+Krylov iteration counts; JSON on stdout.  NSTEPS / CFG_N override for quick runs."""
+import json, math, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2107_07776_b200 as dg
+
+n_el = int(os.environ.get("CFG_N", "96"))
+nsteps = int(os.environ.get("NSTEPS", "20"))
+ku, kp, seed, Re = 2, 1, 4, 1600.0
+t0 = time.time()
+D = dg.DGContext(3, n_el, ku, kp)
+f1 = dg.SynthField(3, seed)
+u = D.zeros(); dg.interpolate_synth_device(D, f1, u)
+umax = float(u.view(D.ncells, 3, -1).pow(2).sum(1).sqrt().max())
+f = dg.SynthField(3, seed, 1.0 / umax)  # max nodal |u| = 1
+for bid in range(6):
+    D.set_dirichlet_fn(bid, f.fn_ptr, f.user_ptr, 0.0)
+u0 = D.zeros(); dg.interpolate_synth_device(D, f, u0)
+H = math.sqrt(3.0) / n_el
+dt = 0.5 * H / (ku * 1.0)
+p0 = D.zeros(dg.SPACE_P)
+bufs = [(u0, p0), (D.zeros(), D.zeros(dg.SPACE_P)), (D.zeros(), D.zeros(dg.SPACE_P))]
+setup = time.time() - t0
+steps = []
+u_nm1, (u_n, p_n) = u0, bufs[0]
+st = torch.cuda.current_stream()
+for n in range(nsteps):
+    u_np1, p_np1 = bufs[(n + 1) % 3]
+    if u_np1.data_ptr() == u_nm1.data_ptr():
+        u_np1, p_np1 = bufs[(n + 2) % 3]
+    sp = dg.StepParams(dt=dt, Re=Re, c=1e3, time=n * dt, restart=50, first_step=(n == 0))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    its = dg.trbdf2_step(D, sp, u_nm1, u_n, p_n, u_np1, p_np1)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ke = float(u_np1.pow(2).sum())
+    steps.append({"step": n, "s": e0.elapsed_time(e1) / 1e3, "its": its, "sum_u2": ke})
+    print(f"step {n}: {steps[-1]['s']:.3f} s its {its}", file=sys.stderr, flush=True)
+    u_nm1, u_n, p_n = u_n, u_np1, p_np1
+tot = sum(s["s"] for s in steps)
+print(json.dumps({"config": f"cfg5: 3D {n_el}^3 affine Q2/Q1, Re 1600, CFL 0.5 (dt {dt:.6e}), GMRES(50)/Jacobi-CG tol 1e-10",
+                  "n_u": D.n_u, "n_p": D.n_p, "setup_s": setup, "steps": nsteps, "total_s": tot,
+                  "s_per_step": tot / nsteps, "umax_scale": 1.0 / umax,
+                  "its_legend": "[gmres s1, gmres s2, cg s1, cg s2, mass-cg s1 (pre), s1 (post), s2 (pre), s2 (post)]",
+                  "per_step": steps}))

@@ -5,9 +5,10 @@ import torch
 import paper_2107_07776_b200 as dg
 cfg = os.environ.get("CFG", "3")
 P = {"1": (2, 32, 2, 1, 0, 100.0, 1e-3, 50), "2": (3, 32, 2, 1, 1, 100.0, 1e-3, 50),
-     "3": (3, 64, 3, 2, 2, 1000.0, 1e-3, 30)}[cfg]
+     "3": (3, 64, 3, 2, 2, 1000.0, 1e-3, 30), "4": (3, 48, 4, 3, 3, 100.0, 1e-3, 50)}[cfg]
 dim, n_el, ku, kp, seed, Re, dt, restart = P
-D = dg.DGContext(dim, n_el, ku, kp)
+# cfg4: interior vertices displaced by U[-0.1h, 0.1h] (seed 3), per-qp geometry
+D = dg.DGContext(dim, n_el, ku, kp, 0.1 / n_el, 3) if cfg == "4" else dg.DGContext(dim, n_el, ku, kp)
 f = dg.SynthField(dim, seed)
 t0 = time.time()
 for bid in range(2 * dim):
