@@ -208,30 +208,35 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
       dc.qcell[Q] = dcell;
       dc.qface[Q] = dface;
       if (dim == 3) {  // compact records for the deformed fast kernels
+        // per cell SoA: cell [7][qx][qy][qz] (the kernels' lane order), face [f][7][qp + Q qq]
         const size_t ncq = g.cell.size() / 10, nfq = g.face.size() / 22;
+        const int nq = Q * Q * Q, nqf = Q * Q;
         std::vector<double> cm(ncq * 7), fn(nfq * 7);
         for (size_t i = 0; i < ncq; ++i) {
           const double* r = &g.cell[i * 10];
           const double jxw = r[9];
-          double* o = &cm[i * 7];
+          const size_t c = i / nq;
+          const int q = (int)(i % nq), qx = q % Q, qy = (q / Q) % Q, qz = q / (Q * Q);
+          double* o = &cm[c * 7 * nq + (qx * Q + qy) + Q * Q * qz];
           int k = 0;
           for (int a = 0; a < 3; ++a)
             for (int b = a; b < 3; ++b) {
               double v = 0.0;
               for (int d = 0; d < 3; ++d) v += r[a * 3 + d] * r[b * 3 + d];
-              o[k++] = jxw * v;
+              o[(k++) * nq] = jxw * v;
             }
-          o[6] = jxw;
+          o[6 * nq] = jxw;
         }
         for (size_t i = 0; i < nfq; ++i) {
           const double* r = &g.face[i * 22];
           const double* n = r + 18;
-          double* o = &fn[i * 7];
+          const size_t cf = i / nqf;  // cell * 6 + face
+          double* o = &fn[cf * 7 * nqf + i % nqf];
           for (int a = 0; a < 3; ++a) {
-            o[a] = r[a * 3] * n[0] + r[a * 3 + 1] * n[1] + r[a * 3 + 2] * n[2];
-            o[3 + a] = r[9 + a * 3] * n[0] + r[9 + a * 3 + 1] * n[1] + r[9 + a * 3 + 2] * n[2];
+            o[a * nqf] = r[a * 3] * n[0] + r[a * 3 + 1] * n[1] + r[a * 3 + 2] * n[2];
+            o[(3 + a) * nqf] = r[9 + a * 3] * n[0] + r[9 + a * 3 + 1] * n[1] + r[9 + a * 3 + 2] * n[2];
           }
-          o[6] = r[21];
+          o[6 * nqf] = r[21];
         }
         double* dcm = (double*)dalloc(cm.size() * sizeof(double));
         double* dfn = (double*)dalloc(fn.size() * sizeof(double));

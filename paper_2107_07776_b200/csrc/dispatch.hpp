@@ -73,7 +73,8 @@ struct DevCtx {
   const double* qcell[kMaxRule] = {};
   const double* qface[kMaxRule] = {};
   // compact per-qp geometry for the deformed fast kernels (fast_deformed.cuh):
-  // cell {detJw Jinv Jinv^T (xx, xy, xz, yy, yz, zz), detJw}; face {Jinv n (3), Jinv_nbr n (3), w ds}
+  // per cell SoA: cell [7][qx][qy][qz] {detJw Jinv Jinv^T (xx, xy, xz, yy, yz, zz), detJw};
+  // face [6][7][qp + Q qq] {Jinv n (3), Jinv_nbr n (3), w ds}
   const double* qcm[kMaxRule] = {};
   const double* qfn[kMaxRule] = {};
   // pass-B (advection) records of the deformed momentum kernel, per cell SoA:

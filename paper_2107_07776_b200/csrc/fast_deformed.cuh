@@ -143,7 +143,6 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
   }
   __syncwarp();
   for (int r = lane; r < Q * Q; r += 32) {  // C3: z pass, metric, z integration
-    const int qx = r / Q, qy = r - qx * Q;
     double vb[N], vy[N], vx[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
@@ -164,9 +163,10 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
         gr[1] = fma(t.B[qz][k], vy[k], gr[1]);
         gr[0] = fma(t.B[qz][k], vx[k], gr[0]);
       }
-      const double* geo = gcell + (size_t)(qx + Q * qy + Q * Q * qz) * 7;
-      const double g00 = __ldg(geo), g01 = __ldg(geo + 1), g02 = __ldg(geo + 2), g11 = __ldg(geo + 3),
-                   g12 = __ldg(geo + 4), g22 = __ldg(geo + 5), jxw = __ldg(geo + 6);
+      constexpr int NQ = Q * Q * Q;  // records [7][qx][qy][qz]: lanes (qx, qy) read consecutive doubles
+      const double* geo = gcell + r + Q * Q * qz;
+      const double g00 = __ldg(geo), g01 = __ldg(geo + NQ), g02 = __ldg(geo + 2 * NQ), g11 = __ldg(geo + 3 * NQ),
+                   g12 = __ldg(geo + 4 * NQ), g22 = __ldg(geo + 5 * NQ), jxw = __ldg(geo + 6 * NQ);
       double ra[3];  // detJw Jinv Jinv^T (reference gradient)
       ra[0] = g00 * gr[0] + g01 * gr[1] + g02 * gr[2];
       ra[1] = g01 * gr[0] + g11 * gr[1] + g12 * gr[2];
@@ -321,11 +321,11 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
           d2o = fma(t.D[qq][q], v[3][q], d2o);
           dnr_o = fma(t.B[qq][q], v[5][q], dnr_o);
         }
-        const double* geo = gface + ((size_t)f * NQF + qp + Q * qq) * 7;
+        const double* geo = gface + (size_t)f * 7 * NQF + qp + Q * qq;  // records [f][7][qp + Q qq]
         double jn[3];  // Jinv n: physical normal derivative = reference gradient . (Jinv n)
 #pragma unroll
-        for (int d = 0; d < 3; ++d) jn[d] = __ldg(geo + d);
-        const double wds = __ldg(geo + 6);
+        for (int d = 0; d < 3; ++d) jn[d] = __ldg(geo + d * NQF);
+        const double wds = __ldg(geo + 6 * NQF);
         double grs[3];
         grs[a] = dnr_s;
         grs[t1] = d1s;
@@ -337,7 +337,7 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
           gro[a] = dnr_o;
           gro[t1] = d1o;
           gro[t2] = d2o;
-          const double dno = __ldg(geo + 3) * gro[0] + __ldg(geo + 4) * gro[1] + __ldg(geo + 5) * gro[2];
+          const double dno = __ldg(geo + 3 * NQF) * gro[0] + __ldg(geo + 4 * NQF) * gro[1] + __ldg(geo + 5 * NQF) * gro[2];
           const double ju = us - uo;
           F = visc * (-0.5 * (dns + dno) + pen * ju) * wds;  // forms.cpp:199-209 / 443-461
           ssym = -0.5 * visc * ju * wds;
