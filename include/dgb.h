@@ -185,6 +185,16 @@ int dgb_gmres(dgb_ctx* ctx, const dgb_operator* op, const dgb_solver_settings* s
               const double* d_b, double* d_x, dgb_solve_result* res, double* hist_host, int hist_cap,
               int* hist_len);
 
+/* Pressure solve (mass_coef M + K_SIP) x = b by CG preconditioned with a hybrid
+ * multigrid V-cycle (DG Q_kp -> continuous Q1 levels, Chebyshev-Jacobi smoothing, dense
+ * coarsest solve).  Same stopping rule as dgb_cg; not
+ * part of the reference (which uses Jacobi): iteration counts differ, solutions agree to
+ * the solver tolerance.  DGB_E_UNSUPPORTED unless the mesh is a uniform Cartesian 3D grid. */
+int dgb_pressure_cg_mg(dgb_ctx* ctx, double mass_coef, const dgb_solver_settings* s, const double* d_b,
+                       double* d_x, dgb_solve_result* res);
+/* z = B r: one application of that V-cycle (symmetric positive definite). */
+int dgb_pressure_mg_vcycle(dgb_ctx* ctx, double mass_coef, const double* d_r, double* d_z);
+
 /* ------------------------------------------------------------------ TR-BDF2 */
 /* One step of the TR-BDF2 projection scheme,
  * entirely on the device.  its[8] = gmres stage 1/2, cg stage 1/2, mass-cg x4. */
@@ -194,6 +204,9 @@ typedef struct {
   double tol_mom, tol_p, tol_mass;
   int max_iter;
   int first_step;
+  /* pressure preconditioner: 0 = Jacobi (the reference's, krylov.cpp:27-41; iteration-count
+   * parity), 1 = hybrid multigrid V-cycle (dgb_pressure_cg_mg; uniform Cartesian 3D meshes) */
+  int pressure_precond;
 } dgb_step_params;
 int dgb_trbdf2_step(dgb_ctx* ctx, const dgb_step_params* p, const double* d_u_nm1, const double* d_u_n,
                     const double* d_p_n, double* d_u_np1, double* d_p_np1, int* its);

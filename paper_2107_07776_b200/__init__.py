@@ -69,7 +69,8 @@ class _Operator(C.Structure):
 class _StepParams(C.Structure):
     _fields_ = [("dt", C.c_double), ("Re", C.c_double), ("c", C.c_double), ("time", C.c_double),
                 ("restart", C.c_int), ("tol_mom", C.c_double), ("tol_p", C.c_double),
-                ("tol_mass", C.c_double), ("max_iter", C.c_int), ("first_step", C.c_int)]
+                ("tol_mass", C.c_double), ("max_iter", C.c_int), ("first_step", C.c_int),
+                ("pressure_precond", C.c_int)]
 
 
 BC_FN = C.CFUNCTYPE(None, _dp, C.c_double, _dp, C.c_void_p)
@@ -132,6 +133,9 @@ def lib() -> C.CDLL:
                                      C.c_void_p, C.c_void_p, C.POINTER(_Result), _dp, C.c_int, _ip]
     L.dgb_trbdf2_step.argtypes = [C.c_void_p, C.POINTER(_StepParams), C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.c_void_p, C.c_void_p, _ip]
+    L.dgb_pressure_cg_mg.argtypes = [C.c_void_p, C.c_double, C.POINTER(_Settings), C.c_void_p, C.c_void_p,
+                                     C.POINTER(_Result)]
+    L.dgb_pressure_mg_vcycle.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
     L.dgb_seeded_uniform.argtypes = [C.c_ulonglong, C.c_size_t, C.c_double, C.c_double, _dp]
     L.dgb_synth_init.argtypes = [C.c_int, C.c_ulonglong, C.c_double, _dp]
     L.dgb_synth_eval.argtypes = [_dp, C.c_double, _dp, C.c_void_p]
@@ -485,6 +489,23 @@ def gmres_solve(V: DGContext, A: LinearOperator, b, s: SolverSettings, M: Option
     return _solve(lib().dgb_gmres, V, A, b, s, M, x)
 
 
+def pressure_cg_mg(V: DGContext, mass_coef: float, b, s: SolverSettings, x) -> SolveResult:
+    """(mass_coef M + K_SIP) x = b by CG with the hybrid multigrid V-cycle (not in the
+    reference, which uses Jacobi: SURVEY 8(f) item 1).  x: initial guess and solution."""
+    res = _Result()
+    st = _Settings(s.rel_tol, s.abs_tol, s.max_iter, s.restart)
+    code = lib().dgb_pressure_cg_mg(V.handle, mass_coef, C.byref(st), _ptr(b), _ptr(x), C.byref(res))
+    if code in (E_NO_CONVERGENCE, E_BREAKDOWN, E_NOT_SPD):
+        raise SolverError(lib().dgb_last_error().decode())
+    _check(code)
+    return SolveResult(res.iterations, res.residual)
+
+
+def pressure_mg_vcycle(V: DGContext, mass_coef: float, r, z) -> None:
+    """z = B r, one V-cycle of the pressure multigrid preconditioner."""
+    _check(lib().dgb_pressure_mg_vcycle(V.handle, mass_coef, _ptr(r), _ptr(z)))
+
+
 # ---------------------------------------------------------------------------
 # TR-BDF2 step (SPEC.md:376-380, SURVEY Appendix A)
 # ---------------------------------------------------------------------------
@@ -500,10 +521,12 @@ class StepParams:
     tol_mass: float = 1e-12
     max_iter: int = 10000
     first_step: bool = True
+    pressure_precond: str = "jacobi"  # "jacobi" (the reference's) or "mg" (pressure_cg_mg)
 
     def _c(self):
+        pc = {"jacobi": 0, "mg": 1}[self.pressure_precond]
         return _StepParams(self.dt, self.Re, self.c, self.time, self.restart, self.tol_mom, self.tol_p,
-                           self.tol_mass, self.max_iter, int(self.first_step))
+                           self.tol_mass, self.max_iter, int(self.first_step), pc)
 
 
 def trbdf2_step(V: DGContext, P: StepParams, u_nm1, u_n, p_n, u_np1, p_np1) -> List[int]:

@@ -329,6 +329,20 @@ int dgb_gmres(dgb_ctx* h, const dgb_operator* op, const dgb_solver_settings* s, 
   return solve(h, true, op, s, inv, b, x, res, hist, cap, hlen);
 }
 
+int dgb_pressure_cg_mg(dgb_ctx* h, double mc, const dgb_solver_settings* s, const double* b, double* x,
+                       dgb_solve_result* res) {
+  NEED(h && s && b && x && res, "null argument");
+  dgb::SolveOut out;
+  const int code = h->c.cg_mg(mc, *s, b, x, out);
+  res->iterations = out.iterations;
+  res->residual = out.residual;
+  return ret(h, code);
+}
+int dgb_pressure_mg_vcycle(dgb_ctx* h, double mc, const double* r, double* z) {
+  NEED(h && r && z, "null argument");
+  return ret(h, h->c.mg_precondition(mc, r, z));
+}
+
 int dgb_trbdf2_step(dgb_ctx* h, const dgb_step_params* p, const double* u_nm1, const double* u_n,
                     const double* p_n, double* u_np1, double* p_np1, int* its) {
   NEED(h && p && u_n && p_n && u_np1 && p_np1 && its, "null argument");

@@ -40,6 +40,7 @@ void* Context::dalloc(size_t bytes) {
 }
 
 Context::~Context() {
+  mg_release(mg_);
   if (device >= 0) cudaSetDevice(device);
   if (dc.stream) cudaStreamSynchronize(dc.stream);
   for (void* p : allocs_) cudaFree(p);
@@ -1013,7 +1014,10 @@ int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const do
     dgb_operator pop{};
     pop.op = DGB_OP_PRESSURE;
     pop.coefs[0] = pmc;
-    OK(cg(pop, s_p, pinv, prhs, p_out, so));
+    if (P.pressure_precond == 1)
+      OK(cg_mg(pmc, s_p, prhs, p_out, so));
+    else
+      OK(cg(pop, s_p, pinv, prhs, p_out, so));
     its[2 + si] = so.iterations;
     phase("pressure cg");
     OK(proj_grad(p_out, ut, its[5 + 2 * si]));

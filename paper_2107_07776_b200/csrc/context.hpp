@@ -21,6 +21,9 @@ struct SolveOut {
   std::vector<double> history;
 };
 
+struct MgHierarchy;
+void mg_release(MgHierarchy* h);
+
 class Context {
  public:
   int dim = 0, ku = 0, kp = 0, device = 0;
@@ -75,6 +78,12 @@ class Context {
   int gmres(const dgb_operator& op, const dgb_solver_settings& s, const double* inv, const double* b, double* x,
             SolveOut& out);
 
+  // pressure multigrid preconditioner (mg.cu; uniform Cartesian 3D meshes)
+  bool mg_supported() const;
+  int mg_setup(double mc);
+  int mg_precondition(double mc, const double* r, double* z);
+  int cg_mg(double mc, const dgb_solver_settings& s, const double* b, double* x, SolveOut& out);
+
   // TR-BDF2 step
   int trbdf2_step(const dgb_step_params& p, const double* u_nm1, const double* u_n, const double* p_n,
                   double* u_np1, double* p_np1, int* its);
@@ -119,6 +128,13 @@ class Context {
   cudaEvent_t ev_start_ = nullptr, ev_in_[kMaxSlabs] = {}, ev_k_[kMaxSlabs] = {};
   size_t gm_n_ = 0;
   int ensure_geometry();
+  MgHierarchy* mg_ = nullptr;
+  int mg_level_apply(int l, const double* x, double* y);
+  int mg_smooth(int l, const double* b, double* x, bool zero_start);
+  int mg_restrict(int l, const double* r_fine, double* r_coarse);
+  int mg_prolong_add(int l, const double* x_coarse, double* x_fine);
+  int mg_vcycle(int l, const double* b, double* x);
+  int mg_lambda_max(int l, double& lmax);
 };
 
 }  // namespace dgb
