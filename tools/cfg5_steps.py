@@ -32,7 +32,8 @@ for n in range(nsteps):
     u_np1, p_np1 = bufs[(n + 1) % 3]
     if u_np1.data_ptr() == u_nm1.data_ptr():
         u_np1, p_np1 = bufs[(n + 2) % 3]
-    sp = dg.StepParams(dt=dt, Re=Re, c=1e3, time=n * dt, restart=50, first_step=(n == 0))
+    sp = dg.StepParams(dt=dt, Re=Re, c=1e3, time=n * dt, restart=50, first_step=(n == 0),
+                       pressure_precond=os.environ.get("PRECOND", "jacobi"))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     its = dg.trbdf2_step(D, sp, u_nm1, u_n, p_n, u_np1, p_np1)
@@ -43,7 +44,8 @@ for n in range(nsteps):
     print(f"step {n}: {steps[-1]['s']:.3f} s its {its}", file=sys.stderr, flush=True)
     u_nm1, u_n, p_n = u_n, u_np1, p_np1
 tot = sum(s["s"] for s in steps)
-print(json.dumps({"config": f"cfg5: 3D {n_el}^3 affine Q2/Q1, Re 1600, CFL 0.5 (dt {dt:.6e}), GMRES(50)/Jacobi-CG tol 1e-10",
+print(json.dumps({"config": f"cfg5: 3D {n_el}^3 affine Q2/Q1, Re 1600, CFL 0.5 (dt {dt:.6e}), GMRES(50) / CG tol 1e-10",
+                  "pressure_precond": os.environ.get("PRECOND", "jacobi"),
                   "n_u": D.n_u, "n_p": D.n_p, "setup_s": setup, "steps": nsteps, "total_s": tot,
                   "s_per_step": tot / nsteps, "umax_scale": 1.0 / umax,
                   "its_legend": "[gmres s1, gmres s2, cg s1, cg s2, mass-cg s1 (pre), s1 (post), s2 (pre), s2 (post)]",
