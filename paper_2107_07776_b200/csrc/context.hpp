@@ -129,6 +129,8 @@ class Context {
   size_t gm_n_ = 0;
   int ensure_geometry();
   MgHierarchy* mg_ = nullptr;
+  mutable int mg_topo_n_ = -1;  // Cartesian topology size (0: none), computed on first use
+  mutable double mg_side_ = 0.0;
   int mg_level_apply(int l, const double* x, double* y);
   int mg_smooth(int l, const double* b, double* x, bool zero_start);
   int mg_restrict(int l, const double* r_fine, double* r_coarse);

@@ -4,11 +4,14 @@
 // reference-parity path keeps Jacobi-CG (dgb_cg); this is dgb_pressure_cg_mg and
 // dgb_step_params::pressure_precond = 1.
 //
-// Uniform Cartesian 3D meshes (DevCtx::ug) only.  Levels:
+// 3D meshes with the lexicographic n x n x n topology of generate_cartesian on a cube
+// (uniform, graded-free; deformed vertex positions allowed: cfg4).  Levels:
 //   0      the DG Q_kp space itself, operator = the fast SIP apply (Context::sip),
 //   1..L   continuous trilinear (Q1) finite elements on vertex grids of n, n/2, n/4, ...
 //          cells per direction, operator = mc M + K assembled as a 27-point tensor
-//          stencil (natural boundary conditions, like the pressure operator);
+//          stencil (natural boundary conditions, like the pressure operator) of the
+//          undeformed grid: exact Galerkin levels on Cartesian meshes, a spectrally
+//          equivalent approximation on deformed ones (vertices moved by <= 10 % of h);
 //   coarsest (n_c <= 4 or odd): exact solve with a dense inverse built on the host.
 // Transfers: DG <- Q1 is the trilinear interpolation at the Gauss-Lobatto nodes of each
 // cell; Q1 fine <- coarse the nested trilinear interpolation; restrictions are their
@@ -258,8 +261,8 @@ __global__ void k_pattern(size_t n, double* x) {
 }
 
 // host: dense (mc M + K) on the (n+1)^3 grid, inverted by Gauss-Jordan (SPD, small)
-bool dense_q1_inverse(int n, double mc, std::vector<double>& inv) {
-  const double h = 1.0 / n;
+bool dense_q1_inverse(int n, double side, double mc, std::vector<double>& inv) {
+  const double h = side / n;
   const int nv = n + 1, m = nv * nv * nv;
   std::vector<double> A((size_t)m * m, 0.0);
   for (int k = 0; k < nv; ++k)
@@ -340,9 +343,41 @@ struct MgHierarchy {
 
 void mg_release(MgHierarchy* h) { delete h; }
 
+// n if the mesh has generate_cartesian's lexicographic n^3 topology (neighbours and
+// boundary ids by index) on a cube of side `side`, else 0
+static int cartesian_topology(const HostMesh& m, double& side) {
+  if (m.dim != 3) return 0;
+  const int n = (int)std::lround(std::cbrt((double)m.ncells));
+  if ((long long)n * n * n != m.ncells || n < 1) return 0;
+  for (int c = 0; c < m.ncells; ++c)
+    for (int f = 0; f < 6; ++f) {
+      const int d = f >> 1, s = f & 1;
+      const int co = d == 0 ? c % n : (d == 1 ? (c / n) % n : c / (n * n));
+      const int stride = d == 0 ? 1 : (d == 1 ? n : n * n);
+      const int want = s == 0 ? (co == 0 ? -1 - f : c - stride) : (co == n - 1 ? -1 - f : c + stride);
+      if (m.nbr[(size_t)c * 6 + f] != want) return 0;
+    }
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (size_t v = 0; v < m.vertices.size() / 3; ++v)
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = std::min(lo[d], m.vertices[v * 3 + d]);
+      hi[d] = std::max(hi[d], m.vertices[v * 3 + d]);
+    }
+  side = hi[0] - lo[0];
+  for (int d = 1; d < 3; ++d)
+    if (std::abs((hi[d] - lo[d]) - side) > 1e-12 * side) return 0;
+  return side > 0.0 ? n : 0;
+}
+
 bool Context::mg_supported() const {
-  if (dim != 3 || !dc.axis || dc.ug.n <= 0 || kp < 1 || kp > 3) return false;
-  int n = dc.ug.n;
+  if (dim != 3 || kp < 1 || kp > 3) return false;
+  if (mg_topo_n_ < 0) {
+    double side = 0.0;
+    mg_topo_n_ = cartesian_topology(mesh, side);
+    mg_side_ = side;
+  }
+  int n = mg_topo_n_;
+  if (n <= 0) return false;
   while (n % 2 == 0 && n > 4) n /= 2;
   return (size_t)(n + 1) * (n + 1) * (n + 1) <= 729;
 }
@@ -477,7 +512,8 @@ int Context::mg_lambda_max(int l, double& lmax) {
 }
 
 int Context::mg_setup(double mc) {
-  if (!mg_supported()) return fail(DGB_E_UNSUPPORTED, "pressure multigrid: needs a uniform Cartesian 3D mesh");
+  if (!mg_supported())
+    return fail(DGB_E_UNSUPPORTED, "pressure multigrid: needs a 3D mesh with Cartesian n^3 topology on a cube");
   if (mg_ && mg_->mc == mc) return DGB_OK;
   if (!mg_) {
     mg_ = new MgHierarchy();
@@ -486,7 +522,7 @@ int Context::mg_setup(double mc) {
     MgLevel L0;
     L0.size = np();
     mg_->lv.push_back(L0);
-    int n = dc.ug.n;
+    int n = mg_topo_n_;
     mg_->lv.push_back(MgLevel{});
     mg_->lv.back().n = n;
     while (n % 2 == 0 && n > 4) {
@@ -498,7 +534,7 @@ int Context::mg_setup(double mc) {
       MgLevel& L = mg_->lv[l];
       if (l > 0) {
         L.size = (size_t)(L.n + 1) * (L.n + 1) * (L.n + 1);
-        L.h = 1.0 / L.n;
+        L.h = mg_side_ / L.n;
       }
       L.inv = mg_->alloc(L.size);
       L.b = mg_->alloc(L.size);
@@ -528,7 +564,7 @@ int Context::mg_setup(double mc) {
   for (size_t l = 0; l + 1 < mg_->lv.size(); ++l) OK(mg_lambda_max((int)l, mg_->lv[l].lmax));
   // coarsest: dense inverse
   std::vector<double> inv;
-  if (!dense_q1_inverse(mg_->lv.back().n, mc, inv)) return fail(DGB_E_NOT_SPD, "pressure multigrid: singular coarse operator");
+  if (!dense_q1_inverse(mg_->lv.back().n, mg_side_, mc, inv)) return fail(DGB_E_NOT_SPD, "pressure multigrid: singular coarse operator");
   CK(cudaMemcpyAsync(mg_->coarse_inv, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
   return DGB_OK;

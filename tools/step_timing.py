@@ -17,7 +17,8 @@ print("dirichlet table", time.time() - t0, "s")
 u0 = D.zeros(); dg.interpolate_synth_device(D, f, u0)
 p0 = D.zeros(dg.SPACE_P)
 u1, p1 = D.zeros(), D.zeros(dg.SPACE_P)
-sp = dg.StepParams(dt=dt, Re=Re, c=1e3, restart=restart, first_step=True)
+sp = dg.StepParams(dt=dt, Re=Re, c=1e3, restart=restart, first_step=True,
+                   pressure_precond=os.environ.get("PRECOND", "jacobi"))
 torch.cuda.synchronize()
 for rep in range(2):
     t0 = time.time(); l0 = D.launch_count()
