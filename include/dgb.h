@@ -197,7 +197,8 @@ int dgb_pressure_mg_vcycle(dgb_ctx* ctx, double mass_coef, const double* d_r, do
 
 /* ------------------------------------------------------------------ TR-BDF2 */
 /* One step of the TR-BDF2 projection scheme,
- * entirely on the device.  its[8] = gmres stage 1/2, cg stage 1/2, mass-cg x4. */
+ * entirely on the device.  its[8] = gmres stage 1/2, cg stage 1/2, mass-cg x4
+ * (its[10] with fixed_point: + fixed-point re-solves of stage 1/2). */
 typedef struct {
   double dt, Re, c, time;
   int restart;
@@ -207,6 +208,13 @@ typedef struct {
   /* pressure preconditioner: 0 = Jacobi (the reference's, krylov.cpp:27-41; iteration-count
    * parity), 1 = hybrid multigrid V-cycle (dgb_pressure_cg_mg; uniform Cartesian 3D meshes) */
   int pressure_precond;
+  /* trbdf2_step_fixedpoint: each momentum predictor solve is repeated
+   * with the advecting field replaced by the latest iterate until the max-norm increment
+   * is below fp_tol (at most fp_max_iter re-solves); its[] then needs 10 entries:
+   * its[8], its[9] = re-solves of stage 1 / 2 (its[0], its[1] sum all GMRES iterations). */
+  int fixed_point;
+  double fp_tol;
+  int fp_max_iter;
 } dgb_step_params;
 int dgb_trbdf2_step(dgb_ctx* ctx, const dgb_step_params* p, const double* d_u_nm1, const double* d_u_n,
                     const double* d_p_n, double* d_u_np1, double* d_p_np1, int* its);

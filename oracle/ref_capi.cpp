@@ -263,7 +263,8 @@ struct Ctx : Base {
     }
   }
 
-  // params: dt, Re, c, time, restart, tol_mom, tol_p, tol_mass, max_iter, first_step
+  // params: dt, Re, c, time, restart, tol_mom, tol_p, tol_mass, max_iter, first_step,
+  //         fixed_point, fp_tol, fp_max_iter; its: 10 (the device order, + fixed-point counts)
   void step(const double* prm, const double* u_nm1, const double* u_n, const double* p_n,
             double* u_np1, double* p_np1, int* its) override {
     oracle_trbdf2::StepParams P;
@@ -277,6 +278,9 @@ struct Ctx : Base {
     P.tol_mass = prm[7];
     P.max_iter = static_cast<int>(prm[8]);
     P.first_step = prm[9] != 0.0;
+    P.fixed_point = prm[10] != 0.0;
+    P.fp_tol = prm[11];
+    P.fp_max_iter = static_cast<int>(prm[12]);
     oracle_trbdf2::StepStats st;
     Field un1, pn1;
     oracle_trbdf2::trbdf2_step(*Vu, *Vp, *geom, bc, P, F(u_nm1, nu()), F(u_n, nu()), F(p_n, np()),
@@ -288,6 +292,8 @@ struct Ctx : Base {
     its[2] = st.cg_its[0];
     its[3] = st.cg_its[1];
     for (int i = 0; i < 4; ++i) its[4 + i] = st.mass_its[i];
+    its[8] = st.fp_its[0];
+    its[9] = st.fp_its[1];
   }
 
   // interior: [cell_in, face_in, cell_out, face_out, hanging] per face (active indices)

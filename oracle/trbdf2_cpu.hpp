@@ -13,6 +13,7 @@
 #include "forms.hpp"
 #include "krylov.hpp"
 
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -31,10 +32,16 @@ struct StepParams {
   double tol_mass = 1e-12;
   int max_iter = 10000;
   bool first_step = true;   // n = 0: w1 = u^0
+  // trbdf2_step_fixedpoint: each predictor solve is iterated with the
+  // advecting field replaced by the latest iterate until the max-norm increment < fp_tol
+  bool fixed_point = false;
+  double fp_tol = 1e-8;
+  int fp_max_iter = 100;
 };
 
 struct StepStats {
-  int gmres_its[2] = {0, 0};
+  int fp_its[2] = {0, 0};     // fixed-point re-solves per stage (0 without fixed_point)
+  int gmres_its[2] = {0, 0};  // summed over the stage's predictor solves
   int cg_its[2] = {0, 0};
   int mass_its[4] = {0, 0, 0, 0};
   double gmres_res[2] = {0, 0};
@@ -76,7 +83,7 @@ int projected_gradient(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionS
 template <int dim>
 void stage(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<dim>& Vp,
            const dgns::GeometryCache<dim>& geom, const dgns::BoundaryTable<dim>& bc,
-           const dgns::MomentumCtx<dim>& ctx, const dgns::MomentumRhs<dim>& rhs, double alpha,
+           const dgns::MomentumCtx<dim>& ctx, const dgns::MomentumRhs<dim>& rhs, Field& w, double alpha,
            const Field& u_guess, const Field& p_old, const StepParams& P, Field& u_new,
            Field& p_new, StepStats& st, int si) {
   const int nu = Vu.n_dofs(), np = Vp.n_dofs();
@@ -101,6 +108,29 @@ void stage(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<dim>& V
       F.data(), sm, &Mu, ustar.data());
   st.gmres_its[si] = rg.iterations;
   st.gmres_res[si] = rg.residual;
+  // fixed point (decision FP1): w is the field every advecting-field pointer of
+  // ctx / rhs refers to; it becomes the latest iterate, then RHS, diagonal and solve again
+  // (initial guess: the latest iterate) until max |u*_i - u*_{i-1}| < fp_tol
+  for (int it = 0; P.fixed_point && it < P.fp_max_iter; ++it) {
+    w = ustar;
+    dgns::momentum_rhs(Vu, Vp, geom, rhs, F);
+    dgns::momentum_diagonal(Vu, geom, ctx, diag);
+    const dgns::JacobiPreconditioner Mf(diag);
+    Field prev = ustar;
+    auto rf = dgns::gmres_solve(
+        nu, [&](const double* x, double* y) {
+          Field xx(x, x + nu);
+          dgns::apply_momentum(Vu, geom, ctx, xx, tmp);
+          std::copy(tmp.begin(), tmp.end(), y);
+        },
+        F.data(), sm, &Mf, ustar.data());
+    st.gmres_its[si] += rf.iterations;
+    st.gmres_res[si] = rf.residual;
+    st.fp_its[si] = it + 1;
+    double inc = 0.0;
+    for (int i = 0; i < nu; ++i) inc = std::max(inc, std::abs(ustar[i] - prev[i]));
+    if (inc < P.fp_tol) break;
+  }
 
   const double adt = alpha * P.dt;
   // u** = u* + alpha dt M^-1 G p_old
@@ -170,7 +200,7 @@ void trbdf2_step(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<d
   r1.time = P.time + g * dt;
   r1.bc = &bc;
   Field u_g, p_g;
-  stage(Vu, Vp, geom, bc, c1, r1, g, u_n, p_n, P, u_g, p_g, st, 0);
+  stage(Vu, Vp, geom, bc, c1, r1, w1, g, u_n, p_n, P, u_g, p_g, st, 0);
 
   // ---- stage 2 (alpha = 1 - gamma) ----
   const double a33 = 1.0 / (2.0 - g);
@@ -195,7 +225,7 @@ void trbdf2_step(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<d
   r2.dir_w = &w2;
   r2.time = P.time + dt;
   r2.bc = &bc;
-  stage(Vu, Vp, geom, bc, c2, r2, 1.0 - g, u_g, p_g, P, u_np1, p_np1, st, 1);
+  stage(Vu, Vp, geom, bc, c2, r2, w2, 1.0 - g, u_g, p_g, P, u_np1, p_np1, st, 1);
 }
 
 }  // namespace oracle_trbdf2

@@ -70,7 +70,8 @@ class _StepParams(C.Structure):
     _fields_ = [("dt", C.c_double), ("Re", C.c_double), ("c", C.c_double), ("time", C.c_double),
                 ("restart", C.c_int), ("tol_mom", C.c_double), ("tol_p", C.c_double),
                 ("tol_mass", C.c_double), ("max_iter", C.c_int), ("first_step", C.c_int),
-                ("pressure_precond", C.c_int)]
+                ("pressure_precond", C.c_int), ("fixed_point", C.c_int), ("fp_tol", C.c_double),
+                ("fp_max_iter", C.c_int)]
 
 
 BC_FN = C.CFUNCTYPE(None, _dp, C.c_double, _dp, C.c_void_p)
@@ -522,21 +523,27 @@ class StepParams:
     max_iter: int = 10000
     first_step: bool = True
     pressure_precond: str = "jacobi"  # "jacobi" (the reference's) or "mg" (pressure_cg_mg)
+    fixed_point: bool = False         # trbdf2_step_fixedpoint
+    fp_tol: float = 1e-8
+    fp_max_iter: int = 100
 
     def _c(self):
         pc = {"jacobi": 0, "mg": 1}[self.pressure_precond]
         return _StepParams(self.dt, self.Re, self.c, self.time, self.restart, self.tol_mom, self.tol_p,
-                           self.tol_mass, self.max_iter, int(self.first_step), pc)
+                           self.tol_mass, self.max_iter, int(self.first_step), pc, int(self.fixed_point),
+                           self.fp_tol, self.fp_max_iter)
 
 
 def trbdf2_step(V: DGContext, P: StepParams, u_nm1, u_n, p_n, u_np1, p_np1) -> List[int]:
-    its = (C.c_int * 8)()
+    """Returns [gmres s1, gmres s2, cg s1, cg s2, mass-cg x4] (+ [fixed-point re-solves s1, s2]
+    when P.fixed_point)."""
+    its = (C.c_int * 10)()
     code = lib().dgb_trbdf2_step(V.handle, C.byref(P._c()), _ptr(u_nm1), _ptr(u_n), _ptr(p_n), _ptr(u_np1),
                                  _ptr(p_np1), its)
     if code in (E_NO_CONVERGENCE, E_BREAKDOWN, E_NOT_SPD):
         raise SolverError(lib().dgb_last_error().decode())
     _check(code)
-    return list(its)
+    return list(its)[: 10 if P.fixed_point else 8]
 
 
 # ---------------------------------------------------------------------------

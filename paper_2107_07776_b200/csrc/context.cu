@@ -949,9 +949,11 @@ int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const do
   double* prhs = scratch_vec(38, NP);
   double* pinv = scratch_vec(39, NP);
   double* p_g = scratch_vec(40, NP);
+  double* fp_prev = P.fixed_point ? scratch_vec(41, NU) : nullptr;  // previous fixed-point iterate
   if (!wv || !F || !inv || !g || !uss || !u_g || !minv || !ut || !prhs || !pinv || !p_g)
     return fail(DGB_E_CUDA, "trbdf2: out of device memory");
-  for (int i = 0; i < 8; ++i) its[i] = 0;
+  if (P.fixed_point && !fp_prev) return fail(DGB_E_CUDA, "trbdf2: out of device memory");
+  for (int i = 0; i < (P.fixed_point ? 10 : 8); ++i) its[i] = 0;
   // DGB_PHASES=1: synchronise and print the wall time of every phase (diagnostics only)
   static const bool phases = std::getenv("DGB_PHASES") != nullptr;
   auto t_last = std::chrono::steady_clock::now();
@@ -998,6 +1000,23 @@ int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const do
     SolveOut so;
     OK(gmres(mop, s_mom, inv, F, u_out, so));
     its[si] = so.iterations;
+    // fixed point (trbdf2_step_fixedpoint; decision FP1 in DESIGN.md): wv, the field every
+    // advecting-field pointer of the operator / rhs refers to, becomes the latest iterate;
+    // rhs, diagonal and solve again (initial guess the latest iterate) until the max-norm
+    // increment < fp_tol.  Same sequence as oracle/trbdf2_cpu.hpp.
+    for (int it = 0; P.fixed_point && it < P.fp_max_iter; ++it) {
+      CK(cudaMemcpyAsync(wv, u_out, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      OK(rhs(rd, F));
+      OK(momentum_diag(mc, wv, g));
+      OK(jacobi_inverse(NU, g, inv));
+      CK(cudaMemcpyAsync(fp_prev, u_out, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      OK(gmres(mop, s_mom, inv, F, u_out, so));
+      its[si] += so.iterations;
+      its[8 + si] = it + 1;
+      double inc = 0.0;
+      OK(max_abs_diff(NU, u_out, fp_prev, &inc));
+      if (inc < P.fp_tol) break;
+    }
     phase("gmres");
     const double adt = alpha * P.dt;
     OK(proj_grad(p_old, ut, its[4 + 2 * si]));

@@ -209,7 +209,9 @@ class RefCtx:
         prm = np.ascontiguousarray(params, dtype=np.float64)
         u1 = np.zeros(self.n_u)
         p1 = np.zeros(self.n_p)
-        its = (C.c_int * 8)()
+        if len(prm) < 13:  # no fixed point
+            prm = np.concatenate([prm, [0.0, 1e-8, 100.0][len(prm) - 10:]])
+        its = (C.c_int * 10)()
         if lib().ref_trbdf2_step(self.h, P(prm), P(u_nm1), P(u_n), P(p_n), P(u1), P(p1), its):
             raise RuntimeError(lib().ref_last_error().decode())
         return u1, p1, list(its)
