@@ -216,6 +216,15 @@ typedef struct {
   double fp_tol;
   int fp_max_iter;
 } dgb_step_params;
+/* The two baseline projection schemes the paper compares against (PAPER.md:182-232,
+ * SPEC.md:391-405): DGB_SCHEME_BCG (Bell-Colella-Glaz, fully nonlinear Crank-Nicolson
+ * predictor solved by fixed point, increment-form Helmholtz) and DGB_SCHEME_GQ_BDF2
+ * (Guermond-Quartapelle BDF2; its first step, first_step != 0, is a BCG step).  Same
+ * params; its[10] = [gmres, 0, cg, 0, mass-cg (pre), mass-cg (post), 0, 0, fixed-point
+ * re-solves, 0].  DGB_SCHEME_TRBDF2 = dgb_trbdf2_step. */
+enum { DGB_SCHEME_TRBDF2 = 0, DGB_SCHEME_BCG = 1, DGB_SCHEME_GQ_BDF2 = 2 };
+int dgb_projection_step(dgb_ctx* ctx, int scheme, const dgb_step_params* p, const double* d_u_nm1,
+                        const double* d_u_n, const double* d_p_n, double* d_u_np1, double* d_p_np1, int* its);
 int dgb_trbdf2_step(dgb_ctx* ctx, const dgb_step_params* p, const double* d_u_nm1, const double* d_u_n,
                     const double* d_p_n, double* d_u_np1, double* d_p_np1, int* its);
 

@@ -58,6 +58,8 @@ struct Base {
                     int* hist_len) = 0;
   virtual void step(const double* params, const double* u_nm1, const double* u_n,
                     const double* p_n, double* u_np1, double* p_np1, int* its) = 0;
+  virtual void scheme_step(int scheme, const double* params, const double* u_nm1, const double* u_n,
+                           const double* p_n, double* u_np1, double* p_np1, int* its) = 0;
   virtual void faces(int* iface, double* imeas, int* bface, double* bmeas) = 0;
   virtual void cell_vertices(double* xv) = 0;
   virtual void bface_points(int rule, double* xq) = 0;
@@ -294,6 +296,32 @@ struct Ctx : Base {
     for (int i = 0; i < 4; ++i) its[4 + i] = st.mass_its[i];
     its[8] = st.fp_its[0];
     its[9] = st.fp_its[1];
+  }
+
+  // scheme 1 = BCG, 2 = GQ-BDF2 (params as step(); its: 10)
+  void scheme_step(int scheme, const double* prm, const double* u_nm1, const double* u_n, const double* p_n,
+                   double* u_np1, double* p_np1, int* its) override {
+    oracle_trbdf2::StepParams P;
+    P.dt = prm[0];
+    P.Re = prm[1];
+    P.c = prm[2];
+    P.time = prm[3];
+    P.restart = static_cast<int>(prm[4]);
+    P.tol_mom = prm[5];
+    P.tol_p = prm[6];
+    P.tol_mass = prm[7];
+    P.max_iter = static_cast<int>(prm[8]);
+    P.first_step = prm[9] != 0.0;
+    P.fp_tol = prm[11];
+    P.fp_max_iter = static_cast<int>(prm[12]);
+    Field un1, pn1;
+    if (scheme == 1)
+      oracle_trbdf2::bcg_step(*Vu, *Vp, *geom, bc, P, F(u_n, nu()), F(p_n, np()), un1, pn1, its);
+    else
+      oracle_trbdf2::gq_bdf2_step(*Vu, *Vp, *geom, bc, P, F(u_nm1 ? u_nm1 : u_n, nu()), F(u_n, nu()),
+                                  F(p_n, np()), un1, pn1, its);
+    std::memcpy(u_np1, un1.data(), sizeof(double) * nu());
+    std::memcpy(p_np1, pn1.data(), sizeof(double) * np());
   }
 
   // interior: [cell_in, face_in, cell_out, face_out, hanging] per face (active indices)
@@ -541,6 +569,16 @@ int ref_trbdf2_step(void* h, const double* params, const double* u_nm1, const do
                     const double* p_n, double* u_np1, double* p_np1, int* its) {
   try {
     static_cast<Base*>(h)->step(params, u_nm1, u_n, p_n, u_np1, p_np1, its);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+int ref_scheme_step(void* h, int scheme, const double* params, const double* u_nm1, const double* u_n,
+                    const double* p_n, double* u_np1, double* p_np1, int* its) {
+  try {
+    static_cast<Base*>(h)->scheme_step(scheme, params, u_nm1, u_n, p_n, u_np1, p_np1, its);
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -228,4 +228,141 @@ void trbdf2_step(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<d
   stage(Vu, Vp, geom, bc, c2, r2, w2, 1.0 - g, u_g, p_g, P, u_np1, p_np1, st, 1);
 }
 
+
+// ---------------------------------------------------------------------------
+// The two baseline projection schemes of PAPER.md:182-232 / SPEC.md:391-405
+// (bcg_step, gq_bdf2_step), restated with the same reference calls.  Decisions
+// (DESIGN.md "Baseline schemes"): BCG solves its fully nonlinear predictor by fixed
+// point with w_0 = u^n, w_{i+1} = (u*_i + u^n) / 2, and uses the increment-form
+// Helmholtz (14) as printed; GQ-BDF2 uses the consistent BDF2 weights 3/(2dt) with the
+// 2/3 dt projection throughout (the printed /dt in Eqs. (15)-(16) read as the effective
+// step 2dt/3), advecting field 2u^n - u^{n-1}, skew coefficient -1/2 (the conservative
+// C_LF of forms.cpp minus 1/2 (div w) u gives (w.grad)u + 1/2 (div w) u), and takes its
+// first step (no u^{n-1}) with BCG.
+// its: [gmres, 0, cg, 0, mass-cg (pre), mass-cg (post), 0, 0, fixed-point re-solves, 0]
+
+/// Predictor GMRES with Jacobi(momentum_diagonal), initial guess x.
+template <int dim>
+dgns::SolveResult predictor(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<dim>& Vp,
+                            const dgns::GeometryCache<dim>& geom, const dgns::MomentumCtx<dim>& ctx,
+                            const dgns::MomentumRhs<dim>& rhs, const StepParams& P, Field& x) {
+  const int nu = Vu.n_dofs();
+  Field F, diag, tmp;
+  dgns::momentum_rhs(Vu, Vp, geom, rhs, F);
+  dgns::momentum_diagonal(Vu, geom, ctx, diag);
+  const dgns::JacobiPreconditioner M(diag);
+  dgns::SolverSettings sm;
+  sm.rel_tol = P.tol_mom;
+  sm.restart = P.restart;
+  sm.max_iter = P.max_iter;
+  return dgns::gmres_solve(
+      nu, [&](const double* xx, double* y) {
+        Field v(xx, xx + nu);
+        dgns::apply_momentum(Vu, geom, ctx, v, tmp);
+        std::copy(tmp.begin(), tmp.end(), y);
+      },
+      F.data(), sm, &M, x.data());
+}
+
+/// Bell-Colella-Glaz step.
+template <int dim>
+void bcg_step(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<dim>& Vp,
+              const dgns::GeometryCache<dim>& geom, const dgns::BoundaryTable<dim>& bc, const StepParams& P,
+              const Field& u_n, const Field& p_n, Field& u_np1, Field& p_np1, int* its) {
+  const int nu = Vu.n_dofs(), np = Vp.n_dofs();
+  const double dt = P.dt, Re = P.Re;
+  for (int i = 0; i < 10; ++i) its[i] = 0;
+  Field w = u_n;
+  dgns::MomentumCtx<dim> c;
+  c.mass_coef = 1.0 / dt;
+  c.visc_coef = 1.0 / (2.0 * Re);
+  c.adv_coef = 0.5;
+  c.skew_coef = 0.0;
+  c.advecting = &w;
+  c.bc = &bc;
+  dgns::MomentumRhs<dim> r;
+  r.mass = {{1.0 / dt, &u_n}};
+  r.visc = {{1.0 / (2.0 * Re), &u_n}};
+  r.adv = {{0.5, &u_n, &w}};
+  r.pres = {{1.0, &p_n}};
+  r.dir_visc_coef = 1.0 / (2.0 * Re);
+  r.dir_adv_coef = 0.5;
+  r.dir_w = &w;
+  r.time = P.time + dt;
+  r.bc = &bc;
+  Field ustar = u_n;
+  its[0] = predictor(Vu, Vp, geom, c, r, P, ustar).iterations;
+  for (int it = 0; it < P.fp_max_iter; ++it) {  // fully nonlinear: w = (u* + u^n) / 2
+    lincomb(0.5, ustar, 0.5, u_n, w);
+    Field prev = ustar;
+    its[0] += predictor(Vu, Vp, geom, c, r, P, ustar).iterations;
+    its[8] = it + 1;
+    double inc = 0.0;
+    for (int i = 0; i < nu; ++i) inc = std::max(inc, std::abs(ustar[i] - prev[i]));
+    if (inc < P.fp_tol) break;
+  }
+  // increment-form Helmholtz (14): (mc M + K) dp = (1/dt) B(u*), dp0 = 0
+  const double mass_coef = 1.0 / (P.c * P.c * dt * dt);
+  Field prhs, hd, tmp;
+  dgns::pressure_rhs(Vu, Vp, geom, 1.0 / dt, ustar, mass_coef, nullptr, &bc, prhs);
+  dgns::helmholtz_diagonal(Vp, geom, mass_coef, hd);
+  const dgns::JacobiPreconditioner Mp(hd);
+  dgns::SolverSettings sp;
+  sp.rel_tol = P.tol_p;
+  sp.max_iter = P.max_iter;
+  Field dp(np, 0.0);
+  its[2] = dgns::cg_solve(
+               np, [&](const double* x, double* y) {
+                 Field xx(x, x + np);
+                 dgns::apply_pressure_helmholtz(Vp, geom, mass_coef, xx, tmp);
+                 std::copy(tmp.begin(), tmp.end(), y);
+               },
+               prhs.data(), sp, &Mp, dp.data())
+               .iterations;
+  Field ut;
+  its[5] = projected_gradient(Vu, Vp, geom, dp, P, ut);
+  u_np1.resize(nu);
+  for (int i = 0; i < nu; ++i) u_np1[i] = ustar[i] - dt * ut[i];
+  p_np1.resize(np);
+  for (int i = 0; i < np; ++i) p_np1[i] = p_n[i] + dp[i];
+}
+
+/// Guermond-Quartapelle BDF2 step; first step (first_step) = BCG.
+template <int dim>
+void gq_bdf2_step(const dgns::FunctionSpace<dim>& Vu, const dgns::FunctionSpace<dim>& Vp,
+                  const dgns::GeometryCache<dim>& geom, const dgns::BoundaryTable<dim>& bc, const StepParams& P,
+                  const Field& u_nm1, const Field& u_n, const Field& p_n, Field& u_np1, Field& p_np1, int* its) {
+  if (P.first_step) {
+    bcg_step(Vu, Vp, geom, bc, P, u_n, p_n, u_np1, p_np1, its);
+    return;
+  }
+  for (int i = 0; i < 10; ++i) its[i] = 0;
+  const double dt = P.dt, Re = P.Re;
+  Field w;
+  lincomb(2.0, u_n, -1.0, u_nm1, w);
+  dgns::MomentumCtx<dim> c;
+  c.mass_coef = 3.0 / (2.0 * dt);
+  c.visc_coef = 1.0 / Re;
+  c.adv_coef = 1.0;
+  c.skew_coef = -0.5;
+  c.advecting = &w;
+  c.bc = &bc;
+  dgns::MomentumRhs<dim> r;
+  r.mass = {{2.0 / dt, &u_n}, {-1.0 / (2.0 * dt), &u_nm1}};
+  r.pres = {{1.0, &p_n}};
+  r.dir_visc_coef = 1.0 / Re;
+  r.dir_adv_coef = 1.0;
+  r.dir_w = &w;
+  r.time = P.time + dt;
+  r.bc = &bc;
+  StepParams Q = P;
+  Q.fixed_point = false;
+  StepStats st;
+  stage(Vu, Vp, geom, bc, c, r, w, 2.0 / 3.0, u_n, p_n, Q, u_np1, p_np1, st, 0);
+  its[0] = st.gmres_its[0];
+  its[2] = st.cg_its[0];
+  its[4] = st.mass_its[0];
+  its[5] = st.mass_its[1];
+}
+
 }  // namespace oracle_trbdf2

@@ -137,6 +137,8 @@ def lib() -> C.CDLL:
     L.dgb_pressure_cg_mg.argtypes = [C.c_void_p, C.c_double, C.POINTER(_Settings), C.c_void_p, C.c_void_p,
                                      C.POINTER(_Result)]
     L.dgb_pressure_mg_vcycle.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
+    L.dgb_projection_step.argtypes = [C.c_void_p, C.c_int, C.POINTER(_StepParams), C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p, _ip]
     L.dgb_seeded_uniform.argtypes = [C.c_ulonglong, C.c_size_t, C.c_double, C.c_double, _dp]
     L.dgb_synth_init.argtypes = [C.c_int, C.c_ulonglong, C.c_double, _dp]
     L.dgb_synth_eval.argtypes = [_dp, C.c_double, _dp, C.c_void_p]
@@ -532,6 +534,21 @@ class StepParams:
         return _StepParams(self.dt, self.Re, self.c, self.time, self.restart, self.tol_mom, self.tol_p,
                            self.tol_mass, self.max_iter, int(self.first_step), pc, int(self.fixed_point),
                            self.fp_tol, self.fp_max_iter)
+
+
+SCHEME_TRBDF2, SCHEME_BCG, SCHEME_GQ_BDF2 = 0, 1, 2
+
+
+def projection_step(V: DGContext, scheme: int, P: StepParams, u_nm1, u_n, p_n, u_np1, p_np1) -> List[int]:
+    """One step of SCHEME_TRBDF2 / SCHEME_BCG / SCHEME_GQ_BDF2; for the two
+    baseline schemes returns [gmres, 0, cg, 0, mass-cg pre, mass-cg post, 0, 0, fixed-point re-solves, 0]."""
+    its = (C.c_int * 10)()
+    code = lib().dgb_projection_step(V.handle, scheme, C.byref(P._c()), _ptr(u_nm1), _ptr(u_n), _ptr(p_n),
+                                     _ptr(u_np1), _ptr(p_np1), its)
+    if code in (E_NO_CONVERGENCE, E_BREAKDOWN, E_NOT_SPD):
+        raise SolverError(lib().dgb_last_error().decode())
+    _check(code)
+    return list(its)[: 10 if (P.fixed_point or scheme != SCHEME_TRBDF2) else 8]
 
 
 def trbdf2_step(V: DGContext, P: StepParams, u_nm1, u_n, p_n, u_np1, p_np1) -> List[int]:

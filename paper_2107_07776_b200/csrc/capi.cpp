@@ -343,6 +343,13 @@ int dgb_pressure_mg_vcycle(dgb_ctx* h, double mc, const double* r, double* z) {
   return ret(h, h->c.mg_precondition(mc, r, z));
 }
 
+int dgb_projection_step(dgb_ctx* h, int scheme, const dgb_step_params* p, const double* u_nm1, const double* u_n,
+                        const double* p_n, double* u_np1, double* p_np1, int* its) {
+  NEED(h && p && u_n && p_n && u_np1 && p_np1 && its, "null argument");
+  NEED(scheme >= DGB_SCHEME_TRBDF2 && scheme <= DGB_SCHEME_GQ_BDF2, "unknown scheme");
+  NEED(p->first_step || u_nm1 || scheme == DGB_SCHEME_BCG, "u_nm1 required after the first step");
+  return ret(h, h->c.projection_step(scheme, *p, u_nm1, u_n, p_n, u_np1, p_np1, its));
+}
 int dgb_trbdf2_step(dgb_ctx* h, const dgb_step_params* p, const double* u_nm1, const double* u_n,
                     const double* p_n, double* u_np1, double* p_np1, int* its) {
   NEED(h && p && u_n && p_n && u_np1 && p_np1 && its, "null argument");

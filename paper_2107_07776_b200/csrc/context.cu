@@ -935,6 +935,16 @@ int Context::set_dirichlet_fn(int id, dgb_bc_fn fn, void* user, double t) {
 // Same call sequence as oracle/trbdf2_cpu.hpp, every operator / solver on the device.
 int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const double* u_n, const double* p_n,
                          double* u_np1, double* p_np1, int* its) {
+  return projection_step(DGB_SCHEME_TRBDF2, P, u_nm1, u_n, p_n, u_np1, p_np1, its);
+}
+
+// scheme: DGB_SCHEME_TRBDF2, DGB_SCHEME_BCG / DGB_SCHEME_GQ_BDF2
+// (decisions in DESIGN.md "Baseline schemes"; same calls as
+// oracle/trbdf2_cpu.hpp bcg_step / gq_bdf2_step)
+int Context::projection_step(int scheme, const dgb_step_params& P, const double* u_nm1, const double* u_n,
+                             const double* p_n, double* u_np1, double* p_np1, int* its) {
+  if (scheme == DGB_SCHEME_GQ_BDF2 && P.first_step) scheme = DGB_SCHEME_BCG;  // no u^{n-1} yet
+  if (scheme == DGB_SCHEME_GQ_BDF2 && !u_nm1) return fail(DGB_E_ARG, "gq_bdf2: u_nm1 required after the first step");
   const size_t NU = nu(), NP = np();
   cudaStream_t st = dc.stream;
   const double gm = 2.0 - std::sqrt(2.0);
@@ -949,11 +959,12 @@ int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const do
   double* prhs = scratch_vec(38, NP);
   double* pinv = scratch_vec(39, NP);
   double* p_g = scratch_vec(40, NP);
-  double* fp_prev = P.fixed_point ? scratch_vec(41, NU) : nullptr;  // previous fixed-point iterate
+  const bool fixed_point = (P.fixed_point && scheme == DGB_SCHEME_TRBDF2) || scheme == DGB_SCHEME_BCG;
+  double* fp_prev = fixed_point ? scratch_vec(41, NU) : nullptr;  // previous fixed-point iterate
   if (!wv || !F || !inv || !g || !uss || !u_g || !minv || !ut || !prhs || !pinv || !p_g)
     return fail(DGB_E_CUDA, "trbdf2: out of device memory");
-  if (P.fixed_point && !fp_prev) return fail(DGB_E_CUDA, "trbdf2: out of device memory");
-  for (int i = 0; i < (P.fixed_point ? 10 : 8); ++i) its[i] = 0;
+  if (fixed_point && !fp_prev) return fail(DGB_E_CUDA, "trbdf2: out of device memory");
+  for (int i = 0; i < (fixed_point || scheme != DGB_SCHEME_TRBDF2 ? 10 : 8); ++i) its[i] = 0;
   // DGB_PHASES=1: synchronise and print the wall time of every phase (diagnostics only)
   static const bool phases = std::getenv("DGB_PHASES") != nullptr;
   auto t_last = std::chrono::steady_clock::now();
@@ -1004,7 +1015,7 @@ int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const do
     // advecting-field pointer of the operator / rhs refers to, becomes the latest iterate;
     // rhs, diagonal and solve again (initial guess the latest iterate) until the max-norm
     // increment < fp_tol.  Same sequence as oracle/trbdf2_cpu.hpp.
-    for (int it = 0; P.fixed_point && it < P.fp_max_iter; ++it) {
+    for (int it = 0; P.fixed_point && scheme == DGB_SCHEME_TRBDF2 && it < P.fp_max_iter; ++it) {
       CK(cudaMemcpyAsync(wv, u_out, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
       OK(rhs(rd, F));
       OK(momentum_diag(mc, wv, g));
@@ -1047,6 +1058,103 @@ int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const do
     return DGB_OK;
   };
 
+  const double Re = P.Re, dt = P.dt;
+  if (scheme == DGB_SCHEME_BCG) {
+    // fully nonlinear CN predictor by fixed point: w_0 = u^n, w_{i+1} = (u*_i + u^n) / 2
+    CK(cudaMemcpyAsync(wv, u_n, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    const double mc[4] = {1.0 / dt, 1.0 / (2.0 * Re), 0.5, 0.0};
+    dgb_rhs_desc rd{};
+    rd.n_mass = 1;
+    rd.mass_coef[0] = 1.0 / dt;
+    rd.mass_f[0] = u_n;
+    rd.n_visc = 1;
+    rd.visc_coef[0] = 1.0 / (2.0 * Re);
+    rd.visc_f[0] = u_n;
+    rd.n_adv = 1;
+    rd.adv_coef[0] = 0.5;
+    rd.adv_f[0] = u_n;
+    rd.adv_w[0] = wv;
+    rd.n_pres = 1;
+    rd.pres_coef[0] = 1.0;
+    rd.pres_f[0] = p_n;
+    rd.dir_visc_coef = 1.0 / (2.0 * Re);
+    rd.dir_adv_coef = 0.5;
+    rd.dir_w = wv;
+    dgb_operator mop{};
+    mop.op = DGB_OP_MOMENTUM;
+    for (int i = 0; i < 4; ++i) mop.coefs[i] = mc[i];
+    mop.d_w = wv;
+    auto predictor = [&](int& its_acc) -> int {
+      OK(rhs(rd, F));
+      OK(momentum_diag(mc, wv, g));
+      OK(jacobi_inverse(NU, g, inv));
+      SolveOut so;
+      OK(gmres(mop, s_mom, inv, F, u_np1, so));
+      its_acc += so.iterations;
+      return DGB_OK;
+    };
+    CK(cudaMemcpyAsync(u_np1, u_n, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    OK(predictor(its[0]));
+    for (int it = 0; it < P.fp_max_iter; ++it) {
+      CK(cudaMemcpyAsync(wv, u_n, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      ++launches;
+      CK(v_axpby(st, NU, 0.5, u_np1, 0.5, wv));
+      CK(cudaMemcpyAsync(fp_prev, u_np1, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      OK(predictor(its[0]));
+      its[8] = it + 1;
+      double inc = 0.0;
+      OK(max_abs_diff(NU, u_np1, fp_prev, &inc));
+      if (inc < P.fp_tol) break;
+    }
+    // increment-form Helmholtz (PAPER.md (14)): (mc M + K) dp = (1/dt) B(u*), dp0 = 0
+    const double pmc = 1.0 / (P.c * P.c * dt * dt);
+    OK(pressure_rhs(1.0 / dt, u_np1, pmc, nullptr, prhs));
+    double* dp = p_g;
+    ++launches;
+    CK(v_fill(st, NP, 0.0, dp));
+    SolveOut so;
+    if (P.pressure_precond == 1) {
+      OK(cg_mg(pmc, s_p, prhs, dp, so));
+    } else {
+      OK(sip_diag(pmc, 0, pinv));
+      OK(jacobi_inverse(NP, pinv, pinv));
+      dgb_operator pop{};
+      pop.op = DGB_OP_PRESSURE;
+      pop.coefs[0] = pmc;
+      OK(cg(pop, s_p, pinv, prhs, dp, so));
+    }
+    its[2] = so.iterations;
+    OK(proj_grad(dp, ut, its[5]));
+    launches += 2;
+    CK(v_axpy(st, NU, -dt, ut, u_np1));
+    CK(cudaMemcpyAsync(p_np1, p_n, NP * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CK(v_axpy(st, NP, 1.0, dp, p_np1));
+    CK(cudaStreamSynchronize(st));
+    return DGB_OK;
+  }
+  if (scheme == DGB_SCHEME_GQ_BDF2) {
+    // BDF2 predictor, advecting field 2u^n - u^{n-1}, skew -1/2, projection with 2/3 dt
+    CK(cudaMemcpyAsync(wv, u_nm1, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    ++launches;
+    CK(v_axpby(st, NU, 2.0, u_n, -1.0, wv));
+    const double mc[4] = {3.0 / (2.0 * dt), 1.0 / Re, 1.0, -0.5};
+    dgb_rhs_desc rd{};
+    rd.n_mass = 2;
+    rd.mass_coef[0] = 2.0 / dt;
+    rd.mass_f[0] = u_n;
+    rd.mass_coef[1] = -1.0 / (2.0 * dt);
+    rd.mass_f[1] = u_nm1;
+    rd.n_pres = 1;
+    rd.pres_coef[0] = 1.0;
+    rd.pres_f[0] = p_n;
+    rd.dir_visc_coef = 1.0 / Re;
+    rd.dir_adv_coef = 1.0;
+    rd.dir_w = wv;
+    OK(stage(0, 2.0 / 3.0, mc, rd, u_n, p_n, u_np1, p_np1));
+    CK(cudaStreamSynchronize(st));
+    return DGB_OK;
+  }
+
   // ---- stage 1
   if (P.first_step)
     CK(cudaMemcpyAsync(wv, u_n, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -1055,7 +1163,6 @@ int Context::trbdf2_step(const dgb_step_params& P, const double* u_nm1, const do
     ++launches;
     CK(v_axpby(st, NU, 1.0 + gm / (2.0 * (1.0 - gm)), u_n, -gm / (2.0 * (1.0 - gm)), wv));
   }
-  const double Re = P.Re, dt = P.dt;
   {
     const double mc[4] = {1.0 / (gm * dt), 1.0 / (2.0 * Re), 0.5, 0.0};
     dgb_rhs_desc rd{};

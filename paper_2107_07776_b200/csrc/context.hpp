@@ -87,6 +87,8 @@ class Context {
   // TR-BDF2 step
   int trbdf2_step(const dgb_step_params& p, const double* u_nm1, const double* u_n, const double* p_n,
                   double* u_np1, double* p_np1, int* its);
+  int projection_step(int scheme, const dgb_step_params& p, const double* u_nm1, const double* u_n,
+                      const double* p_n, double* u_np1, double* p_np1, int* its);
 
   // Dirichlet data
   int set_dirichlet_table(const double* g);

@@ -61,6 +61,7 @@ def lib():
         L.ref_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, _dp, _dp, C.c_double, C.c_double, C.c_int,
                                 C.c_int, C.c_int, _dp, _ip, _dp, _dp, C.c_int, _ip]
         L.ref_trbdf2_step.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _dp, _ip]
+        L.ref_scheme_step.argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _ip]
         L.ref_faces.argtypes = [C.c_void_p, _ip, _dp, _ip, _dp]
         L.ref_cell_vertices.argtypes = [C.c_void_p, _dp]
         L.ref_bface_points.argtypes = [C.c_void_p, C.c_int, _dp]
@@ -213,6 +214,18 @@ class RefCtx:
             prm = np.concatenate([prm, [0.0, 1e-8, 100.0][len(prm) - 10:]])
         its = (C.c_int * 10)()
         if lib().ref_trbdf2_step(self.h, P(prm), P(u_nm1), P(u_n), P(p_n), P(u1), P(p1), its):
+            raise RuntimeError(lib().ref_last_error().decode())
+        return u1, p1, list(its)
+
+    def scheme_step(self, scheme, params, u_nm1, u_n, p_n):
+        """scheme 1 = BCG, 2 = GQ-BDF2 (oracle/trbdf2_cpu.hpp); params as step()."""
+        prm = np.ascontiguousarray(params, dtype=np.float64)
+        if len(prm) < 13:
+            prm = np.concatenate([prm, [0.0, 1e-8, 100.0][len(prm) - 10:]])
+        u1 = np.zeros(self.n_u)
+        p1 = np.zeros(self.n_p)
+        its = (C.c_int * 10)()
+        if lib().ref_scheme_step(self.h, scheme, P(prm), P(u_nm1), P(u_n), P(p_n), P(u1), P(p1), its):
             raise RuntimeError(lib().ref_last_error().decode())
         return u1, p1, list(its)
 
