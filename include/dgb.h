@@ -141,6 +141,15 @@ int dgb_pressure_rhs(dgb_ctx* ctx, double inv_adt, const double* d_u, double mas
 int dgb_pressure_gradient(dgb_ctx* ctx, const double* d_p, double* d_out);
 /* replaces kinetic_energy (forms.hpp:168-170, forms.cpp:1239-1260) */
 int dgb_kinetic_energy(dgb_ctx* ctx, const double* d_u, double* result);
+/* On-device diagnostics: */
+/* L2 norm sqrt(x^T M x) of a field of the velocity (space 0) or pressure (space 1) space. */
+int dgb_l2_norm(dgb_ctx* ctx, int space, const double* d_x, double* result);
+/* check_steady: *steady = max |u_new - u_old| < tol; *diff = that max. */
+int dgb_check_steady(dgb_ctx* ctx, const double* d_u_new, const double* d_u_old, double tol, int* steady,
+                     double* diff);
+/* compute_stability_params: C = k U dt / H, mu = k^2 dt / (Re H^2),
+ * H = min cell diameter (GeometryCache::min_diam, space.hpp:64), k = velocity degree. */
+int dgb_stability_params(dgb_ctx* ctx, double dt, double Re, double U, double* C, double* mu);
 
 /* ------------------------------------------------------------------ vector kernels */
 /* kern::axpy/axpby/scal/dot/max_abs_diff (kernels.hpp:34-43) on device vectors */

@@ -139,6 +139,9 @@ def lib() -> C.CDLL:
     L.dgb_pressure_mg_vcycle.argtypes = [C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
     L.dgb_projection_step.argtypes = [C.c_void_p, C.c_int, C.POINTER(_StepParams), C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p, _ip]
+    L.dgb_l2_norm.argtypes = [C.c_void_p, C.c_int, C.c_void_p, _dp]
+    L.dgb_check_steady.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, _ip, _dp]
+    L.dgb_stability_params.argtypes = [C.c_void_p, C.c_double, C.c_double, C.c_double, _dp, _dp]
     L.dgb_seeded_uniform.argtypes = [C.c_ulonglong, C.c_size_t, C.c_double, C.c_double, _dp]
     L.dgb_synth_init.argtypes = [C.c_int, C.c_ulonglong, C.c_double, _dp]
     L.dgb_synth_eval.argtypes = [_dp, C.c_double, _dp, C.c_void_p]
@@ -412,6 +415,27 @@ def kinetic_energy(V: DGContext, u) -> float:
     r = C.c_double()
     _check(lib().dgb_kinetic_energy(V.handle, _ptr(u), C.byref(r)))
     return r.value
+
+
+def l2_norm(V: DGContext, x, space: int = SPACE_U) -> float:
+    """sqrt(x^T M x) on the device (diagnostics)."""
+    r = C.c_double()
+    _check(lib().dgb_l2_norm(V.handle, space, _ptr(x), C.byref(r)))
+    return r.value
+
+
+def check_steady(V: DGContext, u_new, u_old, tol: float):
+    """(max |u_new - u_old| < tol, that max), computed on the device."""
+    st, d = C.c_int(), C.c_double()
+    _check(lib().dgb_check_steady(V.handle, _ptr(u_new), _ptr(u_old), tol, C.byref(st), C.byref(d)))
+    return bool(st.value), d.value
+
+
+def stability_params(V: DGContext, dt: float, Re: float, U: float):
+    """(C, mu) = (k U dt / H, k^2 dt / (Re H^2)), H = min cell diameter."""
+    c, mu = C.c_double(), C.c_double()
+    _check(lib().dgb_stability_params(V.handle, dt, Re, U, C.byref(c), C.byref(mu)))
+    return c.value, mu.value
 
 
 # ---------------------------------------------------------------------------

@@ -3,6 +3,7 @@
 // context; exceptions never cross the boundary (status codes + last error).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -267,6 +268,37 @@ int dgb_pressure_gradient(dgb_ctx* h, const double* p, double* out) {
 int dgb_kinetic_energy(dgb_ctx* h, const double* u, double* result) {
   NEED(h && u && result, "null argument");
   return ret(h, h->c.kinetic(u, result));
+}
+
+int dgb_l2_norm(dgb_ctx* h, int space, const double* x, double* result) {
+  NEED(h && x && result, "null argument");
+  NEED(space == DGB_SPACE_U || space == DGB_SPACE_P, "space must be 0 or 1");
+  dgb::Context& c = h->c;
+  const size_t n = space == DGB_SPACE_U ? c.nu() : c.np();
+  double* mx = c.scratch_vec(19, n);
+  NEED(mx, "out of device memory");
+  int code = c.mass(space, x, mx);
+  if (code == DGB_OK) code = c.dot(n, x, mx, result);
+  if (code == DGB_OK) *result = std::sqrt(std::max(*result, 0.0));
+  return ret(h, code);
+}
+int dgb_check_steady(dgb_ctx* h, const double* un, const double* uo, double tol, int* steady, double* diff) {
+  NEED(h && un && uo && steady && diff, "null argument");
+  const int code = h->c.max_abs_diff(h->c.nu(), un, uo, diff);
+  *steady = code == DGB_OK && *diff < tol;
+  return ret(h, code);
+}
+int dgb_stability_params(dgb_ctx* h, double dt, double Re, double U, double* C, double* mu) {
+  NEED(h && C && mu, "null argument");
+  NEED(Re > 0.0, "Re must be positive");
+  const auto& d = h->c.mesh.cell_diam;
+  double H = d.empty() ? 0.0 : d[0];
+  for (double v : d) H = std::min(H, v);
+  NEED(H > 0.0, "empty mesh");
+  const double k = h->c.ku;
+  *C = k * U * dt / H;
+  *mu = k * k * dt / (Re * H * H);
+  return DGB_OK;
 }
 
 // ------------------------------------------------------------------ vectors

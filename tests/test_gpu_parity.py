@@ -572,3 +572,27 @@ def test_baseline_schemes_match_oracle(ref, gpu, scheme_name, dim, n_el, ku, kp,
     hu, hp = host(du), host(dp)
     assert rel(hu, u) <= TOL_FIELD
     assert rel(hp - hp.mean(), p - p.mean()) <= TOL_FIELD or rel(hp, p) <= TOL_FIELD
+
+
+def test_diagnostics(ref, gpu):
+    """On-device diagnostics: L2 norms against the reference's kinetic
+    energy (forms.cpp:1239-1260) and its mass apply, check_steady, stability parameters
+    (cfg5's dt gives C = 0.5 by construction)."""
+    R, D = pair(ref, gpu, 3, 3, 2, 1, 0.0)  # Cartesian: the mass and kinetic-energy rules are both exact
+    u = gpu.seeded_uniform(61, R.n_u)
+    p = gpu.seeded_uniform(62, R.n_p)
+    nu = gpu.l2_norm(D, dev(u))
+    assert abs(nu * nu - 2.0 * R.kinetic_energy(u)) <= 1e-12 * nu * nu
+    mp = R.mass(gpu.SPACE_P, p)
+    npn = gpu.l2_norm(D, dev(p), gpu.SPACE_P)
+    assert abs(npn * npn - float(p @ mp)) <= 1e-12 * npn * npn
+    du, du2 = dev(u), dev(u)
+    du2[5] += 1e-6
+    assert gpu.check_steady(D, du, du, 1e-7) == (True, 0.0)
+    steady, d = gpu.check_steady(D, du2, du, 1e-7)
+    assert not steady and abs(d - 1e-6) < 1e-12
+    D5 = gpu.DGContext(3, 8, 2, 1)
+    c, mu = gpu.stability_params(D5, 0.5 * (3 ** 0.5 / 8) / 2.0, 1600.0, 1.0)
+    assert abs(c - 0.5) < 1e-12
+    H = 3 ** 0.5 / 8
+    assert abs(mu - 4 * (0.5 * H / 2.0) / (1600.0 * H * H)) < 1e-12
