@@ -540,4 +540,8 @@ extern "C" int dgb_set_fast_path(dgb_ctx* h, int enable) {
   h->c.use_fast = enable != 0;
   return DGB_OK;
 }
-extern "C" int dgb_fast_path_active(dgb_ctx* h) { return h && h->c.use_fast && h->c.dc.axis ? 1 : 0; }
+// 1: axis-aligned fast kernels (fast_axis.cuh), 2: deformed 3D fast kernels (fast_deformed.cuh), 0: generic
+extern "C" int dgb_fast_path_active(dgb_ctx* h) {
+  if (!h || !h->c.use_fast || h->c.dim != 3) return 0;
+  return h->c.dc.axis ? 1 : (!h->c.dc.affine ? 2 : 0);
+}
