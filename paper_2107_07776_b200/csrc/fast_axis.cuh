@@ -555,14 +555,22 @@ struct MomAxisCfg {
   // quadrature-plane stride of the YB / T tensors, odd so that per-layer items
   // (one plane each) start on different banks
   static constexpr int QQP = QQ | 1;
-  static constexpr int B_R1 = 0;            // TZ/TY/TX [comp][test][l][qxy] (9 QQP N)
-  static constexpr int B_R2 = 9 * QQP * N;  // YB [field][k][qxy] (6 QQP N)
+  // TZ/TY/TX [comp (stride BRC)][test][l][qxy]; K = 2 pads the component stride so S78's
+  // (comp, l) items hit distinct banks (153 = 9 mod 16 collides comp 0 / 2; 154 does not)
+  static constexpr int BRC = 3 * QQP * N + (K == 2 ? 1 : 0);
+  static constexpr int B_R1 = 0;
+  static constexpr int B_R2 = 3 * BRC;  // YB [field][k][qxy] (6 QQP N)
   static constexpr int B_END = B_R2 + 6 * QQP * N;
   // face phase (all 6 faces at once): V1 [8 fields][6][Q x N] -> FB [3][6][N x N];  FL [3][6][Q x N]
   // V1 [field][q][f][qp]: face-Gauss-point rows of all 6 faces contiguous (F2 reads them
   // conflict-free); the q-block stride VB is chosen so F1's (f, q) writes hit distinct banks
-  static constexpr int VB = K == 3 ? 36 : (K == 2 ? 33 : 6 * Q), V1_SIZE = 8 * N * VB;
-  static constexpr int F_V1 = 0, F_FL = V1_SIZE, F_END = F_FL + 18 * QN;
+  // V1F: face stride inside a V1 row (K = 2: 5 instead of Q = 4 with VB = 39 takes F1's
+  // store conflicts from 32 to 24 excess wavefronts per cell at the price of 8 in F2);
+  // FLC: component stride of FL (K = 2: 6 QN + 1 takes F3's read conflicts from 36 to 12)
+  static constexpr int VB = K == 3 ? 36 : (K == 2 ? 39 : 6 * Q), V1_SIZE = 8 * N * VB;
+  static constexpr int V1F = K == 2 ? 5 : Q;
+  static constexpr int FLC = 6 * QN + (K == 2 ? 1 : 0);
+  static constexpr int F_V1 = 0, F_FL = V1_SIZE, F_END = F_FL + 2 * FLC + 6 * QN;
   // neighbour face traces [f (stride NBS)][x0, x1, x2, w_normal][p + N q], filled during S0 /
   // pass A and read by F1; disjoint from the pass-A regions and from V1
   static constexpr int NBS = 4 * NF + 1;
@@ -875,7 +883,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         for (int comp = 0; comp < 3; ++comp) v[comp][p] = CELL(c)[G::O_X + comp * CT + li];
         v[6][p] = CELL(c)[G::O_W + a * CT + li];
       }
-      double* o = WK(c) + G::F_V1 + q * G::VB + f * Q;
+      double* o = WK(c) + G::F_V1 + q * G::VB + f * G::V1F;
 #pragma unroll
       for (int fl = 0; fl < 8; ++fl)
 #pragma unroll
@@ -893,7 +901,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
       const int f = r / Q, qp = r - f * Q;
       const int a = f >> 1, s = f & 1;
       const CellInfo& ci = INFO(c);
-      const double* in = WK(c) + G::F_V1 + f * Q + qp;
+      const double* in = WK(c) + G::F_V1 + f * G::V1F + qp;
       double v[8][N];
 #pragma unroll
       for (int fl = 0; fl < 8; ++fl)
@@ -940,7 +948,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
 #pragma unroll
       for (int comp = 0; comp < 3; ++comp)
 #pragma unroll
-        for (int l = 0; l < N; ++l) o[comp * 6 * QN + Q * l] = out[comp][l];
+        for (int l = 0; l < N; ++l) o[comp * G::FLC + Q * l] = out[comp][l];
     }
     SYNC_CELL();
     // F3: B^T along p, added straight into OUT at the face nodes; one axis at a time so
@@ -951,7 +959,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         const int c = CELLOF(idx, 6 * N), r = RESTOF(idx, c, 6 * N);
         const int cs = r / N, q = r - cs * N;  // cs = comp * 2 + side
         const int comp = cs >> 1, f = 2 * a + (cs & 1);
-        const double* in = WK(c) + G::F_FL + (comp * 6 + f) * QN + Q * q;
+        const double* in = WK(c) + G::F_FL + comp * G::FLC + f * QN + Q * q;
         double v[Q];
 #pragma unroll
         for (int qp = 0; qp < Q; ++qp) v[qp] = in[qp];
@@ -1051,7 +1059,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
           tx[l] = fma(tq.B[qz][l], rx, tx[l]);
         }
       }
-      double* o = WK(c) + G::B_R1 + comp * 3 * G::QQP * N + qxy;
+      double* o = WK(c) + G::B_R1 + comp * G::BRC + qxy;
 #pragma unroll
       for (int l = 0; l < N; ++l) {
         o[G::QQP * l] = tz[l];
@@ -1069,7 +1077,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
     const int c = CELLOF(idx, 3 * N * JH), r = RESTOF(idx, c, 3 * N * JH);
     const int comp = r / (N * JH), r2 = r - comp * N * JH;
     const int l = r2 / JH, j0 = (r2 - l * JH) * NJ;
-    const double* tp = WK(c) + G::B_R1 + comp * 3 * G::QQP * N + G::QQP * l;
+    const double* tp = WK(c) + G::B_R1 + comp * G::BRC + G::QQP * l;
     double acc[NJ][N];  // [j - j0][i]
 #pragma unroll
     for (int j = 0; j < NJ; ++j)
