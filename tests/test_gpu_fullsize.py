@@ -111,3 +111,21 @@ def test_full_trbdf2_step_fast_vs_generic(gpu, n_el, ku, seed, Re, restart):
     assert all(abs(a - b) <= 1 for a, b in zip(res[True][0], res[False][0])), (res[True][0], res[False][0])
     assert rel(res[True][1], res[False][1]) <= 1e-9
     assert rel(res[True][2], res[False][2]) <= 1e-9
+
+
+@pytest.mark.parametrize("n_el,ku,amp", [(64, 3, 0.0), (48, 4, 0.1 / 48)])
+def test_multigrid_pressure_solve_at_full_size(gpu, n_el, ku, amp):
+    """cfg3 / cfg4 sizes: the multigrid-preconditioned pressure CG returns the Jacobi-CG
+    (reference-algorithm) solution to the solver tolerance in a handful of iterations."""
+    import torch
+    D = gpu.DGContext(3, n_el, ku, ku - 1, amp, 3) if amp else gpu.DGContext(3, n_el, ku, ku - 1)
+    mc = 1.0 / (1e6 * G * G * 1e-6)
+    b = torch.from_numpy(gpu.seeded_uniform(77, D.n_p)).cuda()
+    s = gpu.SolverSettings(rel_tol=1e-10, max_iter=20000)
+    d = D.zeros(gpu.SPACE_P)
+    gpu.helmholtz_diagonal(D, mc, d)
+    xj, xm = D.zeros(gpu.SPACE_P), D.zeros(gpu.SPACE_P)
+    rj = gpu.cg_solve(D, gpu.LinearOperator.pressure_helmholtz(mc), b, s, gpu.JacobiPreconditioner(D, d), xj)
+    rm = gpu.pressure_cg_mg(D, mc, b, s, xm)
+    assert rel(xm, xj) <= 1e-7, (rm, rj)
+    assert rm.iterations <= 20 and rj.iterations > 20 * rm.iterations, (rm, rj)
