@@ -169,9 +169,16 @@ __global__ void k_cg_pq_part(size_t n, const double* __restrict__ p, const doubl
   block_reduce_store<1>(acc, partial);
   if (last_block_arrival(&st->cnt_pq)) cg_alpha_finish(gridDim.x, partial, st);
 }
-__global__ void k_cg_alpha_final(int nparts, const double* __restrict__ partial, CgState* st) {
+// two-level: each block sums a contiguous slice of the fused apply's partials into
+// partial[nparts + block]; the last block to arrive sums those and forms alpha
+constexpr int kAlphaBlocks = 64;
+__global__ void __launch_bounds__(256) k_cg_alpha_final(int nparts, double* __restrict__ partial, CgState* st) {
   if (st->done) return;
-  cg_alpha_finish(nparts, partial, st);
+  const int per = (nparts + gridDim.x - 1) / gridDim.x;
+  const int b0 = blockIdx.x * per, n = max(0, min(per, nparts - b0));
+  const double s = block_sum_l2(n, partial + b0);
+  if (threadIdx.x == 0) partial[nparts + blockIdx.x] = s;
+  if (last_block_arrival(&st->cnt_pq)) cg_alpha_finish(gridDim.x, partial + nparts, st);
 }
 __device__ __forceinline__ void cg_upd_finish(int nparts, const double* partial, CgState* st, double* hist);
 __global__ void k_cg_upd_part(size_t n, const double* __restrict__ p, const double* __restrict__ q,
@@ -376,7 +383,7 @@ cudaError_t cg_alpha(cudaStream_t s, size_t n, const double* p, const double* q,
   return cudaGetLastError();
 }
 cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, const double* partial, CgState* st) {
-  k_cg_alpha_final<<<1, kBlasThreads, 0, s>>>(nparts, partial, st);
+  k_cg_alpha_final<<<kAlphaBlocks, 256, 0, s>>>(nparts, const_cast<double*>(partial), st);
   return cudaGetLastError();
 }
 cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q, double* x, double* r,

@@ -92,8 +92,19 @@ __device__ __forceinline__ bool last_block_arrival(unsigned* cnt) {
 // sum of partial[0..nparts) by the whole block, fixed order; L2 loads (written by other SMs)
 __device__ __forceinline__ double block_sum_l2(int nparts, const double* partial) {
   __shared__ double red2[32];
-  double a = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += blockDim.x) a += __ldcg(partial + i);
+  // four independent accumulators: four loads in flight per thread per step (the partial
+  // arrays of the fused CG apply hold ~10^5 entries)
+  const int st = blockDim.x;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  int i = threadIdx.x;
+  for (; i + 3 * st < nparts; i += 4 * st) {
+    a0 += __ldcg(partial + i);
+    a1 += __ldcg(partial + i + st);
+    a2 += __ldcg(partial + i + 2 * st);
+    a3 += __ldcg(partial + i + 3 * st);
+  }
+  for (; i < nparts; i += st) a0 += __ldcg(partial + i);
+  double a = (a0 + a1) + (a2 + a3);
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
   if ((threadIdx.x & 31) == 0) red2[threadIdx.x >> 5] = a;
   __syncthreads();

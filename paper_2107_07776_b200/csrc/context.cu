@@ -641,7 +641,7 @@ int Context::cg(const dgb_operator& op, const dgb_solver_settings& s, const doub
     const bool fused = use_fast && dc.axis && (op.op == DGB_OP_PRESSURE || op.op == DGB_OP_LAPLACE) &&
                        fast_sip3_cg_blocks(dc) > 0;
     const int fblocks = fused ? fast_sip3_cg_blocks(dc) : 0;
-    double* fpart = fused ? scratch_vec(25, fblocks) : nullptr;
+    double* fpart = fused ? scratch_vec(25, fblocks + 64) : nullptr;  // + the second-level partials
     if (fused && !fpart) return fail(DGB_E_CUDA, "cg: out of device memory");
     auto enqueue = [&](int slot) -> int {
       for (int b = 0; b < batch; ++b) {

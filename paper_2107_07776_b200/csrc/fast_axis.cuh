@@ -357,9 +357,9 @@ struct SipAxisCfg {
 };
 
 // CGF: the CG apply q = A p with <p, q> fused into the epilogue (krylov.cpp:84-87):
-// partial[block] = sum over the block's DoFs of p q (alpha: cg_alpha_from_partials;
-// a last-block finish here was slower — one block summing ~16k partials at the tail).
-static_assert(SipAxisCfg<1>::T <= 256 && SipAxisCfg<2>::T <= 256 && SipAxisCfg<3>::T <= 256, "CG reduction buffer");
+// partial[block * warps + warp] = sum over the warp's DoFs of p q (alpha:
+// cg_alpha_from_partials; a last-block finish here was slower — one block summing ~16k
+// partials at the tail).
 struct SipCgArgs {
   double* partial = nullptr;
   CgState* st = nullptr;
@@ -513,17 +513,11 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
       if (CGF) pq[0] = fma(CELL(c)[G::O_U + b0 + k * P::PY], s, pq[0]);
     }
   }
-  if (CGF) {  // deterministic block sum for any blockDim (<= 256): lanes of warp 0 stride, then shuffle
-    __shared__ double red[256];
-    red[tid] = pq[0];
-    __syncthreads();
-    if (tid < 32) {
-      double a = 0.0;
-      for (int i = tid; i < TT; i += 32) a += red[i];
+  if (CGF) {  // one deterministic partial per warp (shuffle tree), no CTA barrier at the tail
+    double a = pq[0];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-      if (tid == 0) cg.partial[blockIdx.x] = a;
-    }
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((tid & 31) == 0) cg.partial[blockIdx.x * (TT / 32) + (tid >> 5)] = a;
   }
 #undef CELL
 #undef INFO

@@ -211,9 +211,9 @@ cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, doub
 
 int fast_sip3_cg_blocks(const DevCtx& c) {
   switch (c.kp) {
-    case 1: return (c.ncells + SipAxisCfg<1>::C - 1) / SipAxisCfg<1>::C;
-    case 2: return (c.ncells + SipAxisCfg<2>::C - 1) / SipAxisCfg<2>::C;
-    case 3: return (c.ncells + SipAxisCfg<3>::C - 1) / SipAxisCfg<3>::C;
+    case 1: return (c.ncells + SipAxisCfg<1>::C - 1) / SipAxisCfg<1>::C * (SipAxisCfg<1>::T / 32);
+    case 2: return (c.ncells + SipAxisCfg<2>::C - 1) / SipAxisCfg<2>::C * (SipAxisCfg<2>::T / 32);
+    case 3: return (c.ncells + SipAxisCfg<3>::C - 1) / SipAxisCfg<3>::C * (SipAxisCfg<3>::T / 32);
   }
   return 0;
 }
