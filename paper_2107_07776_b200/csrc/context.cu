@@ -41,6 +41,7 @@ void* Context::dalloc(size_t bytes) {
 
 Context::~Context() {
   mg_release(mg_);
+  if (cap_stream_) cudaStreamDestroy(cap_stream_);
   if (device >= 0) cudaSetDevice(device);
   if (dc.stream) cudaStreamSynchronize(dc.stream);
   for (void* p : allocs_) cudaFree(p);
@@ -643,7 +644,8 @@ int Context::cg(const dgb_operator& op, const dgb_solver_settings& s, const doub
     const int fblocks = fused ? fast_sip3_cg_blocks(dc) : 0;
     double* fpart = fused ? scratch_vec(25, fblocks + 64) : nullptr;  // + the second-level partials
     if (fused && !fpart) return fail(DGB_E_CUDA, "cg: out of device memory");
-    auto enqueue = [&](int slot) -> int {
+    // one batch of `batch` iterations (kernel launches only)
+    auto batch_kernels = [&](cudaStream_t st) -> int {
       for (int b = 0; b < batch; ++b) {
         if (fused) {
           launches += 4;
@@ -660,6 +662,58 @@ int Context::cg(const dgb_operator& op, const dgb_solver_settings& s, const doub
         OK(apply_op(op, p, q));
         CK(cg_alpha(st, n, p, q, d_partial_, d_cg_));
         CK(cg_update(st, n, p, q, x, r, inv, z, d_partial_, d_cg_, d_hist_));
+      }
+      return DGB_OK;
+    };
+    // The batch is captured once per solve into a CUDA graph and replayed: every kernel
+    // argument (vectors, the device-resident scalars, the skip flag) is fixed for the whole
+    // solve, and on small meshes (cfg1 / cfg2) the iteration is launch-bound.
+    // DGB_NO_GRAPH=1 launches the kernels directly.
+    static const bool no_graph = std::getenv("DGB_NO_GRAPH") != nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    long long graph_launches = 0;
+    if (!no_graph) {
+      const long long l0 = launches;
+      cudaGraph_t graph = nullptr;
+      // captured on a private stream (the context stream may be the legacy default stream,
+      // which cannot be captured); the graph is then launched on the context stream
+      if (!cap_stream_) cudaStreamCreateWithFlags(&cap_stream_, cudaStreamNonBlocking);
+      const cudaError_t cb = cap_stream_ ? cudaStreamBeginCapture(cap_stream_, cudaStreamCaptureModeRelaxed)
+                                         : cudaErrorInvalidResourceHandle;
+      int crc = -1;
+      cudaError_t ce = cudaErrorUnknown, ci = cudaErrorUnknown;
+      if (cb == cudaSuccess) {
+        const cudaStream_t own = dc.stream;
+        dc.stream = cap_stream_;  // operator launches inside apply_op go to the capture
+        crc = batch_kernels(cap_stream_);
+        dc.stream = own;
+        ce = cudaStreamEndCapture(cap_stream_, &graph);
+        if (crc == DGB_OK && ce == cudaSuccess && graph) {
+          ci = cudaGraphInstantiate(&gexec, graph, 0);
+          if (ci != cudaSuccess) gexec = nullptr;
+        }
+        if (graph) cudaGraphDestroy(graph);
+      }
+      cudaGetLastError();  // a failed capture falls back to direct launches
+      if (std::getenv("DGB_GRAPH_DEBUG"))
+        std::fprintf(stderr, "[dgb cg] graph %s (begin %s, batch %d %s, end %s, inst %s)\n",
+                     gexec ? "captured" : "FAILED", cudaGetErrorString(cb), crc, crc ? err.c_str() : "",
+                     cudaGetErrorString(ce), cudaGetErrorString(ci));
+      graph_launches = launches - l0;
+      launches = l0;
+    }
+    struct GraphGuard {
+      cudaGraphExec_t& g;
+      ~GraphGuard() {
+        if (g) cudaGraphExecDestroy(g);
+      }
+    } gguard{gexec};
+    auto enqueue = [&](int slot) -> int {
+      if (gexec) {
+        launches += graph_launches;
+        CK(cudaGraphLaunch(gexec, st));
+      } else {
+        OK(batch_kernels(st));
       }
       CK(cudaMemcpyAsync(&h_cg_[slot], d_cg_, sizeof(CgState), cudaMemcpyDeviceToHost, st));
       CK(cudaEventRecord(poll_ev_[slot], st));

@@ -127,6 +127,7 @@ class Context {
   // host-buffer pipeline: two copy streams + per-slab events
   static constexpr int kMaxSlabs = 32;
   cudaStream_t cp_in_ = nullptr, cp_out_ = nullptr;
+  cudaStream_t cap_stream_ = nullptr;  // CUDA-graph capture of the CG batches
   cudaEvent_t ev_start_ = nullptr, ev_in_[kMaxSlabs] = {}, ev_k_[kMaxSlabs] = {};
   size_t gm_n_ = 0;
   int ensure_geometry();
