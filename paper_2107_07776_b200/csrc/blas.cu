@@ -382,8 +382,8 @@ cudaError_t cg_alpha(cudaStream_t s, size_t n, const double* p, const double* q,
   k_cg_pq_part<<<g, kBlasThreads, 0, s>>>(n, p, q, scratch, st);  // last block computes alpha
   return cudaGetLastError();
 }
-cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, const double* partial, CgState* st) {
-  k_cg_alpha_final<<<kAlphaBlocks, 256, 0, s>>>(nparts, const_cast<double*>(partial), st);
+cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, double* partial, CgState* st) {
+  k_cg_alpha_final<<<kAlphaBlocks, 256, 0, s>>>(nparts, partial, st);
   return cudaGetLastError();
 }
 cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q, double* x, double* r,

@@ -141,7 +141,7 @@ cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q
                       const double* inv, double* z, double* scratch, CgState* st, double* hist);
 // MGS step with the projection read from device memory: w -= (*h) v_i ; *out = <w, v_next>
 // alpha = rho / sum(partial[0..nparts))  (CG with the <p,q> partials from a fused apply)
-cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, const double* partial, CgState* st);
+cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, double* partial, CgState* st);
 
 // ---- one-reduce modified Gram-Schmidt for GMRES (krylov.cpp:140-160 restated).
 // The basis is stored unnormalised, v_j = s_j U_j.  MGS's projections follow

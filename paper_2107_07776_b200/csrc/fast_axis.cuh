@@ -358,8 +358,8 @@ struct SipAxisCfg {
 
 // CGF: the CG apply q = A p with <p, q> fused into the epilogue (krylov.cpp:84-87):
 // partial[block * warps + warp] = sum over the warp's DoFs of p q (alpha:
-// cg_alpha_from_partials; a last-block finish here was slower — one block summing ~16k
-// partials at the tail).
+// cg_alpha_from_partials, a two-level reduction; a single-block finish at the tail of this
+// kernel was slower).
 struct SipCgArgs {
   double* partial = nullptr;
   CgState* st = nullptr;
