@@ -327,6 +327,18 @@ def test_trbdf2_step_cfg1(ref, gpu):
     _step_case(ref, gpu, 2, 32, 2, 1, Re=100.0, dt=1e-3, seed=0, steps=1)
 
 
+def test_trbdf2_cfg1_ten_steps(ref, gpu):
+    """BASELINE configs[0] over 10 consecutive steps (second-order extrapolation from step 1
+    on): per-solve iteration counts within +-1 and end-of-run fields <= 1e-9 (no drift)."""
+    _step_case(ref, gpu, 2, 32, 2, 1, Re=100.0, dt=1e-3, seed=0, steps=10)
+
+
+def test_trbdf2_q3q2_3d_two_steps(ref, gpu):
+    """cfg3's degrees (Q3/Q2), Re 1000, GMRES restart 30, on a 4^3 mesh: the axis-aligned
+    fast kernels inside two full device steps vs the restated reference driver."""
+    _step_case(ref, gpu, 3, 4, 3, 2, Re=1000.0, dt=1e-3, seed=2, steps=2, restart=30)
+
+
 def test_trbdf2_step_3d_small(ref, gpu):
     _step_case(ref, gpu, 3, 3, 2, 1, Re=100.0, dt=1e-3, seed=1, steps=1)
 
