@@ -339,6 +339,12 @@ def test_trbdf2_q3q2_3d_two_steps(ref, gpu):
     _step_case(ref, gpu, 3, 4, 3, 2, Re=1000.0, dt=1e-3, seed=2, steps=2, restart=30)
 
 
+def test_trbdf2_deformed_q4q3_step(ref, gpu):
+    """cfg4's degrees (Q4/Q3) on a distorted 3^3 mesh: the deformed fast kernels
+    (k_momentum_qp / k_sip_qp) inside two full device steps vs the restated driver."""
+    _step_case(ref, gpu, 3, 3, 4, 3, Re=100.0, dt=1e-3, seed=3, steps=2, amp=0.03)
+
+
 def test_trbdf2_step_3d_small(ref, gpu):
     _step_case(ref, gpu, 3, 3, 2, 1, Re=100.0, dt=1e-3, seed=1, steps=1)
 
