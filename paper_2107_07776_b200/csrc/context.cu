@@ -338,12 +338,13 @@ int Context::momentum_diag(const double* coefs, const double* w, double* d) {
   if ((co.adv != 0.0 || co.skew != 0.0) && !w)
     return fail(DGB_E_MISSING_FIELD, "momentum_diagonal: advecting field missing");
   ++launches;
-  if (use_fast && dc.axis) {
-    const cudaError_t e = fast_momentum_diag3(dc, co, w, d);
+  if (use_fast && (dc.axis || !dc.affine)) {
+    const cudaError_t e = dc.axis ? fast_momentum_diag3(dc, co, w, d) : fast_momentum_diag3_qp(dc, co, w, d);
     if (e != cudaErrorNotSupported) {
       CK(e);
       return DGB_OK;
     }
+    cudaGetLastError();
   }
   CK(opu->momentum_diag(dc, co, w, d));
   return DGB_OK;

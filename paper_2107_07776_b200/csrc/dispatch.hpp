@@ -105,6 +105,7 @@ cudaError_t fast_sip3_qp(const DevCtx& c, double mc, int dir, const double* x, d
 cudaError_t fast_momentum3(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);
 cudaError_t fast_momentum3_qp(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);
 cudaError_t fast_momentum_diag3(const DevCtx& c, MomCoef co, const double* w, double* y);
+cudaError_t fast_momentum_diag3_qp(const DevCtx& c, MomCoef co, const double* w, double* y);
 cudaError_t fast_divergence3(const DevCtx& c, const double* u, double* y);
 cudaError_t fast_sip_diag3(const DevCtx& c, double mc, int dir, double* y);
 struct CgState;

@@ -339,6 +339,31 @@ static cudaError_t run_momentum_qp(const DevCtx& c, MomCoef co, const double* w,
   k_momentum_qp<K><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, gcA, gfA, gadv, gfw, co, x, w ? w : x, y);
   return cudaGetLastError();
 }
+template <int K>
+static cudaError_t run_momentum_diag_qp(const DevCtx& c, MomCoef co, const double* w, double* y) {
+  cudaError_t e = ensure_ftab<K + 1, K + 1>();
+  if (e == cudaSuccess) e = ensure_ftab<K + 1, K + 2>();
+  if (e != cudaSuccess) return e;
+  using G = MomDiagQpCfg<K>;
+  const double *gcA = c.qcm[K + 1], *gfA = c.qfn[K + 1], *gadv = c.qadv[K + 2], *gfw = c.qfw[K + 2];
+  if (!gcA || !gfA || !gadv || !gfw) return cudaErrorNotSupported;
+  if ((e = set_smem(k_momentum_diag_qp<K>, G::SMEM)) != cudaSuccess) return e;
+  const int grid = (c.ncells + G::C - 1) / G::C;
+  k_momentum_diag_qp<K><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, gcA, gfA, gadv, gfw, co, w, y);
+  return cudaGetLastError();
+}
+// deformed 3D meshes: the exact momentum diagonal, sum-factorised (fast_deformed.cuh)
+cudaError_t fast_momentum_diag3_qp(const DevCtx& c, MomCoef co, const double* w, double* y) {
+  if (c.dim != 3 || c.affine || co.skew != 0.0 || (co.adv != 0.0 && w == nullptr)) return cudaErrorNotSupported;
+  switch (c.ku) {
+    case 1: return run_momentum_diag_qp<1>(c, co, w, y);
+    case 2: return run_momentum_diag_qp<2>(c, co, w, y);
+    case 3: return run_momentum_diag_qp<3>(c, co, w, y);
+    case 4: return run_momentum_diag_qp<4>(c, co, w, y);
+  }
+  return cudaErrorNotSupported;
+}
+
 // deformed (non-affine) 3D meshes: pass A + LF advection with per-qp geometry (fast_deformed.cuh)
 cudaError_t fast_momentum3_qp(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y) {
   if (c.dim != 3 || c.affine || co.skew != 0.0 || (co.adv != 0.0 && w == nullptr)) return cudaErrorNotSupported;

@@ -469,6 +469,164 @@ __global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const do
   for (int i = lane; i < NB; i += 32) y[(size_t)cid * NB + i] = OUT[i];
 }
 
+// The advecting field's component-independent factors of the deformed momentum operator
+// (apply and diagonal): W1 -> WT[a][q] = -adv (detJ w Jinv w)_a at the rule-B cell points,
+// W2 -> FC = the Lax-Friedrichs weights a_s [6][Q^2] and a_o [6][Q^2] at the rule-B face
+// points (forms.cpp:509-530, :555-573, :592-599).  WS: the cell's staged advecting field
+// (3 components); W: work area (offsets BXO, BYO, FPWO, NWO); one warp per cell.
+template <int N, int QB, int BXO, int BYO, int FPWO, int NWO>
+__device__ __forceinline__ void qp_w_phase(const double* WS, double* W, double* WT, double* FC, const double* nbv,
+                                           const double* tyv, const double* __restrict__ w,
+                                           const double* __restrict__ gadv_c, const double* __restrict__ gfw_c,
+                                           double adv, int lane) {
+  constexpr int NB = N * N * N, NF = N * N, NQB = QB * QB * QB, NQFB = QB * QB;
+  const FTab<N, QB>& tb = c_ft<N, QB>;
+    // the neighbours' advecting-field face layers -> NW (waited for before W2)
+    for (int i = lane; i < 6 * 3 * NF; i += 32) {
+      const int f = i / (3 * NF), r = i - f * 3 * NF, d = r / NF, tn = r - d * NF;
+      const int nb = (int)nbv[f];
+      if (nb < 0) continue;
+      int sl, sp, sq;
+      face_strides<N>(f >> 1, sl, sp, sq);
+      cp_async8(W + NWO + i, w + (size_t)nb * 3 * NB + d * NB + ((f & 1) ? 0 : N - 1) * sl + (tn % N) * sp + (tn / N) * sq);
+    }
+    // ---- W1: advecting field at the rule-B points -> Wt (component-independent)
+#pragma unroll 1
+    for (int d = 0; d < 3; ++d) {
+      const double* Wd = WS + d * NB;
+      for (int jk = lane; jk < NF; jk += 32) {
+        double u[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) u[i] = Wd[i + N * jk];
+#pragma unroll
+        for (int qx = 0; qx < QB; ++qx) {
+          double b = 0.0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) b = fma(tb.B[qx][i], u[i], b);
+          W[BXO + qx * NF + jk] = b;
+        }
+      }
+      __syncwarp();
+      for (int it = lane; it < QB * N; it += 32) {
+        const int qx = it / N, k = it - qx * N;
+        double v[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[j] = W[BXO + qx * NF + j + N * k];
+#pragma unroll
+        for (int qy = 0; qy < QB; ++qy) {
+          double b = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) b = fma(tb.B[qy][j], v[j], b);
+          W[BYO + (qx * QB + qy) * N + k] = b;
+        }
+      }
+      __syncwarp();
+      for (int r = lane; r < QB * QB; r += 32) {
+        const int qx = r / QB, qy = r - qx * QB;
+        double v[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[k] = W[BYO + r * N + k];
+#pragma unroll
+        for (int qz = 0; qz < QB; ++qz) {
+          double b = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) b = fma(tb.B[qz][k], v[k], b);
+          WT[d * NQB + qx + QB * qy + QB * QB * qz] = b;
+        }
+      }
+      __syncwarp();
+    }
+    {
+      const double* g = gadv_c;
+      for (int q = lane; q < NQB; q += 32) {
+        const double w0 = WT[q], w1 = WT[NQB + q], w2 = WT[2 * NQB + q];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double t = __ldg(g + (a * 3 + 0) * NQB + q) * w0 + __ldg(g + (a * 3 + 1) * NQB + q) * w1 +
+                           __ldg(g + (a * 3 + 2) * NQB + q) * w2;
+          WT[a * NQB + q] = -adv * t;
+        }
+      }
+    }
+    // ---- W2: face factors a_s, a_o at the rule-B face points
+    cp_async_wait_all();
+    __syncwarp();
+    for (int it = lane; it < 6 * 2 * N; it += 32) {
+      const int f = it / (2 * N), rem = it - f * 2 * N, side = rem / N, q = rem - side * N;
+      const int a = f >> 1, s = f & 1;
+      const int nb = (int)nbv[f];
+      int sl, sp, sq;
+      face_strides<N>(a, sl, sp, sq);
+      double* fp = W + FPWO + (f * 2 + side) * 3 * N * QB + q * QB;
+#pragma unroll 1
+      for (int d = 0; d < 3; ++d) {
+        double v[N];
+        if (side == 0) {
+          const double* ws = WS + d * NB + (s ? N - 1 : 0) * sl + q * sq;
+#pragma unroll
+          for (int p = 0; p < N; ++p) v[p] = ws[p * sp];
+        } else if (nb >= 0) {
+          const double* wn = W + NWO + (f * 3 + d) * NF + N * q;
+#pragma unroll
+          for (int p = 0; p < N; ++p) v[p] = wn[p];
+        } else {
+#pragma unroll
+          for (int p = 0; p < N; ++p) v[p] = 0.0;
+        }
+#pragma unroll
+        for (int qp = 0; qp < QB; ++qp) {
+          double b = 0.0;
+#pragma unroll
+          for (int p = 0; p < N; ++p) b = fma(tb.B[qp][p], v[p], b);
+          fp[d * N * QB + qp] = b;
+        }
+      }
+    }
+    __syncwarp();
+    for (int it = lane; it < 6 * QB; it += 32) {
+      const int f = it / QB, qp = it - f * QB;
+      const int ty = (int)tyv[f];
+      const double* nw = gfw_c + (size_t)f * 3 * NQFB;
+      double vs[3][N], vo[3][N];
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          vs[d][q] = W[FPWO + (f * 2 + 0) * 3 * N * QB + d * N * QB + q * QB + qp];
+          vo[d][q] = W[FPWO + (f * 2 + 1) * 3 * N * QB + d * N * QB + q * QB + qp];
+        }
+#pragma unroll
+      for (int qq = 0; qq < QB; ++qq) {
+        const int t = qp + QB * qq;
+        double wns = 0.0, wno = 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          double ws = 0.0, wo = 0.0;
+#pragma unroll
+          for (int q = 0; q < N; ++q) {
+            ws = fma(tb.B[qq][q], vs[d][q], ws);
+            wo = fma(tb.B[qq][q], vo[d][q], wo);
+          }
+          const double nd = __ldg(nw + d * NQFB + t);
+          wns = fma(ws, nd, wns);
+          wno = fma(wo, nd, wno);
+        }
+        double as, ao;
+        if (ty == 0) {
+          const double lam = fmax(fabs(wns), fabs(wno));
+          as = 0.5 * adv * (wns + lam);
+          ao = 0.5 * adv * (wno - lam);
+        } else {
+          as = adv * (ty == 2 ? wns : fabs(wns));
+          ao = 0.0;
+        }
+        FC[f * NQFB + t] = as;
+        FC[6 * NQFB + f * NQFB + t] = ao;
+      }
+    }
+    __syncwarp();
+}
+
 // ===========================================================================
 // Momentum operator on deformed hexahedra (apply_momentum, forms.cpp:389-604)
 // ===========================================================================
@@ -577,151 +735,9 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
   for (int f = 0; f < 6; ++f) bdir |= ((int)tyv[f] == 1) << f;
 
   if (passB) {
-    // the neighbours' advecting-field face layers -> NW (waited for before W2)
-    for (int i = lane; i < 6 * 3 * NF; i += 32) {
-      const int f = i / (3 * NF), r = i - f * 3 * NF, d = r / NF, tn = r - d * NF;
-      const int nb = (int)nbv[f];
-      if (nb < 0) continue;
-      int sl, sp, sq;
-      face_strides<N>(f >> 1, sl, sp, sq);
-      cp_async8(W + G::NW + i, w + (size_t)nb * 3 * NB + d * NB + ((f & 1) ? 0 : N - 1) * sl + (tn % N) * sp + (tn / N) * sq);
-    }
-    // ---- W1: advecting field at the rule-B points -> Wt (component-independent)
-    const double* WS = cell + G::O_WS;
-#pragma unroll 1
-    for (int d = 0; d < 3; ++d) {
-      const double* Wd = WS + d * NB;
-      for (int jk = lane; jk < NF; jk += 32) {
-        double u[N];
-#pragma unroll
-        for (int i = 0; i < N; ++i) u[i] = Wd[i + N * jk];
-#pragma unroll
-        for (int qx = 0; qx < QB; ++qx) {
-          double b = 0.0;
-#pragma unroll
-          for (int i = 0; i < N; ++i) b = fma(tb.B[qx][i], u[i], b);
-          W[G::BX + qx * NF + jk] = b;
-        }
-      }
-      __syncwarp();
-      for (int it = lane; it < QB * N; it += 32) {
-        const int qx = it / N, k = it - qx * N;
-        double v[N];
-#pragma unroll
-        for (int j = 0; j < N; ++j) v[j] = W[G::BX + qx * NF + j + N * k];
-#pragma unroll
-        for (int qy = 0; qy < QB; ++qy) {
-          double b = 0.0;
-#pragma unroll
-          for (int j = 0; j < N; ++j) b = fma(tb.B[qy][j], v[j], b);
-          W[G::BY + (qx * QB + qy) * N + k] = b;
-        }
-      }
-      __syncwarp();
-      for (int r = lane; r < QB * QB; r += 32) {
-        const int qx = r / QB, qy = r - qx * QB;
-        double v[N];
-#pragma unroll
-        for (int k = 0; k < N; ++k) v[k] = W[G::BY + r * N + k];
-#pragma unroll
-        for (int qz = 0; qz < QB; ++qz) {
-          double b = 0.0;
-#pragma unroll
-          for (int k = 0; k < N; ++k) b = fma(tb.B[qz][k], v[k], b);
-          WT[d * NQB + qx + QB * qy + QB * QB * qz] = b;
-        }
-      }
-      __syncwarp();
-    }
-    {
-      const double* g = gadv + (size_t)cid * 9 * NQB;
-      for (int q = lane; q < NQB; q += 32) {
-        const double w0 = WT[q], w1 = WT[NQB + q], w2 = WT[2 * NQB + q];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          const double t = __ldg(g + (a * 3 + 0) * NQB + q) * w0 + __ldg(g + (a * 3 + 1) * NQB + q) * w1 +
-                           __ldg(g + (a * 3 + 2) * NQB + q) * w2;
-          WT[a * NQB + q] = -co.adv * t;
-        }
-      }
-    }
-    // ---- W2: face factors a_s, a_o at the rule-B face points
-    cp_async_wait_all();
-    __syncwarp();
-    for (int it = lane; it < 6 * 2 * N; it += 32) {
-      const int f = it / (2 * N), rem = it - f * 2 * N, side = rem / N, q = rem - side * N;
-      const int a = f >> 1, s = f & 1;
-      const int nb = (int)nbv[f];
-      int sl, sp, sq;
-      face_strides<N>(a, sl, sp, sq);
-      double* fp = W + G::FPW + (f * 2 + side) * 3 * N * QB + q * QB;
-#pragma unroll 1
-      for (int d = 0; d < 3; ++d) {
-        double v[N];
-        if (side == 0) {
-          const double* ws = WS + d * NB + (s ? N - 1 : 0) * sl + q * sq;
-#pragma unroll
-          for (int p = 0; p < N; ++p) v[p] = ws[p * sp];
-        } else if (nb >= 0) {
-          const double* wn = W + G::NW + (f * 3 + d) * NF + N * q;
-#pragma unroll
-          for (int p = 0; p < N; ++p) v[p] = wn[p];
-        } else {
-#pragma unroll
-          for (int p = 0; p < N; ++p) v[p] = 0.0;
-        }
-#pragma unroll
-        for (int qp = 0; qp < QB; ++qp) {
-          double b = 0.0;
-#pragma unroll
-          for (int p = 0; p < N; ++p) b = fma(tb.B[qp][p], v[p], b);
-          fp[d * N * QB + qp] = b;
-        }
-      }
-    }
-    __syncwarp();
-    for (int it = lane; it < 6 * QB; it += 32) {
-      const int f = it / QB, qp = it - f * QB;
-      const int ty = (int)tyv[f];
-      const double* nw = gfw + ((size_t)cid * 6 + f) * 3 * NQFB;
-      double vs[3][N], vo[3][N];
-#pragma unroll
-      for (int d = 0; d < 3; ++d)
-#pragma unroll
-        for (int q = 0; q < N; ++q) {
-          vs[d][q] = W[G::FPW + (f * 2 + 0) * 3 * N * QB + d * N * QB + q * QB + qp];
-          vo[d][q] = W[G::FPW + (f * 2 + 1) * 3 * N * QB + d * N * QB + q * QB + qp];
-        }
-#pragma unroll
-      for (int qq = 0; qq < QB; ++qq) {
-        const int t = qp + QB * qq;
-        double wns = 0.0, wno = 0.0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          double ws = 0.0, wo = 0.0;
-#pragma unroll
-          for (int q = 0; q < N; ++q) {
-            ws = fma(tb.B[qq][q], vs[d][q], ws);
-            wo = fma(tb.B[qq][q], vo[d][q], wo);
-          }
-          const double nd = __ldg(nw + d * NQFB + t);
-          wns = fma(ws, nd, wns);
-          wno = fma(wo, nd, wno);
-        }
-        double as, ao;
-        if (ty == 0) {
-          const double lam = fmax(fabs(wns), fabs(wno));
-          as = 0.5 * co.adv * (wns + lam);
-          ao = 0.5 * co.adv * (wno - lam);
-        } else {
-          as = co.adv * (ty == 2 ? wns : fabs(wns));
-          ao = 0.0;
-        }
-        FC[f * NQFB + t] = as;
-        FC[6 * NQFB + f * NQFB + t] = ao;
-      }
-    }
-    __syncwarp();
+    qp_w_phase<N, QB, G::BX, G::BY, G::FPW, G::NW>(cell + G::O_WS, W, WT, FC, nbv, tyv, w,
+                                                   gadv + (size_t)cid * 9 * NQB, gfw + (size_t)cid * 18 * NQFB,
+                                                   co.adv, lane);
   }
 
 #pragma unroll 1
@@ -928,6 +944,342 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
       yc[n] = v;
     }
     __syncwarp();
+  }
+}
+
+}  // namespace dgb
+
+namespace dgb {
+
+// ===========================================================================
+// Momentum diagonal on deformed hexahedra (momentum_diagonal, forms.cpp:606-810)
+// ===========================================================================
+// Exact diagonal, sum-factorised: for basis function i = (ix, iy, iz) every integrand is a
+// product of per-direction factors B^2, D^2 or B D at the quadrature points times a
+// per-point weight, so each term is a tensor contraction of a Q^3 (cell) or Q^2 (face)
+// weight field with those squared tables:
+//   cell, rule k+1: mass detJw B^2B^2B^2 + visc sum_ab G_ab dphi_a dphi_b (G = the compact
+//         metric detJw Jinv Jinv^T);
+//   cell, rule k+2: sum_a Wt_a phi dphi_a (Wt from qp_w_phase: -adv detJw Jinv w);
+//   faces (face-layer nodes only, outward normal, element-centric as in the apply):
+//         rule k+1 visc (C' phi^2 - c1 phi (Jinv n . grad_ref phi)) w ds with C' = the
+//         interior penalty / 2 sigma_K and c1 = 1 / 2 (interior / Dirichlet wall; outlets
+//         none), rule k+2 a_s phi^2 (a_s from qp_w_phase).
+// The value is the same for all three components (forms.cpp:635).  skew != 0: generic.
+template <int K>
+struct MomDiagQpCfg {
+  static constexpr int N = K + 1, QA = K + 1, QB = K + 2, NB = N * N * N, NF = N * N;
+  static constexpr int NQA = QA * QA * QA, NQFA = QA * QA, NQB = QB * QB * QB, NQFB = QB * QB;
+  // W phase (as MomQpCfg)
+  static constexpr int BX = 0, BY = BX + QB * NF, FPW = 0, NW = FPW + 6 * 2 * 3 * N * QB;
+  static constexpr int mx(int a, int b) { return a > b ? a : b; }
+  // diagonal stages (after the W phase): cell z-stage [6][QA^2][N] -> y-stage [3][QA][N^2];
+  // adv z-stage [3][QB^2][N] -> y-stage [2][QB][N^2]; faces: visc Y [6][3][QA][N], adv Y [6][QB][N]
+  static constexpr int CZ = 0, CY = CZ + 6 * QA * QA * N, C_END = CY + 3 * QA * NF;
+  static constexpr int AZ = 0, AY = AZ + 3 * QB * QB * N, A_END = AY + 2 * QB * NF;
+  static constexpr int FV = 0, FA = FV + 6 * 3 * QA * N, FO = FA + 6 * QB * N, F_END = FO + 6 * NF;
+  static constexpr int WORK = mx(mx(NW + 6 * 3 * NF, BY + QB * QB * N), mx(C_END, mx(A_END, F_END)));
+  // per cell: nb | type | pen | WT | FC (advecting field staged here first) | D | WORK
+  static constexpr int O_NB = 0, O_TY = 6, O_PEN = 12, O_WT = 18, O_FC = O_WT + 3 * NQB, O_WS = O_FC,
+                       O_D = O_FC + 2 * 6 * NQFB, O_WK = O_D + NB;
+  static_assert(3 * NB <= 2 * 6 * NQFB, "advecting field must fit in FC");
+  static constexpr int PER = (O_WK + WORK) | 1;
+  static constexpr int C_FIT = (227 * 1024 / 8) / PER;
+  static constexpr int C = C_FIT > 8 ? 8 : C_FIT, T = 32 * C;
+  static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
+};
+
+template <int K>
+__global__ void __launch_bounds__(MomDiagQpCfg<K>::T) k_momentum_diag_qp(
+    MeshArgs m, const double* __restrict__ gcA, const double* __restrict__ gfA, const double* __restrict__ gadv,
+    const double* __restrict__ gfw, MomCoef co, const double* __restrict__ w, double* __restrict__ y) {
+  using G = MomDiagQpCfg<K>;
+  constexpr int N = G::N, QA = G::QA, QB = G::QB, NB = G::NB, NF = G::NF;
+  constexpr int NQA = G::NQA, NQFA = G::NQFA, NQB = G::NQB, NQFB = G::NQFB, C = G::C, PER = G::PER;
+  extern __shared__ double sm[];
+  const int c0 = blockIdx.x * C;
+  const int nc = min(C, m.ncells - c0);
+  const int tid = threadIdx.x, lane = tid & 31, wc = tid >> 5;
+  const bool adv = co.adv != 0.0;
+  const double sfac = (double)(N * N);
+  for (int idx = tid; adv && idx < nc * 3 * NB; idx += G::T) {
+    const int c = idx / (3 * NB), i = idx - c * 3 * NB;
+    cp_async8(sm + c * PER + G::O_WS + i, w + (size_t)c0 * 3 * NB + idx);
+  }
+  for (int idx = tid; idx < nc * 6; idx += G::T) {
+    const int c = idx / 6, f = idx - c * 6;
+    double* cell = sm + c * PER;
+    const int nb = m.nbr[(size_t)(c0 + c) * 6 + f];
+    int ty = 0;
+    if (nb < 0) {
+      const int bid = -1 - nb;
+      ty = (bid >= 0 && bid < 64 && m.bctype[bid] == 1) ? 2 : 1;
+    }
+    cell[G::O_NB + f] = (double)nb;
+    cell[G::O_TY + f] = (double)ty;
+    cell[G::O_PEN + f] = sfac * m.pen[(size_t)(c0 + c) * 6 + f];
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  if (wc >= nc) return;
+  const int cid = c0 + wc;
+  double* cell = sm + wc * PER;
+  double* WT = cell + G::O_WT;
+  double* FC = cell + G::O_FC;
+  double* D = cell + G::O_D;
+  double* W = cell + G::O_WK;
+  const double* nbv = cell + G::O_NB;
+  const double* tyv = cell + G::O_TY;
+  const FTab<N, QA>& ta = c_ft<N, QA>;
+  const FTab<N, QB>& tb = c_ft<N, QB>;
+  if (adv)
+    qp_w_phase<N, QB, G::BX, G::BY, G::FPW, G::NW>(cell + G::O_WS, W, WT, FC, nbv, tyv, w,
+                                                   gadv + (size_t)cid * 9 * NQB, gfw + (size_t)cid * 18 * NQFB,
+                                                   co.adv, lane);
+  // ---- cell, rule k+1: z-contraction per (qx, qy) column of the six weight fields
+  {
+    const double* gc = gcA + (size_t)cid * NQA * 7;  // [7][qx][qy][qz] (see context.cu)
+    for (int r = lane; r < QA * QA; r += 32) {
+      double t[6][N];
+#pragma unroll
+      for (int j = 0; j < 6; ++j)
+#pragma unroll
+        for (int k = 0; k < N; ++k) t[j][k] = 0.0;
+#pragma unroll
+      for (int qz = 0; qz < QA; ++qz) {
+        const double* g = gc + r + QA * QA * qz;
+        const double g00 = __ldg(g), g01 = __ldg(g + NQA), g02 = __ldg(g + 2 * NQA), g11 = __ldg(g + 3 * NQA),
+                     g12 = __ldg(g + 4 * NQA), g22 = __ldg(g + 5 * NQA), jxw = __ldg(g + 6 * NQA);
+        const double vm = co.mass * jxw, v00 = co.visc * g00, v11 = co.visc * g11, v22 = co.visc * g22,
+                     v01 = 2.0 * co.visc * g01, v02 = 2.0 * co.visc * g02, v12 = 2.0 * co.visc * g12;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double b = ta.B[qz][k], d = ta.D[qz][k], b2 = b * b, d2 = d * d, bd = b * d;
+          t[0][k] = fma(b2, vm, fma(d2, v22, t[0][k]));  // -> y B^2, x B^2 (mass + G22)
+          t[1][k] = fma(b2, v00, t[1][k]);               // G00: y B^2, x D^2
+          t[2][k] = fma(b2, v11, t[2][k]);               // G11: y D^2, x B^2
+          t[3][k] = fma(b2, v01, t[3][k]);               // G01: y BD, x BD
+          t[4][k] = fma(bd, v02, t[4][k]);               // G02: y B^2, x BD
+          t[5][k] = fma(bd, v12, t[5][k]);               // G12: y BD, x B^2
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 6; ++j)
+#pragma unroll
+        for (int k = 0; k < N; ++k) W[G::CZ + (j * QA * QA + r) * N + k] = t[j][k];
+    }
+    __syncwarp();
+    for (int it = lane; it < QA * N; it += 32) {  // y-contraction: items (qx, iz)
+      const int qx = it / N, k = it - qx * N;
+      double xb2[N], xd2[N], xbd[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) xb2[j] = xd2[j] = xbd[j] = 0.0;
+#pragma unroll
+      for (int qy = 0; qy < QA; ++qy) {
+        const int o = (qx * QA + qy) * N + k;
+        const double a0 = W[G::CZ + 0 * QA * QA * N + o], a1 = W[G::CZ + 1 * QA * QA * N + o],
+                     a2 = W[G::CZ + 2 * QA * QA * N + o], a3 = W[G::CZ + 3 * QA * QA * N + o],
+                     a4 = W[G::CZ + 4 * QA * QA * N + o], a5 = W[G::CZ + 5 * QA * QA * N + o];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          const double b = ta.B[qy][j], d = ta.D[qy][j], b2 = b * b, d2 = d * d, bd = b * d;
+          xb2[j] = fma(b2, a0, fma(d2, a2, fma(bd, a5, xb2[j])));
+          xd2[j] = fma(b2, a1, xd2[j]);
+          xbd[j] = fma(bd, a3, fma(b2, a4, xbd[j]));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        W[G::CY + 0 * QA * NF + qx * NF + j + N * k] = xb2[j];
+        W[G::CY + 1 * QA * NF + qx * NF + j + N * k] = xd2[j];
+        W[G::CY + 2 * QA * NF + qx * NF + j + N * k] = xbd[j];
+      }
+    }
+    __syncwarp();
+    for (int jk = lane; jk < NF; jk += 32) {  // x-contraction -> D
+      double s[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) s[i] = 0.0;
+#pragma unroll
+      for (int qx = 0; qx < QA; ++qx) {
+        const double xb2 = W[G::CY + qx * NF + jk], xd2 = W[G::CY + QA * NF + qx * NF + jk],
+                     xbd = W[G::CY + 2 * QA * NF + qx * NF + jk];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const double b = ta.B[qx][i], d = ta.D[qx][i];
+          s[i] = fma(b * b, xb2, fma(d * d, xd2, fma(b * d, xbd, s[i])));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) D[i + N * jk] = s[i];
+    }
+    __syncwarp();
+  }
+  // ---- cell, rule k+2: advection sum_a Wt_a phi dphi_a
+  if (adv) {
+    for (int r = lane; r < QB * QB; r += 32) {
+      const int qx = r / QB, qy = r - qx * QB;
+      double u0[N], u1[N], u2[N];
+#pragma unroll
+      for (int k = 0; k < N; ++k) u0[k] = u1[k] = u2[k] = 0.0;
+#pragma unroll
+      for (int qz = 0; qz < QB; ++qz) {
+        const int pt = qx + QB * qy + QB * QB * qz;
+        const double w0 = WT[pt], w1 = WT[NQB + pt], w2 = WT[2 * NQB + pt];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double b = tb.B[qz][k], d = tb.D[qz][k], b2 = b * b;
+          u0[k] = fma(b2, w0, u0[k]);     // term 0: x BD, y B^2
+          u1[k] = fma(b2, w1, u1[k]);     // term 1: x B^2, y BD
+          u2[k] = fma(b * d, w2, u2[k]);  // term 2: x B^2, y B^2
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        W[G::AZ + (0 * QB * QB + r) * N + k] = u0[k];
+        W[G::AZ + (1 * QB * QB + r) * N + k] = u1[k];
+        W[G::AZ + (2 * QB * QB + r) * N + k] = u2[k];
+      }
+    }
+    __syncwarp();
+    for (int it = lane; it < QB * N; it += 32) {
+      const int qx = it / N, k = it - qx * N;
+      double xbd[N], xb2[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) xbd[j] = xb2[j] = 0.0;
+#pragma unroll
+      for (int qy = 0; qy < QB; ++qy) {
+        const int o = (qx * QB + qy) * N + k;
+        const double a0 = W[G::AZ + o], a1 = W[G::AZ + QB * QB * N + o], a2 = W[G::AZ + 2 * QB * QB * N + o];
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          const double b = tb.B[qy][j], d = tb.D[qy][j], b2 = b * b;
+          xbd[j] = fma(b2, a0, xbd[j]);
+          xb2[j] = fma(b * d, a1, fma(b2, a2, xb2[j]));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        W[G::AY + qx * NF + j + N * k] = xbd[j];
+        W[G::AY + QB * NF + qx * NF + j + N * k] = xb2[j];
+      }
+    }
+    __syncwarp();
+    for (int jk = lane; jk < NF; jk += 32) {
+      double s[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) s[i] = D[i + N * jk];
+#pragma unroll
+      for (int qx = 0; qx < QB; ++qx) {
+        const double xbd = W[G::AY + qx * NF + jk], xb2 = W[G::AY + QB * NF + qx * NF + jk];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const double b = tb.B[qx][i], d = tb.D[qx][i];
+          s[i] = fma(b * d, xbd, fma(b * b, xb2, s[i]));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) D[i + N * jk] = s[i];
+    }
+    __syncwarp();
+  }
+  // ---- faces: face-layer nodes (p, q); viscous at rule k+1, Lax-Friedrichs at rule k+2
+  {
+    const double* gf = gfA + (size_t)cid * 6 * NQFA * 7;  // [f][7][qp + Q qq]
+    for (int it = lane; it < 6 * QA; it += 32) {  // V1: along the second tangential axis
+      const int f = it / QA, tp = it - f * QA;
+      const int a = f >> 1, s = f & 1, ty = (int)tyv[f];
+      const int t1 = a == 0 ? 1 : 0, t2 = a == 2 ? 1 : 2;
+      const bool act = co.visc != 0.0 && ty != 2;
+      const double c1 = ty == 0 ? 1.0 : 2.0, cp = (ty == 0 ? 1.0 : 2.0) * cell[G::O_PEN + f];
+      const double dEL = ta.dE[s][s ? N - 1 : 0];
+      double ya[N], yb[N], yc[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) ya[q] = yb[q] = yc[q] = 0.0;
+      if (act) {
+        const double* g = gf + (size_t)f * 7 * NQFA;
+#pragma unroll
+        for (int tq = 0; tq < QA; ++tq) {
+          const int t = tp + QA * tq;
+          double jn[3];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) jn[d] = __ldg(g + d * NQFA + t);
+          const double wds = __ldg(g + 6 * NQFA + t);
+          const double wA = co.visc * wds * (cp - c1 * dEL * jn[a]);
+          const double wB = -co.visc * c1 * wds * jn[t1];
+          const double wC = -co.visc * c1 * wds * jn[t2];
+#pragma unroll
+          for (int q = 0; q < N; ++q) {
+            const double b = ta.B[tq][q], d = ta.D[tq][q];
+            ya[q] = fma(b * b, wA, ya[q]);
+            yb[q] = fma(b * b, wB, yb[q]);
+            yc[q] = fma(b * d, wC, yc[q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        W[G::FV + ((f * 3 + 0) * QA + tp) * N + q] = ya[q] + yc[q];
+        W[G::FV + ((f * 3 + 1) * QA + tp) * N + q] = yb[q];
+      }
+    }
+    for (int it = lane; adv && it < 6 * QB; it += 32) {  // A1
+      const int f = it / QB, tp = it - f * QB;
+      double ya[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) ya[q] = 0.0;
+#pragma unroll
+      for (int tq = 0; tq < QB; ++tq) {
+        const double as = FC[f * NQFB + tp + QB * tq];
+#pragma unroll
+        for (int q = 0; q < N; ++q) ya[q] = fma(tb.B[tq][q] * tb.B[tq][q], as, ya[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < N; ++q) W[G::FA + (f * QB + tp) * N + q] = ya[q];
+    }
+    __syncwarp();
+    for (int it = lane; it < 6 * N; it += 32) {  // V2 / A2: along the first tangential axis
+      const int f = it / N, q = it - f * N;
+      double o[N];
+#pragma unroll
+      for (int p = 0; p < N; ++p) o[p] = 0.0;
+#pragma unroll
+      for (int tp = 0; tp < QA; ++tp) {
+        const double yac = W[G::FV + ((f * 3 + 0) * QA + tp) * N + q], yb = W[G::FV + ((f * 3 + 1) * QA + tp) * N + q];
+#pragma unroll
+        for (int p = 0; p < N; ++p) {
+          const double b = ta.B[tp][p], d = ta.D[tp][p];
+          o[p] = fma(b * b, yac, fma(b * d, yb, o[p]));
+        }
+      }
+      if (adv) {
+#pragma unroll
+        for (int tp = 0; tp < QB; ++tp) {
+          const double ya = W[G::FA + (f * QB + tp) * N + q];
+#pragma unroll
+          for (int p = 0; p < N; ++p) o[p] = fma(tb.B[tp][p] * tb.B[tp][p], ya, o[p]);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < N; ++p) W[G::FO + f * NF + p + N * q] = o[p];
+    }
+    __syncwarp();
+  }
+  // ---- store: cell + face-layer contributions, the same value for the three components
+  double* yc = y + (size_t)cid * 3 * NB;
+  for (int n = lane; n < NB; n += 32) {
+    const int i = n % N, j = (n / N) % N, k = n / NF;
+    const double* fo = W + G::FO;
+    double v = D[n];
+    if (i == 0) v += fo[0 * NF + j + N * k];
+    if (i == N - 1) v += fo[1 * NF + j + N * k];
+    if (j == 0) v += fo[2 * NF + i + N * k];
+    if (j == N - 1) v += fo[3 * NF + i + N * k];
+    if (k == 0) v += fo[4 * NF + i + N * j];
+    if (k == N - 1) v += fo[5 * NF + i + N * j];
+    yc[n] = v;
+    yc[NB + n] = v;
+    yc[2 * NB + n] = v;
   }
 }
 

@@ -544,20 +544,24 @@ def test_deformed_sip_kernel_matches_reference_and_generic(ref, gpu, n_el, kp, a
                                    (2.1, 0.0, 0.7, 0.0), (0.0, 0.0, 1.1, 0.0), (1.9, 0.6, 0.0, 0.0)])
 def test_deformed_momentum_kernel_matches_reference_and_generic(ref, gpu, n_el, ku, amp, outlet, coefs):
     """fast_deformed.cuh k_momentum_qp (pass A through the per-field SIP body at rule k+1,
-    Lax-Friedrichs advection at rule k+2 with per-qp geometry) vs the reference and the
-    generic device kernel on distorted 3D meshes, with walls / an outlet and every
-    combination of mass / viscous / advective coefficients."""
+    Lax-Friedrichs advection at rule k+2 with per-qp geometry) and k_momentum_diag_qp vs
+    the reference and the generic device kernels on distorted 3D meshes, with walls / an
+    outlet and every combination of mass / viscous / advective coefficients."""
     R, D = pair(ref, gpu, 3, n_el, ku, ku - 1 if ku > 1 else 1, amp, outlet=outlet)
     assert not D.affine
     w = gpu.seeded_uniform(41, R.n_u)
     x = gpu.seeded_uniform(42, R.n_u)
     want = R.momentum(coefs, w, x)
+    want_d = R.momentum_diag(coefs, w)
     ctx = gpu.MomentumCtx(*coefs, advecting=dev(w))
     for fast in (True, False):
         D.set_fast_path(fast)
         y = D.zeros()
         gpu.apply_momentum(D, ctx, dev(x), y)
         assert rel(host(y), want) <= TOL_APPLY, fast
+        d = D.zeros()
+        gpu.momentum_diagonal(D, ctx, d)  # k_momentum_diag_qp (fast) / k_momentum_diag
+        assert rel(host(d), want_d) <= TOL_APPLY, ("diag", fast)
     D.set_fast_path(True)
 
 
