@@ -282,10 +282,14 @@ __global__ void k_gs_solve(int k, const double* __restrict__ ab, double* __restr
     g[j] = t * sv[j];
   }
 }
+// zout != nullptr: also zout = dinv (.) w_new (the next Arnoldi step's preconditioned
+// input, unnormalised; the caller rescales the Hessenberg column)
 template <int NV>
 __global__ void __launch_bounds__(kGsThreads) k_gs_update_part(size_t n, GsPack P, const double* __restrict__ g,
                                                              double* __restrict__ w, int want_norm,
-                                                             double* __restrict__ partial) {
+                                                             double* __restrict__ partial,
+                                                             const double* __restrict__ dinv,
+                                                             double* __restrict__ zout) {
   double c[NV];
 #pragma unroll
   for (int j = 0; j < NV; ++j) c[j] = g[j];
@@ -303,6 +307,15 @@ __global__ void __launch_bounds__(kGsThreads) k_gs_update_part(size_t n, GsPack 
       wi.y = fma(-c[j], v[j].y, wi.y);
     }
     w2[i] = wi;
+    if (zout) {
+      double2 zi = wi;
+      if (dinv) {
+        const double2 di = reinterpret_cast<const double2*>(dinv)[i];
+        zi.x *= di.x;
+        zi.y *= di.y;
+      }
+      reinterpret_cast<double2*>(zout)[i] = zi;
+    }
     acc[0] = fma(wi.y, wi.y, fma(wi.x, wi.x, acc[0]));
   }
   if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -311,6 +324,7 @@ __global__ void __launch_bounds__(kGsThreads) k_gs_update_part(size_t n, GsPack 
 #pragma unroll
     for (int j = 0; j < NV; ++j) wi = fma(-c[j], P.u[j][i], wi);
     w[i] = wi;
+    if (zout) zout[i] = dinv ? wi * dinv[i] : wi;
     acc[0] = fma(wi, wi, acc[0]);
   }
   if (want_norm) block_reduce_store<1>(acc, partial);
@@ -424,14 +438,14 @@ cudaError_t gs_solve(cudaStream_t s, int k, const double* d_ab, double* L, int l
   return cudaGetLastError();
 }
 cudaError_t gs_update(cudaStream_t s, size_t n, int nv, const double* const* U, const double* g, double* w,
-                      double* scratch, double* norm_out) {
+                      double* scratch, double* norm_out, const double* dinv, double* zout) {
   if (nv < 1 || nv > kGsChunk) return cudaErrorInvalidValue;
   GsPack P{};
   for (int j = 0; j < nv; ++j) P.u[j] = U[j];
   const int gr = gs_grid(n);
   switch (nv) {
 #define GS_CASE(NV)                                                                          \
-  case NV: k_gs_update_part<NV><<<gr, kGsThreads, 0, s>>>(n, P, g, w, norm_out ? 1 : 0, scratch); break;
+  case NV: k_gs_update_part<NV><<<gr, kGsThreads, 0, s>>>(n, P, g, w, norm_out ? 1 : 0, scratch, dinv, zout); break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6) GS_CASE(7) GS_CASE(8)
     GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12) GS_CASE(13) GS_CASE(14) GS_CASE(15) GS_CASE(16)
 #undef GS_CASE

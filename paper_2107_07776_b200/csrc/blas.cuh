@@ -159,8 +159,9 @@ cudaError_t gs_dots(cudaStream_t s, size_t n, int nv, const double* const* U, co
 cudaError_t gs_solve(cudaStream_t s, int k, const double* d_ab, double* L, int ldl, double* d_s, double sk,
                      double* d_h, double* d_g);
 // w -= sum_{j<nv} g_j U_j ; if norm_out: *norm_out = |w|^2
+// zout (optional): also write zout = dinv (.) w_new (dinv == nullptr: w_new)
 cudaError_t gs_update(cudaStream_t s, size_t n, int nv, const double* const* U, const double* g, double* w,
-                      double* scratch, double* norm_out);
+                      double* scratch, double* norm_out, const double* dinv = nullptr, double* zout = nullptr);
 // z = a * r * d (d may be null: z = a r)
 cudaError_t v_mul_scaled(cudaStream_t s, size_t n, double a, const double* r, const double* d, double* z);
 

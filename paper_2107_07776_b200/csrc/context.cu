@@ -858,8 +858,13 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
     while (k < m && iter < s.max_iter) {
       double* w = gm_basis_[W];
       if (gprof) cudaEventRecord(gev[0], st);
-      ++launches;
-      CK(v_mul_scaled(st, n, sh[k], gm_basis_[k], inv, z));  // z = M^{-1} v_k
+      // z = M^{-1} U_k, unnormalised: for k >= 1 the previous step's last update pass wrote it
+      // (fused); w = A z is then 1 / sh[k] times the true A M^{-1} v_k and the host rescales
+      // the Hessenberg column by sh[k] (sh[0] = 1)
+      if (k == 0) {
+        ++launches;
+        CK(v_mul_scaled(st, n, 1.0, gm_basis_[0], inv, z));
+      }
       OK(apply_op(op, z, w));
       if (gprof) cudaEventRecord(gev[1], st);
       ++iter;
@@ -880,7 +885,7 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
         const bool last = c0 + kGsChunk > k;
         for (int j = 0; j < nv; ++j) Uc[j] = gm_basis_[c0 + j];
         launches += last ? 2 : 1;
-        CK(gs_update(st, n, nv, Uc, d_g + c0, w, gpart, last ? d_h + k + 1 : nullptr));
+        CK(gs_update(st, n, nv, Uc, d_g + c0, w, gpart, last ? d_h + k + 1 : nullptr, inv, last ? z : nullptr));
       }
       if (gprof) cudaEventRecord(gev[3], st);
       CK(cudaMemcpyAsync(h_gm_, d_h, (k + 2) * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -897,8 +902,9 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
         }
         cudaEventRecord(gev[4], st);
       }
-      for (int i = 0; i <= k; ++i) row(i, k) = h_gm_[i];
-      const double hk1 = std::sqrt(h_gm_[k + 1]);
+      for (int i = 0; i <= k; ++i) row(i, k) = sh[k] * h_gm_[i];
+      const double wnorm = std::sqrt(h_gm_[k + 1]);  // of the stored (unnormalised) new vector
+      const double hk1 = sh[k] * wnorm;
       row(k + 1, k) = hk1;
       for (int i = 0; i < k; ++i) {
         const double t = cs[i] * row(i, k) + sn[i] * row(i + 1, k);
@@ -924,7 +930,7 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
       if (k < m) {
         if (!pool(k)) return fail(DGB_E_CUDA, "gmres: out of device memory (basis)");
         std::swap(gm_basis_[k], gm_basis_[W]);
-        sh[k] = 1.0 / hk1;
+        sh[k] = 1.0 / wnorm;
       }
     }
     std::vector<double> y(k, 0.0);
