@@ -249,16 +249,22 @@ def run_device(args):
         dg.apply_momentum(D, ctx, x, y)
         dg.apply_pressure_helmholtz(D, pmc, xp, yp)
 
-    for _ in range(max(3, args.warmup)):
+    # warm-up: at least W steps, and the GPU kept busy while the clock sampler (an
+    # nvidia-smi child, ~0.3 s to start) comes up, so the timed region does not begin
+    # from an idle, down-clocked GPU
+    sampler = ClockSampler(local)
+    sampler.start()
+    t_warm = time.time()
+    nwarm = 0
+    while nwarm < max(3, args.warmup) or (time.time() - t_warm < 0.4 and nwarm < 400):
         step()
+        nwarm += 1
+        if nwarm % 16 == 0:
+            torch.cuda.synchronize()
     torch.cuda.synchronize()
     if ws > 1:
         tdist.barrier()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 2)]
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.3)
-    torch.cuda.synchronize()
     launches0 = D.launch_count()
     ev[0].record(stream)
     for k in range(args.steps):
@@ -356,7 +362,8 @@ def run_device(args):
         "config": {"workload": CFG["workload"], "mesh": "64^3", "degrees": "Q3/Q2", "n_u": D.n_u, "n_p": D.n_p,
                    "Re": CFG["Re"], "dt": CFG["dt"], "c": CFG["c"], "parallelism": f"replicas x{ws}",
                    "l2": "inputs larger than L2 (x, w 403 MB each); the momentum apply streams 1.2 GB between "
-                         "pressure applies"},
+                         "pressure applies",
+                   "warmup_steps_run": nwarm},
         "ops": {"momentum": {"ms": tm * 1e3, "gdofs": D.n_u / tm / 1e9, "tflops_alg": mom_tflops},
                 "pressure": {"ms": tp * 1e3, "gdofs": D.n_p / tp / 1e9, "tflops_alg": prs_tflops}},
         "roofline": roofline, "roofline_hbm": roofline_hbm, "cpu_baseline": cpu,
