@@ -154,7 +154,7 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
     // axis-aligned: every Jinv off-diagonal zero up to rounding (Cartesian generator;
     // the multilinear Jacobian of a box cell can carry ~1e-17 cancellation residue)
     const int st = affine_cell_stride(dim);
-    bool axis = dim == 3;
+    bool axis = true;
     for (int c = 0; c < mesh.ncells && axis; ++c)
       for (int a = 0; a < dim && axis; ++a)
         for (int b = 0; b < dim; ++b)
@@ -163,7 +163,9 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
             axis = false;
             break;
           }
-    dc.axis = axis;
+    dc.axis = axis && dim == 3;
+    dc.axis2 = axis && dim == 2;  // 2D axis-aligned: the line-split scalar SIP (fast_sip2)
+    axis = dc.axis;
     // uniform structured grid (generate_cartesian order, one h): neighbours / boundary ids
     // / geometry follow from the cell index in the fast kernels (no mesh-table loads)
     if (axis) {
@@ -351,8 +353,9 @@ int Context::momentum_diag(const double* coefs, const double* w, double* d) {
 }
 int Context::sip(double mc, int dir, const double* x, double* y) {
   ++launches;
-  if (use_fast && (dc.axis || !dc.affine)) {
-    const cudaError_t e = dc.axis ? fast_sip3(dc, mc, dir, x, y) : fast_sip3_qp(dc, mc, dir, x, y);
+  if (use_fast && (dc.axis || dc.axis2 || !dc.affine)) {
+    const cudaError_t e = dc.axis2 ? fast_sip2(dc, mc, dir, x, y)
+                                   : (dc.axis ? fast_sip3(dc, mc, dir, x, y) : fast_sip3_qp(dc, mc, dir, x, y));
     if (e != cudaErrorNotSupported) {
       CK(e);
       return DGB_OK;

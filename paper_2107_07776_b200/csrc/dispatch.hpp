@@ -67,6 +67,7 @@ struct DevCtx {
   int dim = 0, ku = 0, kp = 0, ncells = 0;
   bool affine = true;
   bool axis = false;  // affine with diagonal Jinv on every cell (fast_axis.cuh)
+  bool axis2 = false;  // the same in 2D (fast_sip2)
   UniformGrid ug;
   MeshArgs mesh;
   const double* aff = nullptr;
@@ -100,6 +101,8 @@ struct OpTable {
 
 // fast axis-aligned 3D kernels (fast_d3.cu); cudaErrorNotSupported when not applicable
 cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, double* y);
+// 2D axis-aligned scalar SIP, one thread per cell (fast_axis.cuh k_sip_axis2)
+cudaError_t fast_sip2(const DevCtx& c, double mc, int dir, const double* x, double* y);
 // deformed (per-qp geometry) 3D meshes (fast_deformed.cuh)
 cudaError_t fast_sip3_qp(const DevCtx& c, double mc, int dir, const double* x, double* y);
 cudaError_t fast_momentum3(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);

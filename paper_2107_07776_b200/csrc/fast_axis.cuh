@@ -330,6 +330,128 @@ __device__ __forceinline__ void sip_line(const FTab<N, N>& t, const CellInfo& ci
 }
 
 // ===========================================================================
+// Scalar SIP, axis-aligned affine, 2D (BASELINE cfg1): the same exact line split
+//   y = mc detJ (M (x) M) u + (S_x (x) M) u + (M (x) S_y) u
+// one thread per cell (the 2D problems are small: the generic kernel's many CTA-wide
+// stages made it latency-bound).  Node (i, j) at i + N j.
+// ===========================================================================
+constexpr int kAffStride2 = 4 + 1 + 4 * 3;
+template <int KP>
+__global__ void __launch_bounds__(128) k_sip_axis2(MeshArgs m, const double* __restrict__ aff, double mc, int dir_bdry,
+                                                   const double* __restrict__ x, double* __restrict__ y) {
+  if (m.skip && *m.skip) return;
+  constexpr int N = KP + 1, NB = N * N;
+  const FTab<N, N>& ta = c_ft<N, N>;
+  const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= m.ncells) return;
+  const double sfac = (double)(N * N);
+  CellInfo ci;
+  {
+    const double* r = aff + (size_t)cell * kAffStride2;
+    ci.ih[0] = r[0];
+    ci.ih[1] = r[3];
+    ci.ih[2] = 0.0;
+    ci.detJ = r[4];
+    ci.A[0] = ci.detJ * ci.ih[0];
+    ci.A[1] = ci.detJ * ci.ih[1];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) {
+      const int nb = m.nbr[(size_t)cell * 4 + f];
+      ci.nb[f] = nb;
+      ci.pen[f] = sfac * m.pen[(size_t)cell * 4 + f];
+      if (nb >= 0) {
+        ci.type[f] = 0;
+        ci.ihn[f] = __ldg(aff + (size_t)nb * kAffStride2 + 3 * (f >> 1));
+      } else {
+        ci.type[f] = 1;  // the scalar operator treats every boundary id alike (walls / natural)
+        ci.ihn[f] = 0.0;
+      }
+    }
+  }
+  const double* u0 = x + (size_t)cell * NB;
+  double u[NB];
+#pragma unroll
+  for (int i = 0; i < NB; ++i) u[i] = __ldg(u0 + i);
+  double out[NB];
+  // mass: mc detJ (M (x) M) u
+  const double cm = mc * ci.detJ;
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int b = 0; b < N; ++b) {
+        double t = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) t = fma(ta.M[i][a], u[a + N * b], t);
+        s = fma(ta.M[j][b], t, s);
+      }
+      out[i + N * j] = cm * s;
+    }
+  const bool dir = dir_bdry != 0;
+  // x-lines: S_x on each row, then M along y
+  {
+    double sx[NB];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double line[N], lL[N], lR[N], o[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) line[i] = u[i + N * j];
+      const int nl = ci.nb[0], nr = ci.nb[1];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        lL[i] = nl >= 0 ? __ldg(x + (size_t)nl * NB + i + N * j) : 0.0;
+        lR[i] = nr >= 0 ? __ldg(x + (size_t)nr * NB + i + N * j) : 0.0;
+      }
+      sip_line<N>(ta, ci, 0, line, lL, lR, dir, 1.0, o);
+#pragma unroll
+      for (int i = 0; i < N; ++i) sx[i + N * j] = o[i];
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int b = 0; b < N; ++b) s = fma(ta.M[j][b], sx[i + N * b], s);
+        out[i + N * j] += s;
+      }
+  }
+  // y-lines: S_y on each column, then M along x
+  {
+    double sy[NB];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double line[N], lL[N], lR[N], o[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) line[j] = u[i + N * j];
+      const int nl = ci.nb[2], nr = ci.nb[3];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        lL[j] = nl >= 0 ? __ldg(x + (size_t)nl * NB + i + N * j) : 0.0;
+        lR[j] = nr >= 0 ? __ldg(x + (size_t)nr * NB + i + N * j) : 0.0;
+      }
+      sip_line<N>(ta, ci, 1, line, lL, lR, dir, 1.0, o);
+#pragma unroll
+      for (int j = 0; j < N; ++j) sy[i + N * j] = o[j];
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < N; ++a) s = fma(ta.M[i][a], sy[a + N * j], s);
+        out[i + N * j] += s;
+      }
+  }
+  double* yo = y + (size_t)cell * NB;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) yo[i] = out[i];
+}
+
+// ===========================================================================
 // Scalar SIP (pressure Helmholtz / Laplacian), axis-aligned affine, 3D.
 //   y = mc detJ (M M M) u + sum_d (S_d (x) M (x) M) u
 // ===========================================================================

@@ -316,6 +316,23 @@ static cudaError_t run_sip_qp(const DevCtx& c, double mc, int dir, const double*
   k_sip_qp<KP><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, gc, gf, mc, dir, x, y);
   return cudaGetLastError();
 }
+template <int KP>
+static cudaError_t run_sip_axis2(const DevCtx& c, double mc, int dir, const double* x, double* y) {
+  const cudaError_t e = ensure_ftab<KP + 1, KP + 1>();
+  if (e != cudaSuccess) return e;
+  k_sip_axis2<KP><<<(c.ncells + 127) / 128, 128, 0, c.stream>>>(c.mesh, c.aff, mc, dir, x, y);
+  return cudaGetLastError();
+}
+cudaError_t fast_sip2(const DevCtx& c, double mc, int dir, const double* x, double* y) {
+  if (c.dim != 2 || !c.axis2 || !c.aff) return cudaErrorNotSupported;
+  switch (c.kp) {
+    case 1: return run_sip_axis2<1>(c, mc, dir, x, y);
+    case 2: return run_sip_axis2<2>(c, mc, dir, x, y);
+    case 3: return run_sip_axis2<3>(c, mc, dir, x, y);
+  }
+  return cudaErrorNotSupported;
+}
+
 cudaError_t fast_sip3_qp(const DevCtx& c, double mc, int dir, const double* x, double* y) {
   if (c.dim != 3 || c.affine) return cudaErrorNotSupported;
   switch (c.kp) {

@@ -618,3 +618,26 @@ def test_diagnostics(ref, gpu):
     assert abs(c - 0.5) < 1e-12
     H = 3 ** 0.5 / 8
     assert abs(mu - 4 * (0.5 * H / 2.0) / (1600.0 * H * H)) < 1e-12
+
+
+@pytest.mark.parametrize("n_el,kp", [(4, 1), (3, 2), (3, 3), (32, 1)])
+def test_2d_axis_sip_kernel_matches_reference_and_generic(ref, gpu, n_el, kp):
+    """fast_axis.cuh k_sip_axis2 (2D line split, one thread per cell) vs the reference and
+    the generic device kernel: pressure Helmholtz and the Dirichlet / natural Laplacian."""
+    R, D = pair(ref, gpu, 2, n_el, kp + 1, kp, 0.0)
+    xp = gpu.seeded_uniform(97, R.n_p)
+    for mc in (2.3, 0.0):
+        want = R.pressure(mc, xp)
+        for fast in (True, False):
+            D.set_fast_path(fast)
+            yp = D.zeros(gpu.SPACE_P)
+            gpu.apply_pressure_helmholtz(D, mc, dev(xp), yp)
+            assert rel(host(yp), want) <= TOL_APPLY, (mc, fast)
+    for dirichlet in (True, False):
+        want = R.laplace(dirichlet, xp)
+        for fast in (True, False):
+            D.set_fast_path(fast)
+            yl = D.zeros(gpu.SPACE_P)
+            gpu.apply_scalar_laplace(D, dirichlet, dev(xp), yl)
+            assert rel(host(yl), want) <= TOL_APPLY, (dirichlet, fast)
+    D.set_fast_path(True)
