@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "blas.cuh"
@@ -517,6 +518,8 @@ int Context::mg_setup(double mc) {
   if (mg_ && mg_->mc == mc) return DGB_OK;
   if (!mg_) {
     mg_ = new MgHierarchy();
+    if (const char* e = std::getenv("DGB_MG_DEGREE")) mg_->degree = std::max(1, std::atoi(e));  // tuning
+    if (const char* e = std::getenv("DGB_MG_RANGE")) mg_->range = std::max(1.5, std::atof(e));
     const std::vector<double> xi = gauss_lobatto(kp + 1);
     for (int i = 0; i <= kp; ++i) mg_->gl.xi[i] = xi[i];
     MgLevel L0;
