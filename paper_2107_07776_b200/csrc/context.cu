@@ -498,6 +498,15 @@ int Context::rhs(const dgb_rhs_desc& ds, double* y) {
     if (e != cudaErrorNotSupported) return cuda_fail(e, "momentum_rhs");
     cudaGetLastError();
   }
+  if (use_fast && !dc.affine && dim == 3) {
+    const cudaError_t e = fast_rhs3_qp(dc, ra, y);
+    if (e == cudaSuccess) {
+      launches += 2 + ra.na;
+      return DGB_OK;
+    }
+    if (e != cudaErrorNotSupported) return cuda_fail(e, "momentum_rhs");
+    cudaGetLastError();
+  }
   ++launches;
   CK(opu->rhs(dc, ra, y));
   return DGB_OK;

@@ -119,6 +119,8 @@ cudaError_t fast_sip3_cg(const DevCtx& c, double mc, int dir, const double* p, d
 int fast_sip3_cg_blocks(const DevCtx& c);  // number of partials fast_sip3_cg writes (0: unsupported)
 // stage right-hand side (momentum_rhs) on axis-aligned 3D meshes; ptmp: pressure-space scratch
 cudaError_t fast_rhs3(const DevCtx& c, const RhsArgs& ra, double* y, double* ptmp);
+// stage right-hand side on deformed 3D meshes (RHS-mode k_momentum_qp + generic pressure / data terms)
+cudaError_t fast_rhs3_qp(const DevCtx& c, const RhsArgs& ra, double* y);
 
 // defined in ops_d{2,3}_k{1..4}.cu
 #define DGB_DECL_OPS(D, K) const OpTable& ops_d##D##_k##K();

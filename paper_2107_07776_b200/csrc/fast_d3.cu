@@ -190,6 +190,75 @@ static cudaError_t run_rhs_axis(const DevCtx& c, const RhsArgs& ra, double* y, d
   return cudaSuccess;
 }
 
+// Deformed 3D meshes: the stage right-hand side as RHS-mode k_momentum_qp launches (one
+// per distinct (field, advecting field) pair, coefficients merged per field: mass,
+// consistency-only viscous, central advective terms), then the pressure and boundary-data
+// terms through the generic kernel (accumulating).
+template <int K>
+static cudaError_t run_rhs_qp(const DevCtx& c, const RhsArgs& ra, double* y) {
+  cudaError_t e = ensure_ftab<K + 1, K + 1>();
+  if (e == cudaSuccess) e = ensure_ftab<K + 1, K + 2>();
+  if (e != cudaSuccess) return e;
+  using G = MomQpCfg<K>;
+  const double *gcA = c.qcm[K + 1], *gfA = c.qfn[K + 1], *gadv = c.qadv[K + 2], *gfw = c.qfw[K + 2];
+  if (!gcA || !gfA || !gadv || !gfw) return cudaErrorNotSupported;
+  struct Call {
+    const double* x;
+    const double* w;
+    MomCoef co;
+  };
+  std::vector<Call> calls;
+  auto find = [&](const double* x, const double* w, bool need_w) -> Call& {
+    for (Call& cl : calls)
+      if (cl.x == x && (!need_w || cl.w == w || cl.w == nullptr)) {
+        if (need_w) cl.w = w;
+        return cl;
+      }
+    calls.push_back(Call{x, need_w ? w : nullptr, MomCoef{0.0, 0.0, 0.0, 0.0}});
+    return calls.back();
+  };
+  for (int i = 0; i < ra.na; ++i) find(ra.af[i], ra.aw[i], true).co.adv -= ra.ac[i];
+  for (int i = 0; i < ra.nm; ++i) find(ra.mf[i], nullptr, false).co.mass += ra.mc[i];
+  for (int i = 0; i < ra.nv; ++i) find(ra.vf[i], nullptr, false).co.visc -= ra.vc[i];
+  const size_t nu = (size_t)c.ncells * 3 * (K + 1) * (K + 1) * (K + 1);
+  if (calls.empty() && (e = cudaMemsetAsync(y, 0, nu * sizeof(double), c.stream)) != cudaSuccess) return e;
+  if ((e = set_smem(k_momentum_qp<K, true>, G::SMEM)) != cudaSuccess) return e;
+  const int grid = (c.ncells + G::C - 1) / G::C;
+  for (size_t i = 0; i < calls.size(); ++i) {
+    const Call& cl = calls[i];
+    k_momentum_qp<K, true><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, gcA, gfA, gadv, gfw, cl.co, cl.x,
+                                                            cl.w ? cl.w : cl.x, y, i > 0 ? 1 : 0);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (ra.np > 0 || ra.dvisc != 0.0 || ra.dadv != 0.0) {
+    RhsArgs rd;
+    rd.np = ra.np;
+    for (int i = 0; i < ra.np; ++i) {
+      rd.pc[i] = ra.pc[i];
+      rd.pf[i] = ra.pf[i];
+    }
+    rd.dvisc = ra.dvisc;
+    rd.dadv = ra.dadv;
+    rd.dir_w = ra.dir_w;
+    rd.gtab = ra.gtab;
+    rd.accumulate = 1;
+    const OpTable* ops = ops_for(3, K);
+    if (!ops) return cudaErrorNotSupported;
+    return ops->rhs(c, rd, y);
+  }
+  return cudaSuccess;
+}
+cudaError_t fast_rhs3_qp(const DevCtx& c, const RhsArgs& ra, double* y) {
+  if (c.dim != 3 || c.affine) return cudaErrorNotSupported;
+  switch (c.ku) {
+    case 1: return run_rhs_qp<1>(c, ra, y);
+    case 2: return run_rhs_qp<2>(c, ra, y);
+    case 3: return run_rhs_qp<3>(c, ra, y);
+    case 4: return run_rhs_qp<4>(c, ra, y);
+  }
+  return cudaErrorNotSupported;
+}
+
 cudaError_t fast_rhs3(const DevCtx& c, const RhsArgs& ra, double* y, double* ptmp) {
   if ((c.kp != c.ku - 1 && ra.np > 0) || !ptmp) return cudaErrorNotSupported;
   switch (c.ku) {

@@ -92,7 +92,10 @@ __device__ __forceinline__ void qp_stage_nbrs(double* NBR, const double* __restr
 // faces where bit f of bdir is set).  U: the cell's nodal values in shared memory; the
 // neighbours' values are read from xg[nb * nstride + noff + node].  Geometry: the
 // compact records of this cell (7 doubles per cell point / per face point).
-template <int N, int Q>
+// RHS: the explicit viscous term of momentum_rhs instead (forms.cpp:839-857 cells,
+// :863-889 interior faces, :919-931 boundary): consistency term only (no penalty, no
+// symmetry term); the caller passes visc = -coef.
+template <int N, int Q, bool RHS = false>
 __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
                                              const double* nbv, const double* penv, int bdir, double mc, double visc,
                                              const double* __restrict__ gcell, const double* __restrict__ gface,
@@ -339,11 +342,11 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
           gro[t2] = d2o;
           const double dno = __ldg(geo + 3 * NQF) * gro[0] + __ldg(geo + 4 * NQF) * gro[1] + __ldg(geo + 5 * NQF) * gro[2];
           const double ju = us - uo;
-          F = visc * (-0.5 * (dns + dno) + pen * ju) * wds;  // forms.cpp:199-209 / 443-461
-          ssym = -0.5 * visc * ju * wds;
+          F = visc * (-0.5 * (dns + dno) + (RHS ? 0.0 : pen * ju)) * wds;  // forms.cpp:199-209 / 443-461
+          ssym = RHS ? 0.0 : -0.5 * visc * ju * wds;
         } else {  // Dirichlet-type boundary, forms.cpp:232-240
-          F = visc * (-dns + 2.0 * pen * us) * wds;
-          ssym = -visc * us * wds;
+          F = visc * (-dns + (RHS ? 0.0 : 2.0 * pen * us)) * wds;
+          ssym = RHS ? 0.0 : -visc * us * wds;
         }
         double rr[3];
 #pragma unroll
@@ -474,7 +477,9 @@ __global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const do
 // W2 -> FC = the Lax-Friedrichs weights a_s [6][Q^2] and a_o [6][Q^2] at the rule-B face
 // points (forms.cpp:509-530, :555-573, :592-599).  WS: the cell's staged advecting field
 // (3 components); W: work area (offsets BXO, BYO, FPWO, NWO); one warp per cell.
-template <int N, int QB, int BXO, int BYO, int FPWO, int NWO>
+// RHS: the central advective flux of momentum_rhs (forms.cpp:1008-1048): no lambda term,
+// w.n f on every boundary face
+template <int N, int QB, int BXO, int BYO, int FPWO, int NWO, bool RHS = false>
 __device__ __forceinline__ void qp_w_phase(const double* WS, double* W, double* WT, double* FC, const double* nbv,
                                            const double* tyv, const double* __restrict__ w,
                                            const double* __restrict__ gadv_c, const double* __restrict__ gfw_c,
@@ -613,11 +618,11 @@ __device__ __forceinline__ void qp_w_phase(const double* WS, double* W, double* 
         }
         double as, ao;
         if (ty == 0) {
-          const double lam = fmax(fabs(wns), fabs(wno));
+          const double lam = RHS ? 0.0 : fmax(fabs(wns), fabs(wno));
           as = 0.5 * adv * (wns + lam);
           ao = 0.5 * adv * (wno - lam);
         } else {
-          as = adv * (ty == 2 ? wns : fabs(wns));
+          as = adv * ((RHS || ty == 2) ? wns : fabs(wns));
           ao = 0.0;
         }
         FC[f * NQFB + t] = as;
@@ -670,13 +675,16 @@ struct MomQpCfg {
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
 
-template <int K>
+// RHS: the explicit stage operator of momentum_rhs (caller passes -visc / -adv
+// coefficients), acc: y += result
+template <int K, bool RHS = false>
 __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, const double* __restrict__ gcA,
                                                                 const double* __restrict__ gfA,
                                                                 const double* __restrict__ gadv,
                                                                 const double* __restrict__ gfw, MomCoef co,
                                                                 const double* __restrict__ x,
-                                                                const double* __restrict__ w, double* __restrict__ y) {
+                                                                const double* __restrict__ w, double* __restrict__ y,
+                                                                int acc = 0) {
   if (m.skip && *m.skip) return;
   using G = MomQpCfg<K>;
   constexpr int N = G::N, QA = G::QA, QB = G::QB, NB = G::NB, NF = G::NF, NQB = G::NQB, NQFB = G::NQFB;
@@ -735,7 +743,7 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
   for (int f = 0; f < 6; ++f) bdir |= ((int)tyv[f] == 1) << f;
 
   if (passB) {
-    qp_w_phase<N, QB, G::BX, G::BY, G::FPW, G::NW>(cell + G::O_WS, W, WT, FC, nbv, tyv, w,
+    qp_w_phase<N, QB, G::BX, G::BY, G::FPW, G::NW, RHS>(cell + G::O_WS, W, WT, FC, nbv, tyv, w,
                                                    gadv + (size_t)cid * 9 * NQB, gfw + (size_t)cid * 18 * NQFB,
                                                    co.adv, lane);
   }
@@ -746,7 +754,7 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
     // ---- pass A: mass + SIP viscous at rule k+1
     if (passA) {
       qp_stage_nbrs<N>(W + QpSipWork<N, QA>::NBR, x, 3 * NB, comp * NB, nbv, lane);
-      qp_sip_field<N, QA>(U, passB ? cell + G::O_NBF : nullptr, nbv, cell + G::O_PEN, bdir, co.mass, co.visc,
+      qp_sip_field<N, QA, RHS>(U, passB ? cell + G::O_NBF : nullptr, nbv, cell + G::O_PEN, bdir, co.mass, co.visc,
                           gcA + (size_t)cid * G::NQA * 7, gfA + (size_t)cid * 6 * G::NQFA * 7, W, OUT, lane);
     } else {
       for (int i = lane; i < NB; i += 32) OUT[i] = 0.0;
@@ -941,7 +949,7 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
         if (k == 0) v += fo[4 * NF + i + N * j];
         if (k == N - 1) v += fo[5 * NF + i + N * j];
       }
-      yc[n] = v;
+      yc[n] = acc ? yc[n] + v : v;
     }
     __syncwarp();
   }

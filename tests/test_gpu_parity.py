@@ -641,3 +641,29 @@ def test_2d_axis_sip_kernel_matches_reference_and_generic(ref, gpu, n_el, kp):
             gpu.apply_scalar_laplace(D, dirichlet, dev(xp), yl)
             assert rel(host(yl), want) <= TOL_APPLY, (dirichlet, fast)
     D.set_fast_path(True)
+
+
+@pytest.mark.parametrize("n_el,ku,amp,outlet", [(2, 2, 0.03, None), (2, 3, 0.03, 1), (2, 4, 0.02, None),
+                                               (3, 2, 0.05, 4)])
+def test_deformed_rhs_matches_reference_and_generic(ref, gpu, n_el, ku, amp, outlet):
+    """Stage RHS on distorted 3D meshes through RHS-mode k_momentum_qp launches (mass,
+    consistency-only viscous, central advective terms) + the generic pressure / data terms,
+    vs the reference and the all-generic path; walls, an outlet, Dirichlet data."""
+    R, D = pair(ref, gpu, 3, n_el, ku, ku - 1, amp, outlet=outlet, dirichlet_seed=5)
+    un = gpu.seeded_uniform(61, R.n_u)
+    ug = gpu.seeded_uniform(62, R.n_u)
+    wx = gpu.seeded_uniform(63, R.n_u)
+    pp = gpu.seeded_uniform(64, R.n_p)
+    want = R.momentum_rhs(mass=[(2.9, un), (-0.7, ug)], visc=[(0.65, un), (0.3, ug)],
+                          adv=[(0.5, un, wx), (0.25, ug, ug)], pres=[(1.0, pp)], dir_visc=0.65, dir_adv=0.5,
+                          dir_w=wx, time=0.0)
+    dun, dug, dwx, dpp = dev(un), dev(ug), dev(wx), dev(pp)
+    spec = gpu.MomentumRhs(mass=[(2.9, dun), (-0.7, dug)], visc=[(0.65, dun), (0.3, dug)],
+                           adv=[(0.5, dun, dwx), (0.25, dug, dug)], pres=[(1.0, dpp)], dir_visc_coef=0.65,
+                           dir_adv_coef=0.5, dir_w=dwx)
+    for fast in (True, False):
+        D.set_fast_path(fast)
+        y = D.zeros()
+        gpu.momentum_rhs(D, spec, y)
+        assert rel(host(y), want) <= TOL_APPLY, fast
+    D.set_fast_path(True)
