@@ -1206,8 +1206,13 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   SYNC_CELL();
   // S78: per (component, z-layer l): y- then x-integration of the three gradient tests,
   //      qx by qx in registers, accumulated into OUT
-  // (items split over halves of the output y-rows so a warp-cell keeps more lanes busy)
-  constexpr int JH = WPC ? 2 : 1, NJ = (N + JH - 1) / JH;
+  // (K = 3: items split over halves of the output y-rows so a warp-cell keeps more lanes
+  // busy; K = 2: unsplit, measured 3% faster at cfg5.  DGB_MOM_JH overrides for tuning)
+#ifdef DGB_MOM_JH
+  constexpr int JH = WPC ? DGB_MOM_JH : 1, NJ = (N + JH - 1) / JH;
+#else
+  constexpr int JH = WPC && K != 2 ? 2 : 1, NJ = (N + JH - 1) / JH;
+#endif
   for (int idx = it0; idx < ITEMS(3 * N * JH); idx += IST) {
     const int c = CELLOF(idx, 3 * N * JH), r = RESTOF(idx, c, 3 * N * JH);
     const int comp = r / (N * JH), r2 = r - comp * N * JH;
