@@ -717,8 +717,8 @@ struct MomAxisCfg {
 template <int K, int MODE> struct MomAxisTune { static constexpr int C = 6, T = 192; static constexpr bool SPLIT = false; };
 template <int MODE> struct MomAxisTune<1, MODE> { static constexpr int C = 16, T = 128; static constexpr bool SPLIT = false; };
 #ifndef DGB_MOM2_C
-#define DGB_MOM2_C 8
-#define DGB_MOM2_T 256
+#define DGB_MOM2_C 6  // 6 cells / 192 threads: 3.63 -> 3.41 ms at cfg5 (after the unsplit S78)
+#define DGB_MOM2_T 192
 #endif
 template <int MODE> struct MomAxisTune<2, MODE> { static constexpr int C = DGB_MOM2_C, T = DGB_MOM2_T; static constexpr bool SPLIT = false; };
 #ifndef DGB_MOM3_C  // tuning overrides for experiments (tools/tune_mom.sh)
