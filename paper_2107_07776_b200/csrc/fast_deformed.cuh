@@ -414,7 +414,10 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
 template <int KP>
 struct SipQpCfg {
   static constexpr int N = KP + 1, Q = KP + 2, NB = N * N * N, NF = N * N, NQ = Q * Q * Q, NQF = Q * Q;
-  static constexpr int C = 4, T = 32 * C;
+#ifndef DGB_SQP_C
+#define DGB_SQP_C 4
+#endif
+  static constexpr int C = DGB_SQP_C, T = 32 * C;
   static constexpr int CS = 7, FS = 7;  // compact cell / face geometry records (DevCtx::qcm / qfn)
   // per cell: U | OUT | info (nb, type as doubles; pen) | work
   static constexpr int O_U = 0, O_OUT = NB, O_NB = 2 * NB, O_TY = O_NB + 6, O_PEN = O_TY + 6, O_WK = O_PEN + 6;
