@@ -2,7 +2,7 @@
 coefficients, w = the synthetic field) and one pressure Helmholtz apply on the seeded
 U[-1,1] vectors through the unmodified reference (oracle/_ref, CPU; its lazy geometry
 build alone takes minutes and ~10+ GB) and through the device fast kernels.
-Usage: python tools/full_apply_parity.py cfg3|cfg4 ; prints a JSON line."""
+Usage: python tools/full_apply_parity.py cfg2|cfg3|cfg4|cfg5 ; prints a JSON line."""
 import json, os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -13,7 +13,8 @@ import paper_2107_07776_b200 as dg
 import reforacle as ref
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
-n_el, ku, amp, seed, Re = {"cfg3": (64, 3, 0.0, 2, 1000.0), "cfg4": (48, 4, 0.1 / 48, 3, 100.0)}[name]
+n_el, ku, amp, seed, Re = {"cfg2": (32, 2, 0.0, 1, 100.0), "cfg3": (64, 3, 0.0, 2, 1000.0),
+                            "cfg4": (48, 4, 0.1 / 48, 3, 100.0), "cfg5": (96, 2, 0.0, 4, 1600.0)}[name]
 kp = ku - 1
 g = 2 - 2 ** 0.5
 coefs = (1 / (g * 1e-3), 1 / (2 * Re), 0.5, 0.0)
