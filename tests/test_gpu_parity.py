@@ -290,8 +290,9 @@ def test_zero_rhs_zero_iterations(gpu):
     assert r.iterations == 0 and float(x.abs().max()) == 0.0
 
 
-def _step_case(ref, gpu, dim, n_el, ku, kp, Re, dt, seed, steps, restart=50, fixed_point=False, amp=0.0):
-    R, D = pair(ref, gpu, dim, n_el, ku, kp, amp, dirichlet_seed=seed)
+def _step_case(ref, gpu, dim, n_el, ku, kp, Re, dt, seed, steps, restart=50, fixed_point=False, amp=0.0,
+               outlet=None):
+    R, D = pair(ref, gpu, dim, n_el, ku, kp, amp, outlet=outlet, dirichlet_seed=seed)
     f = gpu.SynthField(dim, seed)
     u0 = f.interpolate(D)
     p0 = np.zeros(R.n_p)
@@ -343,6 +344,14 @@ def test_trbdf2_deformed_q4q3_step(ref, gpu):
     """cfg4's degrees (Q4/Q3) on a distorted 3^3 mesh: the deformed fast kernels
     (k_momentum_qp / k_sip_qp) inside two full device steps vs the restated driver."""
     _step_case(ref, gpu, 3, 3, 4, 3, Re=100.0, dt=1e-3, seed=3, steps=2, amp=0.03)
+
+
+@pytest.mark.parametrize("dim,n_el,ku,kp,amp", [(2, 8, 2, 1, 0.0), (3, 3, 3, 2, 0.0), (3, 3, 2, 1, 0.04)])
+def test_trbdf2_steps_with_outlet(ref, gpu, dim, n_el, ku, kp, amp):
+    """Two steps with an outlet on boundary id 1 (no Dirichlet data there: natural
+    viscous terms, w.n advective flux, pressure boundary flux dropped) vs the restated
+    driver; fast axis-aligned, deformed and 2D paths."""
+    _step_case(ref, gpu, dim, n_el, ku, kp, Re=100.0, dt=1e-3, seed=1, steps=2, amp=amp, outlet=1)
 
 
 def test_trbdf2_step_3d_small(ref, gpu):
