@@ -218,6 +218,52 @@ def trbdf2_step_time(D, dg, torch, stream, precond="jacobi"):
                       "c 1e3, GMRES restart 30 / CG, rel tol 1e-10 (mass 1e-12); pressure CG preconditioner: " + precond}
 
 
+def cfg5_steps(dg, torch, stream, precond="jacobi", nsteps=20):
+    """BASELINE configs[4]: 20 consecutive TR-BDF2 steps at 96^3 Q2/Q1, Re 1600, initial
+    field (seed 4) scaled to max nodal |u| = 1, dt for CFL 0.5, GMRES(50) /
+    CG at 1e-10, after one discarded warm-up step (first-use allocations).  Same protocol
+    as tools/cfg5_steps.py; CUDA events on the context stream."""
+    import math
+    n_el, ku, kp, seed, Re = 96, 2, 1, 4, 1600.0
+    D = dg.DGContext(3, n_el, ku, kp)
+    f1 = dg.SynthField(3, seed)
+    u = D.zeros()
+    dg.interpolate_synth_device(D, f1, u)
+    umax = float(u.view(D.ncells, 3, -1).pow(2).sum(1).sqrt().max())
+    f = dg.SynthField(3, seed, 1.0 / umax)
+    for bid in range(6):
+        D.set_dirichlet_fn(bid, f.fn_ptr, f.user_ptr, 0.0)
+    u0 = D.zeros()
+    dg.interpolate_synth_device(D, f, u0)
+    dt = 0.5 * (math.sqrt(3.0) / n_el) / ku
+    p0 = D.zeros(dg.SPACE_P)
+    wu, wp = D.zeros(), D.zeros(dg.SPACE_P)
+    dg.trbdf2_step(D, dg.StepParams(dt=dt, Re=Re, c=1e3, restart=50, first_step=True, pressure_precond=precond),
+                   u0, u0, p0, wu, wp)
+    del wu, wp
+    bufs = [(u0, p0), (D.zeros(), D.zeros(dg.SPACE_P)), (D.zeros(), D.zeros(dg.SPACE_P))]
+    u_nm1, (u_n, p_n) = u0, bufs[0]
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    its_all = []
+    e0.record(stream)
+    for n in range(nsteps):
+        u_np1, p_np1 = bufs[(n + 1) % 3]
+        if u_np1.data_ptr() == u_nm1.data_ptr():
+            u_np1, p_np1 = bufs[(n + 2) % 3]
+        sp = dg.StepParams(dt=dt, Re=Re, c=1e3, time=n * dt, restart=50, first_step=(n == 0),
+                           pressure_precond=precond)
+        its_all.append([int(i) for i in dg.trbdf2_step(D, sp, u_nm1, u_n, p_n, u_np1, p_np1)])
+        u_nm1, u_n, p_n = u_n, u_np1, p_np1
+    e1.record(stream)
+    torch.cuda.synchronize()
+    total = e0.elapsed_time(e1) * 1e-3
+    del D, bufs, u, u0
+    torch.cuda.empty_cache()
+    return {"s_per_step": total / nsteps, "total_s": total, "steps": nsteps, "dt": dt,
+            "krylov_its_first_last": [its_all[0], its_all[-1]], "pressure_precond": precond}
+
+
 def run_device(args):
     import torch
     import paper_2107_07776_b200 as dg
@@ -320,6 +366,19 @@ def run_device(args):
                         "note": "same step with the multigrid-preconditioned pressure CG (opt-in; not the reference's "
                                 "Jacobi, so CG iteration counts differ by design; fields agree to the solve tolerance)"}
 
+    # ---- BASELINE configs[4] (cfg5): 20 consecutive steps, the parity (Jacobi) solver and
+    #      the multigrid pressure CG; outside the timed op-apply region
+    cfg5 = None
+    if not args.no_step and not args.no_cfg5:
+        cfg5 = {"config": "cfg5: 3D 96^3 affine Q2/Q1, Re 1600, max|u| = 1, CFL 0.5, GMRES(50) / CG tol 1e-10, "
+                          "20 consecutive steps after one discarded warm-up step"}
+        j = cfg5_steps(dg, torch, stream, "jacobi")
+        m = cfg5_steps(dg, torch, stream, "mg")
+        cfg5.update({"s_per_step": reduce_max(j["s_per_step"]), "dt": j["dt"],
+                     "krylov_its_first_last": j["krylov_its_first_last"],
+                     "mg": {"s_per_step": reduce_max(m["s_per_step"]),
+                            "krylov_its_first_last": m["krylov_its_first_last"]}})
+
     if rank != 0:
         if ws > 1:
             tdist.barrier()
@@ -371,6 +430,7 @@ def run_device(args):
                 "d2h_bytes_per_step": 8 * (D.n_u + D.n_p)},
         "gpu_launches": int(launches), "clocks": clocks, "setup_s": setup_s,
         "trbdf2": trbdf2,
+        "cfg5_steps": cfg5,
     }
     print(json.dumps(line), flush=True)
     if ws > 1:
@@ -386,6 +446,7 @@ def main():
     ap.add_argument("--impl", default="dgb", choices=["dgb", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-step", action="store_true", help="skip the full TR-BDF2 step timing")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 20-step runs")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
