@@ -216,7 +216,8 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
         const size_t ncq = g.cell.size() / 10, nfq = g.face.size() / 22;
         const int nq = Q * Q * Q, nqf = Q * Q;
         std::vector<double> cm(ncq * 7), fn(nfq * 7);
-        for (size_t i = 0; i < ncq; ++i) {
+        parallel_cells(mesh.ncells, [&](int cl0, int cl1) {
+        for (size_t i = (size_t)cl0 * nq; i < (size_t)cl1 * nq; ++i) {
           const double* r = &g.cell[i * 10];
           const double jxw = r[9];
           const size_t c = i / nq;
@@ -231,7 +232,7 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
             }
           o[6 * nq] = jxw;
         }
-        for (size_t i = 0; i < nfq; ++i) {
+        for (size_t i = (size_t)cl0 * 6 * nqf; i < (size_t)cl1 * 6 * nqf; ++i) {
           const double* r = &g.face[i * 22];
           const double* n = r + 18;
           const size_t cf = i / nqf;  // cell * 6 + face
@@ -242,6 +243,7 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
           }
           o[6 * nqf] = r[21];
         }
+        });
         double* dcm = (double*)dalloc(cm.size() * sizeof(double));
         double* dfn = (double*)dalloc(fn.size() * sizeof(double));
         if (!dcm || !dfn) {
@@ -255,7 +257,8 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
         if (Q == ku + 2) {  // advection records of the deformed momentum kernel (SoA per cell)
           const int nq = Q * Q * Q, nqf = Q * Q;
           std::vector<double> ga((size_t)mesh.ncells * 9 * nq), gw((size_t)mesh.ncells * 18 * nqf);
-          for (int c = 0; c < mesh.ncells; ++c) {
+          parallel_cells(mesh.ncells, [&](int cl0, int cl1) {
+          for (int c = cl0; c < cl1; ++c) {
             for (int q = 0; q < nq; ++q) {
               const double* r = &g.cell[((size_t)c * nq + q) * 10];
               for (int i = 0; i < 9; ++i) ga[((size_t)c * 9 + i) * nq + q] = r[9] * r[i];
@@ -266,6 +269,7 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
                 for (int d = 0; d < 3; ++d) gw[(((size_t)c * 6 + f) * 3 + d) * nqf + t] = r[18 + d] * r[21];
               }
           }
+          });
           double* dga = (double*)dalloc(ga.size() * sizeof(double));
           double* dgw = (double*)dalloc(gw.size() * sizeof(double));
           if (!dga || !dgw) {

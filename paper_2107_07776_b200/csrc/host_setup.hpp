@@ -21,6 +21,8 @@
 #include <array>
 #include <cstdint>
 #include <string>
+#include <algorithm>
+#include <thread>
 #include <vector>
 
 namespace dgb {
@@ -87,6 +89,23 @@ struct QpGeometry {
 int cell_geo_stride(int dim);
 int face_geo_stride(int dim);
 void build_qp_geometry(const HostMesh& m, int Q, QpGeometry& g);
+// fn(c0, c1) over [0, n) split into contiguous chunks, one per host thread (setup loops)
+template <class Fn>
+inline void parallel_cells(int n, Fn fn) {
+  const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), 64));
+  if (nt == 1 || n < 4096) {
+    fn(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int per = (n + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const int c0 = t * per, c1 = std::min(n, c0 + per);
+    if (c0 < c1) th.emplace_back(fn, c0, c1);
+  }
+  for (auto& x : th) x.join();
+}
+
 
 /// Per-cell geometry for affine cells: {Jinv (dim^2), detJ} + per face {n (dim), ds}
 int affine_cell_stride(int dim);
