@@ -447,11 +447,27 @@ int Context::sip_diag(double mc, int dir, double* d) {
       return DGB_OK;
     }
   }
+  if (use_fast && !dc.affine && dim == 3) {
+    const cudaError_t e = fast_sip_diag3_qp(dc, mc, dir, d);
+    if (e != cudaErrorNotSupported) {
+      CK(e);
+      return DGB_OK;
+    }
+    cudaGetLastError();
+  }
   CK(opp->sip_diag(dc, mc, dir, d));
   return DGB_OK;
 }
 int Context::mass(int space, const double* x, double* y) {
   ++launches;
+  if (use_fast && !dc.affine && dim == 3) {
+    const cudaError_t e = fast_mass3_qp(dc, space == DGB_SPACE_U ? 0 : 1, x, y);
+    if (e != cudaErrorNotSupported) {
+      CK(e);
+      return DGB_OK;
+    }
+    cudaGetLastError();
+  }
   if (space == DGB_SPACE_U)
     CK(opu->mass(dc, 0, x, y));
   else
@@ -460,6 +476,17 @@ int Context::mass(int space, const double* x, double* y) {
 }
 int Context::mass_diag(int space, double* d) {
   ++launches;
+  if (use_fast && !dc.affine && dim == 3 && space == DGB_SPACE_U) {
+    // the momentum diagonal with mass 1, no viscous / advective terms: the exact mass
+    // diagonal at rule ku+1, the same for the three components (mass_diagonal)
+    const MomCoef co{1.0, 0.0, 0.0, 0.0};
+    const cudaError_t e = fast_momentum_diag3_qp(dc, co, nullptr, d);
+    if (e != cudaErrorNotSupported) {
+      CK(e);
+      return DGB_OK;
+    }
+    cudaGetLastError();
+  }
   if (space == DGB_SPACE_U)
     CK(opu->mass_diag(dc, 0, d));
   else

@@ -105,12 +105,14 @@ cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, doub
 cudaError_t fast_sip2(const DevCtx& c, double mc, int dir, const double* x, double* y);
 // deformed (per-qp geometry) 3D meshes (fast_deformed.cuh)
 cudaError_t fast_sip3_qp(const DevCtx& c, double mc, int dir, const double* x, double* y);
+cudaError_t fast_mass3_qp(const DevCtx& c, int pressure, const double* x, double* y);
 cudaError_t fast_momentum3(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);
 cudaError_t fast_momentum3_qp(const DevCtx& c, MomCoef co, const double* w, const double* x, double* y);
 cudaError_t fast_momentum_diag3(const DevCtx& c, MomCoef co, const double* w, double* y);
 cudaError_t fast_momentum_diag3_qp(const DevCtx& c, MomCoef co, const double* w, double* y);
 cudaError_t fast_divergence3(const DevCtx& c, const double* u, double* y);
 cudaError_t fast_sip_diag3(const DevCtx& c, double mc, int dir, double* y);
+cudaError_t fast_sip_diag3_qp(const DevCtx& c, double mc, int dir, double* y);
 struct CgState;
 // CG apply on the axis-aligned scalar SIP operator with <p, q> fused (fast_axis.cuh
 // k_sip_axis<.., CGF>): q = A p, block partials, alpha written to st by the last block

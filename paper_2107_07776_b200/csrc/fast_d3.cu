@@ -385,6 +385,35 @@ static cudaError_t run_sip_qp(const DevCtx& c, double mc, int dir, const double*
   k_sip_qp<KP><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, gc, gf, mc, dir, x, y);
   return cudaGetLastError();
 }
+template <int N, int Q, int NC>
+static cudaError_t run_mass_qp(const DevCtx& c, const double* x, double* y) {
+  const cudaError_t e = ensure_ftab<N, Q>();
+  if (e != cudaSuccess) return e;
+  const double* gc = c.qcm[Q];
+  if (!gc) return cudaErrorNotSupported;
+  using G = MassQpCfg<N, Q, NC>;
+  k_mass_qp<N, Q, NC><<<(c.ncells + G::W - 1) / G::W, G::T, 0, c.stream>>>(c.mesh, gc, x, y);
+  return cudaGetLastError();
+}
+// deformed mass: velocity (N = ku+1, rule ku+1, 3 components), pressure (N = kp+1, rule kp+2)
+cudaError_t fast_mass3_qp(const DevCtx& c, int pressure, const double* x, double* y) {
+  if (c.dim != 3 || c.affine) return cudaErrorNotSupported;
+  if (!pressure) {
+    switch (c.ku) {
+      case 1: return run_mass_qp<2, 2, 3>(c, x, y);
+      case 2: return run_mass_qp<3, 3, 3>(c, x, y);
+      case 3: return run_mass_qp<4, 4, 3>(c, x, y);
+      case 4: return run_mass_qp<5, 5, 3>(c, x, y);
+    }
+  } else {
+    switch (c.kp) {
+      case 1: return run_mass_qp<2, 3, 1>(c, x, y);
+      case 2: return run_mass_qp<3, 4, 1>(c, x, y);
+      case 3: return run_mass_qp<4, 5, 1>(c, x, y);
+    }
+  }
+  return cudaErrorNotSupported;
+}
 template <int KP>
 static cudaError_t run_sip_axis2(const DevCtx& c, double mc, int dir, const double* x, double* y) {
   const cudaError_t e = ensure_ftab<KP + 1, KP + 1>();
@@ -437,6 +466,32 @@ static cudaError_t run_momentum_diag_qp(const DevCtx& c, MomCoef co, const doubl
   const int grid = (c.ncells + G::C - 1) / G::C;
   k_momentum_diag_qp<K><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, gcA, gfA, gadv, gfw, co, w, y);
   return cudaGetLastError();
+}
+template <int KP>
+static cudaError_t run_sip_diag_qp(const DevCtx& c, double mc, int dir, double* y) {
+  cudaError_t e = ensure_ftab<KP + 1, KP + 2>();
+  if (e != cudaSuccess) return e;
+  using G = MomDiagQpCfg<KP, true>;
+  const double *gc = c.qcm[KP + 2], *gf = c.qfn[KP + 2];
+  if (!gc || !gf) return cudaErrorNotSupported;
+  if ((e = set_smem(k_momentum_diag_qp<KP, true>, G::SMEM)) != cudaSuccess) return e;
+  MomCoef co{};
+  co.mass = mc;
+  co.visc = 1.0;
+  const int grid = (c.ncells + G::C - 1) / G::C;
+  k_momentum_diag_qp<KP, true><<<grid, G::T, G::SMEM, c.stream>>>(c.mesh, gc, gf, nullptr, nullptr, co, nullptr, y,
+                                                                  dir);
+  return cudaGetLastError();
+}
+// deformed 3D meshes: the scalar SIP diagonal through the momentum-diagonal stages
+cudaError_t fast_sip_diag3_qp(const DevCtx& c, double mc, int dir, double* y) {
+  if (c.dim != 3 || c.affine) return cudaErrorNotSupported;
+  switch (c.kp) {
+    case 1: return run_sip_diag_qp<1>(c, mc, dir, y);
+    case 2: return run_sip_diag_qp<2>(c, mc, dir, y);
+    case 3: return run_sip_diag_qp<3>(c, mc, dir, y);
+  }
+  return cudaErrorNotSupported;
 }
 // deformed 3D meshes: the exact momentum diagonal, sum-factorised (fast_deformed.cuh)
 cudaError_t fast_momentum_diag3_qp(const DevCtx& c, MomCoef co, const double* w, double* y) {

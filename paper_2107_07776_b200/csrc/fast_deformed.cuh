@@ -977,9 +977,12 @@ namespace dgb {
 //         interior penalty / 2 sigma_K and c1 = 1 / 2 (interior / Dirichlet wall; outlets
 //         none), rule k+2 a_s phi^2 (a_s from qp_w_phase).
 // The value is the same for all three components (forms.cpp:635).  skew != 0: generic.
-template <int K>
+// SCALAR: the scalar SIP diagonal (pressure Helmholtz / Laplacian, helmholtz_diagonal
+// forms.cpp:246-334) through the same stages: K = kp, rule kp+2, no advection, one
+// component; boundary faces all Dirichlet (sdir = 1) or all natural (sdir = 0).
+template <int K, bool SCALAR = false>
 struct MomDiagQpCfg {
-  static constexpr int N = K + 1, QA = K + 1, QB = K + 2, NB = N * N * N, NF = N * N;
+  static constexpr int N = K + 1, QA = SCALAR ? K + 2 : K + 1, QB = K + 2, NB = N * N * N, NF = N * N;
   static constexpr int NQA = QA * QA * QA, NQFA = QA * QA, NQB = QB * QB * QB, NQFB = QB * QB;
   // W phase (as MomQpCfg)
   static constexpr int BX = 0, BY = BX + QB * NF, FPW = 0, NW = FPW + 6 * 2 * 3 * N * QB;
@@ -1000,18 +1003,19 @@ struct MomDiagQpCfg {
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
 
-template <int K>
-__global__ void __launch_bounds__(MomDiagQpCfg<K>::T) k_momentum_diag_qp(
+template <int K, bool SCALAR = false>
+__global__ void __launch_bounds__(MomDiagQpCfg<K, SCALAR>::T) k_momentum_diag_qp(
     MeshArgs m, const double* __restrict__ gcA, const double* __restrict__ gfA, const double* __restrict__ gadv,
-    const double* __restrict__ gfw, MomCoef co, const double* __restrict__ w, double* __restrict__ y) {
-  using G = MomDiagQpCfg<K>;
+    const double* __restrict__ gfw, MomCoef co, const double* __restrict__ w, double* __restrict__ y,
+    int sdir = 0) {
+  using G = MomDiagQpCfg<K, SCALAR>;
   constexpr int N = G::N, QA = G::QA, QB = G::QB, NB = G::NB, NF = G::NF;
   constexpr int NQA = G::NQA, NQFA = G::NQFA, NQB = G::NQB, NQFB = G::NQFB, C = G::C, PER = G::PER;
   extern __shared__ double sm[];
   const int c0 = blockIdx.x * C;
   const int nc = min(C, m.ncells - c0);
   const int tid = threadIdx.x, lane = tid & 31, wc = tid >> 5;
-  const bool adv = co.adv != 0.0;
+  const bool adv = !SCALAR && co.adv != 0.0;
   const double sfac = (double)(N * N);
   for (int idx = tid; adv && idx < nc * 3 * NB; idx += G::T) {
     const int c = idx / (3 * NB), i = idx - c * 3 * NB;
@@ -1024,7 +1028,7 @@ __global__ void __launch_bounds__(MomDiagQpCfg<K>::T) k_momentum_diag_qp(
     int ty = 0;
     if (nb < 0) {
       const int bid = -1 - nb;
-      ty = (bid >= 0 && bid < 64 && m.bctype[bid] == 1) ? 2 : 1;
+      ty = SCALAR ? (sdir ? 1 : 2) : ((bid >= 0 && bid < 64 && m.bctype[bid] == 1) ? 2 : 1);
     }
     cell[G::O_NB + f] = (double)nb;
     cell[G::O_TY + f] = (double)ty;
@@ -1043,7 +1047,7 @@ __global__ void __launch_bounds__(MomDiagQpCfg<K>::T) k_momentum_diag_qp(
   const double* tyv = cell + G::O_TY;
   const FTab<N, QA>& ta = c_ft<N, QA>;
   const FTab<N, QB>& tb = c_ft<N, QB>;
-  if (adv)
+  if (!SCALAR && adv)
     qp_w_phase<N, QB, G::BX, G::BY, G::FPW, G::NW>(cell + G::O_WS, W, WT, FC, nbv, tyv, w,
                                                    gadv + (size_t)cid * 9 * NQB, gfw + (size_t)cid * 18 * NQFB,
                                                    co.adv, lane);
@@ -1277,7 +1281,7 @@ __global__ void __launch_bounds__(MomDiagQpCfg<K>::T) k_momentum_diag_qp(
     __syncwarp();
   }
   // ---- store: cell + face-layer contributions, the same value for the three components
-  double* yc = y + (size_t)cid * 3 * NB;
+  double* yc = y + (size_t)cid * (SCALAR ? 1 : 3) * NB;
   for (int n = lane; n < NB; n += 32) {
     const int i = n % N, j = (n / N) % N, k = n / NF;
     const double* fo = W + G::FO;
@@ -1289,8 +1293,120 @@ __global__ void __launch_bounds__(MomDiagQpCfg<K>::T) k_momentum_diag_qp(
     if (k == 0) v += fo[4 * NF + i + N * j];
     if (k == N - 1) v += fo[5 * NF + i + N * j];
     yc[n] = v;
-    yc[NB + n] = v;
-    yc[2 * NB + n] = v;
+    if (!SCALAR) {
+      yc[NB + n] = v;
+      yc[2 * NB + n] = v;
+    }
+  }
+}
+
+// ===========================================================================
+// Mass (apply_mass, forms.cpp:337-360) on deformed cells: y = B^T diag(detJ w) B x per
+// component at rule Q, sum-factorised (three forward line passes N -> Q, the pointwise
+// detJ w, three transposed passes Q -> N), detJ w read from the compact per-qp record
+// (plane 6 of qcm[Q], [qx Q + qy + Q^2 qz]) — the generic kernel re-reads the full
+// 10-double record per point and component.  One warp per cell, NC components at once;
+// each line stage works in place on a Q^3 tile per component (a line is read whole
+// into registers before its Q outputs are written).
+// ===========================================================================
+template <int N, int Q, int NC>
+struct MassQpCfg {
+  static constexpr int NB = N * N * N, NQ = Q * Q * Q, W = 4, T = 32 * W;
+  static constexpr int S = NQ | 1;  // odd component stride
+};
+template <int N, int Q, int NC>
+__global__ void __launch_bounds__(MassQpCfg<N, Q, NC>::T, 1) k_mass_qp(MeshArgs m, const double* __restrict__ gc,
+                                                                     const double* __restrict__ x,
+                                                                     double* __restrict__ y) {
+  if (m.skip && *m.skip) return;
+  using G = MassQpCfg<N, Q, NC>;
+  constexpr int NB = G::NB, NQ = G::NQ, S = G::S, QQ = Q * Q;
+  __shared__ double sm[G::W][NC * S];
+  const FTab<N, Q>& tb = c_ft<N, Q>;
+  const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5;
+  const int cell = blockIdx.x * G::W + wc;
+  if (cell >= m.ncells) return;  // warp-uniform; no CTA barrier below
+  double* t = sm[wc];
+  const double* xc = x + (size_t)cell * NC * NB;
+  constexpr int LX = (NC * NB + 31) / 32, LQ = (NQ + 31) / 32;
+  double xv[LX], jv[LQ];  // every global load of the cell issued before the first use
+  const double* jw = gc + (size_t)cell * 7 * NQ + 6 * NQ;
+#pragma unroll
+  for (int j = 0; j < LX; ++j) {
+    const int i = lane + 32 * j;
+    xv[j] = i < NC * NB ? __ldg(xc + i) : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < LQ; ++j) {
+    const int i = lane + 32 * j;
+    const int qx = i % Q, qy = (i / Q) % Q, qz = i / QQ;
+    jv[j] = i < NQ ? __ldg(jw + qx * Q + qy + QQ * qz) : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < LX; ++j) {
+    const int i = lane + 32 * j;
+    if (i < NC * NB) {
+      const int comp = i / NB, r = i - comp * NB;
+      t[comp * S + r % N + Q * ((r / N) % N) + QQ * (r / (N * N))] = xv[j];
+    }
+  }
+  __syncwarp();
+  // forward: lines (comp, a, b) along dir with stride st; a < A, b < Bn
+  auto fwd = [&](int st, int sa, int A, int sb, int Bn) {
+#pragma unroll 1
+    for (int it = lane; it < NC * A * Bn; it += 32) {
+      const int comp = it / (A * Bn), r = it - comp * A * Bn;
+      double* ln = t + comp * S + (r % A) * sa + (r / A) * sb;
+      double u[N];
+#pragma unroll
+      for (int l = 0; l < N; ++l) u[l] = ln[l * st];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        double v = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) v = fma(tb.B[q][l], u[l], v);
+        ln[q * st] = v;
+      }
+    }
+    __syncwarp();
+  };
+  auto bwd = [&](int st, int sa, int A, int sb, int Bn) {
+#pragma unroll 1
+    for (int it = lane; it < NC * A * Bn; it += 32) {
+      const int comp = it / (A * Bn), r = it - comp * A * Bn;
+      double* ln = t + comp * S + (r % A) * sa + (r / A) * sb;
+      double v[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) v[q] = ln[q * st];
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        double u = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) u = fma(tb.B[q][l], v[q], u);
+        ln[l * st] = u;
+      }
+    }
+    __syncwarp();
+  };
+  fwd(1, Q, N, QQ, N);   // x-lines (iy, iz)
+  fwd(Q, 1, Q, QQ, N);   // y-lines (qx, iz)
+  fwd(QQ, 1, Q, Q, Q);   // z-lines (qx, qy)
+#pragma unroll
+  for (int j = 0; j < LQ; ++j) {
+    const int i = lane + 32 * j;
+    if (i < NQ)
+#pragma unroll
+      for (int comp = 0; comp < NC; ++comp) t[comp * S + i] *= jv[j];
+  }
+  __syncwarp();
+  bwd(QQ, 1, Q, Q, Q);   // z-lines (qx, qy)
+  bwd(Q, 1, Q, QQ, N);   // y-lines (qx, iz)
+  bwd(1, Q, N, QQ, N);   // x-lines (iy, iz)
+  double* yc = y + (size_t)cell * NC * NB;
+#pragma unroll
+  for (int i = lane; i < NC * NB; i += 32) {
+    const int comp = i / NB, r = i - comp * NB;
+    yc[i] = t[comp * S + r % N + Q * ((r / N) % N) + QQ * (r / (N * N))];
   }
 }
 

@@ -522,6 +522,32 @@ def test_host_buffer_applies_match_device_applies(ref, gpu, n_el, ku, kp, graded
     assert rel(yph, R.pressure(2.3, xp)) <= TOL_APPLY
 
 
+@pytest.mark.parametrize("n_el,ku,kp,amp", [(3, 1, 1, 0.05), (3, 2, 1, 0.05), (2, 3, 2, 0.04), (2, 4, 3, 0.03)])
+def test_deformed_mass_kernel_matches_reference_and_generic(ref, gpu, n_el, ku, kp, amp):
+    """fast_deformed.cuh k_mass_qp (sum-factorised B^T detJw B from the compact per-qp
+    records) vs the reference apply_mass and the generic device kernel, velocity (rule
+    ku+1, 3 components) and pressure (rule kp+2) spaces on distorted 3D meshes."""
+    R, D = pair(ref, gpu, 3, n_el, ku, kp, amp)
+    assert not D.affine
+    for space, n in ((gpu.SPACE_U, R.n_u), (gpu.SPACE_P, R.n_p)):
+        x = gpu.seeded_uniform(77 + space, n)
+        want = R.mass(space, x)
+        outs = []
+        for fast in (True, False):
+            D.set_fast_path(fast)
+            y = D.zeros(space)
+            gpu.apply_mass(D, space, dev(x), y)
+            outs.append(host(y))
+            assert rel(outs[-1], want) <= TOL_APPLY, (space, fast)
+        assert rel(outs[0], outs[1]) <= 1e-14
+    for fast in (True, False):  # velocity mass diagonal: k_momentum_diag_qp with mass only
+        D.set_fast_path(fast)
+        d = D.zeros()
+        gpu.mass_diagonal(D, gpu.SPACE_U, d)
+        assert rel(host(d), R.mass_diag(gpu.SPACE_U)) <= TOL_APPLY, ("mass diag", fast)
+    D.set_fast_path(True)
+
+
 @pytest.mark.parametrize("n_el,kp,amp", [(3, 1, 0.05), (2, 2, 0.04), (2, 3, 0.03)])
 def test_deformed_sip_kernel_matches_reference_and_generic(ref, gpu, n_el, kp, amp):
     """fast_deformed.cuh k_sip_qp (per-qp geometry streamed) vs the reference and the
@@ -544,6 +570,15 @@ def test_deformed_sip_kernel_matches_reference_and_generic(ref, gpu, n_el, kp, a
             yl = D.zeros(gpu.SPACE_P)
             gpu.apply_scalar_laplace(D, dirichlet, dev(xp), yl)
             assert rel(host(yl), want) <= TOL_APPLY, (dirichlet, fast)
+    # diagonals: k_momentum_diag_qp<kp, SCALAR> vs reference and generic
+    for fast in (True, False):
+        D.set_fast_path(fast)
+        d = D.zeros(gpu.SPACE_P)
+        gpu.helmholtz_diagonal(D, 2.3, d)
+        assert rel(host(d), R.helmholtz_diag(2.3)) <= TOL_APPLY, ("helmholtz diag", fast)
+        for dirichlet in (True, False):
+            gpu.scalar_laplace_diagonal(D, dirichlet, d)
+            assert rel(host(d), R.laplace_diag(dirichlet)) <= TOL_APPLY, ("laplace diag", dirichlet, fast)
     D.set_fast_path(True)
 
 
