@@ -233,8 +233,14 @@ struct GsPack {
 // Pairs of elements per thread (16-byte loads); the basis slots, w and uk are
 // 16-byte aligned (pool allocations); an odd tail element is taken by thread 0.
 constexpr int kGsThreads = 256;
+#ifndef DGB_GSD_MINB  // tuning overrides (tools/tune_gs.sh)
+#define DGB_GSD_MINB 1
+#endif
+#ifndef DGB_GS_CAP
+#define DGB_GS_CAP 8
+#endif
 template <int NV>
-__global__ void __launch_bounds__(kGsThreads) k_gs_dots_part(size_t n, GsPack P, const double* __restrict__ w,
+__global__ void __launch_bounds__(kGsThreads, DGB_GSD_MINB) k_gs_dots_part(size_t n, GsPack P, const double* __restrict__ w,
                                                            const double* __restrict__ uk, int nl,
                                                            double* __restrict__ partial) {
   double acc[2 * NV];
@@ -266,20 +272,48 @@ __global__ void __launch_bounds__(kGsThreads) k_gs_dots_part(size_t n, GsPack P,
   }
   block_reduce_store<2 * NV>(acc, partial);
 }
-__global__ void k_gs_solve(int k, const double* __restrict__ ab, double* __restrict__ L, int ldl,
-                           double* __restrict__ sv, double sk, double* __restrict__ h, double* __restrict__ g) {
-  if (threadIdx.x != 0) return;
-  sv[k] = sk;
-  // row k of the Gram matrix: L[k][j] = <v_k, v_j>, j < k
-  for (int j = 0; j < k; ++j) {
-    const double b = ab[(j / kGsChunk) * 2 * kGsChunk + kGsChunk + (j % kGsChunk)];
-    L[(size_t)k * ldl + j] = sk * sv[j] * b;
+// One warp: row k of the Gram matrix in parallel, then the unit lower-triangular solve
+// h_j = s_j <w, U_j> - sum_{i<j} h_i L_ji with each row's sum split over the lanes
+// (warp tree).  pre: the rows L_0..L_k are first copied into shared memory with all lanes
+// (one round of independent loads instead of a dependent global load per row).
+__global__ void __launch_bounds__(32) k_gs_solve(int k, const double* __restrict__ ab, double* __restrict__ L,
+                                                 int ldl, double* __restrict__ sv, double sk, double* __restrict__ h,
+                                                 double* __restrict__ g, int pre) {
+  extern __shared__ double gsm[];
+  const int lane = threadIdx.x, n = k + 1;
+  double* hs = gsm;          // h_j
+  double* ps = gsm + n;      // s_j <w, U_j>
+  double* ss = gsm + 2 * n;  // s_j
+  double* Ls = gsm + 3 * n;  // rows 0..k (pre)
+  for (int j = lane; j < n; j += 32) {
+    const double svj = j == k ? sk : sv[j];
+    ss[j] = svj;
+    ps[j] = svj * ab[(j / kGsChunk) * 2 * kGsChunk + (j % kGsChunk)];
+    if (j < k) {
+      const double v = sk * svj * ab[(j / kGsChunk) * 2 * kGsChunk + kGsChunk + (j % kGsChunk)];
+      L[(size_t)k * ldl + j] = v;
+      if (pre) Ls[k * n + j] = v;
+    }
   }
-  for (int j = 0; j <= k; ++j) {
-    double t = sv[j] * ab[(j / kGsChunk) * 2 * kGsChunk + (j % kGsChunk)];
-    for (int i = 0; i < j; ++i) t -= h[i] * L[(size_t)j * ldl + i];
-    h[j] = t;
-    g[j] = t * sv[j];
+  if (pre)
+    for (int idx = lane; idx < k * k; idx += 32) {
+      const int j = idx / k, i = idx - j * k;
+      if (i < j) Ls[j * n + i] = L[(size_t)j * ldl + i];
+    }
+  __syncwarp();
+  if (lane == 0) sv[k] = sk;
+  for (int j = 0; j < n; ++j) {
+    double part = 0.0;
+    for (int i = lane; i < j; i += 32) part = fma(hs[i], pre ? Ls[j * n + i] : L[(size_t)j * ldl + i], part);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    const double t = ps[j] - part;
+    if (lane == 0) {
+      hs[j] = t;
+      h[j] = t;
+      g[j] = t * ss[j];
+    }
+    __syncwarp();
   }
 }
 // zout != nullptr: also zout = dinv (.) w_new (the next Arnoldi step's preconditioned
@@ -408,7 +442,7 @@ cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q
 }
 static int gs_grid(size_t n) {
   size_t g = ((n >> 1) + kGsThreads - 1) / kGsThreads;
-  const size_t cap = (size_t)g_sms * 8;
+  const size_t cap = (size_t)g_sms * DGB_GS_CAP;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
@@ -434,7 +468,10 @@ cudaError_t gs_dots(cudaStream_t s, size_t n, int nv, const double* const* U, co
 }
 cudaError_t gs_solve(cudaStream_t s, int k, const double* d_ab, double* L, int ldl, double* d_s, double sk,
                      double* d_h, double* d_g) {
-  k_gs_solve<<<1, 32, 0, s>>>(k, d_ab, L, ldl, d_s, sk, d_h, d_g);
+  const size_t n = (size_t)k + 1;
+  if (3 * n * sizeof(double) > 48 * 1024) return cudaErrorInvalidValue;  // restart > 2047
+  const int pre = (3 * n + n * n) * sizeof(double) <= 48 * 1024;
+  k_gs_solve<<<1, 32, (3 * n + (pre ? n * n : 0)) * sizeof(double), s>>>(k, d_ab, L, ldl, d_s, sk, d_h, d_g, pre);
   return cudaGetLastError();
 }
 cudaError_t gs_update(cudaStream_t s, size_t n, int nv, const double* const* U, const double* g, double* w,
