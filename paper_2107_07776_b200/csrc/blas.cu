@@ -462,6 +462,10 @@ cudaError_t gs_dots(cudaStream_t s, size_t n, int nv, const double* const* U, co
     break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6) GS_CASE(7) GS_CASE(8)
     GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12) GS_CASE(13) GS_CASE(14) GS_CASE(15) GS_CASE(16)
+#if DGB_GS_CHUNK > 16
+    GS_CASE(17) GS_CASE(18) GS_CASE(19) GS_CASE(20) GS_CASE(21) GS_CASE(22) GS_CASE(23) GS_CASE(24)
+    GS_CASE(25) GS_CASE(26) GS_CASE(27) GS_CASE(28) GS_CASE(29) GS_CASE(30) GS_CASE(31) GS_CASE(32)
+#endif
 #undef GS_CASE
   }
   return cudaGetLastError();
@@ -485,6 +489,10 @@ cudaError_t gs_update(cudaStream_t s, size_t n, int nv, const double* const* U, 
   case NV: k_gs_update_part<NV><<<gr, kGsThreads, 0, s>>>(n, P, g, w, norm_out ? 1 : 0, scratch, dinv, zout); break;
     GS_CASE(1) GS_CASE(2) GS_CASE(3) GS_CASE(4) GS_CASE(5) GS_CASE(6) GS_CASE(7) GS_CASE(8)
     GS_CASE(9) GS_CASE(10) GS_CASE(11) GS_CASE(12) GS_CASE(13) GS_CASE(14) GS_CASE(15) GS_CASE(16)
+#if DGB_GS_CHUNK > 16
+    GS_CASE(17) GS_CASE(18) GS_CASE(19) GS_CASE(20) GS_CASE(21) GS_CASE(22) GS_CASE(23) GS_CASE(24)
+    GS_CASE(25) GS_CASE(26) GS_CASE(27) GS_CASE(28) GS_CASE(29) GS_CASE(30) GS_CASE(31) GS_CASE(32)
+#endif
 #undef GS_CASE
   }
   if (norm_out) k_sum_parts<<<1, kBlasThreads, 0, s>>>(gr, 1, scratch, norm_out, 0);

@@ -149,9 +149,15 @@ cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, double* partial, 
 //   h_j = <w, v_j> - sum_{i<j} h_i <v_i, v_j>,
 // which is MGS in exact arithmetic; the second pass applies w -= sum_j h_j v_j
 // and yields |w|^2.  2k+5 vector passes per Arnoldi step instead of 4(k+1).
-constexpr int kGsChunk = 16;
-// a_j = <w, U_j> (j < nv) and b_j = <uk, U_j> (j < nl) for one chunk of <= 16 vectors
-// -> d_ab[0..16) = a, d_ab[16..32) = b
+#ifndef DGB_GS_CHUNK  // basis vectors per Gram-Schmidt pass (16 or 32)
+#define DGB_GS_CHUNK 32
+#endif
+constexpr int kGsChunk = DGB_GS_CHUNK;
+// basis vectors per update pass: 16 (a 32-vector update pass measured slower at cfg3,
+// 148 vs 142 ms per stage, while the 32-vector dot pass is faster, 120 vs 125 ms)
+constexpr int kGsUpdChunk = 16;
+// a_j = <w, U_j> (j < nv) and b_j = <uk, U_j> (j < nl) for one chunk of <= kGsChunk vectors
+// -> d_ab[0..kGsChunk) = a, d_ab[kGsChunk..2 kGsChunk) = b
 cudaError_t gs_dots(cudaStream_t s, size_t n, int nv, const double* const* U, const double* w, const double* uk,
                     int nl, double* scratch, double* d_ab);
 // single-thread solve: row k of L from b, h (MGS projections) and g_j = h_j s_j

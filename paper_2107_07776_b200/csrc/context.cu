@@ -923,9 +923,9 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
       CK(gs_solve(st, k, d_ab, d_L, ldl, d_s, sh[k], d_h, d_g));
       if (gprof) cudaEventRecord(gev[2], st);
       // pass 2: w -= sum_j h_j v_j, |w|^2
-      for (int c0 = 0; c0 <= k; c0 += kGsChunk) {
-        const int nv = std::min(kGsChunk, k + 1 - c0);
-        const bool last = c0 + kGsChunk > k;
+      for (int c0 = 0; c0 <= k; c0 += kGsUpdChunk) {
+        const int nv = std::min(kGsUpdChunk, k + 1 - c0);
+        const bool last = c0 + kGsUpdChunk > k;
         for (int j = 0; j < nv; ++j) Uc[j] = gm_basis_[c0 + j];
         launches += last ? 2 : 1;
         CK(gs_update(st, n, nv, Uc, d_g + c0, w, gpart, last ? d_h + k + 1 : nullptr, inv, last ? z : nullptr));
