@@ -261,6 +261,26 @@ def test_krylov_iteration_parity(ref, gpu, dim, n_el, ku, kp, amp):
     assert rel(host(xu), xu_ref) <= 1e-8
 
 
+def test_gmres_long_restart_multi_chunk(ref, gpu):
+    """GMRES(80) with 147 reference iterations on a 3^3 Q3/Q2 advection-dominated momentum
+    system: Arnoldi steps with up to 80 basis vectors exercise every Gram-Schmidt chunking
+    path (32-vector dot passes, 16-vector update passes); iterations +-1, solution 1e-8."""
+    R, D = pair(ref, gpu, 3, 3, 3, 2)
+    coefs = (10.0, 1e-3, 1.0, 0.0)
+    w = gpu.seeded_uniform(62, R.n_u)
+    bu = gpu.seeded_uniform(63, R.n_u)
+    xu_ref, itu_ref, _ = R.solve(0, 1, coefs, w, bu, np.zeros(R.n_u), restart=80)
+    assert itu_ref > 80
+    ctx = gpu.MomentumCtx(*coefs, advecting=dev(w))
+    diag = D.zeros()
+    gpu.momentum_diagonal(D, ctx, diag)
+    M = gpu.JacobiPreconditioner(D, diag)
+    xu = D.zeros()
+    res = gpu.gmres_solve(D, gpu.LinearOperator.momentum(ctx), dev(bu), gpu.SolverSettings(restart=80), M, xu)
+    assert abs(res.iterations - itu_ref) <= 1
+    assert rel(host(xu), xu_ref) <= 1e-8
+
+
 def test_solver_budget_exhaustion_raises_with_history(ref, gpu):
     """test_krylov.cpp:317-341: SolverError carries a history of length max_iter."""
     R, D = pair(ref, gpu, 2, 4, 2, 1)
