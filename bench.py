@@ -218,6 +218,65 @@ def trbdf2_step_time(D, dg, torch, stream, precond="jacobi"):
                       "c 1e3, GMRES restart 30 / CG, rel tol 1e-10 (mass 1e-12); pressure CG preconditioner: " + precond}
 
 
+def cfg4_run(dg, torch, stream, hbm_peak):
+    """BASELINE configs[3] (cfg4): 48^3 deformed Q4/Q3 (interior vertices displaced by
+    U[-0.1h, 0.1h], seed 3; per-quadrature-point geometry).  Momentum / pressure apply
+    times (CUDA events, 10 applies after 3) against the HBM roofline with SURVEY 8(d)'s
+    per-DoF bytes, then one TR-BDF2 step (second of two from u^0) with the reference's
+    Jacobi CG and with the multigrid pressure CG.  Outside the timed op-apply region."""
+    import time as _t
+    n_el, ku, kp, seed, Re = 48, 4, 3, 3, 100.0
+    t0 = _t.time()
+    D = dg.DGContext(3, n_el, ku, kp, 0.1 / n_el, seed)
+    setup = _t.time() - t0
+    f = dg.SynthField(3, seed)
+    for bid in range(6):
+        D.set_dirichlet_fn(bid, f.fn_ptr, f.user_ptr, 0.0)
+    u0 = D.zeros()
+    dg.interpolate_synth_device(D, f, u0)
+    x = torch.from_numpy(dg.seeded_uniform(seed + 1000, D.n_u)).cuda()
+    xp = torch.from_numpy(dg.seeded_uniform(seed + 2000, D.n_p)).cuda()
+    y, yp = D.zeros(), D.zeros(dg.SPACE_P)
+    g = 2.0 - 2.0 ** 0.5
+    ctx = dg.MomentumCtx(1.0 / (g * 1e-3), 1.0 / (2.0 * Re), 0.5, 0.0, advecting=u0)
+    pmc = 1.0 / (1e6 * g * g * 1e-6)
+    out = {"config": "cfg4: 3D 48^3 unit cube, interior vertices displaced U[-0.1h, 0.1h] (seed 3), Q4/Q3, "
+                     "per-quadrature-point geometry, Re 100, dt 1e-3, GMRES restart 50 / CG tol 1e-10",
+           "setup_s": setup, "fast_path": "deformed" if D.fast_path_active else "generic",
+           "n_u": D.n_u, "n_p": D.n_p}
+    for name, fn, n, bpd in (("momentum", lambda: dg.apply_momentum(D, ctx, x, y), D.n_u, 182.6),
+                             ("pressure", lambda: dg.apply_pressure_helmholtz(D, pmc, xp, yp), D.n_p, 378.5)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(10):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        gbs = bpd * n / ms / 1e6
+        out[name] = {"ms": ms, "gdofs": n / ms / 1e6, "hbm_gbs_alg": gbs, "bytes_per_dof_alg": bpd,
+                     "hbm_frac": gbs / hbm_peak if hbm_peak else None}
+    del x, xp, y, yp
+    p0 = D.zeros(dg.SPACE_P)
+    u1, p1 = D.zeros(), D.zeros(dg.SPACE_P)
+    for precond in ("jacobi", "mg"):
+        sp = dg.StepParams(dt=1e-3, Re=Re, c=1e3, restart=50, first_step=True, pressure_precond=precond)
+        dg.trbdf2_step(D, sp, u0, u0, p0, u1, p1)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        its = dg.trbdf2_step(D, sp, u0, u0, p0, u1, p1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out["step_" + precond] = {"s_per_step": e0.elapsed_time(e1) * 1e-3, "krylov_its": [int(i) for i in its]}
+    del D, u0, p0, u1, p1
+    torch.cuda.empty_cache()
+    return out
+
+
 def cfg5_steps(dg, torch, stream, precond="jacobi", nsteps=20):
     """BASELINE configs[4]: 20 consecutive TR-BDF2 steps at 96^3 Q2/Q1, Re 1600, initial
     field (seed 4) scaled to max nodal |u| = 1, dt for CFL 0.5, GMRES(50) /
@@ -366,6 +425,13 @@ def run_device(args):
                         "note": "same step with the multigrid-preconditioned pressure CG (opt-in; not the reference's "
                                 "Jacobi, so CG iteration counts differ by design; fields agree to the solve tolerance)"}
 
+    # ---- BASELINE configs[3] (cfg4, deformed): applies vs the HBM roofline + one step each solver
+    cfg4 = None
+    if not args.no_step and not args.no_cfg4:
+        cfg4 = cfg4_run(dg, torch, stream, measured_peaks().get("hbm_gbs"))
+        for k in ("step_jacobi", "step_mg"):
+            cfg4[k]["s_per_step"] = reduce_max(cfg4[k]["s_per_step"])
+
     # ---- BASELINE configs[4] (cfg5): 20 consecutive steps, the parity (Jacobi) solver and
     #      the multigrid pressure CG; outside the timed op-apply region
     cfg5 = None
@@ -430,6 +496,7 @@ def run_device(args):
                 "d2h_bytes_per_step": 8 * (D.n_u + D.n_p)},
         "gpu_launches": int(launches), "clocks": clocks, "setup_s": setup_s,
         "trbdf2": trbdf2,
+        "cfg4": cfg4,
         "cfg5_steps": cfg5,
     }
     print(json.dumps(line), flush=True)
@@ -447,6 +514,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-step", action="store_true", help="skip the full TR-BDF2 step timing")
     ap.add_argument("--no-cfg5", action="store_true", help="skip the cfg5 20-step runs")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the cfg4 (deformed) applies and steps")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
