@@ -474,7 +474,13 @@ struct SipAxisCfg {
   static constexpr bool WPG = C % CPW == 0 && T == 32 * (C / CPW);
   static constexpr int O_U = 0, O_SX = P::CT, O_SY = 2 * P::CT, O_SZ = 3 * P::CT, O_UX = 4 * P::CT;
   static constexpr int O_INFO = 5 * P::CT;
-  static constexpr int PER = (O_INFO + kInfoDoubles) | 1;
+  // KP = 1: the per-cell stride is 10 mod 16 doubles and the warp's line items run
+  // cell-fastest (CF): the 8 cells of a warp then sit on distinct even bank pairs and the
+  // second line of each half-warp on the odd ones — conflict-free line stages (bank
+  // simulation: 178 -> 80 wavefronts per warp-group vs an ideal of 80; ncu had 45 % of
+  // the kernel's shared wavefronts as conflicts)
+  static constexpr bool CF = KP == 1 && WPG;
+  static constexpr int PER = CF ? O_INFO + kInfoDoubles + 1 : (O_INFO + kInfoDoubles) | 1;
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
 
@@ -509,6 +515,16 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
   constexpr int IST = WPG ? 32 : TT;
   const int gbase = WPG ? wbase : 0;
   const int gcnt = WPG ? max(0, min(CPW, nc - wbase)) : nc;
+  // item -> (cell of the group, rest): cell-major, or cell-fastest for CF
+  auto split = [&](int idx, int X, int& cl, int& r) {
+    if (G::CF) {
+      cl = gcnt == CPW ? idx % CPW : idx % gcnt;
+      r = gcnt == CPW ? idx / CPW : idx / gcnt;
+    } else {
+      cl = idx / X;
+      r = idx - cl * X;
+    }
+  };
 #define CELL(c) (sm + (c) * PER)
 #define INFO(c) (*reinterpret_cast<CellInfo*>(sm + (c) * PER + G::O_INFO))
 #define SYNC_G()       \
@@ -536,7 +552,9 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
   SYNC_G();
   // A: all-direction lines: S_d on raw lines (+ neighbour lines), and Ux = M_x u
   for (int idx = it0; idx < gcnt * 3 * NF; idx += IST) {
-    const int cl = idx / (3 * NF), c = gbase + cl, r = idx - cl * 3 * NF;
+    int cl, r;
+    split(idx, 3 * NF, cl, r);
+    const int c = gbase + cl;
     const int d = r / NF, tl = r - d * NF;
     const int p = tl % N, q = tl / N;
     const CellInfo& ci = INFO(c);
@@ -570,7 +588,9 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
   SYNC_G();
   // B: x-lines, in place: SY <- M_x SY, SZ <- M_x SZ
   for (int idx = it0; idx < gcnt * NF; idx += IST) {
-    const int cl = idx / NF, c = gbase + cl, tl = idx - cl * NF;
+    int cl, tl;
+    split(idx, NF, cl, tl);
+    const int c = gbase + cl;
     const int b0 = P::idx(0, tl % N, tl / N);
     double a[N], b[N];
 #pragma unroll
@@ -593,7 +613,9 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
   SYNC_G();
   // C: y-lines: SX <- M_y (SX + mc detJ UX) + SY ; SZ <- M_y SZ
   for (int idx = it0; idx < gcnt * NF; idx += IST) {
-    const int cl = idx / NF, c = gbase + cl, tl = idx - cl * NF;
+    int cl, tl;
+    split(idx, NF, cl, tl);
+    const int c = gbase + cl;
     const int b0 = P::idx(tl % N, 0, tl / N);
     const double cm = mc * INFO(c).detJ;
     double a[N], b[N], e[N];
@@ -619,7 +641,9 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
   // D: z-lines: y = M_z SX + SZ   -> global
   double pq[1] = {0.0};
   for (int idx = it0; idx < gcnt * NF; idx += IST) {
-    const int cl = idx / NF, c = gbase + cl, tl = idx - cl * NF;
+    int cl, tl;
+    split(idx, NF, cl, tl);
+    const int c = gbase + cl;
     const int i = tl % N, j = tl / N;
     const int b0 = P::idx(i, j, 0);
     double a[N];
