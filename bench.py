@@ -14,8 +14,10 @@ apply (mass_coef 1/(c^2 gamma^2 dt^2)), on U[-1,1] seeded vectors (seeds
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
 --impl reference times the unmodified reference CPU implementation
-(oracle/_ref/libdgref.so: /root/reference/proj/src compiled as-is) with all
-host threads on a bounded sample of the same workload.
+(oracle/_ref/libdgref.so: /root/reference/proj/src compiled as-is) on the same
+cfg3 workload with all host threads: the 64^3 mesh as z-slabs, one reference
+context per slab (the reference is single-threaded), inputs from the oracle-side
+generator (no product library in that process).
 """
 from __future__ import annotations
 
@@ -41,7 +43,18 @@ CFG = dict(workload="cfg3: 3D 64^3 unit cube affine, Q3/Q2 velocity/pressure, fp
 # algorithmic fp64 flop / DoF and bytes / DoF at cfg3
 FLOP_PER_DOF = {"momentum": 545.9, "pressure": 406.2}
 BYTES_PER_DOF = {"momentum": 24.0, "pressure": 16.0}
-CPU_SAMPLE_NEL = 16   # reference CPU leg: same degrees/coefficients on a 16^3 mesh
+METRIC = "fp64 DG op-apply throughput (momentum + pressure), GDoF/s"
+DATA = "synthetic (seeded; BASELINE cfg3 vector-potential field, U[-1,1] vectors)"
+
+
+def bench_config(ws: int) -> dict:
+    """The config dict both arms print (identical, so the driver can pair them)."""
+    n, ku, kp = CFG["n_el"], CFG["ku"], CFG["kp"]
+    return {"workload": CFG["workload"], "mesh": f"{n}^3", "degrees": f"Q{ku}/Q{kp}",
+            "n_u": 3 * n ** 3 * (ku + 1) ** 3, "n_p": n ** 3 * (kp + 1) ** 3,
+            "Re": CFG["Re"], "dt": CFG["dt"], "c": CFG["c"], "parallelism": f"replicas x{ws}",
+            "l2": "inputs larger than L2 (x, w 403 MB each); the momentum apply streams 1.2 GB between "
+                  "pressure applies"}
 
 
 def coefficients():
@@ -131,59 +144,86 @@ def whole_job_rate(ws: int, units_per_rank: int, ms_max: float) -> float:
 
 
 # ---------------------------------------------------------------------------
-# reference CPU leg
+# reference CPU leg (TEST INFRASTRUCTURE: the unmodified reference, oracle/_ref)
 # ---------------------------------------------------------------------------
-def reference_sample(nthreads: int, napplies: int):
-    """Times the unmodified reference apply_momentum + apply_pressure_helmholtz on
-    nthreads concurrent host threads (the reference is single-threaded; each
-    thread runs its own applies) on a CPU_SAMPLE_NEL^3 mesh, same degrees and
-    coefficients.  Returns (DoF/s, seconds, dofs per thread-step, description)."""
-    import reforacle
-    import paper_2107_07776_b200 as dg  # synthetic inputs only (host code)
-    R = reforacle.RefCtx(CFG["dim"], CPU_SAMPLE_NEL, CFG["ku"], CFG["kp"])
+def reference_slabs(nslabs: int, z_list=None, nthreads: int = 1):
+    """The cfg3 workload for the unmodified reference, cut into z-slabs.
+
+    The 64^3 mesh is split into `nslabs` slabs of 64 x 64 x (64 / nslabs) cells; each
+    slab is its own reference Mesh / GeometryCache / FunctionSpace pair (oracle
+    ref_create_slab: cells bit-identical to the full mesh's, the slab's own z-ends are
+    boundary faces) holding the cfg3 inputs of its cells: w = the seeded
+    vector-potential field interpolated by FunctionSpace::interpolate, x / xp = its
+    contiguous cell range of the full U[-1,1] vectors (seeds 1002 / 2002).  Inputs come
+    from the oracle-side generator only (reforacle; no product library is loaded).
+    Returns the RefCtx list (each ready for pair_rounds) and the DoFs it covers."""
+    import reforacle as ref
+    n, ku, kp = CFG["n_el"], CFG["ku"], CFG["kp"]
+    nz = n // nslabs
+    nbu, nbp = 3 * (ku + 1) ** 3, (kp + 1) ** 3
     mom, pmc = coefficients()
-    f = dg.SynthField(CFG["dim"], CFG["seed"])
-    # w at the reference nodes (host evaluation of the same field)
-    w = np.zeros(R.n_u)
-    xn = np.zeros((R.ncells, (CFG["ku"] + 1) ** 3, 3))
-    reforacle.lib().ref_node_points(R.h, 0, reforacle.P(xn))
-    nb = (CFG["ku"] + 1) ** 3
-    for cell in range(R.ncells):
-        for j in range(nb):
-            v = f.eval(xn[cell, j])
-            for comp in range(3):
-                w[cell * 3 * nb + comp * nb + j] = v[comp]
-    x = dg.seeded_uniform(CFG["seed"] + 1000, R.n_u)
-    xp = dg.seeded_uniform(CFG["seed"] + 2000, R.n_p)
-    t_m = R.bench(0, mom, w, x, nthreads, napplies)
-    t_p = R.bench(1, (pmc, 0, 0, 0), None, xp, nthreads, napplies)
-    dofs = (R.n_u + R.n_p) * nthreads * napplies
-    secs = t_m + t_p
-    desc = (f"{CPU_SAMPLE_NEL}^3 mesh, Q3/Q2, same coefficients; {napplies} momentum + {napplies} pressure "
-            f"applies per thread, {nthreads} thread(s); reference backend {reforacle.lib().ref_backend().decode()}")
-    return dofs / secs, secs, R.n_u + R.n_p, desc, {"momentum_s_per_apply": t_m / napplies,
-                                                      "pressure_s_per_apply": t_p / napplies,
-                                                      "n_u": R.n_u, "n_p": R.n_p}
+    f = ref.SynthField(3, CFG["seed"])
+    x = ref.seeded_uniform(CFG["seed"] + 1000, n ** 3 * nbu)
+    xp = ref.seeded_uniform(CFG["seed"] + 2000, n ** 3 * nbp)
+    ctxs, dofs = [], 0
+    for s in (range(nslabs) if z_list is None else z_list):
+        R = ref.RefCtx.slab(n, s * nz, nz, ku, kp)
+        c0, c1 = s * nz * n * n, (s + 1) * nz * n * n
+        R.pair_setup(mom, f.interpolate(R, nthreads), x[c0 * nbu:c1 * nbu], pmc, xp[c0 * nbp:c1 * nbp])
+        ctxs.append(R)
+        dofs += R.n_u + R.n_p
+    return ctxs, dofs
+
+
+def reference_nslabs(ncores: int) -> int:
+    """Smallest power of two >= the host threads (one slab per thread), within 16..64."""
+    k = 16
+    while k < min(ncores, 64):
+        k *= 2
+    return k
+
+
+def cpu_baseline_1core():
+    """SURVEY 8(d) CPU baseline: the reference on ONE host core, median of 3 applies
+    after one warm-up apply (the warm-up also pays the lazy GeometryCache build), on a
+    bounded sample of the cfg3 workload: one 64 x 64 x 4 z-slab (1/16 of the cells)."""
+    import reforacle as ref
+    ctxs, dofs = reference_slabs(16, z_list=[8])
+    ref.pair_rounds(ctxs, 1, 1)
+    t = float(np.median(ref.pair_rounds(ctxs, 1, 3)))
+    return {"value": dofs / t / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "reference",
+            "sample": "cfg3 workload, one 64x64x4 z-slab of the 64^3 mesh (16,384 of 262,144 cells, cfg3 inputs of "
+                      "those cells): median of 3 momentum+pressure apply pairs after 1 warm-up, 1 core, reference "
+                      f"backend {ref.lib().ref_backend().decode()}",
+            "detail": {"s_per_apply_pair": t, "dofs": dofs,
+                       "modelled_full_cfg3_s_per_apply_pair": t * 16}}
 
 
 def run_reference(args):
     ws, rank, _ = dist_info()
     if rank != 0:
         return
-    nthreads = max(1, os.cpu_count() or 1)
-    for _ in range(args.warmup):
-        pass  # the reference leg warms its lazy geometry cache inside each ref_bench call
-    rate, secs, _, desc, extra = reference_sample(nthreads, max(1, args.steps))
-    val = rate / 1e9
-    line = {"metric": "fp64 DG op-apply throughput (momentum + pressure), GDoF/s", "value": val,
-            "unit": "GDoF/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": secs / max(1, args.steps) * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE cfg3 construction)",
-            "config": {"workload": CFG["workload"], "sample": desc}, "impl": "reference",
-            "cpu_baseline": {"value": val, "unit": "GDoF/s", "cores": nthreads, "kind": "reference",
-                             "sample": desc},
+    import reforacle as ref
+    ncores = max(1, os.cpu_count() or 1)
+    nslabs = reference_nslabs(ncores)
+    t0 = time.time()
+    ctxs, dofs = reference_slabs(nslabs, nthreads=ncores)
+    ref.pair_rounds(ctxs, ncores, max(1, args.warmup))  # the first round builds the lazy geometry
+    setup_s = time.time() - t0
+    times = ref.pair_rounds(ctxs, ncores, max(1, args.steps))
+    secs = float(times.sum())
+    val = dofs * len(times) / secs / 1e9
+    desc = (f"the whole cfg3 64^3 Q3/Q2 workload every step, as {nslabs} z-slabs of 64x64x{CFG['n_el'] // nslabs} "
+            f"cells (one reference context each; slab ends are boundary faces) spread over {ncores} host threads; "
+            f"reference backend {ref.lib().ref_backend().decode()}")
+    line = {"metric": METRIC, "value": val, "unit": "GDoF/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": max(1, args.warmup), "ms_per_step": secs / len(times) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": DATA, "config": bench_config(ws),
+            "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": "GDoF/s", "cores": ncores, "kind": "reference", "sample": desc},
             "e2e": {"value": val, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "detail": extra}
+            "detail": {"dofs_per_step": dofs, "setup_and_warmup_s": setup_s,
+                       "step_s": [float(t) for t in times]}}
     print(json.dumps(line), flush=True)
 
 
@@ -474,21 +514,14 @@ def run_device(args):
     cpu = None
     if ws == 1 and not args.no_cpu:
         try:
-            rate, secs, _, desc, extra = reference_sample(1, 1)
-            cpu = {"value": rate / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "reference", "sample": desc,
-                   "detail": extra}
+            cpu = cpu_baseline_1core()
         except Exception as e:  # oracle not built on this box
             cpu = {"value": None, "unit": "GDoF/s", "cores": 1, "kind": "reference", "sample": f"unavailable: {e}"}
     line = {
-        "metric": "fp64 DG op-apply throughput (momentum + pressure), GDoF/s",
+        "metric": METRIC,
         "value": value, "unit": "GDoF/s", "n_gpus": ws, "steps": args.steps, "warmup": max(3, args.warmup),
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded; BASELINE cfg3 vector-potential field, U[-1,1] vectors)",
-        "config": {"workload": CFG["workload"], "mesh": "64^3", "degrees": "Q3/Q2", "n_u": D.n_u, "n_p": D.n_p,
-                   "Re": CFG["Re"], "dt": CFG["dt"], "c": CFG["c"], "parallelism": f"replicas x{ws}",
-                   "l2": "inputs larger than L2 (x, w 403 MB each); the momentum apply streams 1.2 GB between "
-                         "pressure applies",
-                   "warmup_steps_run": nwarm},
+        "data": DATA, "config": bench_config(ws), "warmup_steps_run": nwarm,
         "ops": {"momentum": {"ms": tm * 1e3, "gdofs": D.n_u / tm / 1e9, "tflops_alg": mom_tflops},
                 "pressure": {"ms": tp * 1e3, "gdofs": D.n_p / tp / 1e9, "tflops_alg": prs_tflops}},
         "roofline": roofline, "roofline_hbm": roofline_hbm, "cpu_baseline": cpu,

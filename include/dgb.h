@@ -152,12 +152,17 @@ int dgb_check_steady(dgb_ctx* ctx, const double* d_u_new, const double* d_u_old,
 int dgb_stability_params(dgb_ctx* ctx, double dt, double Re, double U, double* C, double* mu);
 
 /* ------------------------------------------------------------------ vector kernels */
-/* kern::axpy/axpby/scal/dot/max_abs_diff (kernels.hpp:34-43) on device vectors */
+/* kern::axpy/axpby/scal/dot/max_abs_diff (kernels.hpp:34-43) on device vectors.
+ * axpy = fma(a, x, y) and axpby = fma(a, x, b*y) elementwise, bit-identical to the
+ * reference's AVX2 backend (kernels_avx2.cpp:12-33); dot / norm reassociate the sum
+ * (single-pass block reduction).  dgb_norm = sqrt(dot(x, x)) (the 2-norm the solvers
+ * use, krylov.cpp:54-56; SURVEY 8(b) "fused dgb_axpy/axpby/dot/norm"). */
 int dgb_axpy(dgb_ctx* ctx, size_t n, double a, const double* d_x, double* d_y);
 int dgb_axpby(dgb_ctx* ctx, size_t n, double a, const double* d_x, double b, double* d_y);
 int dgb_scal(dgb_ctx* ctx, size_t n, double a, double* d_x);
 int dgb_dot(dgb_ctx* ctx, size_t n, const double* d_x, const double* d_y, double* result);
 int dgb_max_abs_diff(dgb_ctx* ctx, size_t n, const double* d_x, const double* d_y, double* result);
+int dgb_norm(dgb_ctx* ctx, size_t n, const double* d_x, double* result);
 
 /* ------------------------------------------------------------------ solvers */
 /* SolverSettings (krylov.hpp:24-29) */
@@ -184,7 +189,9 @@ typedef struct {
 /* JacobiPreconditioner (krylov.hpp:40-48): d_inv = 1/d_diag; DGB_E_ZERO_DIAG names the dof. */
 int dgb_jacobi_inverse(dgb_ctx* ctx, size_t n, const double* d_diag, double* d_inv);
 /* cg_solve / gmres_solve (krylov.hpp:58-66): d_x is initial guess and result;
- * d_inv_diag NULL = unpreconditioned.  On DGB_E_NO_CONVERGENCE / BREAKDOWN /
+ * d_inv_diag NULL = unpreconditioned.  Any 8-byte-aligned d_inv_diag is accepted
+ * (GMRES copies one that is not 16-byte aligned to an aligned scratch vector first:
+ * its Gram-Schmidt pass reads it as double2).  On DGB_E_NO_CONVERGENCE / BREAKDOWN /
  * NOT_SPD the residual history (SolverError::history) is copied to hist_host
  * (up to hist_cap entries) and its full length stored in *hist_len. */
 int dgb_cg(dgb_ctx* ctx, const dgb_operator* op, const dgb_solver_settings* s, const double* d_inv_diag,

@@ -12,9 +12,13 @@
 #include "support/dense_oracle.hpp"
 #include "trbdf2_cpu.hpp"
 
+#include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstring>
+#include <cmath>
 #include <memory>
+#include <random>
 #include <string>
 #include <thread>
 #include <vector>
@@ -64,8 +68,11 @@ struct Base {
   virtual void cell_vertices(double* xv) = 0;
   virtual void bface_points(int rule, double* xq) = 0;
   virtual void interpolate_nodes(int space, double* xn) = 0;
+  virtual void interpolate_fn(ref_bc_fn fn, void* user, double* u, int nthreads) = 0;
   virtual double bench(int op, const double* coefs, const double* w, const double* x, int nthreads,
                        int napplies) = 0;
+  virtual void pair_setup(const double* c, const double* w, const double* x, double pmc, const double* xp) = 0;
+  virtual void pair_run() = 0;
   virtual void dense_momentum(const double* c, const double* w, double* A) = 0;
   virtual void dense_scalar_sip(double mc, int dir, int rule, double* A) = 0;
 };
@@ -372,6 +379,29 @@ struct Ctx : Base {
       }
     }
   }
+  // FunctionSpace::interpolate (space.cpp:239-253) with a C callback, the cells split
+  // over nthreads (each thread writes its own cells; same values as the serial loop).
+  void interpolate_fn(ref_bc_fn fn, void* user, double* u, int nthreads) override {
+    const int nc = mesh.n_active(), nb = Vu->nb();
+    auto run = [&](int c0, int c1) {
+      double tmp[3];
+      for (int i = c0; i < c1; ++i) {
+        const int c = mesh.active_cells()[i];
+        const size_t off = static_cast<size_t>(i) * dim * nb;
+        for (int j = 0; j < nb; ++j) {
+          const auto x = mesh.map_point(c, Vu->nodes()[j]);
+          fn(x.data(), 0.0, tmp, user);
+          for (int comp = 0; comp < dim; ++comp) u[off + comp * nb + j] = tmp[comp];
+        }
+      }
+    };
+    nthreads = std::max(1, nthreads);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nthreads; ++t)
+      th.emplace_back(run, static_cast<int>((long long)nc * t / nthreads),
+                      static_cast<int>((long long)nc * (t + 1) / nthreads));
+    for (auto& t : th) t.join();
+  }
   // Throughput of the reference CPU apply: nthreads concurrent independent
   // applies (reference code is single-threaded; caches are warmed first so the
   // lazily-filled GeometryCache / trace tables are read-only during the run).
@@ -401,6 +431,22 @@ struct Ctx : Base {
     for (auto& t : th) t.join();
     const auto t1 = std::chrono::steady_clock::now();
     return std::chrono::duration<double>(t1 - t0).count();
+  }
+  // bench.py reference arm: one apply_momentum + one apply_pressure_helmholtz
+  // (forms.cpp:389-604, 1090-1095) on inputs held by the context; outputs are
+  // resized and zeroed by the callee every call, exactly as in the reference.
+  Field pw, px, pxp, pyu, pyp;
+  double pc[4] = {0, 0, 0, 0}, ppmc = 0.0;
+  void pair_setup(const double* c, const double* w, const double* x, double pmc, const double* xp) override {
+    std::copy(c, c + 4, pc);
+    ppmc = pmc;
+    pw = F(w, nu());
+    px = F(x, nu());
+    pxp = F(xp, np());
+  }
+  void pair_run() override {
+    apply_momentum(*Vu, *geom, mctx(pc, &pw), px, pyu);
+    apply_pressure_helmholtz(*Vp, *geom, ppmc, pxp, pyp);
   }
   void dense_momentum(const double* c, const double* w, double* A) override {
     Field wf = w ? F(w, nu()) : Field();
@@ -448,9 +494,133 @@ Mesh<dim> mesh_from_arrays(int nv, const double* xv, int nc, const int* cv, cons
   return m;
 }
 
+// A z-slab [0,1]^2 x [z0/n, (z0+nz)/n] of generate_cartesian<3>(n, 0, 1)
+// (mesh.cpp:572-615): the same vertex coordinates lo + (hi-lo)*id/n, the same
+// lexicographic vertex / cell order; the slab's own bottom / top faces carry
+// boundary ids 4 / 5.  Every cell is bit-identical to the corresponding cell of
+// the full mesh, so per-cell reference work equals the full config's.
+Mesh<3> slab_mesh(int n, int z0, int nz) {
+  if (n < 1 || nz < 1 || z0 < 0 || z0 + nz > n) throw std::invalid_argument("slab_mesh: bad extent");
+  const int nx = n + 1, nzv = nz + 1;
+  std::vector<double> xv(static_cast<size_t>(nx) * nx * nzv * 3);
+  for (int k = 0; k < nzv; ++k)
+    for (int j = 0; j < nx; ++j)
+      for (int i = 0; i < nx; ++i) {
+        double* p = &xv[3 * ((static_cast<size_t>(k) * nx + j) * nx + i)];
+        p[0] = 0.0 + (1.0 - 0.0) * i / n;
+        p[1] = 0.0 + (1.0 - 0.0) * j / n;
+        p[2] = 0.0 + (1.0 - 0.0) * (z0 + k) / n;
+      }
+  const int nc = n * n * nz;
+  std::vector<int> cv(static_cast<size_t>(nc) * 8), bid(static_cast<size_t>(nc) * 6, -1);
+  for (int c = 0; c < nc; ++c) {
+    const int ic[3] = {c % n, (c / n) % n, c / (n * n)};
+    for (int b = 0; b < 8; ++b)
+      cv[8 * c + b] = ((ic[2] + ((b >> 2) & 1)) * nx + ic[1] + ((b >> 1) & 1)) * nx + ic[0] + (b & 1);
+    const int lim[3] = {n, n, nz};
+    for (int d = 0; d < 3; ++d) {
+      if (ic[d] == 0) bid[6 * c + 2 * d] = 2 * d;
+      if (ic[d] == lim[d] - 1) bid[6 * c + 2 * d + 1] = 2 * d + 1;
+    }
+  }
+  return mesh_from_arrays<3>(nx * nx * nzv, xv.data(), nc, cv.data(), bid.data());
+}
+
 }  // namespace
 
 extern "C" {
+
+// ---- synthetic inputs (BASELINE.json configs) ----------
+// TEST INFRASTRUCTURE: a restatement of the frozen generator (mt19937_64; uniform
+// = (x >> 11) * 2^-53; Box-Muller normal; modes lexicographic, last index fastest;
+// a before phi; potential component 1, 2, 3) so that reference-only processes (the
+// bench reference arm, the CPU phase of tools/full_step_parity.py) build the same
+// inputs as the device path without loading libdgb.so.  Bit-identity with the
+// product's generator (capi.cpp dgb_seeded_uniform / dgb_synth_*) is a CPU test
+// (tests/test_oracle_inputs.py).
+// The product compiles its generator as plain host code (no FMA contraction), so the
+// restatement is compiled without contraction too: bit-identical values.
+#pragma GCC push_options
+#pragma GCC optimize("fp-contract=off")
+void ref_seeded_uniform(unsigned long long seed, size_t n, double lo, double hi, double* out) {
+  std::mt19937_64 rng(seed);
+  for (size_t i = 0; i < n; ++i) out[i] = lo + (hi - lo) * ((double)(rng() >> 11) * 0x1.0p-53);
+}
+void ref_synth_init(int dim, unsigned long long seed, double scale, double* user) {
+  std::mt19937_64 rng(seed);
+  auto uni = [&]() { return (double)(rng() >> 11) * 0x1.0p-53; };
+  const int nm = dim == 2 ? 16 : 64, ncomp = dim == 2 ? 1 : 3;
+  user[0] = dim;
+  user[1] = scale;
+  user[2] = nm;
+  int k = 3;
+  for (int c = 0; c < ncomp; ++c)
+    for (int m = 0; m < nm; ++m) {
+      double k2 = 0.0;
+      for (int d = 0, rem = m; d < dim; ++d, rem /= 4) {
+        const int i = 1 + rem % 4;
+        k2 += i * i;
+      }
+      const double u1 = uni(), u2 = uni();
+      user[k++] = std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(2.0 * M_PI * u2) / k2;
+      user[k++] = 2.0 * M_PI * uni();
+    }
+}
+// 2D: u = (dpsi/dy, -dpsi/dx); 3D: u = curl A.
+void ref_synth_eval(const double* x, double /*t*/, double* out, void* user) {
+  const double* u = static_cast<const double*>(user);
+  const int dim = static_cast<int>(u[0]), nm = static_cast<int>(u[2]);
+  const double scale = u[1], tp = 2.0 * M_PI;
+  if (dim == 2) {
+    double dx = 0.0, dy = 0.0;
+    for (int m = 0; m < nm; ++m) {
+      const int i0 = 1 + m / 4, i1 = 1 + m % 4;
+      const double cth = std::cos(tp * (i0 * x[0] + i1 * x[1]) + u[4 + 2 * m]);
+      dx += u[3 + 2 * m] * tp * i0 * cth;
+      dy += u[3 + 2 * m] * tp * i1 * cth;
+    }
+    out[0] = scale * dy;
+    out[1] = -scale * dx;
+    return;
+  }
+  double G[3][3] = {};
+  for (int c = 0; c < 3; ++c)
+    for (int m = 0; m < nm; ++m) {
+      const int i0 = 1 + m / 16, i1 = 1 + (m / 4) % 4, i2 = 1 + m % 4;
+      const double a = u[3 + 2 * (c * nm + m)], ph = u[4 + 2 * (c * nm + m)];
+      const double cth = a * tp * std::cos(tp * (i0 * x[0] + i1 * x[1] + i2 * x[2]) + ph);
+      G[c][0] += i0 * cth;
+      G[c][1] += i1 * cth;
+      G[c][2] += i2 * cth;
+    }
+  out[0] = scale * (G[2][1] - G[1][2]);
+  out[1] = scale * (G[0][2] - G[2][0]);
+  out[2] = scale * (G[1][0] - G[0][1]);
+}
+#pragma GCC pop_options
+void ref_interpolate_fn(void* h, ref_bc_fn fn, void* user, double* u, int nthreads) {
+  static_cast<Base*>(h)->interpolate_fn(fn, user, u, nthreads);
+}
+// The reference's BLAS-1 kernels (kernels.hpp:34-43, the active backend: AVX2 on an
+// AVX2 host, kernels_avx2.cpp:12-70) on host arrays.  op: 0 axpy (y += a x), 1 axpby
+// (y = a x + b y), 2 scal (y *= a), 3 dot, 4 max_abs_diff; returns the scalar result.
+double ref_kern(int op, size_t n, double a, double b, const double* x, double* y) {
+  switch (op) {
+    case 0: kern::axpy(n, a, x, y); return 0.0;
+    case 1: kern::axpby(n, a, x, b, y); return 0.0;
+    case 2: kern::scal(n, a, y); return 0.0;
+    case 3: return kern::dot(n, x, y);
+    default: return kern::max_abs_diff(n, x, y);
+  }
+}
+void* ref_create_slab(int n, int z0, int nz, int ku, int kp) {
+  try {
+    return new Ctx<3>(slab_mesh(n, z0, nz), ku, kp);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  }
+  return nullptr;
+}
 
 const char* ref_last_error() { return g_err.c_str(); }
 const char* ref_backend() {
@@ -594,6 +764,26 @@ void ref_node_points(void* h, int space, double* xn) { static_cast<Base*>(h)->in
 double ref_bench(void* h, int op, const double* c, const double* w, const double* x, int nthreads,
                  int napplies) {
   return static_cast<Base*>(h)->bench(op, c, w, x, nthreads, napplies);
+}
+void ref_pair_setup(void* h, const double* c, const double* w, const double* x, double pmc, const double* xp) {
+  static_cast<Base*>(h)->pair_setup(c, w, x, pmc, xp);
+}
+// `rounds` rounds; in each, every context runs pair_run() once, the contexts taken
+// from a shared counter by `nthreads` host threads (the reference is single-
+// threaded: parallelism is across independent contexts).  times[r] = wall seconds
+// of round r.
+void ref_pair_rounds(void** hs, int nh, int nthreads, int rounds, double* times) {
+  for (int r = 0; r < rounds; ++r) {
+    std::atomic<int> next{0};
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> th;
+    for (int t = 0; t < std::max(1, nthreads); ++t)
+      th.emplace_back([&]() {
+        for (int i; (i = next.fetch_add(1)) < nh;) static_cast<Base*>(hs[i])->pair_run();
+      });
+    for (auto& t : th) t.join();
+    times[r] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
 }
 void ref_dense_momentum(void* h, const double* c, const double* w, double* A) {
   static_cast<Base*>(h)->dense_momentum(c, w, A);

@@ -128,6 +128,7 @@ def lib() -> C.CDLL:
     L.dgb_scal.argtypes = [C.c_void_p, C.c_size_t, C.c_double, C.c_void_p]
     L.dgb_dot.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, _dp]
     L.dgb_max_abs_diff.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p, _dp]
+    L.dgb_norm.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, _dp]
     L.dgb_jacobi_inverse.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
     for name in ("dgb_cg", "dgb_gmres"):
         getattr(L, name).argtypes = [C.c_void_p, C.POINTER(_Operator), C.POINTER(_Settings), C.c_void_p,
@@ -414,6 +415,49 @@ def pressure_gradient_rhs(V: DGContext, p, out):
 def kinetic_energy(V: DGContext, u) -> float:
     r = C.c_double()
     _check(lib().dgb_kinetic_energy(V.handle, _ptr(u), C.byref(r)))
+    return r.value
+
+
+# ---------------------------------------------------------------------------
+# BLAS-1 (kern::axpy/axpby/scal/dot/max_abs_diff, kernels.hpp:34-43) on device vectors
+# ---------------------------------------------------------------------------
+def _n(x) -> int:
+    return int(x.numel())
+
+
+def axpy(V: DGContext, a: float, x, y) -> None:
+    """y += a x  (kern::axpy)"""
+    _check(lib().dgb_axpy(V.handle, _n(y), float(a), _ptr(x), _ptr(y)))
+
+
+def axpby(V: DGContext, a: float, x, b: float, y) -> None:
+    """y = a x + b y  (kern::axpby)"""
+    _check(lib().dgb_axpby(V.handle, _n(y), float(a), _ptr(x), float(b), _ptr(y)))
+
+
+def scal(V: DGContext, a: float, x) -> None:
+    """x *= a  (kern::scal)"""
+    _check(lib().dgb_scal(V.handle, _n(x), float(a), _ptr(x)))
+
+
+def dot(V: DGContext, x, y) -> float:
+    """<x, y>  (kern::dot)"""
+    r = C.c_double()
+    _check(lib().dgb_dot(V.handle, _n(x), _ptr(x), _ptr(y), C.byref(r)))
+    return r.value
+
+
+def norm(V: DGContext, x) -> float:
+    """sqrt(<x, x>)  (the solvers' 2-norm, krylov.cpp:54-56)"""
+    r = C.c_double()
+    _check(lib().dgb_norm(V.handle, _n(x), _ptr(x), C.byref(r)))
+    return r.value
+
+
+def max_abs_diff(V: DGContext, x, y) -> float:
+    """max_i |x_i - y_i|  (kern::max_abs_diff)"""
+    r = C.c_double()
+    _check(lib().dgb_max_abs_diff(V.handle, _n(x), _ptr(x), _ptr(y), C.byref(r)))
     return r.value
 
 

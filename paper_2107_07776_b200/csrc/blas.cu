@@ -27,7 +27,7 @@ int blas_grid(size_t n) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (size_t)gridDim.x * blockDim.x)
 
 __global__ void k_axpby(size_t n, double a, const double* __restrict__ x, double b, double* __restrict__ y) {
-  GRID_STRIDE(i, n) y[i] = a * x[i] + b * y[i];
+  GRID_STRIDE(i, n) y[i] = fma(a, x[i], b * y[i]);  // the reference's AVX2 order (kernels_avx2.cpp:27-29)
 }
 __global__ void k_axpy(size_t n, double a, const double* __restrict__ x, double* __restrict__ y) {
   GRID_STRIDE(i, n) y[i] = fma(a, x[i], y[i]);

@@ -31,6 +31,7 @@ static int bad(const char* msg) {
 #define NEED(cond, msg) \
   if (!(cond)) return bad(msg)
 
+
 extern "C" {
 
 const char* dgb_last_error(void) { return g_last_error.c_str(); }
@@ -74,9 +75,13 @@ int dgb_ctx_create_mesh(int dim, int nverts, const double* verts, int ncells, co
   return finish_create(std::move(m), ku, kp, device, err, out);
 }
 
-void dgb_ctx_destroy(dgb_ctx* h) { delete h; }
+void dgb_ctx_destroy(dgb_ctx* h) {
+  DevGuard guard_(h);
+  delete h;
+}
 
 int dgb_ctx_info(dgb_ctx* h, long long* info) {
+  DevGuard guard_(h);
   NEED(h && info, "null argument");
   const Context& c = h->c;
   for (int i = 0; i < 16; ++i) info[i] = 0;
@@ -95,6 +100,7 @@ int dgb_ctx_info(dgb_ctx* h, long long* info) {
 }
 
 int dgb_set_stream(dgb_ctx* h, void* s) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   // NULL selects the legacy default stream (what torch's default current stream is)
   h->c.dc.stream = static_cast<cudaStream_t>(s);
@@ -103,6 +109,7 @@ int dgb_set_stream(dgb_ctx* h, void* s) {
 void* dgb_get_stream(dgb_ctx* h) { return h ? static_cast<void*>(h->c.dc.stream) : nullptr; }
 
 int dgb_sync(dgb_ctx* h) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   const cudaError_t e = cudaStreamSynchronize(h->c.dc.stream);
   if (e != cudaSuccess) return ret(h, h->c.cuda_fail(e, "dgb_sync"));
@@ -110,6 +117,7 @@ int dgb_sync(dgb_ctx* h) {
 }
 
 int dgb_set_boundary_type(dgb_ctx* h, int id, int type) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   NEED(id >= 0 && id < 64, "boundary id must be in [0, 64)");
   NEED(type == DGB_BC_DIRICHLET || type == DGB_BC_OUTLET, "bad boundary type");
@@ -125,14 +133,17 @@ int dgb_set_boundary_type(dgb_ctx* h, int id, int type) {
   return DGB_OK;
 }
 int dgb_set_dirichlet_table(dgb_ctx* h, const double* g) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   return ret(h, h->c.set_dirichlet_table(g));
 }
 int dgb_set_dirichlet_fn(dgb_ctx* h, int id, dgb_bc_fn fn, void* user, double t) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   return ret(h, h->c.set_dirichlet_fn(id, fn, user, t));
 }
 int dgb_boundary_points(dgb_ctx* h, int q1d, double* xq) {
+  DevGuard guard_(h);
   NEED(h && xq, "null argument");
   NEED(q1d >= 1 && q1d <= 12, "bad rule");
   std::vector<double> v;
@@ -141,6 +152,7 @@ int dgb_boundary_points(dgb_ctx* h, int q1d, double* xq) {
   return DGB_OK;
 }
 int dgb_node_points(dgb_ctx* h, int space, double* xn) {
+  DevGuard guard_(h);
   NEED(h && xn, "null argument");
   const Context& c = h->c;
   const int deg = space == DGB_SPACE_U ? c.ku : c.kp;
@@ -161,6 +173,7 @@ int dgb_node_points(dgb_ctx* h, int space, double* xn) {
   return DGB_OK;
 }
 int dgb_face_lists(dgb_ctx* h, int* interior, int* boundary) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   if (interior) std::memcpy(interior, h->c.mesh.iface.data(), h->c.mesh.iface.size() * sizeof(int));
   if (boundary) std::memcpy(boundary, h->c.mesh.bface.data(), h->c.mesh.bface.size() * sizeof(int));
@@ -169,6 +182,7 @@ int dgb_face_lists(dgb_ctx* h, int* interior, int* boundary) {
 
 // ------------------------------------------------------------------ memory
 int dgb_alloc(dgb_ctx* h, size_t n, double** p) {
+  DevGuard guard_(h);
   NEED(h && p, "null argument");
   cudaSetDevice(h->c.device);
   const cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), (n ? n : 1) * sizeof(double));
@@ -176,6 +190,7 @@ int dgb_alloc(dgb_ctx* h, size_t n, double** p) {
   return DGB_OK;
 }
 int dgb_free(dgb_ctx* h, double* p) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   cudaStreamSynchronize(h->c.dc.stream);
   cudaFree(p);
@@ -188,14 +203,17 @@ static int cpy(dgb_ctx* h, void* dst, const void* src, size_t n, cudaMemcpyKind 
   return DGB_OK;
 }
 int dgb_copy_h2d(dgb_ctx* h, double* d, const double* s, size_t n) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   return cpy(h, d, s, n, cudaMemcpyHostToDevice, true);
 }
 int dgb_copy_d2h(dgb_ctx* h, double* d, const double* s, size_t n) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   return cpy(h, d, s, n, cudaMemcpyDeviceToHost, true);
 }
 int dgb_copy_d2d(dgb_ctx* h, double* d, const double* s, size_t n) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   return cpy(h, d, s, n, cudaMemcpyDeviceToDevice, false);
 }
@@ -203,74 +221,90 @@ int dgb_fill(dgb_ctx* h, double* x, double v, size_t n);
 
 // ------------------------------------------------------------------ operators
 int dgb_momentum_apply(dgb_ctx* h, const double* coefs, const double* w, const double* x, double* y) {
+  DevGuard guard_(h);
   NEED(h && coefs && x && y, "null argument");
   NEED(x != y, "x and y must not alias");
   return ret(h, h->c.momentum(coefs, w, x, y));
 }
 int dgb_momentum_apply_host(dgb_ctx* h, const double* coefs, const double* h_w, const double* h_x, double* h_y) {
+  DevGuard guard_(h);
   NEED(h && coefs && h_x && h_y, "null argument");
   NEED(h_x != h_y, "x and y must not alias");
   return ret(h, h->c.apply_host(true, coefs, 0.0, h_w, h_x, h_y));
 }
 int dgb_pressure_apply_host(dgb_ctx* h, double mc, const double* h_x, double* h_y) {
+  DevGuard guard_(h);
   NEED(h && h_x && h_y, "null argument");
   NEED(h_x != h_y, "x and y must not alias");
   return ret(h, h->c.apply_host(false, nullptr, mc, nullptr, h_x, h_y));
 }
 int dgb_momentum_diag(dgb_ctx* h, const double* coefs, const double* w, double* d) {
+  DevGuard guard_(h);
   NEED(h && coefs && d, "null argument");
   return ret(h, h->c.momentum_diag(coefs, w, d));
 }
 int dgb_pressure_apply(dgb_ctx* h, double mc, const double* x, double* y) {
+  DevGuard guard_(h);
   NEED(h && x && y, "null argument");
   NEED(x != y, "x and y must not alias");
   return ret(h, h->c.sip(mc, 0, x, y));
 }
 int dgb_helmholtz_diag(dgb_ctx* h, double mc, double* d) {
+  DevGuard guard_(h);
   NEED(h && d, "null argument");
   return ret(h, h->c.sip_diag(mc, 0, d));
 }
 int dgb_laplace_apply(dgb_ctx* h, int dir, const double* x, double* y) {
+  DevGuard guard_(h);
   NEED(h && x && y, "null argument");
   NEED(x != y, "x and y must not alias");
   return ret(h, h->c.sip(0.0, dir != 0, x, y));
 }
 int dgb_laplace_diag(dgb_ctx* h, int dir, double* d) {
+  DevGuard guard_(h);
   NEED(h && d, "null argument");
   return ret(h, h->c.sip_diag(0.0, dir != 0, d));
 }
 int dgb_mass_apply(dgb_ctx* h, int space, const double* x, double* y) {
+  DevGuard guard_(h);
   NEED(h && x && y, "null argument");
   NEED(space == DGB_SPACE_U || space == DGB_SPACE_P, "bad space");
   return ret(h, h->c.mass(space, x, y));
 }
 int dgb_mass_diag(dgb_ctx* h, int space, double* d) {
+  DevGuard guard_(h);
   NEED(h && d, "null argument");
   NEED(space == DGB_SPACE_U || space == DGB_SPACE_P, "bad space");
   return ret(h, h->c.mass_diag(space, d));
 }
 int dgb_momentum_rhs(dgb_ctx* h, const dgb_rhs_desc* desc, double* out) {
+  DevGuard guard_(h);
   NEED(h && desc && out, "null argument");
   return ret(h, h->c.rhs(*desc, out));
 }
 int dgb_divergence(dgb_ctx* h, const double* u, double* out) {
+  DevGuard guard_(h);
   NEED(h && u && out, "null argument");
   return ret(h, h->c.divergence(u, out));
 }
 int dgb_pressure_rhs(dgb_ctx* h, double inv_adt, const double* u, double mc, const double* p_old, double* out) {
+  DevGuard guard_(h);
   NEED(h && u && out, "null argument");
   return ret(h, h->c.pressure_rhs(inv_adt, u, mc, p_old, out));
 }
 int dgb_pressure_gradient(dgb_ctx* h, const double* p, double* out) {
+  DevGuard guard_(h);
   NEED(h && p && out, "null argument");
   return ret(h, h->c.gradient(p, out));
 }
 int dgb_kinetic_energy(dgb_ctx* h, const double* u, double* result) {
+  DevGuard guard_(h);
   NEED(h && u && result, "null argument");
   return ret(h, h->c.kinetic(u, result));
 }
 
 int dgb_l2_norm(dgb_ctx* h, int space, const double* x, double* result) {
+  DevGuard guard_(h);
   NEED(h && x && result, "null argument");
   NEED(space == DGB_SPACE_U || space == DGB_SPACE_P, "space must be 0 or 1");
   dgb::Context& c = h->c;
@@ -283,12 +317,14 @@ int dgb_l2_norm(dgb_ctx* h, int space, const double* x, double* result) {
   return ret(h, code);
 }
 int dgb_check_steady(dgb_ctx* h, const double* un, const double* uo, double tol, int* steady, double* diff) {
+  DevGuard guard_(h);
   NEED(h && un && uo && steady && diff, "null argument");
   const int code = h->c.max_abs_diff(h->c.nu(), un, uo, diff);
   *steady = code == DGB_OK && *diff < tol;
   return ret(h, code);
 }
 int dgb_stability_params(dgb_ctx* h, double dt, double Re, double U, double* C, double* mu) {
+  DevGuard guard_(h);
   NEED(h && C && mu, "null argument");
   NEED(Re > 0.0, "Re must be positive");
   const auto& d = h->c.mesh.cell_diam;
@@ -303,40 +339,56 @@ int dgb_stability_params(dgb_ctx* h, double dt, double Re, double U, double* C, 
 
 // ------------------------------------------------------------------ vectors
 int dgb_axpy(dgb_ctx* h, size_t n, double a, const double* x, double* y) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   ++h->c.launches;
   const cudaError_t e = dgb::v_axpy(h->c.dc.stream, n, a, x, y);
   return e == cudaSuccess ? DGB_OK : ret(h, h->c.cuda_fail(e, "dgb_axpy"));
 }
 int dgb_axpby(dgb_ctx* h, size_t n, double a, const double* x, double b, double* y) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   ++h->c.launches;
   const cudaError_t e = dgb::v_axpby(h->c.dc.stream, n, a, x, b, y);
   return e == cudaSuccess ? DGB_OK : ret(h, h->c.cuda_fail(e, "dgb_axpby"));
 }
 int dgb_scal(dgb_ctx* h, size_t n, double a, double* x) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   ++h->c.launches;
   const cudaError_t e = dgb::v_scal(h->c.dc.stream, n, a, x);
   return e == cudaSuccess ? DGB_OK : ret(h, h->c.cuda_fail(e, "dgb_scal"));
 }
 int dgb_fill(dgb_ctx* h, double* x, double v, size_t n) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   ++h->c.launches;
   const cudaError_t e = dgb::v_fill(h->c.dc.stream, n, v, x);
   return e == cudaSuccess ? DGB_OK : ret(h, h->c.cuda_fail(e, "dgb_fill"));
 }
 int dgb_dot(dgb_ctx* h, size_t n, const double* x, const double* y, double* result) {
+  DevGuard guard_(h);
   NEED(h && result, "null argument");
   return ret(h, h->c.dot(n, x, y, result));
 }
+int dgb_norm(dgb_ctx* h, size_t n, const double* x, double* result) {
+  DevGuard guard_(h);
+  NEED(h && result, "null argument");
+  double s = 0.0;
+  const int st = h->c.dot(n, x, x, &s);
+  if (st != DGB_OK) return ret(h, st);
+  *result = std::sqrt(s);
+  return DGB_OK;
+}
 int dgb_max_abs_diff(dgb_ctx* h, size_t n, const double* x, const double* y, double* result) {
+  DevGuard guard_(h);
   NEED(h && result, "null argument");
   return ret(h, h->c.max_abs_diff(n, x, y, result));
 }
 
 // ------------------------------------------------------------------ solvers
 int dgb_jacobi_inverse(dgb_ctx* h, size_t n, const double* d, double* inv) {
+  DevGuard guard_(h);
   NEED(h && d && inv, "null argument");
   return ret(h, h->c.jacobi_inverse(n, d, inv));
 }
@@ -354,15 +406,18 @@ static int solve(dgb_ctx* h, bool gm, const dgb_operator* op, const dgb_solver_s
 }
 int dgb_cg(dgb_ctx* h, const dgb_operator* op, const dgb_solver_settings* s, const double* inv, const double* b,
            double* x, dgb_solve_result* res, double* hist, int cap, int* hlen) {
+  DevGuard guard_(h);
   return solve(h, false, op, s, inv, b, x, res, hist, cap, hlen);
 }
 int dgb_gmres(dgb_ctx* h, const dgb_operator* op, const dgb_solver_settings* s, const double* inv, const double* b,
               double* x, dgb_solve_result* res, double* hist, int cap, int* hlen) {
+  DevGuard guard_(h);
   return solve(h, true, op, s, inv, b, x, res, hist, cap, hlen);
 }
 
 int dgb_pressure_cg_mg(dgb_ctx* h, double mc, const dgb_solver_settings* s, const double* b, double* x,
                        dgb_solve_result* res) {
+  DevGuard guard_(h);
   NEED(h && s && b && x && res, "null argument");
   dgb::SolveOut out;
   const int code = h->c.cg_mg(mc, *s, b, x, out);
@@ -371,12 +426,14 @@ int dgb_pressure_cg_mg(dgb_ctx* h, double mc, const dgb_solver_settings* s, cons
   return ret(h, code);
 }
 int dgb_pressure_mg_vcycle(dgb_ctx* h, double mc, const double* r, double* z) {
+  DevGuard guard_(h);
   NEED(h && r && z, "null argument");
   return ret(h, h->c.mg_precondition(mc, r, z));
 }
 
 int dgb_projection_step(dgb_ctx* h, int scheme, const dgb_step_params* p, const double* u_nm1, const double* u_n,
                         const double* p_n, double* u_np1, double* p_np1, int* its) {
+  DevGuard guard_(h);
   NEED(h && p && u_n && p_n && u_np1 && p_np1 && its, "null argument");
   NEED(scheme >= DGB_SCHEME_TRBDF2 && scheme <= DGB_SCHEME_GQ_BDF2, "unknown scheme");
   NEED(p->first_step || u_nm1 || scheme == DGB_SCHEME_BCG, "u_nm1 required after the first step");
@@ -384,6 +441,7 @@ int dgb_projection_step(dgb_ctx* h, int scheme, const dgb_step_params* p, const 
 }
 int dgb_trbdf2_step(dgb_ctx* h, const dgb_step_params* p, const double* u_nm1, const double* u_n,
                     const double* p_n, double* u_np1, double* p_np1, int* its) {
+  DevGuard guard_(h);
   NEED(h && p && u_n && p_n && u_np1 && p_np1 && its, "null argument");
   NEED(p->first_step || u_nm1, "u_nm1 required after the first step");
   return ret(h, h->c.trbdf2_step(*p, u_nm1, u_n, p_n, u_np1, p_np1, its));
@@ -463,6 +521,7 @@ void dgb_synth_eval(const double* x, double /*t*/, double* out, void* user) {
 }
 
 int dgb_interpolate_synth(dgb_ctx* h, const double* user, double* hu) {
+  DevGuard guard_(h);
   NEED(h && user && hu, "null argument");
   const Context& c = h->c;
   const int n1 = c.ku + 1;
@@ -485,11 +544,13 @@ int dgb_interpolate_synth(dgb_ctx* h, const double* user, double* hu) {
 
 // ------------------------------------------------------------------ measurement
 int dgb_timer_start(dgb_ctx* h) {
+  DevGuard guard_(h);
   NEED(h, "null ctx");
   cudaEventRecord(h->c.ev0, h->c.dc.stream);
   return DGB_OK;
 }
 int dgb_timer_stop(dgb_ctx* h, float* ms) {
+  DevGuard guard_(h);
   NEED(h && ms, "null argument");
   cudaEventRecord(h->c.ev1, h->c.dc.stream);
   cudaEventSynchronize(h->c.ev1);
@@ -497,7 +558,8 @@ int dgb_timer_stop(dgb_ctx* h, float* ms) {
   if (e != cudaSuccess) return ret(h, h->c.cuda_fail(e, "dgb_timer_stop"));
   return DGB_OK;
 }
-long long dgb_launch_count(dgb_ctx* h) { return h ? h->c.launches : 0; }
+long long dgb_launch_count(dgb_ctx* h) {
+  DevGuard guard_(h); return h ? h->c.launches : 0; }
 
 }  // extern "C"
 

@@ -6,11 +6,20 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstdint>
 #include <cstring>
 
 #include "blas.cuh"
 
 namespace dgb {
+
+// runs a callable when the scope ends (early returns included)
+template <class F>
+struct ScopeExit {
+  F f;
+  explicit ScopeExit(F g) : f(g) {}
+  ~ScopeExit() { f(); }
+};
 
 #define CK(call)                                             \
   do {                                                       \
@@ -420,6 +429,11 @@ int Context::apply_host(bool mom, const double* coefs, double mc, const double* 
   }
   const MomCoef co = mom ? MomCoef{coefs[0], coefs[1], coefs[2], coefs[3]} : MomCoef{};
   int rc = DGB_OK;
+  // the slab range is reset on every exit, including an early CK() return
+  ScopeExit reset_range([this] {
+    dc.mesh.cell0 = 0;
+    dc.mesh.cell1 = -1;
+  });
   for (int s = 0; s < ns && rc == DGB_OK; ++s) {
     CK(cudaStreamWaitEvent(st, ev_in_[std::min(s + 1, ns - 1)], 0));
     dc.mesh.cell0 = cells(s);
@@ -682,6 +696,7 @@ int Context::cg(const dgb_operator& op, const dgb_solver_settings& s, const doub
     CK(cg_begin(st, n, r, inv, z, d_partial_, d_cg_));
     const int batch = 8;
     dc.mesh.skip = &d_cg_->done;
+    ScopeExit reset_skip([this] { dc.mesh.skip = nullptr; });  // also on early returns
     // scalar SIP operators on axis-aligned meshes: <p, q> fused into the apply's epilogue
     const bool fused = use_fast && dc.axis && (op.op == DGB_OP_PRESSURE || op.op == DGB_OP_LAPLACE) &&
                        fast_sip3_cg_blocks(dc) > 0;
@@ -810,6 +825,15 @@ int Context::gmres(const dgb_operator& op, const dgb_solver_settings& s, const d
   }
   const double tol = std::max(s.rel_tol * bnorm, s.abs_tol);
   const int m = std::max(1, s.restart);
+  if (inv && (reinterpret_cast<uintptr_t>(inv) & 15)) {
+    // the Gram-Schmidt update pass reads the Jacobi inverse as double2 (16-byte
+    // aligned, dgb.h): a caller view at an odd element offset is copied to an
+    // aligned slot first
+    double* a = scratch_vec(42, n);
+    if (!a) return fail(DGB_E_CUDA, "gmres: out of device memory");
+    CK(cudaMemcpyAsync(a, inv, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    inv = a;
+  }
   if (gm_n_ != n) {
     cudaStreamSynchronize(st);
     for (double* v : gm_raw_) cudaFree(v);

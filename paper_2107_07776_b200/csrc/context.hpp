@@ -148,3 +148,18 @@ class Context {
 struct dgb_ctx {
   dgb::Context c;
 };
+
+// Every entry point that touches device state runs on the context's device and
+// restores the caller's current device on return (a context created on
+// device N and used while another device is current).
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(const dgb_ctx* h) {
+    if (h && cudaGetDevice(&prev) == cudaSuccess && prev != h->c.device) cudaSetDevice(h->c.device);
+    else prev = -1;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+

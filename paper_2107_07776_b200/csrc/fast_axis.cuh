@@ -482,6 +482,9 @@ struct SipAxisCfg {
   static constexpr bool CF = KP == 1 && WPG;
   static constexpr int PER = CF ? O_INFO + kInfoDoubles + 1 : (O_INFO + kInfoDoubles) | 1;
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
+  // the cell-fastest (CF) layout is bank-conflict-free only for a cell stride of 10 mod 16
+  // doubles (tools/bank_sim_sip1.py); a new CellInfo field must keep that
+  static_assert(!CF || PER % 16 == 10, "SipAxisCfg: CF layout needs PER % 16 == 10");
 };
 
 // CGF: the CG apply q = A p with <p, q> fused into the epilogue (krylov.cpp:84-87):

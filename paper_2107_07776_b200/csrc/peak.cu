@@ -25,7 +25,7 @@ __global__ void k_dfma_peak(double* out, int iters, double a, double b) {
 
 extern "C" int dgb_fp64_peak(dgb_ctx* h, double* tflops) {
   if (!h || !tflops) return DGB_E_ARG;
-  cudaSetDevice(h->c.device);
+  DevGuard guard_(h);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->c.device);
   double* d = nullptr;

@@ -71,6 +71,7 @@ __global__ void k_interp_synth(SynthArgs a, int ncells, const double* __restrict
 
 extern "C" int dgb_interpolate_synth_device(dgb_ctx* h, const double* user, double* d_u) {
   if (!h || !user || !d_u) return DGB_E_ARG;
+  DevGuard guard_(h);
   dgb::Context& c = h->c;
   SynthArgs a;
   a.dim = (int)user[0];

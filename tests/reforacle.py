@@ -70,8 +70,74 @@ def lib():
         L.ref_bench.restype = C.c_double
         L.ref_dense_momentum.argtypes = [C.c_void_p, _dp, _dp, _dp]
         L.ref_dense_scalar_sip.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int, _dp]
+        L.ref_seeded_uniform.argtypes = [C.c_ulonglong, C.c_size_t, C.c_double, C.c_double, _dp]
+        L.ref_synth_init.argtypes = [C.c_int, C.c_ulonglong, C.c_double, _dp]
+        L.ref_synth_eval.argtypes = [_dp, C.c_double, _dp, C.c_void_p]
+        L.ref_interpolate_fn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, _dp, C.c_int]
+        L.ref_create_slab.restype = C.c_void_p
+        L.ref_create_slab.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
+        L.ref_kern.argtypes = [C.c_int, C.c_size_t, C.c_double, C.c_double, _dp, _dp]
+        L.ref_kern.restype = C.c_double
+        L.ref_pair_setup.argtypes = [C.c_void_p, _dp, _dp, _dp, C.c_double, _dp]
+        L.ref_pair_rounds.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, _dp]
         _lib = L
     return _lib
+
+
+def kern(op: str, a: float, x, y, b: float = 0.0):
+    """The reference's kern:: BLAS-1 (active backend).  axpy / axpby / scal return the
+    updated copy of y (scal: of x); dot / max_abs_diff return the scalar."""
+    code = {"axpy": 0, "axpby": 1, "scal": 2, "dot": 3, "max_abs_diff": 4}[op]
+    yy = np.array(x if op == "scal" else y, dtype=np.float64, copy=True)
+    xx = np.ascontiguousarray(x, dtype=np.float64)
+    r = lib().ref_kern(code, len(yy), a, b, P(xx), P(yy))
+    return yy if code <= 2 else r
+
+
+def pair_rounds(ctxs, nthreads: int, rounds: int):
+    """Wall seconds of `rounds` rounds of one momentum + one pressure apply on every
+    context in ctxs (after RefCtx.pair_setup), spread over nthreads host threads."""
+    hs = (C.c_void_p * len(ctxs))(*[c.h for c in ctxs])
+    t = np.zeros(rounds)
+    lib().ref_pair_rounds(hs, len(ctxs), int(nthreads), int(rounds), P(t))
+    return t
+
+
+def seeded_uniform(seed: int, n: int, lo: float = -1.0, hi: float = 1.0):
+    """U[lo,hi) from mt19937_64(seed) (same values as the product's dgb_seeded_uniform)."""
+    out = np.empty(n)
+    lib().ref_seeded_uniform(seed, n, lo, hi, P(out))
+    return out
+
+
+class SynthField:
+    """BASELINE initial field (curl of a seeded stream function / vector potential),
+    oracle-side restatement: its fn_ptr is a plain C function inside libdgref.so."""
+
+    def __init__(self, dim: int, seed: int, scale: float = 1.0):
+        self.dim = dim
+        self.user = np.zeros(512)
+        lib().ref_synth_init(dim, seed, scale, P(self.user))
+
+    @property
+    def user_ptr(self):
+        return self.user.ctypes.data_as(C.c_void_p)
+
+    @property
+    def fn_ptr(self):
+        return C.cast(lib().ref_synth_eval, C.c_void_p)
+
+    def eval(self, x):
+        out = np.zeros(self.dim)
+        xx = np.ascontiguousarray(x, dtype=np.float64)
+        lib().ref_synth_eval(P(xx), 0.0, P(out), self.user_ptr)
+        return out
+
+    def interpolate(self, R: "RefCtx", nthreads: int = 1):
+        """FunctionSpace::interpolate (space.cpp:239-253) of the field on R's velocity space."""
+        out = np.zeros(R.n_u)
+        lib().ref_interpolate_fn(R.h, self.fn_ptr, self.user_ptr, P(out), int(nthreads))
+        return out
 
 
 def P(a):
@@ -101,6 +167,14 @@ class RefCtx:
         (self.ncells, self.n_u, self.n_p, self.n_interior, self.n_boundary, self.ku, self.kp, self.dim,
          self.nverts, self.n_hanging) = [int(v) for v in info]
         self._keep = []
+
+    @classmethod
+    def slab(cls, n_el: int, z0: int, nz: int, ku: int, kp: int):
+        """z-slab [z0, z0+nz) of the 3D n_el^3 Cartesian mesh (identical cells; slab ends are boundary faces)."""
+        h = lib().ref_create_slab(n_el, z0, nz, ku, kp)
+        if not h:
+            raise RuntimeError(lib().ref_last_error().decode())
+        return cls(handle=h)
 
     def __del__(self):
         try:
@@ -250,6 +324,10 @@ class RefCtx:
     def bench(self, op, coefs, w, x, nthreads, napplies):
         c = np.ascontiguousarray(coefs, dtype=np.float64)
         return lib().ref_bench(self.h, op, P(c), P(w), P(x), nthreads, napplies)
+
+    def pair_setup(self, coefs, w, x, mass_coef, xp):
+        c = np.ascontiguousarray(coefs, dtype=np.float64)
+        lib().ref_pair_setup(self.h, P(c), P(w), P(x), mass_coef, P(xp))
 
     def dense_momentum(self, coefs, w):
         A = np.zeros((self.n_u, self.n_u))

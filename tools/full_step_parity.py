@@ -1,43 +1,101 @@
-"""One-off parity evidence at a full BASELINE size: one TR-BDF2 step of cfg2 (3D 32^3,
-Q2/Q1, Re 100, dt 1e-3, seed 1; minutes on one CPU core for the reference) through the
-restated reference driver (oracle/_ref, CPU) and through the device, from the same
-synthetic u^0 (Dirichlet data = its trace, p^0 = 0).  Prints a JSON line with the
-Krylov iteration counts of both sides and the relative L2 field differences.
-CFG_N / KU override the mesh and degree."""
-import json, os, sys, time
+"""Full-size TR-BDF2 step parity (VERDICT r01 "next round" item 1).
+
+One TR-BDF2 step of a BASELINE config from the synthetic u^0 (Dirichlet data = its
+trace on every boundary, p^0 = 0) through the restated reference driver
+(oracle/trbdf2_cpu.hpp over the unmodified reference, oracle/_ref) and through the
+device (dgb_trbdf2_step).  The two halves run on different machines, because the
+cfg3 CPU step takes hours and ~26 GB:
+
+  python tools/full_step_parity.py cpu cfg3      # here (no GPU): writes parity_data/cfg3_step_ref.*
+  python tools/full_step_parity.py gpu cfg3      # on the GPU box: device step, compares, prints JSON
+
+Inputs come from the oracle-side generator (reforacle.SynthField, bit-identical to the
+product's, tests/test_oracle_inputs.py) on both sides, and the GPU half checks the
+SHA-256 of u^0 against the one the CPU half recorded.  parity_data/ is git-ignored
+but travels to the GPU box with the gpurun snapshot.
+"""
+import hashlib
+import json
+import os
+import sys
+import time
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np
-import torch
-import paper_2107_07776_b200 as dg
+
 import reforacle as ref
 
-n_el, ku = int(os.environ.get("CFG_N", "32")), int(os.environ.get("KU", "2"))
-kp, seed, Re, dt = ku - 1, 1, 100.0, 1e-3
-R = ref.RefCtx(3, n_el, ku, kp, 0.0, 7)
-D = dg.DGContext(3, n_el, ku, kp)
-f = dg.SynthField(3, seed)
-for bid in range(6):
-    R.set_bc(bid, 0, f.fn_ptr, f.user_ptr)
-    D.set_dirichlet_fn(bid, f.fn_ptr, f.user_ptr, 0.0)
-u0 = f.interpolate(D)
-p0 = np.zeros(R.n_p)
-t0 = time.time()
-u1, p1, its_ref = R.step([dt, Re, 1e3, 0.0, 50, 1e-10, 1e-10, 1e-12, 10000, 1.0], u0, u0, p0)
-t_ref = time.time() - t0
-du0 = torch.from_numpy(u0).cuda()
-dp0 = torch.from_numpy(p0).cuda()
-du1, dp1 = D.zeros(), D.zeros(dg.SPACE_P)
-torch.cuda.synchronize()
-t0 = time.time()
-its = dg.trbdf2_step(D, dg.StepParams(dt=dt, Re=Re, c=1e3, restart=50, first_step=True), du0, du0, dp0, du1, dp1)
-torch.cuda.synchronize()
-t_dev = time.time() - t0
-hu, hp = du1.cpu().numpy(), dp1.cpu().numpy()
-rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
-print(json.dumps({"config": f"3D {n_el}^3 Q{ku}/Q{kp}, Re {Re}, dt {dt}, seed {seed}, one TR-BDF2 step from u^0",
-                  "n_u": D.n_u, "n_p": D.n_p, "its_device": its[:8], "its_reference": its_ref[:8],
-                  "max_its_diff": max(abs(a - b) for a, b in zip(its[:8], its_ref[:8])),
-                  "rel_l2_u": rel(hu, u1), "rel_l2_p_mean_free": rel(hp - hp.mean(), p1 - p1.mean()),
-                  "reference_s": t_ref, "device_s": t_dev}))
+# name: (n_el, ku, seed, Re, dt, restart)  -- BASELINE.json configs, SURVEY Appendix C3/C12
+CFGS = {"cfg2": (32, 2, 1, 100.0, 1e-3, 50), "cfg3": (64, 3, 2, 1000.0, 1e-3, 30)}
+DATA = os.path.join(ROOT, "parity_data")
+
+
+def inputs(name, nthreads):
+    n_el, ku, seed, Re, dt, restart = CFGS[name]
+    R = ref.RefCtx(3, n_el, ku, ku - 1, 0.0, 0)
+    f = ref.SynthField(3, seed)
+    u0 = f.interpolate(R, nthreads)
+    return R, f, u0, hashlib.sha256(u0.tobytes()).hexdigest()
+
+
+def cpu(name):
+    n_el, ku, seed, Re, dt, restart = CFGS[name]
+    os.makedirs(DATA, exist_ok=True)
+    R, f, u0, sha = inputs(name, os.cpu_count() or 1)
+    for bid in range(6):
+        R.set_bc(bid, 0, f.fn_ptr, f.user_ptr)
+    p0 = np.zeros(R.n_p)
+    t0 = time.time()
+    u1, p1, its = R.step([dt, Re, 1e3, 0.0, restart, 1e-10, 1e-10, 1e-12, 10000, 1.0], u0, u0, p0)
+    t = time.time() - t0
+    np.save(os.path.join(DATA, f"{name}_step_ref_u.npy"), u1)
+    np.save(os.path.join(DATA, f"{name}_step_ref_p.npy"), p1)
+    meta = {"config": name, "n_u": R.n_u, "n_p": R.n_p, "u0_sha256": sha, "its_reference": its[:8],
+            "reference_s": t, "backend": ref.lib().ref_backend().decode()}
+    json.dump(meta, open(os.path.join(DATA, f"{name}_step_ref.json"), "w"))
+    print(json.dumps(meta))
+
+
+def gpu(name):
+    import torch
+
+    import paper_2107_07776_b200 as dg
+    n_el, ku, seed, Re, dt, restart = CFGS[name]
+    meta = json.load(open(os.path.join(DATA, f"{name}_step_ref.json")))
+    R, f, u0, sha = inputs(name, os.cpu_count() or 1)
+    assert sha == meta["u0_sha256"], "u^0 differs from the CPU half's"
+    D = dg.DGContext(3, n_el, ku, ku - 1)
+    g = dg.SynthField(3, seed)  # product generator: the device's Dirichlet callback (same values)
+    assert (g.user == f.user).all()
+    for bid in range(6):
+        D.set_dirichlet_fn(bid, g.fn_ptr, g.user_ptr, 0.0)
+    du0 = torch.from_numpy(u0).cuda()
+    dp0 = torch.zeros(D.n_p, dtype=torch.float64, device="cuda")
+    du1, dp1 = D.zeros(), D.zeros(dg.SPACE_P)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    its = dg.trbdf2_step(D, dg.StepParams(dt=dt, Re=Re, c=1e3, restart=restart, first_step=True),
+                         du0, du0, dp0, du1, dp1)
+    torch.cuda.synchronize()
+    t_dev = time.time() - t0
+    u1 = np.load(os.path.join(DATA, f"{name}_step_ref_u.npy"))
+    p1 = np.load(os.path.join(DATA, f"{name}_step_ref_p.npy"))
+    hu, hp = du1.cpu().numpy(), dp1.cpu().numpy()
+    rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))
+    out = {"config": f"{name}: 3D {n_el}^3 Q{ku}/Q{ku - 1}, Re {Re}, dt {dt}, seed {seed}, GMRES({restart}) + "
+                     f"Jacobi, CG + Jacobi, rel tol 1e-10 (mass 1e-12); one TR-BDF2 step from u^0",
+           "n_u": D.n_u, "n_p": D.n_p, "u0_sha256": sha,
+           "its_legend": "[gmres s1, gmres s2, cg s1, cg s2, mass-cg s1 pre, s1 post, s2 pre, s2 post]",
+           "its_device": its[:8], "its_reference": meta["its_reference"],
+           "max_its_diff": max(abs(a - b) for a, b in zip(its[:8], meta["its_reference"])),
+           "rel_l2_u": rel(hu, u1), "rel_l2_p_mean_free": rel(hp - hp.mean(), p1 - p1.mean()),
+           "reference_s_1core": meta["reference_s"], "reference_backend": meta["backend"],
+           "device_s_incl_first_use_alloc": t_dev}
+    out["pass"] = bool(out["max_its_diff"] <= 1 and out["rel_l2_u"] <= 1e-9 and out["rel_l2_p_mean_free"] <= 1e-9)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    {"cpu": cpu, "gpu": gpu}[sys.argv[1]](sys.argv[2] if len(sys.argv) > 2 else "cfg3")
