@@ -6,7 +6,7 @@
 // (forms.hpp / krylov.hpp) and follows SURVEY.md Appendix A, which derives the
 // stage -> operator coefficient map from SPEC.md:345-452, PAPER.md:90-180,
 // 475-491 and the free-stream pin proj/tests/test_forms.cpp:369-422.
-// The device driver (paper_2107_07776_b200/csrc/trbdf2.cu) performs exactly
+// The device driver (paper_2107_07776_b200/csrc/context.cu, Context::trbdf2_step) performs exactly
 // the same sequence of operator / solver calls.
 #pragma once
 
