@@ -75,6 +75,12 @@ int dgb_set_dirichlet_table(dgb_ctx* ctx, const double* g_host);
  * boundary face with this id and uploads it. */
 typedef void (*dgb_bc_fn)(const double* x, double t, double* out, void* user);
 int dgb_set_dirichlet_fn(dgb_ctx* ctx, int boundary_id, dgb_bc_fn fn, void* user, double t);
+/* Time-dependent Dirichlet data (MomentumRhs::time, forms.cpp:1061-1062): with enable != 0
+ * the callbacks registered by dgb_set_dirichlet_fn (kept, non-owning: fn / user must stay
+ * valid) are re-evaluated at every stage time t* inside dgb_trbdf2_step /
+ * dgb_projection_step (t^n + gamma dt, t^n + dt).  Off by default: BASELINE data is
+ * time-independent and one tabulation serves every step. */
+int dgb_set_dirichlet_time_dependent(dgb_ctx* ctx, int enable);
 /* Physical coordinates of boundary-face quadrature points of rule q1d,
  * [n_boundary_faces][nqf][dim] (GeometryCache::boundary_faces().xq). */
 int dgb_boundary_points(dgb_ctx* ctx, int q1d, double* xq_host);

@@ -151,8 +151,13 @@ class Device {
   }
   dgb_ctx* ctx() const { return ctx_; }
 
-  /// BoundaryTable (forms.hpp:29-51): types + Dirichlet data tabulated at time t.
-  void set_boundary(const dgns::BoundaryTable<dim>& bc, double t) {
+  /// BoundaryTable (forms.hpp:29-51): types + Dirichlet data tabulated at time t.  The
+  /// table's std::functions may depend on t, so device steps re-evaluate them at every
+  /// stage time (dgb_set_dirichlet_time_dependent); bc must outlive the Device's use of
+  /// it, like the reference's non-owning MomentumRhs::bc.  Pass time_dependent = false
+  /// for time-independent data (one tabulation, no host work inside steps).
+  void set_boundary(const dgns::BoundaryTable<dim>& bc, double t, bool time_dependent = true) {
+    check(dgb_set_dirichlet_time_dependent(ctx_, time_dependent ? 1 : 0));
     for (const auto& [id, e] : bc.entries) {
       check(dgb_set_boundary_type(ctx_, id, e.type == dgns::BcType::outlet ? DGB_BC_OUTLET : DGB_BC_DIRICHLET));
       if (e.value) {

@@ -102,6 +102,7 @@ def lib() -> C.CDLL:
     L.dgb_set_boundary_type.argtypes = [C.c_void_p, C.c_int, C.c_int]
     L.dgb_set_dirichlet_table.argtypes = [C.c_void_p, _dp]
     L.dgb_set_dirichlet_fn.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_double]
+    L.dgb_set_dirichlet_time_dependent.argtypes = [C.c_void_p, C.c_int]
     L.dgb_boundary_points.argtypes = [C.c_void_p, C.c_int, _dp]
     L.dgb_node_points.argtypes = [C.c_void_p, C.c_int, _dp]
     L.dgb_face_lists.argtypes = [C.c_void_p, _ip, _ip]
@@ -281,6 +282,11 @@ class DGContext:
     def set_dirichlet_fn(self, boundary_id: int, fn_ptr, user, t: float = 0.0):
         """fn_ptr: a C function pointer (e.g. lib().dgb_synth_eval) with its user data."""
         _check(lib().dgb_set_dirichlet_fn(self._h, boundary_id, C.cast(fn_ptr, C.c_void_p), user, t))
+
+    def set_dirichlet_time_dependent(self, enable: bool):
+        """Re-evaluate the registered Dirichlet callbacks at every stage time of a step
+        (MomentumRhs::time semantics, forms.cpp:1061-1062)."""
+        _check(lib().dgb_set_dirichlet_time_dependent(self._h, int(bool(enable))))
 
     def boundary_points(self, q1d: int):
         import numpy as np

@@ -132,6 +132,12 @@ int dgb_set_boundary_type(dgb_ctx* h, int id, int type) {
   cudaStreamSynchronize(h->c.dc.stream);
   return DGB_OK;
 }
+int dgb_set_dirichlet_time_dependent(dgb_ctx* h, int enable) {
+  DevGuard guard_(h);
+  NEED(h, "null ctx");
+  h->c.g_time_dep_ = enable != 0;
+  return DGB_OK;
+}
 int dgb_set_dirichlet_table(dgb_ctx* h, const double* g) {
   DevGuard guard_(h);
   NEED(h, "null ctx");

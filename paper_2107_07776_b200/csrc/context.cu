@@ -1040,6 +1040,21 @@ int Context::set_dirichlet_table(const double* g) {
   return DGB_OK;
 }
 int Context::set_dirichlet_fn(int id, dgb_bc_fn fn, void* user, double t) {
+  if (id >= 0 && id < 64) bc_fn_[id] = {fn, user};
+  g_time_ = t;
+  return tabulate_dirichlet(id, fn, user, t);
+}
+// Time-dependent data (forms.cpp:1061-1062 evaluates g at MomentumRhs::time): with
+// set_dirichlet_time_dependent(1), every registered callback is re-evaluated at each
+// stage time t* of a step before the stage's RHS.
+int Context::dirichlet_at(double t) {
+  if (!g_time_dep_ || t == g_time_) return DGB_OK;
+  for (int id = 0; id < 64; ++id)
+    if (bc_fn_[id].first) OK(tabulate_dirichlet(id, bc_fn_[id].first, bc_fn_[id].second, t));
+  g_time_ = t;
+  return DGB_OK;
+}
+int Context::tabulate_dirichlet(int id, dgb_bc_fn fn, void* user, double t) {
   const int Q = ku + 2, nq = nqf(Q);
   std::vector<double> xq;
   boundary_points(mesh, Q, xq);
@@ -1222,6 +1237,7 @@ int Context::projection_step(int scheme, const dgb_step_params& P, const double*
       return DGB_OK;
     };
     CK(cudaMemcpyAsync(u_np1, u_n, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    OK(dirichlet_at(P.time + dt));
     OK(predictor(its[0]));
     for (int it = 0; it < P.fp_max_iter; ++it) {
       CK(cudaMemcpyAsync(wv, u_n, NU * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -1278,6 +1294,7 @@ int Context::projection_step(int scheme, const dgb_step_params& P, const double*
     rd.dir_visc_coef = 1.0 / Re;
     rd.dir_adv_coef = 1.0;
     rd.dir_w = wv;
+    OK(dirichlet_at(P.time + dt));
     OK(stage(0, 2.0 / 3.0, mc, rd, u_n, p_n, u_np1, p_np1));
     CK(cudaStreamSynchronize(st));
     return DGB_OK;
@@ -1310,6 +1327,7 @@ int Context::projection_step(int scheme, const dgb_step_params& P, const double*
     rd.dir_visc_coef = 1.0 / (2.0 * Re);
     rd.dir_adv_coef = 0.5;
     rd.dir_w = wv;
+    OK(dirichlet_at(P.time + gm * dt));
     OK(stage(0, gm, mc, rd, u_n, p_n, u_g, p_g));
   }
   // ---- stage 2
@@ -1341,6 +1359,7 @@ int Context::projection_step(int scheme, const dgb_step_params& P, const double*
     rd.dir_visc_coef = a33 / Re;
     rd.dir_adv_coef = a33;
     rd.dir_w = wv;
+    OK(dirichlet_at(P.time + dt));
     OK(stage(1, 1.0 - gm, mc, rd, u_g, p_g, u_np1, p_np1));
   }
   CK(cudaStreamSynchronize(st));

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/dgb.h"
@@ -93,6 +94,11 @@ class Context {
   // Dirichlet data
   int set_dirichlet_table(const double* g);
   int set_dirichlet_fn(int id, dgb_bc_fn fn, void* user, double t);
+  int tabulate_dirichlet(int id, dgb_bc_fn fn, void* user, double t);
+  int dirichlet_at(double t);  // re-tabulate time-dependent data at t (no-op otherwise)
+  std::pair<dgb_bc_fn, void*> bc_fn_[64] = {};
+  bool g_time_dep_ = false;
+  double g_time_ = 0.0;
 
   // device scratch helpers
   double* scratch_vec(int slot, size_t n);  // persistent per-slot device buffers

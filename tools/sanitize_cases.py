@@ -49,4 +49,4 @@ if __name__ == "__main__":
     case(4, 3, steps=True)
     case(3, 4, 0.03, steps=True)
     case(3, 2)
-    case(5, 1)
+    case(2, 4)
