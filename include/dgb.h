@@ -81,6 +81,12 @@ int dgb_set_dirichlet_fn(dgb_ctx* ctx, int boundary_id, dgb_bc_fn fn, void* user
  * dgb_projection_step (t^n + gamma dt, t^n + dt).  Off by default: BASELINE data is
  * time-independent and one tabulation serves every step. */
 int dgb_set_dirichlet_time_dependent(dgb_ctx* ctx, int enable);
+/* Multi-GPU z-slabs (paper_2107_07776_b200/slabs.py): the fast 3D operator
+ * applies (momentum, pressure / Laplacian) compute only cells [cell0, cell1) of the
+ * context (the rank's owned cells; the others are ghost cells whose values the halo
+ * exchange supplies) and leave the other rows of the output untouched.  cell1 < 0 =
+ * all cells (the default).  Other kernels compute every cell. */
+int dgb_set_cell_range(dgb_ctx* ctx, int cell0, int cell1);
 /* Physical coordinates of boundary-face quadrature points of rule q1d,
  * [n_boundary_faces][nqf][dim] (GeometryCache::boundary_faces().xq). */
 int dgb_boundary_points(dgb_ctx* ctx, int q1d, double* xq_host);

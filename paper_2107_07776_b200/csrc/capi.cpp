@@ -132,6 +132,14 @@ int dgb_set_boundary_type(dgb_ctx* h, int id, int type) {
   cudaStreamSynchronize(h->c.dc.stream);
   return DGB_OK;
 }
+int dgb_set_cell_range(dgb_ctx* h, int cell0, int cell1) {
+  DevGuard guard_(h);
+  NEED(h, "null ctx");
+  NEED(cell0 >= 0 && (cell1 < 0 || (cell1 >= cell0 && cell1 <= h->c.mesh.ncells)), "bad cell range");
+  h->c.dc.mesh.cell0 = cell0;
+  h->c.dc.mesh.cell1 = cell1;
+  return DGB_OK;
+}
 int dgb_set_dirichlet_time_dependent(dgb_ctx* h, int enable) {
   DevGuard guard_(h);
   NEED(h, "null ctx");

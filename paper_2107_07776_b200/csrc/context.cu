@@ -429,10 +429,12 @@ int Context::apply_host(bool mom, const double* coefs, double mc, const double* 
   }
   const MomCoef co = mom ? MomCoef{coefs[0], coefs[1], coefs[2], coefs[3]} : MomCoef{};
   int rc = DGB_OK;
-  // the slab range is reset on every exit, including an early CK() return
-  ScopeExit reset_range([this] {
-    dc.mesh.cell0 = 0;
-    dc.mesh.cell1 = -1;
+  // the caller's cell range (dgb_set_cell_range) is restored on every exit, including an
+  // early CK() return
+  const int keep0 = dc.mesh.cell0, keep1 = dc.mesh.cell1;
+  ScopeExit reset_range([this, keep0, keep1] {
+    dc.mesh.cell0 = keep0;
+    dc.mesh.cell1 = keep1;
   });
   for (int s = 0; s < ns && rc == DGB_OK; ++s) {
     CK(cudaStreamWaitEvent(st, ev_in_[std::min(s + 1, ns - 1)], 0));
@@ -446,8 +448,6 @@ int Context::apply_host(bool mom, const double* coefs, double mc, const double* 
     const size_t o = (size_t)cells(s) * nbc, len = (size_t)(cells(s + 1) - cells(s)) * nbc;
     CK(cudaMemcpyAsync(h_y + o, dy + o, len * sizeof(double), cudaMemcpyDeviceToHost, cp_out_));
   }
-  dc.mesh.cell0 = 0;
-  dc.mesh.cell1 = -1;
   CK(cudaStreamSynchronize(cp_out_));
   CK(cudaStreamSynchronize(st));
   return rc;
