@@ -85,7 +85,8 @@ int dgb_set_dirichlet_time_dependent(dgb_ctx* ctx, int enable);
  * applies (momentum, pressure / Laplacian) compute only cells [cell0, cell1) of the
  * context (the rank's owned cells; the others are ghost cells whose values the halo
  * exchange supplies) and leave the other rows of the output untouched.  cell1 < 0 =
- * all cells (the default).  Other kernels compute every cell. */
+ * all cells (the default).  Other kernels (and the momentum apply at k = 4, which has
+ * no axis-aligned fast kernel) compute every cell. */
 int dgb_set_cell_range(dgb_ctx* ctx, int cell0, int cell1);
 /* Physical coordinates of boundary-face quadrature points of rule q1d,
  * [n_boundary_faces][nqf][dim] (GeometryCache::boundary_faces().xq). */

@@ -42,8 +42,12 @@ def test_emulated_ranks_match_single_domain_apply(gpu, n, ku, world):
         ou, op = part.owned(nu), part.owned(npb)
         assert float((ly[ou] - y[c0 * nu:c1 * nu]).norm() / y[c0 * nu:c1 * nu].norm()) <= 1e-14
         assert float((lyp[op] - yp[c0 * npb:c1 * npb]).norm() / yp[c0 * npb:c1 * npb].norm()) <= 1e-14
-        # only the owned cells were computed: the ghost rows are untouched (still zero)
-        assert float(ly[:ou.start].abs().sum() + ly[ou.stop:].abs().sum()) == 0.0
+        # only the owned cells were computed: the ghost rows are untouched (still zero);
+        # the axis-aligned fast momentum kernel covers K <= 3 (K = 4 runs the generic
+        # kernel, which computes every local cell -- same owned result)
+        gp = float(lyp[:op.start].abs().sum() + lyp[op.stop:].abs().sum())
+        gu = float(ly[:ou.start].abs().sum() + ly[ou.stop:].abs().sum())
+        assert gp == 0.0 and (gu == 0.0 or ku == 4)
 
 
 def _free_port():
