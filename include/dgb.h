@@ -88,6 +88,11 @@ int dgb_set_dirichlet_time_dependent(dgb_ctx* ctx, int enable);
  * all cells (the default).  Other kernels (and the momentum apply at k = 4, which has
  * no axis-aligned fast kernel) compute every cell. */
 int dgb_set_cell_range(dgb_ctx* ctx, int cell0, int cell1);
+/* Debug switches.  DGB_DEBUG_POISON_SMEM: every operator kernel first fills its dynamic
+ * shared memory with NaN, so a stage reading a value no earlier stage of the launch wrote
+ * (an uninitialised read / missing barrier) changes the result (tests/test_gpu_race.py). */
+enum { DGB_DEBUG_POISON_SMEM = 1 };
+int dgb_set_debug(dgb_ctx* ctx, int flags);
 /* Physical coordinates of boundary-face quadrature points of rule q1d,
  * [n_boundary_faces][nqf][dim] (GeometryCache::boundary_faces().xq). */
 int dgb_boundary_points(dgb_ctx* ctx, int q1d, double* xq_host);

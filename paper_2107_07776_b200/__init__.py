@@ -104,6 +104,7 @@ def lib() -> C.CDLL:
     L.dgb_set_dirichlet_fn.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_double]
     L.dgb_set_dirichlet_time_dependent.argtypes = [C.c_void_p, C.c_int]
     L.dgb_set_cell_range.argtypes = [C.c_void_p, C.c_int, C.c_int]
+    L.dgb_set_debug.argtypes = [C.c_void_p, C.c_int]
     L.dgb_boundary_points.argtypes = [C.c_void_p, C.c_int, _dp]
     L.dgb_node_points.argtypes = [C.c_void_p, C.c_int, _dp]
     L.dgb_face_lists.argtypes = [C.c_void_p, _ip, _ip]

@@ -132,6 +132,12 @@ int dgb_set_boundary_type(dgb_ctx* h, int id, int type) {
   cudaStreamSynchronize(h->c.dc.stream);
   return DGB_OK;
 }
+int dgb_set_debug(dgb_ctx* h, int flags) {
+  DevGuard guard_(h);
+  NEED(h, "null ctx");
+  h->c.dc.mesh.poison = (flags & DGB_DEBUG_POISON_SMEM) ? 1 : 0;
+  return DGB_OK;
+}
 int dgb_set_cell_range(dgb_ctx* h, int cell0, int cell1) {
   DevGuard guard_(h);
   NEED(h, "null ctx");

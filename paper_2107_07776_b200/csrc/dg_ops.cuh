@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(mom_threads<K>()) k_momentum(MeshArgs m, GeoAr
   using EB = typename L::EB;
   constexpr int NB = L::NB, NF = L::NF, CB = L::CB;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   double* U = sm;
   double* UNB = U + CB * NB;         // NF neighbour blocks
   double* OUT = UNB + CB * NF * NB;
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_sip(MeshArgs m, GeoArgs gq, dou
   using E = typename L::E;
   constexpr int NB = L::NB, NF = L::NF, CB = L::CB, NQ = E::NQ, NQF = E::NQF;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   double* U = sm;
   double* UNB = U + CB * NB;
   double* OUT = UNB + CB * NF * NB;
@@ -445,6 +447,7 @@ __global__ void __launch_bounds__(kThreads) k_mass(MeshArgs m, GeoArgs gq, const
   using E = typename L::E;
   constexpr int NB = E::NB, NQ = E::NQ, CB = L::CB;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   double* U = sm;
   double* OUT = U + CB * NB;
   double* SCR = OUT + CB * NB;
@@ -480,6 +483,7 @@ __global__ void __launch_bounds__(kThreads) k_kinetic(MeshArgs m, GeoArgs gq, co
   using E = typename L::E;
   constexpr int NB = E::NB, NQ = E::NQ, CB = L::CB;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   double* U = sm;
   double* SCR = U + 2 * CB * NB;
   double* QBK = SCR + CB * E::SCR;
@@ -533,6 +537,7 @@ __global__ void __launch_bounds__(kThreads) k_gradient(MeshArgs m, GeoArgs gq, c
   using EU = typename L::EU;
   constexpr int CB = L::CB, NQ = EU::NQ;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   double* P = sm;
   double* OUT = P + CB * EP::NB;
   double* SCR = OUT + CB * EU::NB;
@@ -593,6 +598,7 @@ __global__ void __launch_bounds__(kThreads) k_divergence(MeshArgs m, GeoArgs gq,
   using EU = typename L::EU;
   constexpr int CB = L::CB, NF = L::NF, NQ = EU::NQ, NQF = EU::NQF, NBU = EU::NB;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   double* U = sm;
   double* UNB = U + CB * NBU;
   double* OUT = UNB + CB * NF * NBU;

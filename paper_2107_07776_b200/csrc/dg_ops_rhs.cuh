@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(kThreads) k_momentum_rhs(MeshArgs m, GeoArgs g
   using EP = typename L::EP;
   constexpr int NB = L::NB, NBP = L::NBP, NF = L::NF, CB = L::CB;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   double* U = sm;
   double* UN = U + CB * NB;
   double* OUT = UN + CB * NB;
@@ -418,6 +419,7 @@ __global__ void __launch_bounds__(kThreads) k_momentum_diag(MeshArgs m, GeoArgs 
   using EB = typename L::EB;
   constexpr int N = K + 1, QA = K + 1, QB = K + 2, NB = L::NB, NF = L::NF, CB = L::CB;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   double* U = sm;
   double* UNB = U + CB * NB;
   double* OUT = UNB + CB * NF * NB;

@@ -18,7 +18,24 @@ struct MeshArgs {
   const int* bslot = nullptr;    // [ncells][2dim]: boundary-face index (reference order) or -1
   const int* skip = nullptr;     // device flag: nonzero -> the launch is a no-op (device-side Krylov exit)
   int cell0 = 0, cell1 = -1;     // fast kernels: process cells [cell0, cell1) only (-1: ncells)
+  int poison = 0;                // debug (dgb_set_debug): fill dynamic shared memory with NaN first
 };
+
+#ifdef __CUDACC__
+// Debug check for reads of shared memory that no stage of this launch wrote (the
+// uninitialised-read half of a race detector; compute-sanitizer is not available on the
+// GPU pool): every CTA first fills its dynamic shared memory with a NaN pattern, so a
+// stage that consumed a value before its producer stored it changes the result
+// (tests/test_gpu_race.py compares poisoned and clean launches bit for bit).
+#define DGB_POISON_SMEM(m, sm)                                                             \
+  if ((m).poison) {                                                                       \
+    unsigned nbytes_;                                                                     \
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(nbytes_));                     \
+    for (unsigned i_ = threadIdx.x; i_ < nbytes_ / 8; i_ += blockDim.x)                   \
+      (sm)[i_] = __longlong_as_double(0x7ff8dead0000beefll);                             \
+    __syncthreads();                                                                      \
+  }
+#endif
 
 struct GeoArgs {
   const double* aff = nullptr;    // affine: per cell {Jinv, detJ, per face {n, ds}}

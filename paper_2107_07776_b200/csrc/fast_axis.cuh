@@ -507,6 +507,7 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
   constexpr int N = G::N, NB = G::NB, NF = G::NF, C = G::C, PER = G::PER, TT = G::T;
   const FTab<N, N>& ta = c_ft<N, N>;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   const int c0 = m.cell0 + blockIdx.x * C;
   const int nc = min(C, (m.cell1 < 0 ? m.ncells : m.cell1) - c0);
   const int tid = threadIdx.x;
@@ -772,6 +773,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   const FTab<N, Q>& tq = c_ft<N, Q>;  // k+2 rule: B, D, w (advection)
   const FTab<N, N>& ta = c_ft<N, N>;  // exact M, K, dE
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   const int c0 = m.cell0 + blockIdx.x * C;
   const int nc = min(C, (m.cell1 < 0 ? m.ncells : m.cell1) - c0);
   const int tid = threadIdx.x;
@@ -1336,6 +1338,7 @@ __global__ void __launch_bounds__(PGradCfg<K>::T) k_pgrad_axis(MeshArgs m, Unifo
   constexpr int N = G::N, NP = G::NP, NBP = G::NBP, NB = G::NB, C = G::C, PER = G::PER, TT = G::T;
   const PTab<K>& pt = c_pt<K>;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   const int c0 = blockIdx.x * C;
   const int nc = min(C, m.ncells - c0);
   const int tid = threadIdx.x;
@@ -1460,6 +1463,7 @@ __global__ void __launch_bounds__(MomDiagCfg<K>::T) k_momentum_diag_axis(MeshArg
   const FTab<N, Q>& tq = c_ft<N, Q>;
   const FTab<N, N>& ta = c_ft<N, N>;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   const int c0 = blockIdx.x * C;
   const int nc = min(C, m.ncells - c0);
   const int tid = threadIdx.x, lane = tid & 31, wc = tid >> 5;
@@ -1702,6 +1706,7 @@ __global__ void __launch_bounds__(DivCfg<K>::T) k_div_axis(MeshArgs m, UniformGr
   constexpr int N = G::N, NP = G::NP, NB = G::NB, NBP = G::NBP, C = G::C, PER = G::PER, TT = G::T;
   const PTab<K>& pt = c_pt<K>;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   const int c0 = blockIdx.x * C;
   const int nc = min(C, m.ncells - c0);
   const int tid = threadIdx.x;

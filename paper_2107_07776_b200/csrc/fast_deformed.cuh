@@ -434,6 +434,7 @@ __global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const do
   using G = SipQpCfg<KP>;
   constexpr int N = G::N, Q = G::Q, NB = G::NB, NQ = G::NQ, NQF = G::NQF, C = G::C, PER = G::PER;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   const int c0 = blockIdx.x * C;
   const int nc = min(C, m.ncells - c0);
   const int tid = threadIdx.x, lane = tid & 31, wc = tid >> 5;
@@ -693,6 +694,7 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
   constexpr int N = G::N, QA = G::QA, QB = G::QB, NB = G::NB, NF = G::NF, NQB = G::NQB, NQFB = G::NQFB;
   constexpr int C = G::C, PER = G::PER;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   const int c0 = blockIdx.x * C;
   const int nc = min(C, m.ncells - c0);
   const int tid = threadIdx.x, lane = tid & 31, wc = tid >> 5;
@@ -1012,6 +1014,7 @@ __global__ void __launch_bounds__(MomDiagQpCfg<K, SCALAR>::T) k_momentum_diag_qp
   constexpr int N = G::N, QA = G::QA, QB = G::QB, NB = G::NB, NF = G::NF;
   constexpr int NQA = G::NQA, NQFA = G::NQFA, NQB = G::NQB, NQFB = G::NQFB, C = G::C, PER = G::PER;
   extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
   const int c0 = blockIdx.x * C;
   const int nc = min(C, m.ncells - c0);
   const int tid = threadIdx.x, lane = tid & 31, wc = tid >> 5;
