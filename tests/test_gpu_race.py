@@ -42,7 +42,7 @@ def _ops(gpu, D, seed=1):
 @pytest.mark.parametrize("dim,n_el,ku,amp", [(3, 4, 3, 0.0), (3, 5, 2, 0.0), (3, 6, 1, 0.0), (3, 3, 4, 0.03),
                                              (3, 3, 3, 0.03), (3, 3, 2, 0.03), (3, 2, 4, 0.0), (2, 4, 2, 0.05)])
 def test_poisoned_shared_memory_changes_nothing(gpu, dim, n_el, ku, amp):
-    D = gpu.DGContext(dim, n_el, ku, ku - 1, amp, 3)
+    D = gpu.DGContext(dim, n_el, ku, max(1, ku - 1), amp, 3)
     f = gpu.SynthField(dim, 1)
     for bid in range(2 * dim):
         D.set_dirichlet_fn(bid, f.fn_ptr, f.user_ptr, 0.0)
