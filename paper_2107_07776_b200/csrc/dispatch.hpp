@@ -27,14 +27,15 @@ struct MeshArgs {
 // GPU pool): every CTA first fills its dynamic shared memory with a NaN pattern, so a
 // stage that consumed a value before its producer stored it changes the result
 // (tests/test_gpu_race.py compares poisoned and clean launches bit for bit).
-#define DGB_POISON_SMEM(m, sm)                                                             \
-  if ((m).poison) {                                                                       \
-    unsigned nbytes_;                                                                     \
-    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(nbytes_));                     \
-    for (unsigned i_ = threadIdx.x; i_ < nbytes_ / 8; i_ += blockDim.x)                   \
-      (sm)[i_] = __longlong_as_double(0x7ff8dead0000beefll);                             \
-    __syncthreads();                                                                      \
-  }
+// (out of line, so the check costs the hot kernels no registers when it is off)
+__device__ __noinline__ inline void dgb_poison_smem(double* sm) {
+  unsigned nbytes;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(nbytes));
+  for (unsigned i = threadIdx.x; i < nbytes / 8; i += blockDim.x) sm[i] = __longlong_as_double(0x7ff8dead0000beefll);
+  __syncthreads();
+}
+#define DGB_POISON_SMEM(m, sm) \
+  if ((m).poison) dgb_poison_smem(sm)
 #endif
 
 struct GeoArgs {

@@ -132,6 +132,25 @@ __device__ __forceinline__ int cell_nbr(const MeshArgs& m, const UniformGrid& g,
   if (UNI) return uniform_nbr(g, cell, f);
   return m.nbr[(size_t)cell * 6 + f];
 }
+// All six neighbours of one cell at once (the uniform-grid coordinates take two
+// divisions instead of two per face).
+template <bool UNI>
+__device__ __forceinline__ void cell_nbrs6(const MeshArgs& m, const UniformGrid& g, int cell, int nb[6]) {
+  if (!UNI) {
+#pragma unroll
+    for (int f = 0; f < 6; ++f) nb[f] = m.nbr[(size_t)cell * 6 + f];
+    return;
+  }
+  const int n = g.n;
+  const unsigned q1 = udiv_n(g, (unsigned)cell), q2 = udiv_n(g, q1);
+  const int co[3] = {cell - n * (int)q1, (int)q1 - n * (int)q2, (int)q2};
+  const int stride[3] = {1, n, n * n};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    nb[2 * d] = co[d] == 0 ? -1 - 2 * d : cell - stride[d];
+    nb[2 * d + 1] = co[d] == n - 1 ? -2 - 2 * d : cell + stride[d];
+  }
+}
 
 // Parallel fill of the CellInfo records of nc cells: one thread per (cell, slot),
 // slot 0..5 = faces, slot 6 = cell geometry (independent L2 loads in flight together).
@@ -801,13 +820,6 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
 #define INFO(c) (*reinterpret_cast<CellInfo*>(sm + (c) * PER + G::O_INFO))
 
   // ------------------------------------------------------------------ S0: x, w (padded), info
-  for (int idx = tid; idx < nc * 3 * NB; idx += TT) {
-    const int c = idx / (3 * NB), r = idx - c * 3 * NB;
-    const int comp = r / NB, i = r - comp * NB;
-    const int pi = comp * CT + P::idx(i % N, (i / N) % N, i / NF);
-    cp_async8(CELL(c) + G::O_X + pi, x + (size_t)(c0 + c) * 3 * NB + r);
-    if (MODE != 1) cp_async8(CELL(c) + G::O_W + pi, w + (size_t)(c0 + c) * 3 * NB + r);
-  }
   // Pass-A neighbour lines: every thread issues the loads of ALL its stage-A items now
   // (registers), overlapping the cp.async staging and the info loads.  Neighbours
   // owned by this CTA are read from shared memory later instead.  Items of one
@@ -816,43 +828,124 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
   constexpr int NID = 3 * NF;                      // items per cell and direction
   constexpr int MAXJ = WPC ? (NID + 31) / 32 : (C * NID + TT - 1) / TT;  // items per thread and direction
   double nbL[3][MAXJ][N], nbR[3][MAXJ][N];
+#ifndef DGB_WPC_S0
+#define DGB_WPC_S0 1
+#endif
+  if constexpr (WPC && DGB_WPC_S0) {
+    // one warp stages its own cell: the six neighbours once per warp, element / item
+    // indices from the lane and compile-time loop counters (the CTA-wide loops of the
+    // generic staging spend most of their instructions on index divisions)
+    const int c = wcell, cell = c0 + c;
+    const bool live = c < nc;
+    int nbf[6];
+    cell_nbrs6<UNI>(m, ug, live ? cell : c0, nbf);
+    if (live) {
+      const double* xs = x + (size_t)cell * 3 * NB;
+      const double* ws = w + (size_t)cell * 3 * NB;
 #pragma unroll
-  for (int d = 0; d < 3; ++d)
-#pragma unroll
-    for (int j = 0; j < MAXJ; ++j) {
-      const int it = it0 + j * IST;
-#pragma unroll
-      for (int l = 0; l < N; ++l) nbL[d][j][l] = nbR[d][j][l] = 0.0;
-      if (passA && it < ITEMS(NID)) {
-        const int c = CELLOF(it, NID), r = RESTOF(it, c, NID);
-        int comp, tl;
-        line_item<K, NF>(r, d, comp, tl);
-        const int p = tl % N, q = tl / N;
-        const int nl = cell_nbr<UNI>(m, ug, c0 + c, 2 * d), nr = cell_nbr<UNI>(m, ug, c0 + c, 2 * d + 1);
-        const int gst = d == 0 ? 1 : (d == 1 ? N : NF);
-        const int g0 = comp * NB + (d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q));
-        const bool extL = nl >= 0 && (nl < c0 || nl >= c0 + nc);
-        const bool extR = nr >= 0 && (nr < c0 || nr >= c0 + nc);
-#pragma unroll
-        for (int l = 0; l < N; ++l) {
-          if (extL) nbL[d][j][l] = __ldg(x + (size_t)nl * 3 * NB + g0 + l * gst);
-          if (extR) nbR[d][j][l] = __ldg(x + (size_t)nr * 3 * NB + g0 + l * gst);
+      for (int k = 0; k < (3 * NB + 31) / 32; ++k) {
+        const int e = lane + 32 * k;
+        if (e < 3 * NB) {
+          const int comp = e / NB, i = e - comp * NB;
+          const int pi = comp * CT + P::idx(i % N, (i / N) % N, i / NF);
+          cp_async8(CELL(c) + G::O_X + pi, xs + e);
+          if (MODE != 1) cp_async8(CELL(c) + G::O_W + pi, ws + e);
         }
       }
     }
-  if (faces) {  // neighbour w_a traces on each face (async; zeros on boundary faces)
-    for (int idx = tid; idx < nc * 6 * NF; idx += TT) {
-      const int c = idx / (6 * NF), r = idx - c * 6 * NF;
-      const int f = r / NF, t = r - f * NF;
-      const int a = f >> 1, p = t % N, q = t / N;
-      const int nb = cell_nbr<UNI>(m, ug, c0 + c, f);
-      const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
-      const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + ((f & 1) ? 0 : N - 1) * gst;
-      double* dst = WK(c) + G::F_NB + f * G::NBS + 3 * NF + t;
-      if (nb >= 0)
-        cp_async8(dst, w + (size_t)nb * 3 * NB + a * NB + go);
-      else
-        *dst = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int nl = nbf[2 * d], nr = nbf[2 * d + 1];
+#ifndef DGB_NB_GLOBAL
+#define DGB_NB_GLOBAL 1
+#endif
+      const bool extL = nl >= 0 && (DGB_NB_GLOBAL || nl < c0 || nl >= c0 + nc);
+      const bool extR = nr >= 0 && (DGB_NB_GLOBAL || nr < c0 || nr >= c0 + nc);
+      const int gst = d == 0 ? 1 : (d == 1 ? N : NF);
+#pragma unroll
+      for (int j = 0; j < MAXJ; ++j) {
+        const int r = lane + 32 * j;
+#pragma unroll
+        for (int l = 0; l < N; ++l) nbL[d][j][l] = nbR[d][j][l] = 0.0;
+        if (passA && live && r < NID) {
+          int comp, tl;
+          line_item<K, NF>(r, d, comp, tl);
+          const int p = tl % N, q = tl / N;
+          const int g0 = comp * NB + (d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q));
+#pragma unroll
+          for (int l = 0; l < N; ++l) {
+            if (extL) nbL[d][j][l] = __ldg(x + (size_t)nl * 3 * NB + g0 + l * gst);
+            if (extR) nbR[d][j][l] = __ldg(x + (size_t)nr * 3 * NB + g0 + l * gst);
+          }
+        }
+      }
+    }
+    if (faces && live) {  // neighbour w_a traces on each face (async; zeros on boundary faces)
+#pragma unroll
+      for (int k = 0; k < (6 * NF + 31) / 32; ++k) {
+        const int r = lane + 32 * k;
+        if (r < 6 * NF) {
+          const int f = r / NF, t = r - f * NF;
+          const int a = f >> 1, p = t % N, q = t / N;
+          int nb = nbf[0];
+#pragma unroll
+          for (int ff = 1; ff < 6; ++ff) nb = f == ff ? nbf[ff] : nb;
+          const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
+          const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + ((f & 1) ? 0 : N - 1) * gst;
+          double* dst = WK(c) + G::F_NB + f * G::NBS + 3 * NF + t;
+          if (nb >= 0)
+            cp_async8(dst, w + (size_t)nb * 3 * NB + a * NB + go);
+          else
+            *dst = 0.0;
+        }
+      }
+    }
+  } else {
+    for (int idx = tid; idx < nc * 3 * NB; idx += TT) {
+      const int c = idx / (3 * NB), r = idx - c * 3 * NB;
+      const int comp = r / NB, i = r - comp * NB;
+      const int pi = comp * CT + P::idx(i % N, (i / N) % N, i / NF);
+      cp_async8(CELL(c) + G::O_X + pi, x + (size_t)(c0 + c) * 3 * NB + r);
+      if (MODE != 1) cp_async8(CELL(c) + G::O_W + pi, w + (size_t)(c0 + c) * 3 * NB + r);
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int j = 0; j < MAXJ; ++j) {
+        const int it = it0 + j * IST;
+#pragma unroll
+        for (int l = 0; l < N; ++l) nbL[d][j][l] = nbR[d][j][l] = 0.0;
+        if (passA && it < ITEMS(NID)) {
+          const int c = CELLOF(it, NID), r = RESTOF(it, c, NID);
+          int comp, tl;
+          line_item<K, NF>(r, d, comp, tl);
+          const int p = tl % N, q = tl / N;
+          const int nl = cell_nbr<UNI>(m, ug, c0 + c, 2 * d), nr = cell_nbr<UNI>(m, ug, c0 + c, 2 * d + 1);
+          const int gst = d == 0 ? 1 : (d == 1 ? N : NF);
+          const int g0 = comp * NB + (d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q));
+          const bool extL = nl >= 0 && (nl < c0 || nl >= c0 + nc);
+          const bool extR = nr >= 0 && (nr < c0 || nr >= c0 + nc);
+#pragma unroll
+          for (int l = 0; l < N; ++l) {
+            if (extL) nbL[d][j][l] = __ldg(x + (size_t)nl * 3 * NB + g0 + l * gst);
+            if (extR) nbR[d][j][l] = __ldg(x + (size_t)nr * 3 * NB + g0 + l * gst);
+          }
+        }
+      }
+    if (faces) {  // neighbour w_a traces on each face (async; zeros on boundary faces)
+      for (int idx = tid; idx < nc * 6 * NF; idx += TT) {
+        const int c = idx / (6 * NF), r = idx - c * 6 * NF;
+        const int f = r / NF, t = r - f * NF;
+        const int a = f >> 1, p = t % N, q = t / N;
+        const int nb = cell_nbr<UNI>(m, ug, c0 + c, f);
+        const int gst = a == 0 ? 1 : (a == 1 ? N : NF);
+        const int go = (a == 0 ? N * (p + N * q) : (a == 1 ? p + NF * q : p + N * q)) + ((f & 1) ? 0 : N - 1) * gst;
+        double* dst = WK(c) + G::F_NB + f * G::NBS + 3 * NF + t;
+        if (nb >= 0)
+          cp_async8(dst, w + (size_t)nb * 3 * NB + a * NB + go);
+        else
+          *dst = 0.0;
+      }
     }
   }
   load_info_par<TT, UNI>(sm, PER, G::O_INFO, nc, m, ug, aff, c0, sfac);
@@ -886,7 +979,8 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
 #pragma unroll
         for (int l = 0; l < N; ++l) u[l] = us[l * st];
         const int nl = ci.nb[2 * d], nr = ci.nb[2 * d + 1];
-        const bool inL = nl >= c0 && nl < c0 + nc, inR = nr >= c0 && nr < c0 + nc;
+        const bool inL = !(WPC && DGB_WPC_S0 && DGB_NB_GLOBAL) && nl >= c0 && nl < c0 + nc;
+        const bool inR = !(WPC && DGB_WPC_S0 && DGB_NB_GLOBAL) && nr >= c0 && nr < c0 + nc;
 #pragma unroll
         for (int l = 0; l < N; ++l) {
           uL[l] = inL ? CELL(nl - c0)[G::O_X + b0 + l * st] : nbL[d][j][l];
@@ -1252,6 +1346,73 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int i = 0; i < N; ++i) acc[j][i] = 0.0;
+#ifndef DGB_S78_HOIST
+#define DGB_S78_HOIST 0
+#endif
+#if DGB_S78_HOIST == 1
+    // the y-test columns of this item's output rows, loaded once (j0 is a runtime index:
+    // reading tq.B[qy][j] inside the qx loop re-issued a constant load per use)
+    double By[NJ][Q], Dy[NJ][Q];
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj)
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        const bool ok = j0 + jj < N;
+        By[jj][qy] = ok ? tq.B[qy][j0 + jj] : 0.0;
+        Dy[jj][qy] = ok ? tq.D[qy][j0 + jj] : 0.0;
+      }
+#pragma unroll
+    for (int qx = 0; qx < Q; ++qx) {
+      double vz[Q], vy[Q], vx[Q];
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        vz[qy] = tp[qx + Q * qy];
+        vy[qy] = tp[G::QQP * N + qx + Q * qy];
+        vx[qy] = tp[2 * G::QQP * N + qx + Q * qy];
+      }
+#pragma unroll
+      for (int jj = 0; jj < NJ; ++jj) {
+        // three independent chains (B vz, D vy, B vx) instead of one of length 2Q
+        double sa = 0.0, sd = 0.0, sb = 0.0;
+#pragma unroll
+        for (int qy = 0; qy < Q; ++qy) {
+          sa = fma(By[jj][qy], vz[qy], sa);
+          sd = fma(Dy[jj][qy], vy[qy], sd);
+          sb = fma(By[jj][qy], vx[qy], sb);
+        }
+        sa += sd;
+#pragma unroll
+        for (int i = 0; i < N; ++i) acc[jj][i] = fma(tq.B[qx][i], sa, fma(tq.D[qx][i], sb, acc[jj][i]));
+      }
+    }
+#elif DGB_S78_HOIST == 2
+#pragma unroll
+    for (int qx = 0; qx < Q; ++qx) {
+      double vz[Q], vy[Q], vx[Q];
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        vz[qy] = tp[qx + Q * qy];
+        vy[qy] = tp[G::QQP * N + qx + Q * qy];
+        vx[qy] = tp[2 * G::QQP * N + qx + Q * qy];
+      }
+#pragma unroll
+      for (int jj = 0; jj < NJ; ++jj) {
+        const int j = j0 + jj;
+        if (j < N) {
+          double sa = 0.0, sd = 0.0, sb = 0.0;
+#pragma unroll
+          for (int qy = 0; qy < Q; ++qy) {
+            sa = fma(tq.B[qy][j], vz[qy], sa);
+            sd = fma(tq.D[qy][j], vy[qy], sd);
+            sb = fma(tq.B[qy][j], vx[qy], sb);
+          }
+          sa += sd;
+#pragma unroll
+          for (int i = 0; i < N; ++i) acc[jj][i] = fma(tq.B[qx][i], sa, fma(tq.D[qx][i], sb, acc[jj][i]));
+        }
+      }
+    }
+#else
 #pragma unroll
     for (int qx = 0; qx < Q; ++qx) {
       double vz[Q], vy[Q], vx[Q];
@@ -1277,6 +1438,7 @@ __global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug
         }
       }
     }
+#endif
     double* o = CELL(c) + G::O_OUT + comp * CT + P::idx(0, 0, l);
 #pragma unroll
     for (int jj = 0; jj < NJ; ++jj)
