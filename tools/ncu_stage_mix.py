@@ -1,12 +1,12 @@
 """Per-stage instruction mix / stall reasons of k_momentum_axis from an ncu report
 (--page source --print-source cuda,sass): SASS rows are attributed to the source line
 above them, lines to the kernel stage whose marker comment precedes them.
-usage: python tools/ncu_stage_mix.py report.ncu-rep [kernel-regex]"""
+usage: python tools/ncu_stage_mix.py report.ncu-rep [kernel-regex] [fast_axis.cuh of the captured build]"""
 import collections, csv, re, subprocess, sys
 
 rep = sys.argv[1]
 kern = sys.argv[2] if len(sys.argv) > 2 else "k_momentum_axis"
-src = "paper_2107_07776_b200/csrc/fast_axis.cuh"
+src = sys.argv[3] if len(sys.argv) > 3 else "paper_2107_07776_b200/csrc/fast_axis.cuh"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{kern}"],
                      capture_output=True, text=True).stdout.splitlines()
 rows = list(csv.reader(out))
@@ -18,13 +18,14 @@ stalls = [n for n in h if n.startswith("stall_") and "Not Issued" not in n]
 lines = open(src).read().split("\n")
 # stage markers: (first line, name)
 marks = []
+kstart = next(i for i, t in enumerate(lines, 1) if "k_momentum_axis(MeshArgs" in t)
 for i, t in enumerate(lines, 1):
     m = re.search(r"//\s*(?:-+\s*)?(S0|A|B|C|D|F1|F2|F3|S45|S6|S78|store|pass A|pass B cell|LF advective)\b", t)
-    if m and i >= 765:
+    if m and i >= kstart:
         marks.append((i, m.group(1)))
 def stage(ln):
     if ln < 0: return "other-files"
-    if ln < 765: return "helpers"
+    if ln < kstart: return "helpers"
     name = "pre"
     for i, n in marks:
         if i <= ln: name = n
