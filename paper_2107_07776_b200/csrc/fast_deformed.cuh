@@ -19,6 +19,7 @@
 #pragma once
 
 #include "fast_axis.cuh"
+#include "qp_layouts.hpp"
 
 namespace dgb {
 
@@ -28,17 +29,23 @@ namespace dgb {
 // x-pass arrays; F3 writes FA over FL, F4 writes FON over FP.
 template <int N, int Q>
 struct QpSipWork {
+  using L = QpLay<N, Q>;  // bank-conflict-optimal array layouts (qp_layouts.hpp)
   static constexpr int NF = N * N;
+  static constexpr int mx(int a, int b) { return a > b ? a : b; }
   // cell phase
-  static constexpr int XB = 0, XD = XB + Q * NF, YBB = XD + Q * NF, YDB = YBB + Q * Q * N, YBD = YDB + Q * Q * N,
-                       PP = YBB, R0 = YDB, R1 = YBD, P2 = XB, R02 = XD, CELL_END = YBD + Q * Q * N;
-  // face phase
-  static constexpr int FL = 0, FP = FL + 6 * 4 * NF, FON = FP;
-  static constexpr int FA = 3 * Q <= 4 * N ? FL : FP + 6 * 6 * N * Q;  // over FL when it fits
-  static constexpr int FACE_END = FA + 6 * 3 * Q * N > FP + 6 * 6 * N * Q ? FA + 6 * 3 * Q * N : FP + 6 * 6 * N * Q;
-  // the six neighbour blocks (cp.async-staged by the caller, read in F1): after the cell
-  // phase's arrays, overwritten by F2 onwards
-  static constexpr int NBR = CELL_END, NBR_END = NBR + 6 * N * N * N;
+  static constexpr int XB = 0, XD = XB + L::X_SIZE, YBB = XD + L::X_SIZE, YDB = YBB + L::Y_SIZE,
+                       YBD = YDB + L::Y_SIZE, PP = YBB, R0 = YDB, R1 = YBD, P2 = XB, R02 = XD,
+                       CELL_END = YBD + L::Y_SIZE;
+  // face phase: FL (F1 -> F2), FP (F2 -> F3), FA (F3 -> F4), FON (F4 -> F5); FA reuses FL and
+  // FON reuses FP when they fit (their producers run after the last read of the old array)
+  static constexpr int FL = 0, FP = FL + L::FL_SIZE;
+  static constexpr int FON = L::FO_SIZE <= L::FP_SIZE ? FP : FP + L::FP_SIZE;
+  static constexpr int FA = L::FA_SIZE <= L::FL_SIZE ? FL : mx(FP + L::FP_SIZE, FON + L::FO_SIZE);
+  static constexpr int FACE_END = mx(mx(FP + L::FP_SIZE, FON + L::FO_SIZE), FA + L::FA_SIZE);
+  // the six neighbour blocks (cp.async-staged by the caller during the cell phase, read in
+  // F1): after the cell phase's arrays and after FL, which F1 writes while other lanes still
+  // read the blocks (for N = 2 the round-1 layout let the two overlap), overwritten by F2 on
+  static constexpr int NBR = mx(CELL_END, FL + L::FL_SIZE), NBR_END = NBR + 6 * N * N * N;
   static constexpr int SIZE = NBR_END > FACE_END ? NBR_END : FACE_END;
 };
 
@@ -101,8 +108,16 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
                                              const double* __restrict__ gcell, const double* __restrict__ gface,
                                              double* W, double* OUT, int lane) {
   using Wl = QpSipWork<N, Q>;
+  using L = QpLay<N, Q>;
   constexpr int NF = N * N, NQF = Q * Q;
   const FTab<N, Q>& t = c_ft<N, Q>;
+  // work-array element addresses (qp_layouts.hpp)
+  auto xa = [](int qx, int j, int k) { return qx * L::X_qx + j * L::X_j + k * L::X_k; };
+  auto ya = [](int qx, int qy, int k) { return qx * L::Y_qx + qy * L::Y_qy + k * L::Y_k; };
+  auto fla = [](int f, int fld, int p, int q) { return f * L::FL_f + fld * L::FL_fld + p * L::FL_p + q * L::FL_q; };
+  auto fpa = [](int f, int fld, int q, int qp) { return f * L::FP_f + fld * L::FP_fld + q * L::FP_q + qp * L::FP_qp; };
+  auto faa = [](int f, int part, int qp, int b) { return f * L::FA_f + part * L::FA_part + qp * L::FA_qp + b * L::FA_b; };
+  auto foa = [](int f, int h, int bp, int bq) { return f * L::FO_f + h * L::FO_h + bp * L::FO_bp + bq * L::FO_bq; };
   // ---- cell term
   for (int jk = lane; jk < NF; jk += 32) {  // C1: x pass (values, x-derivative)
     double u[N];
@@ -116,8 +131,8 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
         b = fma(t.B[qx][i], u[i], b);
         d = fma(t.D[qx][i], u[i], d);
       }
-      W[Wl::XB + qx * NF + jk] = b;
-      W[Wl::XD + qx * NF + jk] = d;
+      W[Wl::XB + xa(qx, jk % N, jk / N)] = b;
+      W[Wl::XD + xa(qx, jk % N, jk / N)] = d;
     }
   }
   __syncwarp();
@@ -126,8 +141,8 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
     double vb[N], vd[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      vb[j] = W[Wl::XB + qx * NF + j + N * k];
-      vd[j] = W[Wl::XD + qx * NF + j + N * k];
+      vb[j] = W[Wl::XB + xa(qx, j, k)];
+      vd[j] = W[Wl::XD + xa(qx, j, k)];
     }
 #pragma unroll
     for (int qy = 0; qy < Q; ++qy) {
@@ -138,7 +153,7 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
         db = fma(t.D[qy][j], vb[j], db);
         bd = fma(t.B[qy][j], vd[j], bd);
       }
-      const int o = (qx * Q + qy) * N + k;
+      const int o = ya(qx, qy, k);
       W[Wl::YBB + o] = bb;
       W[Wl::YDB + o] = db;
       W[Wl::YBD + o] = bd;
@@ -149,9 +164,9 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
     double vb[N], vy[N], vx[N];
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      vb[k] = W[Wl::YBB + r * N + k];
-      vy[k] = W[Wl::YDB + r * N + k];
-      vx[k] = W[Wl::YBD + r * N + k];
+      vb[k] = W[Wl::YBB + ya(r / Q, r % Q, k)];
+      vy[k] = W[Wl::YDB + ya(r / Q, r % Q, k)];
+      vx[k] = W[Wl::YBD + ya(r / Q, r % Q, k)];
     }
     double pp[N], r0[N], r1[N];
 #pragma unroll
@@ -187,9 +202,9 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
     }
 #pragma unroll
     for (int k = 0; k < N; ++k) {
-      W[Wl::PP + r * N + k] = pp[k];
-      W[Wl::R0 + r * N + k] = r0[k];
-      W[Wl::R1 + r * N + k] = r1[k];
+      W[Wl::PP + ya(r / Q, r % Q, k)] = pp[k];
+      W[Wl::R0 + ya(r / Q, r % Q, k)] = r0[k];
+      W[Wl::R1 + ya(r / Q, r % Q, k)] = r1[k];
     }
   }
   __syncwarp();
@@ -198,7 +213,7 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
     double p[Q], a0[Q], a1[Q];
 #pragma unroll
     for (int qy = 0; qy < Q; ++qy) {
-      const int o = (qx * Q + qy) * N + k;
+      const int o = ya(qx, qy, k);
       p[qy] = W[Wl::PP + o];
       a0[qy] = W[Wl::R0 + o];
       a1[qy] = W[Wl::R1 + o];
@@ -211,8 +226,8 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
         s = fma(t.B[qy][j], p[qy], fma(t.D[qy][j], a1[qy], s));
         u = fma(t.B[qy][j], a0[qy], u);
       }
-      W[Wl::P2 + qx * NF + j + N * k] = s;
-      W[Wl::R02 + qx * NF + j + N * k] = u;
+      W[Wl::P2 + xa(qx, j, k)] = s;
+      W[Wl::R02 + xa(qx, j, k)] = u;
     }
   }
   __syncwarp();
@@ -220,8 +235,8 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
     double p[Q], a0[Q];
 #pragma unroll
     for (int qx = 0; qx < Q; ++qx) {
-      p[qx] = W[Wl::P2 + qx * NF + jk];
-      a0[qx] = W[Wl::R02 + qx * NF + jk];
+      p[qx] = W[Wl::P2 + xa(qx, jk % N, jk / N)];
+      a0[qx] = W[Wl::R02 + xa(qx, jk % N, jk / N)];
     }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
@@ -259,23 +274,23 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
         if (l == (s ? 0 : N - 1)) vo = v;
       }
     }
-    double* fl = W + Wl::FL + f * 4 * NF;
-    fl[0 * NF + tn] = vs;
-    fl[1 * NF + tn] = dns;
-    fl[2 * NF + tn] = vo;
-    fl[3 * NF + tn] = dno;
+    double* fl = W + Wl::FL;
+    fl[fla(f, 0, p, q)] = vs;
+    fl[fla(f, 1, p, q)] = dns;
+    fl[fla(f, 2, p, q)] = vo;
+    fl[fla(f, 3, p, q)] = dno;
     if (NBF) NBF[f * NF + tn] = vo;
   }
   __syncwarp();
   for (int it = lane; it < 6 * N; it += 32) {  // F2: along p (first tangential axis)
     const int f = it / N, q = it - f * N;
-    const double* fl = W + Wl::FL + f * 4 * NF + N * q;
+    const double* fl = W + Wl::FL;
     double v[4][N];
 #pragma unroll
     for (int fld = 0; fld < 4; ++fld)
 #pragma unroll
-      for (int p = 0; p < N; ++p) v[fld][p] = fl[fld * NF + p];
-    double* fp = W + Wl::FP + f * 6 * N * Q + q * Q;
+      for (int p = 0; p < N; ++p) v[fld][p] = fl[fla(f, fld, p, q)];
+    double* fp = W + Wl::FP;
 #pragma unroll
     for (int qp = 0; qp < Q; ++qp) {
       double o[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -289,7 +304,7 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
         o[5] = fma(t.B[qp][p], v[3][p], o[5]);  // nbr d/dn
       }
 #pragma unroll
-      for (int fld = 0; fld < 6; ++fld) fp[fld * N * Q + qp] = o[fld];
+      for (int fld = 0; fld < 6; ++fld) fp[fpa(f, fld, q, qp)] = o[fld];
     }
   }
   __syncwarp();
@@ -300,12 +315,12 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
     const int nb = (int)nbv[f];
     const double pen = penv[f];
     const bool act = nb >= 0 || ((bdir >> f) & 1);
-    const double* fp = W + Wl::FP + f * 6 * N * Q + qp;
+    const double* fp = W + Wl::FP;
     double v[6][N];
 #pragma unroll
     for (int fld = 0; fld < 6; ++fld)
 #pragma unroll
-      for (int q = 0; q < N; ++q) v[fld][q] = fp[fld * N * Q + q * Q];
+      for (int q = 0; q < N; ++q) v[fld][q] = fp[fpa(f, fld, q, qp)];
     double A1[N], A2[N], A3[N];
 #pragma unroll
     for (int b = 0; b < N; ++b) A1[b] = A2[b] = A3[b] = 0.0;
@@ -359,26 +374,26 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
         }
       }
     }
-    double* fa = W + Wl::FA + f * 3 * Q * N + qp * N;
+    double* fa = W + Wl::FA;
 #pragma unroll
     for (int b = 0; b < N; ++b) {
-      fa[b] = A1[b];
-      fa[Q * N + b] = A2[b];
-      fa[2 * Q * N + b] = A3[b];
+      fa[faa(f, 0, qp, b)] = A1[b];
+      fa[faa(f, 1, qp, b)] = A2[b];
+      fa[faa(f, 2, qp, b)] = A3[b];
     }
   }
   __syncwarp();
   for (int it = lane; it < 6 * N; it += 32) {  // F4: along p -> face-layer (value / tangential) and normal-test parts
     const int f = it / N, bq = it - f * N;
-    const double* fa = W + Wl::FA + f * 3 * Q * N + bq;
+    const double* fa = W + Wl::FA;
     double a1[Q], a2[Q], a3[Q];
 #pragma unroll
     for (int qp = 0; qp < Q; ++qp) {
-      a1[qp] = fa[qp * N];
-      a2[qp] = fa[Q * N + qp * N];
-      a3[qp] = fa[2 * Q * N + qp * N];
+      a1[qp] = fa[faa(f, 0, qp, bq)];
+      a2[qp] = fa[faa(f, 1, qp, bq)];
+      a3[qp] = fa[faa(f, 2, qp, bq)];
     }
-    double* fo = W + Wl::FON + f * 2 * NF;
+    double* fo = W + Wl::FON;
 #pragma unroll
     for (int bp = 0; bp < N; ++bp) {
       double lo = 0.0, ln = 0.0;
@@ -387,8 +402,8 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
         lo = fma(t.B[qp][bp], a1[qp], fma(t.D[qp][bp], a2[qp], lo));
         ln = fma(t.B[qp][bp], a3[qp], ln);
       }
-      fo[bp + N * bq] = lo;
-      fo[NF + bp + N * bq] = ln;
+      fo[foa(f, 0, bp, bq)] = lo;
+      fo[foa(f, 1, bp, bq)] = ln;
     }
   }
   __syncwarp();
@@ -396,14 +411,13 @@ __device__ __forceinline__ void qp_sip_field(const double* U, double* NBF,
   for (int a = 0; a < 3; ++a) {  // F5: per axis, the two faces' contributions along each normal line
     for (int tn = lane; tn < NF; tn += 32) {
       const int p = tn % N, q = tn / N;
-      const double* f0 = W + Wl::FON + (2 * a) * 2 * NF;
-      const double* f1 = W + Wl::FON + (2 * a + 1) * 2 * NF;
-      const double n0 = f0[NF + tn], n1 = f1[NF + tn];
+      const double* fo = W + Wl::FON;
+      const double n0 = fo[foa(2 * a, 1, p, q)], n1 = fo[foa(2 * a + 1, 1, p, q)];
 #pragma unroll
       for (int l = 0; l < N; ++l) {
         double v = t.dE[0][l] * n0 + t.dE[1][l] * n1;
-        if (l == 0) v += f0[tn];
-        if (l == N - 1) v += f1[tn];
+        if (l == 0) v += fo[foa(2 * a, 0, p, q)];
+        if (l == N - 1) v += fo[foa(2 * a + 1, 0, p, q)];
         OUT[face_node<N>(a, l, p, q)] += v;
       }
     }
