@@ -64,6 +64,15 @@ def coefficients():
     return mom, pmc
 
 
+def profile_json(name):
+    """A committed evidence file under profiles/ (None if absent)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -460,6 +469,14 @@ def run_device(args):
         trbdf2 = trbdf2_step_time(D, dg, torch, stream)
         trbdf2["s_per_step"] = reduce_max(trbdf2["s_per_step"])
         mg = trbdf2_step_time(D, dg, torch, stream, "mg")
+        ref3 = profile_json("cfg3_full_step_parity_r02.json")
+        if ref3:  # the same step through the restated reference driver, 1 host core (tools/full_step_parity.py)
+            trbdf2["reference_cpu"] = {"s_per_step": ref3.get("reference_s_1core"), "cores": 1,
+                                       "krylov_its": ref3.get("its_reference"),
+                                       "parity": {k: ref3.get(k) for k in ("max_its_diff", "rel_l2_u",
+                                                                           "rel_l2_p_mean_free")},
+                                       "source": "profiles/cfg3_full_step_parity_r02.json (measured once, "
+                                                 "not in this run)"}
         trbdf2["mg"] = {"s_per_step": reduce_max(mg["s_per_step"]), "krylov_its": mg["krylov_its"],
                         "gpu_launches": mg["gpu_launches"],
                         "note": "same step with the multigrid-preconditioned pressure CG (opt-in; not the reference's "
@@ -480,6 +497,12 @@ def run_device(args):
                           "20 consecutive steps after one discarded warm-up step"}
         j = cfg5_steps(dg, torch, stream, "jacobi")
         m = cfg5_steps(dg, torch, stream, "mg")
+        m5 = profile_json("cfg5_cpu_model_r02.json")
+        if m5:
+            cfg5["reference_cpu_modelled"] = {"s_per_step": m5.get("modelled_s_per_step"), "cores": 1,
+                                              "method": m5.get("method"),
+                                              "source": "profiles/cfg5_cpu_model_r02.json (MODELLED, "
+                                                        "tools/cpu_step_model.py)"}
         cfg5.update({"s_per_step": reduce_max(j["s_per_step"]), "dt": j["dt"],
                      "krylov_its_first_last": j["krylov_its_first_last"],
                      "mg": {"s_per_step": reduce_max(m["s_per_step"]),
