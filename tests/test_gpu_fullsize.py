@@ -1,9 +1,9 @@
 """Full-size (BASELINE cfg2 / cfg3 / cfg5) checks.
 
-(1) Against the unmodified reference (oracle/_ref) on the BASELINE inputs: a cfg2 and a
-cfg3 momentum + pressure apply (the cfg3 reference apply takes ~2 min with its lazy
-geometry build and ~14 GB of host memory), and a full cfg2 TR-BDF2 step through the
-restated reference driver (~5 min on one core).  (2) Size-independent properties: the
+(1) Against the unmodified reference (oracle/_ref) on the BASELINE inputs: a cfg2, a cfg3
+and a cfg4 (deformed) momentum + pressure apply (the cfg3 / cfg4 reference applies take
+minutes with their lazy geometry builds and ~14 GB of host memory), and a full cfg2
+TR-BDF2 step through the restated reference driver (~4 min on one core).  (2) Size-independent properties: the
 fast axis-aligned kernels agree with the generic device kernels, operator linearity,
 symmetry of the pressure Helmholtz operator, and the host-buffer pipeline returns
 exactly the device result.
@@ -44,6 +44,30 @@ def test_full_size_applies_match_reference(ref, gpu, n_el, ku, seed, Re):
     pmc = 1.0 / (1e6 * G * G * 1e-6)
     D = gpu.DGContext(3, n_el, ku, ku - 1)
     assert D.fast_path_active
+    y, yp = D.zeros(), D.zeros(gpu.SPACE_P)
+    gpu.apply_momentum(D, gpu.MomentumCtx(*coefs, advecting=torch.from_numpy(w).cuda()), torch.from_numpy(x).cuda(), y)
+    gpu.apply_pressure_helmholtz(D, pmc, torch.from_numpy(xp).cuda(), yp)
+    y, yp = y.cpu().numpy(), yp.cpu().numpy()
+    del D
+    want_p = R.pressure(pmc, xp)
+    assert np.linalg.norm(yp - want_p) / np.linalg.norm(want_p) <= TOL
+    want = R.momentum(coefs, w, x)
+    assert np.linalg.norm(y - want) / np.linalg.norm(want) <= TOL
+
+
+def test_full_size_deformed_applies_match_reference(ref, gpu):
+    """BASELINE cfg4 at full size (48^3, interior vertices displaced by U[-0.1h, 0.1h] with
+    the reference's own distort(mesh, 0.1/48, 3); Q4/Q3, per-quadrature-point geometry):
+    one momentum and one pressure apply through the deformed fast kernels against the
+    unmodified reference (its lazy geometry build takes minutes); relative L2 <= 1e-12."""
+    import torch
+    n_el, ku, seed, Re = 48, 4, 3, 100.0
+    R = ref.RefCtx(3, n_el, ku, ku - 1, 0.1 / n_el, 3)
+    f, w, x, xp = _cfg_inputs(ref, R, seed)
+    coefs = (1.0 / (G * 1e-3), 1.0 / (2.0 * Re), 0.5, 0.0)
+    pmc = 1.0 / (1e6 * G * G * 1e-6)
+    D = gpu.DGContext(3, n_el, ku, ku - 1, 0.1 / n_el, 3)
+    assert D.fast_path_active and not D.affine
     y, yp = D.zeros(), D.zeros(gpu.SPACE_P)
     gpu.apply_momentum(D, gpu.MomentumCtx(*coefs, advecting=torch.from_numpy(w).cuda()), torch.from_numpy(x).cuda(), y)
     gpu.apply_pressure_helmholtz(D, pmc, torch.from_numpy(xp).cuda(), yp)
