@@ -173,3 +173,28 @@ def test_trbdf2_step_time_dependent_dirichlet(ref, gpu, dim, n_el, ku, amp):
     assert np.linalg.norm(hu - u1) / np.linalg.norm(u1) <= 1e-9
     hp, p1 = hp - hp.mean(), p1 - p1.mean()
     assert np.linalg.norm(hp - p1) / np.linalg.norm(p1) <= 1e-9
+
+
+# ------------------------------------------------------------- caller alignment
+def test_gmres_accepts_a_misaligned_jacobi_inverse(gpu):
+    """dgb_gmres reads the Jacobi inverse as double2 in its Gram-Schmidt update pass; a
+    caller's view at an odd element offset is copied to an aligned slot first (dgb.h),
+    so the solve is the same as with the aligned vector (no misaligned-address fault)."""
+    import torch
+    D = gpu.DGContext(3, 3, 2, 1)
+    w = torch.from_numpy(gpu.seeded_uniform(1, D.n_u)).cuda()
+    b = torch.from_numpy(gpu.seeded_uniform(2, D.n_u)).cuda()
+    ctx = gpu.MomentumCtx(3.7, 0.01, 0.5, 0.0, advecting=w)
+    d = D.zeros()
+    gpu.momentum_diagonal(D, ctx, d)
+    M = gpu.JacobiPreconditioner(D, d)
+    s = gpu.SolverSettings(rel_tol=1e-10, restart=20)
+    x1 = D.zeros()
+    r1 = gpu.gmres_solve(D, gpu.LinearOperator.momentum(ctx), b, s, M, x1)
+    buf = torch.zeros(D.n_u + 1, dtype=torch.float64, device="cuda")
+    buf[1:] = M.inv
+    M.inv = buf[1:]  # data_ptr 8 bytes past a 16-byte boundary
+    assert M.inv.data_ptr() % 16 == 8
+    x2 = D.zeros()
+    r2 = gpu.gmres_solve(D, gpu.LinearOperator.momentum(ctx), b, s, M, x2)
+    assert r1.iterations == r2.iterations and torch.equal(x1, x2)
