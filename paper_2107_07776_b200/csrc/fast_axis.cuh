@@ -491,15 +491,23 @@ struct SipAxisCfg {
   // sync with __syncwarp); chosen so the N^2-item line stages fill 32 lanes
   static constexpr int CPW = KP == 1 ? 8 : (KP == 2 ? 3 : 2);
   static constexpr bool WPG = C % CPW == 0 && T == 32 * (C / CPW);
-  static constexpr int O_U = 0, O_SX = P::CT, O_SY = 2 * P::CT, O_SZ = 3 * P::CT, O_UX = 4 * P::CT;
-  static constexpr int O_INFO = 5 * P::CT;
+#ifndef DGB_SIP2_CTPAD
+#define DGB_SIP2_CTPAD 0
+#endif
+  static constexpr int CTS = P::CT + (KP == 2 ? DGB_SIP2_CTPAD : 0);  // array stride (KP = 2: padded)
+  static constexpr int O_U = 0, O_SX = CTS, O_SY = 2 * CTS, O_SZ = 3 * CTS, O_UX = 4 * CTS;
+  static constexpr int O_INFO = 5 * CTS;
   // KP = 1: the per-cell stride is 10 mod 16 doubles and the warp's line items run
   // cell-fastest (CF): the 8 cells of a warp then sit on distinct even bank pairs and the
   // second line of each half-warp on the odd ones — conflict-free line stages (bank
   // simulation: 178 -> 80 wavefronts per warp-group vs an ideal of 80; ncu had 45 % of
   // the kernel's shared wavefronts as conflicts)
   static constexpr bool CF = KP == 1 && WPG;
-  static constexpr int PER = CF ? O_INFO + kInfoDoubles + 1 : (O_INFO + kInfoDoubles) | 1;
+#ifndef DGB_SIP2_PERPAD  // KP = 2: cell-stride pad (tools/bank_sim_sip2.py: 1131 -> 1026 modelled wavefronts)
+#define DGB_SIP2_PERPAD 6
+#endif
+  static constexpr int PER = CF ? O_INFO + kInfoDoubles + 1
+                                : ((O_INFO + kInfoDoubles) | 1) + (KP == 2 ? DGB_SIP2_PERPAD : 0);
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
   // the cell-fastest (CF) layout is bank-conflict-free only for a cell stride of 10 mod 16
   // doubles (tools/bank_sim_sip1.py); a new CellInfo field must keep that
