@@ -789,7 +789,10 @@ template <> struct MomAxisTune<3, 2> { static constexpr int C = 3, T = 96; stati
 // advective flux with w.n f on every boundary face; the caller passes the negated
 // viscous / advective coefficients.  acc: y += result.
 template <int K, int CC, int TH, int MODE, bool UNI, bool RHS = false>
-__global__ void __launch_bounds__(TH) k_momentum_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff, MomCoef co,
+#ifndef DGB_MOM_MINB  // minimum CTAs per SM promised to ptxas (0: no promise)
+#define DGB_MOM_MINB 2
+#endif
+__global__ void __launch_bounds__(TH, DGB_MOM_MINB) k_momentum_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff, MomCoef co,
                                                       const double* __restrict__ x, const double* __restrict__ w,
                                                       double* __restrict__ y, int acc) {
   if (m.skip && *m.skip) return;
