@@ -56,9 +56,20 @@ int dgb_ctx_create_cartesian(int dim, int n_el, double distort_amp, unsigned dis
  * opposite sides with identical corner order (Cartesian topology). */
 int dgb_ctx_create_mesh(int dim, int nverts, const double* verts, int ncells, const int* cell_vertices,
                         const int* boundary_ids, int ku, int kp, int device, dgb_ctx** out);
+/* Mesh with hanging faces (1-irregular refinement: Mesh::refine_and_coarsen, mesh.hpp:125-128;
+ * subface records mesh.cpp:344-375).  The arrays are the active cells as above plus, for
+ * every hanging subface (FaceInfo with hanging == true, mesh.hpp:46-57; its cell_in is the
+ * fine cell): hang_faces [n_hang][4] = fine cell, fine face, coarse cell, coarse face (active
+ * indices), hang_emb [n_hang][dim*dim] = emb_out.origin[dim] then emb_out.tangent[t][dim],
+ * t < dim-1 (the subface in the coarse cell's reference coordinates).  Conforming faces
+ * must pair as in dgb_ctx_create_mesh.  Such meshes run the generic kernels plus the
+ * subface kernels (hang.cu); the fast paths and the pressure multigrid are off. */
+int dgb_ctx_create_mesh_hanging(int dim, int nverts, const double* verts, int ncells, const int* cell_vertices,
+                                const int* boundary_ids, int n_hang, const int* hang_faces, const double* hang_emb,
+                                int ku, int kp, int device, dgb_ctx** out);
 void dgb_ctx_destroy(dgb_ctx* ctx);
 /* info[16]: ncells, n_u, n_p, n_interior_faces, n_boundary_faces, ku, kp, dim, affine,
- *           nqf_bdry (points per boundary face at rule ku+2), device, 0... */
+ *           nqf_bdry (points per boundary face at rule ku+2), device, n_hanging_subfaces, 0... */
 int dgb_ctx_info(dgb_ctx* ctx, long long* info);
 /* Use an external cudaStream_t (NULL = the legacy default stream); a new context uses its own stream. */
 int dgb_set_stream(dgb_ctx* ctx, void* cuda_stream);

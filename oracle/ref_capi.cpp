@@ -66,6 +66,7 @@ struct Base {
                            const double* p_n, double* u_np1, double* p_np1, int* its) = 0;
   virtual void faces(int* iface, double* imeas, int* bface, double* bmeas) = 0;
   virtual void cell_vertices(double* xv) = 0;
+  virtual void mesh_arrays(double* xv, int* cv, int* bid, double* emb_out) = 0;
   virtual void bface_points(int rule, double* xq) = 0;
   virtual void interpolate_nodes(int space, double* xn) = 0;
   virtual void interpolate_fn(ref_bc_fn fn, void* user, double* u, int nthreads) = 0;
@@ -333,6 +334,29 @@ struct Ctx : Base {
 
   // interior: [cell_in, face_in, cell_out, face_out, hanging] per face (active indices)
   // boundary: [cell_in, face_in, boundary_id]
+  // The active mesh as raw arrays (what a reference-side binding hands the device, see
+  // INTEGRATION.md): every vertex [nverts][dim], active cells' vertex ids [n_active][2^dim]
+  // and boundary ids [n_active][2dim] in active order, and for every interior face
+  // (mesh.faces().interior order) its emb_out (mesh.hpp:28-36): origin[dim], then
+  // tangent[t][dim] for t < dim-1  -> [n_interior][dim*dim].
+  void mesh_arrays(double* xv, int* cv, int* bid, double* emb_out) override {
+    for (size_t v = 0; v < mesh.vertices.size(); ++v)
+      for (int d = 0; d < dim; ++d) xv[v * dim + d] = mesh.vertices[v][d];
+    for (int a = 0; a < mesh.n_active(); ++a) {
+      const auto& c = mesh.cells[mesh.active_cells()[a]];
+      for (int v = 0; v < Mesh<dim>::n_vertices_per_cell; ++v) cv[(size_t)a * Mesh<dim>::n_vertices_per_cell + v] = c.v[v];
+      for (int f = 0; f < Mesh<dim>::n_faces_per_cell; ++f)
+        bid[(size_t)a * Mesh<dim>::n_faces_per_cell + f] = c.boundary_id[f];
+    }
+    const auto& fl = mesh.faces();
+    for (size_t f = 0; f < fl.interior.size(); ++f) {
+      const auto& e = fl.interior[f].emb_out;
+      double* o = emb_out + f * dim * dim;
+      for (int d = 0; d < dim; ++d) o[d] = e.origin[d];
+      for (int t = 0; t < dim - 1; ++t)
+        for (int d = 0; d < dim; ++d) o[dim + t * dim + d] = e.tangent[t][d];
+    }
+  }
   void faces(int* iface, double* imeas, int* bface, double* bmeas) override {
     const auto& fl = mesh.faces();
     for (size_t f = 0; f < fl.interior.size(); ++f) {
@@ -467,6 +491,17 @@ Base* make_cartesian(int n_el, double amp, unsigned seed, int ku, int kp, int re
   Mesh<dim> m = generate_cartesian<dim>(n_el, lo, hi);
   if (amp != 0.0) distort(m, amp, seed);
   if (refine_first) m.refine_and_coarsen({0}, {});
+  return new Ctx<dim>(std::move(m), ku, kp);
+}
+// generate_cartesian (+ distort), then one Mesh::refine_and_coarsen(refine_set, {})
+// (mesh.hpp:125-128; the reference grows the set for 1-irregularity): hanging faces
+template <int dim>
+Base* make_refined(int n_el, double amp, unsigned seed, int ku, int kp, int n_ref, const int* refine) {
+  std::array<double, dim> lo{}, hi{};
+  hi.fill(1.0);
+  Mesh<dim> m = generate_cartesian<dim>(n_el, lo, hi);
+  if (amp != 0.0) distort(m, amp, seed);
+  m.refine_and_coarsen(std::vector<int>(refine, refine + n_ref), {});
   return new Ctx<dim>(std::move(m), ku, kp);
 }
 
@@ -638,6 +673,19 @@ void* ref_create_cartesian(int dim, int n_el, double amp, unsigned seed, int ku,
     g_err = e.what();
   }
   return nullptr;
+}
+void* ref_create_refined(int dim, int n_el, double amp, unsigned seed, int ku, int kp, int n_ref,
+                         const int* refine) {
+  try {
+    if (dim == 2) return make_refined<2>(n_el, amp, seed, ku, kp, n_ref, refine);
+    if (dim == 3) return make_refined<3>(n_el, amp, seed, ku, kp, n_ref, refine);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+  }
+  return nullptr;
+}
+void ref_mesh_arrays(void* h, double* xv, int* cv, int* bid, double* emb_out) {
+  static_cast<Base*>(h)->mesh_arrays(xv, cv, bid, emb_out);
 }
 void* ref_create_from_text(const char* text, int ku, int kp) {
   try {

@@ -94,6 +94,8 @@ def lib() -> C.CDLL:
                                            C.POINTER(C.c_void_p)]
     L.dgb_ctx_create_mesh.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _ip, _ip, C.c_int, C.c_int, C.c_int,
                                       C.POINTER(C.c_void_p)]
+    L.dgb_ctx_create_mesh_hanging.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _ip, _ip, C.c_int, _ip, _dp,
+                                              C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
     L.dgb_ctx_destroy.argtypes = [C.c_void_p]
     L.dgb_ctx_destroy.restype = None
     L.dgb_ctx_info.argtypes = [C.c_void_p, _llp]
@@ -228,19 +230,28 @@ class DGContext:
                                               C.byref(h)))
         else:
             import numpy as np
-            verts, cells, bids = mesh_arrays
+            verts, cells, bids = mesh_arrays[:3]
             verts = np.ascontiguousarray(verts, dtype=np.float64)
             cells = np.ascontiguousarray(cells, dtype=np.int32)
             bids = np.ascontiguousarray(bids, dtype=np.int32)
-            _check(L.dgb_ctx_create_mesh(dim, verts.shape[0], _np_ptr(verts), cells.shape[0],
-                                         cells.ctypes.data_as(_ip), bids.ctypes.data_as(_ip), ku, kp, device,
-                                         C.byref(h)))
+            if len(mesh_arrays) > 3:  # hanging subfaces: (fine, f, coarse, fN) records + emb_out
+                hf = np.ascontiguousarray(mesh_arrays[3], dtype=np.int32).reshape(-1, 4)
+                he = np.ascontiguousarray(mesh_arrays[4], dtype=np.float64).reshape(len(hf), dim * dim)
+                _check(L.dgb_ctx_create_mesh_hanging(dim, verts.shape[0], _np_ptr(verts), cells.shape[0],
+                                                     cells.ctypes.data_as(_ip), bids.ctypes.data_as(_ip), len(hf),
+                                                     hf.ctypes.data_as(_ip), _np_ptr(he), ku, kp, device,
+                                                     C.byref(h)))
+            else:
+                _check(L.dgb_ctx_create_mesh(dim, verts.shape[0], _np_ptr(verts), cells.shape[0],
+                                             cells.ctypes.data_as(_ip), bids.ctypes.data_as(_ip), ku, kp, device,
+                                             C.byref(h)))
         self._h = h
         self.device = device
         info = (C.c_longlong * 16)()
         _check(L.dgb_ctx_info(h, info))
         (self.ncells, self.n_u, self.n_p, self.n_interior, self.n_boundary, self.ku, self.kp, self.dim,
          affine, self.nqf_bdry) = [int(v) for v in info[:10]]
+        self.n_hanging = int(info[11])
         self.affine = bool(affine)
         # run on torch's current stream so torch ops and our kernels are ordered
         with torch.cuda.device(device):

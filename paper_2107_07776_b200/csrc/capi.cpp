@@ -75,6 +75,19 @@ int dgb_ctx_create_mesh(int dim, int nverts, const double* verts, int ncells, co
   return finish_create(std::move(m), ku, kp, device, err, out);
 }
 
+int dgb_ctx_create_mesh_hanging(int dim, int nverts, const double* verts, int ncells, const int* cell_vertices,
+                                const int* boundary_ids, int n_hang, const int* hang_faces, const double* hang_emb,
+                                int ku, int kp, int device, dgb_ctx** out) {
+  NEED(out && verts && cell_vertices, "null argument");
+  NEED(dim == 2 || dim == 3, "dim must be 2 or 3");
+  NEED(nverts > 0 && ncells > 0, "empty mesh");
+  NEED(n_hang >= 0 && (n_hang == 0 || (hang_faces && hang_emb)), "hanging faces: bad record arrays");
+  std::string err;
+  dgb::HostMesh m = dgb::make_from_arrays(dim, nverts, verts, ncells, cell_vertices, boundary_ids, err, n_hang,
+                                          hang_faces, hang_emb);
+  return finish_create(std::move(m), ku, kp, device, err, out);
+}
+
 void dgb_ctx_destroy(dgb_ctx* h) {
   DevGuard guard_(h);
   delete h;
@@ -96,6 +109,7 @@ int dgb_ctx_info(dgb_ctx* h, long long* info) {
   info[8] = c.mesh.affine ? 1 : 0;
   info[9] = c.nqf(c.ku + 2);
   info[10] = c.device;
+  info[11] = c.mesh.n_hang();
   return DGB_OK;
 }
 
@@ -619,7 +633,7 @@ extern "C" int dgb_host_tables(int n, int q, double* B, double* D, double* dE, d
 // generic kernels (0).  Both are parity-tested against the reference.
 extern "C" int dgb_set_fast_path(dgb_ctx* h, int enable) {
   NEED(h, "null ctx");
-  h->c.use_fast = enable != 0;
+  h->c.use_fast = enable != 0 && !h->c.hang_;  // hanging meshes run the generic kernels + hang.cu
   return DGB_OK;
 }
 // 1: axis-aligned fast kernels (fast_axis.cuh), 2: deformed 3D fast kernels (fast_deformed.cuh), 0: generic

@@ -72,6 +72,7 @@ Context::~Context() {
   if (ev0) cudaEventDestroy(ev0);
   if (ev1) cudaEventDestroy(ev1);
   if (own_stream) cudaStreamDestroy(own_stream);
+  hang_release(hang_);
 }
 
 int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
@@ -119,6 +120,7 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
       const int nb = mesh.nbr[s];
       const double fm = mesh.face_measure[s];
       pen[s] = nb >= 0 ? 0.5 * (fm / mesh.cell_measure[c] + fm / mesh.cell_measure[nb]) : fm / mesh.cell_measure[c];
+      if (mesh.hanging(c, f)) pen[s] = 0.0;  // zero-weight slot; hang.cu carries the subface penalty
     }
   for (size_t b = 0; b < n_bface(); ++b) bslot[(size_t)mesh.bface[3 * b] * nf + mesh.bface[3 * b + 1]] = (int)b;
   int* d_nbr = (int*)dalloc(nslot * sizeof(int));
@@ -293,6 +295,17 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
       }
     }
   }
+  // hanging faces: the generic kernels (zero-weight slots) + the subface supplement
+  if (mesh.n_hang() > 0) {
+    use_fast = false;
+    dc.axis = dc.axis2 = false;
+    dc.ug = UniformGrid();
+    hang_ = hang_setup(mesh, ku, kp, e);
+    if (!hang_) {
+      if (e.empty()) e = "hanging faces: setup failed";
+      return DGB_E_CUDA;
+    }
+  }
   // Dirichlet table (rule ku+2), zero until set
   gtab_h_.assign(n_bface() * nqf(ku + 2) * dim, 0.0);
   d_gtab_ = (double*)dalloc(gtab_h_.size() * sizeof(double));
@@ -346,6 +359,10 @@ int Context::momentum(const double* coefs, const double* w, const double* x, dou
     cudaGetLastError();
   }
   CK(opu->momentum(dc, co, w, x, y));
+  if (hang_) {
+    launches += 2;
+    CK(hang_momentum(dc.stream, hang_, co, w, x, y));
+  }
   return DGB_OK;
 }
 int Context::momentum_diag(const double* coefs, const double* w, double* d) {
@@ -362,6 +379,10 @@ int Context::momentum_diag(const double* coefs, const double* w, double* d) {
     cudaGetLastError();
   }
   CK(opu->momentum_diag(dc, co, w, d));
+  if (hang_) {
+    launches += 2;
+    CK(hang_momentum_diag(dc.stream, hang_, co, w, d));
+  }
   return DGB_OK;
 }
 int Context::sip(double mc, int dir, const double* x, double* y) {
@@ -376,6 +397,10 @@ int Context::sip(double mc, int dir, const double* x, double* y) {
     cudaGetLastError();
   }
   CK(opp->sip(dc, mc, dir, x, y));
+  if (hang_) {
+    launches += 2;
+    CK(hang_sip(dc.stream, hang_, x, y));
+  }
   return DGB_OK;
 }
 // Host-buffer applies.  On a uniform lexicographic grid with the fast kernels the cells
@@ -470,6 +495,10 @@ int Context::sip_diag(double mc, int dir, double* d) {
     cudaGetLastError();
   }
   CK(opp->sip_diag(dc, mc, dir, d));
+  if (hang_) {
+    launches += 2;
+    CK(hang_sip_diag(dc.stream, hang_, d));
+  }
   return DGB_OK;
 }
 int Context::mass(int space, const double* x, double* y) {
@@ -554,6 +583,10 @@ int Context::rhs(const dgb_rhs_desc& ds, double* y) {
   }
   ++launches;
   CK(opu->rhs(dc, ra, y));
+  if (hang_) {
+    launches += 2;
+    CK(hang_rhs(dc.stream, hang_, ra, y));
+  }
   return DGB_OK;
 }
 int Context::divergence(const double* u, double* y) {
@@ -566,6 +599,10 @@ int Context::divergence(const double* u, double* y) {
     }
   }
   CK(opu->divergence(dc, u, y));
+  if (hang_) {
+    launches += 2;
+    CK(hang_divergence(dc.stream, hang_, u, y));
+  }
   return DGB_OK;
 }
 int Context::pressure_rhs(double inv_adt, const double* u, double mc, const double* p_old, double* y) {

@@ -13,6 +13,7 @@
 #include "dispatch.hpp"
 #include "blas.cuh"
 #include "host_setup.hpp"
+#include "hang.hpp"
 
 namespace dgb {
 
@@ -36,6 +37,7 @@ class Context {
   int bctype_h[64] = {};
   long long launches = 0;
   bool use_fast = true;  // route axis-aligned 3D applies to fast_axis.cuh
+  HangState* hang_ = nullptr;  // hanging-subface supplement (refined meshes; hang.cu), else null
 
   ~Context();
   int init(HostMesh&& m, int ku, int kp, int device, std::string& err);

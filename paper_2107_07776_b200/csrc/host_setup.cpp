@@ -277,7 +277,10 @@ bool finalize_mesh(HostMesh& m, std::string& err) {
   for (int c = 0; c < m.ncells; ++c)
     for (int f = 0; f < nf; ++f) {
       const int nb = m.nbr[static_cast<size_t>(c) * nf + f];
-      if (nb < 0) {
+      if (m.hanging(c, f)) {  // recorded once per subface, from the fine side (mesh.cpp:344-375)
+        const int h = m.hface[static_cast<size_t>(c) * nf + f];
+        if (h >= 0) m.iface.insert(m.iface.end(), {c, f, m.hrec[4 * h + 2], m.hrec[4 * h + 3]});
+      } else if (nb < 0) {
         m.bface.insert(m.bface.end(), {c, f, -1 - nb});
       } else if (c < nb) {
         m.iface.insert(m.iface.end(), {c, f, nb, f ^ 1});
@@ -355,7 +358,8 @@ HostMesh make_cartesian(int dim, int n_el, double amp, unsigned seed, std::strin
 }
 
 HostMesh make_from_arrays(int dim, int nverts, const double* verts, int ncells, const int* cell_v,
-                          const int* boundary_ids, std::string& err) {
+                          const int* boundary_ids, std::string& err, int n_hang, const int* hang_rec,
+                          const double* hang_emb) {
   HostMesh m;
   m.dim = dim;
   m.ncells = ncells;
@@ -363,12 +367,46 @@ HostMesh make_from_arrays(int dim, int nverts, const double* verts, int ncells, 
   m.vertices.assign(verts, verts + static_cast<size_t>(nverts) * dim);
   m.cell_v.assign(cell_v, cell_v + static_cast<size_t>(ncells) * nv);
   m.nbr.assign(static_cast<size_t>(ncells) * nf, 0);
+  // hanging subfaces (mesh.cpp:344-375): both sides' slots are taken out of the pairing
+  if (n_hang > 0) {
+    if (!hang_rec || !hang_emb) {
+      err = "hanging faces: null record / embedding array";
+      m.ncells = 0;
+      return m;
+    }
+    m.hface.assign(static_cast<size_t>(ncells) * nf, -1);
+    m.hrec.assign(hang_rec, hang_rec + static_cast<size_t>(n_hang) * 4);
+    m.hemb.assign(hang_emb, hang_emb + static_cast<size_t>(n_hang) * dim * dim);
+    for (int h = 0; h < n_hang; ++h) {
+      const int K = hang_rec[4 * h], f = hang_rec[4 * h + 1], N = hang_rec[4 * h + 2], fN = hang_rec[4 * h + 3];
+      if (K < 0 || K >= ncells || N < 0 || N >= ncells || K == N || f < 0 || f >= nf || fN < 0 || fN >= nf ||
+          (boundary_ids && (boundary_ids[static_cast<size_t>(K) * nf + f] >= 0 ||
+                            boundary_ids[static_cast<size_t>(N) * nf + fN] >= 0))) {
+        err = "hanging face record " + std::to_string(h) + " is not an interior fine/coarse face pair";
+        m.ncells = 0;
+        return m;
+      }
+      int& sK = m.hface[static_cast<size_t>(K) * nf + f];
+      int& sN = m.hface[static_cast<size_t>(N) * nf + fN];
+      if (sK != -1 || sN >= 0) {
+        err = "hanging face record " + std::to_string(h) + " reuses a face slot";
+        m.ncells = 0;
+        return m;
+      }
+      sK = h;
+      sN = -2;
+    }
+  }
   std::map<std::array<int, 4>, std::pair<int, int>> open;
   for (int c = 0; c < ncells; ++c)
     for (int f = 0; f < nf; ++f) {
       const int bid = boundary_ids ? boundary_ids[static_cast<size_t>(c) * nf + f] : -1;
       if (bid >= 0) {
         m.nbr[static_cast<size_t>(c) * nf + f] = -1 - bid;
+        continue;
+      }
+      if (m.hanging(c, f)) {
+        m.nbr[static_cast<size_t>(c) * nf + f] = c;  // zero-weight self face (see HostMesh::hrec)
         continue;
       }
       std::array<int, 4> key{-1, -1, -1, -1};
@@ -424,6 +462,29 @@ static void face_ref_point(int dim, int f, int side_override, const Rule1D& r, i
   }
 }
 
+void embed_point(int dim, const double* emb, const Rule1D& r, int t, double* ref) {
+  double xi[2] = {0.0, 0.0};
+  int rem = t;
+  for (int k = 0; k < dim - 1; ++k) {
+    xi[k] = r.x[rem % r.x.size()];
+    rem /= static_cast<int>(r.x.size());
+  }
+  for (int d = 0; d < dim; ++d) {
+    double v = emb[d];
+    for (int k = 0; k < dim - 1; ++k) v += xi[k] * emb[dim + k * dim + d];
+    ref[d] = v;
+  }
+}
+
+void canonical_embedding(int dim, int f, double* emb) {
+  const int a = f / 2;
+  for (int i = 0; i < dim * dim; ++i) emb[i] = 0.0;
+  emb[a] = f % 2;
+  int k = 0;
+  for (int d = 0; d < dim; ++d)
+    if (d != a) emb[dim + (k++) * dim + d] = 1.0;
+}
+
 static double face_weight(int dim, const Rule1D& r, int t) {
   double w = 1.0;
   int rem = t;
@@ -434,7 +495,7 @@ static double face_weight(int dim, const Rule1D& r, int t) {
   return w;
 }
 
-static void face_frame(int dim, int f, const double* J, const double* Jinv, double* n, double& ds) {
+void face_frame(int dim, int f, const double* J, const double* Jinv, double* n, double& ds) {
   const int a = f / 2;
   const double sgn = (f % 2) == 1 ? 1.0 : -1.0;
   double tau[2][3];
@@ -505,7 +566,7 @@ void build_qp_geometry(const HostMesh& m, int Q, QpGeometry& g) {
           invert(dim, J2, o + dim * dim);
         }
         for (int d = 0; d < dim; ++d) o[2 * dim * dim + d] = n[d];
-        o[2 * dim * dim + dim] = ds * face_weight(dim, r, t);
+        o[2 * dim * dim + dim] = m.hanging(c, f) ? 0.0 : ds * face_weight(dim, r, t);
       }
     }
   }
@@ -524,7 +585,7 @@ void build_affine_geometry(const HostMesh& m, std::vector<double>& g) {
       double* of = o + dim * dim + 1 + f * (dim + 1);
       double ds;
       face_frame(dim, f, J, o, of, ds);
-      of[dim] = ds;
+      of[dim] = m.hanging(c, f) ? 0.0 : ds;
     }
   }
 }

@@ -56,6 +56,18 @@ struct HostMesh {
   std::vector<int> iface;  // n_interior x 4: cell_in, face_in, cell_out, face_out
   std::vector<int> bface;  // n_boundary x 3: cell, face, boundary_id
   bool affine = true;      // every cell a parallelepiped (constant Jacobian)
+  // Hanging subfaces of a 1-irregular refined mesh (mesh.cpp:344-375), one record per
+  // fine face: fine cell, fine face, coarse cell, coarse face, and the subface
+  // embedding into the coarse cell's reference cell (FaceInfo::emb_out, mesh.hpp:28-36:
+  // origin[dim], tangent[t][dim] for t < dim-1).  The element-centric kernels see a
+  // hanging (cell, face) slot as an interior face to the cell itself with zero surface
+  // weight (nbr = cell, ds = 0: every face integrand carries w_ds, so it contributes
+  // nothing); hang.cu adds the two-sided subface terms.
+  std::vector<int> hrec;     // n_hang x 4
+  std::vector<double> hemb;  // n_hang x dim*dim
+  std::vector<int> hface;    // ncells x 2dim: -1 conforming / boundary, h >= 0 fine side of record h, -2 coarse side
+  int n_hang() const { return static_cast<int>(hrec.size() / 4); }
+  bool hanging(int c, int f) const { return !hface.empty() && hface[static_cast<size_t>(c) * nf_cell() + f] != -1; }
 
   int nv_cell() const { return 1 << dim; }
   int nf_cell() const { return 2 * dim; }
@@ -66,7 +78,8 @@ struct HostMesh {
 HostMesh make_cartesian(int dim, int n_el, double amp, unsigned seed, std::string& err);
 /// From raw arrays (vertices, cell->vertex, boundary ids per cell face (-1 = none)).
 HostMesh make_from_arrays(int dim, int nverts, const double* verts, int ncells, const int* cell_v,
-                          const int* boundary_ids, std::string& err);
+                          const int* boundary_ids, std::string& err, int n_hang = 0, const int* hang_rec = nullptr,
+                          const double* hang_emb = nullptr);
 /// Recompute measures, diameters, face lists, affinity. Fills err on failure.
 bool finalize_mesh(HostMesh& m, std::string& err);
 
@@ -87,6 +100,14 @@ struct QpGeometry {
   std::vector<double> cell, face;
 };
 int cell_geo_stride(int dim);
+/// Reference point of face-quadrature point t (first face parameter fastest) under an
+/// embedding {origin[dim], tangent[dim-1][dim]} (FaceEmbedding, mesh.hpp:28-36).
+void embed_point(int dim, const double* emb, const Rule1D& r, int t, double* ref);
+/// The canonical embedding of local face f (mesh.cpp:240-248).
+void canonical_embedding(int dim, int f, double* emb);
+/// Surface element of the canonical face-f parameterisation and the unit normal out of
+/// the cell (Nanson, space.cpp:133-142) from J and Jinv at a face point.
+void face_frame(int dim, int f, const double* J, const double* Jinv, double* n, double& ds);
 int face_geo_stride(int dim);
 void build_qp_geometry(const HostMesh& m, int Q, QpGeometry& g);
 // fn(c0, c1) over [0, n) split into contiguous chunks, one per host thread (setup loops)

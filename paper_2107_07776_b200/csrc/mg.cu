@@ -371,7 +371,7 @@ static int cartesian_topology(const HostMesh& m, double& side) {
 }
 
 bool Context::mg_supported() const {
-  if (dim != 3 || kp < 1 || kp > 3) return false;
+  if (dim != 3 || kp < 1 || kp > 3 || hang_) return false;
   if (mg_topo_n_ < 0) {
     double side = 0.0;
     mg_topo_n_ = cartesian_topology(mesh, side);

@@ -33,6 +33,9 @@ def lib():
         L.ref_backend.restype = C.c_char_p
         L.ref_create_cartesian.restype = C.c_void_p
         L.ref_create_cartesian.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint, C.c_int, C.c_int, C.c_int]
+        L.ref_create_refined.restype = C.c_void_p
+        L.ref_create_refined.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint, C.c_int, C.c_int, C.c_int, _ip]
+        L.ref_mesh_arrays.argtypes = [C.c_void_p, _dp, _ip, _ip, _dp]
         L.ref_create_from_text.restype = C.c_void_p
         L.ref_create_from_text.argtypes = [C.c_char_p, C.c_int, C.c_int]
         L.ref_create_from_arrays.restype = C.c_void_p
@@ -167,6 +170,26 @@ class RefCtx:
         (self.ncells, self.n_u, self.n_p, self.n_interior, self.n_boundary, self.ku, self.kp, self.dim,
          self.nverts, self.n_hanging) = [int(v) for v in info]
         self._keep = []
+
+    @classmethod
+    def refined(cls, dim: int, n_el: int, ku: int, kp: int, refine, amp: float = 0.0, seed: int = 0):
+        """generate_cartesian (+ distort) then Mesh::refine_and_coarsen(refine, {}): hanging faces."""
+        r = np.ascontiguousarray(refine, dtype=np.int32)
+        h = lib().ref_create_refined(dim, n_el, amp, seed, ku, kp, len(r), r.ctypes.data_as(_ip))
+        if not h:
+            raise RuntimeError(lib().ref_last_error().decode())
+        return cls(handle=h)
+
+    def mesh_arrays(self):
+        """(vertices [nv][dim], active cell vertices [n][2^dim], boundary ids [n][2dim],
+        interior faces [ni][5] (cell_in, face_in, cell_out, face_out, hanging), emb_out [ni][dim*dim])."""
+        xv = np.zeros((self.nverts, self.dim))
+        cv = np.zeros((self.ncells, 1 << self.dim), dtype=np.int32)
+        bid = np.zeros((self.ncells, 2 * self.dim), dtype=np.int32)
+        emb = np.zeros((self.n_interior, self.dim * self.dim))
+        lib().ref_mesh_arrays(self.h, P(xv), cv.ctypes.data_as(_ip), bid.ctypes.data_as(_ip), P(emb))
+        it, _, _, _ = self.faces()
+        return xv, cv, bid, it, emb
 
     @classmethod
     def slab(cls, n_el: int, z0: int, nz: int, ku: int, kp: int):
