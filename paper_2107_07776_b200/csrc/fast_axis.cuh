@@ -842,6 +842,20 @@ __global__ void __launch_bounds__(TH, DGB_MOM_MINB) k_momentum_axis(MeshArgs m, 
 #ifndef DGB_WPC_S0
 #define DGB_WPC_S0 1
 #endif
+#ifndef DGB_MOM_PF
+#define DGB_MOM_PF 296  // 2 CTAs x 148 SMs ahead: cfg3 1.759 -> 1.749 ms (148 / 592: the same)
+#endif
+  if constexpr (DGB_MOM_PF > 0) {
+    // pull the x / w blocks of the CTA that will run DGB_MOM_PF blocks later into L2, so
+    // that its staging waits on L2 instead of HBM
+    const long long pc0 = (long long)c0 + (long long)DGB_MOM_PF * C;
+    constexpr int LINES = C * 3 * NB * 8 / 128;
+    const long long lim = (m.cell1 < 0 ? m.ncells : m.cell1);
+    if (pc0 + C <= lim && tid < 2 * LINES) {
+      const double* src = (tid < LINES ? x : w) + pc0 * 3 * NB + (size_t)(tid % LINES) * 16;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(src));
+    }
+  }
   if constexpr (WPC && DGB_WPC_S0) {
     // one warp stages its own cell: the six neighbours once per warp, element / item
     // indices from the lane and compile-time loop counters (the CTA-wide loops of the
