@@ -265,7 +265,8 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
         cudaMemcpy(dfn, fn.data(), fn.size() * sizeof(double), cudaMemcpyHostToDevice);
         dc.qcm[Q] = dcm;
         dc.qfn[Q] = dfn;
-        if (Q == ku + 2) {  // advection records of the deformed momentum kernel (SoA per cell)
+        if (Q == ku + 2 || Q == ku + 1) {  // advection records of the deformed momentum kernel (rule k+2) and
+                                            // the records of the mixed velocity-pressure forms (rule k+1)
           const int nq = Q * Q * Q, nqf = Q * Q;
           std::vector<double> ga((size_t)mesh.ncells * 9 * nq), gw((size_t)mesh.ncells * 18 * nqf);
           parallel_cells(mesh.ncells, [&](int cl0, int cl1) {
@@ -575,7 +576,7 @@ int Context::rhs(const dgb_rhs_desc& ds, double* y) {
   if (use_fast && !dc.affine && dim == 3) {
     const cudaError_t e = fast_rhs3_qp(dc, ra, y);
     if (e == cudaSuccess) {
-      launches += 2 + ra.na;
+      launches += 1 + ra.na + (ra.np > 0) + (ra.dvisc != 0.0 || ra.dadv != 0.0);
       return DGB_OK;
     }
     if (e != cudaErrorNotSupported) return cuda_fail(e, "momentum_rhs");
@@ -591,12 +592,13 @@ int Context::rhs(const dgb_rhs_desc& ds, double* y) {
 }
 int Context::divergence(const double* u, double* y) {
   ++launches;
-  if (use_fast && dc.axis) {
-    const cudaError_t e = fast_divergence3(dc, u, y);
+  if (use_fast && (dc.axis || (!dc.affine && dim == 3))) {
+    const cudaError_t e = dc.axis ? fast_divergence3(dc, u, y) : fast_divergence3_qp(dc, u, y);
     if (e != cudaErrorNotSupported) {
       CK(e);
       return DGB_OK;
     }
+    cudaGetLastError();
   }
   CK(opu->divergence(dc, u, y));
   if (hang_) {

@@ -129,6 +129,8 @@ cudaError_t fast_momentum3_qp(const DevCtx& c, MomCoef co, const double* w, cons
 cudaError_t fast_momentum_diag3(const DevCtx& c, MomCoef co, const double* w, double* y);
 cudaError_t fast_momentum_diag3_qp(const DevCtx& c, MomCoef co, const double* w, double* y);
 cudaError_t fast_divergence3(const DevCtx& c, const double* u, double* y);
+// deformed 3D meshes: divergence functional and (inside fast_rhs3_qp) the weak pressure gradient
+cudaError_t fast_divergence3_qp(const DevCtx& c, const double* u, double* y);
 cudaError_t fast_sip_diag3(const DevCtx& c, double mc, int dir, double* y);
 cudaError_t fast_sip_diag3_qp(const DevCtx& c, double mc, int dir, double* y);
 struct CgState;

@@ -974,6 +974,496 @@ __global__ void __launch_bounds__(MomQpCfg<K>::T) k_momentum_qp(MeshArgs m, cons
   }
 }
 
+
+// ===========================================================================
+// Weak pressure gradient of momentum_rhs and the divergence functional on deformed
+// hexahedra (forms.cpp:850-855 / :895-912 / :940-948 and :1118-1197): the two mixed
+// velocity-pressure forms, transposes of each other, both at the velocity rule k+1:
+//   G(p)_{d,i} = (p, d_d phi_i) - <{p} n_d, phi_i>      (velocity tests, component d)
+//   B(u)_i     = (u, grad psi_i) - <{u}.n, psi_i>       (pressure tests)
+// element-centric (normal out of the working cell; {.} = mean on interior faces, the
+// interior trace on walls, nothing on outlets).  One warp per cell, sum-factorised; the
+// geometry enters through the streamed records detJ w Jinv [9][Q^3] and n ds w
+// [6][3][Q^2] of rule k+1 (DevCtx::qadv / qfw, per cell SoA).  KP = K - 1.
+// ===========================================================================
+template <int K>
+struct MixQpCfg {
+  static constexpr int N = K + 1, NP = K, Q = K + 1, NB = N * N * N, NBP = NP * NP * NP, NF = N * N, NFP = NP * NP;
+  static constexpr int NQ = Q * Q * Q, NQF = Q * Q;
+  static constexpr int mx(int a, int b) { return a > b ? a : b; }
+  // pressure gradient: P | PF (nbr layers -> face-node means) | OUT | cell work | face work
+  static constexpr int G_P = 0, G_PF = G_P + NBP, G_OUT = G_PF + 6 * NFP, G_CW = G_OUT + NB;
+  static constexpr int G_X = 0, G_Y = G_X + Q * NFP, G_A = 0, G_XI = G_A + 3 * NQF * N;  // offsets inside cell work
+  static constexpr int G_CWS = mx(G_Y + NQF * NP, G_XI + 2 * Q * NF);
+  static constexpr int G_FP = G_CW + G_CWS, G_FA = G_FP + 6 * NP * Q, G_FO = G_FA + 6 * Q * N, G_END = G_FO + 6 * NF;
+  static constexpr int G_PER = G_END | 1;
+  // divergence: U (3 comps) | UF (nbr layers -> face-node means, 3 comps) | OUT | cell work | face work
+  static constexpr int D_U = 0, D_UF = D_U + 3 * NB, D_OUT = D_UF + 6 * 3 * NF, D_CW = D_OUT + NBP;
+  static constexpr int D_X = 0, D_Y = D_X + Q * NF, D_YS = NQF * N;             // y-pass arrays of the 3 comps
+  static constexpr int D_A = D_Y + 3 * D_YS, D_XI = D_A + 3 * NQF * NP;
+  static constexpr int D_CWS = D_XI + 2 * Q * NFP;
+  static constexpr int D_FP = D_CW + D_CWS, D_FA = D_FP + 6 * 3 * N * Q, D_FO = D_FA + 6 * Q * NP,
+                       D_END = D_FO + 6 * NFP;
+  static constexpr int D_PER = D_END | 1;
+  static constexpr int C = 4, T = 32 * C;
+  static constexpr size_t G_SMEM = (size_t)C * G_PER * sizeof(double);
+  static constexpr size_t D_SMEM = (size_t)C * D_PER * sizeof(double);
+};
+
+struct PresTerms {
+  int n = 0;
+  double c[kMaxTerms];
+  const double* f[kMaxTerms];
+};
+
+// y[cell][d][i] += sum_t c_t G(p_t)
+template <int K>
+__global__ void __launch_bounds__(MixQpCfg<K>::T) k_pgrad_qp(MeshArgs m, const double* __restrict__ gadv,
+                                                              const double* __restrict__ gfw, PresTerms pt,
+                                                              double* __restrict__ y) {
+  using G = MixQpCfg<K>;
+  constexpr int N = G::N, NP = G::NP, Q = G::Q, NB = G::NB, NBP = G::NBP, NF = G::NF, NFP = G::NFP, NQ = G::NQ,
+                NQF = G::NQF;
+  extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
+  const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5;
+  const int cid = blockIdx.x * G::C + wc;
+  if (cid >= m.ncells) return;
+  double* cell = sm + wc * G::G_PER;
+  double* P = cell + G::G_P;
+  double* PF = cell + G::G_PF;
+  double* OUT = cell + G::G_OUT;
+  double* W = cell + G::G_CW;
+  const FTab<N, Q>& tv = c_ft<N, Q>;    // velocity basis at the rule points (Q = N)
+  const FTab<NP, Q>& tp = c_ft<NP, Q>;  // pressure basis at the rule points
+  const double* ga = gadv + (size_t)cid * 9 * NQ;
+  const double* gw = gfw + (size_t)cid * 18 * NQF;
+  prefetch_l2(ga, 9 * NQ * sizeof(double), gadv, gadv + (size_t)m.ncells * 9 * NQ);
+  prefetch_l2(gw, 18 * NQF * sizeof(double), gfw, gfw + (size_t)m.ncells * 18 * NQF);
+  // ---- stage p = sum_t c_t p_t and the face-node means {p}
+  for (int i = lane; i < NBP; i += 32) {
+    double v = 0.0;
+    for (int t = 0; t < pt.n; ++t) v = fma(pt.c[t], pt.f[t][(size_t)cid * NBP + i], v);
+    P[i] = v;
+  }
+  __syncwarp();
+  for (int it = lane; it < 6 * NFP; it += 32) {
+    const int f = it / NFP, r = it - f * NFP, pp = r % NP, qq = r / NP;
+    const int a = f >> 1, s = f & 1;
+    const int nb = m.nbr[(size_t)cid * 6 + f];
+    const double ps = P[face_node<NP>(a, s ? NP - 1 : 0, pp, qq)];
+    double h;
+    if (nb >= 0) {
+      const int nn = face_node<NP>(a, s ? 0 : NP - 1, pp, qq);
+      double po = 0.0;
+      for (int t = 0; t < pt.n; ++t) po = fma(pt.c[t], __ldg(pt.f[t] + (size_t)nb * NBP + nn), po);
+      h = 0.5 * (ps + po);
+    } else {
+      const int bid = -1 - nb;
+      const bool outlet = bid >= 0 && bid < 64 && m.bctype[bid] == 1;
+      h = outlet ? 0.0 : ps;
+    }
+    PF[it] = h;
+  }
+  // ---- p at the cell points: x and y passes (the z pass runs inside the pointwise stage)
+  for (int jk = lane; jk < NFP; jk += 32) {
+    double u[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) u[i] = P[i + NP * jk];
+#pragma unroll
+    for (int qx = 0; qx < Q; ++qx) {
+      double b = 0.0;
+#pragma unroll
+      for (int i = 0; i < NP; ++i) b = fma(tp.B[qx][i], u[i], b);
+      W[G::G_X + qx * NFP + jk] = b;
+    }
+  }
+  __syncwarp();
+  double vcol[(NQF + 31) / 32][NP];  // this lane's (qx, qy) columns of the y pass
+  {
+    // y pass into registers is not possible across lanes; use the work area then reload
+    for (int it = lane; it < Q * NP; it += 32) {
+      const int qx = it / NP, k = it - qx * NP;
+      double v[NP];
+#pragma unroll
+      for (int j = 0; j < NP; ++j) v[j] = W[G::G_X + qx * NFP + j + NP * k];
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        double b = 0.0;
+#pragma unroll
+        for (int j = 0; j < NP; ++j) b = fma(tp.B[qy][j], v[j], b);
+        W[G::G_Y + (qx * Q + qy) * NP + k] = b;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int rr = 0; rr < (NQF + 31) / 32; ++rr) {
+      const int r = lane + 32 * rr;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) vcol[rr][k] = r < NQF ? W[G::G_Y + r * NP + k] : 0.0;
+    }
+    __syncwarp();
+  }
+  // ---- face-point values of {p}: along p, then along q inside the flux stage
+  for (int it = lane; it < 6 * NP; it += 32) {
+    const int f = it / NP, q = it - f * NP;
+    double v[NP];
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) v[pp] = PF[f * NFP + pp + NP * q];
+#pragma unroll
+    for (int qp = 0; qp < Q; ++qp) {
+      double b = 0.0;
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp) b = fma(tp.B[qp][pp], v[pp], b);
+      cell[G::G_FP + (f * NP + q) * Q + qp] = b;
+    }
+  }
+  __syncwarp();
+
+#pragma unroll 1
+  for (int d = 0; d < 3; ++d) {
+    // ---- cell: p(q) (detJ w Jinv)[a][d] against the reference gradient tests
+#pragma unroll
+    for (int rr = 0; rr < (NQF + 31) / 32; ++rr) {
+      const int r = lane + 32 * rr;
+      if (r < NQF) {
+        const int qx = r / Q, qy = r - qx * Q;
+        double a0[N], a1[N], a2[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) a0[k] = a1[k] = a2[k] = 0.0;
+#pragma unroll
+        for (int qz = 0; qz < Q; ++qz) {
+          double val = 0.0;
+#pragma unroll
+          for (int k = 0; k < NP; ++k) val = fma(tp.B[qz][k], vcol[rr][k], val);
+          const int pnt = qx + Q * qy + Q * Q * qz;
+          const double r0 = val * ga[(0 * 3 + d) * NQ + pnt], r1 = val * ga[(1 * 3 + d) * NQ + pnt],
+                       r2 = val * ga[(2 * 3 + d) * NQ + pnt];
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            a0[k] = fma(tv.B[qz][k], r0, a0[k]);
+            a1[k] = fma(tv.B[qz][k], r1, a1[k]);
+            a2[k] = fma(tv.D[qz][k], r2, a2[k]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          W[G::G_A + r * N + k] = a0[k];
+          W[G::G_A + NQF * N + r * N + k] = a1[k];
+          W[G::G_A + 2 * NQF * N + r * N + k] = a2[k];
+        }
+      }
+    }
+    __syncwarp();
+    for (int it = lane; it < Q * N; it += 32) {
+      const int qx = it / N, k = it - qx * N;
+      double p0[Q], p1[Q], p2[Q];
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        const int o = (qx * Q + qy) * N + k;
+        p0[qy] = W[G::G_A + o];
+        p1[qy] = W[G::G_A + NQF * N + o];
+        p2[qy] = W[G::G_A + 2 * NQF * N + o];
+      }
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double s0 = 0.0, s12 = 0.0;
+#pragma unroll
+        for (int qy = 0; qy < Q; ++qy) {
+          s0 = fma(tv.B[qy][j], p0[qy], s0);
+          s12 = fma(tv.D[qy][j], p1[qy], fma(tv.B[qy][j], p2[qy], s12));
+        }
+        W[G::G_XI + qx * NF + j + N * k] = s0;
+        W[G::G_XI + Q * NF + qx * NF + j + N * k] = s12;
+      }
+    }
+    __syncwarp();
+    for (int jk = lane; jk < NF; jk += 32) {
+      double p0[Q], p12[Q];
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        p0[qx] = W[G::G_XI + qx * NF + jk];
+        p12[qx] = W[G::G_XI + Q * NF + qx * NF + jk];
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int qx = 0; qx < Q; ++qx) sacc = fma(tv.D[qx][i], p0[qx], fma(tv.B[qx][i], p12[qx], sacc));
+        OUT[i + N * jk] = sacc;
+      }
+    }
+    // ---- faces: -{p} n_d ds w against the velocity traces
+    for (int it = lane; it < 6 * Q; it += 32) {
+      const int f = it / Q, qp = it - f * Q;
+      double vs[NP], A[N];
+#pragma unroll
+      for (int q = 0; q < NP; ++q) vs[q] = cell[G::G_FP + (f * NP + q) * Q + qp];
+#pragma unroll
+      for (int b = 0; b < N; ++b) A[b] = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < Q; ++qq) {
+        double hv = 0.0;
+#pragma unroll
+        for (int q = 0; q < NP; ++q) hv = fma(tp.B[qq][q], vs[q], hv);
+        const double fl = -hv * gw[(f * 3 + d) * NQF + qp + Q * qq];
+#pragma unroll
+        for (int b = 0; b < N; ++b) A[b] = fma(tv.B[qq][b], fl, A[b]);
+      }
+#pragma unroll
+      for (int b = 0; b < N; ++b) cell[G::G_FA + (f * Q + qp) * N + b] = A[b];
+    }
+    __syncwarp();
+    for (int it = lane; it < 6 * N; it += 32) {
+      const int f = it / N, b = it - f * N;
+      double av[Q];
+#pragma unroll
+      for (int qp = 0; qp < Q; ++qp) av[qp] = cell[G::G_FA + (f * Q + qp) * N + b];
+#pragma unroll
+      for (int bp = 0; bp < N; ++bp) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int qp = 0; qp < Q; ++qp) sacc = fma(tv.B[qp][bp], av[qp], sacc);
+        cell[G::G_FO + f * NF + bp + N * b] = sacc;
+      }
+    }
+    __syncwarp();
+    double* yc = y + ((size_t)cid * 3 + d) * NB;
+    for (int n = lane; n < NB; n += 32) {
+      double v = OUT[n];
+      const int i = n % N, j = (n / N) % N, k = n / NF;
+      const double* fo = cell + G::G_FO;
+      if (i == 0) v += fo[0 * NF + j + N * k];
+      if (i == N - 1) v += fo[1 * NF + j + N * k];
+      if (j == 0) v += fo[2 * NF + i + N * k];
+      if (j == N - 1) v += fo[3 * NF + i + N * k];
+      if (k == 0) v += fo[4 * NF + i + N * j];
+      if (k == N - 1) v += fo[5 * NF + i + N * j];
+      yc[n] += v;
+    }
+    __syncwarp();
+  }
+}
+
+// y[cell][i] = B(u)_i
+template <int K>
+__global__ void __launch_bounds__(MixQpCfg<K>::T) k_div_qp(MeshArgs m, const double* __restrict__ gadv,
+                                                            const double* __restrict__ gfw,
+                                                            const double* __restrict__ u, double* __restrict__ y) {
+  using G = MixQpCfg<K>;
+  constexpr int N = G::N, NP = G::NP, Q = G::Q, NB = G::NB, NBP = G::NBP, NF = G::NF, NFP = G::NFP, NQ = G::NQ,
+                NQF = G::NQF;
+  extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
+  const int lane = threadIdx.x & 31, wc = threadIdx.x >> 5;
+  const int cid = blockIdx.x * G::C + wc;
+  if (cid >= m.ncells) return;
+  double* cell = sm + wc * G::D_PER;
+  double* U = cell + G::D_U;
+  double* UF = cell + G::D_UF;
+  double* OUT = cell + G::D_OUT;
+  double* W = cell + G::D_CW;
+  const FTab<N, Q>& tv = c_ft<N, Q>;
+  const FTab<NP, Q>& tp = c_ft<NP, Q>;
+  const double* ga = gadv + (size_t)cid * 9 * NQ;
+  const double* gw = gfw + (size_t)cid * 18 * NQF;
+  prefetch_l2(ga, 9 * NQ * sizeof(double), gadv, gadv + (size_t)m.ncells * 9 * NQ);
+  prefetch_l2(gw, 18 * NQF * sizeof(double), gfw, gfw + (size_t)m.ncells * 18 * NQF);
+  for (int i = lane; i < 3 * NB; i += 32) cp_async8(U + i, u + (size_t)cid * 3 * NB + i);
+  cp_async_wait_all();
+  __syncwarp();
+  // ---- face-node means {u_d} (walls: the interior trace; outlets: none)
+  for (int it = lane; it < 6 * 3 * NF; it += 32) {
+    const int f = it / (3 * NF), r = it - f * 3 * NF, dd = r / NF, t = r - dd * NF, pp = t % N, qq = t / N;
+    const int a = f >> 1, s = f & 1;
+    const int nb = m.nbr[(size_t)cid * 6 + f];
+    const double us = U[dd * NB + face_node<N>(a, s ? N - 1 : 0, pp, qq)];
+    double h;
+    if (nb >= 0) {
+      h = 0.5 * (us + __ldg(u + (size_t)nb * 3 * NB + dd * NB + face_node<N>(a, s ? 0 : N - 1, pp, qq)));
+    } else {
+      const int bid = -1 - nb;
+      const bool outlet = bid >= 0 && bid < 64 && m.bctype[bid] == 1;
+      h = outlet ? 0.0 : us;
+    }
+    UF[it] = h;
+  }
+  // ---- u_d at the cell points: x / y passes per component
+#pragma unroll 1
+  for (int dd = 0; dd < 3; ++dd) {
+    for (int jk = lane; jk < NF; jk += 32) {
+      double v[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) v[i] = U[dd * NB + i + N * jk];
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) {
+        double b = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) b = fma(tv.B[qx][i], v[i], b);
+        W[G::D_X + qx * NF + jk] = b;
+      }
+    }
+    __syncwarp();
+    for (int it = lane; it < Q * N; it += 32) {
+      const int qx = it / N, k = it - qx * N;
+      double v[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) v[j] = W[G::D_X + qx * NF + j + N * k];
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        double b = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) b = fma(tv.B[qy][j], v[j], b);
+        W[G::D_Y + dd * G::D_YS + (qx * Q + qy) * N + k] = b;
+      }
+    }
+    __syncwarp();
+  }
+  // ---- pointwise: s_a = sum_d u_d (detJ w Jinv)[a][d], z-integrated against the pressure tests
+  for (int r = lane; r < NQF; r += 32) {
+    const int qx = r / Q, qy = r - qx * Q;
+    double v[3][N], a0[NP], a1[NP], a2[NP];
+#pragma unroll
+    for (int dd = 0; dd < 3; ++dd)
+#pragma unroll
+      for (int k = 0; k < N; ++k) v[dd][k] = W[G::D_Y + dd * G::D_YS + r * N + k];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) a0[k] = a1[k] = a2[k] = 0.0;
+#pragma unroll
+    for (int qz = 0; qz < Q; ++qz) {
+      const int pnt = qx + Q * qy + Q * Q * qz;
+      double r0 = 0.0, r1 = 0.0, r2 = 0.0;
+#pragma unroll
+      for (int dd = 0; dd < 3; ++dd) {
+        double val = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) val = fma(tv.B[qz][k], v[dd][k], val);
+        r0 = fma(val, ga[(0 * 3 + dd) * NQ + pnt], r0);
+        r1 = fma(val, ga[(1 * 3 + dd) * NQ + pnt], r1);
+        r2 = fma(val, ga[(2 * 3 + dd) * NQ + pnt], r2);
+      }
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        a0[k] = fma(tp.B[qz][k], r0, a0[k]);
+        a1[k] = fma(tp.B[qz][k], r1, a1[k]);
+        a2[k] = fma(tp.D[qz][k], r2, a2[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      W[G::D_A + r * NP + k] = a0[k];
+      W[G::D_A + NQF * NP + r * NP + k] = a1[k];
+      W[G::D_A + 2 * NQF * NP + r * NP + k] = a2[k];
+    }
+  }
+  __syncwarp();
+  for (int it = lane; it < Q * NP; it += 32) {
+    const int qx = it / NP, k = it - qx * NP;
+    double p0[Q], p1[Q], p2[Q];
+#pragma unroll
+    for (int qy = 0; qy < Q; ++qy) {
+      const int o = (qx * Q + qy) * NP + k;
+      p0[qy] = W[G::D_A + o];
+      p1[qy] = W[G::D_A + NQF * NP + o];
+      p2[qy] = W[G::D_A + 2 * NQF * NP + o];
+    }
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      double s0 = 0.0, s12 = 0.0;
+#pragma unroll
+      for (int qy = 0; qy < Q; ++qy) {
+        s0 = fma(tp.B[qy][j], p0[qy], s0);
+        s12 = fma(tp.D[qy][j], p1[qy], fma(tp.B[qy][j], p2[qy], s12));
+      }
+      W[G::D_XI + qx * NFP + j + NP * k] = s0;
+      W[G::D_XI + Q * NFP + qx * NFP + j + NP * k] = s12;
+    }
+  }
+  __syncwarp();
+  for (int jk = lane; jk < NFP; jk += 32) {
+    double p0[Q], p12[Q];
+#pragma unroll
+    for (int qx = 0; qx < Q; ++qx) {
+      p0[qx] = W[G::D_XI + qx * NFP + jk];
+      p12[qx] = W[G::D_XI + Q * NFP + qx * NFP + jk];
+    }
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int qx = 0; qx < Q; ++qx) sacc = fma(tp.D[qx][i], p0[qx], fma(tp.B[qx][i], p12[qx], sacc));
+      OUT[i + NP * jk] = sacc;
+    }
+  }
+  // ---- faces: -{u}.n ds w against the pressure traces
+  for (int it = lane; it < 6 * 3 * N; it += 32) {
+    const int f = it / (3 * N), r = it - f * 3 * N, dd = r / N, q = r - dd * N;
+    double v[N];
+#pragma unroll
+    for (int pp = 0; pp < N; ++pp) v[pp] = UF[(f * 3 + dd) * NF + pp + N * q];
+#pragma unroll
+    for (int qp = 0; qp < Q; ++qp) {
+      double b = 0.0;
+#pragma unroll
+      for (int pp = 0; pp < N; ++pp) b = fma(tv.B[qp][pp], v[pp], b);
+      cell[G::D_FP + ((f * 3 + dd) * N + q) * Q + qp] = b;
+    }
+  }
+  __syncwarp();
+  for (int it = lane; it < 6 * Q; it += 32) {
+    const int f = it / Q, qp = it - f * Q;
+    double vs[3][N], A[NP];
+#pragma unroll
+    for (int dd = 0; dd < 3; ++dd)
+#pragma unroll
+      for (int q = 0; q < N; ++q) vs[dd][q] = cell[G::D_FP + ((f * 3 + dd) * N + q) * Q + qp];
+#pragma unroll
+    for (int b = 0; b < NP; ++b) A[b] = 0.0;
+#pragma unroll
+    for (int qq = 0; qq < Q; ++qq) {
+      double un = 0.0;
+#pragma unroll
+      for (int dd = 0; dd < 3; ++dd) {
+        double val = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) val = fma(tv.B[qq][q], vs[dd][q], val);
+        un = fma(val, gw[(f * 3 + dd) * NQF + qp + Q * qq], un);
+      }
+#pragma unroll
+      for (int b = 0; b < NP; ++b) A[b] = fma(tp.B[qq][b], -un, A[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < NP; ++b) cell[G::D_FA + (f * Q + qp) * NP + b] = A[b];
+  }
+  __syncwarp();
+  for (int it = lane; it < 6 * NP; it += 32) {
+    const int f = it / NP, b = it - f * NP;
+    double av[Q];
+#pragma unroll
+    for (int qp = 0; qp < Q; ++qp) av[qp] = cell[G::D_FA + (f * Q + qp) * NP + b];
+#pragma unroll
+    for (int bp = 0; bp < NP; ++bp) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int qp = 0; qp < Q; ++qp) sacc = fma(tp.B[qp][bp], av[qp], sacc);
+      cell[G::D_FO + f * NFP + bp + NP * b] = sacc;
+    }
+  }
+  __syncwarp();
+  for (int n = lane; n < NBP; n += 32) {
+    double v = OUT[n];
+    const int i = n % NP, j = (n / NP) % NP, k = n / NFP;
+    const double* fo = cell + G::D_FO;
+    if (i == 0) v += fo[0 * NFP + j + NP * k];
+    if (i == NP - 1) v += fo[1 * NFP + j + NP * k];
+    if (j == 0) v += fo[2 * NFP + i + NP * k];
+    if (j == NP - 1) v += fo[3 * NFP + i + NP * k];
+    if (k == 0) v += fo[4 * NFP + i + NP * j];
+    if (k == NP - 1) v += fo[5 * NFP + i + NP * j];
+    y[(size_t)cid * NBP + n] = v;
+  }
+}
+
 }  // namespace dgb
 
 namespace dgb {

@@ -711,8 +711,9 @@ def test_2d_axis_sip_kernel_matches_reference_and_generic(ref, gpu, n_el, kp):
                                                (3, 2, 0.05, 4)])
 def test_deformed_rhs_matches_reference_and_generic(ref, gpu, n_el, ku, amp, outlet):
     """Stage RHS on distorted 3D meshes through RHS-mode k_momentum_qp launches (mass,
-    consistency-only viscous, central advective terms) + the generic pressure / data terms,
-    vs the reference and the all-generic path; walls, an outlet, Dirichlet data."""
+    consistency-only viscous, central advective terms), k_pgrad_qp (weak pressure gradient)
+    and the generic boundary-data terms, vs the reference and the all-generic path; walls,
+    an outlet, Dirichlet data."""
     R, D = pair(ref, gpu, 3, n_el, ku, ku - 1, amp, outlet=outlet, dirichlet_seed=5)
     un = gpu.seeded_uniform(61, R.n_u)
     ug = gpu.seeded_uniform(62, R.n_u)
@@ -730,4 +731,34 @@ def test_deformed_rhs_matches_reference_and_generic(ref, gpu, n_el, ku, amp, out
         y = D.zeros()
         gpu.momentum_rhs(D, spec, y)
         assert rel(host(y), want) <= TOL_APPLY, fast
+    D.set_fast_path(True)
+
+
+@pytest.mark.parametrize("n_el,ku,amp,outlet", [(2, 2, 0.03, None), (3, 2, 0.05, 4), (2, 3, 0.03, 1),
+                                               (3, 3, 0.04, None), (2, 4, 0.02, 0), (3, 4, 0.03, None)])
+def test_deformed_mixed_forms_match_reference_and_generic(ref, gpu, n_el, ku, amp, outlet):
+    """The mixed velocity-pressure forms on distorted 3D meshes (k_div_qp, k_pgrad_qp):
+    divergence_functional (forms.cpp:1118-1197), pressure_rhs (:1199-1210) and the pressure
+    terms of momentum_rhs alone (:850-855, :895-912, :940-948; two pressure fields with
+    different coefficients), vs the reference and the generic kernels; walls and an outlet."""
+    R, D = pair(ref, gpu, 3, n_el, ku, ku - 1, amp, outlet=outlet)
+    assert D.fast_path_active
+    u = gpu.seeded_uniform(71, R.n_u)
+    p1 = gpu.seeded_uniform(72, R.n_p)
+    p2 = gpu.seeded_uniform(73, R.n_p)
+    want_div = R.divergence(u)
+    want_prhs = R.pressure_rhs(1.7, u, 7.3, p1)
+    want_grad = R.momentum_rhs(pres=[(1.0, p1), (-0.35, p2)], time=0.0)
+    du, dp1, dp2 = dev(u), dev(p1), dev(p2)
+    for fast in (True, False):
+        D.set_fast_path(fast)
+        b = D.zeros(gpu.SPACE_P)
+        gpu.divergence_functional(D, du, b)
+        assert rel(host(b), want_div) <= TOL_APPLY, fast
+        pr = D.zeros(gpu.SPACE_P)
+        gpu.pressure_rhs(D, 1.7, du, 7.3, dp1, pr)
+        assert rel(host(pr), want_prhs) <= TOL_APPLY, fast
+        y = D.zeros()
+        gpu.momentum_rhs(D, gpu.MomentumRhs(pres=[(1.0, dp1), (-0.35, dp2)]), y)
+        assert rel(host(y), want_grad) <= TOL_APPLY, fast
     D.set_fast_path(True)
