@@ -140,8 +140,24 @@ class Device {
       for (int v = 0; v < nv; ++v) cells.push_back(mesh.cells[c].v[v]);
       for (int f = 0; f < nf; ++f) bids.push_back(mesh.cells[c].boundary_id[f]);
     }
-    check(dgb_ctx_create_mesh(dim, (int)mesh.vertices.size(), verts.data(), mesh.n_active(), cells.data(),
-                              bids.data(), Vu.degree(), Vp.degree(), device, &ctx_));
+    // hanging subfaces of a refined mesh (FaceInfo::hanging, mesh.cpp:344-375): the fine
+    // owner, the coarse neighbour and the subface's embedding into the coarse cell
+    std::vector<int> hang;
+    std::vector<double> emb;
+    for (const auto& f : mesh.faces().interior) {
+      if (!f.hanging) continue;
+      hang.insert(hang.end(), {mesh.active_index(f.cell_in), f.face_in, mesh.active_index(f.cell_out), f.face_out});
+      for (int d = 0; d < dim; ++d) emb.push_back(f.emb_out.origin[d]);
+      for (int t = 0; t < dim - 1; ++t)
+        for (int d = 0; d < dim; ++d) emb.push_back(f.emb_out.tangent[t][d]);
+    }
+    if (hang.empty())
+      check(dgb_ctx_create_mesh(dim, (int)mesh.vertices.size(), verts.data(), mesh.n_active(), cells.data(),
+                                bids.data(), Vu.degree(), Vp.degree(), device, &ctx_));
+    else
+      check(dgb_ctx_create_mesh_hanging(dim, (int)mesh.vertices.size(), verts.data(), mesh.n_active(), cells.data(),
+                                        bids.data(), (int)hang.size() / 4, hang.data(), emb.data(), Vu.degree(),
+                                        Vp.degree(), device, &ctx_));
     nu_ = Vu.n_dofs();
     np_ = Vp.n_dofs();
   }

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <random>
+#include <vector>
 
 #include "dgb_reference_adapter.hpp"
 #include "trbdf2_cpu.hpp"
@@ -28,12 +29,14 @@ static Field rnd(int n, unsigned s) {
   return f;
 }
 
+// refine: cells handed to one Mesh::refine_and_coarsen (hanging faces, mesh.cpp:344-375)
 template <int dim>
-static int run(int n_el, double amp, int ku) {
+static int run(int n_el, double amp, int ku, std::vector<int> refine = {}) {
   std::array<double, dim> lo{}, hi{};
   hi.fill(1.0);
   Mesh<dim> mesh = generate_cartesian<dim>(n_el, lo, hi);
   if (amp != 0.0) distort(mesh, amp, 7u);
+  if (!refine.empty()) mesh.refine_and_coarsen(refine, {});
   GeometryCache<dim> geom(mesh);
   FunctionSpace<dim> Vu(mesh, ku, dim), Vp(mesh, ku - 1, 1);
   BoundaryTable<dim> bc;
@@ -208,6 +211,10 @@ int main() {
   bad += run<3>(3, 0.0, 3);
   std::printf("3D 2^3 distorted, Q2/Q1\n");
   bad += run<3>(2, 0.03, 2);
+  std::printf("2D 3x3 distorted, cells 0 and 4 refined (hanging faces), Q2/Q1\n");
+  bad += run<2>(3, 0.04, 2, {0, 4});
+  std::printf("3D 2^3 Cartesian, cell 0 refined (hanging faces), Q2/Q1\n");
+  bad += run<3>(2, 0.0, 2, {0});
   std::printf(bad ? "ADAPTER PARITY FAILED (%d)\n" : "adapter parity ok\n", bad);
   return bad ? 1 : 0;
 }
