@@ -864,7 +864,27 @@ __global__ void __launch_bounds__(TH, DGB_MOM_MINB) k_momentum_axis(MeshArgs m, 
     const bool live = c < nc;
     int nbf[6];
     cell_nbrs6<UNI>(m, ug, live ? cell : c0, nbf);
-    if (live) {
+#ifndef DGB_MOM_S0V2
+#define DGB_MOM_S0V2 1
+#endif
+    constexpr bool S0V2 = DGB_MOM_S0V2 && N == 4;
+    if (S0V2 && live) {
+      // N = 4: element e = lane + 32 k is node (lane & 3, (lane >> 2) & 3, (lane >> 4) + 2 (k & 1)) of
+      // component k >> 1: one lane-dependent base, compile-time offsets per k
+      const int lb = (lane & 3) + P::PX * ((lane >> 2) & 3) + P::PY * (lane >> 4);
+      const unsigned sx = static_cast<unsigned>(__cvta_generic_to_shared(CELL(c) + G::O_X + lb));
+      const double* xs = x + (size_t)cell * 3 * NB + lane;
+      const double* ws = w + (size_t)cell * 3 * NB + lane;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        const unsigned off = ((k >> 1) * CT + 2 * P::PY * (k & 1)) * 8u;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sx + off), "l"(xs + 32 * k) : "memory");
+        if (MODE != 1)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sx + (G::O_W - G::O_X) * 8u + off),
+                       "l"(ws + 32 * k)
+                       : "memory");
+      }
+    } else if (live) {
       const double* xs = x + (size_t)cell * 3 * NB;
       const double* ws = w + (size_t)cell * 3 * NB;
 #pragma unroll
@@ -894,7 +914,12 @@ __global__ void __launch_bounds__(TH, DGB_MOM_MINB) k_momentum_axis(MeshArgs m, 
         for (int l = 0; l < N; ++l) nbL[d][j][l] = nbR[d][j][l] = 0.0;
         if (passA && live && r < NID) {
           int comp, tl;
-          line_item<K, NF>(r, d, comp, tl);
+          if (S0V2) {  // NF = 16: r = lane + 32 j -> component 2 j + (lane >> 4), line lane & 15
+            comp = 2 * j + (lane >> 4);
+            tl = lane & 15;
+          } else {
+            line_item<K, NF>(r, d, comp, tl);
+          }
           const int p = tl % N, q = tl / N;
           const int g0 = comp * NB + (d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q));
 #pragma unroll
@@ -989,6 +1014,25 @@ __global__ void __launch_bounds__(TH, DGB_MOM_MINB) k_momentum_axis(MeshArgs m, 
     constexpr int d = decltype(dtag)::value;
     constexpr int st = d == 0 ? 1 : (d == 1 ? P::PX : P::PY);
     double* sdst = WK(0) + (d == 0 ? G::A_SX : (d == 1 ? G::A_SY : G::A_SZ));
+#ifndef DGB_MOM_FCREG
+#define DGB_MOM_FCREG 1
+#endif
+    // one warp per cell: the cell's line-operator coefficients are the same for every item of
+    // the warp; read them once per direction (the stores of the item loop keep the compiler
+    // from hoisting the shared-memory loads itself)
+    CellInfo cir;
+    if constexpr (WPC && DGB_MOM_FCREG) {
+      const CellInfo& c0i = INFO(wcell);
+      cir.ih[d] = c0i.ih[d];
+      cir.A[d] = c0i.A[d];
+      cir.nb[2 * d] = c0i.nb[2 * d];
+      cir.nb[2 * d + 1] = c0i.nb[2 * d + 1];
+#pragma unroll
+      for (int e = 0; e < 6; ++e) {
+        cir.fc[2 * d][e] = c0i.fc[2 * d][e];
+        cir.fc[2 * d + 1][e] = c0i.fc[2 * d + 1][e];
+      }
+    }
 #pragma unroll
     for (int j = 0; j < MAXJ; ++j) {
       const int it = it0 + j * IST;
@@ -997,7 +1041,7 @@ __global__ void __launch_bounds__(TH, DGB_MOM_MINB) k_momentum_axis(MeshArgs m, 
         int comp, tl;
         line_item<K, NF>(r, d, comp, tl);
         const int p = tl % N, q = tl / N;
-        const CellInfo& ci = INFO(c);
+        const CellInfo& ci = (WPC && DGB_MOM_FCREG) ? cir : INFO(c);
         const int b0 = comp * CT + (d == 0 ? P::idx(0, p, q) : (d == 1 ? P::idx(p, 0, q) : P::idx(p, q, 0)));
         double u[N], o[N], uL[N], uR[N];
         const double* us = CELL(c) + G::O_X + b0;
