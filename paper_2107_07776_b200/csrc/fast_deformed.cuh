@@ -440,8 +440,11 @@ struct SipQpCfg {
   static constexpr size_t SMEM = (size_t)C * PER * sizeof(double);
 };
 
+#ifndef DGB_SQP_MINB
+#define DGB_SQP_MINB 1  // minimum CTAs per SM promised to ptxas (register cap = 64K / (MINB * T))
+#endif
 template <int KP>
-__global__ void __launch_bounds__(SipQpCfg<KP>::T) k_sip_qp(MeshArgs m, const double* __restrict__ gc,
+__global__ void __launch_bounds__(SipQpCfg<KP>::T, DGB_SQP_MINB) k_sip_qp(MeshArgs m, const double* __restrict__ gc,
                                                              const double* __restrict__ gf, double mc, int dir_bdry,
                                                              const double* __restrict__ x, double* __restrict__ y) {
   if (m.skip && *m.skip) return;
