@@ -441,7 +441,8 @@ struct SipQpCfg {
 };
 
 #ifndef DGB_SQP_MINB
-#define DGB_SQP_MINB 1  // minimum CTAs per SM promised to ptxas (register cap = 64K / (MINB * T))
+#define DGB_SQP_MINB 4  // minimum CTAs per SM promised to ptxas: 128 registers, 16 warps per SM
+                        // (cfg4 0.62 ms; MINB 1: 0.86, 5: 0.94; C = 2 / 6 / 8 cells per CTA: 0.82-1.15)
 #endif
 template <int KP>
 __global__ void __launch_bounds__(SipQpCfg<KP>::T, DGB_SQP_MINB) k_sip_qp(MeshArgs m, const double* __restrict__ gc,
