@@ -1083,9 +1083,10 @@ __global__ void __launch_bounds__(MixQpCfg<K>::T) k_pgrad_qp(MeshArgs m, const d
     }
   }
   __syncwarp();
-  double vcol[(NQF + 31) / 32][NP];  // this lane's (qx, qy) columns of the y pass
+  // y pass through the work area; every lane then keeps its (qx, qy) columns in registers for
+  // the three component passes below, which reuse the work area for their z-integrated arrays
+  double vcol[(NQF + 31) / 32][NP];
   {
-    // y pass into registers is not possible across lanes; use the work area then reload
     for (int it = lane; it < Q * NP; it += 32) {
       const int qx = it / NP, k = it - qx * NP;
       double v[NP];
