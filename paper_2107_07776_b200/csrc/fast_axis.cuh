@@ -792,7 +792,10 @@ template <int K, int CC, int TH, int MODE, bool UNI, bool RHS = false>
 #ifndef DGB_MOM_MINB  // minimum CTAs per SM promised to ptxas (0: no promise)
 #define DGB_MOM_MINB 2
 #endif
-__global__ void __launch_bounds__(TH, DGB_MOM_MINB) k_momentum_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff, MomCoef co,
+#ifndef DGB_MOM_MINB2  // the same for K = 2: shared memory allows 3 CTAs of 6 cells, 2 let ptxas take 123
+#define DGB_MOM_MINB2 3  // registers and lose the third CTA (cfg5 3.59 ms; 3: 96 registers, 3.31 ms)
+#endif
+__global__ void __launch_bounds__(TH, K == 2 ? DGB_MOM_MINB2 : DGB_MOM_MINB) k_momentum_axis(MeshArgs m, UniformGrid ug, const double* __restrict__ aff, MomCoef co,
                                                       const double* __restrict__ x, const double* __restrict__ w,
                                                       double* __restrict__ y, int acc) {
   if (m.skip && *m.skip) return;
@@ -1021,7 +1024,7 @@ __global__ void __launch_bounds__(TH, DGB_MOM_MINB) k_momentum_axis(MeshArgs m, 
     // the warp; read them once per direction (the stores of the item loop keep the compiler
     // from hoisting the shared-memory loads itself)
     CellInfo cir;
-    if constexpr (WPC && DGB_MOM_FCREG) {
+    if constexpr (WPC && DGB_MOM_FCREG && K == 3) {  // (K = 2: 3.36 vs 3.31 ms at cfg5, off)
       const CellInfo& c0i = INFO(wcell);
       cir.ih[d] = c0i.ih[d];
       cir.A[d] = c0i.A[d];
@@ -1041,7 +1044,7 @@ __global__ void __launch_bounds__(TH, DGB_MOM_MINB) k_momentum_axis(MeshArgs m, 
         int comp, tl;
         line_item<K, NF>(r, d, comp, tl);
         const int p = tl % N, q = tl / N;
-        const CellInfo& ci = (WPC && DGB_MOM_FCREG) ? cir : INFO(c);
+        const CellInfo& ci = (WPC && DGB_MOM_FCREG && K == 3) ? cir : INFO(c);
         const int b0 = comp * CT + (d == 0 ? P::idx(0, p, q) : (d == 1 ? P::idx(p, 0, q) : P::idx(p, q, 0)));
         double u[N], o[N], uL[N], uR[N];
         const double* us = CELL(c) + G::O_X + b0;
