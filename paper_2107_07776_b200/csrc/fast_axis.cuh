@@ -702,6 +702,190 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
 }
 
 // ===========================================================================
+// Scalar SIP operator on UNIFORM Cartesian 3D grids, one THREAD per cell.
+//
+// With N = 2 or 3 nodes per direction a cell's values fit in registers, so the whole
+// line split  y = sum_d (M (x) M (x) (S_d + mc detJ / 3 M_d)) u  runs thread-serially
+// with compile-time indices: no per-stage shared-memory round trips (k_sip_axis moves
+// ~88 shared wavefronts per Q2 cell, this kernel ~15) and no idle lanes.  A CTA owns a
+// TX x TY x TZ tile of cells; the tile and its face-neighbour halo are staged once by
+// row-wise coalesced cp.async copies (cells are x-fastest, so a box row is one
+// contiguous range; cell stride odd: threads of a warp reading the same node of
+// consecutive cells hit distinct banks), every thread reads its lines and its
+// neighbours' lines from there, and the result goes back through the same buffer so the
+// global stores are coalesced rows too.  CGF: <p, A p> per-warp partials as k_sip_axis.
+// ===========================================================================
+template <int KP>
+struct SipCellCfg {
+  static constexpr int N = KP + 1, NB = N * N * N, NF = N * N;
+  static constexpr int TX = 8, TY = 4, TZ = 4, T = TX * TY * TZ;
+  static constexpr int BX = TX + 2, BY = TY + 2, BZ = TZ + 2, NBOX = BX * BY * BZ;
+  static constexpr int CS = NB | 1;  // odd cell stride
+  static constexpr size_t SMEM = (size_t)NBOX * CS * sizeof(double);
+};
+
+template <int KP, bool CGF = false>
+__global__ void __launch_bounds__(SipCellCfg<KP>::T) k_sip_cell(MeshArgs m, UniformGrid ug, double mc, int dir_bdry,
+                                                                 const double* __restrict__ x,
+                                                                 double* __restrict__ y, SipCgArgs cg) {
+  if (m.skip && *m.skip) return;
+  using G = SipCellCfg<KP>;
+  constexpr int N = G::N, NB = G::NB, NF = G::NF, CS = G::CS;
+  constexpr int TX = G::TX, TY = G::TY, TZ = G::TZ, BX = G::BX, BY = G::BY, BZ = G::BZ;
+  const FTab<N, N>& ta = c_ft<N, N>;
+  extern __shared__ double sm[];
+  DGB_POISON_SMEM(m, sm);
+  const int n = ug.n;
+  const int ntx = (n + TX - 1) / TX, nty = (n + TY - 1) / TY;
+  const int bx = blockIdx.x % ntx, by = (blockIdx.x / ntx) % nty, bz = blockIdx.x / (ntx * nty);
+  // owned z-layers [zlo, zhi): the whole mesh, or the layer range of dgb_set_cell_range
+  // (z-slab applies; the layers next to the range are read as ghosts)
+  const int zlo = m.cell0 / (n * n), zhi = m.cell1 < 0 ? n : m.cell1 / (n * n);
+  const int x0 = bx * TX, y0 = by * TY, z0 = zlo + bz * TZ;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- stage the box rows (tile + face halo; the box's edge rows are never read)
+  {
+    const int xa = max(x0 - 1, 0), xb = min(x0 + TX, n - 1);  // first / last cell of a row inside the domain
+    const int e0 = (xa - (x0 - 1)) * NB, e1 = (xb - (x0 - 1) + 1) * NB;
+    for (int r = warp; r < BY * BZ; r += G::T / 32) {
+      const int rby = r % BY, rbz = r / BY;
+      const bool hy = rby == 0 || rby == BY - 1, hz = rbz == 0 || rbz == BZ - 1;
+      const int gy = y0 - 1 + rby, gz = z0 - 1 + rbz;
+      if ((hy && hz) || gy < 0 || gy >= n || gz < 0 || gz >= n) continue;
+      // tile rows beyond a partial tile's end are only needed as halo of the last row inside
+      const double* src = x + ((size_t)((size_t)gz * n + gy) * n + (x0 - 1)) * NB;  // may point before x: only [e0, e1) is read
+      double* dst = sm + (size_t)BX * (rby + BY * rbz) * CS;
+      for (int e = e0 + lane; e < e1; e += 32) {
+        const int so = CS == NB ? e : (e / NB) * CS + e % NB;
+        cp_async8(dst + so, src + e);
+      }
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int tx = tid % TX, ty = (tid / TX) % TY, tz = tid / (TX * TY);
+  const int gx = x0 + tx, gy = y0 + ty, gz = z0 + tz;
+  const bool live = gx < n && gy < n && gz < zhi;
+  const int bc = (tx + 1) + BX * ((ty + 1) + BY * (tz + 1));
+  const double* U = sm + (size_t)bc * CS;
+  // uniform-grid cell record (the scalar operator treats every boundary face alike:
+  // natural, or Dirichlet-type when dir_bdry; forms.cpp:218-242)
+  CellInfo ci;
+  const double sfac = (double)(N * N);
+  ci.detJ = ug.detJ;
+  const int co[3] = {gx, gy, gz};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    ci.ih[d] = ug.ih;
+    ci.A[d] = ug.detJ * ug.ih;
+#pragma unroll
+    for (int sd = 0; sd < 2; ++sd) {
+      const bool bdry = sd ? co[d] == n - 1 : co[d] == 0;
+      ci.type[2 * d + sd] = bdry ? 1 : 0;
+      ci.pen[2 * d + sd] = sfac * (bdry ? ug.pen_bdry : ug.pen_int);
+      ci.ihn[2 * d + sd] = bdry ? 0.0 : ug.ih;
+    }
+  }
+  const double cm3 = mc * ug.detJ * (1.0 / 3.0);
+  double V[NB], tmp[NB];
+  // A_d = (S_d + cm3 M_d) u on the lines of direction d: node of line t at position l = base(t) + l * st
+  auto lines = [&](auto dtag, double* out) {
+    constexpr int d = decltype(dtag)::value;
+    constexpr int st = d == 0 ? 1 : (d == 1 ? N : NF);
+    constexpr int bst = d == 0 ? 1 : (d == 1 ? BX : BX * BY);
+    const double* UL = U - (size_t)bst * CS;
+    const double* UR = U + (size_t)bst * CS;
+#pragma unroll
+    for (int t = 0; t < NF; ++t) {
+      const int p = t % N, q = t / N;
+      const int b0 = d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q);
+      double u[N], uL[N], uR[N], o[N];
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        u[l] = U[b0 + l * st];
+        uL[l] = UL[b0 + l * st];
+        uR[l] = UR[b0 + l * st];
+      }
+      sip_line<N>(ta, ci, d, u, uL, uR, dir_bdry != 0, 1.0, o);
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) sacc = fma(ta.M[i][l], u[l], sacc);
+        out[b0 + i * st] = fma(cm3, sacc, o[i]);
+      }
+    }
+  };
+  // in-place 1D mass along direction d of a full cell array
+  auto mass = [&](auto dtag, double* a) {
+    constexpr int d = decltype(dtag)::value;
+    constexpr int st = d == 0 ? 1 : (d == 1 ? N : NF);
+#pragma unroll
+    for (int t = 0; t < NF; ++t) {
+      const int p = t % N, q = t / N;
+      const int b0 = d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q);
+      double v[N];
+#pragma unroll
+      for (int l = 0; l < N; ++l) v[l] = a[b0 + l * st];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) sacc = fma(ta.M[i][l], v[l], sacc);
+        a[b0 + i * st] = sacc;
+      }
+    }
+  };
+  using D0 = std::integral_constant<int, 0>;
+  using D1 = std::integral_constant<int, 1>;
+  using D2 = std::integral_constant<int, 2>;
+  double pq = 0.0;
+  if (live) {
+    lines(D0{}, V);    // V = M_y A_x
+    mass(D1{}, V);
+    lines(D1{}, tmp);  // V += M_x A_y
+    mass(D0{}, tmp);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) V[i] += tmp[i];
+    mass(D2{}, V);     // V = M_z (M_y A_x + M_x A_y)
+    lines(D2{}, tmp);  // V += M_y M_x A_z
+    mass(D0{}, tmp);
+    mass(D1{}, tmp);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) V[i] += tmp[i];
+    if (CGF) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i) pq = fma(U[i], V[i], pq);
+    }
+  }
+  if (CGF) {  // one deterministic partial per warp (shuffle tree)
+    double a = pq;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) cg.partial[blockIdx.x * (G::T / 32) + warp] = a;
+  }
+  // ---- results back through the staging buffer: coalesced row stores
+  __syncthreads();  // every neighbour has read this cell's values
+  if (live) {
+    double* O = sm + (size_t)bc * CS;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) O[i] = V[i];
+  }
+  __syncthreads();
+  {
+    const int xe = min(TX, n - x0) * NB;  // doubles of a tile row inside the domain
+    for (int r = warp; r < TY * TZ; r += G::T / 32) {
+      const int rty = r % TY, rtz = r / TY;
+      const int gyr = y0 + rty, gzr = z0 + rtz;
+      if (gyr >= n || gzr >= zhi) continue;
+      double* dst = y + ((size_t)((size_t)gzr * n + gyr) * n + x0) * NB;
+      const double* src = sm + (size_t)(1 + BX * ((rty + 1) + BY * (rtz + 1))) * CS;
+      for (int e = lane; e < xe; e += 32) dst[e] = src[CS == NB ? e : (e / NB) * CS + e % NB];
+    }
+  }
+}
+
+// ===========================================================================
 // Momentum operator, axis-aligned affine, 3D, skew = 0:
 //   mass M x + visc A_sip x     (line-split, exact)
 // + adv C_lf(w) x               (k+2 Gauss rule; sum factorisation)

@@ -2,6 +2,7 @@
 #include "fast_axis.cuh"
 #include "fast_deformed.cuh"
 
+#include <cstdlib>
 #include <vector>
 
 #include "blas.cuh"
@@ -74,12 +75,41 @@ static cudaError_t set_smem(KernelT kern, size_t smem) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+// Uniform Cartesian grids, pressure degrees 1 and 2, whole-mesh applies: the
+// thread-per-cell kernel (DGB_SIP_CELL=0 in the environment keeps k_sip_axis)
+template <int KP>
+static bool sip_cell_applies(const DevCtx& c) {
+  static const bool off = [] {
+    const char* v = std::getenv("DGB_SIP_CELL");
+    return v && v[0] == '0';
+  }();
+  const long long n = c.ug.n, layer = n * n;
+  // the whole mesh or a range of whole z-layers (dgb_set_cell_range: slabs, host-buffer pipeline)
+  return KP <= 2 && !off && n > 1 && n * layer == (long long)c.ncells && c.mesh.cell0 % layer == 0 &&
+         (c.mesh.cell1 < 0 || c.mesh.cell1 % layer == 0);
+}
+template <int KP>
+static int sip_cell_grid(const DevCtx& c) {
+  using G = SipCellCfg<KP>;
+  const int n = c.ug.n, layer = n * n;
+  const int nz = (c.mesh.cell1 < 0 ? n : c.mesh.cell1 / layer) - c.mesh.cell0 / layer;
+  return ((n + G::TX - 1) / G::TX) * ((n + G::TY - 1) / G::TY) * ((nz + G::TZ - 1) / G::TZ);
+}
+
 template <int KP, bool CGF = false>
 static cudaError_t run_sip_axis(const DevCtx& c, double mc, int dir, const double* x, double* y,
                                 SipCgArgs cg = SipCgArgs()) {
   using G = SipAxisCfg<KP>;
   cudaError_t e = ensure_ftab<KP + 1, KP + 1>();
   if (e != cudaSuccess) return e;
+  if constexpr (KP <= 2) {
+    if (sip_cell_applies<KP>(c)) {
+      using S = SipCellCfg<KP>;
+      if ((e = set_smem(k_sip_cell<KP, CGF>, S::SMEM)) != cudaSuccess) return e;
+      k_sip_cell<KP, CGF><<<sip_cell_grid<KP>(c), S::T, S::SMEM, c.stream>>>(c.mesh, c.ug, mc, dir, x, y, cg);
+      return cudaGetLastError();
+    }
+  }
   const int grid = (fast_cells(c) + G::C - 1) / G::C;
   if (c.ug.n > 0) {
     if ((e = set_smem(k_sip_axis<KP, true, CGF>, G::SMEM)) != cudaSuccess) return e;
@@ -328,6 +358,8 @@ cudaError_t fast_sip3(const DevCtx& c, double mc, int dir, const double* x, doub
 }
 
 int fast_sip3_cg_blocks(const DevCtx& c) {
+  if (c.kp == 1 && sip_cell_applies<1>(c)) return sip_cell_grid<1>(c) * (SipCellCfg<1>::T / 32);
+  if (c.kp == 2 && sip_cell_applies<2>(c)) return sip_cell_grid<2>(c) * (SipCellCfg<2>::T / 32);
   switch (c.kp) {
     case 1: return (c.ncells + SipAxisCfg<1>::C - 1) / SipAxisCfg<1>::C * (SipAxisCfg<1>::T / 32);
     case 2: return (c.ncells + SipAxisCfg<2>::C - 1) / SipAxisCfg<2>::C * (SipAxisCfg<2>::T / 32);

@@ -72,16 +72,25 @@ def test_bitwise_determinism_and_cta_order_independence(gpu, n_el, ku):
         gpu.apply_momentum(D, ctx, x, y)
         gpu.apply_pressure_helmholtz(D, 2.3, xp, yp)
         assert torch.equal(y, ref_u) and torch.equal(yp, ref_p)
-    # the same applies as separate launches over cell ranges, issued last range first
+    # the same applies as separate launches over cell ranges, issued last range first.
+    # Whole z-layer ranges keep the pressure apply on the thread-per-cell kernel
+    # (k_sip_cell), arbitrary ranges move it to k_sip_axis: bitwise equality where the
+    # kernel is the same, rounding-level agreement across the two kernels.
     nbu, nbp = D.n_u // D.ncells, D.n_p // D.ncells
-    cuts = [0, 7, D.ncells // 3, D.ncells // 2 + 5, D.ncells]
-    y, yp = D.zeros(), D.zeros(gpu.SPACE_P)
-    for a, b in reversed(list(zip(cuts[:-1], cuts[1:]))):
-        gpu.lib().dgb_set_cell_range(D.handle, a, b)
-        ty, typ = D.zeros(), D.zeros(gpu.SPACE_P)
-        gpu.apply_momentum(D, ctx, x, ty)
-        gpu.apply_pressure_helmholtz(D, 2.3, xp, typ)
-        y[a * nbu:b * nbu] = ty[a * nbu:b * nbu]
-        yp[a * nbp:b * nbp] = typ[a * nbp:b * nbp]
-    gpu.lib().dgb_set_cell_range(D.handle, 0, -1)
-    assert torch.equal(y, ref_u) and torch.equal(yp, ref_p)
+    layer = n_el * n_el
+    for cuts, same_kernel in (([0, layer, 5 * layer, (n_el // 2 + 3) * layer, D.ncells], True),
+                              ([0, 7, D.ncells // 3, D.ncells // 2 + 5, D.ncells], False)):
+        y, yp = D.zeros(), D.zeros(gpu.SPACE_P)
+        for a, b in reversed(list(zip(cuts[:-1], cuts[1:]))):
+            gpu.lib().dgb_set_cell_range(D.handle, a, b)
+            ty, typ = D.zeros(), D.zeros(gpu.SPACE_P)
+            gpu.apply_momentum(D, ctx, x, ty)
+            gpu.apply_pressure_helmholtz(D, 2.3, xp, typ)
+            y[a * nbu:b * nbu] = ty[a * nbu:b * nbu]
+            yp[a * nbp:b * nbp] = typ[a * nbp:b * nbp]
+        gpu.lib().dgb_set_cell_range(D.handle, 0, -1)
+        assert torch.equal(y, ref_u)
+        if same_kernel:
+            assert torch.equal(yp, ref_p)
+        else:
+            assert float((yp - ref_p).norm() / ref_p.norm()) <= 1e-14
