@@ -718,14 +718,28 @@ __global__ void __launch_bounds__(SipAxisCfg<KP>::T) k_sip_axis(MeshArgs m, Unif
 template <int KP>
 struct SipCellCfg {
   static constexpr int N = KP + 1, NB = N * N * N, NF = N * N;
-  static constexpr int TX = 8, TY = 4, TZ = 4, T = TX * TY * TZ;
+  // tile shape and register cap per degree (measured, profiles/experiments_r02.md): long x-rows
+  // stage best; Q1: 80 registers (6 CTAs per SM), Q2: all 255 (2 CTAs per SM, shared-memory bound)
+#ifndef DGB_SIPC_TX
+#define DGB_SIPC_TX 16
+#define DGB_SIPC_TY (KP == 1 ? 2 : 4)
+#define DGB_SIPC_TZ (KP == 1 ? 4 : 2)
+#endif
+#ifndef DGB_SIPC_MINB1
+#define DGB_SIPC_MINB1 6
+#endif
+#ifndef DGB_SIPC_MINB2
+#define DGB_SIPC_MINB2 1
+#endif
+  static constexpr int TX = DGB_SIPC_TX, TY = DGB_SIPC_TY, TZ = DGB_SIPC_TZ, T = TX * TY * TZ;
+  static constexpr int MINB = KP == 1 ? DGB_SIPC_MINB1 : DGB_SIPC_MINB2;
   static constexpr int BX = TX + 2, BY = TY + 2, BZ = TZ + 2, NBOX = BX * BY * BZ;
   static constexpr int CS = NB | 1;  // odd cell stride
   static constexpr size_t SMEM = (size_t)NBOX * CS * sizeof(double);
 };
 
 template <int KP, bool CGF = false>
-__global__ void __launch_bounds__(SipCellCfg<KP>::T) k_sip_cell(MeshArgs m, UniformGrid ug, double mc, int dir_bdry,
+__global__ void __launch_bounds__(SipCellCfg<KP>::T, SipCellCfg<KP>::MINB) k_sip_cell(MeshArgs m, UniformGrid ug, double mc, int dir_bdry,
                                                                  const double* __restrict__ x,
                                                                  double* __restrict__ y, SipCgArgs cg) {
   if (m.skip && *m.skip) return;
@@ -787,75 +801,103 @@ __global__ void __launch_bounds__(SipCellCfg<KP>::T) k_sip_cell(MeshArgs m, Unif
     }
   }
   const double cm3 = mc * ug.detJ * (1.0 / 3.0);
-  double V[NB], tmp[NB];
-  // A_d = (S_d + cm3 M_d) u on the lines of direction d: node of line t at position l = base(t) + l * st
-  auto lines = [&](auto dtag, double* out) {
+  // line t of direction d (nodes base(t) + l * st of the cell array): o = (S_d + cm3 M_d) u
+  auto line = [&](auto dtag, int p, int q, double* o) {
     constexpr int d = decltype(dtag)::value;
     constexpr int st = d == 0 ? 1 : (d == 1 ? N : NF);
     constexpr int bst = d == 0 ? 1 : (d == 1 ? BX : BX * BY);
     const double* UL = U - (size_t)bst * CS;
     const double* UR = U + (size_t)bst * CS;
+    const int b0 = d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q);
+    double u[N], uL[N], uR[N];
 #pragma unroll
-    for (int t = 0; t < NF; ++t) {
-      const int p = t % N, q = t / N;
-      const int b0 = d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q);
-      double u[N], uL[N], uR[N], o[N];
-#pragma unroll
-      for (int l = 0; l < N; ++l) {
-        u[l] = U[b0 + l * st];
-        uL[l] = UL[b0 + l * st];
-        uR[l] = UR[b0 + l * st];
-      }
-      sip_line<N>(ta, ci, d, u, uL, uR, dir_bdry != 0, 1.0, o);
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double sacc = 0.0;
-#pragma unroll
-        for (int l = 0; l < N; ++l) sacc = fma(ta.M[i][l], u[l], sacc);
-        out[b0 + i * st] = fma(cm3, sacc, o[i]);
-      }
+    for (int l = 0; l < N; ++l) {
+      u[l] = U[b0 + l * st];
+      uL[l] = UL[b0 + l * st];
+      uR[l] = UR[b0 + l * st];
     }
-  };
-  // in-place 1D mass along direction d of a full cell array
-  auto mass = [&](auto dtag, double* a) {
-    constexpr int d = decltype(dtag)::value;
-    constexpr int st = d == 0 ? 1 : (d == 1 ? N : NF);
+    sip_line<N>(ta, ci, d, u, uL, uR, dir_bdry != 0, 1.0, o);
 #pragma unroll
-    for (int t = 0; t < NF; ++t) {
-      const int p = t % N, q = t / N;
-      const int b0 = d == 0 ? N * (p + N * q) : (d == 1 ? p + NF * q : p + N * q);
-      double v[N];
+    for (int i = 0; i < N; ++i) {
+      double sacc = 0.0;
 #pragma unroll
-      for (int l = 0; l < N; ++l) v[l] = a[b0 + l * st];
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double sacc = 0.0;
-#pragma unroll
-        for (int l = 0; l < N; ++l) sacc = fma(ta.M[i][l], v[l], sacc);
-        a[b0 + i * st] = sacc;
-      }
+      for (int l = 0; l < N; ++l) sacc = fma(ta.M[i][l], u[l], sacc);
+      o[i] = fma(cm3, sacc, o[i]);
     }
   };
   using D0 = std::integral_constant<int, 0>;
   using D1 = std::integral_constant<int, 1>;
   using D2 = std::integral_constant<int, 2>;
+  // Y = M_y M_x A_z first (the only term whose lines cross the z-planes), then plane by plane
+  // P_k = M_y A_x + M_x A_y (N^2 values) and Y[., ., k'] += M[k'][k] P_k: 1 + 1/N cell arrays live
+  double Y[NB];
   double pq = 0.0;
   if (live) {
-    lines(D0{}, V);    // V = M_y A_x
-    mass(D1{}, V);
-    lines(D1{}, tmp);  // V += M_x A_y
-    mass(D0{}, tmp);
 #pragma unroll
-    for (int i = 0; i < NB; ++i) V[i] += tmp[i];
-    mass(D2{}, V);     // V = M_z (M_y A_x + M_x A_y)
-    lines(D2{}, tmp);  // V += M_y M_x A_z
-    mass(D0{}, tmp);
-    mass(D1{}, tmp);
+    for (int j = 0; j < N; ++j) {
+      double az[N][N];  // [i][k] of row j
 #pragma unroll
-    for (int i = 0; i < NB; ++i) V[i] += tmp[i];
+      for (int i = 0; i < N; ++i) line(D2{}, i, j, az[i]);
+#pragma unroll
+      for (int k = 0; k < N; ++k)  // M_x along i
+#pragma unroll
+        for (int i2 = 0; i2 < N; ++i2) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) sacc = fma(ta.M[i2][i], az[i][k], sacc);
+          Y[i2 + N * j + NF * k] = sacc;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < N; ++k)  // M_y along j, in place
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double v[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) v[j] = Y[i + N * j + NF * k];
+#pragma unroll
+        for (int j2 = 0; j2 < N; ++j2) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) sacc = fma(ta.M[j2][j], v[j], sacc);
+          Y[i + N * j2 + NF * k] = sacc;
+        }
+      }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double ax[N][N], P[N][N];  // ax[j][i]; P[j][i]
+#pragma unroll
+      for (int j = 0; j < N; ++j) line(D0{}, j, k, ax[j]);
+#pragma unroll
+      for (int j2 = 0; j2 < N; ++j2)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) sacc = fma(ta.M[j2][j], ax[j][i], sacc);
+          P[j2][i] = sacc;
+        }
+#pragma unroll
+      for (int i = 0; i < N; ++i) line(D1{}, i, k, ax[i]);  // ax[i][j] now holds A_y
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i2 = 0; i2 < N; ++i2) {
+          double sacc = P[j][i2];
+#pragma unroll
+          for (int i = 0; i < N; ++i) sacc = fma(ta.M[i2][i], ax[i][j], sacc);
+          P[j][i2] = sacc;
+        }
+#pragma unroll
+      for (int k2 = 0; k2 < N; ++k2)
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+#pragma unroll
+          for (int i = 0; i < N; ++i) Y[i + N * j + NF * k2] = fma(ta.M[k2][k], P[j][i], Y[i + N * j + NF * k2]);
+    }
     if (CGF) {
 #pragma unroll
-      for (int i = 0; i < NB; ++i) pq = fma(U[i], V[i], pq);
+      for (int i = 0; i < NB; ++i) pq = fma(U[i], Y[i], pq);
     }
   }
   if (CGF) {  // one deterministic partial per warp (shuffle tree)
@@ -869,7 +911,7 @@ __global__ void __launch_bounds__(SipCellCfg<KP>::T) k_sip_cell(MeshArgs m, Unif
   if (live) {
     double* O = sm + (size_t)bc * CS;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) O[i] = V[i];
+    for (int i = 0; i < NB; ++i) O[i] = Y[i];
   }
   __syncthreads();
   {
