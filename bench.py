@@ -546,7 +546,11 @@ def run_device(args):
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": DATA, "config": bench_config(ws), "warmup_steps_run": nwarm,
         "ops": {"momentum": {"ms": tm * 1e3, "gdofs": D.n_u / tm / 1e9, "tflops_alg": mom_tflops},
-                "pressure": {"ms": tp * 1e3, "gdofs": D.n_p / tp / 1e9, "tflops_alg": prs_tflops}},
+                "pressure": {"ms": tp * 1e3, "gdofs": D.n_p / tp / 1e9, "tflops_alg": prs_tflops,
+                             "fp64_frac_alg": prs_tflops / peak_fp64,
+                             "hbm_frac_alg": BYTES_PER_DOF["pressure"] * D.n_p / tp / 1e9 / peaks.get("hbm_gbs", 6535.7),
+                             "note": "algorithmic = the reference's dense-table flop count (SURVEY 8d, 406.2 flop/DoF); "
+                                     "the exact line split of k_sip_cell executes ~130 flop/DoF"}},
         "roofline": roofline, "roofline_hbm": roofline_hbm, "cpu_baseline": cpu,
         "e2e": {"value": e2e_val, "unit": "GDoF/s", "h2d_bytes_per_step": 8 * (2 * D.n_u + D.n_p),
                 "d2h_bytes_per_step": 8 * (D.n_u + D.n_p)},
