@@ -161,6 +161,23 @@ __global__ void k_cg_dir(size_t n, const double* __restrict__ z, double* __restr
   const double beta = first ? 0.0 : st->rho / st->rho_old;
   GRID_STRIDE(i, n) p[i] = first ? z[i] : fma(beta, p[i], z[i]);
 }
+// the same on pairs of elements (16-byte aligned vectors)
+__global__ void __launch_bounds__(kBlasThreads) k_cg_dir2(size_t n, const double* __restrict__ z,
+                                                          double* __restrict__ p, const CgState* st) {
+  if (st->done) return;
+  const int first = st->first;
+  const double beta = first ? 0.0 : st->rho / st->rho_old;
+  const double2* z2 = reinterpret_cast<const double2*>(z);
+  double2* p2 = reinterpret_cast<double2*>(p);
+  GRID_STRIDE(i, n >> 1) {
+    const double2 zv = z2[i];
+    double2 pv = p2[i];
+    pv.x = first ? zv.x : fma(beta, pv.x, zv.x);
+    pv.y = first ? zv.y : fma(beta, pv.y, zv.y);
+    p2[i] = pv;
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) p[n - 1] = first ? z[n - 1] : fma(beta, p[n - 1], z[n - 1]);
+}
 __global__ void k_cg_pq_part(size_t n, const double* __restrict__ p, const double* __restrict__ q,
                              double* __restrict__ partial, CgState* st) {
   if (st->done) return;
@@ -193,6 +210,58 @@ __global__ void k_cg_upd_part(size_t n, const double* __restrict__ p, const doub
     const double ri = fma(-a, q[i], r[i]);
     r[i] = ri;
     const double zi = inv ? ri * inv[i] : ri;
+    z[i] = zi;
+    acc[0] = fma(ri, ri, acc[0]);
+    acc[1] = fma(ri, zi, acc[1]);
+  }
+  block_reduce_store<2>(acc, partial);
+  if (last_block_arrival(&st->cnt_upd)) cg_upd_finish(gridDim.x, partial, st, hist);
+}
+// the same on pairs of elements (16-byte loads / stores; all vectors 16-byte aligned, an odd
+// tail element is taken by thread 0 of block 0).  The per-element arithmetic and the
+// order of the thread-local sums over a thread's own elements are those of the scalar
+// kernel applied to elements 2i, 2i + 1.
+#ifndef DGB_CG_UPD_VEC
+#define DGB_CG_UPD_VEC 1
+#endif
+__global__ void __launch_bounds__(kBlasThreads) k_cg_upd_part2(size_t n, const double* __restrict__ p,
+                                                               const double* __restrict__ q, double* __restrict__ x,
+                                                               double* __restrict__ r, const double* __restrict__ inv,
+                                                               double* __restrict__ z, double* __restrict__ partial,
+                                                               CgState* st, double* __restrict__ hist) {
+  if (st->done) return;
+  const double a = st->alpha;
+  double acc[2] = {0.0, 0.0};
+  const size_t n2 = n >> 1;
+  const double2* p2 = reinterpret_cast<const double2*>(p);
+  const double2* q2 = reinterpret_cast<const double2*>(q);
+  const double2* i2 = reinterpret_cast<const double2*>(inv);
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* r2 = reinterpret_cast<double2*>(r);
+  double2* z2 = reinterpret_cast<double2*>(z);
+  GRID_STRIDE(i, n2) {
+    const double2 pv = p2[i], qv = q2[i], iv = i2[i];
+    double2 xv = x2[i], rv = r2[i], zv;
+    xv.x = fma(a, pv.x, xv.x);
+    xv.y = fma(a, pv.y, xv.y);
+    rv.x = fma(-a, qv.x, rv.x);
+    rv.y = fma(-a, qv.y, rv.y);
+    zv.x = rv.x * iv.x;
+    zv.y = rv.y * iv.y;
+    x2[i] = xv;
+    r2[i] = rv;
+    z2[i] = zv;
+    acc[0] = fma(rv.x, rv.x, acc[0]);
+    acc[1] = fma(rv.x, zv.x, acc[1]);
+    acc[0] = fma(rv.y, rv.y, acc[0]);
+    acc[1] = fma(rv.y, zv.y, acc[1]);
+  }
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const size_t i = n - 1;
+    x[i] = fma(a, p[i], x[i]);
+    const double ri = fma(-a, q[i], r[i]);
+    r[i] = ri;
+    const double zi = ri * inv[i];
     z[i] = zi;
     acc[0] = fma(ri, ri, acc[0]);
     acc[1] = fma(ri, zi, acc[1]);
@@ -422,7 +491,10 @@ cudaError_t cg_begin(cudaStream_t s, size_t n, const double* r, const double* in
   return cudaGetLastError();
 }
 cudaError_t cg_direction(cudaStream_t s, size_t n, const double* z, double* p, const CgState* st) {
-  k_cg_dir<<<blas_grid(n), kBlasThreads, 0, s>>>(n, z, p, st);
+  if ((((uintptr_t)z | (uintptr_t)p) & 15) == 0)
+    k_cg_dir2<<<blas_grid(n), kBlasThreads, 0, s>>>(n, z, p, st);
+  else
+    k_cg_dir<<<blas_grid(n), kBlasThreads, 0, s>>>(n, z, p, st);
   return cudaGetLastError();
 }
 cudaError_t cg_alpha(cudaStream_t s, size_t n, const double* p, const double* q, double* scratch, CgState* st) {
@@ -437,7 +509,11 @@ cudaError_t cg_alpha_from_partials(cudaStream_t s, int nparts, double* partial, 
 cudaError_t cg_update(cudaStream_t s, size_t n, const double* p, const double* q, double* x, double* r,
                       const double* inv, double* z, double* scratch, CgState* st, double* hist) {
   const int g = blas_grid(n);
-  k_cg_upd_part<<<g, kBlasThreads, 0, s>>>(n, p, q, x, r, inv, z, scratch, st, hist);  // last block finishes
+  const uintptr_t al = (uintptr_t)p | (uintptr_t)q | (uintptr_t)x | (uintptr_t)r | (uintptr_t)inv | (uintptr_t)z;
+  if (DGB_CG_UPD_VEC && inv && (al & 15) == 0)
+    k_cg_upd_part2<<<g, kBlasThreads, 0, s>>>(n, p, q, x, r, inv, z, scratch, st, hist);
+  else
+    k_cg_upd_part<<<g, kBlasThreads, 0, s>>>(n, p, q, x, r, inv, z, scratch, st, hist);  // last block finishes
   return cudaGetLastError();
 }
 static int gs_grid(size_t n) {
