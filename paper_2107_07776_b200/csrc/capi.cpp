@@ -633,7 +633,8 @@ extern "C" int dgb_host_tables(int n, int q, double* B, double* D, double* dE, d
 // generic kernels (0).  Both are parity-tested against the reference.
 extern "C" int dgb_set_fast_path(dgb_ctx* h, int enable) {
   NEED(h, "null ctx");
-  h->c.use_fast = enable != 0 && !h->c.hang_;  // hanging meshes run the generic kernels + hang.cu
+  // refined meshes: the fast kernels only where their cells are axis-aligned (hang_fast_ok)
+  h->c.use_fast = enable != 0 && (!h->c.hang_ || h->c.hang_fast_ok);
   return DGB_OK;
 }
 // 1: axis-aligned fast kernels (fast_axis.cuh), 2: deformed 3D fast kernels (fast_deformed.cuh), 0: generic

@@ -296,10 +296,12 @@ int Context::init(HostMesh&& m, int ku_, int kp_, int device_, std::string& e) {
       }
     }
   }
-  // hanging faces: the generic kernels (zero-weight slots) + the subface supplement
+  // hanging faces: the element-centric kernels see zero-weight slots (the line-split fast
+  // kernels on axis-aligned refined meshes: face type 3; otherwise the generic kernels)
+  // + the subface supplement (hang.cu)
   if (mesh.n_hang() > 0) {
-    use_fast = false;
-    dc.axis = dc.axis2 = false;
+    hang_fast_ok = mesh.affine && (dc.axis || dc.axis2);
+    use_fast = hang_fast_ok;
     dc.ug = UniformGrid();
     hang_ = hang_setup(mesh, ku, kp, e);
     if (!hang_) {
@@ -351,15 +353,17 @@ int Context::momentum(const double* coefs, const double* w, const double* x, dou
   const MomCoef co{coefs[0], coefs[1], coefs[2], coefs[3]};
   if ((co.adv != 0.0 || co.skew != 0.0) && !w) return fail(DGB_E_MISSING_FIELD, "apply_momentum: advecting field missing");
   ++launches;
+  bool done = false;
   if (use_fast && (dc.axis || !dc.affine)) {
     const cudaError_t e = dc.axis ? fast_momentum3(dc, co, w, x, y) : fast_momentum3_qp(dc, co, w, x, y);
     if (e != cudaErrorNotSupported) {
       CK(e);
-      return DGB_OK;
+      done = true;
+    } else {
+      cudaGetLastError();
     }
-    cudaGetLastError();
   }
-  CK(opu->momentum(dc, co, w, x, y));
+  if (!done) CK(opu->momentum(dc, co, w, x, y));
   if (hang_) {
     launches += 2;
     CK(hang_momentum(dc.stream, hang_, co, w, x, y));
@@ -371,15 +375,17 @@ int Context::momentum_diag(const double* coefs, const double* w, double* d) {
   if ((co.adv != 0.0 || co.skew != 0.0) && !w)
     return fail(DGB_E_MISSING_FIELD, "momentum_diagonal: advecting field missing");
   ++launches;
+  bool done = false;
   if (use_fast && (dc.axis || !dc.affine)) {
     const cudaError_t e = dc.axis ? fast_momentum_diag3(dc, co, w, d) : fast_momentum_diag3_qp(dc, co, w, d);
     if (e != cudaErrorNotSupported) {
       CK(e);
-      return DGB_OK;
+      done = true;
+    } else {
+      cudaGetLastError();
     }
-    cudaGetLastError();
   }
-  CK(opu->momentum_diag(dc, co, w, d));
+  if (!done) CK(opu->momentum_diag(dc, co, w, d));
   if (hang_) {
     launches += 2;
     CK(hang_momentum_diag(dc.stream, hang_, co, w, d));
@@ -388,16 +394,18 @@ int Context::momentum_diag(const double* coefs, const double* w, double* d) {
 }
 int Context::sip(double mc, int dir, const double* x, double* y) {
   ++launches;
+  bool done = false;
   if (use_fast && (dc.axis || dc.axis2 || !dc.affine)) {
     const cudaError_t e = dc.axis2 ? fast_sip2(dc, mc, dir, x, y)
                                    : (dc.axis ? fast_sip3(dc, mc, dir, x, y) : fast_sip3_qp(dc, mc, dir, x, y));
     if (e != cudaErrorNotSupported) {
       CK(e);
-      return DGB_OK;
+      done = true;
+    } else {
+      cudaGetLastError();
     }
-    cudaGetLastError();
   }
-  CK(opp->sip(dc, mc, dir, x, y));
+  if (!done) CK(opp->sip(dc, mc, dir, x, y));
   if (hang_) {
     launches += 2;
     CK(hang_sip(dc.stream, hang_, x, y));
@@ -480,22 +488,26 @@ int Context::apply_host(bool mom, const double* coefs, double mc, const double* 
 }
 int Context::sip_diag(double mc, int dir, double* d) {
   ++launches;
+  bool done = false;
   if (use_fast && dc.axis) {
     const cudaError_t e = fast_sip_diag3(dc, mc, dir, d);
     if (e != cudaErrorNotSupported) {
       CK(e);
-      return DGB_OK;
+      done = true;
+    } else {
+      cudaGetLastError();
     }
   }
-  if (use_fast && !dc.affine && dim == 3) {
+  if (!done && use_fast && !dc.affine && dim == 3) {
     const cudaError_t e = fast_sip_diag3_qp(dc, mc, dir, d);
     if (e != cudaErrorNotSupported) {
       CK(e);
-      return DGB_OK;
+      done = true;
+    } else {
+      cudaGetLastError();
     }
-    cudaGetLastError();
   }
-  CK(opp->sip_diag(dc, mc, dir, d));
+  if (!done) CK(opp->sip_diag(dc, mc, dir, d));
   if (hang_) {
     launches += 2;
     CK(hang_sip_diag(dc.stream, hang_, d));
@@ -568,6 +580,10 @@ int Context::rhs(const dgb_rhs_desc& ds, double* y) {
     const cudaError_t e = fast_rhs3(dc, ra, y, ptmp);
     if (e == cudaSuccess) {
       launches += 2 + ra.na + (ra.np > 0 ? ra.np + 1 : 0);
+      if (hang_) {  // refined axis-aligned mesh: the subface terms on top of the fast launches
+        launches += 2;
+        CK(hang_rhs(dc.stream, hang_, ra, y));
+      }
       return DGB_OK;
     }
     if (e != cudaErrorNotSupported) return cuda_fail(e, "momentum_rhs");
@@ -592,15 +608,17 @@ int Context::rhs(const dgb_rhs_desc& ds, double* y) {
 }
 int Context::divergence(const double* u, double* y) {
   ++launches;
+  bool done = false;
   if (use_fast && (dc.axis || (!dc.affine && dim == 3))) {
     const cudaError_t e = dc.axis ? fast_divergence3(dc, u, y) : fast_divergence3_qp(dc, u, y);
     if (e != cudaErrorNotSupported) {
       CK(e);
-      return DGB_OK;
+      done = true;
+    } else {
+      cudaGetLastError();
     }
-    cudaGetLastError();
   }
-  CK(opu->divergence(dc, u, y));
+  if (!done) CK(opu->divergence(dc, u, y));
   if (hang_) {
     launches += 2;
     CK(hang_divergence(dc.stream, hang_, u, y));
@@ -782,7 +800,7 @@ int Context::cg(const dgb_operator& op, const dgb_solver_settings& s, const doub
     dc.mesh.skip = &d_cg_->done;
     ScopeExit reset_skip([this] { dc.mesh.skip = nullptr; });  // also on early returns
     // scalar SIP operators on axis-aligned meshes: <p, q> fused into the apply's epilogue
-    const bool fused = use_fast && dc.axis && (op.op == DGB_OP_PRESSURE || op.op == DGB_OP_LAPLACE) &&
+    const bool fused = use_fast && dc.axis && !hang_ && (op.op == DGB_OP_PRESSURE || op.op == DGB_OP_LAPLACE) &&
                        fast_sip3_cg_blocks(dc) > 0;
     const int fblocks = fused ? fast_sip3_cg_blocks(dc) : 0;
     double* fpart = fused ? scratch_vec(25, fblocks + 64) : nullptr;  // + the second-level partials

@@ -37,6 +37,7 @@ class Context {
   int bctype_h[64] = {};
   long long launches = 0;
   bool use_fast = true;  // route axis-aligned 3D applies to fast_axis.cuh
+  bool hang_fast_ok = false;  // refined mesh whose cells are all axis-aligned boxes: fast kernels + hang.cu
   HangState* hang_ = nullptr;  // hanging-subface supplement (refined meshes; hang.cu), else null
 
   ~Context();

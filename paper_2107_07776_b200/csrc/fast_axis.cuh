@@ -82,7 +82,8 @@ struct CellInfo {
   double pen[6];   // (deg+1)^2 * penalty ratio (interior mean / boundary own)
   double ihn[6];   // neighbour's 1/h_d across each face
   int nb[6];       // neighbour cell, or -1 - boundary id
-  int type[6];     // 0 interior, 1 dirichlet, 2 outlet
+  int type[6];     // 0 interior, 1 dirichlet, 2 outlet, 3 hanging slot (zero weight: the (cell, face)
+                   // slot of a 1-irregular refined mesh, nbr = the cell itself; hang.cu adds its subfaces)
   // branch-free SIP face terms (see face_coefs):  F = cgs gs + cgo go + cus us + cuo uo,
   // GT = gus us + guo uo  (gs / go: own / neighbour reference normal derivative)
   double fc[6][6];
@@ -104,7 +105,7 @@ __device__ __forceinline__ void load_info(CellInfo& ci, const MeshArgs& m, const
     ci.nb[f] = nb;
     ci.pen[f] = sfac * m.pen[(size_t)cell * 6 + f];
     if (nb >= 0) {
-      ci.type[f] = 0;
+      ci.type[f] = nb == cell ? 3 : 0;
       ci.ihn[f] = __ldg(aff + (size_t)nb * kAffStride3 + 4 * (f >> 1));
     } else {
       const int bid = -1 - nb;
@@ -193,6 +194,7 @@ __device__ __forceinline__ void load_info_par(double* base, int per, int off, in
       double ihn = 0.0;
       if (nb >= 0) {
         ihn = __ldg(aff + (size_t)nb * kAffStride3 + 4 * (f >> 1));
+        if (nb == cell) ty = 3;  // hanging slot
       } else {
         const int bid = -1 - nb;
         ty = (bid >= 0 && bid < 64 && m.bctype[bid] == 1) ? 2 : 1;
@@ -226,7 +228,7 @@ __device__ __forceinline__ void face_coefs(CellInfo& ci, int f, bool dirichlet, 
       c[4] = -0.5;
       c[5] = 0.5;
     }
-  } else if (dirichlet && !(ty == 2 && outlet_natural)) {
+  } else if (ty != 3 && dirichlet && !(ty == 2 && outlet_natural)) {
     c[0] = sg * ih;
     if (!consistency_only) {
       c[2] = 2.0 * ci.pen[f];
@@ -379,7 +381,7 @@ __global__ void __launch_bounds__(128) k_sip_axis2(MeshArgs m, const double* __r
       ci.nb[f] = nb;
       ci.pen[f] = sfac * m.pen[(size_t)cell * 4 + f];
       if (nb >= 0) {
-        ci.type[f] = 0;
+        ci.type[f] = nb == cell ? 3 : 0;  // 3: hanging slot (zero weight)
         ci.ihn[f] = __ldg(aff + (size_t)nb * kAffStride2 + 3 * (f >> 1));
       } else {
         ci.type[f] = 1;  // the scalar operator treats every boundary id alike (walls / natural)
@@ -1481,7 +1483,7 @@ __global__ void __launch_bounds__(TH, K == 2 ? DGB_MOM_MINB2 : DGB_MOM_MINB) k_m
           for (int l = 0; l < N; ++l) acc = fma(tq.B[qq][l], v[fl][l], acc);
           val[fl] = acc;
         }
-        const double wq = wbase * tq.w[qq];
+        const double wq = ty == 3 ? 0.0 : wbase * tq.w[qq];  // hanging slot: zero surface weight
         const double wns = sgn * val[6];
         double fl3[3];
         if (ty == 0) {  // forms.cpp:555-573
@@ -2083,7 +2085,8 @@ __global__ void __launch_bounds__(MomDiagCfg<K>::T) k_momentum_diag_axis(MeshArg
           wo = fma(tq.B[qq][q], vo[q], wo);
         }
         const double wns = sgn * ws, wno = sgn * wo;
-        const double cf = ty == 0 ? 0.5 * wns + 0.5 * fmax(fabs(wns), fabs(wno)) : (ty == 2 ? wns : fabs(wns));
+        const double cf = ty == 0 ? 0.5 * wns + 0.5 * fmax(fabs(wns), fabs(wno))
+                                  : (ty == 3 ? 0.0 : (ty == 2 ? wns : fabs(wns)));  // 3: hanging slot
 #pragma unroll
         for (int b = 0; b < N; ++b) g[b] = fma(tq.w[qq] * tq.B[qq][b] * tq.B[qq][b], cf, g[b]);
       }

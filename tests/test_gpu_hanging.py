@@ -27,7 +27,10 @@ def hpair(ref, gpu, dim, n_el, ku, kp, refine, amp=0.0, seed=7, dirichlet_seed=N
     assert (R.n_u, R.n_p, R.ncells, R.n_interior, R.n_boundary) == (D.n_u, D.n_p, D.ncells, D.n_interior,
                                                                      D.n_boundary)
     assert D.n_hanging == R.n_hanging
-    assert not D.fast_path_active
+    # 3D refined meshes whose cells are all axis-aligned boxes run the line-split fast kernels
+    # (hanging slots = zero-weight face type) + the subface supplement; everything else the
+    # generic kernels + the supplement
+    assert D.fast_path_active == (1 if dim == 3 and amp == 0.0 else 0)
     if outlet is not None:
         R.set_bc(outlet, 1)
         D.set_boundary_type(outlet, gpu.BC_OUTLET)
@@ -52,6 +55,7 @@ CASES = [
     (3, 2, 2, 1, [0], 0.0),
     (3, 3, 3, 2, [13], 0.0),       # centre cell: six coarse faces with four subfaces each
     (3, 3, 2, 1, [0, 26], 0.04),
+    (3, 4, 3, 2, [0, 21, 22, 42, 63], 0.0),  # fine cells next to each other, at corners and inside
 ]
 IDS = [f"d{c[0]}n{c[1]}k{c[2]}{c[3]}r{len(c[4])}a{c[5]}" for c in CASES]
 
@@ -238,3 +242,34 @@ def test_bad_hanging_records_rejected(ref, gpu):
         gpu.DGContext(2, 0, 2, 1, mesh_arrays=(xv, cv, bid, rec, emb[hang]))
     with pytest.raises(gpu.DGBError):  # subfaces left out: unmatched interior faces
         gpu.DGContext(2, 0, 2, 1, mesh_arrays=(xv, cv, bid))
+
+
+@pytest.mark.parametrize("n_el,ku,kp,refine", [(3, 2, 1, [0, 13]), (4, 3, 2, [0, 21, 22, 42, 63])])
+def test_fast_kernels_match_generic_on_refined_mesh(ref, gpu, n_el, ku, kp, refine):
+    """Axis-aligned refined meshes: the line-split fast kernels (hanging slots as the
+    zero-weight face type 3) + hang.cu against the generic kernels + hang.cu, every
+    face-carrying operator, with an outlet and Dirichlet data."""
+    R, D = hpair(ref, gpu, 3, n_el, ku, kp, refine, 0.0, dirichlet_seed=5, outlet=1)
+    w, x, un = (gpu.seeded_uniform(s, R.n_u) for s in (51, 52, 53))
+    p = gpu.seeded_uniform(54, R.n_p)
+    dw, dx, dun, dp = dev(w), dev(x), dev(un), dev(p)
+    ctx = gpu.MomentumCtx(1.0 / (0.2929 * 1e-3), 0.005, 0.5, 0.0, advecting=dw)
+    spec = gpu.MomentumRhs(mass=[(2.9, dun)], visc=[(0.65, dun)], adv=[(0.5, dun, dw)], pres=[(1.0, dp)],
+                           dir_visc_coef=0.65, dir_adv_coef=0.5, dir_w=dw)
+    out = {}
+    for fast in (True, False):
+        D.set_fast_path(fast)
+        assert D.fast_path_active == (1 if fast else 0)
+        r = []
+        y = D.zeros(); gpu.apply_momentum(D, ctx, dx, y); r.append(host(y))
+        y = D.zeros(); gpu.momentum_diagonal(D, ctx, y); r.append(host(y))
+        y = D.zeros(gpu.SPACE_P); gpu.apply_pressure_helmholtz(D, 2.3, dp, y); r.append(host(y))
+        y = D.zeros(gpu.SPACE_P); gpu.helmholtz_diagonal(D, 2.3, y); r.append(host(y))
+        y = D.zeros(gpu.SPACE_P); gpu.apply_scalar_laplace(D, True, dp, y); r.append(host(y))
+        y = D.zeros(gpu.SPACE_P); gpu.scalar_laplace_diagonal(D, True, y); r.append(host(y))
+        y = D.zeros(gpu.SPACE_P); gpu.divergence_functional(D, dx, y); r.append(host(y))
+        y = D.zeros(); gpu.momentum_rhs(D, spec, y); r.append(host(y))
+        out[fast] = r
+    D.set_fast_path(True)
+    for a, b in zip(out[True], out[False]):
+        assert rel(a, b) <= TOL_APPLY
