@@ -299,6 +299,9 @@ int dgb_fp64_peak(dgb_ctx* ctx, double* tflops);
  * 1 = axis-aligned (fast_axis.cuh), 2 = deformed (fast_deformed.cuh), 0 = generic only. */
 int dgb_set_fast_path(dgb_ctx* ctx, int enable);
 int dgb_fast_path_active(dgb_ctx* ctx);
+/* Subface kernels of a refined mesh (hang.cu): 0 = no hanging faces, 1 = dense embedded-point
+ * tables (any dim / geometry), 2 = sum-factorised (3D, every subface between axis-aligned boxes). */
+int dgb_hanging_mode(dgb_ctx* ctx);
 /* number of device kernels this context launched so far */
 long long dgb_launch_count(dgb_ctx* ctx);
 

@@ -163,6 +163,7 @@ def lib() -> C.CDLL:
     L.dgb_host_tables.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _dp]
     L.dgb_set_fast_path.argtypes = [C.c_void_p, C.c_int]
     L.dgb_fast_path_active.argtypes = [C.c_void_p]
+    L.dgb_hanging_mode.argtypes = [C.c_void_p]
     _lib = L
     return L
 
@@ -322,6 +323,11 @@ class DGContext:
     @property
     def fast_path_active(self) -> bool:
         return bool(lib().dgb_fast_path_active(self._h))
+
+    @property
+    def hanging_mode(self) -> int:
+        """0: conforming mesh, 1: dense-table subface kernels, 2: sum-factorised (axis-aligned 3D)."""
+        return int(lib().dgb_hanging_mode(self._h))
 
     def launch_count(self) -> int:
         return int(lib().dgb_launch_count(self._h))

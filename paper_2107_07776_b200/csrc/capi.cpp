@@ -637,6 +637,7 @@ extern "C" int dgb_set_fast_path(dgb_ctx* h, int enable) {
   h->c.use_fast = enable != 0 && (!h->c.hang_ || h->c.hang_fast_ok);
   return DGB_OK;
 }
+extern "C" int dgb_hanging_mode(dgb_ctx* h) { return h ? dgb::hang_mode(h->c.hang_) : 0; }
 // 1: axis-aligned fast kernels (fast_axis.cuh), 2: deformed 3D fast kernels (fast_deformed.cuh), 0: generic
 extern "C" int dgb_fast_path_active(dgb_ctx* h) {
   if (!h || !h->c.use_fast || h->c.dim != 3) return 0;

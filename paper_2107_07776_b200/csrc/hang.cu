@@ -17,6 +17,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <vector>
@@ -454,6 +455,292 @@ __global__ void __launch_bounds__(kThr) k_hang_rhs(HangDev H, RhsArgs ra) {
   hstore<DIM>(H, S, h, DIM * nb);
 }
 
+// ------------------------------------------------------------------ axis-aligned 3D subfaces (sum-factorised)
+// Refined meshes whose cells are all axis-aligned boxes (the line-split fast kernels'
+// meshes): the face normal is +-e_a, so only the trace and the reference normal
+// derivative of both sides enter, the subface is the whole fine face, and its embedding
+// into the coarse face is an offset (0 or 1/2 per tangential axis) + a scaling by 1/2.
+// The dense embedded-point tables collapse to 1D tables (fine side: the basis at the
+// Gauss points; coarse side: the basis at o + xi / 2) applied along the two tangential
+// axes: ~6 k FMA per momentum subface instead of ~100 k, no table streaming.  Both sides'
+// integrands differ by a sign only (normal out of the side doing the work), so each
+// integrand field is evaluated once and tested through each side's own tables.
+// One thread per (subface, component) for the momentum apply, per subface for the
+// scalar SIP apply; same per-(subface, side) contribution blocks + k_hang_scatter.
+template <int N, int Q>
+struct HAxTab {
+  double B[3][Q][N];  // basis at the Gauss points xi, at xi / 2, at 1/2 + xi / 2
+  double w[Q];
+  double dE[2][N];    // basis derivatives at 0, 1
+};
+struct HAxDev {
+  const int4* rec = nullptr;     // fine cell, coarse cell, code = a | s_f << 2 | o_p << 3 | o_q << 4, unused
+  const double4* geo = nullptr;  // 1/h_a fine, 1/h_a coarse, |fine face|, mean |F|/|K|
+  const double* tab[3] = {};     // HAxTab<Nu, Nu>, HAxTab<Nu, Nu + 1>, HAxTab<Np, Np + 1>
+};
+
+template <int N>
+__device__ __forceinline__ void hax_strides(int a, int& sl, int& sp, int& sq) {
+  sl = a == 0 ? 1 : (a == 1 ? N : N * N);
+  sp = a == 0 ? N : 1;
+  sq = a == 2 ? N : N * N;
+}
+template <class T>
+__device__ __forceinline__ const T& hax_load_tab(double* sm, const double* __restrict__ g) {
+  for (int i = threadIdx.x; i < (int)(sizeof(T) / sizeof(double)); i += blockDim.x) sm[i] = g[i];
+  __syncthreads();
+  return *reinterpret_cast<const T*>(sm);
+}
+// face-layer values t[p + N q] and reference normal derivatives g[p + N q] on face (a, s)
+template <int N>
+__device__ __forceinline__ void hax_face(const double* __restrict__ u, int a, int s, const double* dEs, double* t,
+                                         double* g) {
+  int sl, sp, sq;
+  hax_strides<N>(a, sl, sp, sq);
+  const int L = s ? N - 1 : 0;
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      const double* b = u + p * sp + q * sq;
+      double gg = 0.0, tt = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        const double v = b[l * sl];
+        gg = fma(dEs[l], v, gg);
+        tt = l == L ? v : tt;
+      }
+      t[p + N * q] = tt;
+      g[p + N * q] = gg;
+    }
+}
+template <int N>
+__device__ __forceinline__ void hax_trace(const double* __restrict__ u, int a, int s, double* t) {
+  int sl, sp, sq;
+  hax_strides<N>(a, sl, sp, sq);
+  const double* b = u + (s ? N - 1 : 0) * sl;
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+#pragma unroll
+    for (int p = 0; p < N; ++p) t[p + N * q] = b[p * sp + q * sq];
+}
+// out[tp + Q tq] += sgn sum_{p, q} Bp[tp][p] Bq[tq][q] f[p + N q]
+template <int N, int Q>
+__device__ __forceinline__ void hax_interp(const double (*Bp)[N], const double (*Bq)[N], const double* f, double sgn,
+                                           double* out) {
+#pragma unroll
+  for (int tq = 0; tq < Q; ++tq) {
+    double r[N];
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      double a = 0.0;
+#pragma unroll
+      for (int q = 0; q < N; ++q) a = fma(Bq[tq][q], f[p + N * q], a);
+      r[p] = sgn * a;
+    }
+#pragma unroll
+    for (int tp = 0; tp < Q; ++tp) {
+      double a = out[tp + Q * tq];
+#pragma unroll
+      for (int p = 0; p < N; ++p) a = fma(Bp[tp][p], r[p], a);
+      out[tp + Q * tq] = a;
+    }
+  }
+}
+// out[p + N q] = sum_{tp, tq} Bp[tp][p] Bq[tq][q] F[tp + Q tq]
+template <int N, int Q>
+__device__ __forceinline__ void hax_back(const double (*Bp)[N], const double (*Bq)[N], const double* F, double* out) {
+#pragma unroll
+  for (int i = 0; i < N * N; ++i) out[i] = 0.0;
+#pragma unroll
+  for (int tq = 0; tq < Q; ++tq) {
+    double z[N];
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      double a = 0.0;
+#pragma unroll
+      for (int tp = 0; tp < Q; ++tp) a = fma(Bp[tp][p], F[tp + Q * tq], a);
+      z[p] = a;
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+      for (int p = 0; p < N; ++p) out[p + N * q] = fma(Bq[tq][q], z[p], out[p + N * q]);
+  }
+}
+// The SIP face terms of one scalar field across one subface (forms.cpp:179-242 /
+// :443-461 with n = +-e_a): writes both sides' contribution blocks
+//   fine:   V_f (value test, face layer) + dE G_f (normal-derivative test)
+//   coarse: the same through the embedded tables, V_c = -I_c^T F
+template <int N, int Q>
+__device__ __forceinline__ void hax_sip_field(const HAxTab<N, Q>& T, int code, double4 ge, double C, double scale,
+                                              const double* __restrict__ uf, const double* __restrict__ uc,
+                                              double* __restrict__ of, double* __restrict__ oc) {
+  const int a = code & 3, sf = (code >> 2) & 1, op = (code >> 3) & 1, oq = (code >> 4) & 1;
+  const double sg = sf ? 1.0 : -1.0, ihf = ge.x, ihc = ge.y, area = ge.z;
+  const double (*B0)[N] = T.B[0];
+  const double (*Bp)[N] = T.B[1 + op];
+  const double (*Bq)[N] = T.B[1 + oq];
+  double F[Q * Q], J[Q * Q];
+#pragma unroll
+  for (int i = 0; i < Q * Q; ++i) F[i] = J[i] = 0.0;
+  {
+    double t[N * N], g[N * N];
+    hax_face<N>(uf, a, sf, T.dE[sf], t, g);
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) g[i] = fma(-0.5 * sg * ihf, g[i], C * t[i]);
+    hax_interp<N, Q>(B0, B0, g, 1.0, F);
+    hax_interp<N, Q>(B0, B0, t, 1.0, J);
+    hax_face<N>(uc, a, 1 - sf, T.dE[1 - sf], t, g);
+#pragma unroll
+    for (int i = 0; i < N * N; ++i) g[i] = fma(-0.5 * sg * ihc, g[i], -C * t[i]);
+    hax_interp<N, Q>(Bp, Bq, g, 1.0, F);
+    hax_interp<N, Q>(Bp, Bq, t, -1.0, J);
+  }
+#pragma unroll
+  for (int tq = 0; tq < Q; ++tq)
+#pragma unroll
+    for (int tp = 0; tp < Q; ++tp) {
+      const double wds = scale * area * T.w[tp] * T.w[tq];
+      F[tp + Q * tq] *= wds;
+      J[tp + Q * tq] *= -0.5 * wds;
+    }
+  int sl, sp, sq;
+  hax_strides<N>(a, sl, sp, sq);
+  double V[N * N], G[N * N];
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    hax_back<N, Q>(side ? Bp : B0, side ? Bq : B0, F, V);
+    hax_back<N, Q>(side ? Bp : B0, side ? Bq : B0, J, G);
+    const int s = side ? 1 - sf : sf, L = s ? N - 1 : 0;
+    const double vs = side ? -1.0 : 1.0, gs = sg * (side ? ihc : ihf);
+    double* o = side ? oc : of;
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+      for (int p = 0; p < N; ++p)
+#pragma unroll
+        for (int l = 0; l < N; ++l)
+          o[l * sl + p * sp + q * sq] = fma(T.dE[s][l], gs * G[p + N * q], l == L ? vs * V[p + N * q] : 0.0);
+  }
+}
+
+constexpr int kAxThr = 64;
+
+template <int NP>
+__global__ void __launch_bounds__(kAxThr) k_hax_sip(HangDev H, HAxDev A, const double* __restrict__ x) {
+  constexpr int Q = NP + 1, NB = NP * NP * NP;
+  using T = HAxTab<NP, Q>;
+  __shared__ double stab[sizeof(T) / sizeof(double)];
+  const T& tab = hax_load_tab<T>(stab, A.tab[2]);
+  const int h = blockIdx.x * kAxThr + threadIdx.x;
+  if (h >= H.n) return;
+  const int4 rc = A.rec[h];
+  const double4 ge = A.geo[h];
+  hax_sip_field<NP, Q>(tab, rc.z, ge, H.sfp * ge.w, 1.0, x + (size_t)rc.x * NB, x + (size_t)rc.y * NB,
+                       H.contrib + (size_t)(2 * h) * NB, H.contrib + (size_t)(2 * h + 1) * NB);
+}
+
+template <int N>
+__global__ void __launch_bounds__(kAxThr) k_hax_momentum(HangDev H, HAxDev A, MomCoef co, const double* __restrict__ w,
+                                                         const double* __restrict__ x) {
+  constexpr int QA = N, QB = N + 1, NB = N * N * N, NF = N * N;
+  using TA = HAxTab<N, QA>;
+  using TB = HAxTab<N, QB>;
+  __shared__ double stab[(sizeof(TA) + sizeof(TB)) / sizeof(double)];
+  const TA& ta = hax_load_tab<TA>(stab, A.tab[0]);
+  const TB& tb = hax_load_tab<TB>(stab + sizeof(TA) / sizeof(double), A.tab[1]);
+  const int idx = blockIdx.x * kAxThr + threadIdx.x;
+  if (idx >= 3 * H.n) return;
+  const int h = idx / 3, comp = idx - 3 * h;
+  const int4 rc = A.rec[h];
+  const double4 ge = A.geo[h];
+  const int code = rc.z;
+  const double* uf = x + (size_t)rc.x * 3 * NB + comp * NB;
+  const double* uc = x + (size_t)rc.y * 3 * NB + comp * NB;
+  double* of = H.contrib + (size_t)(2 * h) * 3 * NB + comp * NB;
+  double* oc = H.contrib + (size_t)(2 * h + 1) * 3 * NB + comp * NB;
+  if (co.visc != 0.0) {  // forms.cpp:443-461
+    hax_sip_field<N, QA>(ta, code, ge, H.sfu * ge.w, co.visc, uf, uc, of, oc);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NB; ++i) of[i] = oc[i] = 0.0;
+  }
+  if (co.adv != 0.0) {  // forms.cpp:555-573 (Lax-Friedrichs), rule k+2
+    const int a = code & 3, sf = (code >> 2) & 1, op = (code >> 3) & 1, oq = (code >> 4) & 1;
+    const double sg = sf ? 1.0 : -1.0, area = ge.z;
+    const double (*B0)[N] = tb.B[0];
+    const double (*Bp)[N] = tb.B[1 + op];
+    const double (*Bq)[N] = tb.B[1 + oq];
+    double tf[NF], tc[NF], wf[NF], wc[NF], Vf[NF], Vc[NF];
+    hax_trace<N>(uf, a, sf, tf);
+    hax_trace<N>(uc, a, 1 - sf, tc);
+    hax_trace<N>(w + (size_t)rc.x * 3 * NB + a * NB, a, sf, wf);
+    hax_trace<N>(w + (size_t)rc.y * 3 * NB + a * NB, a, 1 - sf, wc);
+#pragma unroll
+    for (int i = 0; i < NF; ++i) Vf[i] = Vc[i] = 0.0;
+#pragma unroll
+    for (int tq = 0; tq < QB; ++tq) {
+      double ruf[N], rwf[N], ruc[N], rwc[N];
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          s0 = fma(B0[tq][q], tf[p + N * q], s0);
+          s1 = fma(B0[tq][q], wf[p + N * q], s1);
+          s2 = fma(Bq[tq][q], tc[p + N * q], s2);
+          s3 = fma(Bq[tq][q], wc[p + N * q], s3);
+        }
+        ruf[p] = s0;
+        rwf[p] = s1;
+        ruc[p] = s2;
+        rwc[p] = s3;
+      }
+      double I[QB];
+#pragma unroll
+      for (int tp = 0; tp < QB; ++tp) {
+        double us = 0.0, ws = 0.0, uo = 0.0, wo = 0.0;
+#pragma unroll
+        for (int p = 0; p < N; ++p) {
+          us = fma(B0[tp][p], ruf[p], us);
+          ws = fma(B0[tp][p], rwf[p], ws);
+          uo = fma(Bp[tp][p], ruc[p], uo);
+          wo = fma(Bp[tp][p], rwc[p], wo);
+        }
+        const double wn_s = sg * ws, wn_o = sg * wo;
+        const double lam = fmax(fabs(wn_s), fabs(wn_o));
+        I[tp] = co.adv * (0.5 * (us * wn_s + uo * wn_o) + 0.5 * lam * (us - uo)) * (area * tb.w[tp] * tb.w[tq]);
+      }
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        double zf = 0.0, zc = 0.0;
+#pragma unroll
+        for (int tp = 0; tp < QB; ++tp) {
+          zf = fma(B0[tp][p], I[tp], zf);
+          zc = fma(Bp[tp][p], I[tp], zc);
+        }
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          Vf[p + N * q] = fma(B0[tq][q], zf, Vf[p + N * q]);
+          Vc[p + N * q] = fma(-Bq[tq][q], zc, Vc[p + N * q]);
+        }
+      }
+    }
+    int sl, sp, sq;
+    hax_strides<N>(a, sl, sp, sq);
+    double* bf = of + (sf ? N - 1 : 0) * sl;
+    double* bc = oc + (sf ? 0 : N - 1) * sl;
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        bf[p * sp + q * sq] += Vf[p + N * q];
+        bc[p * sp + q * sq] += Vc[p + N * q];
+      }
+  }
+}
+
 // ------------------------------------------------------------------ deterministic scatter
 // y[cell][rep][blk] += sum of the cell's contribution blocks, in ascending (subface, side) order
 __global__ void __launch_bounds__(kThr) k_hang_scatter(HangDev H, int blk, int rep, double* __restrict__ y) {
@@ -469,8 +756,10 @@ __global__ void __launch_bounds__(kThr) k_hang_scatter(HangDev H, int blk, int r
 }  // namespace
 
 struct HangState {
-  int dim = 0;
+  int dim = 0, ku = 0, kp = 0;
   HangDev d;
+  bool axis = false;  // every subface joins two axis-aligned boxes: the sum-factorised kernels apply
+  HAxDev ax;
   std::vector<void*> allocs;
 };
 
@@ -522,6 +811,96 @@ T* upload(HangState* hs, const std::vector<T>& v) {
   if (!v.empty() && cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
     return nullptr;
   return static_cast<T*>(p);
+}
+}  // namespace
+
+namespace {
+template <int N, int Q>
+void fill_hax_tab(std::vector<double>& out) {
+  HAxTab<N, Q> t;
+  const std::vector<double> nodes = gauss_lobatto(N);
+  const Rule1D r = gauss_legendre(Q);
+  std::vector<double> val, der;
+  for (int k = 0; k < 3; ++k) {
+    std::vector<double> pts(Q);
+    for (int q = 0; q < Q; ++q) pts[q] = k == 0 ? r.x[q] : 0.5 * (k - 1) + 0.5 * r.x[q];
+    lagrange_tables(nodes, pts, val, der);
+    for (int q = 0; q < Q; ++q)
+      for (int j = 0; j < N; ++j) t.B[k][q][j] = val[(size_t)q * N + j];
+  }
+  for (int q = 0; q < Q; ++q) t.w[q] = r.w[q];
+  lagrange_tables(nodes, {0.0, 1.0}, val, der);
+  for (int e = 0; e < 2; ++e)
+    for (int j = 0; j < N; ++j) t.dE[e][j] = der[(size_t)e * N + j];
+  const double* p = reinterpret_cast<const double*>(&t);
+  out.assign(p, p + sizeof(t) / sizeof(double));
+}
+void fill_hax_tab(int N, int Q, std::vector<double>& out) {
+  if (Q == N) {
+    if (N == 2) return fill_hax_tab<2, 2>(out);
+    if (N == 3) return fill_hax_tab<3, 3>(out);
+    if (N == 4) return fill_hax_tab<4, 4>(out);
+    if (N == 5) return fill_hax_tab<5, 5>(out);
+  } else {
+    if (N == 2) return fill_hax_tab<2, 3>(out);
+    if (N == 3) return fill_hax_tab<3, 4>(out);
+    if (N == 4) return fill_hax_tab<4, 5>(out);
+    if (N == 5) return fill_hax_tab<5, 6>(out);
+  }
+  out.clear();
+}
+
+// Axis-aligned boxes on both sides of every subface, opposite faces of one axis, identity
+// orientation, embedding = offset {0, 1/2} + tangents e_p / 2, e_q / 2: the
+// sum-factorised subface kernels apply.  Anything else keeps the dense-table kernels.
+void hang_setup_axis(HangState* hs, const HostMesh& m, const std::vector<double>& pen) {
+  const int n = m.n_hang();
+  std::vector<int4> rec(n);
+  std::vector<double4> geo(n);
+  const double ref[3] = {0.5, 0.5, 0.5};
+  auto near = [](double a, double b) { return std::abs(a - b) <= 1e-12; };
+  for (int h = 0; h < n; ++h) {
+    const int K = m.hrec[4 * h], f = m.hrec[4 * h + 1], Nc = m.hrec[4 * h + 2], fc = m.hrec[4 * h + 3];
+    const int a = f / 2, sf = f % 2;
+    if (fc != (f ^ 1)) return;
+    double Jf[9], Jc[9];
+    jacobian(m, K, ref, Jf);
+    jacobian(m, Nc, ref, Jc);
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        if (i != j && (std::abs(Jf[3 * i + j]) > 1e-13 * std::abs(Jf[4 * i]) ||
+                       std::abs(Jc[3 * i + j]) > 1e-13 * std::abs(Jc[4 * i])))
+          return;
+    if (Jf[4 * a] <= 0.0 || Jc[4 * a] <= 0.0) return;
+    const double* e = &m.hemb[(size_t)h * 9];
+    const int tp = a == 0 ? 1 : 0, tq = a == 2 ? 1 : 2;
+    int o[2];
+    for (int k = 0; k < 2; ++k) {
+      const int ax = k == 0 ? tp : tq;
+      for (int d = 0; d < 3; ++d)
+        if (!near(e[3 + 3 * k + d], d == ax ? 0.5 : 0.0)) return;
+      if (near(e[ax], 0.0))
+        o[k] = 0;
+      else if (near(e[ax], 0.5))
+        o[k] = 1;
+      else
+        return;
+    }
+    if (!near(e[a], (double)(fc % 2))) return;
+    rec[h] = make_int4(K, Nc, a | (sf << 2) | (o[0] << 3) | (o[1] << 4), 0);
+    geo[h] = make_double4(1.0 / Jf[4 * a], 1.0 / Jc[4 * a], m.face_measure[(size_t)K * 6 + f], pen[h]);
+  }
+  std::vector<double> t0, t1, t2;
+  fill_hax_tab(hs->ku + 1, hs->ku + 1, t0);
+  fill_hax_tab(hs->ku + 1, hs->ku + 2, t1);
+  fill_hax_tab(hs->kp + 1, hs->kp + 2, t2);
+  if (t0.empty() || t1.empty() || t2.empty()) return;
+  hs->ax.rec = upload(hs, rec);
+  hs->ax.geo = upload(hs, geo);
+  hs->ax.tab[0] = upload(hs, t0);
+  hs->ax.tab[1] = upload(hs, t1);
+  hs->ax.tab[2] = upload(hs, t2);
+  hs->axis = hs->ax.rec && hs->ax.geo && hs->ax.tab[0] && hs->ax.tab[1] && hs->ax.tab[2];
 }
 }  // namespace
 
@@ -638,10 +1017,21 @@ HangState* hang_setup(const HostMesh& m, int ku, int kp, std::string& err) {
     hang_release(hs);
     return nullptr;
   }
+  hs->ku = ku;
+  hs->kp = kp;
+  if (dim == 3 && m.affine && ku >= 1 && ku <= 4 && kp >= 1 && kp <= 3) hang_setup_axis(hs, m, pen);
   return hs;
 }
 
 namespace {
+// DGB_HANG_AXIS=0 in the environment keeps the dense-table subface kernels (A/B, debugging)
+bool hang_axis_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("DGB_HANG_AXIS");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
 template <class K>
 cudaError_t hlaunch(cudaStream_t st, const HangState* h, K kern, size_t smem) {
   if (smem > 48 * 1024) {
@@ -655,6 +1045,8 @@ cudaError_t scatter(cudaStream_t st, const HangState* h, int blk, int rep, doubl
   return cudaGetLastError();
 }
 }  // namespace
+
+int hang_mode(const HangState* h) { return !h ? 0 : (h->axis && hang_axis_enabled() ? 2 : 1); }
 
 #define HANG_DIM_DISPATCH(KERN, BLK, ...)                                                         \
   do {                                                                                            \
@@ -677,6 +1069,18 @@ cudaError_t scatter(cudaStream_t st, const HangState* h, int blk, int rep, doubl
 cudaError_t hang_momentum(cudaStream_t st, const HangState* h, MomCoef co, const double* w, const double* x,
                           double* y) {
   if (!h || (co.visc == 0.0 && co.adv == 0.0)) return cudaSuccess;
+  if (h->axis && hang_axis_enabled()) {
+    const int grid = (3 * h->d.n + kAxThr - 1) / kAxThr;
+    switch (h->ku) {
+      case 1: k_hax_momentum<2><<<grid, kAxThr, 0, st>>>(h->d, h->ax, co, w, x); break;
+      case 2: k_hax_momentum<3><<<grid, kAxThr, 0, st>>>(h->d, h->ax, co, w, x); break;
+      case 3: k_hax_momentum<4><<<grid, kAxThr, 0, st>>>(h->d, h->ax, co, w, x); break;
+      default: k_hax_momentum<5><<<grid, kAxThr, 0, st>>>(h->d, h->ax, co, w, x); break;
+    }
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return scatter(st, h, 3 * h->d.nbu, 1, y);
+  }
   HANG_DIM_DISPATCH(k_hang_momentum, h->dim * h->d.nbu, co, w, x);
   return scatter(st, h, h->dim * h->d.nbu, 1, y);
 }
@@ -687,6 +1091,17 @@ cudaError_t hang_momentum_diag(cudaStream_t st, const HangState* h, MomCoef co, 
 }
 cudaError_t hang_sip(cudaStream_t st, const HangState* h, const double* x, double* y) {
   if (!h) return cudaSuccess;
+  if (h->axis && hang_axis_enabled()) {
+    const int grid = (h->d.n + kAxThr - 1) / kAxThr;
+    switch (h->kp) {
+      case 1: k_hax_sip<2><<<grid, kAxThr, 0, st>>>(h->d, h->ax, x); break;
+      case 2: k_hax_sip<3><<<grid, kAxThr, 0, st>>>(h->d, h->ax, x); break;
+      default: k_hax_sip<4><<<grid, kAxThr, 0, st>>>(h->d, h->ax, x); break;
+    }
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return scatter(st, h, h->d.nbp, 1, y);
+  }
   HANG_DIM_DISPATCH(k_hang_sip, h->d.nbp, x);
   return scatter(st, h, h->d.nbp, 1, y);
 }

@@ -35,6 +35,8 @@ struct HangState;
 /// Returns nullptr with err set on failure (m.n_hang() == 0: nullptr, err empty).
 HangState* hang_setup(const HostMesh& m, int ku, int kp, std::string& err);
 void hang_release(HangState* h);
+/// 0: none, 1: dense-table subface kernels, 2: sum-factorised axis-aligned subface kernels
+int hang_mode(const HangState* h);
 
 // y += the hanging-subface terms (launched after the element-centric kernel of the op)
 cudaError_t hang_momentum(cudaStream_t st, const HangState* h, MomCoef co, const double* w, const double* x,

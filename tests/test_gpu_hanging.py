@@ -31,6 +31,7 @@ def hpair(ref, gpu, dim, n_el, ku, kp, refine, amp=0.0, seed=7, dirichlet_seed=N
     # (hanging slots = zero-weight face type) + the subface supplement; everything else the
     # generic kernels + the supplement
     assert D.fast_path_active == (1 if dim == 3 and amp == 0.0 else 0)
+    assert D.hanging_mode == (2 if dim == 3 and amp == 0.0 else 1)
     if outlet is not None:
         R.set_bc(outlet, 1)
         D.set_boundary_type(outlet, gpu.BC_OUTLET)

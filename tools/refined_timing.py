@@ -59,4 +59,26 @@ for op, n in (("momentum", D.n_u), ("pressure", D.n_p)):
     tg, yg = res[(False, op)]
     out[op] = {"fast_ms": tf, "generic_ms": tg, "speedup": tg / tf, "fast_gdofs": n / tf / 1e6,
                "rel_l2_fast_vs_generic": float(np.linalg.norm(yf - yg) / np.linalg.norm(yg))}
+# one TR-BDF2 step (Dirichlet data = the synthetic field's trace, Re 1000, dt 1e-3, GMRES(30) / Jacobi-CG)
+if os.environ.get("STEP", "1") != "0":
+    f = dg.SynthField(3, 2)
+    for b in range(6):
+        D.set_dirichlet_fn(b, f.fn_ptr, f.user_ptr, 0.0)
+    u0 = D.zeros(); dg.interpolate_synth_device(D, f, u0)
+    p0 = D.zeros(dg.SPACE_P)
+    sp = dg.StepParams(dt=1e-3, Re=1000.0, c=1e3, restart=30, first_step=True)
+    out["trbdf2_step"] = {}
+    fields = {}
+    for fast in (True, False):
+        D.set_fast_path(fast)
+        u1, p1 = D.zeros(), D.zeros(dg.SPACE_P)
+        for rep in range(2):
+            torch.cuda.synchronize(); t0 = time.time()
+            its = dg.trbdf2_step(D, sp, u0, u0, p0, u1, p1)
+            torch.cuda.synchronize(); t = time.time() - t0
+        out["trbdf2_step"]["fast" if fast else "generic"] = {"s": t, "its": [int(i) for i in its]}
+        fields[fast] = (u1.cpu().numpy(), p1.cpu().numpy())
+    out["trbdf2_step"]["rel_l2_u_fast_vs_generic"] = float(
+        np.linalg.norm(fields[True][0] - fields[False][0]) / np.linalg.norm(fields[False][0]))
+    D.set_fast_path(True)
 print(json.dumps(out))
