@@ -57,6 +57,7 @@ CASES = [
     (3, 3, 3, 2, [13], 0.0),       # centre cell: six coarse faces with four subfaces each
     (3, 3, 2, 1, [0, 26], 0.04),
     (3, 4, 3, 2, [0, 21, 22, 42, 63], 0.0),  # fine cells next to each other, at corners and inside
+    (3, 2, 4, 3, [7], 0.0),        # degree 4 / 3: the N = 5 subface kernels
 ]
 IDS = [f"d{c[0]}n{c[1]}k{c[2]}{c[3]}r{len(c[4])}a{c[5]}" for c in CASES]
 
