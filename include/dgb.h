@@ -97,7 +97,8 @@ int dgb_set_dirichlet_time_dependent(dgb_ctx* ctx, int enable);
  * context (the rank's owned cells; the others are ghost cells whose values the halo
  * exchange supplies) and leave the other rows of the output untouched.  cell1 < 0 =
  * all cells (the default).  Other kernels (and the momentum apply at k = 4, which has
- * no axis-aligned fast kernel) compute every cell. */
+ * no axis-aligned fast kernel) compute every cell.  Meshes with hanging faces accept only
+ * the whole mesh (DGB_E_ARG otherwise): their subface kernels always cover every subface. */
 int dgb_set_cell_range(dgb_ctx* ctx, int cell0, int cell1);
 /* Debug switches.  DGB_DEBUG_POISON_SMEM: every operator kernel first fills its dynamic
  * shared memory with NaN, so a stage reading a value no earlier stage of the launch wrote

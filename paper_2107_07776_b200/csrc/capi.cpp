@@ -156,6 +156,9 @@ int dgb_set_cell_range(dgb_ctx* h, int cell0, int cell1) {
   DevGuard guard_(h);
   NEED(h, "null ctx");
   NEED(cell0 >= 0 && (cell1 < 0 || (cell1 >= cell0 && cell1 <= h->c.mesh.ncells)), "bad cell range");
+  // refined meshes: the subface kernels always cover every hanging face, so only the whole mesh
+  NEED(!h->c.hang_ || (cell0 == 0 && (cell1 < 0 || cell1 == h->c.mesh.ncells)),
+       "cell ranges are not defined on meshes with hanging faces");
   h->c.dc.mesh.cell0 = cell0;
   h->c.dc.mesh.cell1 = cell1;
   return DGB_OK;

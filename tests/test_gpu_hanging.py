@@ -234,6 +234,14 @@ def test_trbdf2_steps_on_refined_mesh(ref, gpu, dim, n_el, ku, kp, refine, steps
     assert rel(hp - hp.mean(), p - p.mean()) <= TOL_FIELD
 
 
+def test_cell_range_rejected_on_refined_mesh(ref, gpu):
+    """The subface kernels always cover every hanging face: owned-cell ranges (z-slabs) are only
+    defined on conforming meshes."""
+    R, D = hpair(ref, gpu, 3, 2, 2, 1, [0])
+    assert gpu.lib().dgb_set_cell_range(D.handle, 0, 4) != 0
+    assert gpu.lib().dgb_set_cell_range(D.handle, 0, -1) == 0
+
+
 def test_bad_hanging_records_rejected(ref, gpu):
     R = ref.RefCtx.refined(2, 2, 2, 1, [0])
     xv, cv, bid, it, emb = R.mesh_arrays()
