@@ -1483,7 +1483,9 @@ __global__ void __launch_bounds__(TH, K == 2 ? DGB_MOM_MINB2 : DGB_MOM_MINB) k_m
           for (int l = 0; l < N; ++l) acc = fma(tq.B[qq][l], v[fl][l], acc);
           val[fl] = acc;
         }
-        const double wq = ty == 3 ? 0.0 : wbase * tq.w[qq];  // hanging slot: zero surface weight
+        // hanging slot (mesh-table variant only: uniform grids have none; the select costs the
+        // K = 2 uniform kernel 1.8 % at cfg5): zero surface weight
+        const double wq = (!UNI && ty == 3) ? 0.0 : wbase * tq.w[qq];
         const double wns = sgn * val[6];
         double fl3[3];
         if (ty == 0) {  // forms.cpp:555-573
@@ -2086,7 +2088,7 @@ __global__ void __launch_bounds__(MomDiagCfg<K>::T) k_momentum_diag_axis(MeshArg
         }
         const double wns = sgn * ws, wno = sgn * wo;
         const double cf = ty == 0 ? 0.5 * wns + 0.5 * fmax(fabs(wns), fabs(wno))
-                                  : (ty == 3 ? 0.0 : (ty == 2 ? wns : fabs(wns)));  // 3: hanging slot
+                                  : ((!UNI && ty == 3) ? 0.0 : (ty == 2 ? wns : fabs(wns)));  // 3: hanging slot
 #pragma unroll
         for (int b = 0; b < N; ++b) g[b] = fma(tq.w[qq] * tq.B[qq][b] * tq.B[qq][b], cf, g[b]);
       }
