@@ -397,7 +397,9 @@ def run_device(args):
     yp = D.zeros(dg.SPACE_P)
     ctx = dg.MomentumCtx(*mom, advecting=w)
     setup_s = time.time() - t0
-    peak_fp64 = dg.fp64_peak_tflops(D)
+    peak_dfma = dg.fp64_peak_tflops(D)
+    peak_dmma = dg.fp64_peak_dmma_tflops(D)
+    peak_fp64 = max(peak_dfma, peak_dmma)  # both measured, the higher is the denominator
 
     def step():
         dg.apply_momentum(D, ctx, x, y)
@@ -529,7 +531,11 @@ def run_device(args):
                 "frac": mom_tflops / peak_fp64, "traffic": traffic,
                 "kernel": "k_momentum (dgb_momentum_apply)",
                 "algorithmic": f"{FLOP_PER_DOF['momentum']} flop/DoF x {D.n_u} DoF per launch (SURVEY 8d)",
-                "peak_source": "DFMA microbenchmark measured live (dgb_fp64_peak); MEASURED_PEAKS.json has no fp64"}
+                "peak_source": "FP64 pipe peak measured live: the higher of the DMMA (mma.sync m8n8k4.f64, "
+                               "dgb_fp64_peak_dmma) and DFMA (dgb_fp64_peak) microbenchmarks; MEASURED_PEAKS.json "
+                               "has no fp64.  The kernels issue DFMA only (DMMA shares the pipe and lost on the line "
+                               "contractions, profiles/experiments_r02.md)",
+                "peak_dfma": peak_dfma, "peak_dmma": peak_dmma, "frac_vs_dfma": mom_tflops / peak_dfma}
     roofline_hbm = {"achieved": BYTES_PER_DOF["momentum"] * D.n_u / tm / 1e9, "peak": peaks.get("hbm_gbs"),
                     "unit": "GB/s",
                     "frac": BYTES_PER_DOF["momentum"] * D.n_u / tm / 1e9 / peaks.get("hbm_gbs", 6535.7)}

@@ -296,6 +296,8 @@ int dgb_timer_start(dgb_ctx* ctx);
 int dgb_timer_stop(dgb_ctx* ctx, float* ms);
 /* fp64 DFMA peak microbenchmark on the context device (TFLOP/s). */
 int dgb_fp64_peak(dgb_ctx* ctx, double* tflops);
+/* the same through the FP64 tensor-core instruction (DMMA, mma.sync m8n8k4.f64): the pipe's upper peak. */
+int dgb_fp64_peak_dmma(dgb_ctx* ctx, double* tflops);
 /* Fast 3D kernels on (default) / off (generic kernels); and which apply:
  * 1 = axis-aligned (fast_axis.cuh), 2 = deformed (fast_deformed.cuh), 0 = generic only. */
 int dgb_set_fast_path(dgb_ctx* ctx, int enable);

@@ -157,6 +157,7 @@ def lib() -> C.CDLL:
     L.dgb_timer_start.argtypes = [C.c_void_p]
     L.dgb_timer_stop.argtypes = [C.c_void_p, C.POINTER(C.c_float)]
     L.dgb_fp64_peak.argtypes = [C.c_void_p, _dp]
+    L.dgb_fp64_peak_dmma.argtypes = [C.c_void_p, _dp]
     L.dgb_launch_count.argtypes = [C.c_void_p]
     L.dgb_launch_count.restype = C.c_longlong
     L.dgb_host_mesh_cartesian.argtypes = [C.c_int, C.c_int, C.c_double, C.c_uint, _llp, _ip, _ip, _dp, _dp, _dp]
@@ -704,6 +705,13 @@ def interpolate_synth_device(V: DGContext, f: "SynthField", out):
 def fp64_peak_tflops(V: DGContext) -> float:
     r = C.c_double()
     _check(lib().dgb_fp64_peak(V.handle, C.byref(r)))
+    return r.value
+
+
+def fp64_peak_dmma_tflops(V: DGContext) -> float:
+    """FP64 peak through the tensor-core instruction (DMMA m8n8k4): the pipe's upper peak."""
+    r = C.c_double()
+    _check(lib().dgb_fp64_peak_dmma(V.handle, C.byref(r)))
     return r.value
 
 
